@@ -1,0 +1,160 @@
+/*
+ * kan_b200.h -- C ABI of the B200-native KAN inference engine.
+ *
+ * Drop-in boundary for the reference's KAN-layer forward path
+ * (reference = arxiv/paper_2603_17230 "KANtize", proj/include/kantize/).
+ * Plain pointers and sizes only: no torch, no C++ types, no exceptions cross
+ * this boundary.  Errors are status codes plus a per-engine message.
+ *
+ * Reference interface each entry point replaces:
+ *   kan_engine_create           model_from_descriptor(json)       io.hpp:357-386
+ *                               (+ Model::validate)                layers.hpp:252-307
+ *   kan_engine_set_coeffs       KanLinearLayer/ConvKanLayer::coeffs layers.hpp:18-64
+ *                               (row layout i*(G+P)+k, layers.hpp:15-17, 36-38)
+ *   kan_engine_configure        EvalOptions{mode, qcfg.bits_w, lut} eval.hpp:37-45,
+ *                               build_bspline_lut(P, k, h)          lut.hpp:103-131,
+ *                               PreparedModel::make (W quant once)  eval.hpp:83-132
+ *   kan_engine_forward          model_forward(model, inputs, opts)  eval.hpp:200-253
+ *   kan_engine_forward_host     same, host buffers (H2D + D2H inside)
+ *   kan_engine_predict          predict(model, inputs, opts)        eval.hpp:255-276
+ *   kan_engine_layer_levels     ActivationLattice::quantize(clamp)  lut.hpp:44-47
+ *   kan_engine_layer_accumulators  the int32 form of the contraction behind
+ *                               tabulated_kan_forward               lut.hpp:217-231
+ *   kan_lut_build               build_bspline_lut                   lut.hpp:103-131
+ *
+ * Error mapping (reference exception -> status):
+ *   std::invalid_argument (bits, LUT params, mode)  -> KAN_ERR_INVALID_ARGUMENT
+ *     quant.hpp:35-38, lut.hpp:104-106, eval.hpp:24
+ *   std::invalid_argument (shape checks)            -> KAN_ERR_SHAPE_MISMATCH
+ *     layers.hpp:102-105, 131-132, 252-307, eval.hpp:213-214
+ *   std::out_of_range (lattice level)               -> KAN_ERR_OUT_OF_RANGE  lut.hpp:142-143
+ *   io_error / format_error / checksum_error        -> KAN_ERR_IO / _FORMAT / _CHECKSUM
+ *     io.hpp:21-29
+ *   std::logic_error                                -> KAN_ERR_LOGIC  eval.hpp:160
+ *
+ * Threading: a handle is used by one host thread at a time (the reference's
+ * forward is reentrant over const inputs; here one handle
+ * per thread or external synchronization).  One handle binds one device.
+ */
+#ifndef KAN_B200_H
+#define KAN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct kan_engine kan_engine;
+
+typedef enum {
+  KAN_OK = 0,
+  KAN_ERR_INVALID_ARGUMENT = 1,
+  KAN_ERR_SHAPE_MISMATCH = 2,
+  KAN_ERR_OUT_OF_RANGE = 3,
+  KAN_ERR_CUDA = 4,
+  KAN_ERR_NCCL = 5,
+  KAN_ERR_IO = 6,
+  KAN_ERR_FORMAT = 7,
+  KAN_ERR_CHECKSUM = 8,
+  KAN_ERR_UNSUPPORTED = 9,
+  KAN_ERR_LOGIC = 10
+} kan_status;
+
+/* Forward datapaths (EvalMode, eval.hpp:17; BF16 is new, FP32 = kFp32,
+ * BSPLINE_LUT = kBsplineLut). */
+typedef enum {
+  KAN_MODE_FP32 = 0,        /* fp32 Cox-de Boor basis + fp32 FFMA contraction */
+  KAN_MODE_BF16 = 1,        /* fp32 basis -> bf16, tcgen05 kind::f16, fp32 accumulate */
+  KAN_MODE_BSPLINE_LUT = 2  /* lattice + quantized LUT, tcgen05 kind::i8, int32 accumulate */
+} kan_mode;
+
+/* Weight quantization on the LUT path. */
+typedef enum {
+  KAN_W_PER_TENSOR_ASYM = 0,  /* the reference's scheme (eval.hpp:70-76): u8 + zero point */
+  KAN_W_PER_CHANNEL_SYM = 1   /* per output channel, symmetric, s8/s4 (engine extension) */
+} kan_wscheme;
+
+typedef enum {
+  KAN_OUT_F32 = 0, /* fp32 logits */
+  KAN_OUT_I8 = 1   /* int8 logits: clamp(llround(y / out_scale), -127, 127) */
+} kan_out_kind;
+
+typedef struct {
+  int mode;         /* kan_mode */
+  int lut_k;        /* LUT address bits per knot interval, 1..8 (lut.hpp:22) */
+  int lut_h;        /* LUT value bits, 2..8 (lut.hpp:75) */
+  int bits_w;       /* weight bits: 1..8 per-tensor, 2..8 per-channel (8 and 4 tested) */
+  int w_scheme;     /* kan_wscheme */
+  int silu_base;    /* 1: add SiLU(x) . w_base (needs kan_engine_set_coeffs base weights) */
+  int out_kind;     /* kan_out_kind */
+  double out_scale; /* int8 logits scale (out_kind == KAN_OUT_I8) */
+  int split_k;      /* 0 = automatic; >= 1 forces the number of K splits per layer */
+} kan_config;
+
+/* Build an engine from the reference's descriptor JSON schema
+ * ({name, grid{intervals,degree}, input[], [domain[lo,hi]], layers[...]},
+ * io.hpp:357-386).  Coefficients start at zero, as model_from_descriptor does. */
+kan_status kan_engine_create(const char* descriptor_json, int device, kan_engine** out);
+void kan_engine_destroy(kan_engine* e);
+const char* kan_engine_last_error(const kan_engine* e);
+
+/* Number of KAN (linear/conv) layers; input feature count (prod of input[]);
+ * output count (Model::output_count, layers.hpp:236-242). */
+int kan_engine_num_kan_layers(const kan_engine* e);
+int64_t kan_engine_input_size(const kan_engine* e);
+int kan_engine_output_count(const kan_engine* e);
+/* shape of KAN layer i: n_in (patch size for conv) and n_out */
+kan_status kan_engine_layer_shape(const kan_engine* e, int layer, int* n_in, int* n_out);
+
+/* Host fp64 coefficients of KAN layer `layer` in the reference row layout
+ * [n_in*(G+P), n_out] (layers.hpp:15-17); base_w: [n_in, n_out] or NULL. */
+kan_status kan_engine_set_coeffs(kan_engine* e, int layer, const double* coeffs, int64_t n,
+                                 const double* base_w, int64_t n_base);
+
+/* Quantize / convert weights once, build tables, upload (PreparedModel::make). */
+kan_status kan_engine_configure(kan_engine* e, const kan_config* cfg);
+
+/* model_forward on device buffers: x [batch, input_size] fp32 row-major (image
+ * models: CHW per row, eval.hpp:212-221); out [batch, output_count] fp32 or int8.
+ * stream: a cudaStream_t (NULL = legacy default stream). */
+kan_status kan_engine_forward(kan_engine* e, const float* x_dev, int64_t batch, void* out_dev,
+                              void* stream);
+/* Same on host buffers: H2D of x and D2H of the outputs are part of the call. */
+kan_status kan_engine_forward_host(kan_engine* e, const float* x_host, int64_t batch,
+                                   void* out_host, void* stream);
+/* predict: argmax of the logits (first maximum wins, eval.hpp:268-272). */
+kan_status kan_engine_predict(kan_engine* e, const float* x_dev, int64_t batch,
+                              int32_t* labels_dev, void* stream);
+
+/* Parity probes ------------------------------------------------------------ */
+/* Lattice levels of fp32 activations under layer `layer`'s grid and lut_k. */
+kan_status kan_engine_layer_levels(kan_engine* e, int layer, const float* x_dev, int64_t n,
+                                   uint16_t* levels_dev, void* stream);
+/* Raw int32 accumulators of one LUT layer given its input levels [batch, n_in]:
+ * acc_s [batch, n_out] (spline part), acc_b [batch, n_out] (SiLU base part;
+ * may be NULL). */
+kan_status kan_engine_layer_accumulators(kan_engine* e, int layer, const uint16_t* levels_dev,
+                                         int64_t batch, int32_t* acc_s_dev, int32_t* acc_b_dev,
+                                         void* stream);
+/* Host copy of the configured table (BsplineLut::entries). Returns entry count. */
+int64_t kan_engine_lut(const kan_engine* e, uint8_t* out, int64_t cap);
+/* Kernels launched by the most recent forward call. */
+int kan_engine_last_launches(const kan_engine* e);
+
+/* build_bspline_lut (lut.hpp:103-131) as a host utility. Returns entry count,
+ * or -KAN_ERR_INVALID_ARGUMENT. */
+int64_t kan_lut_build(int degree, int k, int h, uint8_t* out, int64_t cap);
+
+/* Host utility: the lattice threshold table the GPU level kernel uses,
+ * thr[n] = smallest fp32 x with level(x) >= n for n = 1..L (thr[0] = -inf,
+ * thr[L+1] = NaN), level = ActivationLattice::quantize(clamp_to_domain(x))
+ * (lut.hpp:44-47, grid.hpp:49-56).  `out` holds L+2 floats.  Returns L+2. */
+int64_t kan_lattice_thresholds(int intervals, int degree, double lo, double hi, int k,
+                               float* out, int64_t cap);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

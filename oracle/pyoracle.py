@@ -1,0 +1,408 @@
+"""ctypes bindings for the CPU checkers (TEST INFRASTRUCTURE ONLY).
+
+- ``Oracle``: the C restatement in ``oracle/kan_oracle.c`` (always present
+  once ``make -C oracle`` or ``__graft_entry__.build()`` ran).
+- ``Ref``: the unmodified reference headers compiled into
+  ``oracle/_ref/libkantize_ref.so`` (present where /root/reference was
+  available at build time; the .so travels with the repo snapshot).
+
+Only tests/, __graft_entry__.smoke() and bench.py's CPU-baseline legs import
+this module.  The product package never does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "libkan_oracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libkantize_ref.so")
+
+_dp = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+_fp = np.ctypeslib.ndpointer(dtype=np.float32, flags="C_CONTIGUOUS")
+_u8p = np.ctypeslib.ndpointer(dtype=np.uint8, flags="C_CONTIGUOUS")
+_i8p = np.ctypeslib.ndpointer(dtype=np.int8, flags="C_CONTIGUOUS")
+_u16p = np.ctypeslib.ndpointer(dtype=np.uint16, flags="C_CONTIGUOUS")
+_i32p = np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")
+_i64p = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
+
+
+def build_oracle() -> None:
+    subprocess.run(["make", "-s", "-C", HERE], check=True)
+
+
+class _Grid(C.Structure):
+    _fields_ = [("intervals", C.c_int), ("degree", C.c_int), ("lo", C.c_double),
+                ("hi", C.c_double), ("delta", C.c_double)]
+
+
+class _IntLayer(C.Structure):
+    _fields_ = [("wscheme", C.c_int), ("bits_w", C.c_int), ("silu", C.c_int),
+                ("qw_u8", C.c_void_p), ("s_w", C.c_double), ("z_w", C.c_int64),
+                ("qw_s8", C.c_void_p), ("s_wc", C.c_void_p),
+                ("silu_codes", C.c_void_p), ("s_s", C.c_double), ("z_s", C.c_int64),
+                ("qwb", C.c_void_p), ("s_wb", C.c_void_p)]
+
+
+class Oracle:
+    """The C restatement of the reference hot path (kan_oracle.c)."""
+
+    def __init__(self, path: str = ORACLE_SO):
+        if not os.path.exists(path):
+            build_oracle()
+        L = self.lib = C.CDLL(path)
+        G = C.POINTER(_Grid)
+        L.kor_grid_build.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, G]
+        L.kor_clamp.argtypes = [G, C.c_double]
+        L.kor_clamp.restype = C.c_double
+        L.kor_basis_at_coord.argtypes = [G, C.c_double, _dp]
+        L.kor_knot_coord.argtypes = [G, C.c_double]
+        L.kor_knot_coord.restype = C.c_double
+        L.kor_quant_params.argtypes = [C.c_double, C.c_double, C.c_int, C.POINTER(C.c_double),
+                                       C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+        L.kor_quantize.argtypes = [C.c_double, C.c_double, C.c_int64, C.c_int64, C.c_int64]
+        L.kor_quantize.restype = C.c_int64
+        L.kor_level_of.argtypes = [G, C.c_int, C.c_double]
+        L.kor_level_of.restype = C.c_int64
+        L.kor_levels_f32.argtypes = [G, C.c_int, _fp, C.c_size_t, _u16p]
+        L.kor_lut_size.argtypes = [C.c_int, C.c_int]
+        L.kor_lut_size.restype = C.c_size_t
+        L.kor_build_lut.argtypes = [C.c_int, C.c_int, C.c_int, _u8p, C.c_size_t]
+        L.kor_lut_lookup.argtypes = [G, C.c_int, _u8p, C.c_int64, _u8p, C.POINTER(C.c_int)]
+        L.kor_quantized_basis_reference.argtypes = [G, C.c_int, C.c_int, C.c_int64, _u8p,
+                                                    C.POINTER(C.c_int)]
+        L.kor_linear_forward_fp64.argtypes = [G, C.c_int64, C.c_int, C.c_int, _dp, _dp, _dp]
+        L.kor_lut_forward_fp64.argtypes = [G, C.c_int, C.c_int, C.c_int, C.c_int64, C.c_int,
+                                           C.c_int, _dp, _dp, _dp]
+        L.kor_wquant_per_tensor.argtypes = [_dp, C.c_size_t, C.c_int, _u8p,
+                                            C.POINTER(C.c_double), C.POINTER(C.c_int64)]
+        L.kor_wquant_per_channel_sym.argtypes = [_dp, C.c_int64, C.c_int, C.c_int, _i8p, _dp]
+        L.kor_silu_table.argtypes = [G, C.c_int, _u8p, C.POINTER(C.c_double),
+                                     C.POINTER(C.c_int64)]
+        L.kor_int_accumulate.argtypes = [G, C.c_int, _u8p, C.POINTER(_IntLayer), C.c_int64,
+                                         C.c_int, C.c_int, _u16p, _i32p, _i32p, _i64p]
+        L.kor_int_layer_forward.argtypes = [G, C.c_int, C.c_int, _u8p, C.POINTER(_IntLayer),
+                                            C.c_int64, C.c_int, C.c_int, _u16p, _dp]
+        L.kor_requant_i8.argtypes = [C.c_double, C.c_double]
+        L.kor_requant_i8.restype = C.c_int8
+        L.kor_im2col.argtypes = [_dp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _dp]
+
+    # -- grid / quant ---------------------------------------------------------
+    def grid(self, G, P, lo=-1.0, hi=1.0):
+        g = _Grid()
+        if self.lib.kor_grid_build(G, P, lo, hi, C.byref(g)):
+            raise ValueError("build_grid: bad arguments")
+        return g
+
+    def quant_params(self, a, b, bits):
+        s, z, qh = C.c_double(), C.c_int64(), C.c_int64()
+        if self.lib.kor_quant_params(a, b, bits, C.byref(s), C.byref(z), C.byref(qh)):
+            raise ValueError("compute_quant_params: bad arguments")
+        return s.value, z.value, qh.value
+
+    def basis(self, g, x):
+        nb = g.intervals + g.degree
+        out = np.zeros(nb)
+        xi = self.lib.kor_knot_coord(C.byref(g), x)
+        start = self.lib.kor_basis_at_coord(C.byref(g), xi, out)
+        return out, start
+
+    def level_of(self, g, k, x):
+        return self.lib.kor_level_of(C.byref(g), k, float(x))
+
+    def levels(self, g, k, x):
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        out = np.empty(x.shape, dtype=np.uint16)
+        self.lib.kor_levels_f32(C.byref(g), k, x.ravel(), x.size, out.ravel())
+        return out
+
+    def lut(self, P, k, h):
+        n = self.lib.kor_lut_size(P, k)
+        out = np.zeros(n, dtype=np.uint8)
+        if self.lib.kor_build_lut(P, k, h, out, n) < 0:
+            raise ValueError("build_bspline_lut: bad arguments")
+        return out
+
+    def lut_lookup(self, g, k, lut, a):
+        vals = np.zeros(16, dtype=np.uint8)
+        start = C.c_int()
+        cnt = self.lib.kor_lut_lookup(C.byref(g), k, lut, a, vals, C.byref(start))
+        if cnt < 0:
+            raise IndexError("lut_basis_lookup: lattice level out of range")
+        return vals[:cnt].copy(), start.value
+
+    def quantized_basis_reference(self, g, k, h, a):
+        vals = np.zeros(16, dtype=np.uint8)
+        start = C.c_int()
+        cnt = self.lib.kor_quantized_basis_reference(C.byref(g), k, h, a, vals, C.byref(start))
+        return vals[:cnt].copy(), start.value
+
+    # -- forwards -----------------------------------------------------------
+    def linear_forward(self, g, acts, coeffs):
+        acts = np.ascontiguousarray(acts, dtype=np.float64)
+        coeffs = np.ascontiguousarray(coeffs, dtype=np.float64)
+        M, n_in = acts.shape
+        n_out = coeffs.shape[1]
+        out = np.zeros((M, n_out))
+        self.lib.kor_linear_forward_fp64(C.byref(g), M, n_in, n_out, acts, coeffs, out)
+        return out
+
+    def lut_forward(self, g, k, h, bits_w, acts, coeffs):
+        acts = np.ascontiguousarray(acts, dtype=np.float64)
+        coeffs = np.ascontiguousarray(coeffs, dtype=np.float64)
+        M, n_in = acts.shape
+        n_out = coeffs.shape[1]
+        out = np.zeros((M, n_out))
+        if self.lib.kor_lut_forward_fp64(C.byref(g), k, h, bits_w, M, n_in, n_out, acts,
+                                         coeffs, out):
+            raise ValueError("tabulated_kan_forward failed")
+        return out
+
+    def wquant_per_tensor(self, w, bits):
+        w = np.ascontiguousarray(w, dtype=np.float64)
+        q = np.zeros(w.shape, dtype=np.uint8)
+        s, z = C.c_double(), C.c_int64()
+        if self.lib.kor_wquant_per_tensor(w.ravel(), w.size, bits, q.ravel(), C.byref(s),
+                                          C.byref(z)):
+            raise ValueError("per-tensor quantization failed")
+        return q, s.value, z.value
+
+    def wquant_per_channel(self, w, bits):
+        w = np.ascontiguousarray(w, dtype=np.float64)
+        K, N = w.shape
+        q = np.zeros((K, N), dtype=np.int8)
+        s = np.zeros(N)
+        if self.lib.kor_wquant_per_channel_sym(w, K, N, bits, q, s):
+            raise ValueError("per-channel quantization failed")
+        return q, s
+
+    def silu_table(self, g, k):
+        L = (g.intervals << k) + 1
+        codes = np.zeros(L, dtype=np.uint8)
+        s, z = C.c_double(), C.c_int64()
+        self.lib.kor_silu_table(C.byref(g), k, codes, C.byref(s), C.byref(z))
+        return codes, s.value, z.value
+
+    def int_layer(self, g, k, h, wscheme, bits_w, coeffs, base_w=None):
+        """Quantize one layer's weights the way the engine's LUT path does."""
+        d = {"wscheme": wscheme, "bits_w": bits_w, "silu": base_w is not None,
+             "lut": self.lut(g.degree, k, h)}
+        if wscheme == 0:
+            d["qw_u8"], d["s_w"], d["z_w"] = self.wquant_per_tensor(coeffs, bits_w)
+        else:
+            d["qw_s8"], d["s_wc"] = self.wquant_per_channel(coeffs, bits_w)
+        if base_w is not None:
+            d["silu_codes"], d["s_s"], d["z_s"] = self.silu_table(g, k)
+            d["qwb"], d["s_wb"] = self.wquant_per_channel(base_w, bits_w)
+        return d
+
+    def _int_struct(self, d):
+        s = _IntLayer()
+        s.wscheme, s.bits_w, s.silu = d["wscheme"], d["bits_w"], int(bool(d["silu"]))
+        keep = []
+
+        def ptr(a):
+            keep.append(a)
+            return a.ctypes.data
+
+        if d["wscheme"] == 0:
+            s.qw_u8, s.s_w, s.z_w = ptr(d["qw_u8"]), d["s_w"], d["z_w"]
+        else:
+            s.qw_s8, s.s_wc = ptr(d["qw_s8"]), ptr(d["s_wc"])
+        if d["silu"]:
+            s.silu_codes, s.s_s, s.z_s = ptr(d["silu_codes"]), d["s_s"], d["z_s"]
+            s.qwb, s.s_wb = ptr(d["qwb"]), ptr(d["s_wb"])
+        return s, keep
+
+    def int_accumulate(self, g, k, d, levels, n_out):
+        levels = np.ascontiguousarray(levels, dtype=np.uint16)
+        M, n_in = levels.shape
+        s, keep = self._int_struct(d)
+        acc_s = np.zeros((M, n_out), dtype=np.int32)
+        acc_b = np.zeros((M, n_out), dtype=np.int32)
+        rs = np.zeros(max(M, 1), dtype=np.int64)
+        if self.lib.kor_int_accumulate(C.byref(g), k, d["lut"], C.byref(s), M, n_in, n_out,
+                                       levels, acc_s, acc_b, rs):
+            raise ValueError("int accumulate failed")
+        return acc_s, acc_b, rs[:M]
+
+    def int_layer_forward(self, g, k, h, d, levels, n_out):
+        levels = np.ascontiguousarray(levels, dtype=np.uint16)
+        M, n_in = levels.shape
+        s, keep = self._int_struct(d)
+        y = np.zeros((M, n_out))
+        if self.lib.kor_int_layer_forward(C.byref(g), k, h, d["lut"], C.byref(s), M, n_in,
+                                          n_out, levels, y):
+            raise ValueError("int layer forward failed")
+        return y
+
+    def requant_i8(self, y, s_out):
+        f = np.vectorize(lambda v: self.lib.kor_requant_i8(float(v), s_out), otypes=[np.int8])
+        return f(y)
+
+    def im2col(self, x, kernel, stride, padding):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        Cc, H, W = x.shape
+        Ho = (H + 2 * padding - kernel) // stride + 1
+        Wo = (W + 2 * padding - kernel) // stride + 1
+        out = np.zeros((Ho * Wo, kernel * kernel * Cc))
+        if self.lib.kor_im2col(x, Cc, H, W, kernel, stride, padding, out):
+            raise ValueError("im2col: output dimensions are not positive integers")
+        return out
+
+
+class Ref:
+    """The unmodified reference headers behind oracle/ref_shim.cpp."""
+
+    available = os.path.exists(REF_SO)
+
+    def __init__(self, path: str = REF_SO):
+        L = self.lib = C.CDLL(path)
+        L.ref_last_error.restype = C.c_char_p
+        L.ref_quant_params.argtypes = [C.c_double, C.c_double, C.c_int, C.POINTER(C.c_double),
+                                       C.POINTER(C.c_int64)]
+        L.ref_quantize_value.argtypes = [C.c_double, C.c_double, C.c_double, C.c_int]
+        L.ref_quantize_value.restype = C.c_int64
+        L.ref_level_of.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_int,
+                                   C.c_double]
+        L.ref_level_of.restype = C.c_int64
+        L.ref_levels_f32.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, _fp,
+                                     C.c_int64, _u16p]
+        L.ref_clamp.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_double]
+        L.ref_clamp.restype = C.c_double
+        L.ref_build_lut.argtypes = [C.c_int, C.c_int, C.c_int, _u8p, C.c_int64,
+                                    C.POINTER(C.c_int64)]
+        L.ref_lut_lookup.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int,
+                                     C.c_int64, _u8p, C.POINTER(C.c_int)]
+        L.ref_quantized_basis.argtypes = L.ref_lut_lookup.argtypes
+        L.ref_cox_de_boor.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, _dp]
+        L.ref_linear_forward.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_int64,
+                                         C.c_int, C.c_int, _dp, _dp, _dp]
+        L.ref_lut_forward.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int,
+                                      C.c_int, C.c_int64, C.c_int, C.c_int, _dp, _dp, _dp]
+        L.ref_latticequant_forward.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double,
+                                               C.c_int, C.c_int, C.c_int64, C.c_int, C.c_int,
+                                               _dp, _dp, _dp]
+        L.ref_im2col.argtypes = [_dp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _dp]
+        L.ref_conv_forward.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int,
+                                       C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                       C.c_int, C.c_int, C.c_int, _dp, _dp, _dp]
+        L.ref_validate_descriptor.argtypes = [C.c_char_p]
+        L.ref_model_forward.argtypes = [C.c_char_p, C.POINTER(C.c_void_p), C.c_int, C.c_int,
+                                        C.c_int, C.c_int, C.c_int64, C.c_int64, _dp, C.c_int64,
+                                        _dp, C.c_int, C.c_int64]
+
+    def err(self):
+        return self.lib.ref_last_error().decode()
+
+    def quant_params(self, a, b, bits):
+        s, z = C.c_double(), C.c_int64()
+        if self.lib.ref_quant_params(a, b, bits, C.byref(s), C.byref(z)):
+            raise ValueError(self.err())
+        return s.value, z.value
+
+    def level_of(self, G, P, k, x, lo=-1.0, hi=1.0):
+        return self.lib.ref_level_of(G, P, lo, hi, k, float(x))
+
+    def levels(self, G, P, k, x, lo=-1.0, hi=1.0):
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        out = np.empty(x.shape, dtype=np.uint16)
+        self.lib.ref_levels_f32(G, P, lo, hi, k, x.ravel(), x.size, out.ravel())
+        return out
+
+    def lut(self, P, k, h):
+        buf = np.zeros(4096, dtype=np.uint8)
+        mb = C.c_int64()
+        n = self.lib.ref_build_lut(P, k, h, buf, buf.size, C.byref(mb))
+        if n < 0:
+            raise ValueError(self.err())
+        return buf[:n].copy(), mb.value
+
+    def lut_lookup(self, G, P, k, h, a, lo=-1.0, hi=1.0):
+        vals = np.zeros(16, dtype=np.uint8)
+        st = C.c_int()
+        n = self.lib.ref_lut_lookup(G, P, lo, hi, k, h, a, vals, C.byref(st))
+        if n < 0:
+            raise IndexError(self.err())
+        return vals[:n].copy(), st.value
+
+    def quantized_basis(self, G, P, k, h, a, lo=-1.0, hi=1.0):
+        vals = np.zeros(16, dtype=np.uint8)
+        st = C.c_int()
+        n = self.lib.ref_quantized_basis(G, P, lo, hi, k, h, a, vals, C.byref(st))
+        return vals[:n].copy(), st.value
+
+    def cox_de_boor(self, G, P, x, lo=-1.0, hi=1.0):
+        out = np.zeros(G + P)
+        st = self.lib.ref_cox_de_boor(G, P, lo, hi, x, out)
+        return out, st
+
+    def linear_forward(self, G, P, acts, coeffs, lo=-1.0, hi=1.0):
+        acts = np.ascontiguousarray(acts, dtype=np.float64)
+        coeffs = np.ascontiguousarray(coeffs, dtype=np.float64)
+        out = np.zeros((acts.shape[0], coeffs.shape[1]))
+        if self.lib.ref_linear_forward(G, P, lo, hi, acts.shape[0], acts.shape[1],
+                                       coeffs.shape[1], acts, coeffs, out):
+            raise ValueError(self.err())
+        return out
+
+    def lut_forward(self, G, P, k, h, bits_w, acts, coeffs, lo=-1.0, hi=1.0):
+        acts = np.ascontiguousarray(acts, dtype=np.float64)
+        coeffs = np.ascontiguousarray(coeffs, dtype=np.float64)
+        out = np.zeros((acts.shape[0], coeffs.shape[1]))
+        if self.lib.ref_lut_forward(G, P, lo, hi, k, h, bits_w, acts.shape[0], acts.shape[1],
+                                    coeffs.shape[1], acts, coeffs, out):
+            raise ValueError(self.err())
+        return out
+
+    def latticequant_forward(self, G, P, k, h, acts, coeffs, lo=-1.0, hi=1.0):
+        acts = np.ascontiguousarray(acts, dtype=np.float64)
+        coeffs = np.ascontiguousarray(coeffs, dtype=np.float64)
+        out = np.zeros((acts.shape[0], coeffs.shape[1]))
+        if self.lib.ref_latticequant_forward(G, P, lo, hi, k, h, acts.shape[0], acts.shape[1],
+                                             coeffs.shape[1], acts, coeffs, out):
+            raise ValueError(self.err())
+        return out
+
+    def im2col(self, x, kernel, stride, padding):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        Cc, H, W = x.shape
+        Ho = (H + 2 * padding - kernel) // stride + 1
+        Wo = (W + 2 * padding - kernel) // stride + 1
+        out = np.zeros((max(Ho, 0) * max(Wo, 0), kernel * kernel * Cc))
+        if self.lib.ref_im2col(x, Cc, H, W, kernel, stride, padding, out):
+            raise ValueError(self.err())
+        return out
+
+    def conv_forward(self, G, P, x, coeffs, c_out, kernel, stride, padding, mode=0, k=8, h=8,
+                     bits_w=32, lo=-1.0, hi=1.0):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        coeffs = np.ascontiguousarray(coeffs, dtype=np.float64)
+        Cc, H, W = x.shape
+        Ho = (H + 2 * padding - kernel) // stride + 1
+        Wo = (W + 2 * padding - kernel) // stride + 1
+        out = np.zeros((c_out, Ho, Wo))
+        if self.lib.ref_conv_forward(G, P, lo, hi, mode, k, h, bits_w, Cc, H, W, c_out, kernel,
+                                     stride, padding, x, coeffs, out):
+            raise ValueError(self.err())
+        return out
+
+    def validate_descriptor(self, text: str) -> int:
+        n = self.lib.ref_validate_descriptor(text.encode())
+        if n < 0:
+            raise ValueError(self.err())
+        return n
+
+    def model_forward(self, text, coeffs, inputs, n_out, mode=0, k=8, h=8, bits_w=8,
+                      threads=1, chunk=256):
+        inputs = np.ascontiguousarray(inputs, dtype=np.float64)
+        cs = [np.ascontiguousarray(c, dtype=np.float64) for c in coeffs]
+        ptrs = (C.c_void_p * len(cs))(*[c.ctypes.data for c in cs])
+        out = np.zeros((inputs.shape[0], n_out))
+        if self.lib.ref_model_forward(text.encode(), ptrs, mode, k, h, bits_w, inputs.shape[0],
+                                      inputs.shape[1], inputs, n_out, out, threads, chunk):
+            raise ValueError(self.err())
+        return out

@@ -1,0 +1,11 @@
+"""B200-native KAN inference engine (KANtize hot path: the KAN layer forward).
+
+The compute lives in ``libkan_b200.so`` (CUDA for sm_100a behind the C ABI in
+``include/kan_b200.h``); :mod:`paper_2603_17230_b200.engine` mirrors the
+reference's evaluation interface over it.
+"""
+from .engine import (  # noqa: F401
+    Engine, EvalOptions, KanError, build_bspline_lut, eval_mode_from_string,
+    kan_linear_forward, tabulated_kan_forward, lattice_thresholds, MODE_FP32, MODE_BF16, MODE_BSPLINE_LUT,
+    W_PER_TENSOR_ASYM, W_PER_CHANNEL_SYM, OUT_F32, OUT_I8, PASSTHROUGH_BITS, LIB_PATH,
+)

@@ -1,0 +1,314 @@
+"""Python mirror of the reference's KAN evaluation interface over the C ABI.
+
+The reference (proj/include/kantize/) exposes
+
+  model_from_descriptor(json) -> Model                io.hpp:357-386
+  model_forward(model, inputs, EvalOptions)            eval.hpp:200-253
+  predict(model, inputs, EvalOptions, chunk=256)       eval.hpp:255-276
+  tabulated_kan_forward(acts, layer, lut, bits_w)      lut.hpp:217-231
+  kan_linear_forward(acts, layer)                      layers.hpp:118-121
+  build_bspline_lut(P, k, h)                           lut.hpp:103-131
+  eval_mode_from_string("fp32" | "bspline-lut" ...)    eval.hpp:19-25
+
+This module keeps those names and argument meanings, but every forward runs in
+``libkan_b200.so`` (include/kan_b200.h) on a CUDA device.  There is no CPU
+fallback: if the shared library is missing, importing this module raises.
+torch is used only for device memory and streams.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import os
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libkan_b200.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+        " (the engine has no CPU fallback)")
+
+_lib = C.CDLL(LIB_PATH)
+
+KAN_OK = 0
+_STATUS = {
+    1: ValueError, 2: ValueError, 3: IndexError, 4: RuntimeError, 5: RuntimeError,
+    6: OSError, 7: ValueError, 8: ValueError, 9: NotImplementedError, 10: RuntimeError,
+}
+STATUS_NAMES = {0: "OK", 1: "INVALID_ARGUMENT", 2: "SHAPE_MISMATCH", 3: "OUT_OF_RANGE",
+                4: "CUDA", 5: "NCCL", 6: "IO", 7: "FORMAT", 8: "CHECKSUM", 9: "UNSUPPORTED",
+                10: "LOGIC"}
+
+MODE_FP32, MODE_BF16, MODE_BSPLINE_LUT = 0, 1, 2
+W_PER_TENSOR_ASYM, W_PER_CHANNEL_SYM = 0, 1
+OUT_F32, OUT_I8 = 0, 1
+PASSTHROUGH_BITS = 32  # quant.hpp:15
+
+
+class KanError(Exception):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"[{STATUS_NAMES.get(status, status)}] {msg}")
+        self.status = status
+
+
+class _Config(C.Structure):
+    _fields_ = [("mode", C.c_int), ("lut_k", C.c_int), ("lut_h", C.c_int), ("bits_w", C.c_int),
+                ("w_scheme", C.c_int), ("silu_base", C.c_int), ("out_kind", C.c_int),
+                ("out_scale", C.c_double), ("split_k", C.c_int)]
+
+
+_vp = C.c_void_p
+_lib.kan_engine_create.argtypes = [C.c_char_p, C.c_int, C.POINTER(_vp)]
+_lib.kan_engine_destroy.argtypes = [_vp]
+_lib.kan_engine_last_error.argtypes = [_vp]
+_lib.kan_engine_last_error.restype = C.c_char_p
+_lib.kan_engine_num_kan_layers.argtypes = [_vp]
+_lib.kan_engine_input_size.argtypes = [_vp]
+_lib.kan_engine_input_size.restype = C.c_int64
+_lib.kan_engine_output_count.argtypes = [_vp]
+_lib.kan_engine_layer_shape.argtypes = [_vp, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+_lib.kan_engine_set_coeffs.argtypes = [_vp, C.c_int, _vp, C.c_int64, _vp, C.c_int64]
+_lib.kan_engine_configure.argtypes = [_vp, C.POINTER(_Config)]
+_lib.kan_engine_forward.argtypes = [_vp, _vp, C.c_int64, _vp, _vp]
+_lib.kan_engine_forward_host.argtypes = [_vp, _vp, C.c_int64, _vp, _vp]
+_lib.kan_engine_predict.argtypes = [_vp, _vp, C.c_int64, _vp, _vp]
+_lib.kan_engine_layer_levels.argtypes = [_vp, C.c_int, _vp, C.c_int64, _vp, _vp]
+_lib.kan_engine_layer_accumulators.argtypes = [_vp, C.c_int, _vp, C.c_int64, _vp, _vp, _vp]
+_lib.kan_engine_lut.argtypes = [_vp, _vp, C.c_int64]
+_lib.kan_engine_lut.restype = C.c_int64
+_lib.kan_engine_last_launches.argtypes = [_vp]
+_lib.kan_lut_build.argtypes = [C.c_int, C.c_int, C.c_int, _vp, C.c_int64]
+_lib.kan_lut_build.restype = C.c_int64
+_lib.kan_lattice_thresholds.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, _vp,
+                                        C.c_int64]
+_lib.kan_lattice_thresholds.restype = C.c_int64
+
+# exported symbols declared in include/kan_b200.h (checked by the CPU tests)
+EXPORTED = [
+    "kan_engine_create", "kan_engine_destroy", "kan_engine_last_error",
+    "kan_engine_num_kan_layers", "kan_engine_input_size", "kan_engine_output_count",
+    "kan_engine_layer_shape", "kan_engine_set_coeffs", "kan_engine_configure",
+    "kan_engine_forward", "kan_engine_forward_host", "kan_engine_predict",
+    "kan_engine_layer_levels", "kan_engine_layer_accumulators", "kan_engine_lut",
+    "kan_engine_last_launches", "kan_lut_build", "kan_lattice_thresholds",
+]
+
+
+def lattice_thresholds(G: int, P: int, k: int, lo: float = -1.0, hi: float = 1.0) -> np.ndarray:
+    """The engine's exact fp32 level thresholds (host utility, no GPU)."""
+    n = _lib.kan_lattice_thresholds(G, P, lo, hi, k, None, 0)
+    if n < 0:
+        raise ValueError("lattice_thresholds: bad arguments")
+    out = np.zeros(n, dtype=np.float32)
+    _lib.kan_lattice_thresholds(G, P, lo, hi, k, out.ctypes.data, n)
+    return out
+
+
+def eval_mode_from_string(s: str) -> int:
+    """eval.hpp:19-25, plus the engine's bf16 datapath."""
+    table = {"fp32": MODE_FP32, "bf16": MODE_BF16, "bspline-lut": MODE_BSPLINE_LUT}
+    if s not in table:
+        raise ValueError(f"unknown evaluation mode '{s}'")
+    return table[s]
+
+
+def build_bspline_lut(degree: int, k: int, h: int) -> np.ndarray:
+    """build_bspline_lut (lut.hpp:103-131) through the engine's host code."""
+    n = _lib.kan_lut_build(degree, k, h, None, 0)
+    if n < 0:
+        raise ValueError("build_bspline_lut: bad arguments")
+    out = np.zeros(n, dtype=np.uint8)
+    _lib.kan_lut_build(degree, k, h, out.ctypes.data, n)
+    return out
+
+
+@dataclass
+class EvalOptions:
+    """EvalOptions (eval.hpp:37-45) extended with the engine's choices."""
+    mode: str = "fp32"
+    lut_k: int = 8
+    lut_h: int = 8
+    bits_w: int = 8
+    w_scheme: int = W_PER_CHANNEL_SYM
+    silu_base: bool = False
+    out_kind: int = OUT_F32
+    out_scale: float = 1.0
+    split_k: int = 0
+
+
+def _torch():
+    import torch  # plumbing only: device buffers and streams
+    return torch
+
+
+class Engine:
+    """A configured model on one CUDA device (model_from_descriptor + PreparedModel)."""
+
+    def __init__(self, descriptor, device: int = 0):
+        text = descriptor if isinstance(descriptor, str) else json.dumps(descriptor)
+        try:
+            self.descriptor = json.loads(text)
+        except ValueError:
+            self.descriptor = None  # the C++ parser reports the format error
+        h = _vp()
+        st = _lib.kan_engine_create(text.encode(), device, C.byref(h))
+        self._h = h
+        if st != KAN_OK:
+            msg = _lib.kan_engine_last_error(h).decode() if h else ""
+            self.close()
+            raise _STATUS.get(st, RuntimeError)(KanError(st, msg))
+        self.device = device
+        self.opts: Optional[EvalOptions] = None
+
+    # -- lifetime ---------------------------------------------------------------
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.kan_engine_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, st):
+        if st != KAN_OK:
+            msg = _lib.kan_engine_last_error(self._h).decode()
+            raise _STATUS.get(st, RuntimeError)(KanError(st, msg))
+
+    # -- model shape ---------------------------------------------------------------
+    @property
+    def num_kan_layers(self) -> int:
+        return _lib.kan_engine_num_kan_layers(self._h)
+
+    @property
+    def input_size(self) -> int:
+        return _lib.kan_engine_input_size(self._h)
+
+    @property
+    def output_count(self) -> int:
+        return _lib.kan_engine_output_count(self._h)
+
+    def layer_shape(self, i):
+        a, b = C.c_int(), C.c_int()
+        self._check(_lib.kan_engine_layer_shape(self._h, i, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    # -- weights / configuration -------------------------------------------------
+    def set_coeffs(self, layer: int, coeffs, base_w=None):
+        c = np.ascontiguousarray(coeffs, dtype=np.float64)
+        b = None if base_w is None else np.ascontiguousarray(base_w, dtype=np.float64)
+        self._check(_lib.kan_engine_set_coeffs(self._h, layer, c.ctypes.data, c.size,
+                                               None if b is None else b.ctypes.data,
+                                               0 if b is None else b.size))
+
+    def configure(self, opts: EvalOptions):
+        cfg = _Config(eval_mode_from_string(opts.mode), opts.lut_k, opts.lut_h, opts.bits_w,
+                      opts.w_scheme, int(bool(opts.silu_base)), opts.out_kind,
+                      float(opts.out_scale), opts.split_k)
+        self._check(_lib.kan_engine_configure(self._h, C.byref(cfg)))
+        self.opts = opts
+
+    # -- forward paths -------------------------------------------------------------
+    def _stream(self, stream):
+        torch = _torch()
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        return C.c_void_p(s.cuda_stream)
+
+    def model_forward(self, x, out=None, stream=None):
+        """model_forward (eval.hpp:200-253) on a CUDA fp32 tensor [batch, input_size]."""
+        torch = _torch()
+        assert x.is_cuda and x.dtype == torch.float32 and x.is_contiguous()
+        M = x.shape[0]
+        i8 = self.opts is not None and self.opts.out_kind == OUT_I8
+        if out is None:
+            out = torch.empty((M, self.output_count), device=x.device,
+                              dtype=torch.int8 if i8 else torch.float32)
+        self._check(_lib.kan_engine_forward(self._h, x.data_ptr(), M, out.data_ptr(),
+                                            self._stream(stream)))
+        return out
+
+    def forward_host(self, x: np.ndarray, stream=None) -> np.ndarray:
+        """model_forward on host buffers: H2D and D2H are inside the call."""
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        i8 = self.opts is not None and self.opts.out_kind == OUT_I8
+        out = np.empty((x.shape[0], self.output_count), dtype=np.int8 if i8 else np.float32)
+        self._check(_lib.kan_engine_forward_host(self._h, x.ctypes.data, x.shape[0],
+                                                 out.ctypes.data, self._stream(stream)))
+        return out
+
+    def forward_host_ptr(self, x_ptr: int, batch: int, out_ptr: int, stream=None):
+        self._check(_lib.kan_engine_forward_host(self._h, x_ptr, batch, out_ptr,
+                                                 self._stream(stream)))
+
+    def predict(self, x, stream=None):
+        """predict (eval.hpp:255-276): argmax of the logits, first maximum wins."""
+        torch = _torch()
+        labels = torch.empty(x.shape[0], device=x.device, dtype=torch.int32)
+        self._check(_lib.kan_engine_predict(self._h, x.data_ptr(), x.shape[0],
+                                            labels.data_ptr(), self._stream(stream)))
+        return labels
+
+    # -- parity probes ---------------------------------------------------------------
+    def layer_levels(self, layer: int, x, stream=None):
+        torch = _torch()
+        out = torch.empty(x.shape, device=x.device, dtype=torch.int16)
+        self._check(_lib.kan_engine_layer_levels(self._h, layer, x.data_ptr(), x.numel(),
+                                                 out.data_ptr(), self._stream(stream)))
+        return out.view(torch.uint16) if hasattr(torch, "uint16") else out
+
+    def layer_accumulators(self, layer: int, levels, stream=None):
+        torch = _torch()
+        _, n_out = self.layer_shape(layer)
+        M = levels.shape[0]
+        acc_s = torch.zeros((M, n_out), device=levels.device, dtype=torch.int32)
+        acc_b = torch.zeros((M, n_out), device=levels.device, dtype=torch.int32)
+        self._check(_lib.kan_engine_layer_accumulators(self._h, layer, levels.data_ptr(), M,
+                                                       acc_s.data_ptr(), acc_b.data_ptr(),
+                                                       self._stream(stream)))
+        return acc_s, acc_b
+
+    def lut(self) -> np.ndarray:
+        n = _lib.kan_engine_lut(self._h, None, 0)
+        out = np.zeros(n, dtype=np.uint8)
+        if n:
+            _lib.kan_engine_lut(self._h, out.ctypes.data, n)
+        return out
+
+    @property
+    def last_launches(self) -> int:
+        return _lib.kan_engine_last_launches(self._h)
+
+
+# ---- single-layer conveniences mirroring the reference's layer entry points ----
+
+def _linear_descriptor(n_in, n_out, G, P, lo=-1.0, hi=1.0):
+    return {"name": "layer", "grid": {"intervals": G, "degree": P}, "input": [n_in],
+            "domain": [lo, hi], "layers": [{"type": "linear", "n_in": n_in, "n_out": n_out}]}
+
+
+def tabulated_kan_forward(acts, coeffs, G: int, P: int, k: int, h: int, bits_w: int,
+                          w_scheme: int = W_PER_TENSOR_ASYM, lo=-1.0, hi=1.0, device=0):
+    """tabulated_kan_forward (lut.hpp:217-231) for one linear layer, on the GPU."""
+    n_in, n_out = acts.shape[1], coeffs.shape[1]
+    e = Engine(_linear_descriptor(n_in, n_out, G, P, lo, hi), device)
+    e.set_coeffs(0, coeffs)
+    e.configure(EvalOptions(mode="bspline-lut", lut_k=k, lut_h=h, bits_w=bits_w,
+                            w_scheme=w_scheme))
+    return e.model_forward(acts)
+
+
+def kan_linear_forward(acts, coeffs, G: int, P: int, mode: str = "fp32", lo=-1.0, hi=1.0,
+                       device=0):
+    """kan_linear_forward (layers.hpp:118-121) on the fp32 or bf16 datapath."""
+    n_in, n_out = acts.shape[1], coeffs.shape[1]
+    e = Engine(_linear_descriptor(n_in, n_out, G, P, lo, hi), device)
+    e.set_coeffs(0, coeffs)
+    e.configure(EvalOptions(mode=mode))
+    return e.model_forward(acts)
