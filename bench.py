@@ -1,0 +1,454 @@
+#!/usr/bin/env python
+"""Benchmark of the KAN-layer forward hot path (BASELINE.json metric:
+"KAN samples/sec (int8-LUT path) and % of roofline at 1/2/4/8 B200").
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+A step = one forward pass of the workload over one batch of synthetic input.
+Default workload = BASELINE.json configs[1] (C2): KAN MLP [784,64,10], G=5,
+P=3, batch 4096 per GPU, 8-bit table (k=8, h=8), int8 per-channel weights,
+SiLU base term, hidden outputs requantized to the next layer's lattice, int8
+logits.  For N > 1 (torchrun, one process per GPU, NCCL) every rank runs the
+same per-GPU batch (weak scaling); logits are gathered to rank 0 over NCCL
+once per 16-batch replay.  Rank 0 prints ONE JSON line.
+
+Timing: W untimed warm-up steps, then exactly K steps bracketed by a barrier
+and cudaDeviceSynchronize on both sides, device-timed with CUDA events on the
+launching stream, max over ranks.  Inputs rotate over R resident batches whose
+total exceeds the 126 MB L2, so each step reads its input from HBM.  Steps are
+replayed from CUDA graphs (one graph of R forwards + R single-forward graphs
+for the remainder) so host launch overhead stays out of the device time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+L2_BYTES = 126 * 1024 * 1024
+PAPER_SAMPLES_PER_S = {  # PAPER.md:603, KANMLP2 G=5 8-bit LUT on RTX 3090
+    "c1": 10000 / 5.9e-3, "c2": 10000 / 5.9e-3,
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20000)
+    ap.add_argument("--warmup", type=int, default=200)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=10.0,
+                    help="wall time of the bounded CPU-baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------------
+class ClockSampler:
+    """NVML sampling of SM clocks and clock-event reasons during the timed region."""
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, device: int):
+        self.ok = False
+        self.samples = []
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self._phys(device))
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+
+    @staticmethod
+    def _phys(device):
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        if vis:
+            try:
+                return int(vis.split(",")[device])
+            except (ValueError, IndexError):
+                return device
+        return device
+
+    def _read(self):
+        nv = self.nv
+        mhz = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+        try:
+            rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        except Exception:
+            rs = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+        return (time.perf_counter(), mhz, rs)
+
+    def start(self):
+        if not self.ok:
+            return
+        self._stop = False
+        self.samples.append(self._read())
+
+        def loop():
+            while not self._stop:
+                try:
+                    self.samples.append(self._read())
+                except Exception:
+                    pass
+                time.sleep(0.002)
+        self.th = threading.Thread(target=loop, daemon=True)
+        self.th.start()
+
+    def stop(self):
+        if not self.ok:
+            return
+        self._stop = True
+        self.th.join()
+        self.samples.append(self._read())
+
+    def summary(self, t0, t1):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
+        inside = [s for s in self.samples if t0 <= s[0] <= t1] or self.samples
+        mhz = sorted(s[1] for s in inside)
+        mask = 0
+        for s in inside:
+            mask |= s[2]
+        reasons = [n for b, n in self.REASONS.items() if mask & b and n != "gpu_idle"]
+        return {"sm_mhz": float(np.median(mhz)), "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(inside)}
+
+
+def measured_peaks():
+    for p in (os.path.join(ROOT, "MEASURED_PEAKS.json"), "/root/repo/MEASURED_PEAKS.json"):
+        if os.path.exists(p):
+            with open(p) as f:
+                return json.load(f), "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def measure_int8_peak(dev):
+    """Dense int8 tensor-core peak on this box: cuBLASLt int8 GEMM through
+    torch._int_mm, 8192^3, best of 10 (CUDA events).  None if unavailable."""
+    import torch
+    try:
+        n = 8192
+        a = torch.randint(-127, 127, (n, n), device=dev, dtype=torch.int8)
+        b = torch.randint(-127, 127, (n, n), device=dev, dtype=torch.int8).t().contiguous().t()
+        for _ in range(3):
+            torch._int_mm(a, b)
+        best = float("inf")
+        for _ in range(10):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch._int_mm(a, b)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        return 2 * n ** 3 / (best / 1e3) / 1e12
+    except Exception:
+        return None
+
+
+def committed_traffic(config: str):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        v = d.get(config, {}).get("dram_bytes_per_launch")
+        return v
+    return None
+
+
+# ---------------------------------------------------------------------------------
+def cpu_baseline(wl, seconds: float):
+    """The reference's own CPU path (oracle/_ref = the reference headers compiled
+    unmodified): model_forward in bspline-lut mode with the reference's weight
+    scheme (per-tensor asymmetric u8, eval.hpp:70-76) and no SiLU term (the
+    reference has none), batch sharded over all host threads, 256-row chunks.
+    Falls back to the C restatement (single thread) if oracle/_ref is absent."""
+    from oracle.pyoracle import Oracle, Ref
+    Ws, _ = wl.weights()
+    cores = os.cpu_count() or 1
+    rows = 2048
+    x = wl.inputs(rows, seed=99).astype(np.float64)
+    text = json.dumps(wl.descriptor())
+    if Ref.available:
+        ref = Ref()
+        mode = 2 if wl.mode == "bspline-lut" else 0
+        n = 0
+        t0 = time.perf_counter()
+        while True:
+            ref.model_forward(text, Ws, x, wl.dims[-1], mode=mode, k=wl.lut_k, h=wl.lut_h,
+                              bits_w=8, threads=cores, chunk=256)
+            n += rows
+            if time.perf_counter() - t0 >= seconds:
+                break
+        dt = time.perf_counter() - t0
+        return {"value": n / dt, "unit": "samples/s", "cores": cores, "kind": "reference",
+                "sample": f"{n} samples ({rows}-row calls) of {wl.key} through the reference "
+                          f"model_forward ({'bspline-lut k%d h%d, per-tensor u8 W' % (wl.lut_k, wl.lut_h) if mode == 2 else 'fp32'}"
+                          f", no SiLU term), {cores} threads, {dt:.1f} s"}
+    o = Oracle()
+    g = o.grid(wl.G, wl.P)
+    n = 0
+    t0 = time.perf_counter()
+    while time.perf_counter() - t0 < seconds:
+        h = x[:256]
+        for w in Ws:
+            h = o.lut_forward(g, wl.lut_k, wl.lut_h, 8, h, w)
+        n += 256
+    dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": "samples/s", "cores": 1, "kind": "port",
+            "sample": f"{n} samples of {wl.key} through the C restatement, 1 thread, {dt:.1f} s"}
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU implementation on the host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2603_17230_b200 import configs
+    from oracle.pyoracle import Ref
+    wl = configs.get(args.config)
+    cores = os.cpu_count() or 1
+    rows = 256 * cores  # one >=256-row chunk per thread (weights re-quantized per call)
+    x = wl.inputs(rows, seed=7).astype(np.float64)
+    Ws, _ = wl.weights()
+    text = json.dumps(wl.descriptor())
+    if not Ref.available:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return
+    ref = Ref()
+
+    def step():
+        ref.model_forward(text, Ws, x, wl.dims[-1], mode=2, k=wl.lut_k, h=wl.lut_h, bits_w=8,
+                          threads=cores, chunk=256)
+    steps = min(args.steps, 50)
+    for _ in range(min(args.warmup, 3)):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        step()
+    dt = time.perf_counter() - t0
+    v = rows * steps / dt
+    print(json.dumps({
+        "impl": "reference", "metric": "KAN samples/sec (int8-LUT path)", "value": v,
+        "unit": "samples/s", "n_gpus": args.gpus, "steps": steps, "warmup": min(args.warmup, 3),
+        "ms_per_step": dt / steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": wl.key + ": " + wl.title, "batch_per_step": rows,
+                   "note": "reference CPU path: model_forward bspline-lut, per-tensor u8 W, no SiLU"},
+        "cpu_baseline": {"value": v, "unit": "samples/s", "cores": cores, "kind": "reference",
+                         "sample": f"{steps} steps x {rows} rows, {cores} threads"},
+        "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": f"--steps capped at {steps} so the CPU run stays within minutes",
+    }))
+
+
+# ---------------------------------------------------------------------------------
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2603_17230_b200 import Engine, EvalOptions, OUT_I8, OUT_F32, W_PER_CHANNEL_SYM
+    from paper_2603_17230_b200 import configs
+    from paper_2603_17230_b200.sharding import gather_logits
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    wl = configs.get(args.config)
+    B = wl.batch  # per-GPU batch (weak scaling)
+
+    Ws, Bs = wl.weights()
+    eng = Engine(wl.descriptor(), local)
+    for i, (w, b) in enumerate(zip(Ws, Bs)):
+        eng.set_coeffs(i, w, b)
+    opts = EvalOptions(mode=wl.mode, lut_k=wl.lut_k, lut_h=wl.lut_h, bits_w=wl.bits_w,
+                       w_scheme=W_PER_CHANNEL_SYM, silu_base=wl.silu, out_kind=OUT_F32)
+    eng.configure(opts)
+
+    # rotating resident input batches, total > L2
+    in_bytes = B * wl.dims[0] * 4
+    R = max(2, min(64, math.ceil(2 * L2_BYTES / in_bytes)))
+    R = max(R, 16) if in_bytes < 64 * 1024 * 1024 else R
+    xs = [torch.from_numpy(wl.inputs(B, seed=100 * rank + r)).to(dev) for r in range(R)]
+    if wl.int8_out:
+        y = eng.model_forward(xs[0]).float()
+        s_out = float(y.abs().max().item()) / 127.0
+        opts.out_kind, opts.out_scale = OUT_I8, s_out
+        eng.configure(opts)
+    out_dtype = torch.int8 if wl.int8_out else torch.float32
+    outs = torch.empty((R, B, wl.dims[-1]), device=dev, dtype=out_dtype)
+    st = torch.cuda.Stream(dev)
+    torch.cuda.synchronize()
+    # warm the engine (allocations happen outside graph capture)
+    with torch.cuda.stream(st):
+        for r in range(R):
+            eng.model_forward(xs[r], out=outs[r], stream=st)
+    torch.cuda.synchronize()
+    launches_per_step = eng.last_launches
+
+    big = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(big, stream=st):
+        for r in range(R):
+            eng.model_forward(xs[r], out=outs[r], stream=st)
+    singles = []
+    for r in range(R):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            eng.model_forward(xs[r], out=outs[r], stream=st)
+        singles.append(g)
+    gathered = []
+
+    def run_steps(n):
+        q, rem = divmod(n, R)
+        for _ in range(q):
+            big.replay()
+            if world > 1:
+                gathered.append(gather_logits(outs.view(R * B, -1), R * B * world))
+        for r in range(rem):
+            singles[r].replay()
+
+    with torch.cuda.stream(st):
+        run_steps(args.warmup)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks.start()
+    t_wall0 = time.perf_counter()
+    with torch.cuda.stream(st):
+        ev0.record(st)
+        run_steps(args.steps)
+        ev1.record(st)
+    torch.cuda.synchronize()
+    t_wall1 = time.perf_counter()
+    if world > 1:
+        dist.barrier()
+    clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * B * args.steps / (ms / 1e3)
+
+    # ---- dominant kernel: per-launch device time with CUDA events (engine profiling)
+    prof_steps = min(max(args.steps, 20), 400)
+    eng.set_profiling(True)
+    with torch.cuda.stream(st):
+        for i in range(prof_steps):
+            eng.model_forward(xs[i % R], out=outs[i % R], stream=st)
+    torch.cuda.synchronize()
+    layer_ms = []
+    for li in range(len(wl.dims) - 1):
+        tot, cnt = eng.layer_time_ms(li)
+        layer_ms.append(tot / max(cnt, 1))
+    eng.set_profiling(False)
+    lut = wl.mode == "bspline-lut"
+    peaks, peak_src = measured_peaks()
+    # bound of the dominant (largest-time) layer
+    dom = int(np.argmax(layer_ms))
+    bytes_l = wl.layer_bytes_per_launch(dom, B)
+    ops_l = wl.layer_ops_per_launch(dom, B)
+    int8_peak_tops = peaks.get("int8_tops", 4500.0)
+    if lut and "int8_tops" not in peaks and ops_l / bytes_l > 4500e12 / (peaks["hbm_gbs"] * 1e9):
+        meas = measure_int8_peak(dev)
+        if meas:
+            peaks["int8_tops"] = int8_peak_tops = meas
+    t_l = layer_ms[dom] / 1e3
+    ai = ops_l / bytes_l
+    tensor_peak = int8_peak_tops * 1e12 if lut else peaks.get("bf16_tflops", 1677.7) * 1e12
+    hbm_peak = peaks["hbm_gbs"] * 1e9
+    if ai < tensor_peak / hbm_peak:
+        roof = {"bound": "hbm", "achieved": bytes_l / t_l / 1e9, "peak": peaks["hbm_gbs"],
+                "unit": "GB/s"}
+    else:
+        roof = {"bound": "tensor", "achieved": ops_l / t_l / 1e12,
+                "peak": tensor_peak / 1e12, "unit": "TOP/s" if lut else "TFLOP/s"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"] = committed_traffic(wl.key)
+    roof["kernel"] = f"kan_gather_gemm layer {dom} ({wl.dims[dom]}->{wl.dims[dom + 1]})"
+    roof["per_launch"] = {"algorithmic_bytes": bytes_l, "algorithmic_ops": ops_l,
+                          "avg_ms": layer_ms[dom], "launches_timed": prof_steps}
+    roof["peak_source"] = peak_src + (
+        "" if not lut or "int8_tops" in peaks else "; int8 peak = datasheet 4.5 POPS dense")
+    roof["layer_avg_ms"] = layer_ms
+    roof["share_of_step"] = layer_ms[dom] / (ms / args.steps)
+
+    # ---- e2e through the public API: host buffers, H2D + forward + D2H every step
+    e2e_steps = max(10, min(args.steps, 300))
+    hx = [torch.from_numpy(wl.inputs(B, seed=500 + r)).pin_memory() for r in range(4)]
+    hout = torch.empty((B, wl.dims[-1]), dtype=out_dtype).pin_memory()
+    for i in range(3):
+        eng.forward_host_ptr(hx[i % 4].data_ptr(), B, hout.data_ptr(), stream=st)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for i in range(e2e_steps):
+        eng.forward_host_ptr(hx[i % 4].data_ptr(), B, hout.data_ptr(), stream=st)
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = {"value": world * B * e2e_steps / e2e_s, "unit": "samples/s",
+           "h2d_bytes_per_step": in_bytes, "d2h_bytes_per_step": B * wl.dims[-1] *
+           (1 if wl.int8_out else 4), "steps": e2e_steps,
+           "api": "kan_engine_forward_host (pinned host buffers, stream-synchronous)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(wl, args.cpu_seconds)
+        except Exception as ex:  # report, never hide
+            cpu = {"value": None, "error": str(ex)}
+
+    if rank == 0:
+        paper = PAPER_SAMPLES_PER_S.get(wl.key)
+        line = {
+            "metric": "KAN samples/sec (int8-LUT path)" if lut else f"KAN samples/sec ({wl.mode} path)",
+            "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": (value / paper) if paper else None,
+            "dtype": "u8" if lut else wl.mode, "data": "synthetic",
+            "config": {"workload": wl.key + ": " + wl.title, "batch_per_gpu": B,
+                       "global_batch": B * world, "parallelism": f"dp{world}",
+                       "l2": f"inputs rotate over {R} resident batches "
+                             f"({R * in_bytes / 2**20:.0f} MiB > 126 MiB L2)",
+                       "launch": f"CUDA graphs ({R}-forward graph + single-forward graphs)",
+                       "vs_baseline_ref": "PAPER.md:603 KANMLP2 G=5 8-bit LUT, RTX 3090, "
+                                          "1.69M samples/s" if paper else None},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clocks.summary(t_wall0, t_wall1),
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -142,6 +142,12 @@ kan_status kan_engine_layer_accumulators(kan_engine* e, int layer, const uint16_
 int64_t kan_engine_lut(const kan_engine* e, uint8_t* out, int64_t cap);
 /* Kernels launched by the most recent forward call. */
 int kan_engine_last_launches(const kan_engine* e);
+/* Per-layer kernel timing: when on, every forward brackets each KAN layer's
+ * launch with CUDA events on the launching stream; kan_engine_layer_time_ms
+ * waits for them and returns the accumulated device time and launch count of
+ * layer `layer` since profiling was (re)enabled. */
+kan_status kan_engine_set_profiling(kan_engine* e, int on);
+kan_status kan_engine_layer_time_ms(kan_engine* e, int layer, double* total_ms, int64_t* count);
 
 /* build_bspline_lut (lut.hpp:103-131) as a host utility. Returns entry count,
  * or -KAN_ERR_INVALID_ARGUMENT. */

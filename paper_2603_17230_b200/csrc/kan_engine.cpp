@@ -27,9 +27,9 @@
 
 namespace kan {
 // kernels (kan_gemm.cu / kan_fp32.cu)
-cudaError_t launch_gather_gemm(bool bf16, int nbp, const CUtensorMap& xmap, const GemmParams& p,
-                               size_t smem, cudaStream_t st);
-size_t gemm_smem_bytes(bool bf16, int nbp, int BN, int S, int x_kind, int L, int silu);
+cudaError_t launch_gather_gemm(bool bf16, int nbp, int mode, const CUtensorMap& xmap,
+                               const GemmParams& p, size_t smem, cudaStream_t st);
+size_t gemm_smem_bytes(bool bf16, int nbp, int BN, int S, int x_kind, int tab_bytes);
 int gemm_ips(bool bf16, int nbp);
 int gemm_gs(bool bf16, int nbp);
 cudaError_t launch_levels(const float* x, int64_t n, const float* thr, float lo, float inv_step,
@@ -168,8 +168,8 @@ struct kan_engine {
   Lattice lat;
   std::vector<PreparedLayer> prep;
   DevBuf<float> d_thr;
-  DevBuf<uint32_t> d_vals;
-  DevBuf<uint8_t> d_silu;
+  DevBuf<uint8_t> d_tab;  // smem table blob (see GemmParams::tab)
+  int tab_bytes = 0, off_thr = 0, off_pat = 0, off_silu = 0;
   double s_s = 1.0;
   int64_t z_s = 0;
   // workspaces
@@ -180,6 +180,37 @@ struct kan_engine {
   DevBuf<float> logits_tmp;
   DevBuf<uint8_t> io_in, io_out;
   int last_launches = 0;
+  // per-layer kernel timing (kan_engine_set_profiling)
+  struct PendingTiming {
+    int layer;
+    cudaEvent_t a, b;
+  };
+  bool profiling = false;
+  std::vector<PendingTiming> pending;
+  std::vector<double> layer_ms;
+  std::vector<int64_t> layer_count;
+  void drain_timings() {
+    if (layer_ms.size() < static_cast<size_t>(n_kan)) {
+      layer_ms.resize(static_cast<size_t>(n_kan), 0.0);
+      layer_count.resize(static_cast<size_t>(n_kan), 0);
+    }
+    for (auto& t : pending) {
+      float ms = 0.f;
+      if (cudaEventSynchronize(t.b) == cudaSuccess && cudaEventElapsedTime(&ms, t.a, t.b) == cudaSuccess) {
+        layer_ms[static_cast<size_t>(t.layer)] += ms;
+        layer_count[static_cast<size_t>(t.layer)] += 1;
+      }
+      cudaEventDestroy(t.a);
+      cudaEventDestroy(t.b);
+    }
+    pending.clear();
+  }
+  ~kan_engine() {
+    for (auto& t : pending) {
+      cudaEventDestroy(t.a);
+      cudaEventDestroy(t.b);
+    }
+  }
 
   int64_t input_size() const {
     int64_t n = 1;
@@ -528,10 +559,9 @@ void configure(kan_engine* e, const kan_config* c) {
     e->lut = build_lut(g.P, cfg.lut_k, cfg.lut_h);  // validates P, k, h like the reference
     e->lat = Lattice::of(g, cfg.lut_k);
     const int64_t L = e->lat.L;
-    std::vector<uint32_t> vals(static_cast<size_t>(L) + 1);
-    for (int64_t a = 0; a <= L; ++a) vals[static_cast<size_t>(a)] = lut_pack(g, cfg.lut_k, e->lut, a);
-    e->d_vals.upload(vals);
-    e->d_thr.upload(level_thresholds(g, e->lat));
+    const std::vector<float> thr = level_thresholds(g, e->lat);
+    e->d_thr.upload(thr);
+    std::vector<uint8_t> codes;
     if (cfg.silu_base) {
       std::vector<double> v(static_cast<size_t>(L) + 1);
       double lo = 0.0, hi = 0.0;
@@ -544,11 +574,47 @@ void configure(kan_engine* e, const kan_config* c) {
       const QParams sq = quant_params(lo, hi, 8);
       e->s_s = sq.scale;
       e->z_s = sq.zp;
-      std::vector<uint8_t> codes(static_cast<size_t>(L) + 1);
+      codes.resize(static_cast<size_t>(L) + 1);
       for (int64_t a = 0; a <= L; ++a)
         codes[static_cast<size_t>(a)] = static_cast<uint8_t>(quantize(v[static_cast<size_t>(a)], sq));
-      e->d_silu.upload(codes);
     }
+    // smem table blob: per level the threshold pair and the basis-row pattern
+    // (the P+1 LUT codes of lut_basis_lookup placed at the support offset)
+    const int nbp = g.nb() <= 8 ? 8 : 16;
+    auto a16 = [](size_t n) { return (n + 15) / 16 * 16; };
+    std::vector<uint8_t> blob;
+    const size_t nl = static_cast<size_t>(L) + 1;
+    if (nbp == 8) {
+      e->off_thr = 0;
+      e->off_pat = 8;
+      blob.assign(nl * 16, 0);
+      for (size_t a = 0; a < nl; ++a) {
+        const uint64_t pat = static_cast<uint64_t>(lut_pack(g, cfg.lut_k, e->lut, static_cast<int64_t>(a)))
+                             << (8 * (a >> cfg.lut_k));
+        std::memcpy(&blob[a * 16], &thr[a], 4);
+        std::memcpy(&blob[a * 16 + 4], &thr[a + 1], 4);
+        std::memcpy(&blob[a * 16 + 8], &pat, 8);
+      }
+    } else {
+      e->off_thr = 0;
+      e->off_pat = static_cast<int>(a16(nl * 8));
+      blob.assign(static_cast<size_t>(e->off_pat) + nl * 16, 0);
+      for (size_t a = 0; a < nl; ++a) {
+        std::memcpy(&blob[a * 8], &thr[a], 4);
+        std::memcpy(&blob[a * 8 + 4], &thr[a + 1], 4);
+        const uint32_t v = lut_pack(g, cfg.lut_k, e->lut, static_cast<int64_t>(a));
+        const size_t jj = a >> cfg.lut_k;
+        for (int r = 0; r < 4; ++r)
+          if (jj + r < 16) blob[static_cast<size_t>(e->off_pat) + a * 16 + jj + r] = static_cast<uint8_t>(v >> (8 * r));
+      }
+    }
+    e->off_silu = static_cast<int>(blob.size());
+    if (!codes.empty()) {
+      blob.insert(blob.end(), codes.begin(), codes.end());
+      blob.resize(a16(blob.size()), 0);
+    }
+    e->tab_bytes = static_cast<int>(blob.size());
+    e->d_tab.upload(blob);
     if (cfg.w_scheme == KAN_W_PER_TENSOR_ASYM && (cfg.bits_w < 1 || cfg.bits_w > 8))
       throw InvalidArgument("compute_quant_params: bits must be in [1,8] or 32");
   } else {
@@ -574,9 +640,9 @@ void configure(kan_engine* e, const kan_config* c) {
 }
 
 // choose ring depth for the smem budget
-int pick_stages(bool bf16, int nbp, int BN, int x_kind, int L, int silu) {
+int pick_stages(bool bf16, int nbp, int BN, int x_kind, int tab_bytes) {
   for (int S = 8; S >= 2; --S)
-    if (gemm_smem_bytes(bf16, nbp, BN, S, x_kind, L, silu) <= 232448) return S;
+    if (gemm_smem_bytes(bf16, nbp, BN, S, x_kind, tab_bytes) <= 232448) return S;
   throw Unsupported("tile configuration exceeds shared memory");
 }
 
@@ -607,9 +673,11 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
   p.x_kind = io.x_kind;
   p.L = bf16 ? 0 : static_cast<int>(e->lat.L);
   p.k = e->lat.k;
-  p.thr = e->d_thr.p;
-  p.vals = e->d_vals.p;
-  p.silu_codes = e->d_silu.p;
+  p.tab = e->d_tab.p;
+  p.tab_bytes = e->tab_bytes;
+  p.off_thr = e->off_thr;
+  p.off_pat = e->off_pat;
+  p.off_silu = e->off_silu;
   p.lo_f = static_cast<float>(e->grid.lo);
   p.inv_step_f = bf16 ? 0.f : static_cast<float>(1.0 / e->lat.step);
   p.flo = static_cast<float>(e->grid.lo);
@@ -633,11 +701,11 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
   p.splits = splits;
   p.groups_per_split = gps;
   if (splits > 1) {
-    const size_t mn = static_cast<size_t>(M) * pl.N;
-    if (e->ws_s.n < mn) e->ws_s.alloc(mn, true);
-    if (pl.silu && !bf16 && e->ws_b.n < mn) e->ws_b.alloc(mn, true);
-    const size_t rsz = static_cast<size_t>(pl.n_tiles_n) * M;
-    if (e->ws_rowsum.n < rsz) e->ws_rowsum.alloc(rsz, true);
+    const size_t mn = static_cast<size_t>(splits) * p.m_tiles * 128 * pl.n_tiles_n * pl.BN;
+    if (e->ws_s.n < mn) e->ws_s.alloc(mn);
+    if (pl.silu && !bf16 && e->ws_b.n < mn) e->ws_b.alloc(mn);
+    const size_t rsz = static_cast<size_t>(pl.n_tiles_n) * splits * p.m_tiles * 128;
+    if (e->ws_rowsum.n < rsz) e->ws_rowsum.alloc(rsz);
     const size_t ct = static_cast<size_t>(tiles);
     if (e->counters.n < ct) e->counters.alloc(ct, true);
   }
@@ -663,10 +731,13 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
   p.out_scale = e->cfg.out_scale;
   const int box_cols = pl.IPS;
   const CUtensorMap xmap = make_xmap(io.x, io.x_kind, M, pl.n_in, io.ld_x, box_cols);
-  const int S = pick_stages(bf16, pl.nbp, pl.BN, io.x_kind, p.L, pl.silu);
+  const int tb = bf16 ? 0 : e->tab_bytes;
+  const int S = pick_stages(bf16, pl.nbp, pl.BN, io.x_kind, tb);
   p.S = S;
-  const size_t smem = gemm_smem_bytes(bf16, pl.nbp, pl.BN, S, io.x_kind, p.L, pl.silu);
-  ck(launch_gather_gemm(bf16, pl.nbp, xmap, p, smem, st), "gather_gemm launch");
+  const size_t smem = gemm_smem_bytes(bf16, pl.nbp, pl.BN, S, io.x_kind, tb);
+  // kernel variant: 0 plain, 1 per-tensor zero point (reference scheme), 2 SiLU base
+  const int mode = pl.silu ? 2 : ((!bf16 && pl.wscheme == KAN_W_PER_TENSOR_ASYM) ? 1 : 0);
+  ck(launch_gather_gemm(bf16, pl.nbp, mode, xmap, p, smem, st), "gather_gemm launch");
   e->last_launches += 1;
 }
 
@@ -749,6 +820,12 @@ void forward(kan_engine* e, const float* x, int64_t M, void* out, cudaStream_t s
       dst = e->act[pp].p;
       out_kind = lut ? EPI_LEVEL : EPI_F32;
     }
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    if (e->profiling) {
+      ck(cudaEventCreate(&ev0), "cudaEventCreate");
+      ck(cudaEventCreate(&ev1), "cudaEventCreate");
+      ck(cudaEventRecord(ev0, st), "cudaEventRecord");
+    }
     if (fp32) {
       run_fp32_layer(e, pl, M, static_cast<const float*>(cur), cur_ld, static_cast<float*>(dst),
                      ld_out, st);
@@ -757,6 +834,10 @@ void forward(kan_engine* e, const float* x, int64_t M, void* out, cudaStream_t s
       io.epi = out_kind;
       io.ld_out = ld_out;
       run_gemm_layer(e, pl, M, io, st);
+    }
+    if (e->profiling) {
+      ck(cudaEventRecord(ev1, st), "cudaEventRecord");
+      e->pending.push_back({l.kan_index, ev0, ev1});
     }
     cur = dst;
     cur_kind = lut ? X_U16 : X_F32;
@@ -995,6 +1076,28 @@ int64_t kan_engine_lut(const kan_engine* e, uint8_t* out, int64_t cap) {
 }
 
 int kan_engine_last_launches(const kan_engine* e) { return e ? e->last_launches : 0; }
+
+kan_status kan_engine_set_profiling(kan_engine* e, int on) {
+  if (!e) return KAN_ERR_INVALID_ARGUMENT;
+  return guarded(e, [&] {
+    DeviceGuard dg(e->device);
+    e->drain_timings();
+    e->layer_ms.assign(static_cast<size_t>(e->n_kan), 0.0);
+    e->layer_count.assign(static_cast<size_t>(e->n_kan), 0);
+    e->profiling = on != 0;
+  });
+}
+
+kan_status kan_engine_layer_time_ms(kan_engine* e, int layer, double* total_ms, int64_t* count) {
+  if (!e) return KAN_ERR_INVALID_ARGUMENT;
+  return guarded(e, [&] {
+    if (layer < 0 || layer >= e->n_kan) throw InvalidArgument("KAN layer index out of range");
+    DeviceGuard dg(e->device);
+    e->drain_timings();
+    if (total_ms) *total_ms = e->layer_ms[static_cast<size_t>(layer)];
+    if (count) *count = e->layer_count[static_cast<size_t>(layer)];
+  });
+}
 
 int64_t kan_lut_build(int degree, int k, int h, uint8_t* out, int64_t cap) {
   try {

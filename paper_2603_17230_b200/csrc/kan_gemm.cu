@@ -7,18 +7,22 @@
 //     -> matmul (matrix.hpp:64-80)
 // and, on the float path, kan_linear_forward<RecursiveBasis> (layers.hpp:118-121).
 //
-// One CTA computes a 128-row x BN-column output tile.  Warp roles:
+// One CTA computes a 128-row x BN-column output tile over a range of K.
+// Warp roles:
 //   warps 0..NPW-1  producers: read the activation tile TMA put in smem,
-//                   quantize each activation to its lattice level (exact, via
-//                   a threshold table), expand the level into its basis row
-//                   (u8 LUT codes, or bf16 basis values) and write the A tile
-//                   straight into smem in the UMMA K-major 128B-swizzle layout;
-//                   afterwards they run the epilogue (TMEM -> regs -> global).
-//   warp NPW        loader: TMA for the activation tile, one bulk copy per
-//                   stage for the pre-swizzled weight tile.
+//                   quantize each activation to its lattice level (exact: an
+//                   fp32 guess corrected against host-computed thresholds),
+//                   fetch the level's precomputed basis-row pattern (u8 LUT
+//                   codes at the support offset) and write the A tile straight
+//                   into smem in the UMMA K-major 128B-swizzle layout; the
+//                   bf16 path evaluates the basis in fp32 instead.  Afterwards
+//                   they run the epilogue (TMEM -> regs -> global).
+//   warp NPW        loader: one bulk copy for the lattice tables, then per stage
+//                   a TMA 2D load of the activation tile and a bulk copy of the
+//                   pre-swizzled weight tile.
 //   warp NPW+1      TMEM allocation and the single-thread tcgen05.mma issuer.
-// The int32 accumulators live in TMEM; the K loop is a ring of S stages, each
-// 128 bytes of K (4 MMAs of K=32 bytes).
+// Accumulators live in TMEM (int32 on the LUT path, fp32 on bf16); the K loop
+// is a ring of S stages of 128 bytes of K each (4 MMAs of K = 32 bytes).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -48,19 +52,22 @@ __device__ __forceinline__ int lattice_level_f64(double y, double lo, double hi_
   return static_cast<int>(a);
 }
 
-// Level of an fp32 activation: fp32 guess, then exact correction against the
-// host-computed thresholds thr[n] = min{x : level(x) >= n}.
+// fp32 guess of the lattice level (exact after one threshold correction)
+__device__ __forceinline__ int level_guess(float x, float lo, float inv_step, float Lf) {
+  float t = (x - lo) * inv_step;
+  t = fminf(fmaxf(t, 0.0f), Lf);  // NaN -> 0 (fmaxf returns the non-NaN operand)
+  return __float2int_rn(t);
+}
+
+// Level of an fp32 activation against thr[n] = min{x : level(x) >= n}.
 __device__ __forceinline__ int lattice_level_f32(float x, const float* thr, float lo,
                                                  float inv_step, int L) {
-  float t = (x - lo) * inv_step;
-  t = fminf(fmaxf(t, 0.0f), static_cast<float>(L));
-  int g = __float2int_rn(t);
+  int g = level_guess(x, lo, inv_step, static_cast<float>(L));
   g += (x >= thr[g + 1]) ? 1 : 0;
   g -= (x < thr[g]) ? 1 : 0;
   return g;
 }
 
-// ---------------------------------------------------------------------------
 // float basis (bf16 path): local Cox-de Boor triangle in fp32 (grid.hpp:124-140
 // restricted to the P+1 supported functions), knot units.
 template <int PMAX>
@@ -79,20 +86,25 @@ __device__ __forceinline__ int basis_f32(float x, float lo, float hi_open, float
     const float rd = 1.0f / static_cast<float>(d);
 #pragma unroll
     for (int r = 0; r <= d; ++r) {
-      const int i = j - d + r;  // basis index at degree d
-      const float left = (r == 0) ? 0.f : N[PMAX - d + r];        // B_i^{d-1}
-      const float right = (r == d) ? 0.f : N[PMAX - d + r + 1];   // B_{i+1}^{d-1}
+      const int i = j - d + r;
+      const float left = (r == 0) ? 0.f : N[PMAX - d + r];       // B_i^{d-1}
+      const float right = (r == d) ? 0.f : N[PMAX - d + r + 1];  // B_{i+1}^{d-1}
       const float d1 = (xi - static_cast<float>(i)) * rd;
       const float d2 = (static_cast<float>(i + d + 1) - xi) * rd;
       N[PMAX - d + r] = d1 * left + d2 * right;
     }
   }
-  // shift so that N[r] = basis (j - P + r)
   if (P < PMAX) {
+    const int sh = PMAX - P;
 #pragma unroll
-    for (int r = 0; r <= PMAX; ++r) N[r] = (r + PMAX - P <= PMAX) ? N[r + PMAX - P] : 0.f;
+    for (int r = 0; r <= PMAX; ++r) {
+      float v = 0.f;
+#pragma unroll
+      for (int q = 0; q <= PMAX; ++q) v = (q == r + sh) ? N[q] : v;
+      N[r] = v;
+    }
   }
-  return j - P;  // support start
+  return j - P;
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
@@ -100,44 +112,168 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// shift `bits` of new data into the top of a 128-bit little-endian register
+__device__ __forceinline__ void shift_in(uint32_t (&w)[4], uint32_t v, int bits) {
+  w[0] = __funnelshift_r(w[0], w[1], bits);
+  w[1] = __funnelshift_r(w[1], w[2], bits);
+  w[2] = __funnelshift_r(w[2], w[3], bits);
+  w[3] = __funnelshift_r(w[3], v, bits);
+}
+
 // ---------------------------------------------------------------------------
+enum { MODE_PLAIN = 0, MODE_ZP = 1, MODE_SILU = 2 };
+
 template <bool BF16, int NBP, int NPW>
 struct Cfg {
   static constexpr int NP = NPW * 32;
   static constexpr int ESZ = BF16 ? 2 : 1;
-  static constexpr int IPS = 128 / (NBP * ESZ);   // inputs per 128-byte K stage
-  static constexpr int GS = (BF16 ? 64 : 128) / IPS;  // spline stages per silu group
-  static constexpr int RPT = 1024 / NP;           // rows per producer thread per stage
+  static constexpr int IPS = 128 / (NBP * ESZ);       // inputs per 128-byte K stage
+  static constexpr int GS = (BF16 ? 64 : 128) / IPS;  // spline stages per base group
+  static constexpr int RPT = 1024 / NP;               // rows per producer thread per stage
   static constexpr int ROW_STEP = NP / 8;
 };
 
-template <bool BF16, int NBP, int NPW>
+// Fill one 16-byte A chunk (row r, chunk c) for a spline stage.
+template <bool BF16, int NBP, int MODE>
+struct Producer {
+  // LUT path, fp32 or u16 activations
+  static __device__ __forceinline__ uint4 lut_chunk(const GemmParams& p, const uint8_t* tab,
+                                                    const uint8_t* xt, int r, int c, int ips,
+                                                    int i_base, uint32_t& rsum,
+                                                    uint32_t (&silu)[4]) {
+    constexpr int IPC = (NBP == 8) ? 2 : 1;
+    int a[IPC];
+    uint32_t pat[4];
+    const float Lf = static_cast<float>(p.L);
+    if constexpr (NBP == 8) {
+      const uint4* ent = reinterpret_cast<const uint4*>(tab);
+      uint2 pp[2];
+      if (p.x_kind == X_F32) {
+        const float2 xv = *reinterpret_cast<const float2*>(xt + (r * ips + c * 2) * 4);
+        const float xs[2] = {xv.x, xv.y};
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          int g = level_guess(xs[e], p.lo_f, p.inv_step_f, Lf);
+          const uint4 en = ent[g];
+          const int d = (xs[e] >= __uint_as_float(en.y) ? 1 : 0) -
+                        (xs[e] < __uint_as_float(en.x) ? 1 : 0);
+          pp[e] = make_uint2(en.z, en.w);
+          if (d != 0) {
+            g += d;
+            const uint4 e2 = ent[g];
+            pp[e] = make_uint2(e2.z, e2.w);
+          }
+          a[e] = g;
+        }
+      } else {
+        const uint32_t v2 = *reinterpret_cast<const uint32_t*>(xt + (r * ips + c * 2) * 2);
+        a[0] = static_cast<int>(v2 & 0xFFFF);
+        a[1] = static_cast<int>(v2 >> 16);
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const uint4 en = ent[a[e]];
+          pp[e] = make_uint2(en.z, en.w);
+        }
+      }
+      pat[0] = pp[0].x;
+      pat[1] = pp[0].y;
+      pat[2] = pp[1].x;
+      pat[3] = pp[1].y;
+      if constexpr (MODE == MODE_ZP) {
+        const int i0 = i_base + 2 * c;
+        if (i0 < p.n_in) rsum = __dp4a(pat[1], 0x01010101u, __dp4a(pat[0], 0x01010101u, rsum));
+        if (i0 + 1 < p.n_in)
+          rsum = __dp4a(pat[3], 0x01010101u, __dp4a(pat[2], 0x01010101u, rsum));
+      }
+      if constexpr (MODE == MODE_SILU) {
+        const uint8_t* sc = tab + p.off_silu;
+        shift_in(silu, static_cast<uint32_t>(sc[a[0]]) | (static_cast<uint32_t>(sc[a[1]]) << 8), 16);
+      }
+    } else {
+      const float2* thr = reinterpret_cast<const float2*>(tab + p.off_thr);
+      const uint4* pats = reinterpret_cast<const uint4*>(tab + p.off_pat);
+      if (p.x_kind == X_F32) {
+        const float x = *reinterpret_cast<const float*>(xt + (r * ips + c) * 4);
+        int g = level_guess(x, p.lo_f, p.inv_step_f, Lf);
+        const float2 t = thr[g];
+        g += (x >= t.y ? 1 : 0) - (x < t.x ? 1 : 0);
+        a[0] = g;
+      } else {
+        a[0] = *reinterpret_cast<const uint16_t*>(xt + (r * ips + c) * 2);
+      }
+      const uint4 pv = pats[a[0]];
+      pat[0] = pv.x;
+      pat[1] = pv.y;
+      pat[2] = pv.z;
+      pat[3] = pv.w;
+      if constexpr (MODE == MODE_ZP) {
+        if (i_base + c < p.n_in) {
+#pragma unroll
+          for (int w = 0; w < 4; ++w) rsum = __dp4a(pat[w], 0x01010101u, rsum);
+        }
+      }
+      if constexpr (MODE == MODE_SILU) {
+        const uint8_t* sc = tab + p.off_silu;
+        shift_in(silu, static_cast<uint32_t>(sc[a[0]]), 8);
+      }
+    }
+    return make_uint4(pat[0], pat[1], pat[2], pat[3]);
+  }
+
+  // bf16 path: fp32 Cox-de Boor basis, 8 bf16 per chunk
+  static __device__ __forceinline__ uint4 bf16_chunk(const GemmParams& p, const uint8_t* xt, int r,
+                                                     int c, int ips, int s, uint32_t (&silu)[4]) {
+    constexpr int PMAX = 3;
+    const int in_idx = (NBP == 8) ? c : (c >> 1);
+    const int half = (NBP == 8) ? 0 : (c & 1);
+    const float x = *reinterpret_cast<const float*>(xt + (r * ips + in_idx) * 4);
+    float Nv[PMAX + 1];
+    const int jj = basis_f32<PMAX>(x, p.flo, p.fhi_open, p.finv_delta, p.G, p.P, Nv);
+    float v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int rr = 8 * half + e - jj;
+      float val = 0.f;
+#pragma unroll
+      for (int q = 0; q <= PMAX; ++q) val = (rr == q) ? Nv[q] : val;
+      v[e] = val;
+    }
+    if constexpr (MODE == MODE_SILU) {
+      if (NBP == 8 || (s & 1) == half) {
+        const float xc = fminf(fmaxf(x, p.flo), p.fhi_open);
+        const float sv = xc / (1.0f + __expf(-xc));
+        const __nv_bfloat16 b = __float2bfloat16_rn(sv);
+        shift_in(silu, static_cast<uint32_t>(*reinterpret_cast<const uint16_t*>(&b)), 16);
+      }
+    }
+    return make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]),
+                      pack_bf16(v[6], v[7]));
+  }
+};
+
+template <bool BF16, int NBP, int NPW, int MODE>
 __global__ void __launch_bounds__(NPW * 32 + 64, 1)
     kan_gather_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const GemmParams p) {
   using C = Cfg<BF16, NBP, NPW>;
+  constexpr bool SILU = (MODE == MODE_SILU);
+  constexpr bool HAS_B = SILU && !BF16;  // separate base accumulator (LUT path)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  // 1024-align the dynamic smem base (SW128 atoms)
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  // 1024-align the dynamic smem base (SW128 atoms); pointer arithmetic on the
+  // __shared__ array keeps the shared address space visible to the compiler.
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
 
   const int S = p.S;
   const int BN = p.BN;
-  const uint32_t a_bytes = 16384;
+  constexpr uint32_t a_bytes = 16384;
   const uint32_t b_bytes = static_cast<uint32_t>(BN) * 128u;
   const uint32_t xesz = (p.x_kind == X_F32) ? 4u : 2u;
   const uint32_t x_bytes = 128u * C::IPS * xesz;
   uint8_t* sA = smem;
   uint8_t* sB = sA + static_cast<size_t>(S) * a_bytes;
   uint8_t* sX = sB + static_cast<size_t>(S) * b_bytes;
-  uint8_t* sT = sX + static_cast<size_t>(S) * x_bytes;  // tables
-  float* t_thr = reinterpret_cast<float*>(sT);
-  const int L = p.L;
-  const int nthr = BF16 ? 0 : ((p.x_kind == X_F32) ? L + 2 : 0);
-  uint32_t* t_vals = reinterpret_cast<uint32_t*>(t_thr + ((nthr + 3) & ~3));
-  const int nvals = BF16 ? 0 : L + 1;
-  uint8_t* t_silu = reinterpret_cast<uint8_t*>(t_vals + ((nvals + 3) & ~3));
-  const int nsilu = (!BF16 && p.silu) ? L + 1 : 0;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(t_silu + ((nsilu + 15) & ~15));
+  uint8_t* sT = sX + static_cast<size_t>(S) * x_bytes;  // lattice tables (LUT path)
+  const int tab_bytes = BF16 ? 0 : p.tab_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sT + tab_bytes);
   int32_t* s_rowsum = reinterpret_cast<int32_t*>(bars + 4 * S + 2);
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(s_rowsum + 128);
   uint32_t* s_flag = s_tmem + 1;
@@ -149,27 +285,22 @@ __global__ void __launch_bounds__(NPW * 32 + 64, 1)
   const int split = blockIdx.z;
   const int m0 = m_tile * 128;
 
-  // groups handled by this CTA
+  // groups of K stages handled by this CTA
   const int g0 = split * p.groups_per_split;
   const int g1 = min(p.n_groups, g0 + p.groups_per_split);
-  const int spg = C::GS + p.silu;  // schedule stages per full group
+  const int spg = C::GS + (SILU ? 1 : 0);  // schedule stages per full group
+
   auto bar_full_x = [&](int s) { return smem_u32(bars + s); };
   auto bar_full_b = [&](int s) { return smem_u32(bars + S + s); };
   auto bar_full_a = [&](int s) { return smem_u32(bars + 2 * S + s); };
   auto bar_empty = [&](int s) { return smem_u32(bars + 3 * S + s); };
   const uint32_t bar_tmem_full = smem_u32(bars + 4 * S);
+  const uint32_t bar_tab = smem_u32(bars + 4 * S + 1);
 
-  const uint32_t tmem_cols = [&] {
-    uint32_t need = static_cast<uint32_t>(BN) * ((!BF16 && p.silu) ? 2u : 1u);
-    uint32_t c = 32;
-    while (c < need) c <<= 1;
-    return c;
-  }();
+  uint32_t tmem_cols = 32;
+  while (tmem_cols < static_cast<uint32_t>(BN) * (HAS_B ? 2u : 1u)) tmem_cols <<= 1;
 
-  // ---- setup: tables, barriers, TMEM -------------------------------------
-  for (int i = threadIdx.x; i < nthr; i += blockDim.x) t_thr[i] = p.thr[i];
-  for (int i = threadIdx.x; i < nvals; i += blockDim.x) t_vals[i] = p.vals[i];
-  for (int i = threadIdx.x; i < nsilu; i += blockDim.x) t_silu[i] = p.silu_codes[i];
+  // ---- setup: barriers, TMEM ----------------------------------------------
   if (threadIdx.x < 128) s_rowsum[threadIdx.x] = 0;
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -179,6 +310,7 @@ __global__ void __launch_bounds__(NPW * 32 + 64, 1)
       mbar_init(bar_empty(s), 1);
     }
     mbar_init(bar_tmem_full, 1);
+    mbar_init(bar_tab, 1);
     mbar_fence_init();
   }
   if (warp == NPW && lane == 0) tma_prefetch(&xmap);
@@ -191,10 +323,14 @@ __global__ void __launch_bounds__(NPW * 32 + 64, 1)
   if (warp == NPW) {
     // ============================ loader ==================================
     if (lane == 0) {
+      if (tab_bytes > 0) {
+        mbar_arrive_tx(bar_tab, static_cast<uint32_t>(tab_bytes));
+        bulk_load(smem_u32(sT), p.tab, static_cast<uint32_t>(tab_bytes), bar_tab);
+      }
       int idx = 0;
       for (int g = g0; g < g1; ++g) {
         const int nsp = min(C::GS, p.n_spline_stages - g * C::GS);
-        for (int s = 0; s < nsp + p.silu; ++s, ++idx) {
+        for (int s = 0; s < nsp + (SILU ? 1 : 0); ++s, ++idx) {
           const int slot = idx % S;
           const uint32_t ph = (idx / S) & 1;
           mbar_wait(bar_empty(slot), ph ^ 1);
@@ -220,15 +356,15 @@ __global__ void __launch_bounds__(NPW * 32 + 64, 1)
       bool first_s = true, first_b = true;
       for (int g = g0; g < g1; ++g) {
         const int nsp = min(C::GS, p.n_spline_stages - g * C::GS);
-        for (int s = 0; s < nsp + p.silu; ++s, ++idx) {
+        for (int s = 0; s < nsp + (SILU ? 1 : 0); ++s, ++idx) {
           const int slot = idx % S;
           const uint32_t ph = (idx / S) & 1;
           mbar_wait(bar_full_a(slot), ph);
           mbar_wait(bar_full_b(slot), ph);
           tc_fence_after();
-          const bool is_base = (s >= nsp);
-          const uint32_t d = tmem + ((is_base && !BF16) ? static_cast<uint32_t>(BN) : 0u);
-          bool& first = (is_base && !BF16) ? first_b : first_s;
+          const bool is_base = HAS_B && (s >= nsp);
+          const uint32_t d = tmem + (is_base ? static_cast<uint32_t>(BN) : 0u);
+          const bool first = is_base ? first_b : first_s;
           const uint32_t a_addr = smem_u32(sA + static_cast<size_t>(slot) * a_bytes);
           const uint32_t b_addr = smem_u32(sB + static_cast<size_t>(slot) * b_bytes);
 #pragma unroll
@@ -241,7 +377,10 @@ __global__ void __launch_bounds__(NPW * 32 + 64, 1)
             else
               mma_i8(d, ad, bd, idesc, acc);
           }
-          first = false;
+          if (is_base)
+            first_b = false;
+          else
+            first_s = false;
           tc_commit(bar_empty(slot));
         }
       }
@@ -260,18 +399,12 @@ __global__ void __launch_bounds__(NPW * 32 + 64, 1)
 #pragma unroll
       for (int w = 0; w < 4; ++w) silu_w[j][w] = 0;
     }
-    // shift `bits` of new data into the top of a 128-bit little-endian register
-    auto shift_in = [](uint32_t(&w)[4], uint32_t v, int bits) {
-      w[0] = __funnelshift_r(w[0], w[1], bits);
-      w[1] = __funnelshift_r(w[1], w[2], bits);
-      w[2] = __funnelshift_r(w[2], w[3], bits);
-      w[3] = __funnelshift_r(w[3], v, bits);
-    };
+    if (tab_bytes > 0) mbar_wait(bar_tab, 0);
 
     int idx = 0;
     for (int g = g0; g < g1; ++g) {
       const int nsp = min(C::GS, p.n_spline_stages - g * C::GS);
-      for (int s = 0; s < nsp + p.silu; ++s, ++idx) {
+      for (int s = 0; s < nsp + (SILU ? 1 : 0); ++s, ++idx) {
         const int slot = idx % S;
         const uint32_t ph = (idx / S) & 1;
         mbar_wait(bar_full_x(slot), ph);
@@ -283,90 +416,14 @@ __global__ void __launch_bounds__(NPW * 32 + 64, 1)
           for (int j = 0; j < C::RPT; ++j) {
             const int r = r0 + j * C::ROW_STEP;
             uint4 out;
-            if constexpr (!BF16) {
-              constexpr int IPC = (NBP == 8) ? 2 : 1;
-              int a[IPC];
-              if (p.x_kind == X_F32) {
-                const float* xr = reinterpret_cast<const float*>(xt) + r * C::IPS + c * IPC;
-                if constexpr (IPC == 2) {
-                  const float2 xv = *reinterpret_cast<const float2*>(xr);
-                  a[0] = lattice_level_f32(xv.x, t_thr, p.lo_f, p.inv_step_f, L);
-                  a[1] = lattice_level_f32(xv.y, t_thr, p.lo_f, p.inv_step_f, L);
-                } else {
-                  a[0] = lattice_level_f32(xr[0], t_thr, p.lo_f, p.inv_step_f, L);
-                }
-              } else {
-                const uint16_t* xr =
-                    reinterpret_cast<const uint16_t*>(xt) + r * C::IPS + c * IPC;
-                if constexpr (IPC == 2) {
-                  const uint32_t v2 = *reinterpret_cast<const uint32_t*>(xr);
-                  a[0] = static_cast<int>(v2 & 0xFFFF);
-                  a[1] = static_cast<int>(v2 >> 16);
-                } else {
-                  a[0] = xr[0];
-                }
-              }
-              if constexpr (NBP == 8) {
-                const uint32_t v0 = t_vals[a[0]], v1 = t_vals[a[1]];
-                const unsigned long long p0 = static_cast<unsigned long long>(v0)
-                                              << (8 * (a[0] >> p.k));
-                const unsigned long long p1 = static_cast<unsigned long long>(v1)
-                                              << (8 * (a[1] >> p.k));
-                out = make_uint4(static_cast<uint32_t>(p0), static_cast<uint32_t>(p0 >> 32),
-                                 static_cast<uint32_t>(p1), static_cast<uint32_t>(p1 >> 32));
-                if (p.zp) {
-                  const int i0 = i_base + 2 * c;
-                  if (i0 < p.n_in) rsum[j] = __dp4a(v0, 0x01010101u, rsum[j]);
-                  if (i0 + 1 < p.n_in) rsum[j] = __dp4a(v1, 0x01010101u, rsum[j]);
-                }
-                if (p.silu) {
-                  const uint32_t sc = static_cast<uint32_t>(t_silu[a[0]]) |
-                                      (static_cast<uint32_t>(t_silu[a[1]]) << 8);
-                  shift_in(silu_w[j], sc, 16);
-                }
-              } else {
-                const uint32_t v0 = t_vals[a[0]];
-                const int jj = a[0] >> p.k;
-                const int wi = jj >> 2, sh = (jj & 3) * 8;
-                const uint32_t lo = v0 << sh;
-                const uint32_t hi = sh ? (v0 >> (32 - sh)) : 0u;
-                out.x = (wi == 0) ? lo : 0u;
-                out.y = (wi == 1) ? lo : ((wi == 0) ? hi : 0u);
-                out.z = (wi == 2) ? lo : ((wi == 1) ? hi : 0u);
-                out.w = (wi == 3) ? lo : ((wi == 2) ? hi : 0u);
-                if (p.zp && i_base + c < p.n_in) rsum[j] = __dp4a(v0, 0x01010101u, rsum[j]);
-                if (p.silu) shift_in(silu_w[j], static_cast<uint32_t>(t_silu[a[0]]), 8);
-              }
-            } else {
-              // bf16 basis values
-              constexpr int PMAX = 3;
-              const int in_idx = (NBP == 8) ? c : (c >> 1);
-              const int half = (NBP == 8) ? 0 : (c & 1);
-              const float x = reinterpret_cast<const float*>(xt)[r * C::IPS + in_idx];
-              float Nv[PMAX + 1];
-              const int jj = basis_f32<PMAX>(x, p.flo, p.fhi_open, p.finv_delta, p.G, p.P, Nv);
-              float v[8];
-#pragma unroll
-              for (int e = 0; e < 8; ++e) {
-                const int rr = 8 * half + e - jj;
-                float val = 0.f;
-#pragma unroll
-                for (int q = 0; q <= PMAX; ++q) val = (rr == q) ? Nv[q] : val;
-                v[e] = val;
-              }
-              out = make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]),
-                               pack_bf16(v[6], v[7]));
-              if (p.silu && (NBP == 8 || (s & 1) == half)) {
-                const float xc = fminf(fmaxf(x, p.flo), p.fhi_open);
-                const float sv = xc / (1.0f + __expf(-xc));
-                const __nv_bfloat16 b = __float2bfloat16_rn(sv);
-                const uint32_t bits = *reinterpret_cast<const uint16_t*>(&b);
-                shift_in(silu_w[j], bits, 16);
-              }
-            }
+            if constexpr (!BF16)
+              out = Producer<BF16, NBP, MODE>::lut_chunk(p, sT, xt, r, c, C::IPS, i_base, rsum[j],
+                                                         silu_w[j]);
+            else
+              out = Producer<BF16, NBP, MODE>::bf16_chunk(p, xt, r, c, C::IPS, s, silu_w[j]);
             *reinterpret_cast<uint4*>(a_tile + sw128_off(r, c)) = out;
           }
-        } else {
+        } else if constexpr (SILU) {
           // base (SiLU) stage: flush the per-thread 16-byte chunk of each row,
           // first padding the shift register for stages the last group lacks.
           // (bf16 with NBP=16: a thread contributes on stages of parity c&1.)
@@ -393,7 +450,7 @@ __global__ void __launch_bounds__(NPW * 32 + 64, 1)
     }
 
     // ---- row sums of the basis codes (per-tensor zero-point correction) ----
-    if (p.zp) {
+    if constexpr (MODE == MODE_ZP) {
 #pragma unroll
       for (int j = 0; j < C::RPT; ++j) {
         int v = static_cast<int>(rsum[j]);
@@ -414,19 +471,24 @@ __global__ void __launch_bounds__(NPW * 32 + 64, 1)
     const int row = m0 + rloc;
     const uint32_t t_row = tmem + (static_cast<uint32_t>(wq * 32) << 16);
     const int nchunks = BN / 16;
-    const bool has_b = (!BF16 && p.silu);
     int32_t rowsum = s_rowsum[rloc];
     const size_t tile_id = static_cast<size_t>(m_tile) * p.n_tiles_n + n_tile;
+    const int Mpad = p.m_tiles * 128;
+    const int Npad = p.n_tiles_n * BN;
 
     auto finish = [&](int col0, const uint32_t(&ra)[16], const uint32_t(&rb)[16], int32_t rs) {
       if (row >= p.M) return;
+      const size_t base = static_cast<size_t>(row) * p.ld_out + col0;
+      const int nvalid = min(16, p.N - col0);
       if (p.epi == EPI_RAW) {
+        uint32_t* o = reinterpret_cast<uint32_t*>(p.out) + base;
+        uint32_t* o2 = reinterpret_cast<uint32_t*>(p.out2) + base;
+#pragma unroll
         for (int e = 0; e < 16; ++e) {
-          const int j = col0 + e;
-          if (j >= p.N) break;
-          reinterpret_cast<uint32_t*>(p.out)[static_cast<size_t>(row) * p.ld_out + j] = ra[e];
-          if (has_b && p.out2)
-            reinterpret_cast<uint32_t*>(p.out2)[static_cast<size_t>(row) * p.ld_out + j] = rb[e];
+          if (e < nvalid) {
+            o[e] = ra[e];
+            if (HAS_B && p.out2) o2[e] = rb[e];
+          }
         }
         return;
       }
@@ -434,15 +496,15 @@ __global__ void __launch_bounds__(NPW * 32 + 64, 1)
 #pragma unroll
       for (int e = 0; e < 16; ++e) {
         const int j = min(col0 + e, p.N - 1);
-        if (BF16) {
+        if constexpr (BF16) {
           y[e] = static_cast<double>(__uint_as_float(ra[e]));
-        } else if (p.wscheme == 0) {
+        } else if constexpr (MODE == MODE_ZP) {
           const long long v = static_cast<long long>(static_cast<int32_t>(ra[e])) -
                               p.z_w * static_cast<long long>(rs);
           y[e] = __dmul_rn(static_cast<double>(v), p.f_tensor);
         } else {
           double v = __dmul_rn(static_cast<double>(static_cast<int32_t>(ra[e])), p.fs[j]);
-          if (has_b) {
+          if constexpr (HAS_B) {
             const long long vb =
                 static_cast<long long>(static_cast<int32_t>(rb[e])) - p.corr_b[j];
             v = __dadd_rn(v, __dmul_rn(static_cast<double>(vb), p.fb[j]));
@@ -450,8 +512,6 @@ __global__ void __launch_bounds__(NPW * 32 + 64, 1)
           y[e] = v;
         }
       }
-      const size_t base = static_cast<size_t>(row) * p.ld_out + col0;
-      const int nvalid = min(16, p.N - col0);
       if (p.epi == EPI_F32) {
         float* o = reinterpret_cast<float*>(p.out) + base;
         if (nvalid == 16 && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
@@ -461,7 +521,9 @@ __global__ void __launch_bounds__(NPW * 32 + 64, 1)
                 make_float4(__double2float_rn(y[e]), __double2float_rn(y[e + 1]),
                             __double2float_rn(y[e + 2]), __double2float_rn(y[e + 3]));
         } else {
-          for (int e = 0; e < nvalid; ++e) o[e] = __double2float_rn(y[e]);
+#pragma unroll
+          for (int e = 0; e < 16; ++e)
+            if (e < nvalid) o[e] = __double2float_rn(y[e]);
         }
       } else if (p.epi == EPI_LEVEL) {
         uint16_t* o = reinterpret_cast<uint16_t*>(p.out) + base;
@@ -476,14 +538,19 @@ __global__ void __launch_bounds__(NPW * 32 + 64, 1)
           *reinterpret_cast<uint4*>(o) = make_uint4(lv[0], lv[1], lv[2], lv[3]);
           *reinterpret_cast<uint4*>(o + 8) = make_uint4(lv[4], lv[5], lv[6], lv[7]);
         } else {
-          for (int e = 0; e < nvalid; ++e) o[e] = static_cast<uint16_t>(lv[e / 2] >> (16 * (e & 1)));
+#pragma unroll
+          for (int e = 0; e < 16; ++e)
+            if (e < nvalid) o[e] = static_cast<uint16_t>(lv[e / 2] >> (16 * (e & 1)));
         }
       } else {  // EPI_I8
         int8_t* o = reinterpret_cast<int8_t*>(p.out) + base;
-        for (int e = 0; e < nvalid; ++e) {
-          long long q = llround_ref(__ddiv_rn(y[e], p.out_scale));
-          q = q < -127 ? -127 : (q > 127 ? 127 : q);
-          o[e] = static_cast<int8_t>(q);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          if (e < nvalid) {
+            long long q = llround_ref(__ddiv_rn(y[e], p.out_scale));
+            q = q < -127 ? -127 : (q > 127 ? 127 : q);
+            o[e] = static_cast<int8_t>(q);
+          }
         }
       }
     };
@@ -492,33 +559,34 @@ __global__ void __launch_bounds__(NPW * 32 + 64, 1)
       for (int cc = wh; cc < nchunks; cc += NPW / 4) {
         uint32_t ra[16], rb[16];
         tmem_ld16(t_row + cc * 16, ra);
-        if (has_b) tmem_ld16(t_row + BN + cc * 16, rb);
+        if constexpr (HAS_B) tmem_ld16(t_row + BN + cc * 16, rb);
         tmem_wait_ld();
         finish(n_tile * BN + cc * 16, ra, rb, rowsum);
       }
     } else {
-      // split-K: integer partial sums are exact and associative -> bit-exact
+      // split-K: store this split's partial tile, the last CTA sums the
+      // partials in split order (exact for int32, deterministic for fp32)
+      const size_t pbase = (static_cast<size_t>(split) * Mpad + rloc + m0) * Npad + n_tile * BN;
       for (int cc = wh; cc < nchunks; cc += NPW / 4) {
         uint32_t ra[16], rb[16];
         tmem_ld16(t_row + cc * 16, ra);
-        if (has_b) tmem_ld16(t_row + BN + cc * 16, rb);
+        if constexpr (HAS_B) tmem_ld16(t_row + BN + cc * 16, rb);
         tmem_wait_ld();
-        if (row < p.M) {
-          const int col0 = n_tile * BN + cc * 16;
-          for (int e = 0; e < 16; ++e) {
-            const int j = col0 + e;
-            if (j >= p.N) break;
-            const size_t o = static_cast<size_t>(row) * p.N + j;
-            if (BF16)
-              atomicAdd(reinterpret_cast<float*>(p.ws_s) + o, __uint_as_float(ra[e]));
-            else
-              atomicAdd(p.ws_s + o, static_cast<int32_t>(ra[e]));
-            if (has_b) atomicAdd(p.ws_b + o, static_cast<int32_t>(rb[e]));
-          }
+        uint4* ps = reinterpret_cast<uint4*>(p.ws_s + pbase + cc * 16);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          ps[q] = make_uint4(ra[4 * q], ra[4 * q + 1], ra[4 * q + 2], ra[4 * q + 3]);
+        if constexpr (HAS_B) {
+          uint4* pb = reinterpret_cast<uint4*>(p.ws_b + pbase + cc * 16);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            pb[q] = make_uint4(rb[4 * q], rb[4 * q + 1], rb[4 * q + 2], rb[4 * q + 3]);
         }
       }
-      if (p.zp && wh == 0 && row < p.M)
-        atomicAdd(p.ws_rowsum + static_cast<size_t>(n_tile) * p.M + row, rowsum);
+      if constexpr (MODE == MODE_ZP) {
+        if (wh == 0)
+          p.ws_rowsum[(static_cast<size_t>(n_tile) * p.splits + split) * Mpad + m0 + rloc] = rowsum;
+      }
       __threadfence();
       asm volatile("bar.sync 1, %0;" ::"r"(C::NP) : "memory");
       if (threadIdx.x == 0) {
@@ -528,26 +596,50 @@ __global__ void __launch_bounds__(NPW * 32 + 64, 1)
       asm volatile("bar.sync 1, %0;" ::"r"(C::NP) : "memory");
       if (*s_flag) {
         __threadfence();
-        if (p.zp && row < p.M)
-          rowsum = *reinterpret_cast<volatile int32_t*>(p.ws_rowsum +
-                                                        static_cast<size_t>(n_tile) * p.M + row);
-        asm volatile("bar.sync 1, %0;" ::"r"(C::NP) : "memory");
-        if (p.zp && wh == 0 && row < p.M) p.ws_rowsum[static_cast<size_t>(n_tile) * p.M + row] = 0;
+        if constexpr (MODE == MODE_ZP) {
+          rowsum = 0;
+          for (int z = 0; z < p.splits; ++z)
+            rowsum += __ldcg(p.ws_rowsum + (static_cast<size_t>(n_tile) * p.splits + z) * Mpad +
+                             m0 + rloc);
+        }
         for (int cc = wh; cc < nchunks; cc += NPW / 4) {
           uint32_t ra[16], rb[16];
-          const int col0 = n_tile * BN + cc * 16;
 #pragma unroll
           for (int e = 0; e < 16; ++e) {
             ra[e] = 0;
             rb[e] = 0;
-            const int j = col0 + e;
-            if (row < p.M && j < p.N) {
-              const size_t o = static_cast<size_t>(row) * p.N + j;
-              ra[e] = static_cast<uint32_t>(atomicExch(p.ws_s + o, 0));
-              if (has_b) rb[e] = static_cast<uint32_t>(atomicExch(p.ws_b + o, 0));
+          }
+          for (int z = 0; z < p.splits; ++z) {
+            const size_t zb = (static_cast<size_t>(z) * Mpad + rloc + m0) * Npad + n_tile * BN + cc * 16;
+            const int4* ps = reinterpret_cast<const int4*>(p.ws_s + zb);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int4 v = __ldcg(ps + q);
+              if constexpr (BF16) {
+                ra[4 * q] = __float_as_uint(__uint_as_float(ra[4 * q]) + __int_as_float(v.x));
+                ra[4 * q + 1] = __float_as_uint(__uint_as_float(ra[4 * q + 1]) + __int_as_float(v.y));
+                ra[4 * q + 2] = __float_as_uint(__uint_as_float(ra[4 * q + 2]) + __int_as_float(v.z));
+                ra[4 * q + 3] = __float_as_uint(__uint_as_float(ra[4 * q + 3]) + __int_as_float(v.w));
+              } else {
+                ra[4 * q] += static_cast<uint32_t>(v.x);
+                ra[4 * q + 1] += static_cast<uint32_t>(v.y);
+                ra[4 * q + 2] += static_cast<uint32_t>(v.z);
+                ra[4 * q + 3] += static_cast<uint32_t>(v.w);
+              }
+            }
+            if constexpr (HAS_B) {
+              const int4* pb = reinterpret_cast<const int4*>(p.ws_b + zb);
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const int4 v = __ldcg(pb + q);
+                rb[4 * q] += static_cast<uint32_t>(v.x);
+                rb[4 * q + 1] += static_cast<uint32_t>(v.y);
+                rb[4 * q + 2] += static_cast<uint32_t>(v.z);
+                rb[4 * q + 3] += static_cast<uint32_t>(v.w);
+              }
             }
           }
-          finish(col0, ra, rb, rowsum);
+          finish(n_tile * BN + cc * 16, ra, rb, rowsum);
         }
         if (threadIdx.x == 0) p.counters[tile_id] = 0u;
       }
@@ -564,45 +656,51 @@ __global__ void __launch_bounds__(NPW * 32 + 64, 1)
 
 // ---------------------------------------------------------------------------
 // host-side launch helpers (called from kan_engine.cpp)
-template <bool BF16, int NBP, int NPW>
+constexpr int kNPW = 8;
+
+template <bool BF16, int NBP, int MODE>
 static cudaError_t launch_impl(const CUtensorMap& xmap, const GemmParams& p, size_t smem,
                                cudaStream_t st) {
-  auto kfn = kan_gather_gemm_kernel<BF16, NBP, NPW>;
+  auto kfn = kan_gather_gemm_kernel<BF16, NBP, kNPW, MODE>;
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   dim3 grid(p.n_tiles_n, p.m_tiles, p.splits);
-  kfn<<<grid, NPW * 32 + 64, smem, st>>>(xmap, p);
+  kfn<<<grid, kNPW * 32 + 64, smem, st>>>(xmap, p);
   return cudaGetLastError();
 }
 
 int gemm_ips(bool bf16, int nbp) { return 128 / (nbp * (bf16 ? 2 : 1)); }
 int gemm_gs(bool bf16, int nbp) { return (bf16 ? 64 : 128) / gemm_ips(bf16, nbp); }
-constexpr int kNPW = 8;
 int gemm_threads() { return kNPW * 32 + 64; }
 
-size_t gemm_smem_bytes(bool bf16, int nbp, int BN, int S, int x_kind, int L, int silu) {
+size_t gemm_smem_bytes(bool bf16, int nbp, int BN, int S, int x_kind, int tab_bytes) {
   const size_t a = 16384, b = static_cast<size_t>(BN) * 128;
   const size_t x = 128u * gemm_ips(bf16, nbp) * (x_kind == X_F32 ? 4 : 2);
-  size_t t = 0;
-  if (!bf16) {
-    const size_t nthr = (x_kind == X_F32) ? L + 2 : 0;
-    t += ((nthr + 3) & ~size_t(3)) * 4;
-    t += ((L + 1 + 3) & ~size_t(3)) * 4;
-    if (silu) t += (L + 1 + 15) & ~size_t(15);
-  }
-  t += (4 * S + 2) * 8 + 128 * 4 + 16;
+  const size_t t = (bf16 ? 0 : static_cast<size_t>(tab_bytes)) + (4 * S + 2) * 8 + 128 * 4 + 16;
   return 1024 + S * (a + b + x) + t;
 }
 
-cudaError_t launch_gather_gemm(bool bf16, int nbp, const CUtensorMap& xmap, const GemmParams& p,
-                               size_t smem, cudaStream_t st) {
+cudaError_t launch_gather_gemm(bool bf16, int nbp, int mode, const CUtensorMap& xmap,
+                               const GemmParams& p, size_t smem, cudaStream_t st) {
   if (bf16) {
-    if (nbp == 8) return launch_impl<true, 8, kNPW>(xmap, p, smem, st);
-    return launch_impl<true, 16, kNPW>(xmap, p, smem, st);
+    if (mode == MODE_SILU)
+      return nbp == 8 ? launch_impl<true, 8, MODE_SILU>(xmap, p, smem, st)
+                      : launch_impl<true, 16, MODE_SILU>(xmap, p, smem, st);
+    return nbp == 8 ? launch_impl<true, 8, MODE_PLAIN>(xmap, p, smem, st)
+                    : launch_impl<true, 16, MODE_PLAIN>(xmap, p, smem, st);
   }
-  if (nbp == 8) return launch_impl<false, 8, kNPW>(xmap, p, smem, st);
-  return launch_impl<false, 16, kNPW>(xmap, p, smem, st);
+  switch (mode) {
+    case MODE_ZP:
+      return nbp == 8 ? launch_impl<false, 8, MODE_ZP>(xmap, p, smem, st)
+                      : launch_impl<false, 16, MODE_ZP>(xmap, p, smem, st);
+    case MODE_SILU:
+      return nbp == 8 ? launch_impl<false, 8, MODE_SILU>(xmap, p, smem, st)
+                      : launch_impl<false, 16, MODE_SILU>(xmap, p, smem, st);
+    default:
+      return nbp == 8 ? launch_impl<false, 8, MODE_PLAIN>(xmap, p, smem, st)
+                      : launch_impl<false, 16, MODE_PLAIN>(xmap, p, smem, st);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -620,8 +718,8 @@ __global__ void kan_levels_kernel(const float* __restrict__ x, int64_t n,
 
 cudaError_t launch_levels(const float* x, int64_t n, const float* thr, float lo, float inv_step,
                           int L, uint16_t* out, cudaStream_t st) {
-  int64_t nb_ = (n + 255) / 256;
-  int blocks = static_cast<int>(nb_ < 148 * 8 ? nb_ : 148 * 8);
+  const int64_t nb = (n + 255) / 256;
+  int blocks = static_cast<int>(nb < 148 * 8 ? nb : 148 * 8);
   if (blocks < 1) blocks = 1;
   kan_levels_kernel<<<blocks, 256, (L + 2) * sizeof(float), st>>>(x, n, thr, lo, inv_step, L,
                                                                    out);

@@ -23,10 +23,13 @@ struct GemmParams {
   int n_spline_stages, n_groups, silu;
   int total_stages;  // length of the pre-tiled weight schedule per n-tile
   int x_kind;
-  // lattice tables (LUT path)
-  const float* thr;       // [L+2]: thr[n] = smallest fp32 with level >= n; thr[0]=-inf, thr[L+1]=NaN
-  const uint32_t* vals;   // [L+1]: packed LUT values of the P+1 supported bases
-  const uint8_t* silu_codes;  // [L+1]
+  // lattice tables (LUT path), one contiguous blob copied to smem per CTA:
+  //   NBP = 8 : ent[g] (16 B) = {thr[g], thr[g+1], row pattern bytes 0-7}
+  //   NBP = 16: thr pair[g] (8 B) at off_thr, row pattern[g] (16 B) at off_pat
+  //   SiLU codes [L+1] (u8) at off_silu
+  // thr[n] = smallest fp32 with level >= n; thr[0] = -inf, thr[L+1] = NaN.
+  const uint8_t* tab;
+  int tab_bytes, off_thr, off_pat, off_silu;
   int L, k;
   float lo_f, inv_step_f;
   // float basis (bf16 path)
@@ -35,12 +38,13 @@ struct GemmParams {
   // pre-tiled, pre-swizzled weights: [n_tiles_n][total_stages][BN*128] bytes
   const uint8_t* wt;
   int b_signed;
-  // split-K
+  // split-K: every split writes its partial tile, the last CTA of a tile sums
+  // them in split order (int32 sums are exact; fp32 sums are deterministic)
   int splits, groups_per_split;
-  int32_t* ws_s;
-  int32_t* ws_b;
-  int32_t* ws_rowsum;  // [n_tiles_n][M]
-  unsigned* counters;  // [m_tiles * n_tiles_n]
+  int32_t* ws_s;       // [splits][m_tiles*128][n_tiles_n*BN]
+  int32_t* ws_b;       // same, SiLU-base accumulator
+  int32_t* ws_rowsum;  // [n_tiles_n][splits][m_tiles*128]
+  unsigned* counters;  // [m_tiles * n_tiles_n], self-resetting
   // epilogue
   int epi;
   void* out;

