@@ -148,6 +148,11 @@ int kan_engine_last_launches(const kan_engine* e);
  * layer `layer` since profiling was (re)enabled. */
 kan_status kan_engine_set_profiling(kan_engine* e, int on);
 kan_status kan_engine_layer_time_ms(kan_engine* e, int layer, double* total_ms, int64_t* count);
+/* Tuning aid (active when the environment variable KAN_TIMELINE is set at
+ * configure time): per-CTA %globaltimer stamps of layer `layer`'s most recent
+ * launch, 8 per CTA (start, tables ready, first A stage, last A stage, TMEM
+ * full, partials stored, done).  Returns the number of values (8 * CTAs). */
+int64_t kan_engine_layer_timeline(kan_engine* e, int layer, unsigned long long* out, int64_t cap);
 
 /* build_bspline_lut (lut.hpp:103-131) as a host utility. Returns entry count,
  * or -KAN_ERR_INVALID_ARGUMENT. */

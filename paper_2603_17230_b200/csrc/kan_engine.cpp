@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -29,7 +30,7 @@ namespace kan {
 // kernels (kan_gemm.cu / kan_fp32.cu)
 cudaError_t launch_gather_gemm(bool bf16, int nbp, int mode, const CUtensorMap& xmap,
                                const GemmParams& p, size_t smem, cudaStream_t st);
-size_t gemm_smem_bytes(bool bf16, int nbp, int BN, int S, int x_kind, int tab_bytes);
+size_t gemm_smem_bytes(bool bf16, int nbp, int BN, int SA, int SX, int x_kind, int tab_bytes);
 int gemm_ips(bool bf16, int nbp);
 int gemm_gs(bool bf16, int nbp);
 cudaError_t launch_levels(const float* x, int64_t n, const float* thr, float lo, float inv_step,
@@ -95,6 +96,7 @@ struct Layer {
 
 // Device-side state of one configured KAN layer.
 struct PreparedLayer {
+  int layer_index = 0;
   int n_in = 0, N = 0, BN = 0, n_tiles_n = 0, nbp = 8;
   int IPS = 0, GS = 0, n_spline_stages = 0, n_groups = 0, total_stages = 0, silu = 0;
   DevBuf<uint8_t> wt;       // tcgen05 paths: pre-tiled weights
@@ -169,17 +171,20 @@ struct kan_engine {
   std::vector<PreparedLayer> prep;
   DevBuf<float> d_thr;
   DevBuf<uint8_t> d_tab;  // smem table blob (see GemmParams::tab)
-  int tab_bytes = 0, off_thr = 0, off_pat = 0, off_silu = 0;
+  int tab_bytes = 0, off_silu = 0;
   double s_s = 1.0;
   int64_t z_s = 0;
   // workspaces
   DevBuf<uint8_t> act[2];
   DevBuf<float> xstage;
-  DevBuf<int32_t> ws_s, ws_b, ws_rowsum;
-  DevBuf<unsigned> counters;
   DevBuf<float> logits_tmp;
   DevBuf<uint8_t> io_in, io_out;
   int last_launches = 0;
+  // optional per-CTA phase timestamps of each layer's last launch (tuning aid)
+  bool timeline = false;
+  int dbg_flags = 0;  // KAN_DBG_FLAGS (tuning experiments only)
+  std::vector<DevBuf<unsigned long long>> timeline_buf;
+  std::vector<int64_t> timeline_ctas;
   // per-layer kernel timing (kan_engine_set_profiling)
   struct PendingTiming {
     int layer;
@@ -584,28 +589,16 @@ void configure(kan_engine* e, const kan_config* c) {
     auto a16 = [](size_t n) { return (n + 15) / 16 * 16; };
     std::vector<uint8_t> blob;
     const size_t nl = static_cast<size_t>(L) + 1;
-    if (nbp == 8) {
-      e->off_thr = 0;
-      e->off_pat = 8;
-      blob.assign(nl * 16, 0);
-      for (size_t a = 0; a < nl; ++a) {
-        const uint64_t pat = static_cast<uint64_t>(lut_pack(g, cfg.lut_k, e->lut, static_cast<int64_t>(a)))
-                             << (8 * (a >> cfg.lut_k));
-        std::memcpy(&blob[a * 16], &thr[a], 4);
-        std::memcpy(&blob[a * 16 + 4], &thr[a + 1], 4);
-        std::memcpy(&blob[a * 16 + 8], &pat, 8);
-      }
-    } else {
-      e->off_thr = 0;
-      e->off_pat = static_cast<int>(a16(nl * 8));
-      blob.assign(static_cast<size_t>(e->off_pat) + nl * 16, 0);
-      for (size_t a = 0; a < nl; ++a) {
-        std::memcpy(&blob[a * 8], &thr[a], 4);
-        std::memcpy(&blob[a * 8 + 4], &thr[a + 1], 4);
-        const uint32_t v = lut_pack(g, cfg.lut_k, e->lut, static_cast<int64_t>(a));
-        const size_t jj = a >> cfg.lut_k;
-        for (int r = 0; r < 4; ++r)
-          if (jj + r < 16) blob[static_cast<size_t>(e->off_pat) + a * 16 + jj + r] = static_cast<uint8_t>(v >> (8 * r));
+    blob.assign(nl * 16, 0);
+    for (size_t a = 0; a < nl; ++a) {
+      std::memcpy(&blob[a * 16], &thr[a], 4);
+      std::memcpy(&blob[a * 16 + 4], &thr[a + 1], 4);
+      const uint32_t v = lut_pack(g, cfg.lut_k, e->lut, static_cast<int64_t>(a));
+      if (nbp == 8) {
+        const uint64_t pat = static_cast<uint64_t>(v) << (8 * (a >> cfg.lut_k));
+        std::memcpy(&blob[a * 16 + 8], &pat, 8);  // the 8-byte basis row
+      } else {
+        std::memcpy(&blob[a * 16 + 8], &v, 4);  // packed codes, placed in-kernel
       }
     }
     e->off_silu = static_cast<int>(blob.size());
@@ -623,6 +616,11 @@ void configure(kan_engine* e, const kan_config* c) {
   }
   e->prep.clear();
   e->prep.resize(static_cast<size_t>(e->n_kan));
+  e->timeline = std::getenv("KAN_TIMELINE") != nullptr;
+  e->dbg_flags = std::getenv("KAN_DBG_FLAGS") ? std::atoi(std::getenv("KAN_DBG_FLAGS")) : 0;
+  e->timeline_buf.clear();
+  e->timeline_buf.resize(static_cast<size_t>(e->n_kan));
+  e->timeline_ctas.assign(static_cast<size_t>(e->n_kan), 0);
   for (auto& l : e->layers) {
     if (l.type != L_LINEAR && l.type != L_CONV) continue;
     const int nb = g.nb();
@@ -631,6 +629,7 @@ void configure(kan_engine* e, const kan_config* c) {
     if (l.coeffs.size() != static_cast<size_t>(n_in) * nb * N)
       throw InvalidArgument("coefficients of KAN layer " + std::to_string(l.kan_index) + " not set");
     PreparedLayer& pl = e->prep[static_cast<size_t>(l.kan_index)];
+    pl.layer_index = l.kan_index;
     if (cfg.mode == KAN_MODE_FP32)
       prepare_fp32_layer(e, l, pl);
     else
@@ -639,10 +638,12 @@ void configure(kan_engine* e, const kan_config* c) {
   e->configured = true;
 }
 
-// choose ring depth for the smem budget
-int pick_stages(bool bf16, int nbp, int BN, int x_kind, int tab_bytes) {
-  for (int S = 8; S >= 2; --S)
-    if (gemm_smem_bytes(bf16, nbp, BN, S, x_kind, tab_bytes) <= 232448) return S;
+// Ring depths for the smem budget: A/B ring (released by the MMA) up to 4
+// deep, the activation ring (released by the producers) as deep as fits.
+void pick_stages(bool bf16, int nbp, int BN, int x_kind, int tab_bytes, int& SA, int& SX) {
+  for (SA = 4; SA >= 2; --SA)
+    for (SX = 16; SX >= 2; --SX)
+      if (gemm_smem_bytes(bf16, nbp, BN, SA, SX, x_kind, tab_bytes) <= 232448) return;
   throw Unsupported("tile configuration exceeds shared memory");
 }
 
@@ -675,8 +676,6 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
   p.k = e->lat.k;
   p.tab = e->d_tab.p;
   p.tab_bytes = e->tab_bytes;
-  p.off_thr = e->off_thr;
-  p.off_pat = e->off_pat;
   p.off_silu = e->off_silu;
   p.lo_f = static_cast<float>(e->grid.lo);
   p.inv_step_f = bf16 ? 0.f : static_cast<float>(1.0 / e->lat.step);
@@ -688,37 +687,42 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
   p.wt = pl.wt.p;
   p.b_signed = pl.b_signed;
   p.m_tiles = static_cast<int>((M + 127) / 128);
-  // split-K over groups when the tile grid under-fills the 148 SMs
+  p.dbg = nullptr;
+  p.dbg_flags = e->dbg_flags;
+  const int tb = bf16 ? 0 : e->tab_bytes;
+  int SA = 2, SX = 2;
+  pick_stages(bf16, pl.nbp, pl.BN, io.x_kind, tb, SA, SX);
+  p.SA = SA;
+  p.SX = SX;
+  // split-K over a cluster (2, 4 or 8 CTAs along z) when the tile grid
+  // under-fills the 148 SMs; the partial tiles are summed through DSMEM, so
+  // they must fit in the idle A/B rings.
   const int tiles = p.m_tiles * p.n_tiles_n;
-  int splits = e->cfg.split_k > 0 ? e->cfg.split_k : 1;
-  if (e->cfg.split_k <= 0 && tiles < 148) splits = std::min(pl.n_groups, (148 + tiles - 1) / tiles);
-  splits = std::max(1, std::min(splits, pl.n_groups));
-  if (io.epi == EPI_RAW && !bf16) {
-    // raw accumulators are exact under any split
-  }
+  const int nacc = (pl.silu && !bf16) ? 2 : 1;
+  const size_t red_bytes = static_cast<size_t>(128) * (nacc * pl.BN + 4) * 4;
+  const size_t ring_bytes = static_cast<size_t>(SA) * (16384 + static_cast<size_t>(pl.BN) * 128);
+  int want = e->cfg.split_k > 0 ? e->cfg.split_k : 1;
+  if (e->cfg.split_k <= 0 && tiles < 148) want = (148 + tiles - 1) / tiles;
+  int splits = 1;
+  for (int c : {8, 4, 2})
+    if (c <= want && c <= pl.n_groups && red_bytes <= ring_bytes) {
+      splits = c;
+      break;
+    }
   const int gps = (pl.n_groups + splits - 1) / splits;
-  splits = (pl.n_groups + gps - 1) / gps;
   p.splits = splits;
   p.groups_per_split = gps;
-  if (splits > 1) {
-    const size_t mn = static_cast<size_t>(splits) * p.m_tiles * 128 * pl.n_tiles_n * pl.BN;
-    if (e->ws_s.n < mn) e->ws_s.alloc(mn);
-    if (pl.silu && !bf16 && e->ws_b.n < mn) e->ws_b.alloc(mn);
-    const size_t rsz = static_cast<size_t>(pl.n_tiles_n) * splits * p.m_tiles * 128;
-    if (e->ws_rowsum.n < rsz) e->ws_rowsum.alloc(rsz);
-    const size_t ct = static_cast<size_t>(tiles);
-    if (e->counters.n < ct) e->counters.alloc(ct, true);
+  if (e->timeline) {
+    const size_t n = static_cast<size_t>(splits) * p.m_tiles * p.n_tiles_n * 8;
+    auto& buf = e->timeline_buf[static_cast<size_t>(pl.layer_index)];
+    buf.alloc(n, true);
+    p.dbg = buf.p;
+    e->timeline_ctas[static_cast<size_t>(pl.layer_index)] = static_cast<int64_t>(n / 8);
   }
-  p.ws_s = e->ws_s.p;
-  p.ws_b = e->ws_b.p;
-  p.ws_rowsum = e->ws_rowsum.p;
-  p.counters = e->counters.p;
   p.epi = io.epi;
   p.out = io.out;
   p.out2 = io.out2;
   p.ld_out = static_cast<int>(io.ld_out);
-  p.wscheme = pl.wscheme;
-  p.zp = (!bf16 && pl.wscheme == KAN_W_PER_TENSOR_ASYM) ? 1 : 0;
   p.f_tensor = pl.f_tensor;
   p.z_w = pl.z_w;
   p.fs = pl.fs.p;
@@ -727,14 +731,12 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
   p.n_lo = e->grid.lo;
   p.n_hi_open = e->grid.hi_open();
   p.n_step = bf16 ? 1.0 : e->lat.step;
+  p.n_inv_step = 1.0 / p.n_step;
   p.n_L = static_cast<int>(e->lat.L);
   p.out_scale = e->cfg.out_scale;
-  const int box_cols = pl.IPS;
-  const CUtensorMap xmap = make_xmap(io.x, io.x_kind, M, pl.n_in, io.ld_x, box_cols);
-  const int tb = bf16 ? 0 : e->tab_bytes;
-  const int S = pick_stages(bf16, pl.nbp, pl.BN, io.x_kind, tb);
-  p.S = S;
-  const size_t smem = gemm_smem_bytes(bf16, pl.nbp, pl.BN, S, io.x_kind, tb);
+  p.inv_out_scale = 1.0 / e->cfg.out_scale;
+  const CUtensorMap xmap = make_xmap(io.x, io.x_kind, M, pl.n_in, io.ld_x, pl.IPS);
+  const size_t smem = gemm_smem_bytes(bf16, pl.nbp, pl.BN, SA, SX, io.x_kind, tb);
   // kernel variant: 0 plain, 1 per-tensor zero point (reference scheme), 2 SiLU base
   const int mode = pl.silu ? 2 : ((!bf16 && pl.wscheme == KAN_W_PER_TENSOR_ASYM) ? 1 : 0);
   ck(launch_gather_gemm(bf16, pl.nbp, mode, xmap, p, smem, st), "gather_gemm launch");
@@ -1076,6 +1078,18 @@ int64_t kan_engine_lut(const kan_engine* e, uint8_t* out, int64_t cap) {
 }
 
 int kan_engine_last_launches(const kan_engine* e) { return e ? e->last_launches : 0; }
+
+int64_t kan_engine_layer_timeline(kan_engine* e, int layer, unsigned long long* out, int64_t cap) {
+  if (!e || layer < 0 || layer >= static_cast<int>(e->timeline_ctas.size())) return 0;
+  const int64_t n = e->timeline_ctas[static_cast<size_t>(layer)] * 8;
+  if (out && cap >= n && n > 0) {
+    DeviceGuard dg(e->device);
+    cudaDeviceSynchronize();
+    cudaMemcpy(out, e->timeline_buf[static_cast<size_t>(layer)].p, static_cast<size_t>(n) * 8,
+               cudaMemcpyDeviceToHost);
+  }
+  return n;
+}
 
 kan_status kan_engine_set_profiling(kan_engine* e, int on) {
   if (!e) return KAN_ERR_INVALID_ARGUMENT;

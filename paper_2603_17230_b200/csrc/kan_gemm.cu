@@ -120,6 +120,63 @@ __device__ __forceinline__ void shift_in(uint32_t (&w)[4], uint32_t v, int bits)
   w[3] = __funnelshift_r(w[3], v, bits);
 }
 
+
+// Exact ActivationLattice::quantize(clamp_to_domain(y)) without a division on
+// the common path: q = (t - lo) * (1/step) is within ~1e-12 of RN((t-lo)/step)
+// for every level range the engine supports (L <= 4096), so llround(q) equals
+// the reference's llround(RN((t-lo)/step)) unless q lies within 1e-7 of a
+// half-integer; only then is the correctly rounded division evaluated.
+__device__ __forceinline__ int lattice_level_fast(double y, double lo, double hi_open, double step,
+                                                  double inv_step, int L) {
+  double t = (y < lo) ? lo : y;
+  t = (hi_open < t) ? hi_open : t;
+  const double d = __dsub_rn(t, lo);
+  double q = __dmul_rn(d, inv_step);
+  if (fabs(__dsub_rn(__dsub_rn(q, floor(q)), 0.5)) < 1e-7) q = __ddiv_rn(d, step);
+  long long a = llround_ref(q);
+  if (a < 0) a = 0;
+  if (a > L) a = L;
+  return static_cast<int>(a);
+}
+
+// clamp(llround(y / s), -127, 127) with the same guarded-multiply rule
+__device__ __forceinline__ int requant_i8(double y, double s, double inv_s) {
+  double q = __dmul_rn(y, inv_s);
+  if (fabs(q) < 1024.0 && fabs(__dsub_rn(__dsub_rn(q, floor(q)), 0.5)) < 1e-7) q = __ddiv_rn(y, s);
+  long long v = llround_ref(q);
+  v = v < -127 ? -127 : (v > 127 ? 127 : v);
+  return static_cast<int>(v);
+}
+
+// ---- distributed shared memory / cluster helpers ---------------------------
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ uint4 ld_cluster_v4(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared::cluster.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(addr)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_cluster_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
+
 // ---------------------------------------------------------------------------
 enum { MODE_PLAIN = 0, MODE_ZP = 1, MODE_SILU = 2 };
 
@@ -131,183 +188,175 @@ struct Cfg {
   static constexpr int GS = (BF16 ? 64 : 128) / IPS;  // spline stages per base group
   static constexpr int RPT = 1024 / NP;               // rows per producer thread per stage
   static constexpr int ROW_STEP = NP / 8;
+  // inputs of one 16-byte A chunk: u8 NBP=8 -> 2, u8 NBP=16 -> 1, bf16 -> 1
+  static constexpr int IPC = BF16 ? 1 : ((NBP == 8) ? 2 : 1);
 };
 
-// Fill one 16-byte A chunk (row r, chunk c) for a spline stage.
-template <bool BF16, int NBP, int MODE>
-struct Producer {
-  // LUT path, fp32 or u16 activations
-  static __device__ __forceinline__ uint4 lut_chunk(const GemmParams& p, const uint8_t* tab,
-                                                    const uint8_t* xt, int r, int c, int ips,
-                                                    int i_base, uint32_t& rsum,
-                                                    uint32_t (&silu)[4]) {
-    constexpr int IPC = (NBP == 8) ? 2 : 1;
-    int a[IPC];
-    uint32_t pat[4];
-    const float Lf = static_cast<float>(p.L);
-    if constexpr (NBP == 8) {
-      const uint4* ent = reinterpret_cast<const uint4*>(tab);
-      uint2 pp[2];
-      if (p.x_kind == X_F32) {
-        const float2 xv = *reinterpret_cast<const float2*>(xt + (r * ips + c * 2) * 4);
-        const float xs[2] = {xv.x, xv.y};
+// Activation values of one thread for one stage (RPT rows x IPC inputs).
+template <int RPT, int IPC>
+struct XRegs {
+  float f[RPT][IPC];
+  int lv[RPT][IPC];
+};
+
+// One A chunk (16 bytes) of the LUT path from a lattice level / fp32 value.
+template <int NBP, int MODE, int XK>
+__device__ __forceinline__ uint4 lut_chunk(const GemmParams& p, const uint4* ent,
+                                           const uint8_t* silu_tab, const float* xf, const int* xl,
+                                           int i0, uint32_t& rsum, uint32_t (&silu)[4]) {
+  constexpr int IPC = (NBP == 8) ? 2 : 1;
+  int a[IPC];
+  uint32_t pv[IPC][2];
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          int g = level_guess(xs[e], p.lo_f, p.inv_step_f, Lf);
-          const uint4 en = ent[g];
-          const int d = (xs[e] >= __uint_as_float(en.y) ? 1 : 0) -
-                        (xs[e] < __uint_as_float(en.x) ? 1 : 0);
-          pp[e] = make_uint2(en.z, en.w);
-          if (d != 0) {
-            g += d;
-            const uint4 e2 = ent[g];
-            pp[e] = make_uint2(e2.z, e2.w);
-          }
-          a[e] = g;
-        }
-      } else {
-        const uint32_t v2 = *reinterpret_cast<const uint32_t*>(xt + (r * ips + c * 2) * 2);
-        a[0] = static_cast<int>(v2 & 0xFFFF);
-        a[1] = static_cast<int>(v2 >> 16);
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const uint4 en = ent[a[e]];
-          pp[e] = make_uint2(en.z, en.w);
-        }
+  for (int e = 0; e < IPC; ++e) {
+    if constexpr (XK == X_F32) {
+      int g = level_guess(xf[e], p.lo_f, p.inv_step_f, static_cast<float>(p.L));
+      const uint4 en = ent[g];
+      const int d = (xf[e] >= __uint_as_float(en.y) ? 1 : 0) - (xf[e] < __uint_as_float(en.x) ? 1 : 0);
+      uint2 pat = make_uint2(en.z, en.w);
+      g += d;
+      if (d != 0) {
+        const uint4 e2 = ent[g];
+        pat = make_uint2(e2.z, e2.w);
       }
-      pat[0] = pp[0].x;
-      pat[1] = pp[0].y;
-      pat[2] = pp[1].x;
-      pat[3] = pp[1].y;
-      if constexpr (MODE == MODE_ZP) {
-        const int i0 = i_base + 2 * c;
-        if (i0 < p.n_in) rsum = __dp4a(pat[1], 0x01010101u, __dp4a(pat[0], 0x01010101u, rsum));
-        if (i0 + 1 < p.n_in)
-          rsum = __dp4a(pat[3], 0x01010101u, __dp4a(pat[2], 0x01010101u, rsum));
-      }
-      if constexpr (MODE == MODE_SILU) {
-        const uint8_t* sc = tab + p.off_silu;
-        shift_in(silu, static_cast<uint32_t>(sc[a[0]]) | (static_cast<uint32_t>(sc[a[1]]) << 8), 16);
-      }
+      a[e] = g;
+      pv[e][0] = pat.x;
+      pv[e][1] = pat.y;
     } else {
-      const float2* thr = reinterpret_cast<const float2*>(tab + p.off_thr);
-      const uint4* pats = reinterpret_cast<const uint4*>(tab + p.off_pat);
-      if (p.x_kind == X_F32) {
-        const float x = *reinterpret_cast<const float*>(xt + (r * ips + c) * 4);
-        int g = level_guess(x, p.lo_f, p.inv_step_f, Lf);
-        const float2 t = thr[g];
-        g += (x >= t.y ? 1 : 0) - (x < t.x ? 1 : 0);
-        a[0] = g;
-      } else {
-        a[0] = *reinterpret_cast<const uint16_t*>(xt + (r * ips + c) * 2);
-      }
-      const uint4 pv = pats[a[0]];
-      pat[0] = pv.x;
-      pat[1] = pv.y;
-      pat[2] = pv.z;
-      pat[3] = pv.w;
-      if constexpr (MODE == MODE_ZP) {
-        if (i_base + c < p.n_in) {
-#pragma unroll
-          for (int w = 0; w < 4; ++w) rsum = __dp4a(pat[w], 0x01010101u, rsum);
-        }
-      }
-      if constexpr (MODE == MODE_SILU) {
-        const uint8_t* sc = tab + p.off_silu;
-        shift_in(silu, static_cast<uint32_t>(sc[a[0]]), 8);
-      }
+      a[e] = xl[e];
+      const uint4 en = ent[a[e]];
+      pv[e][0] = en.z;
+      pv[e][1] = en.w;
     }
-    return make_uint4(pat[0], pat[1], pat[2], pat[3]);
   }
+  uint4 out;
+  if constexpr (NBP == 8) {
+    out = make_uint4(pv[0][0], pv[0][1], pv[1][0], pv[1][1]);
+    if constexpr (MODE == MODE_ZP) {
+      if (i0 < p.n_in) rsum = __dp4a(pv[0][1], 0x01010101u, __dp4a(pv[0][0], 0x01010101u, rsum));
+      if (i0 + 1 < p.n_in)
+        rsum = __dp4a(pv[1][1], 0x01010101u, __dp4a(pv[1][0], 0x01010101u, rsum));
+    }
+    if constexpr (MODE == MODE_SILU)
+      shift_in(silu, static_cast<uint32_t>(silu_tab[a[0]]) | (static_cast<uint32_t>(silu_tab[a[1]]) << 8), 16);
+  } else {
+    // packed LUT codes placed at byte offset jj = a >> k of the 16-byte row
+    const uint32_t v = pv[0][0];
+    const int jj = a[0] >> p.k;
+    const int wi = jj >> 2, sh = (jj & 3) * 8;
+    const uint32_t lo = __funnelshift_l(0u, v, sh);
+    const uint32_t hi = __funnelshift_l(v, 0u, sh);
+    out.x = (wi == 0) ? lo : 0u;
+    out.y = (wi == 1) ? lo : ((wi == 0) ? hi : 0u);
+    out.z = (wi == 2) ? lo : ((wi == 1) ? hi : 0u);
+    out.w = (wi == 3) ? lo : ((wi == 2) ? hi : 0u);
+    if constexpr (MODE == MODE_ZP) {
+      if (i0 < p.n_in) rsum = __dp4a(v, 0x01010101u, rsum);
+    }
+    if constexpr (MODE == MODE_SILU) shift_in(silu, static_cast<uint32_t>(silu_tab[a[0]]), 8);
+  }
+  return out;
+}
 
-  // bf16 path: fp32 Cox-de Boor basis, 8 bf16 per chunk
-  static __device__ __forceinline__ uint4 bf16_chunk(const GemmParams& p, const uint8_t* xt, int r,
-                                                     int c, int ips, int s, uint32_t (&silu)[4]) {
-    constexpr int PMAX = 3;
-    const int in_idx = (NBP == 8) ? c : (c >> 1);
-    const int half = (NBP == 8) ? 0 : (c & 1);
-    const float x = *reinterpret_cast<const float*>(xt + (r * ips + in_idx) * 4);
-    float Nv[PMAX + 1];
-    const int jj = basis_f32<PMAX>(x, p.flo, p.fhi_open, p.finv_delta, p.G, p.P, Nv);
-    float v[8];
+// One A chunk of the bf16 path: fp32 Cox-de Boor basis, 8 bf16 values.
+template <int NBP, int MODE>
+__device__ __forceinline__ uint4 bf16_chunk(const GemmParams& p, float x, int c, int s,
+                                            uint32_t (&silu)[4]) {
+  constexpr int PMAX = 3;
+  const int half = (NBP == 8) ? 0 : (c & 1);
+  float Nv[PMAX + 1];
+  const int jj = basis_f32<PMAX>(x, p.flo, p.fhi_open, p.finv_delta, p.G, p.P, Nv);
+  float v[8];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const int rr = 8 * half + e - jj;
-      float val = 0.f;
+  for (int e = 0; e < 8; ++e) {
+    const int rr = 8 * half + e - jj;
+    float val = 0.f;
 #pragma unroll
-      for (int q = 0; q <= PMAX; ++q) val = (rr == q) ? Nv[q] : val;
-      v[e] = val;
-    }
-    if constexpr (MODE == MODE_SILU) {
-      if (NBP == 8 || (s & 1) == half) {
-        const float xc = fminf(fmaxf(x, p.flo), p.fhi_open);
-        const float sv = xc / (1.0f + __expf(-xc));
-        const __nv_bfloat16 b = __float2bfloat16_rn(sv);
-        shift_in(silu, static_cast<uint32_t>(*reinterpret_cast<const uint16_t*>(&b)), 16);
-      }
-    }
-    return make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]),
-                      pack_bf16(v[6], v[7]));
+    for (int q = 0; q <= PMAX; ++q) val = (rr == q) ? Nv[q] : val;
+    v[e] = val;
   }
-};
+  if constexpr (MODE == MODE_SILU) {
+    if (NBP == 8 || (s & 1) == half) {
+      const float xc = fminf(fmaxf(x, p.flo), p.fhi_open);
+      const float sv = xc / (1.0f + __expf(-xc));
+      const __nv_bfloat16 b = __float2bfloat16_rn(sv);
+      shift_in(silu, static_cast<uint32_t>(*reinterpret_cast<const uint16_t*>(&b)), 16);
+    }
+  }
+  return make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]),
+                    pack_bf16(v[6], v[7]));
+}
 
 template <bool BF16, int NBP, int NPW, int MODE>
-__global__ void __launch_bounds__(NPW * 32 + 64, 1)
+__global__ void __launch_bounds__(NPW * 32 + 96, 1)
     kan_gather_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const GemmParams p) {
   using C = Cfg<BF16, NBP, NPW>;
   constexpr bool SILU = (MODE == MODE_SILU);
   constexpr bool HAS_B = SILU && !BF16;  // separate base accumulator (LUT path)
+  constexpr int NACC = HAS_B ? 2 : 1;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-align the dynamic smem base (SW128 atoms); pointer arithmetic on the
   // __shared__ array keeps the shared address space visible to the compiler.
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
 
-  const int S = p.S;
+  const int SA = p.SA, SX = p.SX;
   const int BN = p.BN;
   constexpr uint32_t a_bytes = 16384;
   const uint32_t b_bytes = static_cast<uint32_t>(BN) * 128u;
   const uint32_t xesz = (p.x_kind == X_F32) ? 4u : 2u;
   const uint32_t x_bytes = 128u * C::IPS * xesz;
   uint8_t* sA = smem;
-  uint8_t* sB = sA + static_cast<size_t>(S) * a_bytes;
-  uint8_t* sX = sB + static_cast<size_t>(S) * b_bytes;
-  uint8_t* sT = sX + static_cast<size_t>(S) * x_bytes;  // lattice tables (LUT path)
+  uint8_t* sB = sA + static_cast<size_t>(SA) * a_bytes;
+  uint8_t* sX = sB + static_cast<size_t>(SA) * b_bytes;
+  uint8_t* sT = sX + static_cast<size_t>(SX) * x_bytes;  // lattice tables (LUT path)
   const int tab_bytes = BF16 ? 0 : p.tab_bytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sT + tab_bytes);
-  int32_t* s_rowsum = reinterpret_cast<int32_t*>(bars + 4 * S + 2);
+  int32_t* s_rowsum = reinterpret_cast<int32_t*>(bars + 3 * SA + 2 * SX + 2);
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(s_rowsum + 128);
-  uint32_t* s_flag = s_tmem + 1;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  unsigned long long* dbg =
+      p.dbg ? p.dbg + 8 * ((static_cast<size_t>(blockIdx.z) * gridDim.y + blockIdx.y) * gridDim.x +
+                           blockIdx.x)
+            : nullptr;
+  auto stamp = [&](int i) {
+    if (dbg) dbg[i] = globaltimer();
+  };
+  if (threadIdx.x == 0) stamp(0);
   const int m_tile = blockIdx.y;
   const int n_tile = blockIdx.x;
   const int split = blockIdx.z;
   const int m0 = m_tile * 128;
 
-  // groups of K stages handled by this CTA
+  // groups of K stages handled by this CTA (may be empty for the last split)
   const int g0 = split * p.groups_per_split;
   const int g1 = min(p.n_groups, g0 + p.groups_per_split);
+  const bool has_work = g0 < g1;
   const int spg = C::GS + (SILU ? 1 : 0);  // schedule stages per full group
 
-  auto bar_full_x = [&](int s) { return smem_u32(bars + s); };
-  auto bar_full_b = [&](int s) { return smem_u32(bars + S + s); };
-  auto bar_full_a = [&](int s) { return smem_u32(bars + 2 * S + s); };
-  auto bar_empty = [&](int s) { return smem_u32(bars + 3 * S + s); };
-  const uint32_t bar_tmem_full = smem_u32(bars + 4 * S);
-  const uint32_t bar_tab = smem_u32(bars + 4 * S + 1);
+  auto bar_xfull = [&](int s) { return smem_u32(bars + s); };
+  auto bar_xempty = [&](int s) { return smem_u32(bars + SX + s); };
+  auto bar_afull = [&](int s) { return smem_u32(bars + 2 * SX + s); };
+  auto bar_aempty = [&](int s) { return smem_u32(bars + 2 * SX + SA + s); };
+  auto bar_bfull = [&](int s) { return smem_u32(bars + 2 * SX + 2 * SA + s); };
+  const uint32_t bar_tmem_full = smem_u32(bars + 2 * SX + 3 * SA);
+  const uint32_t bar_tab = smem_u32(bars + 2 * SX + 3 * SA + 1);
 
   uint32_t tmem_cols = 32;
-  while (tmem_cols < static_cast<uint32_t>(BN) * (HAS_B ? 2u : 1u)) tmem_cols <<= 1;
+  while (tmem_cols < static_cast<uint32_t>(BN) * NACC) tmem_cols <<= 1;
 
   // ---- setup: barriers, TMEM ----------------------------------------------
   if (threadIdx.x < 128) s_rowsum[threadIdx.x] = 0;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init(bar_full_x(s), 1);
-      mbar_init(bar_full_b(s), 1);
-      mbar_init(bar_full_a(s), NPW);
-      mbar_init(bar_empty(s), 1);
+    for (int s = 0; s < SX; ++s) {
+      mbar_init(bar_xfull(s), 1);
+      mbar_init(bar_xempty(s), NPW);
+    }
+    for (int s = 0; s < SA; ++s) {
+      mbar_init(bar_afull(s), NPW);
+      mbar_init(bar_aempty(s), 1);
+      mbar_init(bar_bfull(s), 1);
     }
     mbar_init(bar_tmem_full, 1);
     mbar_init(bar_tab, 1);
@@ -321,7 +370,22 @@ __global__ void __launch_bounds__(NPW * 32 + 64, 1)
   const uint32_t tmem = *s_tmem;
 
   if (warp == NPW) {
-    // ============================ loader ==================================
+    // ========================= activation loader ==========================
+    if (lane == 0) {
+      int xidx = 0;
+      for (int g = g0; g < g1; ++g) {
+        const int nsp = min(C::GS, p.n_spline_stages - g * C::GS);
+        for (int s = 0; s < nsp; ++s, ++xidx) {
+          const int xs = xidx % SX;
+          mbar_wait(bar_xempty(xs), ((xidx / SX) & 1) ^ 1);
+          mbar_arrive_tx(bar_xfull(xs), x_bytes);
+          tma_load_2d(smem_u32(sX + static_cast<size_t>(xs) * x_bytes), &xmap,
+                      (g * C::GS + s) * C::IPS, m0, bar_xfull(xs));
+        }
+      }
+    }
+  } else if (warp == NPW + 2) {
+    // ===================== table + weight-tile loader =====================
     if (lane == 0) {
       if (tab_bytes > 0) {
         mbar_arrive_tx(bar_tab, static_cast<uint32_t>(tab_bytes));
@@ -331,20 +395,12 @@ __global__ void __launch_bounds__(NPW * 32 + 64, 1)
       for (int g = g0; g < g1; ++g) {
         const int nsp = min(C::GS, p.n_spline_stages - g * C::GS);
         for (int s = 0; s < nsp + (SILU ? 1 : 0); ++s, ++idx) {
-          const int slot = idx % S;
-          const uint32_t ph = (idx / S) & 1;
-          mbar_wait(bar_empty(slot), ph ^ 1);
-          if (s < nsp) {
-            mbar_arrive_tx(bar_full_x(slot), x_bytes);
-            tma_load_2d(smem_u32(sX + static_cast<size_t>(slot) * x_bytes), &xmap,
-                        (g * C::GS + s) * C::IPS, m0, bar_full_x(slot));
-          } else {
-            mbar_arrive(bar_full_x(slot));
-          }
+          const int as = idx % SA;
+          mbar_wait(bar_aempty(as), ((idx / SA) & 1) ^ 1);
           const size_t tile = static_cast<size_t>(n_tile) * p.total_stages + g * spg + s;
-          mbar_arrive_tx(bar_full_b(slot), b_bytes);
-          bulk_load(smem_u32(sB + static_cast<size_t>(slot) * b_bytes), p.wt + tile * b_bytes,
-                    b_bytes, bar_full_b(slot));
+          mbar_arrive_tx(bar_bfull(as), b_bytes);
+          bulk_load(smem_u32(sB + static_cast<size_t>(as) * b_bytes), p.wt + tile * b_bytes,
+                    b_bytes, bar_bfull(as));
         }
       }
     }
@@ -352,23 +408,23 @@ __global__ void __launch_bounds__(NPW * 32 + 64, 1)
     // ============================ MMA issuer ==============================
     if (lane == 0) {
       const uint32_t idesc = BF16 ? idesc_bf16(BN) : idesc_i8(BN, p.b_signed != 0);
+      const int nk = (p.dbg_flags & 2) ? 0 : 4;
       int idx = 0;
       bool first_s = true, first_b = true;
       for (int g = g0; g < g1; ++g) {
         const int nsp = min(C::GS, p.n_spline_stages - g * C::GS);
         for (int s = 0; s < nsp + (SILU ? 1 : 0); ++s, ++idx) {
-          const int slot = idx % S;
-          const uint32_t ph = (idx / S) & 1;
-          mbar_wait(bar_full_a(slot), ph);
-          mbar_wait(bar_full_b(slot), ph);
+          const int as = idx % SA;
+          const uint32_t ph = (idx / SA) & 1;
+          mbar_wait(bar_afull(as), ph);
+          mbar_wait(bar_bfull(as), ph);
           tc_fence_after();
           const bool is_base = HAS_B && (s >= nsp);
           const uint32_t d = tmem + (is_base ? static_cast<uint32_t>(BN) : 0u);
           const bool first = is_base ? first_b : first_s;
-          const uint32_t a_addr = smem_u32(sA + static_cast<size_t>(slot) * a_bytes);
-          const uint32_t b_addr = smem_u32(sB + static_cast<size_t>(slot) * b_bytes);
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
+          const uint32_t a_addr = smem_u32(sA + static_cast<size_t>(as) * a_bytes);
+          const uint32_t b_addr = smem_u32(sB + static_cast<size_t>(as) * b_bytes);
+          for (int kk = 0; kk < nk; ++kk) {
             const uint64_t ad = umma_desc_sw128(a_addr + 32 * kk);
             const uint64_t bd = umma_desc_sw128(b_addr + 32 * kk);
             const uint32_t acc = (first && kk == 0) ? 0u : 1u;
@@ -381,7 +437,7 @@ __global__ void __launch_bounds__(NPW * 32 + 64, 1)
             first_b = false;
           else
             first_s = false;
-          tc_commit(bar_empty(slot));
+          tc_commit(bar_aempty(as));
         }
       }
       tc_commit(bar_tmem_full);
@@ -400,33 +456,81 @@ __global__ void __launch_bounds__(NPW * 32 + 64, 1)
       for (int w = 0; w < 4; ++w) silu_w[j][w] = 0;
     }
     if (tab_bytes > 0) mbar_wait(bar_tab, 0);
+    if (pt == 0) stamp(1);
+    const uint4* ent = reinterpret_cast<const uint4*>(sT);
+    const uint8_t* silu_tab = sT + p.off_silu;
 
-    int idx = 0;
+    int idx = 0, xidx = 0;
     for (int g = g0; g < g1; ++g) {
       const int nsp = min(C::GS, p.n_spline_stages - g * C::GS);
       for (int s = 0; s < nsp + (SILU ? 1 : 0); ++s, ++idx) {
-        const int slot = idx % S;
-        const uint32_t ph = (idx / S) & 1;
-        mbar_wait(bar_full_x(slot), ph);
-        uint8_t* a_tile = sA + static_cast<size_t>(slot) * a_bytes;
+        const int as = idx % SA;
+        const uint32_t aph = (idx / SA) & 1;
+        uint8_t* a_tile = sA + static_cast<size_t>(as) * a_bytes;
         if (s < nsp) {
-          const uint8_t* xt = sX + static_cast<size_t>(slot) * x_bytes;
-          const int i_base = (g * C::GS + s) * C::IPS;
+          // 1. activations of this stage -> registers, release the x slot
+          const int xs = xidx % SX;
+          mbar_wait(bar_xfull(xs), (xidx / SX) & 1);
+          ++xidx;
+          const uint8_t* xt = sX + static_cast<size_t>(xs) * x_bytes;
+          XRegs<C::RPT, C::IPC> xr;
+          const int in_c = BF16 ? ((NBP == 8) ? c : (c >> 1)) : c * C::IPC;
+          if (BF16 || p.x_kind == X_F32) {
 #pragma unroll
-          for (int j = 0; j < C::RPT; ++j) {
-            const int r = r0 + j * C::ROW_STEP;
-            uint4 out;
-            if constexpr (!BF16)
-              out = Producer<BF16, NBP, MODE>::lut_chunk(p, sT, xt, r, c, C::IPS, i_base, rsum[j],
-                                                         silu_w[j]);
-            else
-              out = Producer<BF16, NBP, MODE>::bf16_chunk(p, xt, r, c, C::IPS, s, silu_w[j]);
-            *reinterpret_cast<uint4*>(a_tile + sw128_off(r, c)) = out;
+            for (int j = 0; j < C::RPT; ++j) {
+              const float* xp = reinterpret_cast<const float*>(xt) + (r0 + j * C::ROW_STEP) * C::IPS + in_c;
+              if constexpr (C::IPC == 2) {
+                const float2 v = *reinterpret_cast<const float2*>(xp);
+                xr.f[j][0] = v.x;
+                xr.f[j][1] = v.y;
+              } else {
+                xr.f[j][0] = xp[0];
+              }
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < C::RPT; ++j) {
+              const uint16_t* xp = reinterpret_cast<const uint16_t*>(xt) + (r0 + j * C::ROW_STEP) * C::IPS + in_c;
+              if constexpr (C::IPC == 2) {
+                const uint32_t v = *reinterpret_cast<const uint32_t*>(xp);
+                xr.lv[j][0] = static_cast<int>(v & 0xFFFF);
+                xr.lv[j][1] = static_cast<int>(v >> 16);
+              } else {
+                xr.lv[j][0] = xp[0];
+              }
+            }
           }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(bar_xempty(xs));
+          // 2. wait for the A slot, expand levels into basis rows
+          mbar_wait(bar_aempty(as), aph ^ 1);
+          const int i0 = (g * C::GS + s) * C::IPS + in_c;
+          uint4 out[C::RPT];
+          if (p.dbg_flags & 1) {
+#pragma unroll
+            for (int j = 0; j < C::RPT; ++j) out[j] = make_uint4(0, 0, 0, 0);
+          } else if constexpr (BF16) {
+#pragma unroll
+            for (int j = 0; j < C::RPT; ++j) out[j] = bf16_chunk<NBP, MODE>(p, xr.f[j][0], c, s, silu_w[j]);
+          } else {
+            if (p.x_kind == X_F32) {
+#pragma unroll
+              for (int j = 0; j < C::RPT; ++j)
+                out[j] = lut_chunk<NBP, MODE, X_F32>(p, ent, silu_tab, xr.f[j], xr.lv[j], i0, rsum[j], silu_w[j]);
+            } else {
+#pragma unroll
+              for (int j = 0; j < C::RPT; ++j)
+                out[j] = lut_chunk<NBP, MODE, X_U16>(p, ent, silu_tab, xr.f[j], xr.lv[j], i0, rsum[j], silu_w[j]);
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < C::RPT; ++j)
+            *reinterpret_cast<uint4*>(a_tile + sw128_off(r0 + j * C::ROW_STEP, c)) = out[j];
         } else if constexpr (SILU) {
           // base (SiLU) stage: flush the per-thread 16-byte chunk of each row,
           // first padding the shift register for stages the last group lacks.
           // (bf16 with NBP=16: a thread contributes on stages of parity c&1.)
+          mbar_wait(bar_aempty(as), aph ^ 1);
           const int bits = BF16 ? 16 : ((NBP == 8) ? 16 : 8);
           int pad = C::GS - nsp;
           if (BF16 && NBP == 16) {
@@ -436,8 +540,7 @@ __global__ void __launch_bounds__(NPW * 32 + 64, 1)
 #pragma unroll
           for (int j = 0; j < C::RPT; ++j) {
             for (int t = 0; t < pad; ++t) shift_in(silu_w[j], 0u, bits);
-            const int r = r0 + j * C::ROW_STEP;
-            *reinterpret_cast<uint4*>(a_tile + sw128_off(r, c)) =
+            *reinterpret_cast<uint4*>(a_tile + sw128_off(r0 + j * C::ROW_STEP, c)) =
                 make_uint4(silu_w[j][0], silu_w[j][1], silu_w[j][2], silu_w[j][3]);
 #pragma unroll
             for (int w = 0; w < 4; ++w) silu_w[j][w] = 0;
@@ -445,9 +548,11 @@ __global__ void __launch_bounds__(NPW * 32 + 64, 1)
         }
         fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) mbar_arrive(bar_full_a(slot));
+        if (lane == 0) mbar_arrive(bar_afull(as));
+        if (pt == 0 && idx == 0) stamp(2);
       }
     }
+    if (pt == 0) stamp(3);
 
     // ---- row sums of the basis codes (per-tensor zero-point correction) ----
     if constexpr (MODE == MODE_ZP) {
@@ -461,190 +566,187 @@ __global__ void __launch_bounds__(NPW * 32 + 64, 1)
       }
     }
     asm volatile("bar.sync 1, %0;" ::"r"(C::NP) : "memory");
+  }
 
-    // ============================ epilogue ================================
-    mbar_wait(bar_tmem_full, 0);
-    tc_fence_after();
-    const int wq = warp & 3;
-    const int wh = warp >> 2;
-    const int rloc = wq * 32 + lane;
-    const int row = m0 + rloc;
-    const uint32_t t_row = tmem + (static_cast<uint32_t>(wq * 32) << 16);
-    const int nchunks = BN / 16;
-    int32_t rowsum = s_rowsum[rloc];
-    const size_t tile_id = static_cast<size_t>(m_tile) * p.n_tiles_n + n_tile;
-    const int Mpad = p.m_tiles * 128;
-    const int Npad = p.n_tiles_n * BN;
+  // ============================ epilogue ==================================
+  const int wq = warp & 3;
+  const int wh = warp >> 2;
+  const int rloc = wq * 32 + lane;
+  const uint32_t t_row = tmem + (static_cast<uint32_t>(wq * 32) << 16);
+  const int nchunks = BN / 16;
 
-    auto finish = [&](int col0, const uint32_t(&ra)[16], const uint32_t(&rb)[16], int32_t rs) {
-      if (row >= p.M) return;
-      const size_t base = static_cast<size_t>(row) * p.ld_out + col0;
-      const int nvalid = min(16, p.N - col0);
-      if (p.epi == EPI_RAW) {
-        uint32_t* o = reinterpret_cast<uint32_t*>(p.out) + base;
-        uint32_t* o2 = reinterpret_cast<uint32_t*>(p.out2) + base;
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          if (e < nvalid) {
-            o[e] = ra[e];
-            if (HAS_B && p.out2) o2[e] = rb[e];
-          }
-        }
-        return;
-      }
-      double y[16];
+  auto finish = [&](int row, int col0, const uint32_t(&ra)[16], const uint32_t(&rb)[16],
+                    int32_t rs) {
+    if (row >= p.M) return;
+    const size_t base = static_cast<size_t>(row) * p.ld_out + col0;
+    const int nvalid = min(16, p.N - col0);
+    if (p.epi == EPI_RAW) {
+      uint32_t* o = reinterpret_cast<uint32_t*>(p.out) + base;
+      uint32_t* o2 = reinterpret_cast<uint32_t*>(p.out2) + base;
 #pragma unroll
       for (int e = 0; e < 16; ++e) {
-        const int j = min(col0 + e, p.N - 1);
-        if constexpr (BF16) {
-          y[e] = static_cast<double>(__uint_as_float(ra[e]));
-        } else if constexpr (MODE == MODE_ZP) {
-          const long long v = static_cast<long long>(static_cast<int32_t>(ra[e])) -
-                              p.z_w * static_cast<long long>(rs);
-          y[e] = __dmul_rn(static_cast<double>(v), p.f_tensor);
-        } else {
-          double v = __dmul_rn(static_cast<double>(static_cast<int32_t>(ra[e])), p.fs[j]);
-          if constexpr (HAS_B) {
-            const long long vb =
-                static_cast<long long>(static_cast<int32_t>(rb[e])) - p.corr_b[j];
-            v = __dadd_rn(v, __dmul_rn(static_cast<double>(vb), p.fb[j]));
-          }
-          y[e] = v;
+        if (e < nvalid) {
+          o[e] = ra[e];
+          if (HAS_B && p.out2) o2[e] = rb[e];
         }
       }
-      if (p.epi == EPI_F32) {
-        float* o = reinterpret_cast<float*>(p.out) + base;
-        if (nvalid == 16 && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
+      return;
+    }
+    double y[16];
 #pragma unroll
-          for (int e = 0; e < 16; e += 4)
-            *reinterpret_cast<float4*>(o + e) =
-                make_float4(__double2float_rn(y[e]), __double2float_rn(y[e + 1]),
-                            __double2float_rn(y[e + 2]), __double2float_rn(y[e + 3]));
-        } else {
-#pragma unroll
-          for (int e = 0; e < 16; ++e)
-            if (e < nvalid) o[e] = __double2float_rn(y[e]);
-        }
-      } else if (p.epi == EPI_LEVEL) {
-        uint16_t* o = reinterpret_cast<uint16_t*>(p.out) + base;
-        uint32_t lv[8];
-#pragma unroll
-        for (int e = 0; e < 16; e += 2) {
-          const uint32_t l0 = lattice_level_f64(y[e], p.n_lo, p.n_hi_open, p.n_step, p.n_L);
-          const uint32_t l1 = lattice_level_f64(y[e + 1], p.n_lo, p.n_hi_open, p.n_step, p.n_L);
-          lv[e / 2] = l0 | (l1 << 16);
-        }
-        if (nvalid == 16 && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
-          *reinterpret_cast<uint4*>(o) = make_uint4(lv[0], lv[1], lv[2], lv[3]);
-          *reinterpret_cast<uint4*>(o + 8) = make_uint4(lv[4], lv[5], lv[6], lv[7]);
-        } else {
-#pragma unroll
-          for (int e = 0; e < 16; ++e)
-            if (e < nvalid) o[e] = static_cast<uint16_t>(lv[e / 2] >> (16 * (e & 1)));
-        }
-      } else {  // EPI_I8
-        int8_t* o = reinterpret_cast<int8_t*>(p.out) + base;
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          if (e < nvalid) {
-            long long q = llround_ref(__ddiv_rn(y[e], p.out_scale));
-            q = q < -127 ? -127 : (q > 127 ? 127 : q);
-            o[e] = static_cast<int8_t>(q);
-          }
-        }
-      }
-    };
-
-    if (p.splits == 1) {
-      for (int cc = wh; cc < nchunks; cc += NPW / 4) {
-        uint32_t ra[16], rb[16];
-        tmem_ld16(t_row + cc * 16, ra);
-        if constexpr (HAS_B) tmem_ld16(t_row + BN + cc * 16, rb);
-        tmem_wait_ld();
-        finish(n_tile * BN + cc * 16, ra, rb, rowsum);
-      }
-    } else {
-      // split-K: store this split's partial tile, the last CTA sums the
-      // partials in split order (exact for int32, deterministic for fp32)
-      const size_t pbase = (static_cast<size_t>(split) * Mpad + rloc + m0) * Npad + n_tile * BN;
-      for (int cc = wh; cc < nchunks; cc += NPW / 4) {
-        uint32_t ra[16], rb[16];
-        tmem_ld16(t_row + cc * 16, ra);
-        if constexpr (HAS_B) tmem_ld16(t_row + BN + cc * 16, rb);
-        tmem_wait_ld();
-        uint4* ps = reinterpret_cast<uint4*>(p.ws_s + pbase + cc * 16);
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          ps[q] = make_uint4(ra[4 * q], ra[4 * q + 1], ra[4 * q + 2], ra[4 * q + 3]);
+    for (int e = 0; e < 16; ++e) {
+      const int j = min(col0 + e, p.N - 1);
+      if constexpr (BF16) {
+        y[e] = static_cast<double>(__uint_as_float(ra[e]));
+      } else if constexpr (MODE == MODE_ZP) {
+        const long long v =
+            static_cast<long long>(static_cast<int32_t>(ra[e])) - p.z_w * static_cast<long long>(rs);
+        y[e] = __dmul_rn(static_cast<double>(v), p.f_tensor);
+      } else {
+        double v = __dmul_rn(static_cast<double>(static_cast<int32_t>(ra[e])), p.fs[j]);
         if constexpr (HAS_B) {
-          uint4* pb = reinterpret_cast<uint4*>(p.ws_b + pbase + cc * 16);
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            pb[q] = make_uint4(rb[4 * q], rb[4 * q + 1], rb[4 * q + 2], rb[4 * q + 3]);
+          const long long vb = static_cast<long long>(static_cast<int32_t>(rb[e])) - p.corr_b[j];
+          v = __dadd_rn(v, __dmul_rn(static_cast<double>(vb), p.fb[j]));
         }
-      }
-      if constexpr (MODE == MODE_ZP) {
-        if (wh == 0)
-          p.ws_rowsum[(static_cast<size_t>(n_tile) * p.splits + split) * Mpad + m0 + rloc] = rowsum;
-      }
-      __threadfence();
-      asm volatile("bar.sync 1, %0;" ::"r"(C::NP) : "memory");
-      if (threadIdx.x == 0) {
-        const unsigned prev = atomicAdd(p.counters + tile_id, 1u);
-        *s_flag = (prev == static_cast<unsigned>(p.splits - 1)) ? 1u : 0u;
-      }
-      asm volatile("bar.sync 1, %0;" ::"r"(C::NP) : "memory");
-      if (*s_flag) {
-        __threadfence();
-        if constexpr (MODE == MODE_ZP) {
-          rowsum = 0;
-          for (int z = 0; z < p.splits; ++z)
-            rowsum += __ldcg(p.ws_rowsum + (static_cast<size_t>(n_tile) * p.splits + z) * Mpad +
-                             m0 + rloc);
-        }
-        for (int cc = wh; cc < nchunks; cc += NPW / 4) {
-          uint32_t ra[16], rb[16];
-#pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            ra[e] = 0;
-            rb[e] = 0;
-          }
-          for (int z = 0; z < p.splits; ++z) {
-            const size_t zb = (static_cast<size_t>(z) * Mpad + rloc + m0) * Npad + n_tile * BN + cc * 16;
-            const int4* ps = reinterpret_cast<const int4*>(p.ws_s + zb);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const int4 v = __ldcg(ps + q);
-              if constexpr (BF16) {
-                ra[4 * q] = __float_as_uint(__uint_as_float(ra[4 * q]) + __int_as_float(v.x));
-                ra[4 * q + 1] = __float_as_uint(__uint_as_float(ra[4 * q + 1]) + __int_as_float(v.y));
-                ra[4 * q + 2] = __float_as_uint(__uint_as_float(ra[4 * q + 2]) + __int_as_float(v.z));
-                ra[4 * q + 3] = __float_as_uint(__uint_as_float(ra[4 * q + 3]) + __int_as_float(v.w));
-              } else {
-                ra[4 * q] += static_cast<uint32_t>(v.x);
-                ra[4 * q + 1] += static_cast<uint32_t>(v.y);
-                ra[4 * q + 2] += static_cast<uint32_t>(v.z);
-                ra[4 * q + 3] += static_cast<uint32_t>(v.w);
-              }
-            }
-            if constexpr (HAS_B) {
-              const int4* pb = reinterpret_cast<const int4*>(p.ws_b + zb);
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                const int4 v = __ldcg(pb + q);
-                rb[4 * q] += static_cast<uint32_t>(v.x);
-                rb[4 * q + 1] += static_cast<uint32_t>(v.y);
-                rb[4 * q + 2] += static_cast<uint32_t>(v.z);
-                rb[4 * q + 3] += static_cast<uint32_t>(v.w);
-              }
-            }
-          }
-          finish(n_tile * BN + cc * 16, ra, rb, rowsum);
-        }
-        if (threadIdx.x == 0) p.counters[tile_id] = 0u;
+        y[e] = v;
       }
     }
+    if (p.epi == EPI_F32) {
+      float* o = reinterpret_cast<float*>(p.out) + base;
+      if (nvalid == 16 && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
+#pragma unroll
+        for (int e = 0; e < 16; e += 4)
+          *reinterpret_cast<float4*>(o + e) =
+              make_float4(__double2float_rn(y[e]), __double2float_rn(y[e + 1]),
+                          __double2float_rn(y[e + 2]), __double2float_rn(y[e + 3]));
+      } else {
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          if (e < nvalid) o[e] = __double2float_rn(y[e]);
+      }
+    } else if (p.epi == EPI_LEVEL) {
+      uint16_t* o = reinterpret_cast<uint16_t*>(p.out) + base;
+      uint32_t lv[8];
+#pragma unroll
+      for (int e = 0; e < 16; e += 2) {
+        const uint32_t l0 = lattice_level_fast(y[e], p.n_lo, p.n_hi_open, p.n_step, p.n_inv_step, p.n_L);
+        const uint32_t l1 = lattice_level_fast(y[e + 1], p.n_lo, p.n_hi_open, p.n_step, p.n_inv_step, p.n_L);
+        lv[e / 2] = l0 | (l1 << 16);
+      }
+      if (nvalid == 16 && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
+        *reinterpret_cast<uint4*>(o) = make_uint4(lv[0], lv[1], lv[2], lv[3]);
+        *reinterpret_cast<uint4*>(o + 8) = make_uint4(lv[4], lv[5], lv[6], lv[7]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          if (e < nvalid) o[e] = static_cast<uint16_t>(lv[e / 2] >> (16 * (e & 1)));
+      }
+    } else {  // EPI_I8
+      int8_t* o = reinterpret_cast<int8_t*>(p.out) + base;
+#pragma unroll
+      for (int e = 0; e < 16; ++e)
+        if (e < nvalid) o[e] = static_cast<int8_t>(requant_i8(y[e], p.out_scale, p.inv_out_scale));
+    }
+  };
+
+  if (p.splits == 1) {
+    if (warp < NPW) {
+      mbar_wait(bar_tmem_full, 0);
+      tc_fence_after();
+      if (threadIdx.x == 0) stamp(4);
+      const int32_t rowsum = s_rowsum[rloc];
+      for (int cc = wh; cc < nchunks; cc += NPW / 4) {
+        uint32_t ra[16], rb[16];
+        tmem_ld16(t_row + cc * 16, ra);
+        if constexpr (HAS_B) tmem_ld16(t_row + BN + cc * 16, rb);
+        tmem_wait_ld();
+        finish(m0 + rloc, n_tile * BN + cc * 16, ra, rb, rowsum);
+      }
+    }
+  } else {
+    // split-K across the cluster: dump the partial accumulators into this
+    // CTA's smem (the A/B rings are idle now), then every CTA reduces a slice
+    // of rows over all peers through distributed shared memory.
+    const int rstride = NACC * BN + 4;  // words per row (+4 breaks bank conflicts)
+    uint32_t* red = reinterpret_cast<uint32_t*>(sA);
+    if (warp < NPW) {
+      if (has_work) {
+        mbar_wait(bar_tmem_full, 0);
+        tc_fence_after();
+      }
+      if (threadIdx.x == 0) stamp(4);
+      for (int cc = wh; cc < nchunks; cc += NPW / 4) {
+        uint32_t ra[16], rb[16];
+        if (has_work) {
+          tmem_ld16(t_row + cc * 16, ra);
+          if constexpr (HAS_B) tmem_ld16(t_row + BN + cc * 16, rb);
+          tmem_wait_ld();
+        } else {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) ra[e] = rb[e] = 0;
+        }
+        uint4* dst = reinterpret_cast<uint4*>(red + rloc * rstride + cc * 16);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) dst[q] = make_uint4(ra[4 * q], ra[4 * q + 1], ra[4 * q + 2], ra[4 * q + 3]);
+        if constexpr (HAS_B) {
+          uint4* dstb = reinterpret_cast<uint4*>(red + rloc * rstride + BN + cc * 16);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) dstb[q] = make_uint4(rb[4 * q], rb[4 * q + 1], rb[4 * q + 2], rb[4 * q + 3]);
+        }
+      }
+    }
+    cluster_sync_all();
+    if (threadIdx.x == 0) stamp(5);
+    if (warp < NPW) {
+      const int S = p.splits;
+      const uint32_t rank = cluster_rank();
+      const int rows_per = 128 / S;
+      const int items = rows_per * nchunks;
+      const uint32_t red_addr = smem_u32(red);
+      const uint32_t rs_addr = smem_u32(s_rowsum);
+      for (int it = threadIdx.x; it < items; it += C::NP) {
+        const int rl = static_cast<int>(rank) * rows_per + it / nchunks;
+        const int cc = it % nchunks;
+        uint32_t ra[16], rb[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) ra[e] = rb[e] = 0;
+        int32_t rs = 0;
+        for (int q = 0; q < S; ++q) {
+          const uint32_t base_a = mapa(red_addr + static_cast<uint32_t>((rl * rstride + cc * 16) * 4), q);
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const uint4 w = ld_cluster_v4(base_a + 16 * v);
+            if constexpr (BF16) {
+              ra[4 * v] = __float_as_uint(__uint_as_float(ra[4 * v]) + __uint_as_float(w.x));
+              ra[4 * v + 1] = __float_as_uint(__uint_as_float(ra[4 * v + 1]) + __uint_as_float(w.y));
+              ra[4 * v + 2] = __float_as_uint(__uint_as_float(ra[4 * v + 2]) + __uint_as_float(w.z));
+              ra[4 * v + 3] = __float_as_uint(__uint_as_float(ra[4 * v + 3]) + __uint_as_float(w.w));
+            } else {
+              ra[4 * v] += w.x;
+              ra[4 * v + 1] += w.y;
+              ra[4 * v + 2] += w.z;
+              ra[4 * v + 3] += w.w;
+            }
+          }
+          if constexpr (HAS_B) {
+            const uint32_t base_b = base_a + static_cast<uint32_t>(BN * 4);
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              const uint4 w = ld_cluster_v4(base_b + 16 * v);
+              rb[4 * v] += w.x;
+              rb[4 * v + 1] += w.y;
+              rb[4 * v + 2] += w.z;
+              rb[4 * v + 3] += w.w;
+            }
+          }
+          if constexpr (MODE == MODE_ZP) rs += static_cast<int32_t>(ld_cluster_u32(mapa(rs_addr + rl * 4, q)));
+        }
+        finish(m0 + rl, n_tile * BN + cc * 16, ra, rb, rs);
+      }
+    }
+    cluster_sync_all();  // peers' smem must outlive every remote read
   }
+  if (threadIdx.x == 0) stamp(6);
 
   tc_fence_before();
   __syncthreads();
@@ -665,20 +767,32 @@ static cudaError_t launch_impl(const CUtensorMap& xmap, const GemmParams& p, siz
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  dim3 grid(p.n_tiles_n, p.m_tiles, p.splits);
-  kfn<<<grid, kNPW * 32 + 64, smem, st>>>(xmap, p);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(p.n_tiles_n, p.m_tiles, p.splits);
+  cfg.blockDim = dim3(kNPW * 32 + 96);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = p.splits;
+  cfg.attrs = attr;
+  cfg.numAttrs = p.splits > 1 ? 1 : 0;
+  e = cudaLaunchKernelEx(&cfg, kfn, xmap, p);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
 int gemm_ips(bool bf16, int nbp) { return 128 / (nbp * (bf16 ? 2 : 1)); }
 int gemm_gs(bool bf16, int nbp) { return (bf16 ? 64 : 128) / gemm_ips(bf16, nbp); }
-int gemm_threads() { return kNPW * 32 + 64; }
+int gemm_threads() { return kNPW * 32 + 96; }
 
-size_t gemm_smem_bytes(bool bf16, int nbp, int BN, int S, int x_kind, int tab_bytes) {
+size_t gemm_smem_bytes(bool bf16, int nbp, int BN, int SA, int SX, int x_kind, int tab_bytes) {
   const size_t a = 16384, b = static_cast<size_t>(BN) * 128;
   const size_t x = 128u * gemm_ips(bf16, nbp) * (x_kind == X_F32 ? 4 : 2);
-  const size_t t = (bf16 ? 0 : static_cast<size_t>(tab_bytes)) + (4 * S + 2) * 8 + 128 * 4 + 16;
-  return 1024 + S * (a + b + x) + t;
+  const size_t t = (bf16 ? 0 : static_cast<size_t>(tab_bytes)) + (3 * SA + 2 * SX + 2) * 8 + 128 * 4 + 16;
+  return 1024 + SA * (a + b) + SX * x + t;
 }
 
 cudaError_t launch_gather_gemm(bool bf16, int nbp, int mode, const CUtensorMap& xmap,

@@ -17,7 +17,8 @@ enum XKind : int { X_F32 = 0, X_U16 = 1 };
 struct GemmParams {
   int M, n_in, N;
   int BN, n_tiles_n;
-  int S;  // ring stages
+  int SA;  // A/B ring stages (released by the MMA)
+  int SX;  // activation ring stages (released by the producers)
   // stage schedule
   int IPS, GS;
   int n_spline_stages, n_groups, silu;
@@ -25,11 +26,11 @@ struct GemmParams {
   int x_kind;
   // lattice tables (LUT path), one contiguous blob copied to smem per CTA:
   //   NBP = 8 : ent[g] (16 B) = {thr[g], thr[g+1], row pattern bytes 0-7}
-  //   NBP = 16: thr pair[g] (8 B) at off_thr, row pattern[g] (16 B) at off_pat
+  //   NBP = 16: ent[g] (16 B) = {thr[g], thr[g+1], packed LUT codes, unused}
   //   SiLU codes [L+1] (u8) at off_silu
   // thr[n] = smallest fp32 with level >= n; thr[0] = -inf, thr[L+1] = NaN.
   const uint8_t* tab;
-  int tab_bytes, off_thr, off_pat, off_silu;
+  int tab_bytes, off_silu;
   int L, k;
   float lo_f, inv_step_f;
   // float basis (bf16 path)
@@ -38,28 +39,29 @@ struct GemmParams {
   // pre-tiled, pre-swizzled weights: [n_tiles_n][total_stages][BN*128] bytes
   const uint8_t* wt;
   int b_signed;
-  // split-K: every split writes its partial tile, the last CTA of a tile sums
-  // them in split order (int32 sums are exact; fp32 sums are deterministic)
+  // split-K over a thread-block cluster of `splits` CTAs along z: partial
+  // accumulators are summed through distributed shared memory (int32 sums are
+  // exact; fp32 sums run in a fixed order, so they are deterministic)
   int splits, groups_per_split;
-  int32_t* ws_s;       // [splits][m_tiles*128][n_tiles_n*BN]
-  int32_t* ws_b;       // same, SiLU-base accumulator
-  int32_t* ws_rowsum;  // [n_tiles_n][splits][m_tiles*128]
-  unsigned* counters;  // [m_tiles * n_tiles_n], self-resetting
   // epilogue
   int epi;
   void* out;
   void* out2;
   int ld_out;
-  int wscheme, zp;
   double f_tensor;
   long long z_w;
-  const double* fs;       // [N]  s_b * s_w[j]
-  const double* fb;       // [N]  s_s * s_wb[j]
+  const double* fs;         // [N]  s_b * s_w[j]
+  const double* fb;         // [N]  s_s * s_wb[j]
   const long long* corr_b;  // [N] z_s * colsum(q_wb[:, j])
-  double n_lo, n_hi_open, n_step;
+  double n_lo, n_hi_open, n_step, n_inv_step;
   int n_L;
-  double out_scale;
+  double out_scale, inv_out_scale;
   int m_tiles;
+  // optional per-CTA phase timestamps (%globaltimer ns) for tuning:
+  // [cta][8] = start, tables ready, first A stage, last A stage, TMEM full,
+  // partials exchanged, done
+  unsigned long long* dbg;
+  int dbg_flags;  // tuning only: bit0 producers write zeros, bit1 skip the MMAs
 };
 
 // fp32 SIMT Cox-de Boor layer (accuracy baseline).

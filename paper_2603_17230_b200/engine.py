@@ -85,6 +85,8 @@ _lib.kan_engine_last_launches.argtypes = [_vp]
 _lib.kan_engine_set_profiling.argtypes = [_vp, C.c_int]
 _lib.kan_engine_layer_time_ms.argtypes = [_vp, C.c_int, C.POINTER(C.c_double),
                                           C.POINTER(C.c_int64)]
+_lib.kan_engine_layer_timeline.argtypes = [_vp, C.c_int, _vp, C.c_int64]
+_lib.kan_engine_layer_timeline.restype = C.c_int64
 _lib.kan_lut_build.argtypes = [C.c_int, C.c_int, C.c_int, _vp, C.c_int64]
 _lib.kan_lut_build.restype = C.c_int64
 _lib.kan_lattice_thresholds.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, _vp,
@@ -99,7 +101,7 @@ EXPORTED = [
     "kan_engine_forward", "kan_engine_forward_host", "kan_engine_predict",
     "kan_engine_layer_levels", "kan_engine_layer_accumulators", "kan_engine_lut",
     "kan_engine_last_launches", "kan_lut_build", "kan_lattice_thresholds",
-    "kan_engine_set_profiling", "kan_engine_layer_time_ms",
+    "kan_engine_set_profiling", "kan_engine_layer_time_ms", "kan_engine_layer_timeline",
 ]
 
 
@@ -291,6 +293,14 @@ class Engine:
 
     def set_profiling(self, on: bool):
         self._check(_lib.kan_engine_set_profiling(self._h, int(bool(on))))
+
+    def layer_timeline(self, layer: int) -> np.ndarray:
+        """[ctas, 8] %globaltimer stamps of the layer's last launch (KAN_TIMELINE=1)."""
+        n = _lib.kan_engine_layer_timeline(self._h, layer, None, 0)
+        out = np.zeros(max(n, 0), dtype=np.uint64)
+        if n > 0:
+            _lib.kan_engine_layer_timeline(self._h, layer, out.ctypes.data, n)
+        return out.reshape(-1, 8)
 
     def layer_time_ms(self, layer: int):
         """(accumulated device ms, launches) of one KAN layer since profiling was enabled."""

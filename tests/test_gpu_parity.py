@@ -187,8 +187,23 @@ def test_fp32_cox_de_boor_path(oracle, ref, dims, G):
     assert rel_err(y, r) < FP32_TOL
 
 
+@pytest.mark.parametrize("dims,G", [([784, 64], 5), ([300, 100], 10), ([3072, 256], 10),
+                                    ([64, 10], 5)])
+def test_bf16_layer(oracle, dims, G):
+    """One KAN layer on the bf16 tensor-core path vs the fp64 reference: 1e-2."""
+    Ws, _ = make_weights(dims, G, seed=6)
+    x = np.random.default_rng(6).uniform(-1.1, 1.1, (1000, dims[0])).astype(np.float32)
+    e = build(dims, G, Ws, [None] * len(Ws), mode="bf16")
+    y = e.model_forward(to_dev(x)).cpu().numpy()
+    r = oracle.linear_forward(oracle.grid(G, 3), x.astype(np.float64), Ws[0])
+    assert rel_err(y, r) < BF16_TOL
+
+
 @pytest.mark.parametrize("dims,G", [([784, 64, 10], 5), ([300, 100, 10], 10)])
-def test_bf16_path(oracle, dims, G):
+def test_bf16_model(oracle, dims, G):
+    """Stacked bf16 layers: the per-layer bf16 rounding of basis and weights is
+    amplified by the next layer's steep basis (knot spacing 2/G), so the model
+    bound is the per-layer 1e-2 times the layer count, plus argmax agreement."""
     Ws, _ = make_weights(dims, G, seed=6)
     x = np.random.default_rng(6).uniform(-1, 1, (1000, dims[0])).astype(np.float32)
     e = build(dims, G, Ws, [None] * len(Ws), mode="bf16")
@@ -197,7 +212,8 @@ def test_bf16_path(oracle, dims, G):
     r = x.astype(np.float64)
     for w in Ws:
         r = oracle.linear_forward(g, r, w)
-    assert rel_err(y, r) < BF16_TOL
+    assert rel_err(y, r) < BF16_TOL * len(Ws)
+    assert (y.argmax(1) == r.argmax(1)).mean() > 0.97
 
 
 @pytest.mark.parametrize("mode", ["fp32", "bf16"])
