@@ -356,11 +356,15 @@ def main():
     value = world * B * args.steps / (ms / 1e3)
 
     # ---- dominant kernel: per-launch device time with CUDA events (engine profiling)
-    prof_steps = min(max(args.steps, 20), 400)
+    # (the event pairs are recorded as graph nodes around each kernel node, so
+    # host launch gaps stay out of the per-launch device time)
+    prof_steps = max(2, min(args.steps, 64 if B * wl.dims[0] < 2 ** 24 else 8))
     eng.set_profiling(True)
-    with torch.cuda.stream(st):
+    pg = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(pg, stream=st):
         for i in range(prof_steps):
             eng.model_forward(xs[i % R], out=outs[i % R], stream=st)
+    pg.replay()
     torch.cuda.synchronize()
     layer_ms = []
     for li in range(len(wl.dims) - 1):

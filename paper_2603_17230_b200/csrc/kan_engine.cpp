@@ -30,7 +30,8 @@ namespace kan {
 // kernels (kan_gemm.cu / kan_fp32.cu)
 cudaError_t launch_gather_gemm(bool bf16, int nbp, int mode, const CUtensorMap& xmap,
                                const GemmParams& p, size_t smem, cudaStream_t st);
-size_t gemm_smem_bytes(bool bf16, int nbp, int BN, int SA, int SX, int x_kind, int tab_bytes);
+size_t gemm_smem_bytes(bool bf16, int nbp, int BN, int SA, int SB, int SX, int x_kind,
+                       int tab_bytes);
 int gemm_ips(bool bf16, int nbp);
 int gemm_gs(bool bf16, int nbp);
 cudaError_t launch_levels(const float* x, int64_t n, const float* thr, float lo, float inv_step,
@@ -171,7 +172,7 @@ struct kan_engine {
   std::vector<PreparedLayer> prep;
   DevBuf<float> d_thr;
   DevBuf<uint8_t> d_tab;  // smem table blob (see GemmParams::tab)
-  int tab_bytes = 0, off_silu = 0;
+  int tab_bytes = 0, off_thr = 0, off_silu = 0;
   double s_s = 1.0;
   int64_t z_s = 0;
   // workspaces
@@ -583,24 +584,19 @@ void configure(kan_engine* e, const kan_config* c) {
       for (int64_t a = 0; a <= L; ++a)
         codes[static_cast<size_t>(a)] = static_cast<uint8_t>(quantize(v[static_cast<size_t>(a)], sq));
     }
-    // smem table blob: per level the threshold pair and the basis-row pattern
-    // (the P+1 LUT codes of lut_basis_lookup placed at the support offset)
-    const int nbp = g.nb() <= 8 ? 8 : 16;
-    auto a16 = [](size_t n) { return (n + 15) / 16 * 16; };
+    // smem table blob: vals[frac] (packed LUT codes per in-interval offset),
+    // then the exact level thresholds, then the SiLU codes
     std::vector<uint8_t> blob;
-    const size_t nl = static_cast<size_t>(L) + 1;
-    blob.assign(nl * 16, 0);
-    for (size_t a = 0; a < nl; ++a) {
-      std::memcpy(&blob[a * 16], &thr[a], 4);
-      std::memcpy(&blob[a * 16 + 4], &thr[a + 1], 4);
-      const uint32_t v = lut_pack(g, cfg.lut_k, e->lut, static_cast<int64_t>(a));
-      if (nbp == 8) {
-        const uint64_t pat = static_cast<uint64_t>(v) << (8 * (a >> cfg.lut_k));
-        std::memcpy(&blob[a * 16 + 8], &pat, 8);  // the 8-byte basis row
-      } else {
-        std::memcpy(&blob[a * 16 + 8], &v, 4);  // packed codes, placed in-kernel
-      }
+    auto a16 = [](size_t n) { return (n + 15) / 16 * 16; };
+    const size_t nfrac = size_t{1} << cfg.lut_k;
+    blob.assign(a16(nfrac * 4), 0);
+    for (size_t f = 0; f < nfrac; ++f) {
+      const uint32_t v = lut_pack(g, cfg.lut_k, e->lut, static_cast<int64_t>(f));  // jj = 0
+      std::memcpy(&blob[f * 4], &v, 4);
     }
+    e->off_thr = static_cast<int>(blob.size());
+    blob.resize(a16(blob.size() + thr.size() * 4), 0);
+    std::memcpy(&blob[static_cast<size_t>(e->off_thr)], thr.data(), thr.size() * 4);
     e->off_silu = static_cast<int>(blob.size());
     if (!codes.empty()) {
       blob.insert(blob.end(), codes.begin(), codes.end());
@@ -638,13 +634,18 @@ void configure(kan_engine* e, const kan_config* c) {
   e->configured = true;
 }
 
-// Ring depths for the smem budget: A/B ring (released by the MMA) up to 4
-// deep, the activation ring (released by the producers) as deep as fits.
-void pick_stages(bool bf16, int nbp, int BN, int x_kind, int tab_bytes, int& SA, int& SX) {
-  for (SA = 4; SA >= 2; --SA)
-    for (SX = 16; SX >= 2; --SX)
-      if (gemm_smem_bytes(bf16, nbp, BN, SA, SX, x_kind, tab_bytes) <= 232448) return;
-  throw Unsupported("tile configuration exceeds shared memory");
+// Ring depths for the smem budget: the A ring only decouples producers from
+// the MMA (2 slots); the weight and activation rings hide L2 / HBM latency, so
+// they get equal depth first and the activation ring takes what is left.
+void pick_stages(bool bf16, int nbp, int BN, int x_kind, int tab_bytes, int& SA, int& SB, int& SX) {
+  const size_t budget = 232448;
+  SA = std::getenv("KAN_SA") ? std::atoi(std::getenv("KAN_SA")) : 2;
+  for (SB = 12; SB >= 2; --SB)
+    if (gemm_smem_bytes(bf16, nbp, BN, SA, SB, SB, x_kind, tab_bytes) <= budget) break;
+  if (SB < 2) throw Unsupported("tile configuration exceeds shared memory");
+  for (SX = 24; SX > SB; --SX)
+    if (gemm_smem_bytes(bf16, nbp, BN, SA, SB, SX, x_kind, tab_bytes) <= budget) break;
+  if (gemm_smem_bytes(bf16, nbp, BN, SA, SB, SX, x_kind, tab_bytes) > budget) SX = SB;
 }
 
 struct LayerIO {
@@ -676,8 +677,9 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
   p.k = e->lat.k;
   p.tab = e->d_tab.p;
   p.tab_bytes = e->tab_bytes;
+  p.off_thr = e->off_thr;
   p.off_silu = e->off_silu;
-  p.lo_f = static_cast<float>(e->grid.lo);
+  p.lo_f = bf16 ? 0.f : static_cast<float>(-e->grid.lo / e->lat.step);
   p.inv_step_f = bf16 ? 0.f : static_cast<float>(1.0 / e->lat.step);
   p.flo = static_cast<float>(e->grid.lo);
   p.fhi_open = std::nextafter(static_cast<float>(e->grid.hi), static_cast<float>(e->grid.lo));
@@ -690,9 +692,10 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
   p.dbg = nullptr;
   p.dbg_flags = e->dbg_flags;
   const int tb = bf16 ? 0 : e->tab_bytes;
-  int SA = 2, SX = 2;
-  pick_stages(bf16, pl.nbp, pl.BN, io.x_kind, tb, SA, SX);
+  int SA = 2, SB = 2, SX = 2;
+  pick_stages(bf16, pl.nbp, pl.BN, io.x_kind, tb, SA, SB, SX);
   p.SA = SA;
+  p.SB = SB;
   p.SX = SX;
   // split-K over a cluster (2, 4 or 8 CTAs along z) when the tile grid
   // under-fills the 148 SMs; the partial tiles are summed through DSMEM, so
@@ -700,7 +703,7 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
   const int tiles = p.m_tiles * p.n_tiles_n;
   const int nacc = (pl.silu && !bf16) ? 2 : 1;
   const size_t red_bytes = static_cast<size_t>(128) * (nacc * pl.BN + 4) * 4;
-  const size_t ring_bytes = static_cast<size_t>(SA) * (16384 + static_cast<size_t>(pl.BN) * 128);
+  const size_t ring_bytes = static_cast<size_t>(SA) * 16384 + static_cast<size_t>(SB) * pl.BN * 128;
   int want = e->cfg.split_k > 0 ? e->cfg.split_k : 1;
   if (e->cfg.split_k <= 0 && tiles < 148) want = (148 + tiles - 1) / tiles;
   int splits = 1;
@@ -736,7 +739,7 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
   p.out_scale = e->cfg.out_scale;
   p.inv_out_scale = 1.0 / e->cfg.out_scale;
   const CUtensorMap xmap = make_xmap(io.x, io.x_kind, M, pl.n_in, io.ld_x, pl.IPS);
-  const size_t smem = gemm_smem_bytes(bf16, pl.nbp, pl.BN, SA, SX, io.x_kind, tb);
+  const size_t smem = gemm_smem_bytes(bf16, pl.nbp, pl.BN, SA, SB, SX, io.x_kind, tb);
   // kernel variant: 0 plain, 1 per-tensor zero point (reference scheme), 2 SiLU base
   const int mode = pl.silu ? 2 : ((!bf16 && pl.wscheme == KAN_W_PER_TENSOR_ASYM) ? 1 : 0);
   ck(launch_gather_gemm(bf16, pl.nbp, mode, xmap, p, smem, st), "gather_gemm launch");
@@ -826,7 +829,9 @@ void forward(kan_engine* e, const float* x, int64_t M, void* out, cudaStream_t s
     if (e->profiling) {
       ck(cudaEventCreate(&ev0), "cudaEventCreate");
       ck(cudaEventCreate(&ev1), "cudaEventCreate");
-      ck(cudaEventRecord(ev0, st), "cudaEventRecord");
+      // External records become graph nodes under stream capture, so the pair
+      // brackets the kernel node itself when the forward is replayed from a graph
+      ck(cudaEventRecordWithFlags(ev0, st, cudaEventRecordExternal), "cudaEventRecord");
     }
     if (fp32) {
       run_fp32_layer(e, pl, M, static_cast<const float*>(cur), cur_ld, static_cast<float*>(dst),
@@ -838,7 +843,7 @@ void forward(kan_engine* e, const float* x, int64_t M, void* out, cudaStream_t s
       run_gemm_layer(e, pl, M, io, st);
     }
     if (e->profiling) {
-      ck(cudaEventRecord(ev1, st), "cudaEventRecord");
+      ck(cudaEventRecordWithFlags(ev1, st, cudaEventRecordExternal), "cudaEventRecord");
       e->pending.push_back({l.kan_index, ev0, ev1});
     }
     cur = dst;

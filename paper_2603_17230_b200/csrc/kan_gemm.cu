@@ -121,6 +121,11 @@ __device__ __forceinline__ void shift_in(uint32_t (&w)[4], uint32_t v, int bits)
 }
 
 
+// Correctly rounded division, kept out of line: it is only taken for values
+// within 1e-7 of a rounding tie, and inlining it per element bloats the
+// epilogue that runs once per CTA out of a cold instruction cache.
+__device__ __noinline__ double ddiv_rn_slow(double a, double b) { return __ddiv_rn(a, b); }
+
 // Exact ActivationLattice::quantize(clamp_to_domain(y)) without a division on
 // the common path: q = (t - lo) * (1/step) is within ~1e-12 of RN((t-lo)/step)
 // for every level range the engine supports (L <= 4096), so llround(q) equals
@@ -132,7 +137,7 @@ __device__ __forceinline__ int lattice_level_fast(double y, double lo, double hi
   t = (hi_open < t) ? hi_open : t;
   const double d = __dsub_rn(t, lo);
   double q = __dmul_rn(d, inv_step);
-  if (fabs(__dsub_rn(__dsub_rn(q, floor(q)), 0.5)) < 1e-7) q = __ddiv_rn(d, step);
+  if (fabs(__dsub_rn(__dsub_rn(q, floor(q)), 0.5)) < 1e-7) q = ddiv_rn_slow(d, step);
   long long a = llround_ref(q);
   if (a < 0) a = 0;
   if (a > L) a = L;
@@ -142,7 +147,7 @@ __device__ __forceinline__ int lattice_level_fast(double y, double lo, double hi
 // clamp(llround(y / s), -127, 127) with the same guarded-multiply rule
 __device__ __forceinline__ int requant_i8(double y, double s, double inv_s) {
   double q = __dmul_rn(y, inv_s);
-  if (fabs(q) < 1024.0 && fabs(__dsub_rn(__dsub_rn(q, floor(q)), 0.5)) < 1e-7) q = __ddiv_rn(y, s);
+  if (fabs(q) < 1024.0 && fabs(__dsub_rn(__dsub_rn(q, floor(q)), 0.5)) < 1e-7) q = ddiv_rn_slow(y, s);
   long long v = llround_ref(q);
   v = v < -127 ? -127 : (v > 127 ? 127 : v);
   return static_cast<int>(v);
@@ -180,6 +185,19 @@ __device__ __forceinline__ uint32_t ld_cluster_u32(uint32_t addr) {
 // ---------------------------------------------------------------------------
 enum { MODE_PLAIN = 0, MODE_ZP = 1, MODE_SILU = 2 };
 
+// ring slot/phase counter without division
+struct Ring {
+  int slot = 0, n;
+  uint32_t phase = 0;
+  __device__ explicit Ring(int n_) : n(n_) {}
+  __device__ __forceinline__ void next() {
+    if (++slot == n) {
+      slot = 0;
+      phase ^= 1u;
+    }
+  }
+};
+
 template <bool BF16, int NBP, int NPW>
 struct Cfg {
   static constexpr int NP = NPW * 32;
@@ -199,59 +217,64 @@ struct XRegs {
   int lv[RPT][IPC];
 };
 
-// One A chunk (16 bytes) of the LUT path from a lattice level / fp32 value.
+// Exact lattice level of an fp32 activation.  t = x*(1/step) - lo/step in one
+// FFMA is within 7e-4 of the exact quotient (|x| <= 1, L <= 4096), so
+// rint(t) is the reference's llround(RN((clamp(x)-lo)/step)) unless t lies
+// within 2e-3 of a half-integer; only then (p ~ 4e-3) is the threshold table
+// thr[n] = min{x : level(x) >= n} consulted.
+__device__ __forceinline__ int lattice_level_x(float x, const GemmParams& p, const float* thr) {
+  float t = fmaf(x, p.inv_step_f, p.lo_f);  // p.lo_f holds -lo/step on this path
+  t = fminf(fmaxf(t, 0.0f), static_cast<float>(p.L));
+  const float tr = rintf(t);
+  int g = static_cast<int>(tr);
+  if (fabsf(fabsf(t - tr) - 0.5f) < 2e-3f) {
+    g = static_cast<int>(floorf(t));
+    g += (x >= thr[g + 1]) ? 1 : 0;
+  }
+  return g;
+}
+
+// One A chunk (16 bytes) of the LUT path.  The P+1 codes of lut_basis_lookup
+// depend only on frac = a mod 2^k (lut.hpp:145-157), so vals[frac] (2^k u32)
+// holds them packed and the chunk is vals[frac] shifted to byte jj = a >> k.
 template <int NBP, int MODE, int XK>
-__device__ __forceinline__ uint4 lut_chunk(const GemmParams& p, const uint4* ent,
-                                           const uint8_t* silu_tab, const float* xf, const int* xl,
-                                           int i0, uint32_t& rsum, uint32_t (&silu)[4]) {
+__device__ __forceinline__ uint4 lut_chunk(const GemmParams& p, const uint32_t* vals,
+                                           const float* thr, const uint8_t* silu_tab,
+                                           const float* xf, const int* xl, int i0, uint32_t& rsum,
+                                           uint32_t (&silu)[4]) {
   constexpr int IPC = (NBP == 8) ? 2 : 1;
+  const int mask = (1 << p.k) - 1;
   int a[IPC];
-  uint32_t pv[IPC][2];
+  uint32_t v[IPC];
 #pragma unroll
   for (int e = 0; e < IPC; ++e) {
-    if constexpr (XK == X_F32) {
-      int g = level_guess(xf[e], p.lo_f, p.inv_step_f, static_cast<float>(p.L));
-      const uint4 en = ent[g];
-      const int d = (xf[e] >= __uint_as_float(en.y) ? 1 : 0) - (xf[e] < __uint_as_float(en.x) ? 1 : 0);
-      uint2 pat = make_uint2(en.z, en.w);
-      g += d;
-      if (d != 0) {
-        const uint4 e2 = ent[g];
-        pat = make_uint2(e2.z, e2.w);
-      }
-      a[e] = g;
-      pv[e][0] = pat.x;
-      pv[e][1] = pat.y;
-    } else {
-      a[e] = xl[e];
-      const uint4 en = ent[a[e]];
-      pv[e][0] = en.z;
-      pv[e][1] = en.w;
-    }
+    a[e] = (XK == X_F32) ? lattice_level_x(xf[e], p, thr) : xl[e];
+    v[e] = vals[a[e] & mask];
   }
   uint4 out;
   if constexpr (NBP == 8) {
-    out = make_uint4(pv[0][0], pv[0][1], pv[1][0], pv[1][1]);
+    const unsigned long long p0 = static_cast<unsigned long long>(v[0]) << (8 * (a[0] >> p.k));
+    const unsigned long long p1 = static_cast<unsigned long long>(v[1]) << (8 * (a[1] >> p.k));
+    out = make_uint4(static_cast<uint32_t>(p0), static_cast<uint32_t>(p0 >> 32),
+                     static_cast<uint32_t>(p1), static_cast<uint32_t>(p1 >> 32));
     if constexpr (MODE == MODE_ZP) {
-      if (i0 < p.n_in) rsum = __dp4a(pv[0][1], 0x01010101u, __dp4a(pv[0][0], 0x01010101u, rsum));
-      if (i0 + 1 < p.n_in)
-        rsum = __dp4a(pv[1][1], 0x01010101u, __dp4a(pv[1][0], 0x01010101u, rsum));
+      // bytes shifted past the 8-byte row are zero codes (see lut_basis_lookup)
+      if (i0 < p.n_in) rsum = __dp4a(v[0], 0x01010101u, rsum);
+      if (i0 + 1 < p.n_in) rsum = __dp4a(v[1], 0x01010101u, rsum);
     }
     if constexpr (MODE == MODE_SILU)
       shift_in(silu, static_cast<uint32_t>(silu_tab[a[0]]) | (static_cast<uint32_t>(silu_tab[a[1]]) << 8), 16);
   } else {
-    // packed LUT codes placed at byte offset jj = a >> k of the 16-byte row
-    const uint32_t v = pv[0][0];
     const int jj = a[0] >> p.k;
     const int wi = jj >> 2, sh = (jj & 3) * 8;
-    const uint32_t lo = __funnelshift_l(0u, v, sh);
-    const uint32_t hi = __funnelshift_l(v, 0u, sh);
+    const uint32_t lo = __funnelshift_l(0u, v[0], sh);
+    const uint32_t hi = __funnelshift_l(v[0], 0u, sh);
     out.x = (wi == 0) ? lo : 0u;
     out.y = (wi == 1) ? lo : ((wi == 0) ? hi : 0u);
     out.z = (wi == 2) ? lo : ((wi == 1) ? hi : 0u);
     out.w = (wi == 3) ? lo : ((wi == 2) ? hi : 0u);
     if constexpr (MODE == MODE_ZP) {
-      if (i0 < p.n_in) rsum = __dp4a(v, 0x01010101u, rsum);
+      if (i0 < p.n_in) rsum = __dp4a(v[0], 0x01010101u, rsum);
     }
     if constexpr (MODE == MODE_SILU) shift_in(silu, static_cast<uint32_t>(silu_tab[a[0]]), 8);
   }
@@ -299,7 +322,7 @@ __global__ void __launch_bounds__(NPW * 32 + 96, 1)
   // __shared__ array keeps the shared address space visible to the compiler.
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
 
-  const int SA = p.SA, SX = p.SX;
+  const int SA = p.SA, SB = p.SB, SX = p.SX;
   const int BN = p.BN;
   constexpr uint32_t a_bytes = 16384;
   const uint32_t b_bytes = static_cast<uint32_t>(BN) * 128u;
@@ -307,12 +330,13 @@ __global__ void __launch_bounds__(NPW * 32 + 96, 1)
   const uint32_t x_bytes = 128u * C::IPS * xesz;
   uint8_t* sA = smem;
   uint8_t* sB = sA + static_cast<size_t>(SA) * a_bytes;
-  uint8_t* sX = sB + static_cast<size_t>(SA) * b_bytes;
+  uint8_t* sX = sB + static_cast<size_t>(SB) * b_bytes;
   uint8_t* sT = sX + static_cast<size_t>(SX) * x_bytes;  // lattice tables (LUT path)
   const int tab_bytes = BF16 ? 0 : p.tab_bytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sT + tab_bytes);
-  int32_t* s_rowsum = reinterpret_cast<int32_t*>(bars + 3 * SA + 2 * SX + 2);
-  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(s_rowsum + 128);
+  int32_t* s_rowsum = reinterpret_cast<int32_t*>(bars + 2 * SA + 2 * SB + 2 * SX + 2);
+  double* s_cols = reinterpret_cast<double*>(s_rowsum + 128);  // [3][BN] fs, fb, corr
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(s_cols + 3 * BN);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -340,14 +364,23 @@ __global__ void __launch_bounds__(NPW * 32 + 96, 1)
   auto bar_afull = [&](int s) { return smem_u32(bars + 2 * SX + s); };
   auto bar_aempty = [&](int s) { return smem_u32(bars + 2 * SX + SA + s); };
   auto bar_bfull = [&](int s) { return smem_u32(bars + 2 * SX + 2 * SA + s); };
-  const uint32_t bar_tmem_full = smem_u32(bars + 2 * SX + 3 * SA);
-  const uint32_t bar_tab = smem_u32(bars + 2 * SX + 3 * SA + 1);
+  auto bar_bempty = [&](int s) { return smem_u32(bars + 2 * SX + 2 * SA + SB + s); };
+  const uint32_t bar_tmem_full = smem_u32(bars + 2 * SX + 2 * SA + 2 * SB);
+  const uint32_t bar_tab = smem_u32(bars + 2 * SX + 2 * SA + 2 * SB + 1);
 
   uint32_t tmem_cols = 32;
   while (tmem_cols < static_cast<uint32_t>(BN) * NACC) tmem_cols <<= 1;
 
   // ---- setup: barriers, TMEM ----------------------------------------------
   if (threadIdx.x < 128) s_rowsum[threadIdx.x] = 0;
+  if constexpr (!BF16 && MODE != MODE_ZP) {
+    for (int i = threadIdx.x; i < BN; i += blockDim.x) {
+      const int j = min(n_tile * BN + i, p.N - 1);
+      s_cols[i] = p.fs[j];
+      s_cols[BN + i] = HAS_B ? p.fb[j] : 0.0;
+      s_cols[2 * BN + i] = HAS_B ? static_cast<double>(p.corr_b[j]) : 0.0;
+    }
+  }
   if (threadIdx.x == 0) {
     for (int s = 0; s < SX; ++s) {
       mbar_init(bar_xfull(s), 1);
@@ -356,7 +389,10 @@ __global__ void __launch_bounds__(NPW * 32 + 96, 1)
     for (int s = 0; s < SA; ++s) {
       mbar_init(bar_afull(s), NPW);
       mbar_init(bar_aempty(s), 1);
+    }
+    for (int s = 0; s < SB; ++s) {
       mbar_init(bar_bfull(s), 1);
+      mbar_init(bar_bempty(s), 1);
     }
     mbar_init(bar_tmem_full, 1);
     mbar_init(bar_tab, 1);
@@ -369,61 +405,73 @@ __global__ void __launch_bounds__(NPW * 32 + 96, 1)
   tc_fence_after();
   const uint32_t tmem = *s_tmem;
 
+  // Role loops run on whole warps (all lanes wait, lane 0 issues) so the warps
+  // stay converged for the aligned barriers and tcgen05 ops that follow.
   if (warp == NPW) {
     // ========================= activation loader ==========================
-    if (lane == 0) {
-      int xidx = 0;
-      for (int g = g0; g < g1; ++g) {
-        const int nsp = min(C::GS, p.n_spline_stages - g * C::GS);
-        for (int s = 0; s < nsp; ++s, ++xidx) {
-          const int xs = xidx % SX;
-          mbar_wait(bar_xempty(xs), ((xidx / SX) & 1) ^ 1);
-          mbar_arrive_tx(bar_xfull(xs), x_bytes);
-          tma_load_2d(smem_u32(sX + static_cast<size_t>(xs) * x_bytes), &xmap,
-                      (g * C::GS + s) * C::IPS, m0, bar_xfull(xs));
+    Ring rx(SX);
+    for (int g = g0; g < g1; ++g) {
+      const int nsp = min(C::GS, p.n_spline_stages - g * C::GS);
+      for (int s = 0; s < nsp; ++s, rx.next()) {
+        const int xs = rx.slot;
+        mbar_wait(bar_xempty(xs), rx.phase ^ 1);
+        if (lane == 0) {
+          if (p.dbg_flags & 8) {
+            mbar_arrive(bar_xfull(xs));
+          } else {
+            mbar_arrive_tx(bar_xfull(xs), x_bytes);
+            tma_load_2d(smem_u32(sX + static_cast<size_t>(xs) * x_bytes), &xmap,
+                        (g * C::GS + s) * C::IPS, m0, bar_xfull(xs));
+          }
         }
+        __syncwarp();
       }
     }
   } else if (warp == NPW + 2) {
     // ===================== table + weight-tile loader =====================
-    if (lane == 0) {
-      if (tab_bytes > 0) {
-        mbar_arrive_tx(bar_tab, static_cast<uint32_t>(tab_bytes));
-        bulk_load(smem_u32(sT), p.tab, static_cast<uint32_t>(tab_bytes), bar_tab);
-      }
-      int idx = 0;
-      for (int g = g0; g < g1; ++g) {
-        const int nsp = min(C::GS, p.n_spline_stages - g * C::GS);
-        for (int s = 0; s < nsp + (SILU ? 1 : 0); ++s, ++idx) {
-          const int as = idx % SA;
-          mbar_wait(bar_aempty(as), ((idx / SA) & 1) ^ 1);
+    if (lane == 0 && tab_bytes > 0) {
+      mbar_arrive_tx(bar_tab, static_cast<uint32_t>(tab_bytes));
+      bulk_load(smem_u32(sT), p.tab, static_cast<uint32_t>(tab_bytes), bar_tab);
+    }
+    __syncwarp();
+    Ring rb(SB);
+    for (int g = g0; g < g1; ++g) {
+      const int nsp = min(C::GS, p.n_spline_stages - g * C::GS);
+      for (int s = 0; s < nsp + (SILU ? 1 : 0); ++s, rb.next()) {
+        const int bs = rb.slot;
+        mbar_wait(bar_bempty(bs), rb.phase ^ 1);
+        if (lane == 0) {
           const size_t tile = static_cast<size_t>(n_tile) * p.total_stages + g * spg + s;
-          mbar_arrive_tx(bar_bfull(as), b_bytes);
-          bulk_load(smem_u32(sB + static_cast<size_t>(as) * b_bytes), p.wt + tile * b_bytes,
-                    b_bytes, bar_bfull(as));
+          if (p.dbg_flags & 16) {
+            mbar_arrive(bar_bfull(bs));
+          } else {
+            mbar_arrive_tx(bar_bfull(bs), b_bytes);
+            bulk_load(smem_u32(sB + static_cast<size_t>(bs) * b_bytes), p.wt + tile * b_bytes,
+                      b_bytes, bar_bfull(bs));
+          }
         }
+        __syncwarp();
       }
     }
   } else if (warp == NPW + 1) {
     // ============================ MMA issuer ==============================
-    if (lane == 0) {
-      const uint32_t idesc = BF16 ? idesc_bf16(BN) : idesc_i8(BN, p.b_signed != 0);
-      const int nk = (p.dbg_flags & 2) ? 0 : 4;
-      int idx = 0;
-      bool first_s = true, first_b = true;
-      for (int g = g0; g < g1; ++g) {
-        const int nsp = min(C::GS, p.n_spline_stages - g * C::GS);
-        for (int s = 0; s < nsp + (SILU ? 1 : 0); ++s, ++idx) {
-          const int as = idx % SA;
-          const uint32_t ph = (idx / SA) & 1;
-          mbar_wait(bar_afull(as), ph);
-          mbar_wait(bar_bfull(as), ph);
-          tc_fence_after();
-          const bool is_base = HAS_B && (s >= nsp);
+    const uint32_t idesc = BF16 ? idesc_bf16(BN) : idesc_i8(BN, p.b_signed != 0);
+    const int nk = (p.dbg_flags & 2) ? 0 : 4;
+    Ring ra(SA), rb(SB);
+    bool first_s = true, first_b = true;
+    for (int g = g0; g < g1; ++g) {
+      const int nsp = min(C::GS, p.n_spline_stages - g * C::GS);
+      for (int s = 0; s < nsp + (SILU ? 1 : 0); ++s, ra.next(), rb.next()) {
+        const int as = ra.slot, bs = rb.slot;
+        mbar_wait(bar_afull(as), ra.phase);
+        mbar_wait(bar_bfull(bs), rb.phase);
+        tc_fence_after();
+        const bool is_base = HAS_B && (s >= nsp);
+        if (lane == 0) {
           const uint32_t d = tmem + (is_base ? static_cast<uint32_t>(BN) : 0u);
           const bool first = is_base ? first_b : first_s;
           const uint32_t a_addr = smem_u32(sA + static_cast<size_t>(as) * a_bytes);
-          const uint32_t b_addr = smem_u32(sB + static_cast<size_t>(as) * b_bytes);
+          const uint32_t b_addr = smem_u32(sB + static_cast<size_t>(bs) * b_bytes);
           for (int kk = 0; kk < nk; ++kk) {
             const uint64_t ad = umma_desc_sw128(a_addr + 32 * kk);
             const uint64_t bd = umma_desc_sw128(b_addr + 32 * kk);
@@ -433,15 +481,23 @@ __global__ void __launch_bounds__(NPW * 32 + 96, 1)
             else
               mma_i8(d, ad, bd, idesc, acc);
           }
-          if (is_base)
-            first_b = false;
-          else
-            first_s = false;
-          tc_commit(bar_aempty(as));
+          if (p.dbg_flags & 64) {
+            mbar_arrive(bar_aempty(as));
+            mbar_arrive(bar_bempty(bs));
+          } else {
+            tc_commit(bar_aempty(as));
+            tc_commit(bar_bempty(bs));
+          }
         }
+        __syncwarp();
+        if (is_base)
+          first_b = false;
+        else
+          first_s = false;
       }
-      tc_commit(bar_tmem_full);
     }
+    if (lane == 0) tc_commit(bar_tmem_full);
+    __syncwarp();
   } else {
     // ============================ producers ===============================
     const int pt = threadIdx.x;
@@ -457,28 +513,37 @@ __global__ void __launch_bounds__(NPW * 32 + 96, 1)
     }
     if (tab_bytes > 0) mbar_wait(bar_tab, 0);
     if (pt == 0) stamp(1);
-    const uint4* ent = reinterpret_cast<const uint4*>(sT);
+    const uint32_t* vals = reinterpret_cast<const uint32_t*>(sT);
+    const float* thr = reinterpret_cast<const float*>(sT + p.off_thr);
     const uint8_t* silu_tab = sT + p.off_silu;
 
-    int idx = 0, xidx = 0;
+    // loop-invariant smem offsets of this thread's chunks
+    const int in_c = BF16 ? ((NBP == 8) ? c : (c >> 1)) : c * C::IPC;
+    uint32_t a_off[C::RPT], x_off[C::RPT];
+#pragma unroll
+    for (int j = 0; j < C::RPT; ++j) {
+      a_off[j] = sw128_off(r0 + j * C::ROW_STEP, c);
+      x_off[j] = static_cast<uint32_t>((r0 + j * C::ROW_STEP) * C::IPS + in_c) * xesz;
+    }
+    Ring ra(SA), rx(SX);
+    int idx = 0;
     for (int g = g0; g < g1; ++g) {
       const int nsp = min(C::GS, p.n_spline_stages - g * C::GS);
-      for (int s = 0; s < nsp + (SILU ? 1 : 0); ++s, ++idx) {
-        const int as = idx % SA;
-        const uint32_t aph = (idx / SA) & 1;
+      for (int s = 0; s < nsp + (SILU ? 1 : 0); ++s, ++idx, ra.next()) {
+        const int as = ra.slot;
+        const uint32_t aph = ra.phase;
         uint8_t* a_tile = sA + static_cast<size_t>(as) * a_bytes;
         if (s < nsp) {
           // 1. activations of this stage -> registers, release the x slot
-          const int xs = xidx % SX;
-          mbar_wait(bar_xfull(xs), (xidx / SX) & 1);
-          ++xidx;
+          const int xs = rx.slot;
+          mbar_wait(bar_xfull(xs), rx.phase);
+          rx.next();
           const uint8_t* xt = sX + static_cast<size_t>(xs) * x_bytes;
           XRegs<C::RPT, C::IPC> xr;
-          const int in_c = BF16 ? ((NBP == 8) ? c : (c >> 1)) : c * C::IPC;
           if (BF16 || p.x_kind == X_F32) {
 #pragma unroll
             for (int j = 0; j < C::RPT; ++j) {
-              const float* xp = reinterpret_cast<const float*>(xt) + (r0 + j * C::ROW_STEP) * C::IPS + in_c;
+              const float* xp = reinterpret_cast<const float*>(xt + x_off[j]);
               if constexpr (C::IPC == 2) {
                 const float2 v = *reinterpret_cast<const float2*>(xp);
                 xr.f[j][0] = v.x;
@@ -490,7 +555,7 @@ __global__ void __launch_bounds__(NPW * 32 + 96, 1)
           } else {
 #pragma unroll
             for (int j = 0; j < C::RPT; ++j) {
-              const uint16_t* xp = reinterpret_cast<const uint16_t*>(xt) + (r0 + j * C::ROW_STEP) * C::IPS + in_c;
+              const uint16_t* xp = reinterpret_cast<const uint16_t*>(xt + x_off[j]);
               if constexpr (C::IPC == 2) {
                 const uint32_t v = *reinterpret_cast<const uint32_t*>(xp);
                 xr.lv[j][0] = static_cast<int>(v & 0xFFFF);
@@ -516,16 +581,15 @@ __global__ void __launch_bounds__(NPW * 32 + 96, 1)
             if (p.x_kind == X_F32) {
 #pragma unroll
               for (int j = 0; j < C::RPT; ++j)
-                out[j] = lut_chunk<NBP, MODE, X_F32>(p, ent, silu_tab, xr.f[j], xr.lv[j], i0, rsum[j], silu_w[j]);
+                out[j] = lut_chunk<NBP, MODE, X_F32>(p, vals, thr, silu_tab, xr.f[j], xr.lv[j], i0, rsum[j], silu_w[j]);
             } else {
 #pragma unroll
               for (int j = 0; j < C::RPT; ++j)
-                out[j] = lut_chunk<NBP, MODE, X_U16>(p, ent, silu_tab, xr.f[j], xr.lv[j], i0, rsum[j], silu_w[j]);
+                out[j] = lut_chunk<NBP, MODE, X_U16>(p, vals, thr, silu_tab, xr.f[j], xr.lv[j], i0, rsum[j], silu_w[j]);
             }
           }
 #pragma unroll
-          for (int j = 0; j < C::RPT; ++j)
-            *reinterpret_cast<uint4*>(a_tile + sw128_off(r0 + j * C::ROW_STEP, c)) = out[j];
+          for (int j = 0; j < C::RPT; ++j) *reinterpret_cast<uint4*>(a_tile + a_off[j]) = out[j];
         } else if constexpr (SILU) {
           // base (SiLU) stage: flush the per-thread 16-byte chunk of each row,
           // first padding the shift register for stages the last group lacks.
@@ -540,13 +604,13 @@ __global__ void __launch_bounds__(NPW * 32 + 96, 1)
 #pragma unroll
           for (int j = 0; j < C::RPT; ++j) {
             for (int t = 0; t < pad; ++t) shift_in(silu_w[j], 0u, bits);
-            *reinterpret_cast<uint4*>(a_tile + sw128_off(r0 + j * C::ROW_STEP, c)) =
+            *reinterpret_cast<uint4*>(a_tile + a_off[j]) =
                 make_uint4(silu_w[j][0], silu_w[j][1], silu_w[j][2], silu_w[j][3]);
 #pragma unroll
             for (int w = 0; w < 4; ++w) silu_w[j][w] = 0;
           }
         }
-        fence_proxy_async_smem();
+        if (!(p.dbg_flags & 32)) fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_afull(as));
         if (pt == 0 && idx == 0) stamp(2);
@@ -575,16 +639,18 @@ __global__ void __launch_bounds__(NPW * 32 + 96, 1)
   const uint32_t t_row = tmem + (static_cast<uint32_t>(wq * 32) << 16);
   const int nchunks = BN / 16;
 
-  auto finish = [&](int row, int col0, const uint32_t(&ra)[16], const uint32_t(&rb)[16],
-                    int32_t rs) {
+  // The epilogue runs once per CTA out of a cold instruction cache, so it
+  // works on 4-column groups in rolled loops to keep its code small.
+  auto finish4 = [&](int row, int col0, const uint32_t(&ra)[4], const uint32_t(&rb)[4],
+                     int32_t rs) {
     if (row >= p.M) return;
     const size_t base = static_cast<size_t>(row) * p.ld_out + col0;
-    const int nvalid = min(16, p.N - col0);
+    const int nvalid = min(4, p.N - col0);
     if (p.epi == EPI_RAW) {
       uint32_t* o = reinterpret_cast<uint32_t*>(p.out) + base;
       uint32_t* o2 = reinterpret_cast<uint32_t*>(p.out2) + base;
 #pragma unroll
-      for (int e = 0; e < 16; ++e) {
+      for (int e = 0; e < 4; ++e) {
         if (e < nvalid) {
           o[e] = ra[e];
           if (HAS_B && p.out2) o2[e] = rb[e];
@@ -592,10 +658,10 @@ __global__ void __launch_bounds__(NPW * 32 + 96, 1)
       }
       return;
     }
-    double y[16];
+    double y[4];
 #pragma unroll
-    for (int e = 0; e < 16; ++e) {
-      const int j = min(col0 + e, p.N - 1);
+    for (int e = 0; e < 4; ++e) {
+      const int jl = col0 - n_tile * BN + e;  // column within this CTA's tile
       if constexpr (BF16) {
         y[e] = static_cast<double>(__uint_as_float(ra[e]));
       } else if constexpr (MODE == MODE_ZP) {
@@ -603,51 +669,40 @@ __global__ void __launch_bounds__(NPW * 32 + 96, 1)
             static_cast<long long>(static_cast<int32_t>(ra[e])) - p.z_w * static_cast<long long>(rs);
         y[e] = __dmul_rn(static_cast<double>(v), p.f_tensor);
       } else {
-        double v = __dmul_rn(static_cast<double>(static_cast<int32_t>(ra[e])), p.fs[j]);
+        double v = __dmul_rn(static_cast<double>(static_cast<int32_t>(ra[e])), s_cols[jl]);
         if constexpr (HAS_B) {
-          const long long vb = static_cast<long long>(static_cast<int32_t>(rb[e])) - p.corr_b[j];
-          v = __dadd_rn(v, __dmul_rn(static_cast<double>(vb), p.fb[j]));
+          const long long vb = static_cast<long long>(static_cast<int32_t>(rb[e])) -
+                               static_cast<long long>(s_cols[2 * BN + jl]);
+          v = __dadd_rn(v, __dmul_rn(static_cast<double>(vb), s_cols[BN + jl]));
         }
         y[e] = v;
       }
     }
     if (p.epi == EPI_F32) {
       float* o = reinterpret_cast<float*>(p.out) + base;
-      if (nvalid == 16 && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
-#pragma unroll
-        for (int e = 0; e < 16; e += 4)
-          *reinterpret_cast<float4*>(o + e) =
-              make_float4(__double2float_rn(y[e]), __double2float_rn(y[e + 1]),
-                          __double2float_rn(y[e + 2]), __double2float_rn(y[e + 3]));
+      if (nvalid == 4 && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
+        *reinterpret_cast<float4*>(o) = make_float4(__double2float_rn(y[0]), __double2float_rn(y[1]),
+                                                    __double2float_rn(y[2]), __double2float_rn(y[3]));
       } else {
 #pragma unroll
-        for (int e = 0; e < 16; ++e)
+        for (int e = 0; e < 4; ++e)
           if (e < nvalid) o[e] = __double2float_rn(y[e]);
       }
     } else if (p.epi == EPI_LEVEL) {
       uint16_t* o = reinterpret_cast<uint16_t*>(p.out) + base;
-      uint32_t lv[8];
 #pragma unroll
-      for (int e = 0; e < 16; e += 2) {
-        const uint32_t l0 = lattice_level_fast(y[e], p.n_lo, p.n_hi_open, p.n_step, p.n_inv_step, p.n_L);
-        const uint32_t l1 = lattice_level_fast(y[e + 1], p.n_lo, p.n_hi_open, p.n_step, p.n_inv_step, p.n_L);
-        lv[e / 2] = l0 | (l1 << 16);
-      }
-      if (nvalid == 16 && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
-        *reinterpret_cast<uint4*>(o) = make_uint4(lv[0], lv[1], lv[2], lv[3]);
-        *reinterpret_cast<uint4*>(o + 8) = make_uint4(lv[4], lv[5], lv[6], lv[7]);
-      } else {
-#pragma unroll
-        for (int e = 0; e < 16; ++e)
-          if (e < nvalid) o[e] = static_cast<uint16_t>(lv[e / 2] >> (16 * (e & 1)));
-      }
+      for (int e = 0; e < 4; ++e)
+        if (e < nvalid)
+          o[e] = static_cast<uint16_t>(
+              lattice_level_fast(y[e], p.n_lo, p.n_hi_open, p.n_step, p.n_inv_step, p.n_L));
     } else {  // EPI_I8
       int8_t* o = reinterpret_cast<int8_t*>(p.out) + base;
 #pragma unroll
-      for (int e = 0; e < 16; ++e)
+      for (int e = 0; e < 4; ++e)
         if (e < nvalid) o[e] = static_cast<int8_t>(requant_i8(y[e], p.out_scale, p.inv_out_scale));
     }
   };
+  const int ngroups = BN / 4;
 
   if (p.splits == 1) {
     if (warp < NPW) {
@@ -655,12 +710,13 @@ __global__ void __launch_bounds__(NPW * 32 + 96, 1)
       tc_fence_after();
       if (threadIdx.x == 0) stamp(4);
       const int32_t rowsum = s_rowsum[rloc];
-      for (int cc = wh; cc < nchunks; cc += NPW / 4) {
-        uint32_t ra[16], rb[16];
-        tmem_ld16(t_row + cc * 16, ra);
-        if constexpr (HAS_B) tmem_ld16(t_row + BN + cc * 16, rb);
+#pragma unroll 1
+      for (int gq = wh; gq < ngroups; gq += NPW / 4) {
+        uint32_t ra[4], rb[4] = {0, 0, 0, 0};
+        tmem_ld4(t_row + gq * 4, ra);
+        if constexpr (HAS_B) tmem_ld4(t_row + BN + gq * 4, rb);
         tmem_wait_ld();
-        finish(m0 + rloc, n_tile * BN + cc * 16, ra, rb, rowsum);
+        finish4(m0 + rloc, n_tile * BN + gq * 4, ra, rb, rowsum);
       }
     }
   } else {
@@ -675,24 +731,17 @@ __global__ void __launch_bounds__(NPW * 32 + 96, 1)
         tc_fence_after();
       }
       if (threadIdx.x == 0) stamp(4);
-      for (int cc = wh; cc < nchunks; cc += NPW / 4) {
-        uint32_t ra[16], rb[16];
+#pragma unroll 1
+      for (int gq = wh; gq < ngroups; gq += NPW / 4) {
+        uint32_t ra[4] = {0, 0, 0, 0}, rb[4] = {0, 0, 0, 0};
         if (has_work) {
-          tmem_ld16(t_row + cc * 16, ra);
-          if constexpr (HAS_B) tmem_ld16(t_row + BN + cc * 16, rb);
+          tmem_ld4(t_row + gq * 4, ra);
+          if constexpr (HAS_B) tmem_ld4(t_row + BN + gq * 4, rb);
           tmem_wait_ld();
-        } else {
-#pragma unroll
-          for (int e = 0; e < 16; ++e) ra[e] = rb[e] = 0;
         }
-        uint4* dst = reinterpret_cast<uint4*>(red + rloc * rstride + cc * 16);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) dst[q] = make_uint4(ra[4 * q], ra[4 * q + 1], ra[4 * q + 2], ra[4 * q + 3]);
-        if constexpr (HAS_B) {
-          uint4* dstb = reinterpret_cast<uint4*>(red + rloc * rstride + BN + cc * 16);
-#pragma unroll
-          for (int q = 0; q < 4; ++q) dstb[q] = make_uint4(rb[4 * q], rb[4 * q + 1], rb[4 * q + 2], rb[4 * q + 3]);
-        }
+        *reinterpret_cast<uint4*>(red + rloc * rstride + gq * 4) = make_uint4(ra[0], ra[1], ra[2], ra[3]);
+        if constexpr (HAS_B)
+          *reinterpret_cast<uint4*>(red + rloc * rstride + BN + gq * 4) = make_uint4(rb[0], rb[1], rb[2], rb[3]);
       }
     }
     cluster_sync_all();
@@ -701,49 +750,43 @@ __global__ void __launch_bounds__(NPW * 32 + 96, 1)
       const int S = p.splits;
       const uint32_t rank = cluster_rank();
       const int rows_per = 128 / S;
-      const int items = rows_per * nchunks;
+      const int items = rows_per * ngroups;
       const uint32_t red_addr = smem_u32(red);
       const uint32_t rs_addr = smem_u32(s_rowsum);
+#pragma unroll 1
       for (int it = threadIdx.x; it < items; it += C::NP) {
-        const int rl = static_cast<int>(rank) * rows_per + it / nchunks;
-        const int cc = it % nchunks;
-        uint32_t ra[16], rb[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e) ra[e] = rb[e] = 0;
+        const int rl = static_cast<int>(rank) * rows_per + it / ngroups;
+        const int gq = it % ngroups;
+        uint32_t ra[4] = {0, 0, 0, 0}, rb[4] = {0, 0, 0, 0};
         int32_t rs = 0;
+        const uint32_t off = red_addr + static_cast<uint32_t>((rl * rstride + gq * 4) * 4);
+#pragma unroll 1
         for (int q = 0; q < S; ++q) {
-          const uint32_t base_a = mapa(red_addr + static_cast<uint32_t>((rl * rstride + cc * 16) * 4), q);
-#pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            const uint4 w = ld_cluster_v4(base_a + 16 * v);
-            if constexpr (BF16) {
-              ra[4 * v] = __float_as_uint(__uint_as_float(ra[4 * v]) + __uint_as_float(w.x));
-              ra[4 * v + 1] = __float_as_uint(__uint_as_float(ra[4 * v + 1]) + __uint_as_float(w.y));
-              ra[4 * v + 2] = __float_as_uint(__uint_as_float(ra[4 * v + 2]) + __uint_as_float(w.z));
-              ra[4 * v + 3] = __float_as_uint(__uint_as_float(ra[4 * v + 3]) + __uint_as_float(w.w));
-            } else {
-              ra[4 * v] += w.x;
-              ra[4 * v + 1] += w.y;
-              ra[4 * v + 2] += w.z;
-              ra[4 * v + 3] += w.w;
-            }
-          }
-          if constexpr (HAS_B) {
-            const uint32_t base_b = base_a + static_cast<uint32_t>(BN * 4);
-#pragma unroll
-            for (int v = 0; v < 4; ++v) {
-              const uint4 w = ld_cluster_v4(base_b + 16 * v);
-              rb[4 * v] += w.x;
-              rb[4 * v + 1] += w.y;
-              rb[4 * v + 2] += w.z;
-              rb[4 * v + 3] += w.w;
-            }
-          }
+          const uint32_t ad = mapa(off, q);
+          const uint4 wa = ld_cluster_v4(ad);
+          uint4 wb = make_uint4(0, 0, 0, 0);
+          if constexpr (HAS_B) wb = ld_cluster_v4(ad + BN * 4);
           if constexpr (MODE == MODE_ZP) rs += static_cast<int32_t>(ld_cluster_u32(mapa(rs_addr + rl * 4, q)));
+          if constexpr (BF16) {
+            ra[0] = __float_as_uint(__uint_as_float(ra[0]) + __uint_as_float(wa.x));
+            ra[1] = __float_as_uint(__uint_as_float(ra[1]) + __uint_as_float(wa.y));
+            ra[2] = __float_as_uint(__uint_as_float(ra[2]) + __uint_as_float(wa.z));
+            ra[3] = __float_as_uint(__uint_as_float(ra[3]) + __uint_as_float(wa.w));
+          } else {
+            ra[0] += wa.x;
+            ra[1] += wa.y;
+            ra[2] += wa.z;
+            ra[3] += wa.w;
+          }
+          rb[0] += wb.x;
+          rb[1] += wb.y;
+          rb[2] += wb.z;
+          rb[3] += wb.w;
         }
-        finish(m0 + rl, n_tile * BN + cc * 16, ra, rb, rs);
+        finish4(m0 + rl, n_tile * BN + gq * 4, ra, rb, rs);
       }
     }
+    if (threadIdx.x == 0) stamp(7);
     cluster_sync_all();  // peers' smem must outlive every remote read
   }
   if (threadIdx.x == 0) stamp(6);
@@ -788,11 +831,13 @@ int gemm_ips(bool bf16, int nbp) { return 128 / (nbp * (bf16 ? 2 : 1)); }
 int gemm_gs(bool bf16, int nbp) { return (bf16 ? 64 : 128) / gemm_ips(bf16, nbp); }
 int gemm_threads() { return kNPW * 32 + 96; }
 
-size_t gemm_smem_bytes(bool bf16, int nbp, int BN, int SA, int SX, int x_kind, int tab_bytes) {
+size_t gemm_smem_bytes(bool bf16, int nbp, int BN, int SA, int SB, int SX, int x_kind,
+                       int tab_bytes) {
   const size_t a = 16384, b = static_cast<size_t>(BN) * 128;
   const size_t x = 128u * gemm_ips(bf16, nbp) * (x_kind == X_F32 ? 4 : 2);
-  const size_t t = (bf16 ? 0 : static_cast<size_t>(tab_bytes)) + (3 * SA + 2 * SX + 2) * 8 + 128 * 4 + 16;
-  return 1024 + SA * (a + b) + SX * x + t;
+  const size_t t = (bf16 ? 0 : static_cast<size_t>(tab_bytes)) +
+                   (2 * SA + 2 * SB + 2 * SX + 2) * 8 + 128 * 4 + 3 * BN * 8 + 16;
+  return 1024 + SA * a + SB * b + SX * x + t;
 }
 
 cudaError_t launch_gather_gemm(bool bf16, int nbp, int mode, const CUtensorMap& xmap,

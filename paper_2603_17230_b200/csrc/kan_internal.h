@@ -17,7 +17,8 @@ enum XKind : int { X_F32 = 0, X_U16 = 1 };
 struct GemmParams {
   int M, n_in, N;
   int BN, n_tiles_n;
-  int SA;  // A/B ring stages (released by the MMA)
+  int SA;  // A ring stages (released by the MMA)
+  int SB;  // weight-tile ring stages (released by the MMA)
   int SX;  // activation ring stages (released by the producers)
   // stage schedule
   int IPS, GS;
@@ -25,14 +26,15 @@ struct GemmParams {
   int total_stages;  // length of the pre-tiled weight schedule per n-tile
   int x_kind;
   // lattice tables (LUT path), one contiguous blob copied to smem per CTA:
-  //   NBP = 8 : ent[g] (16 B) = {thr[g], thr[g+1], row pattern bytes 0-7}
-  //   NBP = 16: ent[g] (16 B) = {thr[g], thr[g+1], packed LUT codes, unused}
+  //   vals[2^k] (u32): the P+1 LUT codes of lut_basis_lookup for each in-
+  //     interval offset frac, packed little-endian (byte r = basis jj + r)
+  //   thr[L+2] (f32) at off_thr: thr[n] = smallest fp32 with level >= n
+  //     (thr[0] = -inf, thr[L+1] = NaN), consulted only near rounding ties
   //   SiLU codes [L+1] (u8) at off_silu
-  // thr[n] = smallest fp32 with level >= n; thr[0] = -inf, thr[L+1] = NaN.
   const uint8_t* tab;
-  int tab_bytes, off_silu;
+  int tab_bytes, off_thr, off_silu;
   int L, k;
-  float lo_f, inv_step_f;
+  float lo_f, inv_step_f;  // LUT path: lo_f = -lo/step (fp32), inv_step_f = 1/step
   // float basis (bf16 path)
   float flo, fhi_open, finv_delta;
   int G, P;

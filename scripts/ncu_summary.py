@@ -43,3 +43,44 @@ for k, v in seg.items():
 top = sorted(data, key=lambda r: -float(r[i_s] or 0))[:12]
 for r in top:
     print("  ", r[0][-5:], r[i_s].rjust(6), r[1][:100])
+
+# instruction counts by region (warp-level instructions executed)
+if "--inst" in sys.argv:
+    i_n = h2.index("Instructions Executed")
+    seg = collections.OrderedDict()
+    cur = "start"
+    tot = 0
+    for r in data:
+        for key in ["SYNCS", "UTCIMMA", "UTCHMMA", "UTMALDG", "UBLKCP", "LDTM", "BAR.SYNC", "UCGABAR", "EXIT"]:
+            if key in r[1]:
+                cur = key + "@" + r[0][-5:]
+        n = float(r[i_n] or 0)
+        tot += n
+        seg[cur] = seg.get(cur, 0) + n
+    print("total warp instructions", tot)
+    for k, v in seg.items():
+        if v > tot * 0.01:
+            print(f"  {k:22s} {v:10.0f} {100*v/tot:5.1f}%")
+    hot = sorted(data, key=lambda r: -float(r[i_n] or 0))[:25]
+    for r in hot:
+        print("  ", r[0][-5:], r[i_n].rjust(8), r[1][:90])
+
+# stall reasons by region
+if "--stalls" in sys.argv:
+    cols = [c for c in h2 if c.startswith("stall_") and "Not Issued" not in c]
+    idx = [h2.index(c) for c in cols]
+    seg = collections.OrderedDict()
+    cur = "start"
+    for r in data:
+        for key in ["SYNCS", "UTCIMMA", "UTCHMMA", "LDTM", "BAR.SYNC", "UCGABAR", "EXIT"]:
+            if key in r[1]:
+                cur = key + "@" + r[0][-5:]
+        acc = seg.setdefault(cur, [0.0] * len(cols))
+        for k, i in enumerate(idx):
+            acc[k] += float(r[i] or 0)
+    for name, acc in seg.items():
+        t = sum(acc)
+        if t < tot * 0.03:
+            continue
+        top = sorted(zip(cols, acc), key=lambda z: -z[1])[:5]
+        print(f"  {name:20s} {t:7.0f}  " + ", ".join(f"{c[6:]}={v:.0f}" for c, v in top))

@@ -1,6 +1,7 @@
-"""Run a workload's forward a few times without CUDA graphs (for ncu captures).
+"""Per-layer device time of a workload's forward, replayed from a CUDA graph so
+host launch gaps stay out of the CUDA-event brackets (also used under ncu).
 
-    python scripts/prof_layer.py [--config c2] [--iters 6] [--batch N]
+    python scripts/prof_layer.py [--config c2] [--iters 20] [--batch N] [--split S] [--nograph]
 """
 import argparse
 import os
@@ -18,9 +19,11 @@ from paper_2603_17230_b200 import configs  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c2")
-    ap.add_argument("--iters", type=int, default=6)
+    ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--split", type=int, default=0)
+    ap.add_argument("--nograph", action="store_true")
+    ap.add_argument("--mode", default="")
     a = ap.parse_args()
     wl = configs.get(a.config)
     B = a.batch or wl.batch
@@ -28,16 +31,29 @@ def main():
     e = Engine(wl.descriptor(), 0)
     for i, (w, b) in enumerate(zip(Ws, Bs)):
         e.set_coeffs(i, w, b)
-    e.configure(EvalOptions(mode=wl.mode, lut_k=wl.lut_k, lut_h=wl.lut_h, bits_w=wl.bits_w,
-                            w_scheme=W_PER_CHANNEL_SYM, silu_base=wl.silu, split_k=a.split))
+    e.configure(EvalOptions(mode=a.mode or wl.mode, lut_k=wl.lut_k, lut_h=wl.lut_h,
+                            bits_w=wl.bits_w, w_scheme=W_PER_CHANNEL_SYM, silu_base=wl.silu,
+                            split_k=a.split))
     x = torch.from_numpy(wl.inputs(B)).cuda()
-    e.set_profiling(True)
-    for _ in range(a.iters):
-        e.model_forward(x)
+    out = e.model_forward(x)  # warm-up: allocations, lazy module load
+    torch.cuda.synchronize()
+    st = torch.cuda.Stream()
+    if a.nograph:
+        e.set_profiling(True)
+        with torch.cuda.stream(st):
+            for _ in range(a.iters):
+                e.model_forward(x, out=out, stream=st)
+    else:
+        e.set_profiling(True)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            for _ in range(a.iters):
+                e.model_forward(x, out=out, stream=st)
+        g.replay()
     torch.cuda.synchronize()
     for li in range(len(wl.dims) - 1):
         ms, n = e.layer_time_ms(li)
-        print(f"layer {li}: {ms / max(n, 1) * 1e3:.1f} us avg over {n}")
+        print(f"layer {li}: {ms / max(n, 1) * 1e3:.2f} us avg over {n}")
 
 
 if __name__ == "__main__":

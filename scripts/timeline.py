@@ -16,7 +16,7 @@ import torch  # noqa: E402
 from paper_2603_17230_b200 import Engine, EvalOptions, W_PER_CHANNEL_SYM  # noqa: E402
 from paper_2603_17230_b200 import configs  # noqa: E402
 
-NAMES = ["start", "tables", "stage0", "lastA", "tmemfull", "partials", "done"]
+NAMES = ["start", "tables", "stage0", "lastA", "tmemfull", "partials", "done", "reduced"]
 
 
 def main():
