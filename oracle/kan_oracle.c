@@ -354,6 +354,36 @@ int kor_wquant_per_channel_sym(const double* w, int64_t K, int N, int bits, int8
   return 0;
 }
 
+/* Joint per-channel symmetric quantization of spline + base weights (see
+ * kan_oracle.h).  Rounding is quantize_value's llround (quant.hpp:52). */
+int kor_wquant_joint(const double* w, const double* wb, int64_t K, int n_in, int N, int bits,
+                     double ratio, int8_t* q, int8_t* qb, double* scale) {
+  if (bits < 2 || bits > 8) return -1;
+  const int64_t Q = ((int64_t)1 << (bits - 1)) - 1;
+  for (int j = 0; j < N; ++j) {
+    double mx = 0.0;
+    for (int64_t c = 0; c < K; ++c) {
+      const double v = fabs(w[c * N + j]);
+      mx = (mx < v) ? v : mx;
+    }
+    for (int i = 0; i < n_in; ++i) {
+      const double v = fabs(wb[(int64_t)i * N + j] * ratio);
+      mx = (mx < v) ? v : mx;
+    }
+    const double s = (mx > 0.0) ? mx / (double)Q : 1.0;
+    scale[j] = s;
+    for (int64_t c = 0; c < K; ++c) {
+      int64_t v = llround(w[c * N + j] / s);
+      q[c * N + j] = (int8_t)(v < -Q ? -Q : (v > Q ? Q : v));
+    }
+    for (int i = 0; i < n_in; ++i) {
+      int64_t v = llround((wb[(int64_t)i * N + j] * ratio) / s);
+      qb[(int64_t)i * N + j] = (int8_t)(v < -Q ? -Q : (v > Q ? Q : v));
+    }
+  }
+  return 0;
+}
+
 /* SiLU at every lattice point: v_a = silu(lo + a*step) (ActivationLattice::
  * dequantize, lut.hpp:49), quantized unsigned 8-bit over the zero-spanning
  * range of {v_a} with compute_quant_params / quantize_value (quant.hpp:33-54). */
@@ -411,7 +441,7 @@ int kor_int_accumulate(const kor_grid* g, int k, const uint8_t* lut, const kor_i
       }
     }
     for (int j = 0; j < n_out; ++j) {
-      acc_s[m * n_out + j] = (int32_t)as[j];
+      acc_s[m * n_out + j] = (int32_t)(as[j] + ab[j]); /* single accumulator */
       if (acc_b) acc_b[m * n_out + j] = (int32_t)ab[j];
     }
     if (rowsum) rowsum[m] = rs;
@@ -423,14 +453,15 @@ int kor_int_accumulate(const kor_grid* g, int k, const uint8_t* lut, const kor_i
 
 /* Epilogue (fp64, no contraction):
  *   wscheme 0: y = (double)(acc - z_w*rowsum) * (s_b*s_w)
- *   wscheme 1: y = (double)acc_s * (s_b*s_w[j])
- *              [+ (double)(acc_b - z_s*colsum_b[j]) * (s_s*s_wb[j])]
+ *   wscheme 1: y = (double)(acc - z_s*colsum_b[j]) * (s_b*s_j)   (acc = spline + base;
+ *              colsum_b = 0 without the SiLU term)
  * s_b = value_qp.scale of the table = 1/(2^h-1) (lut.hpp:112). */
 double kor_int_epilogue(const kor_grid* g, int h, const kor_int_layer* L, int n_in, int n_out,
                         int j, int32_t acc_s, int32_t acc_b, int64_t rowsum, int64_t colsum_b) {
   (void)g;
   (void)n_in;
   (void)n_out;
+  (void)acc_b;
   double sb;
   int64_t zb, hb;
   kor_quant_params(0.0, 1.0, h, &sb, &zb, &hb);
@@ -438,13 +469,9 @@ double kor_int_epilogue(const kor_grid* g, int h, const kor_int_layer* L, int n_
     const double f = sb * L->s_w;
     return (double)((int64_t)acc_s - L->z_w * rowsum) * f;
   }
-  const double fs = sb * L->s_wc[j];
-  double y = (double)acc_s * fs;
-  if (L->silu) {
-    const double fb = L->s_s * L->s_wb[j];
-    y = y + (double)((int64_t)acc_b - L->z_s * colsum_b) * fb;
-  }
-  return y;
+  const double f = sb * L->s_wc[j];
+  const int64_t corr = L->silu ? L->z_s * colsum_b : 0;
+  return (double)((int64_t)acc_s - corr) * f;
 }
 
 int kor_int_layer_forward(const kor_grid* g, int k, int h, const uint8_t* lut,

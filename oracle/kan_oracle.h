@@ -80,6 +80,14 @@ int kor_wquant_per_tensor(const double* w, size_t n, int bits, uint8_t* q, doubl
 /* ---- per-output-channel symmetric weight quantization (engine extension) - */
 int kor_wquant_per_channel_sym(const double* w, int64_t K, int N, int bits, int8_t* q,
                                double* scale);
+/* Joint per-output-channel symmetric quantization of a layer with a SiLU base
+ * term (engine extension): spline rows w [K, N] and base rows wb [n_in, N]
+ * share one scale per output channel, in spline-code units:
+ *   m_j = max(max_c |w[c,j]|, max_i |wb[i,j]*ratio|), ratio = s_s / s_b,
+ *   s_j = m_j / Q (1 for an all-zero column), q = clamp(llround(v / s_j), +-Q)
+ * with v = w[c,j] (spline) or wb[i,j]*ratio (base). */
+int kor_wquant_joint(const double* w, const double* wb, int64_t K, int n_in, int N, int bits,
+                     double ratio, int8_t* q, int8_t* qb, double* scale);
 /* SiLU code table on the lattice (engine extension): L+1 u8 codes, scale, zp */
 int kor_silu_table(const kor_grid* g, int k, uint8_t* codes, double* scale, int64_t* zp);
 
@@ -88,7 +96,9 @@ int kor_silu_table(const kor_grid* g, int k, uint8_t* codes, double* scale, int6
  * Spline part: acc_s[m,j] = sum_c qb[m,c] * qw[c,j]
  *   wscheme 0 (reference, per-tensor asym u8): qw = u8 codes, rowsum[m] = sum_c qb[m,c]
  *   wscheme 1 (per-channel symmetric s8):      qw = s8 codes
- * Base part (silu != 0): acc_b[m,j] = sum_i qs[level[m,i]] * qwb[i,j]. */
+ * Base part (silu != 0): acc_b[m,j] = sum_i qs[level[m,i]] * qwb[i,j], and the
+ * engine's single accumulator is acc_s + acc_b (joint scale, kor_wquant_joint):
+ * acc_s returns that sum, acc_b the base part alone. */
 typedef struct {
   int wscheme; /* 0 per-tensor asym (reference), 1 per-channel sym */
   int bits_w;

@@ -80,6 +80,8 @@ class Oracle:
         L.kor_wquant_per_tensor.argtypes = [_dp, C.c_size_t, C.c_int, _u8p,
                                             C.POINTER(C.c_double), C.POINTER(C.c_int64)]
         L.kor_wquant_per_channel_sym.argtypes = [_dp, C.c_int64, C.c_int, C.c_int, _i8p, _dp]
+        L.kor_wquant_joint.argtypes = [_dp, _dp, C.c_int64, C.c_int, C.c_int, C.c_int,
+                                       C.c_double, _i8p, _i8p, _dp]
         L.kor_silu_table.argtypes = [G, C.c_int, _u8p, C.POINTER(C.c_double),
                                      C.POINTER(C.c_int64)]
         L.kor_int_accumulate.argtypes = [G, C.c_int, _u8p, C.POINTER(_IntLayer), C.c_int64,
@@ -192,12 +194,26 @@ class Oracle:
              "lut": self.lut(g.degree, k, h)}
         if wscheme == 0:
             d["qw_u8"], d["s_w"], d["z_w"] = self.wquant_per_tensor(coeffs, bits_w)
-        else:
+        elif base_w is None:
             d["qw_s8"], d["s_wc"] = self.wquant_per_channel(coeffs, bits_w)
         if base_w is not None:
             d["silu_codes"], d["s_s"], d["z_s"] = self.silu_table(g, k)
-            d["qwb"], d["s_wb"] = self.wquant_per_channel(base_w, bits_w)
+            s_b = 1.0 / ((1 << h) - 1)
+            d["qw_s8"], d["qwb"], d["s_wc"] = self.wquant_joint(coeffs, base_w, bits_w,
+                                                                d["s_s"] / s_b)
+            d["s_wb"] = np.zeros(coeffs.shape[1])
         return d
+
+    def wquant_joint(self, w, wb, bits, ratio):
+        w = np.ascontiguousarray(w, dtype=np.float64)
+        wb = np.ascontiguousarray(wb, dtype=np.float64)
+        K, N = w.shape
+        q = np.zeros((K, N), dtype=np.int8)
+        qb = np.zeros(wb.shape, dtype=np.int8)
+        s = np.zeros(N)
+        if self.lib.kor_wquant_joint(w, wb, K, wb.shape[0], N, bits, ratio, q, qb, s):
+            raise ValueError("joint quantization failed")
+        return q, qb, s
 
     def _int_struct(self, d):
         s = _IntLayer()

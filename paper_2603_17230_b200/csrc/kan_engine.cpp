@@ -34,6 +34,7 @@ size_t gemm_smem_bytes(bool bf16, int nbp, int BN, int SA, int SB, int SX, int x
                        int tab_bytes);
 int gemm_ips(bool bf16, int nbp);
 int gemm_gs(bool bf16, int nbp);
+int gemm_tmem_slots(int BN);
 cudaError_t launch_levels(const float* x, int64_t n, const float* thr, float lo, float inv_step,
                           int L, uint16_t* out, cudaStream_t st);
 cudaError_t launch_argmax(const float* logits, int64_t M, int N, int ld, int32_t* out,
@@ -143,11 +144,16 @@ static CUtensorMap make_xmap(const void* base, int x_kind, int64_t rows, int col
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * esz)};
   cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), 128u};
   cuuint32_t estr[2] = {1u, 1u};
+  // rows of 64 / 32 bytes are swizzled so the producers' row-per-lane 16-byte
+  // reads are bank-conflict free (kan_gemm.cu xtile_off)
+  const size_t row_bytes = static_cast<size_t>(box_cols) * esz;
+  const CUtensorMapSwizzle sw = row_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                : row_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                                  : CU_TENSOR_MAP_SWIZZLE_NONE;
   CUresult r = get_encode_fn()(
       &m, x_kind == X_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_UINT16, 2,
-      const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
   return m;
 }
@@ -356,6 +362,38 @@ void quant_per_channel(const std::vector<double>& w, int64_t K, int N, int bits,
 // per-tensor asymmetric quantization, exactly maybe_fake_quant_weights'
 // parameters (eval.hpp:70-76 -> RangeCalibrator(widen) + zero_spanning +
 // compute_quant_params, quant.hpp:97-125)
+// Joint per-output-channel symmetric quantization of spline rows w [K, N] and
+// base rows wb [n_in, N] (base values scaled by `ratio` into spline-code
+// units): one scale s_j = max(|w[:,j]|, |wb[:,j]*ratio|) / Q per channel.
+void quant_joint(const std::vector<double>& w, const std::vector<double>& wb, int64_t K, int n_in,
+                 int N, int bits, double ratio, std::vector<int8_t>& q, std::vector<int8_t>& qb,
+                 std::vector<double>& s) {
+  if (bits < 2 || bits > 8) throw InvalidArgument("per-channel weight bits must be in [2,8]");
+  const int64_t Q = (int64_t{1} << (bits - 1)) - 1;
+  q.assign(static_cast<size_t>(K * N), 0);
+  qb.assign(static_cast<size_t>(n_in) * N, 0);
+  s.assign(static_cast<size_t>(N), 1.0);
+  auto clampq = [Q](int64_t v) { return static_cast<int8_t>(v < -Q ? -Q : (v > Q ? Q : v)); };
+  for (int j = 0; j < N; ++j) {
+    double mx = 0.0;
+    for (int64_t c = 0; c < K; ++c) {
+      const double v = std::fabs(w[static_cast<size_t>(c * N + j)]);
+      mx = (mx < v) ? v : mx;
+    }
+    for (int i = 0; i < n_in; ++i) {
+      const double v = std::fabs(wb[static_cast<size_t>(i) * N + j] * ratio);
+      mx = (mx < v) ? v : mx;
+    }
+    const double sj = (mx > 0.0) ? mx / static_cast<double>(Q) : 1.0;
+    s[static_cast<size_t>(j)] = sj;
+    for (int64_t c = 0; c < K; ++c)
+      q[static_cast<size_t>(c * N + j)] = clampq(std::llround(w[static_cast<size_t>(c * N + j)] / sj));
+    for (int i = 0; i < n_in; ++i)
+      qb[static_cast<size_t>(i) * N + j] =
+          clampq(std::llround((wb[static_cast<size_t>(i) * N + j] * ratio) / sj));
+  }
+}
+
 void quant_per_tensor(const std::vector<double>& w, int bits, std::vector<uint8_t>& q,
                       QParams& qp) {
   if (w.empty()) throw InvalidArgument("empty coefficient matrix");
@@ -378,21 +416,14 @@ void quant_per_tensor(const std::vector<double>& w, int bits, std::vector<uint8_
 
 // Position of group-input gi inside the SiLU stage's 128-byte K row; must
 // match the producer's shift-register order in kan_gemm.cu.
+// Producer thread (row r, K-half h) handles inputs [h*IPS/2, (h+1)*IPS/2) of
+// every stage and shifts their SiLU codes into a 64-byte register that it
+// writes as bytes [64h, 64h+64) of the base stage's row, in stage order.
 int silu_pos(bool bf16, int nbp, int gi) {
-  if (!bf16) {
-    if (nbp == 8) {
-      const int sp = gi / 16, e = gi % 16, c = e / 2, sub = e % 2;
-      return 16 * c + 2 * sp + sub;  // byte
-    }
-    const int sp = gi / 8, c = gi % 8;
-    return 16 * c + sp;
-  }
-  if (nbp == 8) {
-    const int sp = gi / 8, c = gi % 8;
-    return 8 * c + sp;  // bf16 element
-  }
-  const int sp = gi / 4, e = gi % 4, c = 2 * e + (sp & 1);
-  return 8 * c + (sp >> 1);
+  const int ips = gemm_ips(bf16, nbp);
+  const int half = ips / 2;
+  const int s = gi / ips, h = (gi % ips) / half, e = gi % half;
+  return h * (bf16 ? 32 : 64) + s * half + e;  // element index in the 128-byte row
 }
 
 void prepare_gemm_layer(kan_engine* e, const Layer& l, PreparedLayer& pl, bool bf16) {
@@ -435,12 +466,20 @@ void prepare_gemm_layer(kan_engine* e, const Layer& l, PreparedLayer& pl, bool b
       quant_per_tensor(l.coeffs, cfg.bits_w, qw_u8, qpt);
       pl.b_signed = 0;
     } else if (cfg.w_scheme == KAN_W_PER_CHANNEL_SYM) {
-      quant_per_channel(l.coeffs, static_cast<int64_t>(n_in) * nb, N, cfg.bits_w, qw_s8, s_w);
+      if (pl.silu) {
+        // one scale per output channel over the spline AND base weights, the
+        // base weights expressed in spline-code units (ratio = s_s / s_b), so
+        // both parts share a single int32 accumulator
+        const double ratio = e->s_s / quant_params(0.0, 1.0, cfg.lut_h).scale;
+        quant_joint(l.coeffs, l.base_w, static_cast<int64_t>(n_in) * nb, n_in, N, cfg.bits_w,
+                    ratio, qw_s8, qwb, s_w);
+      } else {
+        quant_per_channel(l.coeffs, static_cast<int64_t>(n_in) * nb, N, cfg.bits_w, qw_s8, s_w);
+      }
       pl.b_signed = 1;
     } else {
       throw InvalidArgument("unknown weight scheme");
     }
-    if (pl.silu) quant_per_channel(l.base_w, n_in, N, cfg.bits_w, qwb, s_wb);
   }
   const int GI = pl.GS * pl.IPS;  // inputs per group
   for (int nt = 0; nt < pl.n_tiles_n; ++nt) {
@@ -506,7 +545,6 @@ void prepare_gemm_layer(kan_engine* e, const Layer& l, PreparedLayer& pl, bool b
       for (int j = 0; j < N; ++j) {
         fs[static_cast<size_t>(j)] = s_b * s_w[static_cast<size_t>(j)];
         if (pl.silu) {
-          fb[static_cast<size_t>(j)] = e->s_s * s_wb[static_cast<size_t>(j)];
           long long cs = 0;
           for (int i = 0; i < n_in; ++i) cs += qwb[static_cast<size_t>(i) * N + j];
           corr[static_cast<size_t>(j)] = e->z_s * cs;
@@ -639,7 +677,7 @@ void configure(kan_engine* e, const kan_config* c) {
 // they get equal depth first and the activation ring takes what is left.
 void pick_stages(bool bf16, int nbp, int BN, int x_kind, int tab_bytes, int& SA, int& SB, int& SX) {
   const size_t budget = 232448;
-  SA = std::getenv("KAN_SA") ? std::atoi(std::getenv("KAN_SA")) : 2;
+  SA = gemm_tmem_slots(BN);  // the A ring lives in TMEM
   for (SB = 12; SB >= 2; --SB)
     if (gemm_smem_bytes(bf16, nbp, BN, SA, SB, SB, x_kind, tab_bytes) <= budget) break;
   if (SB < 2) throw Unsupported("tile configuration exceeds shared memory");
@@ -701,9 +739,9 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
   // under-fills the 148 SMs; the partial tiles are summed through DSMEM, so
   // they must fit in the idle A/B rings.
   const int tiles = p.m_tiles * p.n_tiles_n;
-  const int nacc = (pl.silu && !bf16) ? 2 : 1;
-  const size_t red_bytes = static_cast<size_t>(128) * (nacc * pl.BN + 4) * 4;
-  const size_t ring_bytes = static_cast<size_t>(SA) * 16384 + static_cast<size_t>(SB) * pl.BN * 128;
+  const size_t red_bytes = static_cast<size_t>(128) * (pl.BN + 4) * 4;
+  const size_t ring_bytes = static_cast<size_t>(SB) * pl.BN * 128 +
+                            static_cast<size_t>(SX) * 128 * pl.IPS * (io.x_kind == X_F32 ? 4 : 2);
   int want = e->cfg.split_k > 0 ? e->cfg.split_k : 1;
   if (e->cfg.split_k <= 0 && tiles < 148) want = (148 + tiles - 1) / tiles;
   int splits = 1;
@@ -826,12 +864,16 @@ void forward(kan_engine* e, const float* x, int64_t M, void* out, cudaStream_t s
       out_kind = lut ? EPI_LEVEL : EPI_F32;
     }
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    unsigned ev_flags = cudaEventRecordDefault;
     if (e->profiling) {
       ck(cudaEventCreate(&ev0), "cudaEventCreate");
       ck(cudaEventCreate(&ev1), "cudaEventCreate");
       // External records become graph nodes under stream capture, so the pair
       // brackets the kernel node itself when the forward is replayed from a graph
-      ck(cudaEventRecordWithFlags(ev0, st, cudaEventRecordExternal), "cudaEventRecord");
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      ck(cudaStreamIsCapturing(st, &cs), "cudaStreamIsCapturing");
+      ev_flags = cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault;
+      ck(cudaEventRecordWithFlags(ev0, st, ev_flags), "cudaEventRecord");
     }
     if (fp32) {
       run_fp32_layer(e, pl, M, static_cast<const float*>(cur), cur_ld, static_cast<float*>(dst),
@@ -843,7 +885,7 @@ void forward(kan_engine* e, const float* x, int64_t M, void* out, cudaStream_t s
       run_gemm_layer(e, pl, M, io, st);
     }
     if (e->profiling) {
-      ck(cudaEventRecordWithFlags(ev1, st, cudaEventRecordExternal), "cudaEventRecord");
+      ck(cudaEventRecordWithFlags(ev1, st, ev_flags), "cudaEventRecord");
       e->pending.push_back({l.kan_index, ev0, ev1});
     }
     cur = dst;

@@ -8,21 +8,22 @@
 // and, on the float path, kan_linear_forward<RecursiveBasis> (layers.hpp:118-121).
 //
 // One CTA computes a 128-row x BN-column output tile over a range of K.
-// Warp roles:
-//   warps 0..NPW-1  producers: read the activation tile TMA put in smem,
-//                   quantize each activation to its lattice level (exact: an
-//                   fp32 guess corrected against host-computed thresholds),
-//                   fetch the level's precomputed basis-row pattern (u8 LUT
-//                   codes at the support offset) and write the A tile straight
-//                   into smem in the UMMA K-major 128B-swizzle layout; the
-//                   bf16 path evaluates the basis in fp32 instead.  Afterwards
-//                   they run the epilogue (TMEM -> regs -> global).
-//   warp NPW        loader: one bulk copy for the lattice tables, then per stage
-//                   a TMA 2D load of the activation tile and a bulk copy of the
-//                   pre-swizzled weight tile.
-//   warp NPW+1      TMEM allocation and the single-thread tcgen05.mma issuer.
-// Accumulators live in TMEM (int32 on the LUT path, fp32 on bf16); the K loop
-// is a ring of S stages of 128 bytes of K each (4 MMAs of K = 32 bytes).
+// The dense basis ("A") tile never touches shared memory: producers write it
+// straight into tensor memory, where tcgen05.mma reads it (A-from-TMEM form).
+// Warp roles (352 threads, one CTA per SM):
+//   warps 0..7   producers.  Thread (warp w, lane l) owns row 32*(w%4)+l and
+//                K-half w/4 of every 128-byte K stage: it reads its row's
+//                activations from the TMA-filled (swizzled) smem tile, computes
+//                each lattice level (fp32 estimate + exact tie test), expands
+//                it into the row of LUT codes (vals[frac] << 8*jj) -- or the
+//                fp32 Cox-de Boor basis in bf16 on the float path -- and stores
+//                its 64 bytes into the TMEM A ring with one tcgen05.st.  They
+//                also build the SiLU base rows and run the epilogue.
+//   warp 8       TMA loader of the activation ring (released by producers).
+//   warp 9       TMEM allocation + single-thread tcgen05.mma issuer.
+//   warp 10      bulk-copy loader of the lattice tables and the pre-swizzled
+//                weight (B) tiles (ring released by the MMA).
+// The int32 (LUT) or fp32 (bf16) accumulator lives in TMEM columns [0, BN).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -185,6 +186,7 @@ __device__ __forceinline__ uint32_t ld_cluster_u32(uint32_t addr) {
 // ---------------------------------------------------------------------------
 enum { MODE_PLAIN = 0, MODE_ZP = 1, MODE_SILU = 2 };
 
+
 // ring slot/phase counter without division
 struct Ring {
   int slot = 0, n;
@@ -198,24 +200,55 @@ struct Ring {
   }
 };
 
-template <bool BF16, int NBP, int NPW>
+template <bool BF16, int NBP>
 struct Cfg {
-  static constexpr int NP = NPW * 32;
   static constexpr int ESZ = BF16 ? 2 : 1;
   static constexpr int IPS = 128 / (NBP * ESZ);       // inputs per 128-byte K stage
-  static constexpr int GS = (BF16 ? 64 : 128) / IPS;  // spline stages per base group
-  static constexpr int RPT = 1024 / NP;               // rows per producer thread per stage
-  static constexpr int ROW_STEP = NP / 8;
-  // inputs of one 16-byte A chunk: u8 NBP=8 -> 2, u8 NBP=16 -> 1, bf16 -> 1
-  static constexpr int IPC = BF16 ? 1 : ((NBP == 8) ? 2 : 1);
+  static constexpr int HALF = IPS / 2;                // inputs per producer thread per stage
+  static constexpr int GS = (BF16 ? 64 : 128) / IPS;  // spline stages per SiLU group
+  static constexpr int SW = HALF * ESZ / 4;           // SiLU code words per thread per stage
 };
 
-// Activation values of one thread for one stage (RPT rows x IPC inputs).
-template <int RPT, int IPC>
-struct XRegs {
-  float f[RPT][IPC];
-  int lv[RPT][IPC];
-};
+// A-from-TMEM MMAs (M = 128, B K-major in smem)
+__device__ __forceinline__ void mma_i8_ts(uint32_t d, uint32_t a_tmem, uint64_t bdesc,
+                                          uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma_f16_ts(uint32_t d, uint32_t a_tmem, uint64_t bdesc,
+                                           uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+      "r"(r[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+// Byte offset of 16-byte chunk `c` of row `r` in a TMA tile whose rows are
+// `row_bytes` wide and written with the matching swizzle (64 B rows:
+// SWIZZLE_64B, 32 B rows: SWIZZLE_32B, 16 B rows: none).  The swizzle makes a
+// warp's row-per-lane 16-byte reads bank-conflict free.
+__device__ __forceinline__ uint32_t xtile_off(int r, int c, int row_bytes) {
+  const int sw = row_bytes == 64 ? ((r >> 1) & 3) : (row_bytes == 32 ? ((r >> 2) & 1) : 0);
+  return static_cast<uint32_t>(r * row_bytes + ((c ^ sw) << 4));
+}
 
 // Exact lattice level of an fp32 activation.  t = x*(1/step) - lo/step in one
 // FFMA is within 7e-4 of the exact quotient (|x| <= 1, L <= 4096), so
@@ -234,109 +267,121 @@ __device__ __forceinline__ int lattice_level_x(float x, const GemmParams& p, con
   return g;
 }
 
-// One A chunk (16 bytes) of the LUT path.  The P+1 codes of lut_basis_lookup
-// depend only on frac = a mod 2^k (lut.hpp:145-157), so vals[frac] (2^k u32)
-// holds them packed and the chunk is vals[frac] shifted to byte jj = a >> k.
-template <int NBP, int MODE, int XK>
-__device__ __forceinline__ uint4 lut_chunk(const GemmParams& p, const uint32_t* vals,
-                                           const float* thr, const uint8_t* silu_tab,
-                                           const float* xf, const int* xl, int i0, uint32_t& rsum,
-                                           uint32_t (&silu)[4]) {
-  constexpr int IPC = (NBP == 8) ? 2 : 1;
-  const int mask = (1 << p.k) - 1;
-  int a[IPC];
-  uint32_t v[IPC];
-#pragma unroll
-  for (int e = 0; e < IPC; ++e) {
-    a[e] = (XK == X_F32) ? lattice_level_x(xf[e], p, thr) : xl[e];
-    v[e] = vals[a[e] & mask];
-  }
-  uint4 out;
-  if constexpr (NBP == 8) {
-    const unsigned long long p0 = static_cast<unsigned long long>(v[0]) << (8 * (a[0] >> p.k));
-    const unsigned long long p1 = static_cast<unsigned long long>(v[1]) << (8 * (a[1] >> p.k));
-    out = make_uint4(static_cast<uint32_t>(p0), static_cast<uint32_t>(p0 >> 32),
-                     static_cast<uint32_t>(p1), static_cast<uint32_t>(p1 >> 32));
-    if constexpr (MODE == MODE_ZP) {
-      // bytes shifted past the 8-byte row are zero codes (see lut_basis_lookup)
-      if (i0 < p.n_in) rsum = __dp4a(v[0], 0x01010101u, rsum);
-      if (i0 + 1 < p.n_in) rsum = __dp4a(v[1], 0x01010101u, rsum);
-    }
-    if constexpr (MODE == MODE_SILU)
-      shift_in(silu, static_cast<uint32_t>(silu_tab[a[0]]) | (static_cast<uint32_t>(silu_tab[a[1]]) << 8), 16);
-  } else {
-    const int jj = a[0] >> p.k;
-    const int wi = jj >> 2, sh = (jj & 3) * 8;
-    const uint32_t lo = __funnelshift_l(0u, v[0], sh);
-    const uint32_t hi = __funnelshift_l(v[0], 0u, sh);
-    out.x = (wi == 0) ? lo : 0u;
-    out.y = (wi == 1) ? lo : ((wi == 0) ? hi : 0u);
-    out.z = (wi == 2) ? lo : ((wi == 1) ? hi : 0u);
-    out.w = (wi == 3) ? lo : ((wi == 2) ? hi : 0u);
-    if constexpr (MODE == MODE_ZP) {
-      if (i0 < p.n_in) rsum = __dp4a(v[0], 0x01010101u, rsum);
-    }
-    if constexpr (MODE == MODE_SILU) shift_in(silu, static_cast<uint32_t>(silu_tab[a[0]]), 8);
-  }
-  return out;
-}
-
-// One A chunk of the bf16 path: fp32 Cox-de Boor basis, 8 bf16 values.
+// 64 bytes of one A row (this thread's K-half of a stage) on the LUT path.
+// The P+1 codes of lut_basis_lookup depend only on frac = a mod 2^k
+// (lut.hpp:145-157): vals[frac] holds them packed, and an input's NBP-byte
+// row segment is vals[frac] shifted to byte jj = a >> k.
 template <int NBP, int MODE>
-__device__ __forceinline__ uint4 bf16_chunk(const GemmParams& p, float x, int c, int s,
-                                            uint32_t (&silu)[4]) {
-  constexpr int PMAX = 3;
-  const int half = (NBP == 8) ? 0 : (c & 1);
-  float Nv[PMAX + 1];
-  const int jj = basis_f32<PMAX>(x, p.flo, p.fhi_open, p.finv_delta, p.G, p.P, Nv);
-  float v[8];
+__device__ __forceinline__ void lut_row(const GemmParams& p, const uint32_t* vals,
+                                        const uint8_t* silu_tab, const int (&a)[128 / NBP / 2],
+                                        int i0, uint32_t (&w)[16], uint32_t& rsum,
+                                        uint32_t (&sil)[16]) {
+  constexpr int H = 128 / NBP / 2;  // inputs in this thread's half
+  const int mask = (1 << p.k) - 1;
 #pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    const int rr = 8 * half + e - jj;
-    float val = 0.f;
-#pragma unroll
-    for (int q = 0; q <= PMAX; ++q) val = (rr == q) ? Nv[q] : val;
-    v[e] = val;
+  for (int e = 0; e < H; ++e) {
+    const uint32_t v = vals[a[e] & mask];
+    const int jj = a[e] >> p.k;
+    if constexpr (NBP == 8) {
+      const unsigned long long pt = static_cast<unsigned long long>(v) << (8 * jj);
+      w[2 * e] = static_cast<uint32_t>(pt);
+      w[2 * e + 1] = static_cast<uint32_t>(pt >> 32);
+    } else {
+      const int wi = jj >> 2, sh = (jj & 3) * 8;
+      const uint32_t lo = __funnelshift_l(0u, v, sh);
+      const uint32_t hi = __funnelshift_l(v, 0u, sh);
+      w[4 * e] = (wi == 0) ? lo : 0u;
+      w[4 * e + 1] = (wi == 1) ? lo : ((wi == 0) ? hi : 0u);
+      w[4 * e + 2] = (wi == 2) ? lo : ((wi == 1) ? hi : 0u);
+      w[4 * e + 3] = (wi == 3) ? lo : ((wi == 2) ? hi : 0u);
+    }
+    if constexpr (MODE == MODE_ZP) {
+      // codes shifted past the row end are zero (see lut_basis_lookup)
+      if (i0 + e < p.n_in) rsum = __dp4a(v, 0x01010101u, rsum);
+    }
   }
   if constexpr (MODE == MODE_SILU) {
-    if (NBP == 8 || (s & 1) == half) {
-      const float xc = fminf(fmaxf(x, p.flo), p.fhi_open);
-      const float sv = xc / (1.0f + __expf(-xc));
-      const __nv_bfloat16 b = __float2bfloat16_rn(sv);
-      shift_in(silu, static_cast<uint32_t>(*reinterpret_cast<const uint16_t*>(&b)), 16);
-    }
+    // append this stage's H SiLU codes (H bytes) to the 64-byte shift register
+    uint32_t nw[H / 4];
+#pragma unroll
+    for (int q = 0; q < H / 4; ++q)
+      nw[q] = static_cast<uint32_t>(silu_tab[a[4 * q]]) |
+              (static_cast<uint32_t>(silu_tab[a[4 * q + 1]]) << 8) |
+              (static_cast<uint32_t>(silu_tab[a[4 * q + 2]]) << 16) |
+              (static_cast<uint32_t>(silu_tab[a[4 * q + 3]]) << 24);
+#pragma unroll
+    for (int q = 0; q < 16 - H / 4; ++q) sil[q] = sil[q + H / 4];
+#pragma unroll
+    for (int q = 0; q < H / 4; ++q) sil[16 - H / 4 + q] = nw[q];
   }
-  return make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]),
-                    pack_bf16(v[6], v[7]));
 }
 
-template <bool BF16, int NBP, int NPW, int MODE>
-__global__ void __launch_bounds__(NPW * 32 + 96, 1)
+// 64 bytes of one A row on the bf16 path: fp32 Cox-de Boor basis -> bf16.
+template <int NBP, int MODE>
+__device__ __forceinline__ void bf16_row(const GemmParams& p, const float (&x)[128 / NBP / 4],
+                                         uint32_t (&w)[16], uint32_t (&sil)[16]) {
+  constexpr int H = 128 / NBP / 4;  // inputs in this thread's half (bf16: NBP*2 bytes each)
+  constexpr int PMAX = 3;
+#pragma unroll
+  for (int e = 0; e < H; ++e) {
+    float Nv[PMAX + 1];
+    const int jj = basis_f32<PMAX>(x[e], p.flo, p.fhi_open, p.finv_delta, p.G, p.P, Nv);
+#pragma unroll
+    for (int q = 0; q < NBP / 2; ++q) {
+      float v2[2];
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const int rr = 2 * q + t - jj;
+        float val = 0.f;
+#pragma unroll
+        for (int m = 0; m <= PMAX; ++m) val = (rr == m) ? Nv[m] : val;
+        v2[t] = val;
+      }
+      w[e * (NBP / 2) + q] = pack_bf16(v2[0], v2[1]);
+    }
+  }
+  if constexpr (MODE == MODE_SILU) {
+    uint32_t nw[H / 2];
+#pragma unroll
+    for (int q = 0; q < H / 2; ++q) {
+      float s2[2];
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const float xc = fminf(fmaxf(x[2 * q + t], p.flo), p.fhi_open);
+        s2[t] = xc / (1.0f + __expf(-xc));
+      }
+      nw[q] = pack_bf16(s2[0], s2[1]);
+    }
+#pragma unroll
+    for (int q = 0; q < 16 - H / 2; ++q) sil[q] = sil[q + H / 2];
+#pragma unroll
+    for (int q = 0; q < H / 2; ++q) sil[16 - H / 2 + q] = nw[q];
+  }
+}
+
+template <bool BF16, int NBP, int MODE>
+__global__ void __launch_bounds__(352, 1)
     kan_gather_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const GemmParams p) {
-  using C = Cfg<BF16, NBP, NPW>;
+  using C = Cfg<BF16, NBP>;
+  constexpr int NPW = 8, NP = 256;
   constexpr bool SILU = (MODE == MODE_SILU);
-  constexpr bool HAS_B = SILU && !BF16;  // separate base accumulator (LUT path)
-  constexpr int NACC = HAS_B ? 2 : 1;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  // 1024-align the dynamic smem base (SW128 atoms); pointer arithmetic on the
-  // __shared__ array keeps the shared address space visible to the compiler.
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
 
   const int SA = p.SA, SB = p.SB, SX = p.SX;
   const int BN = p.BN;
-  constexpr uint32_t a_bytes = 16384;
   const uint32_t b_bytes = static_cast<uint32_t>(BN) * 128u;
   const uint32_t xesz = (p.x_kind == X_F32) ? 4u : 2u;
-  const uint32_t x_bytes = 128u * C::IPS * xesz;
-  uint8_t* sA = smem;
-  uint8_t* sB = sA + static_cast<size_t>(SA) * a_bytes;
+  const int x_row_bytes = C::IPS * static_cast<int>(xesz);
+  const uint32_t x_bytes = 128u * static_cast<uint32_t>(x_row_bytes);
+  uint8_t* sB = smem;
   uint8_t* sX = sB + static_cast<size_t>(SB) * b_bytes;
   uint8_t* sT = sX + static_cast<size_t>(SX) * x_bytes;  // lattice tables (LUT path)
   const int tab_bytes = BF16 ? 0 : p.tab_bytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sT + tab_bytes);
   int32_t* s_rowsum = reinterpret_cast<int32_t*>(bars + 2 * SA + 2 * SB + 2 * SX + 2);
-  double* s_cols = reinterpret_cast<double*>(s_rowsum + 128);  // [3][BN] fs, fb, corr
-  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(s_cols + 3 * BN);
+  double* s_cols = reinterpret_cast<double*>(s_rowsum + 128);  // [2][BN]: scale, correction
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(s_cols + 2 * BN);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -353,11 +398,10 @@ __global__ void __launch_bounds__(NPW * 32 + 96, 1)
   const int split = blockIdx.z;
   const int m0 = m_tile * 128;
 
-  // groups of K stages handled by this CTA (may be empty for the last split)
   const int g0 = split * p.groups_per_split;
   const int g1 = min(p.n_groups, g0 + p.groups_per_split);
   const bool has_work = g0 < g1;
-  const int spg = C::GS + (SILU ? 1 : 0);  // schedule stages per full group
+  const int spg = C::GS + (SILU ? 1 : 0);
 
   auto bar_xfull = [&](int s) { return smem_u32(bars + s); };
   auto bar_xempty = [&](int s) { return smem_u32(bars + SX + s); };
@@ -368,17 +412,17 @@ __global__ void __launch_bounds__(NPW * 32 + 96, 1)
   const uint32_t bar_tmem_full = smem_u32(bars + 2 * SX + 2 * SA + 2 * SB);
   const uint32_t bar_tab = smem_u32(bars + 2 * SX + 2 * SA + 2 * SB + 1);
 
-  uint32_t tmem_cols = 32;
-  while (tmem_cols < static_cast<uint32_t>(BN) * NACC) tmem_cols <<= 1;
+  // TMEM: accumulator in columns [0, BN), A ring slots of 32 columns from acol0
+  constexpr uint32_t tmem_cols = 512;
+  const uint32_t acol0 = static_cast<uint32_t>((BN + 31) / 32 * 32);
 
-  // ---- setup: barriers, TMEM ----------------------------------------------
+  // ---- setup -------------------------------------------------------------
   if (threadIdx.x < 128) s_rowsum[threadIdx.x] = 0;
   if constexpr (!BF16 && MODE != MODE_ZP) {
     for (int i = threadIdx.x; i < BN; i += blockDim.x) {
       const int j = min(n_tile * BN + i, p.N - 1);
       s_cols[i] = p.fs[j];
-      s_cols[BN + i] = HAS_B ? p.fb[j] : 0.0;
-      s_cols[2 * BN + i] = HAS_B ? static_cast<double>(p.corr_b[j]) : 0.0;
+      s_cols[BN + i] = SILU ? static_cast<double>(p.corr_b[j]) : 0.0;
     }
   }
   if (threadIdx.x == 0) {
@@ -413,16 +457,11 @@ __global__ void __launch_bounds__(NPW * 32 + 96, 1)
     for (int g = g0; g < g1; ++g) {
       const int nsp = min(C::GS, p.n_spline_stages - g * C::GS);
       for (int s = 0; s < nsp; ++s, rx.next()) {
-        const int xs = rx.slot;
-        mbar_wait(bar_xempty(xs), rx.phase ^ 1);
+        mbar_wait(bar_xempty(rx.slot), rx.phase ^ 1);
         if (lane == 0) {
-          if (p.dbg_flags & 8) {
-            mbar_arrive(bar_xfull(xs));
-          } else {
-            mbar_arrive_tx(bar_xfull(xs), x_bytes);
-            tma_load_2d(smem_u32(sX + static_cast<size_t>(xs) * x_bytes), &xmap,
-                        (g * C::GS + s) * C::IPS, m0, bar_xfull(xs));
-          }
+          mbar_arrive_tx(bar_xfull(rx.slot), x_bytes);
+          tma_load_2d(smem_u32(sX + static_cast<size_t>(rx.slot) * x_bytes), &xmap,
+                      (g * C::GS + s) * C::IPS, m0, bar_xfull(rx.slot));
         }
         __syncwarp();
       }
@@ -438,17 +477,12 @@ __global__ void __launch_bounds__(NPW * 32 + 96, 1)
     for (int g = g0; g < g1; ++g) {
       const int nsp = min(C::GS, p.n_spline_stages - g * C::GS);
       for (int s = 0; s < nsp + (SILU ? 1 : 0); ++s, rb.next()) {
-        const int bs = rb.slot;
-        mbar_wait(bar_bempty(bs), rb.phase ^ 1);
+        mbar_wait(bar_bempty(rb.slot), rb.phase ^ 1);
         if (lane == 0) {
           const size_t tile = static_cast<size_t>(n_tile) * p.total_stages + g * spg + s;
-          if (p.dbg_flags & 16) {
-            mbar_arrive(bar_bfull(bs));
-          } else {
-            mbar_arrive_tx(bar_bfull(bs), b_bytes);
-            bulk_load(smem_u32(sB + static_cast<size_t>(bs) * b_bytes), p.wt + tile * b_bytes,
-                      b_bytes, bar_bfull(bs));
-          }
+          mbar_arrive_tx(bar_bfull(rb.slot), b_bytes);
+          bulk_load(smem_u32(sB + static_cast<size_t>(rb.slot) * b_bytes), p.wt + tile * b_bytes,
+                    b_bytes, bar_bfull(rb.slot));
         }
         __syncwarp();
       }
@@ -458,204 +492,176 @@ __global__ void __launch_bounds__(NPW * 32 + 96, 1)
     const uint32_t idesc = BF16 ? idesc_bf16(BN) : idesc_i8(BN, p.b_signed != 0);
     const int nk = (p.dbg_flags & 2) ? 0 : 4;
     Ring ra(SA), rb(SB);
-    bool first_s = true, first_b = true;
+    bool first = true;
     for (int g = g0; g < g1; ++g) {
       const int nsp = min(C::GS, p.n_spline_stages - g * C::GS);
       for (int s = 0; s < nsp + (SILU ? 1 : 0); ++s, ra.next(), rb.next()) {
-        const int as = ra.slot, bs = rb.slot;
-        mbar_wait(bar_afull(as), ra.phase);
-        mbar_wait(bar_bfull(bs), rb.phase);
+        mbar_wait(bar_afull(ra.slot), ra.phase);
+        mbar_wait(bar_bfull(rb.slot), rb.phase);
         tc_fence_after();
-        const bool is_base = HAS_B && (s >= nsp);
         if (lane == 0) {
-          const uint32_t d = tmem + (is_base ? static_cast<uint32_t>(BN) : 0u);
-          const bool first = is_base ? first_b : first_s;
-          const uint32_t a_addr = smem_u32(sA + static_cast<size_t>(as) * a_bytes);
-          const uint32_t b_addr = smem_u32(sB + static_cast<size_t>(bs) * b_bytes);
+          const uint32_t a_tmem = tmem + acol0 + 32u * static_cast<uint32_t>(ra.slot);
+          const uint32_t b_addr = smem_u32(sB + static_cast<size_t>(rb.slot) * b_bytes);
           for (int kk = 0; kk < nk; ++kk) {
-            const uint64_t ad = umma_desc_sw128(a_addr + 32 * kk);
             const uint64_t bd = umma_desc_sw128(b_addr + 32 * kk);
             const uint32_t acc = (first && kk == 0) ? 0u : 1u;
             if (BF16)
-              mma_f16(d, ad, bd, idesc, acc);
+              mma_f16_ts(tmem, a_tmem + 8 * kk, bd, idesc, acc);
             else
-              mma_i8(d, ad, bd, idesc, acc);
+              mma_i8_ts(tmem, a_tmem + 8 * kk, bd, idesc, acc);
           }
-          if (p.dbg_flags & 64) {
-            mbar_arrive(bar_aempty(as));
-            mbar_arrive(bar_bempty(bs));
-          } else {
-            tc_commit(bar_aempty(as));
-            tc_commit(bar_bempty(bs));
-          }
+          tc_commit(bar_aempty(ra.slot));
+          tc_commit(bar_bempty(rb.slot));
         }
         __syncwarp();
-        if (is_base)
-          first_b = false;
-        else
-          first_s = false;
+        first = false;
       }
     }
     if (lane == 0) tc_commit(bar_tmem_full);
     __syncwarp();
   } else {
     // ============================ producers ===============================
-    const int pt = threadIdx.x;
-    const int c = pt & 7;
-    const int r0 = pt >> 3;
-    uint32_t silu_w[C::RPT][4];
-    uint32_t rsum[C::RPT];
+    const int quarter = warp & 3;
+    const int h = warp >> 2;  // K-half of each stage this thread fills
+    const int r = quarter * 32 + lane;
+    const uint32_t t_lane = static_cast<uint32_t>(quarter * 32) << 16;
+    uint32_t sil[16];
 #pragma unroll
-    for (int j = 0; j < C::RPT; ++j) {
-      rsum[j] = 0;
-#pragma unroll
-      for (int w = 0; w < 4; ++w) silu_w[j][w] = 0;
-    }
+    for (int q = 0; q < 16; ++q) sil[q] = 0;
+    uint32_t rsum = 0;
     if (tab_bytes > 0) mbar_wait(bar_tab, 0);
-    if (pt == 0) stamp(1);
+    if (threadIdx.x == 0) stamp(1);
     const uint32_t* vals = reinterpret_cast<const uint32_t*>(sT);
     const float* thr = reinterpret_cast<const float*>(sT + p.off_thr);
     const uint8_t* silu_tab = sT + p.off_silu;
+    constexpr int H = C::HALF;
 
-    // loop-invariant smem offsets of this thread's chunks
-    const int in_c = BF16 ? ((NBP == 8) ? c : (c >> 1)) : c * C::IPC;
-    uint32_t a_off[C::RPT], x_off[C::RPT];
-#pragma unroll
-    for (int j = 0; j < C::RPT; ++j) {
-      a_off[j] = sw128_off(r0 + j * C::ROW_STEP, c);
-      x_off[j] = static_cast<uint32_t>((r0 + j * C::ROW_STEP) * C::IPS + in_c) * xesz;
-    }
     Ring ra(SA), rx(SX);
     int idx = 0;
     for (int g = g0; g < g1; ++g) {
       const int nsp = min(C::GS, p.n_spline_stages - g * C::GS);
       for (int s = 0; s < nsp + (SILU ? 1 : 0); ++s, ++idx, ra.next()) {
-        const int as = ra.slot;
-        const uint32_t aph = ra.phase;
-        uint8_t* a_tile = sA + static_cast<size_t>(as) * a_bytes;
+        uint32_t w[16];
         if (s < nsp) {
-          // 1. activations of this stage -> registers, release the x slot
-          const int xs = rx.slot;
-          mbar_wait(bar_xfull(xs), rx.phase);
-          rx.next();
-          const uint8_t* xt = sX + static_cast<size_t>(xs) * x_bytes;
-          XRegs<C::RPT, C::IPC> xr;
-          if (BF16 || p.x_kind == X_F32) {
-#pragma unroll
-            for (int j = 0; j < C::RPT; ++j) {
-              const float* xp = reinterpret_cast<const float*>(xt + x_off[j]);
-              if constexpr (C::IPC == 2) {
-                const float2 v = *reinterpret_cast<const float2*>(xp);
-                xr.f[j][0] = v.x;
-                xr.f[j][1] = v.y;
-              } else {
-                xr.f[j][0] = xp[0];
-              }
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < C::RPT; ++j) {
-              const uint16_t* xp = reinterpret_cast<const uint16_t*>(xt + x_off[j]);
-              if constexpr (C::IPC == 2) {
-                const uint32_t v = *reinterpret_cast<const uint32_t*>(xp);
-                xr.lv[j][0] = static_cast<int>(v & 0xFFFF);
-                xr.lv[j][1] = static_cast<int>(v >> 16);
-              } else {
-                xr.lv[j][0] = xp[0];
-              }
-            }
-          }
-          __syncwarp();
-          if (lane == 0) mbar_arrive(bar_xempty(xs));
-          // 2. wait for the A slot, expand levels into basis rows
-          mbar_wait(bar_aempty(as), aph ^ 1);
-          const int i0 = (g * C::GS + s) * C::IPS + in_c;
-          uint4 out[C::RPT];
-          if (p.dbg_flags & 1) {
-#pragma unroll
-            for (int j = 0; j < C::RPT; ++j) out[j] = make_uint4(0, 0, 0, 0);
-          } else if constexpr (BF16) {
-#pragma unroll
-            for (int j = 0; j < C::RPT; ++j) out[j] = bf16_chunk<NBP, MODE>(p, xr.f[j][0], c, s, silu_w[j]);
-          } else {
-            if (p.x_kind == X_F32) {
-#pragma unroll
-              for (int j = 0; j < C::RPT; ++j)
-                out[j] = lut_chunk<NBP, MODE, X_F32>(p, vals, thr, silu_tab, xr.f[j], xr.lv[j], i0, rsum[j], silu_w[j]);
+          // 1. this thread's activations of the stage -> registers; free the slot
+          mbar_wait(bar_xfull(rx.slot), rx.phase);
+          const uint8_t* xt = sX + static_cast<size_t>(rx.slot) * x_bytes;
+          const int i0 = (g * C::GS + s) * C::IPS + h * H;
+          if constexpr (BF16) {
+            float x[H];
+            if constexpr (H == 4) {
+              const float4 v = *reinterpret_cast<const float4*>(xt + xtile_off(r, h, x_row_bytes));
+              x[0] = v.x;
+              x[1] = v.y;
+              x[2] = v.z;
+              x[3] = v.w;
             } else {
+              const float2 v = *reinterpret_cast<const float2*>(xt + r * x_row_bytes + 8 * h);
+              x[0] = v.x;
+              x[1] = v.y;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar_xempty(rx.slot));
+            rx.next();
+            if (p.dbg_flags & 1) {
 #pragma unroll
-              for (int j = 0; j < C::RPT; ++j)
-                out[j] = lut_chunk<NBP, MODE, X_U16>(p, vals, thr, silu_tab, xr.f[j], xr.lv[j], i0, rsum[j], silu_w[j]);
+              for (int q = 0; q < 16; ++q) w[q] = 0;
+            } else {
+              bf16_row<NBP, MODE>(p, x, w, sil);
+            }
+          } else {
+            int a[H];
+            if (p.x_kind == X_F32) {
+              float x[H];
+#pragma unroll
+              for (int q = 0; q < H / 4; ++q) {
+                const float4 v =
+                    *reinterpret_cast<const float4*>(xt + xtile_off(r, h * (H / 4) + q, x_row_bytes));
+                x[4 * q] = v.x;
+                x[4 * q + 1] = v.y;
+                x[4 * q + 2] = v.z;
+                x[4 * q + 3] = v.w;
+              }
+              __syncwarp();
+              if (lane == 0) mbar_arrive(bar_xempty(rx.slot));
+#pragma unroll
+              for (int e = 0; e < H; ++e) a[e] = lattice_level_x(x[e], p, thr);
+            } else {
+              if constexpr (H == 8) {
+                const uint4 v = *reinterpret_cast<const uint4*>(xt + xtile_off(r, h, x_row_bytes));
+                const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  a[2 * q] = static_cast<int>(vv[q] & 0xFFFF);
+                  a[2 * q + 1] = static_cast<int>(vv[q] >> 16);
+                }
+              } else {
+                const uint2 v = *reinterpret_cast<const uint2*>(xt + r * x_row_bytes + 8 * h);
+                a[0] = static_cast<int>(v.x & 0xFFFF);
+                a[1] = static_cast<int>(v.x >> 16);
+                a[2] = static_cast<int>(v.y & 0xFFFF);
+                a[3] = static_cast<int>(v.y >> 16);
+              }
+              __syncwarp();
+              if (lane == 0) mbar_arrive(bar_xempty(rx.slot));
+            }
+            rx.next();
+            if (p.dbg_flags & 1) {
+#pragma unroll
+              for (int q = 0; q < 16; ++q) w[q] = 0;
+            } else {
+              lut_row<NBP, MODE>(p, vals, silu_tab, a, i0, w, rsum, sil);
             }
           }
+        } else {
+          // base (SiLU) stage: this thread's 64 bytes are its shift register,
+          // padded for the stages a short last group lacks
+          for (int t = nsp; t < C::GS; ++t) {
 #pragma unroll
-          for (int j = 0; j < C::RPT; ++j) *reinterpret_cast<uint4*>(a_tile + a_off[j]) = out[j];
-        } else if constexpr (SILU) {
-          // base (SiLU) stage: flush the per-thread 16-byte chunk of each row,
-          // first padding the shift register for stages the last group lacks.
-          // (bf16 with NBP=16: a thread contributes on stages of parity c&1.)
-          mbar_wait(bar_aempty(as), aph ^ 1);
-          const int bits = BF16 ? 16 : ((NBP == 8) ? 16 : 8);
-          int pad = C::GS - nsp;
-          if (BF16 && NBP == 16) {
-            pad = 0;
-            for (int t = nsp; t < C::GS; ++t) pad += ((t & 1) == (c & 1)) ? 1 : 0;
+            for (int q = 0; q < 16 - C::SW; ++q) sil[q] = sil[q + C::SW];
+#pragma unroll
+            for (int q = 16 - C::SW; q < 16; ++q) sil[q] = 0;
           }
 #pragma unroll
-          for (int j = 0; j < C::RPT; ++j) {
-            for (int t = 0; t < pad; ++t) shift_in(silu_w[j], 0u, bits);
-            *reinterpret_cast<uint4*>(a_tile + a_off[j]) =
-                make_uint4(silu_w[j][0], silu_w[j][1], silu_w[j][2], silu_w[j][3]);
-#pragma unroll
-            for (int w = 0; w < 4; ++w) silu_w[j][w] = 0;
+          for (int q = 0; q < 16; ++q) {
+            w[q] = sil[q];
+            sil[q] = 0;
           }
         }
-        if (!(p.dbg_flags & 32)) fence_proxy_async_smem();
+        // 2. the A slot must be free (its previous MMAs retired), then store
+        mbar_wait(bar_aempty(ra.slot), ra.phase ^ 1);
+        tc_fence_after();
+        tmem_st16(tmem + t_lane + acol0 + 32u * static_cast<uint32_t>(ra.slot) + 16u * h, w);
+        tmem_wait_st();
+        tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(bar_afull(as));
-        if (pt == 0 && idx == 0) stamp(2);
+        if (lane == 0) mbar_arrive(bar_afull(ra.slot));
+        if (threadIdx.x == 0 && idx == 0) stamp(2);
       }
     }
-    if (pt == 0) stamp(3);
-
-    // ---- row sums of the basis codes (per-tensor zero-point correction) ----
-    if constexpr (MODE == MODE_ZP) {
-#pragma unroll
-      for (int j = 0; j < C::RPT; ++j) {
-        int v = static_cast<int>(rsum[j]);
-        v += __shfl_xor_sync(0xffffffffu, v, 1);
-        v += __shfl_xor_sync(0xffffffffu, v, 2);
-        v += __shfl_xor_sync(0xffffffffu, v, 4);
-        if (c == 0) s_rowsum[r0 + j * C::ROW_STEP] = v;
-      }
-    }
-    asm volatile("bar.sync 1, %0;" ::"r"(C::NP) : "memory");
+    if (threadIdx.x == 0) stamp(3);
+    if constexpr (MODE == MODE_ZP) atomicAdd(&s_rowsum[r], static_cast<int>(rsum));
+    asm volatile("bar.sync 1, %0;" ::"r"(NP) : "memory");
   }
 
   // ============================ epilogue ==================================
+  // The epilogue runs once per CTA out of a cold instruction cache, so it
+  // works on 4-column groups in rolled loops to keep its code small.
   const int wq = warp & 3;
   const int wh = warp >> 2;
   const int rloc = wq * 32 + lane;
   const uint32_t t_row = tmem + (static_cast<uint32_t>(wq * 32) << 16);
-  const int nchunks = BN / 16;
+  const int ngroups = BN / 4;
 
-  // The epilogue runs once per CTA out of a cold instruction cache, so it
-  // works on 4-column groups in rolled loops to keep its code small.
-  auto finish4 = [&](int row, int col0, const uint32_t(&ra)[4], const uint32_t(&rb)[4],
-                     int32_t rs) {
+  auto finish4 = [&](int row, int col0, const uint32_t(&ra)[4], int32_t rs) {
     if (row >= p.M) return;
     const size_t base = static_cast<size_t>(row) * p.ld_out + col0;
     const int nvalid = min(4, p.N - col0);
     if (p.epi == EPI_RAW) {
       uint32_t* o = reinterpret_cast<uint32_t*>(p.out) + base;
-      uint32_t* o2 = reinterpret_cast<uint32_t*>(p.out2) + base;
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        if (e < nvalid) {
-          o[e] = ra[e];
-          if (HAS_B && p.out2) o2[e] = rb[e];
-        }
-      }
+      for (int e = 0; e < 4; ++e)
+        if (e < nvalid) o[e] = ra[e];
       return;
     }
     double y[4];
@@ -669,13 +675,9 @@ __global__ void __launch_bounds__(NPW * 32 + 96, 1)
             static_cast<long long>(static_cast<int32_t>(ra[e])) - p.z_w * static_cast<long long>(rs);
         y[e] = __dmul_rn(static_cast<double>(v), p.f_tensor);
       } else {
-        double v = __dmul_rn(static_cast<double>(static_cast<int32_t>(ra[e])), s_cols[jl]);
-        if constexpr (HAS_B) {
-          const long long vb = static_cast<long long>(static_cast<int32_t>(rb[e])) -
-                               static_cast<long long>(s_cols[2 * BN + jl]);
-          v = __dadd_rn(v, __dmul_rn(static_cast<double>(vb), s_cols[BN + jl]));
-        }
-        y[e] = v;
+        const long long v = static_cast<long long>(static_cast<int32_t>(ra[e])) -
+                            static_cast<long long>(s_cols[BN + jl]);
+        y[e] = __dmul_rn(static_cast<double>(v), s_cols[jl]);
       }
     }
     if (p.epi == EPI_F32) {
@@ -702,7 +704,6 @@ __global__ void __launch_bounds__(NPW * 32 + 96, 1)
         if (e < nvalid) o[e] = static_cast<int8_t>(requant_i8(y[e], p.out_scale, p.inv_out_scale));
     }
   };
-  const int ngroups = BN / 4;
 
   if (p.splits == 1) {
     if (warp < NPW) {
@@ -712,19 +713,18 @@ __global__ void __launch_bounds__(NPW * 32 + 96, 1)
       const int32_t rowsum = s_rowsum[rloc];
 #pragma unroll 1
       for (int gq = wh; gq < ngroups; gq += NPW / 4) {
-        uint32_t ra[4], rb[4] = {0, 0, 0, 0};
+        uint32_t ra[4];
         tmem_ld4(t_row + gq * 4, ra);
-        if constexpr (HAS_B) tmem_ld4(t_row + BN + gq * 4, rb);
         tmem_wait_ld();
-        finish4(m0 + rloc, n_tile * BN + gq * 4, ra, rb, rowsum);
+        finish4(m0 + rloc, n_tile * BN + gq * 4, ra, rowsum);
       }
     }
   } else {
     // split-K across the cluster: dump the partial accumulators into this
-    // CTA's smem (the A/B rings are idle now), then every CTA reduces a slice
+    // CTA's smem (the B/x rings are idle now), then every CTA reduces a slice
     // of rows over all peers through distributed shared memory.
-    const int rstride = NACC * BN + 4;  // words per row (+4 breaks bank conflicts)
-    uint32_t* red = reinterpret_cast<uint32_t*>(sA);
+    const int rstride = BN + 4;  // words per row (+4 breaks bank conflicts)
+    uint32_t* red = reinterpret_cast<uint32_t*>(sB);
     if (warp < NPW) {
       if (has_work) {
         mbar_wait(bar_tmem_full, 0);
@@ -733,15 +733,12 @@ __global__ void __launch_bounds__(NPW * 32 + 96, 1)
       if (threadIdx.x == 0) stamp(4);
 #pragma unroll 1
       for (int gq = wh; gq < ngroups; gq += NPW / 4) {
-        uint32_t ra[4] = {0, 0, 0, 0}, rb[4] = {0, 0, 0, 0};
+        uint32_t ra[4] = {0, 0, 0, 0};
         if (has_work) {
           tmem_ld4(t_row + gq * 4, ra);
-          if constexpr (HAS_B) tmem_ld4(t_row + BN + gq * 4, rb);
           tmem_wait_ld();
         }
         *reinterpret_cast<uint4*>(red + rloc * rstride + gq * 4) = make_uint4(ra[0], ra[1], ra[2], ra[3]);
-        if constexpr (HAS_B)
-          *reinterpret_cast<uint4*>(red + rloc * rstride + BN + gq * 4) = make_uint4(rb[0], rb[1], rb[2], rb[3]);
       }
     }
     cluster_sync_all();
@@ -754,18 +751,15 @@ __global__ void __launch_bounds__(NPW * 32 + 96, 1)
       const uint32_t red_addr = smem_u32(red);
       const uint32_t rs_addr = smem_u32(s_rowsum);
 #pragma unroll 1
-      for (int it = threadIdx.x; it < items; it += C::NP) {
+      for (int it = threadIdx.x; it < items; it += NP) {
         const int rl = static_cast<int>(rank) * rows_per + it / ngroups;
         const int gq = it % ngroups;
-        uint32_t ra[4] = {0, 0, 0, 0}, rb[4] = {0, 0, 0, 0};
+        uint32_t ra[4] = {0, 0, 0, 0};
         int32_t rs = 0;
         const uint32_t off = red_addr + static_cast<uint32_t>((rl * rstride + gq * 4) * 4);
 #pragma unroll 1
         for (int q = 0; q < S; ++q) {
-          const uint32_t ad = mapa(off, q);
-          const uint4 wa = ld_cluster_v4(ad);
-          uint4 wb = make_uint4(0, 0, 0, 0);
-          if constexpr (HAS_B) wb = ld_cluster_v4(ad + BN * 4);
+          const uint4 wa = ld_cluster_v4(mapa(off, q));
           if constexpr (MODE == MODE_ZP) rs += static_cast<int32_t>(ld_cluster_u32(mapa(rs_addr + rl * 4, q)));
           if constexpr (BF16) {
             ra[0] = __float_as_uint(__uint_as_float(ra[0]) + __uint_as_float(wa.x));
@@ -778,12 +772,8 @@ __global__ void __launch_bounds__(NPW * 32 + 96, 1)
             ra[2] += wa.z;
             ra[3] += wa.w;
           }
-          rb[0] += wb.x;
-          rb[1] += wb.y;
-          rb[2] += wb.z;
-          rb[3] += wb.w;
         }
-        finish4(m0 + rl, n_tile * BN + gq * 4, ra, rb, rs);
+        finish4(m0 + rl, n_tile * BN + gq * 4, ra, rs);
       }
     }
     if (threadIdx.x == 0) stamp(7);
@@ -801,18 +791,20 @@ __global__ void __launch_bounds__(NPW * 32 + 96, 1)
 
 // ---------------------------------------------------------------------------
 // host-side launch helpers (called from kan_engine.cpp)
-constexpr int kNPW = 8;
-
 template <bool BF16, int NBP, int MODE>
 static cudaError_t launch_impl(const CUtensorMap& xmap, const GemmParams& p, size_t smem,
                                cudaStream_t st) {
-  auto kfn = kan_gather_gemm_kernel<BF16, NBP, kNPW, MODE>;
-  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
-  if (e != cudaSuccess) return e;
+  auto kfn = kan_gather_gemm_kernel<BF16, NBP, MODE>;
+  static size_t configured = 0;  // per instantiation: raise the smem limit once
+  if (smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(p.n_tiles_n, p.m_tiles, p.splits);
-  cfg.blockDim = dim3(kNPW * 32 + 96);
+  cfg.blockDim = dim3(352);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -822,22 +814,28 @@ static cudaError_t launch_impl(const CUtensorMap& xmap, const GemmParams& p, siz
   attr[0].val.clusterDim.z = p.splits;
   cfg.attrs = attr;
   cfg.numAttrs = p.splits > 1 ? 1 : 0;
-  e = cudaLaunchKernelEx(&cfg, kfn, xmap, p);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kfn, xmap, p);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
 int gemm_ips(bool bf16, int nbp) { return 128 / (nbp * (bf16 ? 2 : 1)); }
 int gemm_gs(bool bf16, int nbp) { return (bf16 ? 64 : 128) / gemm_ips(bf16, nbp); }
-int gemm_threads() { return kNPW * 32 + 96; }
+int gemm_threads() { return 352; }
+// TMEM A-ring depth: 32-column slots after the BN accumulator columns
+int gemm_tmem_slots(int BN) {
+  const int acol0 = (BN + 31) / 32 * 32;
+  const int n = (512 - acol0) / 32;
+  return n < 8 ? n : 8;
+}
 
 size_t gemm_smem_bytes(bool bf16, int nbp, int BN, int SA, int SB, int SX, int x_kind,
                        int tab_bytes) {
-  const size_t a = 16384, b = static_cast<size_t>(BN) * 128;
+  const size_t b = static_cast<size_t>(BN) * 128;
   const size_t x = 128u * gemm_ips(bf16, nbp) * (x_kind == X_F32 ? 4 : 2);
   const size_t t = (bf16 ? 0 : static_cast<size_t>(tab_bytes)) +
-                   (2 * SA + 2 * SB + 2 * SX + 2) * 8 + 128 * 4 + 3 * BN * 8 + 16;
-  return 1024 + SA * a + SB * b + SX * x + t;
+                   (2 * SA + 2 * SB + 2 * SX + 2) * 8 + 128 * 4 + 2 * BN * 8 + 16;
+  return 1024 + SB * b + SX * x + t;
 }
 
 cudaError_t launch_gather_gemm(bool bf16, int nbp, int mode, const CUtensorMap& xmap,

@@ -121,17 +121,10 @@ def test_silu_permutation_is_a_bijection():
     """Host-side SiLU K positions (kan_engine.cpp silu_pos) mirror the producer's
     shift-register order; each group's positions must be a permutation."""
     def silu_pos(bf16, nbp, gi):
-        if not bf16:
-            if nbp == 8:
-                sp, e = divmod(gi, 16)
-                return 16 * (e // 2) + 2 * sp + e % 2
-            sp, c = divmod(gi, 8)
-            return 16 * c + sp
-        if nbp == 8:
-            sp, c = divmod(gi, 8)
-            return 8 * c + sp
-        sp, e = divmod(gi, 4)
-        return 8 * (2 * e + (sp & 1)) + (sp >> 1)
+        ips = 128 // (nbp * (2 if bf16 else 1))
+        half = ips // 2
+        s, h, e = gi // ips, (gi % ips) // half, gi % half
+        return h * (32 if bf16 else 64) + s * half + e
     for bf16, n in ((False, 128), (True, 64)):
         for nbp in (8, 16):
             pos = [silu_pos(bf16, nbp, gi) for gi in range(n)]
