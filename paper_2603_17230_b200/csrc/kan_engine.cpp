@@ -144,10 +144,11 @@ static CUtensorMap make_xmap(const void* base, int x_kind, int64_t rows, int col
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * esz)};
   cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), 128u};
   cuuint32_t estr[2] = {1u, 1u};
-  // rows of 64 / 32 bytes are swizzled so the producers' row-per-lane 16-byte
+  // rows of 128 / 64 / 32 bytes are swizzled so the producers' row-per-lane 16-byte
   // reads are bank-conflict free (kan_gemm.cu xtile_off)
   const size_t row_bytes = static_cast<size_t>(box_cols) * esz;
-  const CUtensorMapSwizzle sw = row_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+  const CUtensorMapSwizzle sw = row_bytes == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
+                                : row_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
                                 : row_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
                                                   : CU_TENSOR_MAP_SWIZZLE_NONE;
   CUresult r = get_encode_fn()(
@@ -414,16 +415,22 @@ void quant_per_tensor(const std::vector<double>& w, int bits, std::vector<uint8_
   for (size_t i = 0; i < w.size(); ++i) q[i] = static_cast<uint8_t>(quantize(w[i], qp));
 }
 
-// Position of group-input gi inside the SiLU stage's 128-byte K row; must
+// Position of group-input gi inside the SiLU stage's KSTAGE-byte K row; must
 // match the producer's shift-register order in kan_gemm.cu.
-// Producer thread (row r, K-half h) handles inputs [h*IPS/2, (h+1)*IPS/2) of
-// every stage and shifts their SiLU codes into a 64-byte register that it
+// Producer thread (row r, K-quarter h) handles inputs [h*IPS/4, (h+1)*IPS/4)
+// of every stage and shifts their SiLU codes into a 64-byte register that it
 // writes as bytes [64h, 64h+64) of the base stage's row, in stage order.
 int silu_pos(bool bf16, int nbp, int gi) {
   const int ips = gemm_ips(bf16, nbp);
-  const int half = ips / 2;
-  const int s = gi / ips, h = (gi % ips) / half, e = gi % half;
-  return h * (bf16 ? 32 : 64) + s * half + e;  // element index in the 128-byte row
+  const int q = ips / 4;
+  const int s = gi / ips, h = (gi % ips) / q, e = gi % q;
+  return h * (bf16 ? 32 : 64) + s * q + e;  // element index in the stage row
+}
+
+// byte offset of K byte kb of weight row n in a stage tile: KSTAGE/128 SW128
+// blocks of [BN rows][128 B], one per 128 bytes of K
+static inline size_t tile_off(int BN, int n, int kb) {
+  return static_cast<size_t>(kb >> 7) * BN * 128 + sw128_off_host(n, (kb & 127) >> 4) + (kb & 15);
 }
 
 void prepare_gemm_layer(kan_engine* e, const Layer& l, PreparedLayer& pl, bool bf16) {
@@ -450,7 +457,7 @@ void prepare_gemm_layer(kan_engine* e, const Layer& l, PreparedLayer& pl, bool b
   const int last = pl.n_spline_stages - (pl.n_groups - 1) * pl.GS;
   pl.total_stages = (pl.n_groups - 1) * (pl.GS + pl.silu) + last + pl.silu;
   const int BN = pl.BN;
-  const size_t tile_bytes = static_cast<size_t>(BN) * 128;
+  const size_t tile_bytes = static_cast<size_t>(BN) * KSTAGE;
   std::vector<uint8_t> wt(static_cast<size_t>(pl.n_tiles_n) * pl.total_stages * tile_bytes, 0);
   const int esz = bf16 ? 2 : 1;
 
@@ -500,7 +507,7 @@ void prepare_gemm_layer(kan_engine* e, const Layer& l, PreparedLayer& pl, bool b
                 const size_t src = (static_cast<size_t>(i) * nb + b) * N + j;
                 const int elem = ii * nbp + b;
                 const int kb = elem * esz;
-                uint8_t* dst = tile + sw128_off_host(n, kb >> 4) + (kb & 15);
+                uint8_t* dst = tile + tile_off(BN, n, kb);
                 if (bf16) {
                   const __nv_bfloat16 bv = __float2bfloat16_rn(static_cast<float>(l.coeffs[src]));
                   std::memcpy(dst, &bv, 2);
@@ -517,7 +524,7 @@ void prepare_gemm_layer(kan_engine* e, const Layer& l, PreparedLayer& pl, bool b
               if (i >= n_in) break;
               const int elem = silu_pos(bf16, nbp, gi);
               const int kb = elem * esz;
-              uint8_t* dst = tile + sw128_off_host(n, kb >> 4) + (kb & 15);
+              uint8_t* dst = tile + tile_off(BN, n, kb);
               const size_t src = static_cast<size_t>(i) * N + j;
               if (bf16) {
                 const __nv_bfloat16 bv = __float2bfloat16_rn(static_cast<float>(l.base_w[src]));
@@ -740,7 +747,7 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
   // they must fit in the idle A/B rings.
   const int tiles = p.m_tiles * p.n_tiles_n;
   const size_t red_bytes = static_cast<size_t>(128) * (pl.BN + 4) * 4;
-  const size_t ring_bytes = static_cast<size_t>(SB) * pl.BN * 128 +
+  const size_t ring_bytes = static_cast<size_t>(SB) * pl.BN * KSTAGE +
                             static_cast<size_t>(SX) * 128 * pl.IPS * (io.x_kind == X_F32 ? 4 : 2);
   int want = e->cfg.split_k > 0 ? e->cfg.split_k : 1;
   if (e->cfg.split_k <= 0 && tiles < 148) want = (148 + tiles - 1) / tiles;

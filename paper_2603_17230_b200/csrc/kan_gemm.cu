@@ -7,21 +7,22 @@
 //     -> matmul (matrix.hpp:64-80)
 // and, on the float path, kan_linear_forward<RecursiveBasis> (layers.hpp:118-121).
 //
-// One CTA computes a 128-row x BN-column output tile over a range of K.
+// One CTA computes a 128-row x BN-column output tile over a range of K, in
+// KSTAGE (256) byte K stages of eight 32-byte tcgen05.mma steps.
 // The dense basis ("A") tile never touches shared memory: producers write it
 // straight into tensor memory, where tcgen05.mma reads it (A-from-TMEM form).
-// Warp roles (352 threads, one CTA per SM):
-//   warps 0..7   producers.  Thread (warp w, lane l) owns row 32*(w%4)+l and
-//                K-half w/4 of every 128-byte K stage: it reads its row's
-//                activations from the TMA-filled (swizzled) smem tile, computes
-//                each lattice level (fp32 estimate + exact tie test), expands
-//                it into the row of LUT codes (vals[frac] << 8*jj) -- or the
-//                fp32 Cox-de Boor basis in bf16 on the float path -- and stores
-//                its 64 bytes into the TMEM A ring with one tcgen05.st.  They
-//                also build the SiLU base rows and run the epilogue.
-//   warp 8       TMA loader of the activation ring (released by producers).
-//   warp 9       TMEM allocation + single-thread tcgen05.mma issuer.
-//   warp 10      bulk-copy loader of the lattice tables and the pre-swizzled
+// Warp roles (608 threads, one CTA per SM):
+//   warps 0..15  producers.  Thread (warp w, lane l) owns row 32*(w%4)+l and
+//                K-quarter w/4 of every stage: it reads its row's activations
+//                from the TMA-filled (swizzled) smem tile, computes each
+//                lattice level (fp32 estimate + exact tie test), expands it
+//                into the row of LUT codes (vals[frac] << 8*jj) -- or the fp32
+//                Cox-de Boor basis in bf16 on the float path -- and stores its
+//                64 bytes into the TMEM A ring with one tcgen05.st.  They also
+//                build the SiLU base rows and run the epilogue.
+//   warp 16      TMA loader of the activation ring (released by producers).
+//   warp 17      TMEM allocation + single-thread tcgen05.mma issuer.
+//   warp 18      bulk-copy loader of the lattice tables and the pre-swizzled
 //                weight (B) tiles (ring released by the MMA).
 // The int32 (LUT) or fp32 (bf16) accumulator lives in TMEM columns [0, BN).
 #include <cuda.h>
@@ -203,10 +204,10 @@ struct Ring {
 template <bool BF16, int NBP>
 struct Cfg {
   static constexpr int ESZ = BF16 ? 2 : 1;
-  static constexpr int IPS = 128 / (NBP * ESZ);       // inputs per 128-byte K stage
-  static constexpr int HALF = IPS / 2;                // inputs per producer thread per stage
-  static constexpr int GS = (BF16 ? 64 : 128) / IPS;  // spline stages per SiLU group
-  static constexpr int SW = HALF * ESZ / 4;           // SiLU code words per thread per stage
+  static constexpr int IPS = KSTAGE / (NBP * ESZ);  // inputs per K stage
+  static constexpr int Q = IPS / 4;                 // inputs per producer thread per stage
+  static constexpr int GS = KSTAGE / ESZ / IPS;     // spline stages per SiLU group
+  static constexpr int SW = Q * ESZ / 4;            // SiLU code words per thread per stage
 };
 
 // A-from-TMEM MMAs (M = 128, B K-major in smem)
@@ -242,12 +243,33 @@ __device__ __forceinline__ void tmem_wait_st() {
 }
 
 // Byte offset of 16-byte chunk `c` of row `r` in a TMA tile whose rows are
-// `row_bytes` wide and written with the matching swizzle (64 B rows:
-// SWIZZLE_64B, 32 B rows: SWIZZLE_32B, 16 B rows: none).  The swizzle makes a
-// warp's row-per-lane 16-byte reads bank-conflict free.
+// `row_bytes` wide and written with the matching swizzle (128 / 64 / 32 B rows:
+// SWIZZLE_128B / 64B / 32B).  The swizzle makes a warp's row-per-lane 16-byte
+// reads bank-conflict free.
 __device__ __forceinline__ uint32_t xtile_off(int r, int c, int row_bytes) {
-  const int sw = row_bytes == 64 ? ((r >> 1) & 3) : (row_bytes == 32 ? ((r >> 2) & 1) : 0);
+  const int sw = row_bytes == 128 ? (r & 7)
+                 : row_bytes == 64 ? ((r >> 1) & 3)
+                                   : ((r >> 2) & 1);
   return static_cast<uint32_t>(r * row_bytes + ((c ^ sw) << 4));
+}
+
+// This thread's NB activation bytes (NB = 8, 16 or 32) at byte `off` of row r.
+template <int NB>
+__device__ __forceinline__ void load_x(const uint8_t* xt, int r, int off, int row_bytes,
+                                       uint32_t (&d)[NB / 4]) {
+  if constexpr (NB == 32) {
+    const uint4 a = *reinterpret_cast<const uint4*>(xt + xtile_off(r, off >> 4, row_bytes));
+    const uint4 b = *reinterpret_cast<const uint4*>(xt + xtile_off(r, (off >> 4) + 1, row_bytes));
+    d[0] = a.x; d[1] = a.y; d[2] = a.z; d[3] = a.w;
+    d[4] = b.x; d[5] = b.y; d[6] = b.z; d[7] = b.w;
+  } else if constexpr (NB == 16) {
+    const uint4 a = *reinterpret_cast<const uint4*>(xt + xtile_off(r, off >> 4, row_bytes));
+    d[0] = a.x; d[1] = a.y; d[2] = a.z; d[3] = a.w;
+  } else {
+    const uint2 a =
+        *reinterpret_cast<const uint2*>(xt + xtile_off(r, off >> 4, row_bytes) + (off & 15));
+    d[0] = a.x; d[1] = a.y;
+  }
 }
 
 // Exact lattice level of an fp32 activation.  t = x*(1/step) - lo/step in one
@@ -267,16 +289,17 @@ __device__ __forceinline__ int lattice_level_x(float x, const GemmParams& p, con
   return g;
 }
 
-// 64 bytes of one A row (this thread's K-half of a stage) on the LUT path.
+// 64 bytes of one A row (this thread's K-quarter of a stage) on the LUT path.
 // The P+1 codes of lut_basis_lookup depend only on frac = a mod 2^k
 // (lut.hpp:145-157): vals[frac] holds them packed, and an input's NBP-byte
-// row segment is vals[frac] shifted to byte jj = a >> k.
+// row segment is vals[frac] shifted to byte jj = a >> k (branch-free: clamped
+// funnel shifts give zero for words the codes do not reach).
 template <int NBP, int MODE>
 __device__ __forceinline__ void lut_row(const GemmParams& p, const uint32_t* vals,
-                                        const uint8_t* silu_tab, const int (&a)[128 / NBP / 2],
+                                        const uint8_t* silu_tab, const int (&a)[64 / NBP],
                                         int i0, uint32_t (&w)[16], uint32_t& rsum,
                                         uint32_t (&sil)[16]) {
-  constexpr int H = 128 / NBP / 2;  // inputs in this thread's half
+  constexpr int H = 64 / NBP;  // inputs in this thread's quarter
   const int mask = (1 << p.k) - 1;
 #pragma unroll
   for (int e = 0; e < H; ++e) {
@@ -287,13 +310,11 @@ __device__ __forceinline__ void lut_row(const GemmParams& p, const uint32_t* val
       w[2 * e] = static_cast<uint32_t>(pt);
       w[2 * e + 1] = static_cast<uint32_t>(pt >> 32);
     } else {
-      const int wi = jj >> 2, sh = (jj & 3) * 8;
-      const uint32_t lo = __funnelshift_l(0u, v, sh);
-      const uint32_t hi = __funnelshift_l(v, 0u, sh);
-      w[4 * e] = (wi == 0) ? lo : 0u;
-      w[4 * e + 1] = (wi == 1) ? lo : ((wi == 0) ? hi : 0u);
-      w[4 * e + 2] = (wi == 2) ? lo : ((wi == 1) ? hi : 0u);
-      w[4 * e + 3] = (wi == 3) ? lo : ((wi == 2) ? hi : 0u);
+      const uint32_t sft = 8u * static_cast<uint32_t>(jj);
+      w[4 * e] = __funnelshift_lc(0u, v, sft);
+#pragma unroll
+      for (uint32_t q = 1; q < 4; ++q)
+        w[4 * e + q] = __funnelshift_lc(0u, v, sft - 32u * q) | __funnelshift_rc(v, 0u, 32u * q - sft);
     }
     if constexpr (MODE == MODE_ZP) {
       // codes shifted past the row end are zero (see lut_basis_lookup)
@@ -318,9 +339,9 @@ __device__ __forceinline__ void lut_row(const GemmParams& p, const uint32_t* val
 
 // 64 bytes of one A row on the bf16 path: fp32 Cox-de Boor basis -> bf16.
 template <int NBP, int MODE>
-__device__ __forceinline__ void bf16_row(const GemmParams& p, const float (&x)[128 / NBP / 4],
+__device__ __forceinline__ void bf16_row(const GemmParams& p, const float (&x)[32 / NBP],
                                          uint32_t (&w)[16], uint32_t (&sil)[16]) {
-  constexpr int H = 128 / NBP / 4;  // inputs in this thread's half (bf16: NBP*2 bytes each)
+  constexpr int H = 32 / NBP;  // inputs in this thread's quarter (bf16: NBP*2 bytes each)
   constexpr int PMAX = 3;
 #pragma unroll
   for (int e = 0; e < H; ++e) {
@@ -360,17 +381,17 @@ __device__ __forceinline__ void bf16_row(const GemmParams& p, const float (&x)[1
 }
 
 template <bool BF16, int NBP, int MODE>
-__global__ void __launch_bounds__(352, 1)
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
     kan_gather_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const GemmParams p) {
   using C = Cfg<BF16, NBP>;
-  constexpr int NPW = 8, NP = 256;
+  constexpr int NPW = GEMM_PRODUCER_WARPS, NP = 32 * NPW;
   constexpr bool SILU = (MODE == MODE_SILU);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
 
   const int SA = p.SA, SB = p.SB, SX = p.SX;
   const int BN = p.BN;
-  const uint32_t b_bytes = static_cast<uint32_t>(BN) * 128u;
+  const uint32_t b_bytes = static_cast<uint32_t>(BN) * KSTAGE;
   const uint32_t xesz = (p.x_kind == X_F32) ? 4u : 2u;
   const int x_row_bytes = C::IPS * static_cast<int>(xesz);
   const uint32_t x_bytes = 128u * static_cast<uint32_t>(x_row_bytes);
@@ -412,8 +433,9 @@ __global__ void __launch_bounds__(352, 1)
   const uint32_t bar_tmem_full = smem_u32(bars + 2 * SX + 2 * SA + 2 * SB);
   const uint32_t bar_tab = smem_u32(bars + 2 * SX + 2 * SA + 2 * SB + 1);
 
-  // TMEM: accumulator in columns [0, BN), A ring slots of 32 columns from acol0
+  // TMEM: accumulator in columns [0, BN), A ring slots of KSTAGE/4 columns from acol0
   constexpr uint32_t tmem_cols = 512;
+  constexpr uint32_t acols = KSTAGE / 4;
   const uint32_t acol0 = static_cast<uint32_t>((BN + 31) / 32 * 32);
 
   // ---- setup -------------------------------------------------------------
@@ -490,7 +512,7 @@ __global__ void __launch_bounds__(352, 1)
   } else if (warp == NPW + 1) {
     // ============================ MMA issuer ==============================
     const uint32_t idesc = BF16 ? idesc_bf16(BN) : idesc_i8(BN, p.b_signed != 0);
-    const int nk = (p.dbg_flags & 2) ? 0 : 4;
+    const int nk = (p.dbg_flags & 2) ? 0 : KSTAGE / 32;
     Ring ra(SA), rb(SB);
     bool first = true;
     for (int g = g0; g < g1; ++g) {
@@ -500,10 +522,11 @@ __global__ void __launch_bounds__(352, 1)
         mbar_wait(bar_bfull(rb.slot), rb.phase);
         tc_fence_after();
         if (lane == 0) {
-          const uint32_t a_tmem = tmem + acol0 + 32u * static_cast<uint32_t>(ra.slot);
+          const uint32_t a_tmem = tmem + acol0 + acols * static_cast<uint32_t>(ra.slot);
           const uint32_t b_addr = smem_u32(sB + static_cast<size_t>(rb.slot) * b_bytes);
           for (int kk = 0; kk < nk; ++kk) {
-            const uint64_t bd = umma_desc_sw128(b_addr + 32 * kk);
+            // K step kk: SW128 block kk/4 of the stage's weight tile, 32 bytes in
+            const uint64_t bd = umma_desc_sw128(b_addr + (kk >> 2) * BN * 128 + 32 * (kk & 3));
             const uint32_t acc = (first && kk == 0) ? 0u : 1u;
             if (BF16)
               mma_f16_ts(tmem, a_tmem + 8 * kk, bd, idesc, acc);
@@ -522,7 +545,7 @@ __global__ void __launch_bounds__(352, 1)
   } else {
     // ============================ producers ===============================
     const int quarter = warp & 3;
-    const int h = warp >> 2;  // K-half of each stage this thread fills
+    const int h = warp >> 2;  // K-quarter of each stage this thread fills
     const int r = quarter * 32 + lane;
     const uint32_t t_lane = static_cast<uint32_t>(quarter * 32) << 16;
     uint32_t sil[16];
@@ -534,7 +557,8 @@ __global__ void __launch_bounds__(352, 1)
     const uint32_t* vals = reinterpret_cast<const uint32_t*>(sT);
     const float* thr = reinterpret_cast<const float*>(sT + p.off_thr);
     const uint8_t* silu_tab = sT + p.off_silu;
-    constexpr int H = C::HALF;
+    constexpr int H = C::Q;
+    const int xoff = h * H * static_cast<int>(xesz);  // this thread's bytes in the x row
 
     Ring ra(SA), rx(SX);
     int idx = 0;
@@ -548,21 +572,14 @@ __global__ void __launch_bounds__(352, 1)
           const uint8_t* xt = sX + static_cast<size_t>(rx.slot) * x_bytes;
           const int i0 = (g * C::GS + s) * C::IPS + h * H;
           if constexpr (BF16) {
-            float x[H];
-            if constexpr (H == 4) {
-              const float4 v = *reinterpret_cast<const float4*>(xt + xtile_off(r, h, x_row_bytes));
-              x[0] = v.x;
-              x[1] = v.y;
-              x[2] = v.z;
-              x[3] = v.w;
-            } else {
-              const float2 v = *reinterpret_cast<const float2*>(xt + r * x_row_bytes + 8 * h);
-              x[0] = v.x;
-              x[1] = v.y;
-            }
+            uint32_t xr[H];
+            load_x<4 * H>(xt, r, xoff, x_row_bytes, xr);
             __syncwarp();
             if (lane == 0) mbar_arrive(bar_xempty(rx.slot));
             rx.next();
+            float x[H];
+#pragma unroll
+            for (int e = 0; e < H; ++e) x[e] = __uint_as_float(xr[e]);
             if (p.dbg_flags & 1) {
 #pragma unroll
               for (int q = 0; q < 16; ++q) w[q] = 0;
@@ -572,38 +589,22 @@ __global__ void __launch_bounds__(352, 1)
           } else {
             int a[H];
             if (p.x_kind == X_F32) {
-              float x[H];
-#pragma unroll
-              for (int q = 0; q < H / 4; ++q) {
-                const float4 v =
-                    *reinterpret_cast<const float4*>(xt + xtile_off(r, h * (H / 4) + q, x_row_bytes));
-                x[4 * q] = v.x;
-                x[4 * q + 1] = v.y;
-                x[4 * q + 2] = v.z;
-                x[4 * q + 3] = v.w;
-              }
+              uint32_t xr[H];
+              load_x<4 * H>(xt, r, xoff, x_row_bytes, xr);
               __syncwarp();
               if (lane == 0) mbar_arrive(bar_xempty(rx.slot));
 #pragma unroll
-              for (int e = 0; e < H; ++e) a[e] = lattice_level_x(x[e], p, thr);
+              for (int e = 0; e < H; ++e) a[e] = lattice_level_x(__uint_as_float(xr[e]), p, thr);
             } else {
-              if constexpr (H == 8) {
-                const uint4 v = *reinterpret_cast<const uint4*>(xt + xtile_off(r, h, x_row_bytes));
-                const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                  a[2 * q] = static_cast<int>(vv[q] & 0xFFFF);
-                  a[2 * q + 1] = static_cast<int>(vv[q] >> 16);
-                }
-              } else {
-                const uint2 v = *reinterpret_cast<const uint2*>(xt + r * x_row_bytes + 8 * h);
-                a[0] = static_cast<int>(v.x & 0xFFFF);
-                a[1] = static_cast<int>(v.x >> 16);
-                a[2] = static_cast<int>(v.y & 0xFFFF);
-                a[3] = static_cast<int>(v.y >> 16);
-              }
+              uint32_t xr[H / 2];
+              load_x<2 * H>(xt, r, xoff, x_row_bytes, xr);
               __syncwarp();
               if (lane == 0) mbar_arrive(bar_xempty(rx.slot));
+#pragma unroll
+              for (int q = 0; q < H / 2; ++q) {
+                a[2 * q] = static_cast<int>(xr[q] & 0xFFFF);
+                a[2 * q + 1] = static_cast<int>(xr[q] >> 16);
+              }
             }
             rx.next();
             if (p.dbg_flags & 1) {
@@ -631,7 +632,7 @@ __global__ void __launch_bounds__(352, 1)
         // 2. the A slot must be free (its previous MMAs retired), then store
         mbar_wait(bar_aempty(ra.slot), ra.phase ^ 1);
         tc_fence_after();
-        tmem_st16(tmem + t_lane + acol0 + 32u * static_cast<uint32_t>(ra.slot) + 16u * h, w);
+        tmem_st16(tmem + t_lane + acol0 + acols * static_cast<uint32_t>(ra.slot) + 16u * h, w);
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
@@ -804,7 +805,7 @@ static cudaError_t launch_impl(const CUtensorMap& xmap, const GemmParams& p, siz
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(p.n_tiles_n, p.m_tiles, p.splits);
-  cfg.blockDim = dim3(352);
+  cfg.blockDim = dim3(GEMM_THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -819,19 +820,19 @@ static cudaError_t launch_impl(const CUtensorMap& xmap, const GemmParams& p, siz
   return cudaGetLastError();
 }
 
-int gemm_ips(bool bf16, int nbp) { return 128 / (nbp * (bf16 ? 2 : 1)); }
-int gemm_gs(bool bf16, int nbp) { return (bf16 ? 64 : 128) / gemm_ips(bf16, nbp); }
-int gemm_threads() { return 352; }
-// TMEM A-ring depth: 32-column slots after the BN accumulator columns
+int gemm_ips(bool bf16, int nbp) { return KSTAGE / (nbp * (bf16 ? 2 : 1)); }
+int gemm_gs(bool bf16, int nbp) { return KSTAGE / (bf16 ? 2 : 1) / gemm_ips(bf16, nbp); }
+int gemm_threads() { return GEMM_THREADS; }
+// TMEM A-ring depth: KSTAGE/4-column slots after the BN accumulator columns
 int gemm_tmem_slots(int BN) {
   const int acol0 = (BN + 31) / 32 * 32;
-  const int n = (512 - acol0) / 32;
+  const int n = (512 - acol0) / (KSTAGE / 4);
   return n < 8 ? n : 8;
 }
 
 size_t gemm_smem_bytes(bool bf16, int nbp, int BN, int SA, int SB, int SX, int x_kind,
                        int tab_bytes) {
-  const size_t b = static_cast<size_t>(BN) * 128;
+  const size_t b = static_cast<size_t>(BN) * KSTAGE;
   const size_t x = 128u * gemm_ips(bf16, nbp) * (x_kind == X_F32 ? 4 : 2);
   const size_t t = (bf16 ? 0 : static_cast<size_t>(tab_bytes)) +
                    (2 * SA + 2 * SB + 2 * SX + 2) * 8 + 128 * 4 + 2 * BN * 8 + 16;

@@ -13,6 +13,12 @@ enum EpiKind : int {
 
 enum XKind : int { X_F32 = 0, X_U16 = 1 };
 
+// K bytes per pipeline stage of the gather GEMM: eight 32-byte tcgen05.mma
+// K-steps; the stage's weight tile is two 128-byte-wide SW128 blocks.
+constexpr int KSTAGE = 256;
+constexpr int GEMM_PRODUCER_WARPS = 16;
+constexpr int GEMM_THREADS = 32 * (GEMM_PRODUCER_WARPS + 3);
+
 // One fused gather + tcgen05 GEMM launch (one KAN layer, linear form).
 struct GemmParams {
   int M, n_in, N;

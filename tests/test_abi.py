@@ -121,11 +121,11 @@ def test_silu_permutation_is_a_bijection():
     """Host-side SiLU K positions (kan_engine.cpp silu_pos) mirror the producer's
     shift-register order; each group's positions must be a permutation."""
     def silu_pos(bf16, nbp, gi):
-        ips = 128 // (nbp * (2 if bf16 else 1))
-        half = ips // 2
-        s, h, e = gi // ips, (gi % ips) // half, gi % half
-        return h * (32 if bf16 else 64) + s * half + e
-    for bf16, n in ((False, 128), (True, 64)):
+        ips = 256 // (nbp * (2 if bf16 else 1))
+        q = ips // 4
+        s, h, e = gi // ips, (gi % ips) // q, gi % q
+        return h * (32 if bf16 else 64) + s * q + e
+    for bf16, n in ((False, 256), (True, 128)):
         for nbp in (8, 16):
             pos = [silu_pos(bf16, nbp, gi) for gi in range(n)]
             assert sorted(pos) == list(range(n))
