@@ -135,6 +135,12 @@ void kor_levels_f32(const kor_grid* g, int k, const float* x, size_t n, uint16_t
   for (size_t i = 0; i < n; ++i) out[i] = (uint16_t)kor_level_of(g, k, (double)x[i]);
 }
 
+/* next-layer levels of fp64 layer outputs: the consuming layer clamps
+ * (layers.hpp:111) and quantizes (lut.hpp:44-47) */
+void kor_levels_f64(const kor_grid* g, int k, const double* y, size_t n, uint16_t* out) {
+  for (size_t i = 0; i < n; ++i) out[i] = (uint16_t)kor_level_of(g, k, y[i]);
+}
+
 /* entries = ceil((P+1)/2) * 2^k + 1 (lut.hpp:118-119) */
 size_t kor_lut_size(int P, int k) { return (size_t)((P + 2) / 2) * ((size_t)1 << k) + 1; }
 

@@ -56,6 +56,7 @@ int64_t kor_lattice_quantize(const kor_grid* g, int k, double x);
 /* level of a raw activation (clamp_to_domain first, as kan_linear_forward does) */
 int64_t kor_level_of(const kor_grid* g, int k, double x);
 void kor_levels_f32(const kor_grid* g, int k, const float* x, size_t n, uint16_t* out);
+void kor_levels_f64(const kor_grid* g, int k, const double* y, size_t n, uint16_t* out);
 size_t kor_lut_size(int P, int k);
 int kor_build_lut(int P, int k, int h, uint8_t* entries, size_t cap);
 /* returns count (number of values written); -1 when the level is out of range */

@@ -68,6 +68,7 @@ class Oracle:
         L.kor_level_of.argtypes = [G, C.c_int, C.c_double]
         L.kor_level_of.restype = C.c_int64
         L.kor_levels_f32.argtypes = [G, C.c_int, _fp, C.c_size_t, _u16p]
+        L.kor_levels_f64.argtypes = [G, C.c_int, _dp, C.c_size_t, _u16p]
         L.kor_lut_size.argtypes = [C.c_int, C.c_int]
         L.kor_lut_size.restype = C.c_size_t
         L.kor_build_lut.argtypes = [C.c_int, C.c_int, C.c_int, _u8p, C.c_size_t]
@@ -270,6 +271,137 @@ class Oracle:
         return out
 
 
+    def levels_f64(self, g, k, y):
+        """Next-layer lattice levels of fp64 layer outputs (clamp + quantize)."""
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        out = np.zeros(y.shape, dtype=np.uint16)
+        self.lib.kor_levels_f64(C.byref(g), k, y.ravel(), y.size, out.ravel())
+        return out
+
+    @staticmethod
+    def im2col_levels(lv, kernel, stride, padding, pad_level):
+        """im2col (layers.hpp:126-154) over lattice levels [M, C, H, W] ->
+        [M*Ho*Wo, C*K*K] in the reference's channel-major column order.  Padded
+        taps hold level(0.0) (the reference leaves them 0.0 and the basis is
+        evaluated there).  Output size uses floor semantics; with a stride that
+        does not divide the padded span this equals the reference on the input
+        zero-extended at the bottom/right (stride-2 recipe)."""
+        M, Cc, H, W = lv.shape
+        Ho = (H + 2 * padding - kernel) // stride + 1
+        Wo = (W + 2 * padding - kernel) // stride + 1
+        ph = max(H + 2 * padding, stride * (Ho - 1) + kernel)
+        pw = max(W + 2 * padding, stride * (Wo - 1) + kernel)
+        pad = np.full((M, Cc, ph, pw), pad_level, dtype=np.uint16)
+        pad[:, :, padding:padding + H, padding:padding + W] = lv
+        taps = []
+        for ky in range(kernel):
+            for kx in range(kernel):
+                taps.append(pad[:, :, ky:ky + stride * (Ho - 1) + 1:stride,
+                                kx:kx + stride * (Wo - 1) + 1:stride])
+        t = np.stack(taps, axis=2)  # [M, C, KK, Ho, Wo]
+        return np.ascontiguousarray(t.transpose(0, 3, 4, 1, 2)).reshape(M * Ho * Wo,
+                                                                        Cc * kernel * kernel)
+
+    @staticmethod
+    def storage_kinds(desc):
+        """Engine storage rule (kan_engine.cpp plan_buffers): a stored tensor keeps
+        fp32 values when a consumer needs values (residual add, average pool;
+        passed back through maxpool / flatten views), else lattice levels.
+        Returns (per-layer flags, flag for the model input)."""
+        layers = desc["layers"]
+        named, src = {"input": -1}, []
+        for i, l in enumerate(layers):
+            src.append(named[l["input_from"]] if "input_from" in l else i - 1)
+            if "id" in l:
+                named[l["id"]] = i
+        need = [False] * len(layers)
+        need_in = [False]
+
+        def mark(t):
+            if t >= 0:
+                need[t] = True
+            else:
+                need_in[0] = True
+        for i in range(len(layers) - 1, -1, -1):
+            l = layers[i]
+            if "residual" in l:
+                mark(named[l["residual"]])
+            if l["type"] == "global_avgpool":
+                mark(src[i])
+            if l["type"] in ("maxpool", "flatten") and need[i]:
+                mark(src[i])
+        return need, need_in[0]
+
+    def int_model_forward(self, desc, Ws, Bs, x, k, h, wscheme, bits_w):
+        """The engine's integer LUT path over a model descriptor, layer by layer:
+        levels -> (im2col) -> integer layer -> fp64 epilogue (+ residual) ->
+        stored as next-layer levels, or as fp32 values where a consumer needs
+        values (storage_kinds); returns the last layer's fp64 output ([M, N] for
+        linear, [M, C, Ho, Wo] for conv)."""
+        G, P = desc["grid"]["intervals"], desc["grid"]["degree"]
+        lo, hi = desc.get("domain", [-1.0, 1.0])
+        g = self.grid(G, P, lo, hi)
+        lvl0 = self.level_of(g, k, 0.0)
+        need, need_in = self.storage_kinds(desc)
+        M = x.shape[0]
+        x = np.ascontiguousarray(x, np.float32).reshape(M, *desc["input"])
+        tens = {-1: ("f32", x) if (need_in or len(desc["input"]) == 1)
+                else ("lv", self.levels(g, k, x))}
+        named = {"input": -1}
+
+        def levels(t):
+            return self.levels(g, k, t[1]) if t[0] == "f32" else t[1]
+        ki = 0
+        y = None
+        layers = desc["layers"]
+        for i, l in enumerate(layers):
+            src = named[l["input_from"]] if "input_from" in l else i - 1
+            t = tens[src]
+            typ = l["type"]
+            last = i + 1 == len(layers)
+            if typ in ("conv", "linear"):
+                d = self.int_layer(g, k, h, wscheme, bits_w, Ws[ki], Bs[ki])
+                N = Ws[ki].shape[1]
+                ki += 1
+                lv = levels(t)
+                if typ == "conv":
+                    kk, s_, p_ = l["kernel"], l.get("stride", 1), l.get("padding", 0)
+                    Ho = (lv.shape[2] + 2 * p_ - kk) // s_ + 1
+                    Wo = (lv.shape[3] + 2 * p_ - kk) // s_ + 1
+                    cols = self.im2col_levels(lv, kk, s_, p_, lvl0)
+                    y = self.int_layer_forward(g, k, h, d, cols, N)
+                    y = y.reshape(M, Ho, Wo, N).transpose(0, 3, 1, 2)
+                else:
+                    y = self.int_layer_forward(g, k, h, d, lv.reshape(M, -1), N)
+                if "residual" in l:
+                    r = tens[named[l["residual"]]]
+                    assert r[0] == "f32"
+                    y = y + r[1].astype(np.float64)
+                if last:
+                    return y
+                tens[i] = ("f32", y.astype(np.float32)) if need[i] else ("lv", self.levels_f64(g, k, y))
+            elif typ == "maxpool":
+                w = l.get("window", 2)
+                a = t[1]
+                Ho, Wo = a.shape[2] // w, a.shape[3] // w
+                v = a[:, :, :Ho * w, :Wo * w].reshape(M, a.shape[1], Ho, w, Wo, w)
+                tens[i] = (t[0], v.max(axis=(3, 5)))
+            elif typ == "global_avgpool":
+                assert t[0] == "f32"
+                v = t[1].reshape(M, t[1].shape[1], -1)
+                acc = np.zeros(v.shape[:2])
+                for q in range(v.shape[2]):  # position order, one rounding per add
+                    acc = acc + v[:, :, q].astype(np.float64)
+                tens[i] = ("f32", (acc / v.shape[2]).astype(np.float32))
+            elif typ == "flatten":
+                tens[i] = (t[0], t[1].reshape(M, -1))
+            else:
+                raise ValueError(typ)
+            if "id" in l:
+                named[l["id"]] = i
+        return y
+
+
 class Ref:
     """The unmodified reference headers behind oracle/ref_shim.cpp."""
 
@@ -307,6 +439,8 @@ class Ref:
                                        C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                        C.c_int, C.c_int, C.c_int, _dp, _dp, _dp]
         L.ref_validate_descriptor.argtypes = [C.c_char_p]
+        L.ref_graph_forward.argtypes = [C.c_char_p, C.POINTER(C.c_void_p), C.c_int, C.c_int,
+                                        C.c_int, C.c_int64, _dp, C.c_int64, _dp, C.c_int]
         L.ref_model_forward.argtypes = [C.c_char_p, C.POINTER(C.c_void_p), C.c_int, C.c_int,
                                         C.c_int, C.c_int, C.c_int64, C.c_int64, _dp, C.c_int64,
                                         _dp, C.c_int, C.c_int64]
@@ -403,6 +537,18 @@ class Ref:
         out = np.zeros((c_out, Ho, Wo))
         if self.lib.ref_conv_forward(G, P, lo, hi, mode, k, h, bits_w, Cc, H, W, c_out, kernel,
                                      stride, padding, x, coeffs, out):
+            raise ValueError(self.err())
+        return out
+
+    def graph_forward(self, text, coeffs, inputs, n_out, k=8, h=8, bits_w=8, threads=1):
+        """Harness composition of reference functions for extended descriptors
+        (residual blocks, global average pool, floor-stride convs); LUT mode."""
+        inputs = np.ascontiguousarray(inputs, dtype=np.float64)
+        cs = [np.ascontiguousarray(c, dtype=np.float64) for c in coeffs]
+        ptrs = (C.c_void_p * len(cs))(*[c.ctypes.data for c in cs])
+        out = np.zeros((inputs.shape[0], n_out))
+        if self.lib.ref_graph_forward(text.encode(), ptrs, k, h, bits_w, inputs.shape[0], inputs,
+                                      n_out, out, threads):
             raise ValueError(self.err())
         return out
 

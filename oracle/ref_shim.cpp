@@ -274,4 +274,156 @@ int ref_model_forward(const char* json_text, const double* const* coeff_ptrs, in
   return fail(e);
 }
 
+// Harness composition for descriptors the reference cannot express (the
+// engine's additive extension: named tensors id / input_from / residual,
+// global_avgpool, "conv_output": "floor"), built ONLY from reference
+// functions: convkan_forward with LutBasis over maybe_fake_quant_weights
+// (eval.hpp:70-76, 185-188), kan_linear_forward, maxpool2, flatten.  Residual
+// adds and the global average pool are harness fp64 loops; a stride that does
+// not divide the padded span runs the reference on the input zero-extended at
+// the bottom/right and crops (SURVEY.md 8(c) stride-2 recipe).  Used as the
+// CPU baseline for ResKAN18 (C5); samples are sharded over std::threads.
+int ref_graph_forward(const char* json_text, const double* const* coeff_ptrs, int k, int h,
+                      int bits_w, int64_t M, const double* inputs, int64_t n_out, double* out,
+                      int threads) try {
+  const nlohmann::json j = nlohmann::json::parse(json_text);
+  const GridSpec grid = build_grid(j["grid"]["intervals"].get<int>(), j["grid"]["degree"].get<int>(),
+                                   j.contains("domain") ? j["domain"][0].get<double>() : -1.0,
+                                   j.contains("domain") ? j["domain"][1].get<double>() : 1.0);
+  const BsplineLut lut = build_bspline_lut(grid.degree(), k, h);
+  const LutBasis basis{&grid, &lut, ActivationLattice::of(grid, k)};
+  const std::vector<int> in_shape = j["input"].get<std::vector<int>>();
+  struct L {
+    std::string type, id, from, res;
+    ConvKanLayer conv;
+    KanLinearLayer lin;
+    int window = 2;
+  };
+  std::vector<L> layers;
+  int li = 0;
+  for (const auto& jl : j["layers"]) {
+    L l;
+    l.type = jl["type"].get<std::string>();
+    if (jl.contains("id")) l.id = jl["id"].get<std::string>();
+    if (jl.contains("input_from")) l.from = jl["input_from"].get<std::string>();
+    if (jl.contains("residual")) l.res = jl["residual"].get<std::string>();
+    if (l.type == "conv") {
+      l.conv = ConvKanLayer::zeros(jl["c_in"].get<int>(), jl["c_out"].get<int>(), jl["kernel"].get<int>(),
+                                   jl.value("stride", 1), jl.value("padding", 0), grid);
+      std::copy(coeff_ptrs[li], coeff_ptrs[li] + l.conv.coeffs.size(), l.conv.coeffs.flat().begin());
+      l.conv.coeffs = detail::maybe_fake_quant_weights(l.conv.coeffs, bits_w);
+      ++li;
+    } else if (l.type == "linear") {
+      l.lin = KanLinearLayer::zeros(jl["n_in"].get<int>(), jl["n_out"].get<int>(), grid);
+      std::copy(coeff_ptrs[li], coeff_ptrs[li] + l.lin.coeffs.size(), l.lin.coeffs.flat().begin());
+      l.lin.coeffs = detail::maybe_fake_quant_weights(l.lin.coeffs, bits_w);
+      ++li;
+    } else if (l.type == "maxpool") {
+      l.window = jl.value("window", 2);
+    }
+    layers.push_back(std::move(l));
+  }
+  const int64_t D = in_shape.size() == 3 ? int64_t{in_shape[0]} * in_shape[1] * in_shape[2] : in_shape[0];
+  // a value is either an image (Tensor3) or a flat vector
+  struct V {
+    bool img = false;
+    Tensor3 t;
+    std::vector<double> v;
+  };
+  auto run_sample = [&](const double* x, double* y) {
+    std::vector<std::pair<std::string, V>> named;
+    V cur;
+    if (in_shape.size() == 3) {
+      cur.img = true;
+      cur.t = Tensor3(in_shape[0], in_shape[1], in_shape[2]);
+      std::copy(x, x + D, cur.t.data.begin());
+    } else {
+      cur.v.assign(x, x + D);
+    }
+    named.push_back({"input", cur});
+    auto get = [&](const std::string& n) -> const V& {
+      for (auto& kv : named)
+        if (kv.first == n) return kv.second;
+      throw std::invalid_argument("unknown tensor " + n);
+    };
+    for (const auto& l : layers) {
+      V src = l.from.empty() ? cur : get(l.from);
+      V o;
+      if (l.type == "conv") {
+        const ConvKanLayer& c = l.conv;
+        Tensor3 t = src.t;
+        const int ho = (t.height + 2 * c.padding - c.kernel) / c.stride + 1;
+        const int wo = (t.width + 2 * c.padding - c.kernel) / c.stride + 1;
+        int eh = t.height, ew = t.width;
+        while ((eh + 2 * c.padding - c.kernel) % c.stride) ++eh;
+        while ((ew + 2 * c.padding - c.kernel) % c.stride) ++ew;
+        if (eh != t.height || ew != t.width) {
+          Tensor3 ext(t.channels, eh, ew);
+          for (int ch = 0; ch < t.channels; ++ch)
+            for (int yy = 0; yy < t.height; ++yy)
+              for (int xx = 0; xx < t.width; ++xx) ext.at(ch, yy, xx) = t.at(ch, yy, xx);
+          t = std::move(ext);
+        }
+        Tensor3 r = convkan_forward(t, c, basis);
+        o.img = true;
+        o.t = Tensor3(r.channels, ho, wo);
+        for (int ch = 0; ch < r.channels; ++ch)
+          for (int yy = 0; yy < ho; ++yy)
+            for (int xx = 0; xx < wo; ++xx) o.t.at(ch, yy, xx) = r.at(ch, yy, xx);
+      } else if (l.type == "linear") {
+        const std::vector<double>& in = src.img ? src.t.data : src.v;
+        const Matrix r = kan_linear_forward(make_matrix(1, static_cast<int64_t>(in.size()), in.data()),
+                                            l.lin, basis);
+        o.v.assign(r.flat().begin(), r.flat().end());
+      } else if (l.type == "maxpool") {
+        o.img = true;
+        o.t = maxpool2(src.t, l.window);
+      } else if (l.type == "flatten") {
+        o.v = flatten(src.t);
+      } else if (l.type == "global_avgpool") {
+        const int hw = src.t.height * src.t.width;
+        o.v.assign(static_cast<std::size_t>(src.t.channels), 0.0);
+        for (int ch = 0; ch < src.t.channels; ++ch) {
+          double acc = 0.0;
+          for (int q = 0; q < hw; ++q) acc += src.t.data[static_cast<std::size_t>(ch) * hw + q];
+          o.v[static_cast<std::size_t>(ch)] = acc / hw;
+        }
+      } else {
+        throw std::invalid_argument("unknown layer type " + l.type);
+      }
+      if (!l.res.empty()) {
+        const V& r = get(l.res);
+        std::vector<double>& dst = o.img ? o.t.data : o.v;
+        const std::vector<double>& add = r.img ? r.t.data : r.v;
+        for (std::size_t q = 0; q < dst.size(); ++q) dst[q] += add[q];
+      }
+      if (!l.id.empty()) named.push_back({l.id, o});
+      cur = std::move(o);
+    }
+    const std::vector<double>& res = cur.img ? cur.t.data : cur.v;
+    std::copy(res.begin(), res.begin() + n_out, y);
+  };
+  if (threads < 1) threads = 1;
+  std::vector<std::thread> pool;
+  std::vector<std::string> errs(static_cast<std::size_t>(threads));
+  for (int t = 0; t < threads; ++t) {
+    pool.emplace_back([&, t] {
+      try {
+        for (int64_t s = t; s < M; s += threads) run_sample(inputs + s * D, out + s * n_out);
+      } catch (const std::exception& e) {
+        errs[static_cast<std::size_t>(t)] = e.what();
+      }
+    });
+  }
+  for (auto& th : pool) th.join();
+  for (auto& e : errs)
+    if (!e.empty()) {
+      g_err = e;
+      return -1;
+    }
+  return 0;
+} catch (const std::exception& e) {
+  return fail(e);
+}
+
 }  // extern "C"

@@ -1,14 +1,16 @@
 """The five BASELINE.json workloads, as descriptors + seeded synthetic data.
 
-Descriptors use the reference's JSON schema (io.hpp:357-386).  Data is
-synthetic with the shapes and distributions BASELINE.json states (MNIST /
-CIFAR are not available and are not used):
+Descriptors use the reference's JSON schema (io.hpp:357-386), extended
+additively for ResKAN18 (named tensors ``id`` / ``input_from`` / ``residual``
+and a ``global_avgpool`` layer).  Data is synthetic with the
+shapes and distributions BASELINE.json states (MNIST / CIFAR are not
+available and are not used):
   inputs  ~ U[-1, 1] fp32
   spline coefficients ~ N(0, std) (0.1 for C1/C2, 0.05 for C3-C5)
   base (SiLU) weights  ~ N(0, 1/sqrt(n_in))
 Algorithmic work follows SURVEY.md 8(d): ops/sample = 2 * sum N_out * N_in_eff
-* (G+P) (cost.hpp:71, the dense contraction count), bytes/sample = fp32 input +
-output + weights once per batch.
+* (G+P) (cost.hpp:71, the dense contraction count; conv N_in_eff = K^2 C_in
+per output pixel), bytes/sample = fp32 input + output + weights once per batch.
 """
 from __future__ import annotations
 
@@ -18,11 +20,74 @@ from typing import List, Optional
 import numpy as np
 
 
+def walk_shapes(desc: dict) -> List[dict]:
+    """Per-layer input/output shapes of a descriptor (Model::validate's walk,
+    layers.hpp:252-307, with the engine's named-tensor extension)."""
+    shp = list(desc["input"])
+    named = {"input": shp}
+    out = []
+    for i, l in enumerate(desc["layers"]):
+        s = named[l["input_from"]] if "input_from" in l else shp
+        t = l["type"]
+        if t == "linear":
+            o = [l["n_out"]]
+        elif t == "conv":
+            k, st, p = l["kernel"], l.get("stride", 1), l.get("padding", 0)
+            o = [l["c_out"], (s[1] + 2 * p - k) // st + 1, (s[2] + 2 * p - k) // st + 1]
+        elif t == "maxpool":
+            w = l.get("window", 2)
+            o = [s[0], s[1] // w, s[2] // w]
+        elif t == "global_avgpool":
+            o = [s[0]]
+        elif t == "flatten":
+            o = [int(np.prod(s))]
+        else:
+            raise ValueError(t)
+        out.append({"type": t, "in": s, "out": o, "layer": l})
+        shp = o
+        if "id" in l:
+            named[l["id"]] = o
+    return out
+
+
+def reskan18_layers(width=(64, 128, 256, 512), n_classes=10, in_ch=3) -> list:
+    """ResNet-18 topology with every conv a KAN conv: 3x3 stem, 4 stages of 2
+    basic blocks, 1x1 stride-2 projection shortcuts, global average pool,
+    linear classifier.  Same 20 conv + 1 linear layers, in the same order, as the
+    reference's descriptors/reskan18.json, with the residual structure and the
+    pooling stated explicitly."""
+    L = []
+
+    def conv(ci, co, k=3, s=1, p=1, **kw):
+        d = {"type": "conv", "c_in": ci, "c_out": co, "kernel": k, "stride": s, "padding": p}
+        d.update(kw)
+        L.append(d)
+
+    conv(in_ch, width[0], id="b0")
+    prev, c = "b0", width[0]
+    bi = 1
+    for si, w in enumerate(width):
+        for blk in range(2):
+            down = si > 0 and blk == 0
+            if down:
+                conv(c, w, k=1, s=2, p=0, input_from=prev, id=f"sc{bi}")
+                conv(c, w, s=2, input_from=prev)
+                conv(w, w, residual=f"sc{bi}", id=f"b{bi}")
+            else:
+                conv(c, w, input_from=prev)
+                conv(w, w, residual=prev, id=f"b{bi}")
+            prev, c = f"b{bi}", w
+            bi += 1
+    L.append({"type": "global_avgpool"})
+    L.append({"type": "linear", "n_in": width[-1], "n_out": n_classes})
+    return L
+
+
 @dataclass
 class Workload:
     key: str
     title: str
-    dims: List[int]
+    dims: List[int]  # MLP widths, or [input size] for descriptor-defined models
     G: int
     P: int
     batch: int
@@ -34,34 +99,66 @@ class Workload:
     silu: bool = True
     int8_out: bool = False
     seed: int = 0
+    input_shape: Optional[List[int]] = None
+    layers: Optional[list] = None
     extra: dict = field(default_factory=dict)
 
     def descriptor(self) -> dict:
+        if self.layers is not None:
+            d = {"name": self.key, "grid": {"intervals": self.G, "degree": self.P},
+                 "input": list(self.input_shape), "layers": self.layers}
+            d.update(self.extra.get("descriptor", {}))
+            return d
         return {"name": self.key, "grid": {"intervals": self.G, "degree": self.P},
                 "input": [self.dims[0]],
                 "layers": [{"type": "linear", "n_in": a, "n_out": b}
                            for a, b in zip(self.dims, self.dims[1:])]}
 
+    def kan_layers(self) -> List[dict]:
+        """KAN layers in order: reference inputs (conv: K^2 C_in), outputs, output
+        pixels per sample, and input / output elements per sample."""
+        res = []
+        for s in walk_shapes(self.descriptor()):
+            l = s["layer"]
+            if s["type"] == "linear":
+                res.append({"n_in": l["n_in"], "n_out": l["n_out"], "pix": 1,
+                            "in_elems": int(np.prod(s["in"])), "out_elems": l["n_out"]})
+            elif s["type"] == "conv":
+                pix = s["out"][1] * s["out"][2]
+                res.append({"n_in": l["kernel"] ** 2 * l["c_in"], "n_out": l["c_out"], "pix": pix,
+                            "in_elems": int(np.prod(s["in"])), "out_elems": int(np.prod(s["out"]))})
+        return res
+
+    @property
+    def n_kan(self) -> int:
+        return len(self.kan_layers())
+
+    @property
+    def input_size(self) -> int:
+        return int(np.prod(self.input_shape)) if self.input_shape else self.dims[0]
+
     def weights(self):
         rng = np.random.default_rng(self.seed)
         nb = self.G + self.P
         Ws, Bs = [], []
-        for a, b in zip(self.dims, self.dims[1:]):
+        for kl in self.kan_layers():
+            a, b = kl["n_in"], kl["n_out"]
             Ws.append(rng.normal(0.0, self.std, (a * nb, b)))
             Bs.append(rng.normal(0.0, 1.0 / np.sqrt(a), (a, b)) if self.silu else None)
         return Ws, Bs
 
     def inputs(self, rows: int, seed: int = 1) -> np.ndarray:
         rng = np.random.default_rng(self.seed * 1000 + seed)
-        return rng.uniform(-1.0, 1.0, (rows, self.dims[0])).astype(np.float32)
+        return rng.uniform(-1.0, 1.0, (rows, self.input_size)).astype(np.float32)
 
     # -- algorithmic work (SURVEY.md 8(d)) --------------------------------------------
     def ops_per_sample(self) -> int:
         nb = self.G + self.P
-        return int(sum(2 * b * a * nb for a, b in zip(self.dims, self.dims[1:])))
+        return int(sum(2 * kl["pix"] * kl["n_in"] * nb * kl["n_out"] for kl in self.kan_layers()))
 
     def weight_bytes(self, layer: int) -> int:
-        a, b = self.dims[layer], self.dims[layer + 1]
+        kl = self.kan_layers()[layer]
+        a, b = kl["n_in"], kl["n_out"]
         nb = self.G + self.P
         esz = 2 if self.mode == "bf16" else (4 if self.mode == "fp32" else 1)
         return a * nb * b * esz + (a * b * esz if self.silu else 0)
@@ -71,15 +168,16 @@ class Workload:
         weights once.  Inputs are fp32 for layer 0; hidden activations are u16
         lattice levels on the LUT path and fp32 on the float paths."""
         lut = self.mode == "bspline-lut"
-        a, b = self.dims[layer], self.dims[layer + 1]
+        kls = self.kan_layers()
+        kl = kls[layer]
         in_b = 4 if layer == 0 else (2 if lut else 4)
-        last = layer == len(self.dims) - 2
+        last = layer == len(kls) - 1
         out_b = (1 if self.int8_out else 4) if last else (2 if lut else 4)
-        return batch * (a * in_b + b * out_b) + self.weight_bytes(layer)
+        return batch * (kl["in_elems"] * in_b + kl["out_elems"] * out_b) + self.weight_bytes(layer)
 
     def layer_ops_per_launch(self, layer: int, batch: int) -> int:
-        a, b = self.dims[layer], self.dims[layer + 1]
-        return 2 * batch * a * (self.G + self.P) * b
+        kl = self.kan_layers()[layer]
+        return 2 * batch * kl["pix"] * kl["n_in"] * (self.G + self.P) * kl["n_out"]
 
 
 WORKLOADS = {
@@ -95,6 +193,17 @@ WORKLOADS = {
                    [3072, 1024, 1024, 10], 10, 3, 65536, 0.05),
     "c3bf16": Workload("c3bf16", "Wide KAN MLP [3072,1024,1024,10] G=10 batch 65536, bf16 path",
                        [3072, 1024, 1024, 10], 10, 3, 65536, 0.05, mode="bf16"),
+    # configs[3]
+    "c4": Workload("c4", "KAN conv 3x3 s1 p1 64->64 on 32x32, G=5 P=3 batch 256, LUT k8/h8 + int8 W "
+                         "(implicit im2col)",
+                   [64 * 32 * 32], 5, 3, 256, 0.05, input_shape=[64, 32, 32],
+                   layers=[{"type": "conv", "c_in": 64, "c_out": 64, "kernel": 3, "stride": 1,
+                            "padding": 1}]),
+    # configs[4]
+    "c5": Workload("c5", "ResKAN18 (ResNet-18 topology, KAN convs) on 3x32x32, G=5 P=3 batch 8192, "
+                         "LUT k8/h3 (3-bit table) + int8 W",
+                   [3 * 32 * 32], 5, 3, 8192, 0.05, lut_h=3, input_shape=[3, 32, 32],
+                   layers=reskan18_layers(), extra={"descriptor": {"conv_output": "floor"}}),
 }
 
 

@@ -40,6 +40,13 @@ cudaError_t launch_levels(const float* x, int64_t n, const float* thr, float lo,
 cudaError_t launch_argmax(const float* logits, int64_t M, int N, int ld, int32_t* out,
                           cudaStream_t st);
 cudaError_t launch_fp32_layer(const Fp32Params& p, cudaStream_t st);
+cudaError_t launch_nchw_to_nhwc(bool levels, const float* in, int64_t n_img, int C, int HW,
+                                void* out, int ldc, const float* thr, float lo, float inv_step,
+                                int L, cudaStream_t st);
+cudaError_t launch_maxpool(bool levels, const void* in, int64_t n_img, int H, int W, int C,
+                           int ld_in, int win, void* out, int ld_out, cudaStream_t st);
+cudaError_t launch_avgpool(const void* in, int64_t n_img, int HW, int C, int ld_in, void* out,
+                           int ld_out, cudaStream_t st);
 
 struct CudaError : std::runtime_error {
   using std::runtime_error::runtime_error;
@@ -85,13 +92,34 @@ struct DevBuf {
   }
 };
 
-enum LayerType { L_LINEAR, L_CONV, L_MAXPOOL, L_FLATTEN };
+enum LayerType { L_LINEAR, L_CONV, L_MAXPOOL, L_FLATTEN, L_AVGPOOL };
+
+// Per-sample tensor shape (Model::validate's bookkeeping, layers.hpp:252-307).
+// `hw`/`fc` record, for a flat tensor made by flattening an image tensor that
+// a layer produced (stored NHWC), its H*W and C: the consuming linear layer
+// permutes its coefficient rows from the reference's channel-major order.
+struct Shape {
+  bool flat = true;
+  int c = 0, h = 0, w = 0, d = 0;
+  int hw = 0, fc = 0;
+  bool operator==(const Shape& o) const {
+    return flat == o.flat && (flat ? d == o.d : (c == o.c && h == o.h && w == o.w));
+  }
+};
 
 struct Layer {
   LayerType type = L_LINEAR;
   int n_in = 0, n_out = 0;  // linear: features; conv: patch size / c_out
   int c_in = 0, c_out = 0, kernel = 0, stride = 1, padding = 0, window = 2;
   int kan_index = -1;
+  // engine descriptor extension (additive): named tensors for residual blocks
+  std::string id, input_from, residual;
+  int src = -1;      // layer whose output feeds this layer (-1: model input)
+  int res_src = -2;  // layer whose output is added before re-quantization (-2: none)
+  Shape in, out;
+  // LUT path storage of this layer's output: fp32 values when some consumer
+  // needs values (a residual add, average pooling), else exact lattice levels
+  bool store_f32 = false;
   std::vector<double> coeffs;  // reference layout [n_in*nb, n_out]
   std::vector<double> base_w;  // [n_in, n_out]
 };
@@ -100,6 +128,7 @@ struct Layer {
 struct PreparedLayer {
   int layer_index = 0;
   int n_in = 0, N = 0, BN = 0, n_tiles_n = 0, nbp = 8;
+  int cps = 0;  // conv: IPS-wide channel chunks per tap
   int IPS = 0, GS = 0, n_spline_stages = 0, n_groups = 0, total_stages = 0, silu = 0;
   DevBuf<uint8_t> wt;       // tcgen05 paths: pre-tiled weights
   DevBuf<float> w32, wb32;  // fp32 path
@@ -169,6 +198,8 @@ struct kan_engine {
   Grid grid;
   std::vector<int> input_shape;
   std::vector<Layer> layers;
+  bool conv_floor = false;  // descriptor "conv_output": "floor"
+  bool input_f32 = false;   // the NHWC copy of the model input keeps fp32 values
   int n_kan = 0;
   std::string err;
   // configuration
@@ -182,9 +213,13 @@ struct kan_engine {
   int tab_bytes = 0, off_thr = 0, off_silu = 0;
   double s_s = 1.0;
   int64_t z_s = 0;
-  // workspaces
-  DevBuf<uint8_t> act[2];
+  // workspaces: activation buffer slot of each layer's stored output (-1:
+  // none -- views, the last layer, or the model input); slots are reused
+  // once every consumer of their tensor has run
+  std::vector<int> slot_of;
+  std::vector<DevBuf<uint8_t>> slots;
   DevBuf<float> xstage;
+  DevBuf<uint8_t> xnhwc;  // NHWC copy of an image model's input
   DevBuf<float> logits_tmp;
   DevBuf<uint8_t> io_in, io_out;
   int last_launches = 0;
@@ -230,10 +265,11 @@ struct kan_engine {
     for (int d : input_shape) n *= d;
     return n;
   }
+  // values per sample of the model output (the last layer's tensor, flattened)
   int output_count() const {
-    for (auto it = layers.rbegin(); it != layers.rend(); ++it)
-      if (it->type == L_LINEAR || it->type == L_CONV) return it->type == L_LINEAR ? it->n_out : it->c_out;
-    throw InvalidArgument("Model::output_count: model has no KAN layers");
+    if (layers.empty()) throw InvalidArgument("Model::output_count: model has no layers");
+    const Shape& o = layers.back().out;
+    return o.flat ? o.d : o.c * o.h * o.w;
   }
   Layer& kan_layer(int i) {
     for (auto& l : layers)
@@ -286,49 +322,97 @@ kan_status guarded(kan_engine* e, F&& f) {
   }
 }
 
-// Model::validate (layers.hpp:252-307)
+// Model::validate (layers.hpp:252-307), extended additively with named
+// tensors (id / input_from / residual) and global average pooling.
 void validate(kan_engine* e) {
-  bool flat = e->input_shape.size() == 1;
-  int c = 0, h = 0, w = 0, d = 0;
-  if (flat) {
-    d = e->input_shape[0];
+  Shape cur;
+  if (e->input_shape.size() == 1) {
+    cur.d = e->input_shape[0];
   } else if (e->input_shape.size() == 3) {
-    c = e->input_shape[0];
-    h = e->input_shape[1];
-    w = e->input_shape[2];
+    cur.flat = false;
+    cur.c = e->input_shape[0];
+    cur.h = e->input_shape[1];
+    cur.w = e->input_shape[2];
   } else {
     throw ShapeMismatch("Model::validate: input_shape must be [D] or [C,H,W]");
   }
-  int idx = 0;
+  struct Named {
+    int layer;
+    Shape shape;
+  };
+  std::vector<std::pair<std::string, Named>> named{{"input", {-1, cur}}};
+  auto find = [&](const std::string& n, const std::string& si) -> const Named& {
+    for (auto& kv : named)
+      if (kv.first == n) return kv.second;
+    throw FormatError("model_from_descriptor: layer " + si + " refers to unknown tensor '" + n + "'");
+  };
+  int idx = 0, prev = -1;
   for (auto& l : e->layers) {
     const std::string si = std::to_string(idx);
+    Shape s = cur;
+    l.src = prev;
+    if (!l.input_from.empty()) {
+      const Named& nm = find(l.input_from, si);
+      s = nm.shape;
+      l.src = nm.layer;
+    }
+    l.in = s;
+    Shape o;
     if (l.type == L_LINEAR) {
-      if (!flat) throw ShapeMismatch("Model::validate: linear layer " + si + " applied to unflattened tensor");
-      if (d != l.n_in)
+      if (!s.flat) throw ShapeMismatch("Model::validate: linear layer " + si + " applied to unflattened tensor");
+      if (s.d != l.n_in)
         throw ShapeMismatch("Model::validate: layer " + si + " expects " + std::to_string(l.n_in) +
-                            " inputs, got " + std::to_string(d));
-      d = l.n_out;
+                            " inputs, got " + std::to_string(s.d));
+      o.d = l.n_out;
     } else if (l.type == L_CONV) {
-      if (flat) throw ShapeMismatch("Model::validate: conv layer " + si + " applied to flat input");
-      if (c != l.c_in)
+      if (s.flat) throw ShapeMismatch("Model::validate: conv layer " + si + " applied to flat input");
+      if (s.c != l.c_in)
         throw ShapeMismatch("Model::validate: layer " + si + " expects " + std::to_string(l.c_in) +
-                            " channels, got " + std::to_string(c));
-      const int sh = h + 2 * l.padding - l.kernel, sw = w + 2 * l.padding - l.kernel;
-      if (sh < 0 || sw < 0 || sh % l.stride || sw % l.stride)
+                            " channels, got " + std::to_string(s.c));
+      const int sh = s.h + 2 * l.padding - l.kernel, sw = s.w + 2 * l.padding - l.kernel;
+      // the reference requires the stride to divide the padded span
+      // (layers.hpp:131-132); "conv_output": "floor" opts into floor
+      // semantics (= the reference on the bottom/right zero-extended input)
+      if (sh < 0 || sw < 0 || (!e->conv_floor && (sh % l.stride || sw % l.stride)))
         throw ShapeMismatch("Model::validate: layer " + si +
                             " output dimensions are not positive integers for " +
-                            std::to_string(h) + "x" + std::to_string(w) + " input");
-      c = l.c_out;
-      h = sh / l.stride + 1;
-      w = sw / l.stride + 1;
+                            std::to_string(s.h) + "x" + std::to_string(s.w) + " input");
+      o.flat = false;
+      o.c = l.c_out;
+      o.h = sh / l.stride + 1;
+      o.w = sw / l.stride + 1;
     } else if (l.type == L_MAXPOOL) {
-      if (flat) throw ShapeMismatch("Model::validate: pool layer on flat input");
-      h /= l.window;
-      w /= l.window;
+      if (s.flat) throw ShapeMismatch("Model::validate: pool layer on flat input");
+      o = s;
+      o.h = s.h / l.window;
+      o.w = s.w / l.window;
+    } else if (l.type == L_AVGPOOL) {
+      if (s.flat) throw ShapeMismatch("Model::validate: pool layer on flat input");
+      o.d = s.c;
     } else {
-      if (flat) throw ShapeMismatch("Model::validate: flatten on flat input");
-      d = c * h * w;
-      flat = true;
+      if (s.flat) throw ShapeMismatch("Model::validate: flatten on flat input");
+      o.d = s.c * s.h * s.w;
+      if (l.src >= 0) {  // a layer's output is stored NHWC
+        o.hw = s.h * s.w;
+        o.fc = s.c;
+      }
+    }
+    if (!l.residual.empty()) {
+      if (l.type != L_LINEAR && l.type != L_CONV)
+        throw FormatError("model_from_descriptor: layer " + si + ": residual needs a KAN layer");
+      const Named& nm = find(l.residual, si);
+      if (!(nm.shape == o))
+        throw ShapeMismatch("Model::validate: layer " + si + " residual '" + l.residual +
+                            "' has a different shape");
+      l.res_src = nm.layer;
+    }
+    l.out = o;
+    cur = o;
+    prev = idx;
+    if (!l.id.empty()) {
+      for (auto& kv : named)
+        if (kv.first == l.id) throw FormatError("model_from_descriptor: duplicate tensor id '" + l.id + "'");
+      named.push_back({l.id, {idx, o}});
     }
     ++idx;
   }
@@ -433,6 +517,44 @@ static inline size_t tile_off(int BN, int n, int kb) {
   return static_cast<size_t>(kb >> 7) * BN * 128 + sw128_off_host(n, (kb & 127) >> 4) + (kb & 15);
 }
 
+// round a row pitch (elements) so the byte pitch is a multiple of 16 (TMA)
+int64_t pitch16(int64_t n, int esz) {
+  const int64_t q = 16 / esz;
+  return (n + q - 1) / q * q;
+}
+
+// bytes per element of the activations a layer stores for the next one:
+// u16 lattice levels on the LUT path, fp32 on the float paths
+int act_esz(const kan_engine* e) { return e->cfg.mode == KAN_MODE_BSPLINE_LUT ? 2 : 4; }
+
+// GEMM input order -> reference coefficient row (or -1 for padding).
+//   conv: tap-major, then channel (im2col is channel-major, layers.hpp:140-149),
+//         channels padded to whole IPS chunks per tap;
+//   linear after flattening a stored NHWC tensor: pixel-major, then channel
+//         (flatten is channel-major, layers.hpp:210), channels at the stored pitch;
+//   otherwise the identity.
+std::vector<int> input_perm(const kan_engine* e, const Layer& l, int ips, int& cps) {
+  std::vector<int> perm;
+  cps = 0;
+  if (l.type == L_CONV) {
+    const int KK = l.kernel * l.kernel;
+    cps = (l.c_in + ips - 1) / ips;
+    const int cin_pad = cps * ips;
+    perm.assign(static_cast<size_t>(KK) * cin_pad, -1);
+    for (int t = 0; t < KK; ++t)
+      for (int c = 0; c < l.c_in; ++c) perm[static_cast<size_t>(t) * cin_pad + c] = c * KK + t;
+  } else if (l.in.hw > 0) {
+    const int ldc = static_cast<int>(pitch16(l.in.fc, act_esz(e)));
+    perm.assign(static_cast<size_t>(l.in.hw) * ldc, -1);
+    for (int q = 0; q < l.in.hw; ++q)
+      for (int c = 0; c < l.in.fc; ++c) perm[static_cast<size_t>(q) * ldc + c] = c * l.in.hw + q;
+  } else {
+    perm.resize(static_cast<size_t>(l.n_in));
+    for (int i = 0; i < l.n_in; ++i) perm[static_cast<size_t>(i)] = i;
+  }
+  return perm;
+}
+
 void prepare_gemm_layer(kan_engine* e, const Layer& l, PreparedLayer& pl, bool bf16) {
   const kan_config& cfg = e->cfg;
   const Grid& g = e->grid;
@@ -440,18 +562,24 @@ void prepare_gemm_layer(kan_engine* e, const Layer& l, PreparedLayer& pl, bool b
   const int nbp = nb <= 8 ? 8 : 16;
   if (nb > 16) throw Unsupported("G + P > 16 is not supported by the tcgen05 path");
   if (g.P > 3) throw Unsupported("degree > 3 is not supported by the tcgen05 path");
-  const int n_in = l.type == L_LINEAR ? l.n_in : l.kernel * l.kernel * l.c_in;
+  const int n_ref = l.n_in;  // reference inputs (conv: kernel^2 * c_in)
   const int N = l.type == L_LINEAR ? l.n_out : l.c_out;
+  pl.IPS = gemm_ips(bf16, nbp);
+  pl.GS = gemm_gs(bf16, nbp);
+  const std::vector<int> perm = input_perm(e, l, pl.IPS, pl.cps);
+  const int n_in = static_cast<int>(perm.size());  // GEMM inputs
+  bool holes = false;
+  for (int v : perm) holes = holes || v < 0;
   pl.n_in = n_in;
   pl.N = N;
   pl.nbp = nbp;
   pl.BN = N > 256 ? 256 : std::max(16, (N + 15) / 16 * 16);
   pl.n_tiles_n = (N + pl.BN - 1) / pl.BN;
-  pl.IPS = gemm_ips(bf16, nbp);
-  pl.GS = gemm_gs(bf16, nbp);
   pl.silu = cfg.silu_base ? 1 : 0;
-  if (pl.silu && l.base_w.size() != static_cast<size_t>(n_in) * N)
+  if (pl.silu && l.base_w.size() != static_cast<size_t>(n_ref) * N)
     throw InvalidArgument("silu_base requires base weights [n_in, n_out] for every KAN layer");
+  if (!bf16 && cfg.w_scheme == KAN_W_PER_TENSOR_ASYM && holes && l.type != L_CONV)
+    throw Unsupported("per-tensor weights after a padded flatten are not supported");
   pl.n_spline_stages = (n_in + pl.IPS - 1) / pl.IPS;
   pl.n_groups = (pl.n_spline_stages + pl.GS - 1) / pl.GS;
   const int last = pl.n_spline_stages - (pl.n_groups - 1) * pl.GS;
@@ -478,10 +606,10 @@ void prepare_gemm_layer(kan_engine* e, const Layer& l, PreparedLayer& pl, bool b
         // base weights expressed in spline-code units (ratio = s_s / s_b), so
         // both parts share a single int32 accumulator
         const double ratio = e->s_s / quant_params(0.0, 1.0, cfg.lut_h).scale;
-        quant_joint(l.coeffs, l.base_w, static_cast<int64_t>(n_in) * nb, n_in, N, cfg.bits_w,
+        quant_joint(l.coeffs, l.base_w, static_cast<int64_t>(n_ref) * nb, n_ref, N, cfg.bits_w,
                     ratio, qw_s8, qwb, s_w);
       } else {
-        quant_per_channel(l.coeffs, static_cast<int64_t>(n_in) * nb, N, cfg.bits_w, qw_s8, s_w);
+        quant_per_channel(l.coeffs, static_cast<int64_t>(n_ref) * nb, N, cfg.bits_w, qw_s8, s_w);
       }
       pl.b_signed = 1;
     } else {
@@ -503,8 +631,10 @@ void prepare_gemm_layer(kan_engine* e, const Layer& l, PreparedLayer& pl, bool b
             for (int ii = 0; ii < pl.IPS; ++ii) {
               const int i = i0 + ii;
               if (i >= n_in) break;
+              const int ir = perm[static_cast<size_t>(i)];
+              if (ir < 0) continue;
               for (int b = 0; b < nb; ++b) {
-                const size_t src = (static_cast<size_t>(i) * nb + b) * N + j;
+                const size_t src = (static_cast<size_t>(ir) * nb + b) * N + j;
                 const int elem = ii * nbp + b;
                 const int kb = elem * esz;
                 uint8_t* dst = tile + tile_off(BN, n, kb);
@@ -522,10 +652,12 @@ void prepare_gemm_layer(kan_engine* e, const Layer& l, PreparedLayer& pl, bool b
             for (int gi = 0; gi < GI; ++gi) {
               const int i = grp * GI + gi;
               if (i >= n_in) break;
+              const int ir = perm[static_cast<size_t>(i)];
+              if (ir < 0) continue;
               const int elem = silu_pos(bf16, nbp, gi);
               const int kb = elem * esz;
               uint8_t* dst = tile + tile_off(BN, n, kb);
-              const size_t src = static_cast<size_t>(i) * N + j;
+              const size_t src = static_cast<size_t>(ir) * N + j;
               if (bf16) {
                 const __nv_bfloat16 bv = __float2bfloat16_rn(static_cast<float>(l.base_w[src]));
                 std::memcpy(dst, &bv, 2);
@@ -553,7 +685,7 @@ void prepare_gemm_layer(kan_engine* e, const Layer& l, PreparedLayer& pl, bool b
         fs[static_cast<size_t>(j)] = s_b * s_w[static_cast<size_t>(j)];
         if (pl.silu) {
           long long cs = 0;
-          for (int i = 0; i < n_in; ++i) cs += qwb[static_cast<size_t>(i) * N + j];
+          for (int i = 0; i < n_ref; ++i) cs += qwb[static_cast<size_t>(i) * N + j];
           corr[static_cast<size_t>(j)] = e->z_s * cs;
         }
       }
@@ -595,6 +727,63 @@ void prepare_fp32_layer(kan_engine* e, const Layer& l, PreparedLayer& pl) {
   }
 }
 
+// Static activation-buffer plan: a flatten is a view of its source; a stored
+// tensor lives until its last consumer (next layer, input_from or residual).
+void plan_buffers(kan_engine* e) {
+  const int n = static_cast<int>(e->layers.size());
+  std::vector<int> owner(static_cast<size_t>(n), -1), last_use(static_cast<size_t>(n), -1);
+  for (int i = 0; i < n; ++i) {
+    const Layer& l = e->layers[static_cast<size_t>(i)];
+    owner[static_cast<size_t>(i)] = l.type == L_FLATTEN ? (l.src >= 0 ? owner[static_cast<size_t>(l.src)] : -1) : i;
+  }
+  for (int i = 0; i < n; ++i) {
+    const Layer& l = e->layers[static_cast<size_t>(i)];
+    for (int r : {l.src, l.res_src})
+      if (r >= 0 && owner[static_cast<size_t>(r)] >= 0)
+        last_use[static_cast<size_t>(owner[static_cast<size_t>(r)])] =
+            std::max(last_use[static_cast<size_t>(owner[static_cast<size_t>(r)])], i);
+  }
+  e->slot_of.assign(static_cast<size_t>(n), -1);
+  std::vector<int> free_slots;
+  int n_slots = 0;
+  for (int i = 0; i < n; ++i) {
+    const Layer& l = e->layers[static_cast<size_t>(i)];
+    if (l.type != L_FLATTEN && i + 1 < n) {
+      int sl;
+      if (!free_slots.empty()) {
+        sl = free_slots.back();
+        free_slots.pop_back();
+      } else {
+        sl = n_slots++;
+      }
+      e->slot_of[static_cast<size_t>(i)] = sl;
+    }
+    for (int j = 0; j <= i; ++j)
+      if (last_use[static_cast<size_t>(j)] == i && e->slot_of[static_cast<size_t>(j)] >= 0)
+        free_slots.push_back(e->slot_of[static_cast<size_t>(j)]);
+  }
+  e->slots.clear();
+  e->slots.resize(static_cast<size_t>(n_slots));
+  // storage kinds: walk backwards so a view / maxpool passes the need for
+  // values on to the tensor it reads
+  std::vector<bool> need(static_cast<size_t>(n), false);
+  bool need_in = false;
+  auto mark = [&](int t) {
+    if (t >= 0)
+      need[static_cast<size_t>(t)] = true;
+    else if (t == -1)
+      need_in = true;
+  };
+  for (int i = n - 1; i >= 0; --i) {
+    const Layer& l = e->layers[static_cast<size_t>(i)];
+    if (l.res_src != -2) mark(l.res_src);
+    if (l.type == L_AVGPOOL) mark(l.src);
+    if ((l.type == L_MAXPOOL || l.type == L_FLATTEN) && need[static_cast<size_t>(i)]) mark(l.src);
+  }
+  for (int i = 0; i < n; ++i) e->layers[static_cast<size_t>(i)].store_f32 = need[static_cast<size_t>(i)];
+  e->input_f32 = need_in;
+}
+
 void configure(kan_engine* e, const kan_config* c) {
   if (!c) throw InvalidArgument("configure: null config");
   DeviceGuard dg(e->device);
@@ -603,8 +792,18 @@ void configure(kan_engine* e, const kan_config* c) {
     throw InvalidArgument("unknown evaluation mode");
   e->cfg = cfg;
   e->configured = false;
-  for (auto& l : e->layers)
-    if (l.type == L_CONV) throw Unsupported("conv layers: implicit-im2col path not built yet");
+  const Layer& lastl = e->layers.back();
+  if (lastl.type != L_LINEAR && lastl.type != L_CONV)
+    throw Unsupported("the last layer must be a KAN layer");
+  if (cfg.mode == KAN_MODE_FP32) {
+    for (auto& l : e->layers)
+      if (l.type != L_LINEAR || l.src != static_cast<int>(&l - e->layers.data()) - 1 || l.res_src != -2)
+        throw Unsupported("fp32 mode runs dense layer stacks; conv, pooling and residual layers run "
+                          "on the bf16 and bspline-lut paths");
+  }
+  if (lastl.type == L_CONV && cfg.out_kind == KAN_OUT_I8)
+    throw InvalidArgument("int8 outputs are produced by linear output layers only");
+  plan_buffers(e);
   const Grid& g = e->grid;
   if (cfg.mode == KAN_MODE_BSPLINE_LUT) {
     e->lut = build_lut(g.P, cfg.lut_k, cfg.lut_h);  // validates P, k, h like the reference
@@ -696,12 +895,65 @@ void pick_stages(bool bf16, int nbp, int BN, int x_kind, int tab_bytes, int& SA,
 struct LayerIO {
   const void* x;
   int x_kind;
-  int64_t ld_x;
+  int64_t ld_x;  // dense: row pitch; conv: channel pitch of a stored NHWC tensor
   void* out;
   int epi;
   int64_t ld_out;
   void* out2;
+  // conv input geometry (per image)
+  const Layer* conv = nullptr;
+  int64_t n_img = 0;
+  // residual add and NCHW output
+  int res_kind = 0;
+  const void* res = nullptr;
+  int64_t ld_res = 0;
+  int out_hw = 0;
 };
+
+// 4D tensor map over stored NHWC conv activations: dims (C, W, H, N), box
+// (IPS, Wo*s, bh*s, bn) with element strides (1, s, s, 1), so one load is one
+// tap's window for the tile's output pixels.  Padded taps fall outside the
+// tensor (negative or past-the-end W/H coordinates; zero fill).
+static CUtensorMap make_conv_xmap(const LayerIO& io, const Layer& l, int ips, int bh, int bn) {
+  CUtensorMap m;
+  std::memset(&m, 0, sizeof m);
+  const int H = l.in.h, W = l.in.w, Cc = l.in.c, s = l.stride, Wo = l.out.w;
+  const bool f32 = io.x_kind == X_F32;
+  const size_t esz = f32 ? 4 : 2;
+  cuuint64_t dims[4];
+  cuuint64_t strides[3];
+  cuuint32_t box[4];
+  cuuint32_t estr[4] = {1u, 1u, 1u, 1u};
+  CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_NONE;
+  {
+    const uint64_t ldc = static_cast<uint64_t>(io.ld_x);
+    dims[0] = static_cast<cuuint64_t>(Cc);
+    dims[1] = static_cast<cuuint64_t>(W);
+    dims[2] = static_cast<cuuint64_t>(H);
+    dims[3] = static_cast<cuuint64_t>(io.n_img);
+    strides[0] = ldc * esz;
+    strides[1] = ldc * esz * W;
+    strides[2] = ldc * esz * W * H;
+    box[0] = static_cast<cuuint32_t>(ips);
+    box[1] = static_cast<cuuint32_t>(Wo * s);
+    box[2] = static_cast<cuuint32_t>(bh * s);
+    box[3] = static_cast<cuuint32_t>(bn);
+    estr[1] = estr[2] = static_cast<cuuint32_t>(s);
+    const size_t row_bytes = static_cast<size_t>(ips) * esz;
+    sw = row_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+         : row_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+         : row_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                           : CU_TENSOR_MAP_SWIZZLE_NONE;
+  }
+  for (int i = 0; i < 4; ++i)
+    if (box[i] > 256) throw Unsupported("conv tile exceeds the TMA box limits");
+  CUresult r = get_encode_fn()(
+      &m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_UINT16, 4,
+      const_cast<void*>(io.x), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (conv) failed (" + std::to_string(r) + ")");
+  return m;
+}
 
 void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& io, cudaStream_t st) {
   const bool bf16 = e->cfg.mode == KAN_MODE_BF16;
@@ -783,7 +1035,46 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
   p.n_L = static_cast<int>(e->lat.L);
   p.out_scale = e->cfg.out_scale;
   p.inv_out_scale = 1.0 / e->cfg.out_scale;
-  const CUtensorMap xmap = make_xmap(io.x, io.x_kind, M, pl.n_in, io.ld_x, pl.IPS);
+  p.n_ch = pl.n_in;
+  p.res_kind = io.res_kind;
+  p.res = io.res;
+  p.ld_res = static_cast<int>(io.ld_res);
+  p.out_hw = io.out_hw;
+  CUtensorMap xmap;
+  if (io.conv) {
+    // M tile = bn images x bh output rows x Wo columns (rows contiguous in M)
+    const Layer& l = *io.conv;
+    const int Ho = l.out.h, Wo = l.out.w;
+    if (Wo > 128 || 128 % Wo != 0) throw Unsupported("conv output width must divide 128");
+    int bh, bn;
+    if (Ho * Wo >= 128) {
+      bh = 128 / Wo;
+      bn = 1;
+      if (Ho % bh != 0) throw Unsupported("conv output rows must tile by 128 / width");
+    } else {
+      if (128 % (Ho * Wo) != 0) throw Unsupported("conv output map must divide 128 pixels");
+      bh = Ho;
+      bn = 128 / (Ho * Wo);
+    }
+    p.conv = 1;
+    p.ksz = l.kernel;
+    p.cstride = l.stride;
+    p.pad = l.padding;
+    p.cps = pl.cps;
+    p.H = l.in.h;
+    p.W = l.in.w;
+    p.Ho = Ho;
+    p.Wo = Wo;
+    p.bh = bh;
+    p.bn_img = bn;
+    p.tpi = Ho / bh;
+    p.pimg = bh * Wo;
+    p.lvl0 = bf16 ? 0 : static_cast<int>(e->lat.quantize(0.0));
+    p.n_ch = l.c_in;
+    xmap = make_conv_xmap(io, l, pl.IPS, bh, bn);
+  } else {
+    xmap = make_xmap(io.x, io.x_kind, M, pl.n_in, io.ld_x, pl.IPS);
+  }
   const size_t smem = gemm_smem_bytes(bf16, pl.nbp, pl.BN, SA, SB, SX, io.x_kind, tb);
   // kernel variant: 0 plain, 1 per-tensor zero point (reference scheme), 2 SiLU base
   const int mode = pl.silu ? 2 : ((!bf16 && pl.wscheme == KAN_W_PER_TENSOR_ASYM) ? 1 : 0);
@@ -814,62 +1105,147 @@ void run_fp32_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const float* x,
   e->last_launches += 1;
 }
 
-// round a row pitch (elements) so the byte pitch is a multiple of 16 (TMA)
-int64_t pitch16(int64_t n, int esz) {
-  const int64_t q = 16 / esz;
-  return (n + q - 1) / q * q;
-}
+// A stored activation tensor.  Dense: [M, ld] rows.  Image: NHWC with channel
+// pitch ld, except the model input, which is the caller's NCHW fp32 rows.
+struct Act {
+  const void* p = nullptr;
+  int kind = X_F32;
+  bool nchw = false;
+  int64_t ld = 0;
+};
 
+// model_forward (eval.hpp:200-253): run the layer graph on the caller's stream.
+// KAN layers are one fused gather-GEMM launch each; pooling layers are small
+// elementwise kernels; flatten is a view (the consuming linear layer's
+// coefficient rows were permuted at configure time).
 void forward(kan_engine* e, const float* x, int64_t M, void* out, cudaStream_t st) {
   if (!e->configured) throw LogicError("forward: engine not configured");
   if (M < 0) throw InvalidArgument("forward: negative batch");
   DeviceGuard dg(e->device);
   e->last_launches = 0;
   if (M == 0) return;
-  if (e->input_shape.size() != 1) throw Unsupported("image models: conv path not built yet");
-  const int64_t D = e->input_size();
   const bool lut = e->cfg.mode == KAN_MODE_BSPLINE_LUT;
   const bool fp32 = e->cfg.mode == KAN_MODE_FP32;
-  // input pitch must be a multiple of 16 bytes for TMA
-  const float* xin = x;
-  int64_t ldx = D;
-  if (!fp32 && (D * 4) % 16 != 0) {
-    ldx = pitch16(D, 4);
-    e->xstage.alloc(static_cast<size_t>(M * ldx));
-    ck(cudaMemcpy2DAsync(e->xstage.p, ldx * 4, x, D * 4, D * 4, M, cudaMemcpyDeviceToDevice, st),
+  const int esz = act_esz(e);
+  // the model input: dense rows need a 16-byte pitch for TMA
+  Act in;
+  in.p = x;
+  in.kind = X_F32;
+  in.nchw = e->input_shape.size() == 3;
+  in.ld = e->input_size();
+  if (!in.nchw && !fp32 && (in.ld * 4) % 16 != 0) {
+    const int64_t D = in.ld;
+    in.ld = pitch16(D, 4);
+    e->xstage.alloc(static_cast<size_t>(M * in.ld));
+    ck(cudaMemcpy2DAsync(e->xstage.p, in.ld * 4, x, D * 4, D * 4, M, cudaMemcpyDeviceToDevice, st),
        "stage input");
-    xin = e->xstage.p;
+    in.p = e->xstage.p;
   }
-  // count KAN layers
-  std::vector<const Layer*> kl;
-  for (auto& l : e->layers)
-    if (l.type == L_LINEAR) kl.push_back(&l);
-  const void* cur = xin;
-  int cur_kind = X_F32;
-  int64_t cur_ld = ldx;
-  int pp = 0;
-  for (size_t li = 0; li < kl.size(); ++li) {
-    const Layer& l = *kl[li];
-    PreparedLayer& pl = e->prep[static_cast<size_t>(l.kan_index)];
-    const bool last = li + 1 == kl.size();
-    LayerIO io{};
-    io.x = cur;
-    io.x_kind = cur_kind;
-    io.ld_x = cur_ld;
-    void* dst;
-    int64_t ld_out;
-    int out_kind;
-    if (last) {
-      dst = out;
-      ld_out = pl.N;
-      out_kind = (lut && e->cfg.out_kind == KAN_OUT_I8) ? EPI_I8 : EPI_F32;
-    } else {
-      const int esz = lut ? 2 : 4;
-      ld_out = pitch16(pl.N, esz);
-      e->act[pp].alloc(static_cast<size_t>(M * ld_out * esz));
-      dst = e->act[pp].p;
-      out_kind = lut ? EPI_LEVEL : EPI_F32;
+  const int nl = static_cast<int>(e->layers.size());
+  // image models: the conv / pooling layers read NHWC, so the NCHW model input
+  // is transposed once (and quantized to lattice levels on the LUT path)
+  if (in.nchw) {
+    bool used_as_image = false;
+    for (const auto& l : e->layers)
+      used_as_image = used_as_image || (l.src < 0 && l.type != L_FLATTEN);
+    if (used_as_image) {
+      for (const auto& l : e->layers)
+        if (l.src < 0 && l.type == L_FLATTEN)
+          throw Unsupported("the model input cannot feed both a flatten and an image layer");
+      const int C = e->input_shape[0], HW = e->input_shape[1] * e->input_shape[2];
+      const bool levels = lut && !e->input_f32;
+      const int isz = levels ? 2 : 4;
+      const int64_t ldc = pitch16(C, isz);
+      e->xnhwc.alloc(static_cast<size_t>(M * HW * ldc * isz));
+      ck(launch_nchw_to_nhwc(levels, x, M, C, HW, e->xnhwc.p, static_cast<int>(ldc),
+                             levels ? e->d_thr.p : nullptr, static_cast<float>(e->grid.lo),
+                             levels ? static_cast<float>(1.0 / e->lat.step) : 0.f,
+                             levels ? static_cast<int>(e->lat.L) : 0, st),
+         "input transpose");
+      e->last_launches += 1;
+      in.p = e->xnhwc.p;
+      in.kind = levels ? X_U16 : X_F32;
+      in.nchw = false;
+      in.ld = ldc;
     }
+  }
+  std::vector<Act> acts(static_cast<size_t>(nl));
+  auto slot = [&](int i, size_t bytes) -> void* {
+    auto& b = e->slots[static_cast<size_t>(e->slot_of[static_cast<size_t>(i)])];
+    b.alloc(bytes);
+    return b.p;
+  };
+  for (int i = 0; i < nl; ++i) {
+    const Layer& l = e->layers[static_cast<size_t>(i)];
+    const Act src = l.src < 0 ? in : acts[static_cast<size_t>(l.src)];
+    const bool last = i + 1 == nl;
+    Act& dst = acts[static_cast<size_t>(i)];
+    if (l.type == L_FLATTEN) {
+      dst = src;
+      dst.ld = src.nchw ? static_cast<int64_t>(l.in.c) * l.in.h * l.in.w
+                        : static_cast<int64_t>(l.in.h) * l.in.w * src.ld;
+      dst.nchw = false;
+      continue;
+    }
+    if (l.type == L_MAXPOOL || l.type == L_AVGPOOL) {
+      if (src.nchw) throw Unsupported("pooling the model input is not supported");
+      const int C = l.in.c;
+      const int sz = src.kind == X_U16 ? 2 : 4;
+      dst.kind = src.kind;
+      dst.nchw = false;
+      dst.ld = pitch16(C, sz);
+      if (l.type == L_MAXPOOL) {
+        void* o = slot(i, static_cast<size_t>(M) * l.out.h * l.out.w * dst.ld * sz);
+        ck(launch_maxpool(src.kind == X_U16, src.p, M, l.in.h, l.in.w, C, static_cast<int>(src.ld),
+                          l.window, o, static_cast<int>(dst.ld), st),
+           "maxpool launch");
+        dst.p = o;
+      } else {
+        if (src.kind != X_F32) throw LogicError("average pooling reads fp32 values");
+        void* o = slot(i, static_cast<size_t>(M) * dst.ld * 4);
+        ck(launch_avgpool(src.p, M, l.in.h * l.in.w, C, static_cast<int>(src.ld), o,
+                          static_cast<int>(dst.ld), st),
+           "avgpool launch");
+        dst.p = o;
+      }
+      e->last_launches += 1;
+      continue;
+    }
+    // ---- KAN layer ----
+    PreparedLayer& pl = e->prep[static_cast<size_t>(l.kan_index)];
+    const bool conv = l.type == L_CONV;
+    const int64_t rows = conv ? M * l.out.h * l.out.w : M;
+    LayerIO io{};
+    io.x = src.p;
+    io.x_kind = src.kind;
+    io.ld_x = src.ld;
+    if (conv) {
+      if (src.nchw) throw LogicError("conv input must be stored NHWC");
+      io.conv = &l;
+      io.n_img = M;
+    }
+    if (l.res_src != -2) {
+      if (l.res_src < 0) throw Unsupported("residual from the model input is not supported");
+      const Act& r = acts[static_cast<size_t>(l.res_src)];
+      if (r.kind != X_F32) throw LogicError("residual tensors are stored as fp32 values");
+      io.res_kind = 2;
+      io.res = r.p;
+      io.ld_res = r.ld;
+    }
+    void* o;
+    if (last) {
+      o = out;
+      io.ld_out = pl.N;
+      io.epi = (lut && e->cfg.out_kind == KAN_OUT_I8) ? EPI_I8 : EPI_F32;
+      if (conv) io.out_hw = l.out.h * l.out.w;
+    } else {
+      const bool levels = lut && !l.store_f32;
+      const int osz = levels ? 2 : 4;
+      io.ld_out = pitch16(pl.N, osz);
+      o = slot(i, static_cast<size_t>(rows * io.ld_out * osz));
+      io.epi = levels ? EPI_LEVEL : EPI_F32;
+    }
+    io.out = o;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     unsigned ev_flags = cudaEventRecordDefault;
     if (e->profiling) {
@@ -882,23 +1258,19 @@ void forward(kan_engine* e, const float* x, int64_t M, void* out, cudaStream_t s
       ev_flags = cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault;
       ck(cudaEventRecordWithFlags(ev0, st, ev_flags), "cudaEventRecord");
     }
-    if (fp32) {
-      run_fp32_layer(e, pl, M, static_cast<const float*>(cur), cur_ld, static_cast<float*>(dst),
-                     ld_out, st);
-    } else {
-      io.out = dst;
-      io.epi = out_kind;
-      io.ld_out = ld_out;
-      run_gemm_layer(e, pl, M, io, st);
-    }
+    if (fp32)
+      run_fp32_layer(e, pl, M, static_cast<const float*>(src.p), src.ld, static_cast<float*>(o),
+                     io.ld_out, st);
+    else
+      run_gemm_layer(e, pl, rows, io, st);
     if (e->profiling) {
       ck(cudaEventRecordWithFlags(ev1, st, ev_flags), "cudaEventRecord");
       e->pending.push_back({l.kan_index, ev0, ev1});
     }
-    cur = dst;
-    cur_kind = lut ? X_U16 : X_F32;
-    cur_ld = ld_out;
-    pp ^= 1;
+    dst.p = o;
+    dst.kind = io.epi == EPI_LEVEL ? X_U16 : X_F32;
+    dst.nchw = false;
+    dst.ld = io.ld_out;
   }
 }
 
@@ -923,6 +1295,11 @@ kan_status kan_engine_create(const char* descriptor_json, int device, kan_engine
     }
     e->grid = Grid::build(j.at("grid").at("intervals").integer(), j.at("grid").at("degree").integer(), lo, hi);
     if (j.has("name")) e->name = j.at("name").string();
+    if (j.has("conv_output")) {
+      const std::string co = j.at("conv_output").string();
+      if (co != "floor" && co != "exact") throw FormatError("model_from_descriptor: conv_output must be 'exact' or 'floor'");
+      e->conv_floor = co == "floor";
+    }
     for (const auto& d : j.at("input").arr) e->input_shape.push_back(d.integer());
     int kan_idx = 0;
     for (const auto& jl : j.at("layers").arr) {
@@ -948,9 +1325,14 @@ kan_status kan_engine_create(const char* descriptor_json, int device, kan_engine
         l.window = jl.value_int("window", 2);
       } else if (type == "flatten") {
         l.type = L_FLATTEN;
+      } else if (type == "global_avgpool") {
+        l.type = L_AVGPOOL;
       } else {
         throw FormatError("model_from_descriptor: unknown layer type '" + type + "'");
       }
+      if (jl.has("id")) l.id = jl.at("id").string();
+      if (jl.has("input_from")) l.input_from = jl.at("input_from").string();
+      if (jl.has("residual")) l.residual = jl.at("residual").string();
       e->layers.push_back(std::move(l));
     }
     e->n_kan = kan_idx;

@@ -318,7 +318,7 @@ __device__ __forceinline__ void lut_row(const GemmParams& p, const uint32_t* val
     }
     if constexpr (MODE == MODE_ZP) {
       // codes shifted past the row end are zero (see lut_basis_lookup)
-      if (i0 + e < p.n_in) rsum = __dp4a(v, 0x01010101u, rsum);
+      if (i0 + e < p.n_ch) rsum = __dp4a(v, 0x01010101u, rsum);
     }
   }
   if constexpr (MODE == MODE_SILU) {
@@ -380,6 +380,29 @@ __device__ __forceinline__ void bf16_row(const GemmParams& p, const float (&x)[3
   }
 }
 
+// Walk over the conv taps in spline-stage order (tap-major, channel chunk
+// minor), without divisions in the loop.
+struct TapWalk {
+  int cc = 0, kx = 0, ky = 0;
+  __device__ TapWalk(const GemmParams& p, int sp0) {
+    if (p.conv) {
+      const int t = sp0 / p.cps;
+      cc = sp0 - t * p.cps;
+      ky = t / p.ksz;
+      kx = t - ky * p.ksz;
+    }
+  }
+  __device__ __forceinline__ void next(const GemmParams& p) {
+    if (++cc == p.cps) {
+      cc = 0;
+      if (++kx == p.ksz) {
+        kx = 0;
+        ++ky;
+      }
+    }
+  }
+};
+
 template <bool BF16, int NBP, int MODE>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     kan_gather_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const GemmParams p) {
@@ -418,6 +441,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int n_tile = blockIdx.x;
   const int split = blockIdx.z;
   const int m0 = m_tile * 128;
+  // conv tiles: first image and first output row of this M tile
+  const int n0 = p.conv ? (m_tile / p.tpi) * p.bn_img : 0;
+  const int y0 = p.conv ? (m_tile % p.tpi) * p.bh : 0;
 
   const int g0 = split * p.groups_per_split;
   const int g1 = min(p.n_groups, g0 + p.groups_per_split);
@@ -476,14 +502,26 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   if (warp == NPW) {
     // ========================= activation loader ==========================
     Ring rx(SX);
+    TapWalk tw(p, g0 * C::GS);
     for (int g = g0; g < g1; ++g) {
       const int nsp = min(C::GS, p.n_spline_stages - g * C::GS);
-      for (int s = 0; s < nsp; ++s, rx.next()) {
+      for (int s = 0; s < nsp; ++s, rx.next(), tw.next(p)) {
         mbar_wait(bar_xempty(rx.slot), rx.phase ^ 1);
         if (lane == 0) {
+          const uint32_t dst = smem_u32(sX + static_cast<size_t>(rx.slot) * x_bytes);
           mbar_arrive_tx(bar_xfull(rx.slot), x_bytes);
-          tma_load_2d(smem_u32(sX + static_cast<size_t>(rx.slot) * x_bytes), &xmap,
-                      (g * C::GS + s) * C::IPS, m0, bar_xfull(rx.slot));
+          if (!p.conv) {
+            tma_load_2d(dst, &xmap, (g * C::GS + s) * C::IPS, m0, bar_xfull(rx.slot));
+          } else {
+            // the tap's input window: rows y0*stride + ky - pad.., columns kx - pad..
+            // (element strides in the tensor map step by the conv stride)
+            int iy = y0 * p.cstride + tw.ky - p.pad, ix = tw.kx - p.pad;
+            if (p.dbg_flags & 4) {  // tuning/debug only: never negative coordinates
+              iy = max(iy, 0);
+              ix = max(ix, 0);
+            }
+            tma_load_4d(dst, &xmap, tw.cc * C::IPS, ix, iy, n0, bar_xfull(rx.slot));
+          }
         }
         __syncwarp();
       }
@@ -559,6 +597,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const uint8_t* silu_tab = sT + p.off_silu;
     constexpr int H = C::Q;
     const int xoff = h * H * static_cast<int>(xesz);  // this thread's bytes in the x row
+    // conv: this row's output pixel
+    int oy = 0, ox = 0;
+    if (p.conv) {
+      const int pix = r % p.pimg;
+      const int yy = pix / p.Wo;
+      oy = y0 + yy;
+      ox = pix - yy * p.Wo;
+    }
+    TapWalk tw(p, g0 * C::GS);
 
     Ring ra(SA), rx(SX);
     int idx = 0;
@@ -570,7 +617,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           // 1. this thread's activations of the stage -> registers; free the slot
           mbar_wait(bar_xfull(rx.slot), rx.phase);
           const uint8_t* xt = sX + static_cast<size_t>(rx.slot) * x_bytes;
-          const int i0 = (g * C::GS + s) * C::IPS + h * H;
+          const int i0 = (p.conv ? tw.cc * C::IPS : (g * C::GS + s) * C::IPS) + h * H;
+          // padded conv taps read level(0.0) (layers.hpp:146-147 leaves them 0.0)
+          bool padtap = false;
+          if (p.conv) {
+            const int iy = oy * p.cstride + tw.ky - p.pad, ix = ox * p.cstride + tw.kx - p.pad;
+            padtap = static_cast<unsigned>(iy) >= static_cast<unsigned>(p.H) ||
+                     static_cast<unsigned>(ix) >= static_cast<unsigned>(p.W);
+          }
+          tw.next(p);
           if constexpr (BF16) {
             uint32_t xr[H];
             load_x<4 * H>(xt, r, xoff, x_row_bytes, xr);
@@ -602,8 +657,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               if (lane == 0) mbar_arrive(bar_xempty(rx.slot));
 #pragma unroll
               for (int q = 0; q < H / 2; ++q) {
-                a[2 * q] = static_cast<int>(xr[q] & 0xFFFF);
-                a[2 * q + 1] = static_cast<int>(xr[q] >> 16);
+                a[2 * q] = padtap ? p.lvl0 : static_cast<int>(xr[q] & 0xFFFF);
+                a[2 * q + 1] = padtap ? p.lvl0 : static_cast<int>(xr[q] >> 16);
               }
             }
             rx.next();
@@ -681,7 +736,23 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         y[e] = __dmul_rn(static_cast<double>(v), s_cols[jl]);
       }
     }
-    if (p.epi == EPI_F32) {
+    if (p.res_kind) {
+      // residual add of a stored fp32 tensor (engine extension, GemmParams::res_kind)
+      const float* rr = reinterpret_cast<const float*>(p.res) + static_cast<size_t>(row) * p.ld_res + col0;
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (e < nvalid) y[e] = __dadd_rn(y[e], static_cast<double>(rr[e]));
+    }
+    if (p.epi == EPI_F32 && p.out_hw > 0) {
+      // NCHW model output (convkan_forward reshapes rows to [c_out, H, W], layers.hpp:179-184)
+      const int hw = p.out_hw;
+      const int img = row / hw;
+      float* o = reinterpret_cast<float*>(p.out) + static_cast<size_t>(img) * p.N * hw +
+                 static_cast<size_t>(col0) * hw + (row - img * hw);
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (e < nvalid) o[static_cast<size_t>(e) * hw] = __double2float_rn(y[e]);
+    } else if (p.epi == EPI_F32) {
       float* o = reinterpret_cast<float*>(p.out) + base;
       if (nvalid == 4 && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
         *reinterpret_cast<float4*>(o) = make_float4(__double2float_rn(y[0]), __double2float_rn(y[1]),
@@ -881,6 +952,123 @@ cudaError_t launch_levels(const float* x, int64_t n, const float* thr, float lo,
   if (blocks < 1) blocks = 1;
   kan_levels_kernel<<<blocks, 256, (L + 2) * sizeof(float), st>>>(x, n, thr, lo, inv_step, L,
                                                                    out);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Pooling over stored activations (NHWC; u16 lattice levels on the LUT path,
+// fp32 on the float paths).
+//
+// maxpool2 (layers.hpp:193-210): max over window x window, stride = window.
+// The lattice level is monotone in x, so the max of levels is the level of
+// the max the reference feeds the next layer.
+template <class T>
+__global__ void kan_maxpool_kernel(const T* __restrict__ in, int64_t n_img, int H, int W, int C,
+                                   int ld_in, int win, T* __restrict__ out, int ld_out) {
+  const int Ho = H / win, Wo = W / win;
+  const int64_t total = n_img * Ho * Wo * C;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(i % C);
+    const int64_t q = i / C;
+    const int ox = static_cast<int>(q % Wo);
+    const int oy = static_cast<int>((q / Wo) % Ho);
+    const int64_t n = q / (static_cast<int64_t>(Wo) * Ho);
+    T best = in[((n * H + oy * win) * W + ox * win) * ld_in + c];
+    for (int dy = 0; dy < win; ++dy)
+      for (int dx = 0; dx < win; ++dx) {
+        const T v = in[((n * H + oy * win + dy) * W + ox * win + dx) * ld_in + c];
+        best = v > best ? v : best;
+      }
+    out[((n * Ho + oy) * Wo + ox) * ld_out + c] = best;
+  }
+}
+
+// Global average pool (engine extension for ResKAN18): mean over the H*W
+// positions of each channel of stored fp32 values, summed in position order
+// in fp64, rounded to fp32.
+__global__ void kan_avgpool_f32_kernel(const float* __restrict__ in, int64_t n_img, int HW, int C,
+                                       int ld_in, float* __restrict__ out, int ld_out) {
+  const int64_t total = n_img * C;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(i % C);
+    const int64_t n = i / C;
+    const float* src = in + n * HW * ld_in + c;
+    double acc = 0.0;
+    for (int q = 0; q < HW; ++q) acc = __dadd_rn(acc, static_cast<double>(src[q * ld_in]));
+    out[n * ld_out + c] = __double2float_rn(__ddiv_rn(acc, static_cast<double>(HW)));
+  }
+}
+
+static int pool_blocks(int64_t total) {
+  const int64_t nb = (total + 255) / 256;
+  return static_cast<int>(nb < 148 * 16 ? (nb < 1 ? 1 : nb) : 148 * 16);
+}
+
+cudaError_t launch_maxpool(bool levels, const void* in, int64_t n_img, int H, int W, int C,
+                           int ld_in, int win, void* out, int ld_out, cudaStream_t st) {
+  const int64_t total = n_img * (H / win) * (W / win) * C;
+  if (total == 0) return cudaSuccess;
+  if (levels)
+    kan_maxpool_kernel<uint16_t><<<pool_blocks(total), 256, 0, st>>>(
+        static_cast<const uint16_t*>(in), n_img, H, W, C, ld_in, win, static_cast<uint16_t*>(out), ld_out);
+  else
+    kan_maxpool_kernel<float><<<pool_blocks(total), 256, 0, st>>>(
+        static_cast<const float*>(in), n_img, H, W, C, ld_in, win, static_cast<float*>(out), ld_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_avgpool(const void* in, int64_t n_img, int HW, int C, int ld_in, void* out,
+                           int ld_out, cudaStream_t st) {
+  const int64_t total = n_img * C;
+  if (total == 0) return cudaSuccess;
+  kan_avgpool_f32_kernel<<<pool_blocks(total), 256, 0, st>>>(
+      static_cast<const float*>(in), n_img, HW, C, ld_in, static_cast<float*>(out), ld_out);
+  return cudaGetLastError();
+}
+
+// NCHW fp32 model input -> NHWC (lattice levels on the LUT path, fp32 on the
+// float paths) for the conv layers' TMA, which needs the innermost (channel)
+// box start 16-byte aligned.  32x32 (pixel x channel) tiles through smem;
+// levels as lattice_level_f32 (exact ActivationLattice::quantize of clamp(x)).
+template <bool LEVELS>
+__global__ void kan_nchw_to_nhwc_kernel(const float* __restrict__ in, int C, int HW,
+                                        void* __restrict__ out, int ldc,
+                                        const float* __restrict__ thr, float lo, float inv_step,
+                                        int L) {
+  __shared__ float tile[32][33];
+  const int64_t n = blockIdx.z;
+  const int p0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+  const float* src = in + n * C * HW;
+  for (int cy = threadIdx.y; cy < 32; cy += 8) {
+    const int c = c0 + cy, q = p0 + threadIdx.x;
+    tile[cy][threadIdx.x] = (c < C && q < HW) ? src[static_cast<int64_t>(c) * HW + q] : 0.f;
+  }
+  __syncthreads();
+  for (int py = threadIdx.y; py < 32; py += 8) {
+    const int q = p0 + py, c = c0 + threadIdx.x;
+    if (q < HW && c < C) {
+      const float v = tile[threadIdx.x][py];
+      const int64_t o = (n * HW + q) * ldc + c;
+      if constexpr (LEVELS)
+        static_cast<uint16_t*>(out)[o] = static_cast<uint16_t>(lattice_level_f32(v, thr, lo, inv_step, L));
+      else
+        static_cast<float*>(out)[o] = v;
+    }
+  }
+}
+
+cudaError_t launch_nchw_to_nhwc(bool levels, const float* in, int64_t n_img, int C, int HW,
+                                void* out, int ldc, const float* thr, float lo, float inv_step,
+                                int L, cudaStream_t st) {
+  if (n_img == 0) return cudaSuccess;
+  const dim3 grid((HW + 31) / 32, (C + 31) / 32, static_cast<unsigned>(n_img));
+  const dim3 block(32, 8);
+  if (levels)
+    kan_nchw_to_nhwc_kernel<true><<<grid, block, 0, st>>>(in, C, HW, out, ldc, thr, lo, inv_step, L);
+  else
+    kan_nchw_to_nhwc_kernel<false><<<grid, block, 0, st>>>(in, C, HW, out, ldc, thr, lo, inv_step, L);
   return cudaGetLastError();
 }
 

@@ -44,7 +44,7 @@ struct GemmParams {
   // float basis (bf16 path)
   float flo, fhi_open, finv_delta;
   int G, P;
-  // pre-tiled, pre-swizzled weights: [n_tiles_n][total_stages][BN*128] bytes
+  // pre-tiled, pre-swizzled weights: [n_tiles_n][total_stages][BN*KSTAGE] bytes
   const uint8_t* wt;
   int b_signed;
   // split-K over a thread-block cluster of `splits` CTAs along z: partial
@@ -65,6 +65,18 @@ struct GemmParams {
   int n_L;
   double out_scale, inv_out_scale;
   int m_tiles;
+  // implicit im2col (conv layers; conv == 0 for dense [M, n_in] rows).  K runs
+  // tap-major: spline stage sp covers tap sp / cps, channels (sp % cps)*IPS...
+  // An M tile is bn_img images x bh output rows x Wo columns (pimg = bh*Wo
+  // pixels per image); rows stay contiguous in M = (n, oy, ox).
+  int conv, ksz, cstride, pad, cps, H, W, Ho, Wo, bh, bn_img, tpi, pimg;
+  int lvl0;    // lattice level of 0.0 (padded taps of u16 level inputs)
+  int n_ch;    // valid inputs per row chunk (dense: n_in; conv: c_in)
+  // epilogue residual add (engine extension): 2 = stored fp32 values, 0 = none
+  int res_kind;
+  const void* res;
+  int ld_res;
+  int out_hw;  // EPI_F32: >0 writes NCHW (H*W per channel), 0 row-major
   // optional per-CTA phase timestamps (%globaltimer ns) for tuning:
   // [cta][8] = start, tables ready, first A stage, last A stage, TMEM full,
   // partials exchanged, done

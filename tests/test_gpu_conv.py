@@ -1,0 +1,151 @@
+"""GPU parity of the conv path (implicit im2col through 4D TMA) and of the
+ResKAN18 building blocks (stride-2 convs, 1x1 projection shortcuts, residual
+adds, pooling, flatten), through the C ABI, against the CPU oracle
+(oracle/pyoracle.py Oracle.int_model_forward) and the compiled reference.
+
+Bar: bit-exact on the integer LUT path; 1e-2 norm-relative on the bf16 path.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+from paper_2603_17230_b200 import (  # noqa: E402
+    Engine, EvalOptions, W_PER_CHANNEL_SYM, W_PER_TENSOR_ASYM, configs)
+
+
+def conv_desc(C, H, W, co, k, s, p, floor=False):
+    d = {"name": "conv", "grid": {"intervals": 5, "degree": 3}, "input": [C, H, W],
+         "layers": [{"type": "conv", "c_in": C, "c_out": co, "kernel": k, "stride": s,
+                     "padding": p}]}
+    if floor:
+        d["conv_output"] = "floor"
+    return d
+
+
+def weights_for(desc, G=5, P=3, seed=0, std=0.05, silu=True):
+    wl = configs.Workload("t", "t", [0], G, P, 1, std, silu=silu, seed=seed,
+                          input_shape=desc["input"], layers=desc["layers"])
+    return wl.weights()
+
+
+def build(desc, Ws, Bs, **opts):
+    e = Engine(desc, 0)
+    for i, (w, b) in enumerate(zip(Ws, Bs)):
+        e.set_coeffs(i, w, b)
+    e.configure(EvalOptions(**opts))
+    return e
+
+
+def to_dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).cuda()
+
+
+def rel_err(a, b):
+    a = np.asarray(a, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+CONV_CASES = [
+    # C, H, W, c_out, k, s, p, silu, wscheme, batch, split
+    (64, 32, 32, 64, 3, 1, 1, True, W_PER_CHANNEL_SYM, 2, 0),   # C4 shape
+    (16, 8, 8, 24, 3, 1, 1, False, W_PER_CHANNEL_SYM, 5, 0),    # 2 images per M tile, ragged
+    (3, 16, 16, 16, 3, 1, 1, True, W_PER_CHANNEL_SYM, 3, 0),    # stem: c_in < one chunk
+    (8, 8, 8, 8, 3, 1, 1, False, W_PER_TENSOR_ASYM, 4, 0),      # reference weight scheme
+    (64, 16, 16, 32, 3, 1, 1, True, W_PER_CHANNEL_SYM, 2, 2),   # split-K over a cluster
+    (32, 4, 4, 300, 3, 1, 1, True, W_PER_CHANNEL_SYM, 9, 0),    # 8 images per tile, 2 N tiles
+    (5, 8, 8, 7, 1, 1, 0, True, W_PER_CHANNEL_SYM, 4, 0),       # 1x1
+]
+
+
+@pytest.mark.parametrize("C,H,W,co,k,s,p,silu,ws,batch,split", CONV_CASES)
+def test_conv_layer_bit_exact(oracle, C, H, W, co, k, s, p, silu, ws, batch, split):
+    desc = conv_desc(C, H, W, co, k, s, p)
+    Ws, Bs = weights_for(desc, seed=C + co, silu=silu)
+    x = np.random.default_rng(C * 7 + co).uniform(-1.05, 1.05, (batch, C * H * W)).astype(np.float32)
+    e = build(desc, Ws, Bs, mode="bspline-lut", lut_k=8, lut_h=8, bits_w=8, w_scheme=ws,
+              silu_base=silu, split_k=split)
+    y = e.model_forward(to_dev(x)).cpu().numpy()
+    yo = oracle.int_model_forward(desc, Ws, Bs, x, 8, 8, ws, 8)
+    np.testing.assert_array_equal(y, yo.astype(np.float32).reshape(batch, -1))
+
+
+def test_conv_reference_scheme_matches_reference_conv(oracle, ref):
+    """Reference weight scheme (per-tensor u8, no SiLU): the GPU conv equals
+    convkan_forward with LutBasis (layers.hpp:162-190) to fp32 rounding."""
+    desc = conv_desc(8, 8, 8, 6, 3, 1, 1)
+    Ws, _ = weights_for(desc, seed=3, silu=False)
+    x = np.random.default_rng(3).uniform(-1, 1, (3, 8 * 64)).astype(np.float32)
+    e = build(desc, Ws, [None], mode="bspline-lut", lut_k=8, lut_h=8, bits_w=8,
+              w_scheme=W_PER_TENSOR_ASYM)
+    y = e.model_forward(to_dev(x)).cpu().numpy().reshape(3, 6, 8, 8)
+    for n in range(3):
+        r = ref.conv_forward(5, 3, x[n].reshape(8, 8, 8).astype(np.float64), Ws[0], 6, 3, 1, 1,
+                             mode=1, k=8, h=8, bits_w=8)
+        assert rel_err(y[n], r) < 1e-6
+
+
+@pytest.mark.parametrize("k,s,p", [(3, 2, 1), (1, 2, 0)])
+def test_strided_conv_on_levels_bit_exact(oracle, k, s, p):
+    """Stride-2 convs read stored NHWC levels through TMA element strides."""
+    desc = {"name": "s2", "grid": {"intervals": 5, "degree": 3}, "input": [3, 16, 16],
+            "conv_output": "floor",
+            "layers": [{"type": "conv", "c_in": 3, "c_out": 32, "kernel": 3, "stride": 1, "padding": 1},
+                       {"type": "conv", "c_in": 32, "c_out": 40, "kernel": k, "stride": s, "padding": p}]}
+    Ws, Bs = weights_for(desc, seed=k)
+    x = np.random.default_rng(k).uniform(-1, 1, (3, 3 * 256)).astype(np.float32)
+    e = build(desc, Ws, Bs, mode="bspline-lut", lut_k=8, lut_h=8, bits_w=8,
+              w_scheme=W_PER_CHANNEL_SYM, silu_base=True)
+    y = e.model_forward(to_dev(x)).cpu().numpy()
+    yo = oracle.int_model_forward(desc, Ws, Bs, x, 8, 8, W_PER_CHANNEL_SYM, 8)
+    np.testing.assert_array_equal(y, yo.astype(np.float32).reshape(3, -1))
+
+
+@pytest.mark.parametrize("h", [3, 8])
+def test_small_reskan_bit_exact(oracle, h):
+    """ResKAN18 topology at reduced width / resolution: stem, identity and
+    projection residual blocks, stride 2, global average pool, linear head."""
+    layers = configs.reskan18_layers(width=(16, 32), n_classes=10, in_ch=3)
+    desc = {"name": "reskan-small", "grid": {"intervals": 5, "degree": 3}, "input": [3, 16, 16],
+            "conv_output": "floor", "layers": layers}
+    Ws, Bs = weights_for(desc, seed=h)
+    x = np.random.default_rng(h).uniform(-1, 1, (6, 3 * 256)).astype(np.float32)
+    e = build(desc, Ws, Bs, mode="bspline-lut", lut_k=8, lut_h=h, bits_w=8,
+              w_scheme=W_PER_CHANNEL_SYM, silu_base=True)
+    y = e.model_forward(to_dev(x)).cpu().numpy()
+    yo = oracle.int_model_forward(desc, Ws, Bs, x, 8, h, W_PER_CHANNEL_SYM, 8)
+    np.testing.assert_array_equal(y, yo.astype(np.float32))
+    # one launch per KAN layer + the input transpose + the pooling kernel
+    assert e.last_launches == len(Ws) + 2
+
+
+def test_maxpool_flatten_linear_bit_exact(oracle):
+    """conv -> maxpool -> flatten -> linear (the reference's LeKAN-style stack):
+    the linear layer's rows are permuted to the stored NHWC order."""
+    desc = {"name": "cnn", "grid": {"intervals": 5, "degree": 3}, "input": [1, 16, 16],
+            "layers": [{"type": "conv", "c_in": 1, "c_out": 8, "kernel": 3, "stride": 1, "padding": 1},
+                       {"type": "maxpool", "window": 2},
+                       {"type": "flatten"},
+                       {"type": "linear", "n_in": 8 * 8 * 8, "n_out": 10}]}
+    Ws, Bs = weights_for(desc, seed=5)
+    x = np.random.default_rng(5).uniform(-1, 1, (7, 256)).astype(np.float32)
+    e = build(desc, Ws, Bs, mode="bspline-lut", lut_k=8, lut_h=8, bits_w=8,
+              w_scheme=W_PER_CHANNEL_SYM, silu_base=True)
+    y = e.model_forward(to_dev(x)).cpu().numpy()
+    yo = oracle.int_model_forward(desc, Ws, Bs, x, 8, 8, W_PER_CHANNEL_SYM, 8)
+    np.testing.assert_array_equal(y, yo.astype(np.float32))
+
+
+def test_bf16_conv_vs_reference(ref):
+    """bf16 path (fp32 Cox-de Boor basis -> bf16 tcgen05): 1e-2 norm-relative
+    against the reference's fp64 convkan_forward."""
+    desc = conv_desc(16, 8, 8, 16, 3, 1, 1)
+    Ws, _ = weights_for(desc, seed=11, silu=False)
+    x = np.random.default_rng(11).uniform(-1, 1, (2, 16 * 64)).astype(np.float32)
+    e = build(desc, Ws, [None], mode="bf16")
+    y = e.model_forward(to_dev(x)).cpu().numpy().reshape(2, 16, 8, 8)
+    r = np.stack([ref.conv_forward(5, 3, x[n].reshape(16, 8, 8).astype(np.float64), Ws[0], 16, 3,
+                                   1, 1) for n in range(2)])
+    assert rel_err(y, r) < 1e-2
