@@ -172,6 +172,26 @@ def committed_traffic(config: str):
 
 
 # ---------------------------------------------------------------------------------
+def ref_forward(ref, wl, Ws, x, threads):
+    """One call of the reference's CPU path on rows x: model_forward for models
+    the reference's descriptor schema expresses (bspline-lut mode, per-tensor u8
+    W, eval.hpp:70-76, no SiLU term -- the reference has none); for ResKAN18 the
+    harness composition of reference functions (oracle/ref_shim.cpp
+    ref_graph_forward)."""
+    text = json.dumps(wl.descriptor())
+    if wl.reference_expressible:
+        return ref.model_forward(text, Ws, x, wl.out_size, mode=2, k=wl.lut_k, h=wl.lut_h,
+                                 bits_w=8, threads=threads, chunk=256)
+    return ref.graph_forward(text, Ws, x, wl.out_size, k=wl.lut_k, h=wl.lut_h, bits_w=8,
+                             threads=threads)
+
+
+def cpu_rows(wl, cores):
+    """Rows per reference call: 256-row chunks per thread for the MLPs; for the
+    conv models (0.6-9 GOP per sample) one sample per thread."""
+    return 2048 if wl.layers is None else cores
+
+
 def cpu_baseline(wl, seconds: float):
     """The reference's own CPU path (oracle/_ref = the reference headers compiled
     unmodified): model_forward in bspline-lut mode with the reference's weight
@@ -181,29 +201,30 @@ def cpu_baseline(wl, seconds: float):
     from oracle.pyoracle import Oracle, Ref
     Ws, _ = wl.weights()
     cores = os.cpu_count() or 1
-    rows = 2048
+    rows = cpu_rows(wl, cores)
     x = wl.inputs(rows, seed=99).astype(np.float64)
-    text = json.dumps(wl.descriptor())
     if Ref.available:
         ref = Ref()
-        mode = 2 if wl.mode == "bspline-lut" else 0
         n = 0
         t0 = time.perf_counter()
         while True:
-            ref.model_forward(text, Ws, x, wl.dims[-1], mode=mode, k=wl.lut_k, h=wl.lut_h,
-                              bits_w=8, threads=cores, chunk=256)
+            ref_forward(ref, wl, Ws, x, cores)
             n += rows
             if time.perf_counter() - t0 >= seconds:
                 break
         dt = time.perf_counter() - t0
+        how = ("model_forward" if wl.reference_expressible else
+               "convkan_forward/kan_linear_forward composition (ref_graph_forward)")
         return {"value": n / dt, "unit": "samples/s", "cores": cores, "kind": "reference",
                 "sample": f"{n} samples ({rows}-row calls) of {wl.key} through the reference "
-                          f"model_forward ({'bspline-lut k%d h%d, per-tensor u8 W' % (wl.lut_k, wl.lut_h) if mode == 2 else 'fp32'}"
-                          f", no SiLU term), {cores} threads, {dt:.1f} s"}
+                          f"{how} (bspline-lut k{wl.lut_k} h{wl.lut_h}, per-tensor u8 W, no SiLU "
+                          f"term), {cores} threads, {dt:.1f} s"}
     o = Oracle()
     g = o.grid(wl.G, wl.P)
     n = 0
     t0 = time.perf_counter()
+    if wl.layers is not None:
+        raise RuntimeError("oracle/_ref not built: no CPU baseline for conv models")
     while time.perf_counter() - t0 < seconds:
         h = x[:256]
         for w in Ws:
@@ -223,20 +244,22 @@ def run_reference(args):
     from oracle.pyoracle import Ref
     wl = configs.get(args.config)
     cores = os.cpu_count() or 1
-    rows = 256 * cores  # one >=256-row chunk per thread (weights re-quantized per call)
+    # MLPs: one >=256-row chunk per thread; conv models: one sample per thread
+    rows = 256 * cores if wl.layers is None else cores
     x = wl.inputs(rows, seed=7).astype(np.float64)
     Ws, _ = wl.weights()
-    text = json.dumps(wl.descriptor())
     if not Ref.available:
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
         return
     ref = Ref()
 
     def step():
-        ref.model_forward(text, Ws, x, wl.dims[-1], mode=2, k=wl.lut_k, h=wl.lut_h, bits_w=8,
-                          threads=cores, chunk=256)
-    steps = min(args.steps, 50)
-    for _ in range(min(args.warmup, 3)):
+        ref_forward(ref, wl, Ws, x, cores)
+    t0 = time.perf_counter()
+    step()  # first warm-up step also sizes the run (whole run within ~2 minutes)
+    t_step = time.perf_counter() - t0
+    steps = max(1, min(args.steps, 50, int(120.0 / max(t_step, 1e-3))))
+    for _ in range(min(args.warmup, 3) - 1):
         step()
     t0 = time.perf_counter()
     for _ in range(steps):
@@ -249,11 +272,14 @@ def run_reference(args):
         "ms_per_step": dt / steps * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": wl.key + ": " + wl.title, "batch_per_step": rows,
-                   "note": "reference CPU path: model_forward bspline-lut, per-tensor u8 W, no SiLU"},
+                   "note": "reference CPU path: " + (
+                       "model_forward" if wl.reference_expressible else
+                       "composition of convkan_forward / kan_linear_forward (ref_graph_forward)")
+                   + f" bspline-lut k{wl.lut_k} h{wl.lut_h}, per-tensor u8 W, no SiLU"},
         "cpu_baseline": {"value": v, "unit": "samples/s", "cores": cores, "kind": "reference",
                          "sample": f"{steps} steps x {rows} rows, {cores} threads"},
         "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "note": f"--steps capped at {steps} so the CPU run stays within minutes",
+        "note": f"--steps capped at {steps} so the CPU run stays within about two minutes",
     }))
 
 
@@ -288,7 +314,7 @@ def main():
     eng.configure(opts)
 
     # rotating resident input batches, total > L2
-    in_bytes = B * wl.dims[0] * 4
+    in_bytes = B * wl.input_size * 4
     R = max(2, min(64, math.ceil(2 * L2_BYTES / in_bytes)))
     R = max(R, 16) if in_bytes < 64 * 1024 * 1024 else R
     xs = [torch.from_numpy(wl.inputs(B, seed=100 * rank + r)).to(dev) for r in range(R)]
@@ -298,7 +324,7 @@ def main():
         opts.out_kind, opts.out_scale = OUT_I8, s_out
         eng.configure(opts)
     out_dtype = torch.int8 if wl.int8_out else torch.float32
-    outs = torch.empty((R, B, wl.dims[-1]), device=dev, dtype=out_dtype)
+    outs = torch.empty((R, B, wl.out_size), device=dev, dtype=out_dtype)
     st = torch.cuda.Stream(dev)
     torch.cuda.synchronize()
     # warm the engine (allocations happen outside graph capture)
@@ -358,7 +384,7 @@ def main():
     # ---- dominant kernel: per-launch device time with CUDA events (engine profiling)
     # (the event pairs are recorded as graph nodes around each kernel node, so
     # host launch gaps stay out of the per-launch device time)
-    prof_steps = max(2, min(args.steps, 64 if B * wl.dims[0] < 2 ** 24 else 8))
+    prof_steps = max(2, min(args.steps, 64 if B * wl.input_size < 2 ** 24 else 8))
     eng.set_profiling(True)
     pg = torch.cuda.CUDAGraph()
     with torch.cuda.graph(pg, stream=st):
@@ -367,7 +393,7 @@ def main():
     pg.replay()
     torch.cuda.synchronize()
     layer_ms = []
-    for li in range(len(wl.dims) - 1):
+    for li in range(wl.n_kan):
         tot, cnt = eng.layer_time_ms(li)
         layer_ms.append(tot / max(cnt, 1))
     eng.set_profiling(False)
@@ -394,7 +420,9 @@ def main():
                 "peak": tensor_peak / 1e12, "unit": "TOP/s" if lut else "TFLOP/s"}
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["traffic"] = committed_traffic(wl.key)
-    roof["kernel"] = f"kan_gather_gemm layer {dom} ({wl.dims[dom]}->{wl.dims[dom + 1]})"
+    kl = wl.kan_layers()[dom]
+    roof["kernel"] = (f"kan_gather_gemm KAN layer {dom} ({kl['n_in']}->{kl['n_out']}"
+                      + (f", {kl['pix']} px/sample)" if kl["pix"] > 1 else ")"))
     roof["per_launch"] = {"algorithmic_bytes": bytes_l, "algorithmic_ops": ops_l,
                           "avg_ms": layer_ms[dom], "launches_timed": prof_steps}
     roof["peak_source"] = peak_src + (
@@ -405,7 +433,7 @@ def main():
     # ---- e2e through the public API: host buffers, H2D + forward + D2H every step
     e2e_steps = max(10, min(args.steps, 300))
     hx = [torch.from_numpy(wl.inputs(B, seed=500 + r)).pin_memory() for r in range(4)]
-    hout = torch.empty((B, wl.dims[-1]), dtype=out_dtype).pin_memory()
+    hout = torch.empty((B, wl.out_size), dtype=out_dtype).pin_memory()
     for i in range(3):
         eng.forward_host_ptr(hx[i % 4].data_ptr(), B, hout.data_ptr(), stream=st)
     if world > 1:
@@ -419,7 +447,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     e2e = {"value": world * B * e2e_steps / e2e_s, "unit": "samples/s",
-           "h2d_bytes_per_step": in_bytes, "d2h_bytes_per_step": B * wl.dims[-1] *
+           "h2d_bytes_per_step": in_bytes, "d2h_bytes_per_step": B * wl.out_size *
            (1 if wl.int8_out else 4), "steps": e2e_steps,
            "api": "kan_engine_forward_host (pinned host buffers, stream-synchronous)"}
 

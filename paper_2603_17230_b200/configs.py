@@ -134,6 +134,21 @@ class Workload:
         return len(self.kan_layers())
 
     @property
+    def out_size(self) -> int:
+        """Values per sample of the model output (the last layer, flattened)."""
+        return int(np.prod(walk_shapes(self.descriptor())[-1]["out"]))
+
+    @property
+    def reference_expressible(self) -> bool:
+        """True when the reference's own model_forward can run this model: no
+        engine descriptor extensions, and a flat (linear) output layer
+        (model_forward returns flat logits, eval.hpp:200-253)."""
+        d = self.descriptor()
+        ext = {"id", "input_from", "residual"}
+        return d["layers"][-1]["type"] == "linear" and "conv_output" not in d and all(
+            l["type"] != "global_avgpool" and not (ext & set(l)) for l in d["layers"])
+
+    @property
     def input_size(self) -> int:
         return int(np.prod(self.input_shape)) if self.input_shape else self.dims[0]
 

@@ -31,10 +31,11 @@ namespace kan {
 cudaError_t launch_gather_gemm(bool bf16, int nbp, int mode, const CUtensorMap& xmap,
                                const GemmParams& p, size_t smem, cudaStream_t st);
 size_t gemm_smem_bytes(bool bf16, int nbp, int BN, int SA, int SB, int SX, int x_kind,
-                       int tab_bytes);
+                       int tab_bytes, bool silu);
 int gemm_ips(bool bf16, int nbp);
 int gemm_gs(bool bf16, int nbp);
-int gemm_tmem_slots(int BN);
+int gemm_tmem_slots(int BN, int nacc);
+int gemm_tmem_accs(int BN, int splits);
 cudaError_t launch_levels(const float* x, int64_t n, const float* thr, float lo, float inv_step,
                           int L, uint16_t* out, cudaStream_t st);
 cudaError_t launch_argmax(const float* logits, int64_t M, int N, int ld, int32_t* out,
@@ -209,8 +210,12 @@ struct kan_engine {
   Lattice lat;
   std::vector<PreparedLayer> prep;
   DevBuf<float> d_thr;
-  DevBuf<uint8_t> d_tab;  // smem table blob (see GemmParams::tab)
-  int tab_bytes = 0, off_thr = 0, off_silu = 0;
+  // smem table blobs (see GemmParams::tab): [0] shared tables, [1] lane-
+  // private copies (NBP = 8 only; used where shared memory allows)
+  struct TabSet {
+    DevBuf<uint8_t> buf;
+    int bytes = 0, off_thr = 0, off_silu = 0, off_c64 = 0;
+  } tabs[2];
   double s_s = 1.0;
   int64_t z_s = 0;
   // workspaces: activation buffer slot of each layer's stored output (-1:
@@ -226,6 +231,7 @@ struct kan_engine {
   // optional per-CTA phase timestamps of each layer's last launch (tuning aid)
   bool timeline = false;
   int dbg_flags = 0;  // KAN_DBG_FLAGS (tuning experiments only)
+  int force_tab = -1;  // KAN_TABLES=0/1 forces the table variant (tuning only)
   std::vector<DevBuf<unsigned long long>> timeline_buf;
   std::vector<int64_t> timeline_ctas;
   // per-layer kernel timing (kan_engine_set_profiling)
@@ -829,25 +835,52 @@ void configure(kan_engine* e, const kan_config* c) {
         codes[static_cast<size_t>(a)] = static_cast<uint8_t>(quantize(v[static_cast<size_t>(a)], sq));
     }
     // smem table blob: vals[frac] (packed LUT codes per in-interval offset),
-    // then the exact level thresholds, then the SiLU codes
-    std::vector<uint8_t> blob;
+    // then the exact level thresholds, then the SiLU codes, then (NBP = 8)
+    // the per-level 8-byte code rows
     auto a16 = [](size_t n) { return (n + 15) / 16 * 16; };
     const size_t nfrac = size_t{1} << cfg.lut_k;
-    blob.assign(a16(nfrac * 4), 0);
-    for (size_t f = 0; f < nfrac; ++f) {
-      const uint32_t v = lut_pack(g, cfg.lut_k, e->lut, static_cast<int64_t>(f));  // jj = 0
-      std::memcpy(&blob[f * 4], &v, 4);
+    std::vector<uint32_t> vals(nfrac);
+    for (size_t f = 0; f < nfrac; ++f)
+      vals[f] = lut_pack(g, cfg.lut_k, e->lut, static_cast<int64_t>(f));  // jj = 0
+    for (int variant = 0; variant < 2; ++variant) {
+      auto& ts = e->tabs[variant];
+      if (variant == 1 && g.nb() > 8) {
+        ts.bytes = 0;
+        continue;
+      }
+      const size_t rep = variant == 1 ? 32 : 1;  // copies, interleaved by lane
+      std::vector<uint8_t> blob(a16(nfrac * 4 * rep), 0);
+      for (size_t f = 0; f < nfrac; ++f)
+        for (size_t l = 0; l < rep; ++l) std::memcpy(&blob[(f * rep + l) * 4], &vals[f], 4);
+      ts.off_thr = static_cast<int>(blob.size());
+      blob.resize(a16(blob.size() + thr.size() * 4), 0);
+      std::memcpy(&blob[static_cast<size_t>(ts.off_thr)], thr.data(), thr.size() * 4);
+      ts.off_silu = static_cast<int>(blob.size());
+      if (!codes.empty()) {
+        if (variant == 0) {
+          blob.insert(blob.end(), codes.begin(), codes.end());
+        } else {  // 4 codes per word, word w of lane l at (w*32 + l)*4
+          const size_t words = (codes.size() + 3) / 4;
+          blob.resize(blob.size() + words * 32 * 4, 0);
+          for (size_t a = 0; a < codes.size(); ++a)
+            for (size_t l = 0; l < 32; ++l)
+              blob[static_cast<size_t>(ts.off_silu) + ((a / 4) * 32 + l) * 4 + (a % 4)] = codes[a];
+        }
+        blob.resize(a16(blob.size()), 0);
+      }
+      ts.off_c64 = static_cast<int>(blob.size());
+      if (variant == 0 && g.nb() <= 8) {  // NBP = 8: one 8-byte code row per level
+        blob.resize(blob.size() + static_cast<size_t>(L + 1) * 8, 0);
+        for (int64_t a = 0; a <= L; ++a) {
+          const uint64_t v = static_cast<uint64_t>(lut_pack(g, cfg.lut_k, e->lut, a)) << (8 * (a >> cfg.lut_k));
+          std::memcpy(&blob[static_cast<size_t>(ts.off_c64) + static_cast<size_t>(a) * 8], &v, 8);
+        }
+        blob.resize(a16(blob.size()), 0);  // cp.async.bulk sizes are multiples of 16 bytes
+      }
+      if (blob.size() % 16 != 0) throw LogicError("table blob must be a multiple of 16 bytes");
+      ts.bytes = static_cast<int>(blob.size());
+      ts.buf.upload(blob);
     }
-    e->off_thr = static_cast<int>(blob.size());
-    blob.resize(a16(blob.size() + thr.size() * 4), 0);
-    std::memcpy(&blob[static_cast<size_t>(e->off_thr)], thr.data(), thr.size() * 4);
-    e->off_silu = static_cast<int>(blob.size());
-    if (!codes.empty()) {
-      blob.insert(blob.end(), codes.begin(), codes.end());
-      blob.resize(a16(blob.size()), 0);
-    }
-    e->tab_bytes = static_cast<int>(blob.size());
-    e->d_tab.upload(blob);
     if (cfg.w_scheme == KAN_W_PER_TENSOR_ASYM && (cfg.bits_w < 1 || cfg.bits_w > 8))
       throw InvalidArgument("compute_quant_params: bits must be in [1,8] or 32");
   } else {
@@ -858,6 +891,7 @@ void configure(kan_engine* e, const kan_config* c) {
   e->prep.resize(static_cast<size_t>(e->n_kan));
   e->timeline = std::getenv("KAN_TIMELINE") != nullptr;
   e->dbg_flags = std::getenv("KAN_DBG_FLAGS") ? std::atoi(std::getenv("KAN_DBG_FLAGS")) : 0;
+  e->force_tab = std::getenv("KAN_TABLES") ? std::atoi(std::getenv("KAN_TABLES")) : -1;
   e->timeline_buf.clear();
   e->timeline_buf.resize(static_cast<size_t>(e->n_kan));
   e->timeline_ctas.assign(static_cast<size_t>(e->n_kan), 0);
@@ -881,15 +915,16 @@ void configure(kan_engine* e, const kan_config* c) {
 // Ring depths for the smem budget: the A ring only decouples producers from
 // the MMA (2 slots); the weight and activation rings hide L2 / HBM latency, so
 // they get equal depth first and the activation ring takes what is left.
-void pick_stages(bool bf16, int nbp, int BN, int x_kind, int tab_bytes, int& SA, int& SB, int& SX) {
+void pick_stages(bool bf16, int nbp, int BN, int x_kind, int tab_bytes, bool silu, int nacc, int& SA,
+                 int& SB, int& SX) {
   const size_t budget = 232448;
-  SA = gemm_tmem_slots(BN);  // the A ring lives in TMEM
+  SA = gemm_tmem_slots(BN, nacc);  // the A ring lives in TMEM
   for (SB = 12; SB >= 2; --SB)
-    if (gemm_smem_bytes(bf16, nbp, BN, SA, SB, SB, x_kind, tab_bytes) <= budget) break;
+    if (gemm_smem_bytes(bf16, nbp, BN, SA, SB, SB, x_kind, tab_bytes, silu) <= budget) break;
   if (SB < 2) throw Unsupported("tile configuration exceeds shared memory");
   for (SX = 24; SX > SB; --SX)
-    if (gemm_smem_bytes(bf16, nbp, BN, SA, SB, SX, x_kind, tab_bytes) <= budget) break;
-  if (gemm_smem_bytes(bf16, nbp, BN, SA, SB, SX, x_kind, tab_bytes) > budget) SX = SB;
+    if (gemm_smem_bytes(bf16, nbp, BN, SA, SB, SX, x_kind, tab_bytes, silu) <= budget) break;
+  if (gemm_smem_bytes(bf16, nbp, BN, SA, SB, SX, x_kind, tab_bytes, silu) > budget) SX = SB;
 }
 
 struct LayerIO {
@@ -972,10 +1007,6 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
   p.x_kind = io.x_kind;
   p.L = bf16 ? 0 : static_cast<int>(e->lat.L);
   p.k = e->lat.k;
-  p.tab = e->d_tab.p;
-  p.tab_bytes = e->tab_bytes;
-  p.off_thr = e->off_thr;
-  p.off_silu = e->off_silu;
   p.lo_f = bf16 ? 0.f : static_cast<float>(-e->grid.lo / e->lat.step);
   p.inv_step_f = bf16 ? 0.f : static_cast<float>(1.0 / e->lat.step);
   p.flo = static_cast<float>(e->grid.lo);
@@ -988,12 +1019,25 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
   p.m_tiles = static_cast<int>((M + 127) / 128);
   p.dbg = nullptr;
   p.dbg_flags = e->dbg_flags;
-  const int tb = bf16 ? 0 : e->tab_bytes;
+  // table variant: the lane-private copies when they leave deep enough rings
   int SA = 2, SB = 2, SX = 2;
-  pick_stages(bf16, pl.nbp, pl.BN, io.x_kind, tb, SA, SB, SX);
-  p.SA = SA;
-  p.SB = SB;
-  p.SX = SX;
+  int variant = 0;
+  if (!bf16 && e->tabs[1].bytes > 0) {
+    try {
+      pick_stages(bf16, pl.nbp, pl.BN, io.x_kind, e->tabs[1].bytes, pl.silu != 0, 1, SA, SB, SX);
+      if (SB >= 3 && SX >= 4 && e->force_tab != 0) variant = 1;
+    } catch (const Unsupported&) {
+    }
+  }
+  const auto& ts = e->tabs[variant];
+  const int tb = bf16 ? 0 : ts.bytes;
+  pick_stages(bf16, pl.nbp, pl.BN, io.x_kind, tb, pl.silu != 0, 1, SA, SB, SX);
+  p.tab = ts.buf.p;
+  p.tab_bytes = ts.bytes;
+  p.off_thr = ts.off_thr;
+  p.off_silu = ts.off_silu;
+  p.off_c64 = ts.off_c64;
+  p.rep = variant;
   // split-K over a cluster (2, 4 or 8 CTAs along z) when the tile grid
   // under-fills the 148 SMs; the partial tiles are summed through DSMEM, so
   // they must fit in the idle A/B rings.
@@ -1012,6 +1056,12 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
   const int gps = (pl.n_groups + splits - 1) / splits;
   p.splits = splits;
   p.groups_per_split = gps;
+  // persistent launches double-buffer the accumulator when TMEM allows
+  p.nacc = gemm_tmem_accs(pl.BN, splits);
+  SA = gemm_tmem_slots(pl.BN, p.nacc);
+  p.SA = SA;
+  p.SB = SB;
+  p.SX = SX;
   if (e->timeline) {
     const size_t n = static_cast<size_t>(splits) * p.m_tiles * p.n_tiles_n * 8;
     auto& buf = e->timeline_buf[static_cast<size_t>(pl.layer_index)];
@@ -1075,7 +1125,7 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
   } else {
     xmap = make_xmap(io.x, io.x_kind, M, pl.n_in, io.ld_x, pl.IPS);
   }
-  const size_t smem = gemm_smem_bytes(bf16, pl.nbp, pl.BN, SA, SB, SX, io.x_kind, tb);
+  const size_t smem = gemm_smem_bytes(bf16, pl.nbp, pl.BN, SA, SB, SX, io.x_kind, tb, pl.silu != 0);
   // kernel variant: 0 plain, 1 per-tensor zero point (reference scheme), 2 SiLU base
   const int mode = pl.silu ? 2 : ((!bf16 && pl.wscheme == KAN_W_PER_TENSOR_ASYM) ? 1 : 0);
   ck(launch_gather_gemm(bf16, pl.nbp, mode, xmap, p, smem, st), "gather_gemm launch");

@@ -289,58 +289,81 @@ __device__ __forceinline__ int lattice_level_x(float x, const GemmParams& p, con
   return g;
 }
 
-// 64 bytes of one A row (this thread's K-quarter of a stage) on the LUT path.
-// The P+1 codes of lut_basis_lookup depend only on frac = a mod 2^k
-// (lut.hpp:145-157): vals[frac] holds them packed, and an input's NBP-byte
-// row segment is vals[frac] shifted to byte jj = a >> k (branch-free: clamped
-// funnel shifts give zero for words the codes do not reach).
+// 64 bytes of one A row (this thread's K-quarter of a stage) on the LUT path,
+// plus the stage's SiLU code words.  The P+1 codes of lut_basis_lookup
+// (lut.hpp:136-160) placed at byte jj = a >> k of the input's NBP-byte row
+// segment: for NBP = 8 one 64-bit entry per level (c64[a], built on the host
+// from the same lookup); for NBP = 16 vals[frac] (frac = a mod 2^k) shifted
+// into place with clamped funnel shifts (branch-free).
 template <int NBP, int MODE>
 __device__ __forceinline__ void lut_row(const GemmParams& p, const uint32_t* vals,
-                                        const uint8_t* silu_tab, const int (&a)[64 / NBP],
-                                        int i0, uint32_t (&w)[16], uint32_t& rsum,
-                                        uint32_t (&sil)[16]) {
+                                        const uint2* c64, const uint8_t* silu_tab,
+                                        const int (&a)[64 / NBP], int i0, uint32_t (&w)[16],
+                                        uint32_t& rsum, uint32_t (&nw)[16 / NBP]) {
   constexpr int H = 64 / NBP;  // inputs in this thread's quarter
   const int mask = (1 << p.k) - 1;
+  const uint32_t lane = threadIdx.x & 31;
 #pragma unroll
   for (int e = 0; e < H; ++e) {
-    const uint32_t v = vals[a[e] & mask];
-    const int jj = a[e] >> p.k;
     if constexpr (NBP == 8) {
-      const unsigned long long pt = static_cast<unsigned long long>(v) << (8 * jj);
-      w[2 * e] = static_cast<uint32_t>(pt);
-      w[2 * e + 1] = static_cast<uint32_t>(pt >> 32);
+      if (p.rep) {
+        // lane-private copy of vals: conflict-free
+        const uint32_t v = vals[((static_cast<uint32_t>(a[e]) & mask) << 5) | lane];
+        const unsigned long long pt = static_cast<unsigned long long>(v) << (8 * (a[e] >> p.k));
+        w[2 * e] = static_cast<uint32_t>(pt);
+        w[2 * e + 1] = static_cast<uint32_t>(pt >> 32);
+        if constexpr (MODE == MODE_ZP) {
+          // codes shifted past the row end are zero (see lut_basis_lookup)
+          if (i0 + e < p.n_ch) rsum = __dp4a(v, 0x01010101u, rsum);
+        }
+      } else {
+        const uint2 c = c64[a[e]];
+        w[2 * e] = c.x;
+        w[2 * e + 1] = c.y;
+        if constexpr (MODE == MODE_ZP) {
+          if (i0 + e < p.n_ch) rsum = __dp4a(c.y, 0x01010101u, __dp4a(c.x, 0x01010101u, rsum));
+        }
+      }
     } else {
-      const uint32_t sft = 8u * static_cast<uint32_t>(jj);
+      const uint32_t v = vals[a[e] & mask];
+      const uint32_t sft = 8u * static_cast<uint32_t>(a[e] >> p.k);
       w[4 * e] = __funnelshift_lc(0u, v, sft);
 #pragma unroll
       for (uint32_t q = 1; q < 4; ++q)
         w[4 * e + q] = __funnelshift_lc(0u, v, sft - 32u * q) | __funnelshift_rc(v, 0u, 32u * q - sft);
-    }
-    if constexpr (MODE == MODE_ZP) {
-      // codes shifted past the row end are zero (see lut_basis_lookup)
-      if (i0 + e < p.n_ch) rsum = __dp4a(v, 0x01010101u, rsum);
+      if constexpr (MODE == MODE_ZP) {
+        if (i0 + e < p.n_ch) rsum = __dp4a(v, 0x01010101u, rsum);
+      }
     }
   }
   if constexpr (MODE == MODE_SILU) {
-    // append this stage's H SiLU codes (H bytes) to the 64-byte shift register
-    uint32_t nw[H / 4];
+    if (NBP == 8 && p.rep) {
+      // lane-private packed codes: word (a >> 2) of this lane, byte a & 3
+      const uint32_t* srep = reinterpret_cast<const uint32_t*>(silu_tab);
 #pragma unroll
-    for (int q = 0; q < H / 4; ++q)
-      nw[q] = static_cast<uint32_t>(silu_tab[a[4 * q]]) |
-              (static_cast<uint32_t>(silu_tab[a[4 * q + 1]]) << 8) |
-              (static_cast<uint32_t>(silu_tab[a[4 * q + 2]]) << 16) |
-              (static_cast<uint32_t>(silu_tab[a[4 * q + 3]]) << 24);
+      for (int q = 0; q < H / 4; ++q) {
+        uint32_t wd[4];
 #pragma unroll
-    for (int q = 0; q < 16 - H / 4; ++q) sil[q] = sil[q + H / 4];
+        for (int t = 0; t < 4; ++t) wd[t] = srep[((static_cast<uint32_t>(a[4 * q + t]) >> 2) << 5) | lane];
+        const uint32_t lo = __byte_perm(wd[0], wd[1], (a[4 * q] & 3) | ((4 + (a[4 * q + 1] & 3)) << 4));
+        const uint32_t hi = __byte_perm(wd[2], wd[3], (a[4 * q + 2] & 3) | ((4 + (a[4 * q + 3] & 3)) << 4));
+        nw[q] = __byte_perm(lo, hi, 0x5410);
+      }
+    } else {
 #pragma unroll
-    for (int q = 0; q < H / 4; ++q) sil[16 - H / 4 + q] = nw[q];
+      for (int q = 0; q < H / 4; ++q)
+        nw[q] = static_cast<uint32_t>(silu_tab[a[4 * q]]) |
+                (static_cast<uint32_t>(silu_tab[a[4 * q + 1]]) << 8) |
+                (static_cast<uint32_t>(silu_tab[a[4 * q + 2]]) << 16) |
+                (static_cast<uint32_t>(silu_tab[a[4 * q + 3]]) << 24);
+    }
   }
 }
 
 // 64 bytes of one A row on the bf16 path: fp32 Cox-de Boor basis -> bf16.
 template <int NBP, int MODE>
 __device__ __forceinline__ void bf16_row(const GemmParams& p, const float (&x)[32 / NBP],
-                                         uint32_t (&w)[16], uint32_t (&sil)[16]) {
+                                         uint32_t (&w)[16], uint32_t (&nw)[16 / NBP]) {
   constexpr int H = 32 / NBP;  // inputs in this thread's quarter (bf16: NBP*2 bytes each)
   constexpr int PMAX = 3;
 #pragma unroll
@@ -362,7 +385,6 @@ __device__ __forceinline__ void bf16_row(const GemmParams& p, const float (&x)[3
     }
   }
   if constexpr (MODE == MODE_SILU) {
-    uint32_t nw[H / 2];
 #pragma unroll
     for (int q = 0; q < H / 2; ++q) {
       float s2[2];
@@ -373,10 +395,6 @@ __device__ __forceinline__ void bf16_row(const GemmParams& p, const float (&x)[3
       }
       nw[q] = pack_bf16(s2[0], s2[1]);
     }
-#pragma unroll
-    for (int q = 0; q < 16 - H / 2; ++q) sil[q] = sil[q + H / 2];
-#pragma unroll
-    for (int q = 0; q < H / 2; ++q) sil[16 - H / 2 + q] = nw[q];
   }
 }
 
@@ -408,6 +426,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     kan_gather_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const GemmParams p) {
   using C = Cfg<BF16, NBP>;
   constexpr int NPW = GEMM_PRODUCER_WARPS, NP = 32 * NPW;
+  constexpr int W_X = NPW, W_MMA = NPW + 1, W_B = NPW + 2, W_EPI = NPW + 3;  // + 4 epilogue warps
   constexpr bool SILU = (MODE == MODE_SILU);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -423,32 +442,49 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   uint8_t* sT = sX + static_cast<size_t>(SX) * x_bytes;  // lattice tables (LUT path)
   const int tab_bytes = BF16 ? 0 : p.tab_bytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sT + tab_bytes);
-  int32_t* s_rowsum = reinterpret_cast<int32_t*>(bars + 2 * SA + 2 * SB + 2 * SX + 2);
-  double* s_cols = reinterpret_cast<double*>(s_rowsum + 128);  // [2][BN]: scale, correction
-  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(s_cols + 2 * BN);
+  int32_t* s_rowsum = reinterpret_cast<int32_t*>(bars + 2 * SA + 2 * SB + 2 * SX + 9);  // [2][4][128]
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(s_rowsum + 2 * 4 * 128);
+  // SiLU code staging (MODE_SILU): word wd of K-quarter h of row r at
+  // ((h*8 + wd/2)*128 + r)*2 + (wd&1) -- written once per spline stage, read
+  // back by the same thread for the group's base stage (conflict-free).
+  // Offset arithmetic from smem keeps the compiler on shared-memory accesses.
+  const uint32_t sil_off = ((static_cast<uint32_t>(reinterpret_cast<uint8_t*>(s_tmem + 4) - smem)) + 15u) & ~15u;
+  uint32_t* s_sil = reinterpret_cast<uint32_t*>(smem + sil_off);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  unsigned long long* dbg =
-      p.dbg ? p.dbg + 8 * ((static_cast<size_t>(blockIdx.z) * gridDim.y + blockIdx.y) * gridDim.x +
-                           blockIdx.x)
-            : nullptr;
+  unsigned long long* dbg = p.dbg ? p.dbg + 8 * (static_cast<size_t>(blockIdx.z) * gridDim.x + blockIdx.x)
+                                  : nullptr;
   auto stamp = [&](int i) {
     if (dbg) dbg[i] = globaltimer();
   };
   if (threadIdx.x == 0) stamp(0);
-  const int m_tile = blockIdx.y;
-  const int n_tile = blockIdx.x;
-  const int split = blockIdx.z;
-  const int m0 = m_tile * 128;
-  // conv tiles: first image and first output row of this M tile
-  const int n0 = p.conv ? (m_tile / p.tpi) * p.bn_img : 0;
-  const int y0 = p.conv ? (m_tile % p.tpi) * p.bh : 0;
 
-  const int g0 = split * p.groups_per_split;
-  const int g1 = min(p.n_groups, g0 + p.groups_per_split);
+  // Tiles: 1D index, N tile fastest (CTAs sharing an activation tile run
+  // together).  splits == 1: persistent, this CTA takes tiles blockIdx.x,
+  // blockIdx.x + gridDim.x, ...; splits > 1: one tile per CTA, K groups split
+  // over the cluster along z.
+  const bool persistent = p.splits == 1;
+  const int n_tiles = p.m_tiles * p.n_tiles_n;
+  const int tile_step = persistent ? static_cast<int>(gridDim.x) : n_tiles;
+  const int split = blockIdx.z;
+  const int g0 = persistent ? 0 : split * p.groups_per_split;
+  const int g1 = persistent ? p.n_groups : min(p.n_groups, g0 + p.groups_per_split);
   const bool has_work = g0 < g1;
   const int spg = C::GS + (SILU ? 1 : 0);
+  struct Tile {
+    int m0, n_tile, n0, y0;
+  };
+  auto tile_of = [&](int t) {
+    Tile r;
+    const int mt = t / p.n_tiles_n;
+    r.n_tile = t - mt * p.n_tiles_n;
+    r.m0 = mt * 128;
+    // conv tiles: first image and first output row of the M tile
+    r.n0 = p.conv ? (mt / p.tpi) * p.bn_img : 0;
+    r.y0 = p.conv ? (mt % p.tpi) * p.bh : 0;
+    return r;
+  };
 
   auto bar_xfull = [&](int s) { return smem_u32(bars + s); };
   auto bar_xempty = [&](int s) { return smem_u32(bars + SX + s); };
@@ -456,23 +492,23 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   auto bar_aempty = [&](int s) { return smem_u32(bars + 2 * SX + SA + s); };
   auto bar_bfull = [&](int s) { return smem_u32(bars + 2 * SX + 2 * SA + s); };
   auto bar_bempty = [&](int s) { return smem_u32(bars + 2 * SX + 2 * SA + SB + s); };
-  const uint32_t bar_tmem_full = smem_u32(bars + 2 * SX + 2 * SA + 2 * SB);
-  const uint32_t bar_tab = smem_u32(bars + 2 * SX + 2 * SA + 2 * SB + 1);
+  uint64_t* bx = bars + 2 * SX + 2 * SA + 2 * SB;
+  auto bar_accfull = [&](int b) { return smem_u32(bx + b); };
+  auto bar_accempty = [&](int b) { return smem_u32(bx + 2 + b); };
+  auto bar_rsfull = [&](int b) { return smem_u32(bx + 4 + b); };
+  auto bar_rsempty = [&](int b) { return smem_u32(bx + 6 + b); };
+  const uint32_t bar_tab = smem_u32(bx + 8);
 
-  // TMEM: accumulator in columns [0, BN), A ring slots of KSTAGE/4 columns from acol0
+  // TMEM: nacc accumulators of BNa columns (two when they fit, so the epilogue
+  // of one tile overlaps the next tile's MMAs), then the A ring of KSTAGE/4-
+  // column slots
   constexpr uint32_t tmem_cols = 512;
   constexpr uint32_t acols = KSTAGE / 4;
-  const uint32_t acol0 = static_cast<uint32_t>((BN + 31) / 32 * 32);
+  const uint32_t BNa = static_cast<uint32_t>((BN + 31) / 32 * 32);
+  const int nacc = p.nacc;
+  const uint32_t acol0 = static_cast<uint32_t>(nacc) * BNa;
 
   // ---- setup -------------------------------------------------------------
-  if (threadIdx.x < 128) s_rowsum[threadIdx.x] = 0;
-  if constexpr (!BF16 && MODE != MODE_ZP) {
-    for (int i = threadIdx.x; i < BN; i += blockDim.x) {
-      const int j = min(n_tile * BN + i, p.N - 1);
-      s_cols[i] = p.fs[j];
-      s_cols[BN + i] = SILU ? static_cast<double>(p.corr_b[j]) : 0.0;
-    }
-  }
   if (threadIdx.x == 0) {
     for (int s = 0; s < SX; ++s) {
       mbar_init(bar_xfull(s), 1);
@@ -486,229 +522,25 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       mbar_init(bar_bfull(s), 1);
       mbar_init(bar_bempty(s), 1);
     }
-    mbar_init(bar_tmem_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(bar_accfull(b), 1);
+      mbar_init(bar_accempty(b), 4);
+      mbar_init(bar_rsfull(b), NPW);
+      mbar_init(bar_rsempty(b), 4);
+    }
     mbar_init(bar_tab, 1);
     mbar_fence_init();
   }
-  if (warp == NPW && lane == 0) tma_prefetch(&xmap);
-  if (warp == NPW + 1) tmem_alloc(smem_u32(s_tmem), tmem_cols);
+  if (warp == W_X && lane == 0) tma_prefetch(&xmap);
+  if (warp == W_MMA) tmem_alloc(smem_u32(s_tmem), tmem_cols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *s_tmem;
 
-  // Role loops run on whole warps (all lanes wait, lane 0 issues) so the warps
-  // stay converged for the aligned barriers and tcgen05 ops that follow.
-  if (warp == NPW) {
-    // ========================= activation loader ==========================
-    Ring rx(SX);
-    TapWalk tw(p, g0 * C::GS);
-    for (int g = g0; g < g1; ++g) {
-      const int nsp = min(C::GS, p.n_spline_stages - g * C::GS);
-      for (int s = 0; s < nsp; ++s, rx.next(), tw.next(p)) {
-        mbar_wait(bar_xempty(rx.slot), rx.phase ^ 1);
-        if (lane == 0) {
-          const uint32_t dst = smem_u32(sX + static_cast<size_t>(rx.slot) * x_bytes);
-          mbar_arrive_tx(bar_xfull(rx.slot), x_bytes);
-          if (!p.conv) {
-            tma_load_2d(dst, &xmap, (g * C::GS + s) * C::IPS, m0, bar_xfull(rx.slot));
-          } else {
-            // the tap's input window: rows y0*stride + ky - pad.., columns kx - pad..
-            // (element strides in the tensor map step by the conv stride)
-            int iy = y0 * p.cstride + tw.ky - p.pad, ix = tw.kx - p.pad;
-            if (p.dbg_flags & 4) {  // tuning/debug only: never negative coordinates
-              iy = max(iy, 0);
-              ix = max(ix, 0);
-            }
-            tma_load_4d(dst, &xmap, tw.cc * C::IPS, ix, iy, n0, bar_xfull(rx.slot));
-          }
-        }
-        __syncwarp();
-      }
-    }
-  } else if (warp == NPW + 2) {
-    // ===================== table + weight-tile loader =====================
-    if (lane == 0 && tab_bytes > 0) {
-      mbar_arrive_tx(bar_tab, static_cast<uint32_t>(tab_bytes));
-      bulk_load(smem_u32(sT), p.tab, static_cast<uint32_t>(tab_bytes), bar_tab);
-    }
-    __syncwarp();
-    Ring rb(SB);
-    for (int g = g0; g < g1; ++g) {
-      const int nsp = min(C::GS, p.n_spline_stages - g * C::GS);
-      for (int s = 0; s < nsp + (SILU ? 1 : 0); ++s, rb.next()) {
-        mbar_wait(bar_bempty(rb.slot), rb.phase ^ 1);
-        if (lane == 0) {
-          const size_t tile = static_cast<size_t>(n_tile) * p.total_stages + g * spg + s;
-          mbar_arrive_tx(bar_bfull(rb.slot), b_bytes);
-          bulk_load(smem_u32(sB + static_cast<size_t>(rb.slot) * b_bytes), p.wt + tile * b_bytes,
-                    b_bytes, bar_bfull(rb.slot));
-        }
-        __syncwarp();
-      }
-    }
-  } else if (warp == NPW + 1) {
-    // ============================ MMA issuer ==============================
-    const uint32_t idesc = BF16 ? idesc_bf16(BN) : idesc_i8(BN, p.b_signed != 0);
-    const int nk = (p.dbg_flags & 2) ? 0 : KSTAGE / 32;
-    Ring ra(SA), rb(SB);
-    bool first = true;
-    for (int g = g0; g < g1; ++g) {
-      const int nsp = min(C::GS, p.n_spline_stages - g * C::GS);
-      for (int s = 0; s < nsp + (SILU ? 1 : 0); ++s, ra.next(), rb.next()) {
-        mbar_wait(bar_afull(ra.slot), ra.phase);
-        mbar_wait(bar_bfull(rb.slot), rb.phase);
-        tc_fence_after();
-        if (lane == 0) {
-          const uint32_t a_tmem = tmem + acol0 + acols * static_cast<uint32_t>(ra.slot);
-          const uint32_t b_addr = smem_u32(sB + static_cast<size_t>(rb.slot) * b_bytes);
-          for (int kk = 0; kk < nk; ++kk) {
-            // K step kk: SW128 block kk/4 of the stage's weight tile, 32 bytes in
-            const uint64_t bd = umma_desc_sw128(b_addr + (kk >> 2) * BN * 128 + 32 * (kk & 3));
-            const uint32_t acc = (first && kk == 0) ? 0u : 1u;
-            if (BF16)
-              mma_f16_ts(tmem, a_tmem + 8 * kk, bd, idesc, acc);
-            else
-              mma_i8_ts(tmem, a_tmem + 8 * kk, bd, idesc, acc);
-          }
-          tc_commit(bar_aempty(ra.slot));
-          tc_commit(bar_bempty(rb.slot));
-        }
-        __syncwarp();
-        first = false;
-      }
-    }
-    if (lane == 0) tc_commit(bar_tmem_full);
-    __syncwarp();
-  } else {
-    // ============================ producers ===============================
-    const int quarter = warp & 3;
-    const int h = warp >> 2;  // K-quarter of each stage this thread fills
-    const int r = quarter * 32 + lane;
-    const uint32_t t_lane = static_cast<uint32_t>(quarter * 32) << 16;
-    uint32_t sil[16];
-#pragma unroll
-    for (int q = 0; q < 16; ++q) sil[q] = 0;
-    uint32_t rsum = 0;
-    if (tab_bytes > 0) mbar_wait(bar_tab, 0);
-    if (threadIdx.x == 0) stamp(1);
-    const uint32_t* vals = reinterpret_cast<const uint32_t*>(sT);
-    const float* thr = reinterpret_cast<const float*>(sT + p.off_thr);
-    const uint8_t* silu_tab = sT + p.off_silu;
-    constexpr int H = C::Q;
-    const int xoff = h * H * static_cast<int>(xesz);  // this thread's bytes in the x row
-    // conv: this row's output pixel
-    int oy = 0, ox = 0;
-    if (p.conv) {
-      const int pix = r % p.pimg;
-      const int yy = pix / p.Wo;
-      oy = y0 + yy;
-      ox = pix - yy * p.Wo;
-    }
-    TapWalk tw(p, g0 * C::GS);
-
-    Ring ra(SA), rx(SX);
-    int idx = 0;
-    for (int g = g0; g < g1; ++g) {
-      const int nsp = min(C::GS, p.n_spline_stages - g * C::GS);
-      for (int s = 0; s < nsp + (SILU ? 1 : 0); ++s, ++idx, ra.next()) {
-        uint32_t w[16];
-        if (s < nsp) {
-          // 1. this thread's activations of the stage -> registers; free the slot
-          mbar_wait(bar_xfull(rx.slot), rx.phase);
-          const uint8_t* xt = sX + static_cast<size_t>(rx.slot) * x_bytes;
-          const int i0 = (p.conv ? tw.cc * C::IPS : (g * C::GS + s) * C::IPS) + h * H;
-          // padded conv taps read level(0.0) (layers.hpp:146-147 leaves them 0.0)
-          bool padtap = false;
-          if (p.conv) {
-            const int iy = oy * p.cstride + tw.ky - p.pad, ix = ox * p.cstride + tw.kx - p.pad;
-            padtap = static_cast<unsigned>(iy) >= static_cast<unsigned>(p.H) ||
-                     static_cast<unsigned>(ix) >= static_cast<unsigned>(p.W);
-          }
-          tw.next(p);
-          if constexpr (BF16) {
-            uint32_t xr[H];
-            load_x<4 * H>(xt, r, xoff, x_row_bytes, xr);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(bar_xempty(rx.slot));
-            rx.next();
-            float x[H];
-#pragma unroll
-            for (int e = 0; e < H; ++e) x[e] = __uint_as_float(xr[e]);
-            if (p.dbg_flags & 1) {
-#pragma unroll
-              for (int q = 0; q < 16; ++q) w[q] = 0;
-            } else {
-              bf16_row<NBP, MODE>(p, x, w, sil);
-            }
-          } else {
-            int a[H];
-            if (p.x_kind == X_F32) {
-              uint32_t xr[H];
-              load_x<4 * H>(xt, r, xoff, x_row_bytes, xr);
-              __syncwarp();
-              if (lane == 0) mbar_arrive(bar_xempty(rx.slot));
-#pragma unroll
-              for (int e = 0; e < H; ++e) a[e] = lattice_level_x(__uint_as_float(xr[e]), p, thr);
-            } else {
-              uint32_t xr[H / 2];
-              load_x<2 * H>(xt, r, xoff, x_row_bytes, xr);
-              __syncwarp();
-              if (lane == 0) mbar_arrive(bar_xempty(rx.slot));
-#pragma unroll
-              for (int q = 0; q < H / 2; ++q) {
-                a[2 * q] = padtap ? p.lvl0 : static_cast<int>(xr[q] & 0xFFFF);
-                a[2 * q + 1] = padtap ? p.lvl0 : static_cast<int>(xr[q] >> 16);
-              }
-            }
-            rx.next();
-            if (p.dbg_flags & 1) {
-#pragma unroll
-              for (int q = 0; q < 16; ++q) w[q] = 0;
-            } else {
-              lut_row<NBP, MODE>(p, vals, silu_tab, a, i0, w, rsum, sil);
-            }
-          }
-        } else {
-          // base (SiLU) stage: this thread's 64 bytes are its shift register,
-          // padded for the stages a short last group lacks
-          for (int t = nsp; t < C::GS; ++t) {
-#pragma unroll
-            for (int q = 0; q < 16 - C::SW; ++q) sil[q] = sil[q + C::SW];
-#pragma unroll
-            for (int q = 16 - C::SW; q < 16; ++q) sil[q] = 0;
-          }
-#pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            w[q] = sil[q];
-            sil[q] = 0;
-          }
-        }
-        // 2. the A slot must be free (its previous MMAs retired), then store
-        mbar_wait(bar_aempty(ra.slot), ra.phase ^ 1);
-        tc_fence_after();
-        tmem_st16(tmem + t_lane + acol0 + acols * static_cast<uint32_t>(ra.slot) + 16u * h, w);
-        tmem_wait_st();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(bar_afull(ra.slot));
-        if (threadIdx.x == 0 && idx == 0) stamp(2);
-      }
-    }
-    if (threadIdx.x == 0) stamp(3);
-    if constexpr (MODE == MODE_ZP) atomicAdd(&s_rowsum[r], static_cast<int>(rsum));
-    asm volatile("bar.sync 1, %0;" ::"r"(NP) : "memory");
-  }
-
-  // ============================ epilogue ==================================
-  // The epilogue runs once per CTA out of a cold instruction cache, so it
-  // works on 4-column groups in rolled loops to keep its code small.
-  const int wq = warp & 3;
-  const int wh = warp >> 2;
-  const int rloc = wq * 32 + lane;
-  const uint32_t t_row = tmem + (static_cast<uint32_t>(wq * 32) << 16);
-  const int ngroups = BN / 4;
-
+  // Epilogue of 4 accumulator columns of one output row (fp64, then the
+  // requested output: raw, fp32, next-layer level, int8), shared by the
+  // persistent epilogue warps and the split-K reduction.
   auto finish4 = [&](int row, int col0, const uint32_t(&ra)[4], int32_t rs) {
     if (row >= p.M) return;
     const size_t base = static_cast<size_t>(row) * p.ld_out + col0;
@@ -723,7 +555,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     double y[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const int jl = col0 - n_tile * BN + e;  // column within this CTA's tile
+      const int j = min(col0 + e, p.N - 1);
       if constexpr (BF16) {
         y[e] = static_cast<double>(__uint_as_float(ra[e]));
       } else if constexpr (MODE == MODE_ZP) {
@@ -731,9 +563,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             static_cast<long long>(static_cast<int32_t>(ra[e])) - p.z_w * static_cast<long long>(rs);
         y[e] = __dmul_rn(static_cast<double>(v), p.f_tensor);
       } else {
-        const long long v = static_cast<long long>(static_cast<int32_t>(ra[e])) -
-                            static_cast<long long>(s_cols[BN + jl]);
-        y[e] = __dmul_rn(static_cast<double>(v), s_cols[jl]);
+        const long long v = static_cast<long long>(static_cast<int32_t>(ra[e])) - (SILU ? p.corr_b[j] : 0ll);
+        y[e] = __dmul_rn(static_cast<double>(v), p.fs[j]);
       }
     }
     if (p.res_kind) {
@@ -776,46 +607,311 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         if (e < nvalid) o[e] = static_cast<int8_t>(requant_i8(y[e], p.out_scale, p.inv_out_scale));
     }
   };
-
-  if (p.splits == 1) {
-    if (warp < NPW) {
-      mbar_wait(bar_tmem_full, 0);
-      tc_fence_after();
-      if (threadIdx.x == 0) stamp(4);
-      const int32_t rowsum = s_rowsum[rloc];
-#pragma unroll 1
-      for (int gq = wh; gq < ngroups; gq += NPW / 4) {
-        uint32_t ra[4];
-        tmem_ld4(t_row + gq * 4, ra);
-        tmem_wait_ld();
-        finish4(m0 + rloc, n_tile * BN + gq * 4, ra, rowsum);
+  // Role loops run on whole warps (all lanes wait, lane 0 issues) so the warps
+  // stay converged for the aligned barriers and tcgen05 ops that follow.
+  if (warp == W_X) {
+    // ========================= activation loader ==========================
+    Ring rx(SX);
+    for (int t = blockIdx.x; t < n_tiles; t += tile_step) {
+      const Tile tl = tile_of(t);
+      TapWalk tw(p, g0 * C::GS);
+      for (int g = g0; g < g1; ++g) {
+        const int nsp = min(C::GS, p.n_spline_stages - g * C::GS);
+        for (int s = 0; s < nsp; ++s, rx.next(), tw.next(p)) {
+          mbar_wait(bar_xempty(rx.slot), rx.phase ^ 1);
+          if (lane == 0) {
+            const uint32_t dst = smem_u32(sX + static_cast<size_t>(rx.slot) * x_bytes);
+            mbar_arrive_tx(bar_xfull(rx.slot), x_bytes);
+            if (!p.conv) {
+              tma_load_2d(dst, &xmap, (g * C::GS + s) * C::IPS, tl.m0, bar_xfull(rx.slot));
+            } else {
+              // the tap's input window: rows y0*stride + ky - pad.., columns kx - pad..
+              // (element strides in the tensor map step by the conv stride)
+              const int iy = tl.y0 * p.cstride + tw.ky - p.pad, ix = tw.kx - p.pad;
+              tma_load_4d(dst, &xmap, tw.cc * C::IPS, ix, iy, tl.n0, bar_xfull(rx.slot));
+            }
+          }
+          __syncwarp();
+        }
       }
     }
-  } else {
-    // split-K across the cluster: dump the partial accumulators into this
-    // CTA's smem (the B/x rings are idle now), then every CTA reduces a slice
-    // of rows over all peers through distributed shared memory.
-    const int rstride = BN + 4;  // words per row (+4 breaks bank conflicts)
-    uint32_t* red = reinterpret_cast<uint32_t*>(sB);
-    if (warp < NPW) {
+  } else if (warp == W_B) {
+    // ===================== table + weight-tile loader =====================
+    if (lane == 0 && tab_bytes > 0) {
+      mbar_arrive_tx(bar_tab, static_cast<uint32_t>(tab_bytes));
+      bulk_load(smem_u32(sT), p.tab, static_cast<uint32_t>(tab_bytes), bar_tab);
+    }
+    __syncwarp();
+    Ring rb(SB);
+    for (int t = blockIdx.x; t < n_tiles; t += tile_step) {
+      const Tile tl = tile_of(t);
+      for (int g = g0; g < g1; ++g) {
+        const int nsp = min(C::GS, p.n_spline_stages - g * C::GS);
+        for (int s = 0; s < nsp + (SILU ? 1 : 0); ++s, rb.next()) {
+          mbar_wait(bar_bempty(rb.slot), rb.phase ^ 1);
+          if (lane == 0) {
+            const size_t wt = static_cast<size_t>(tl.n_tile) * p.total_stages + g * spg + s;
+            mbar_arrive_tx(bar_bfull(rb.slot), b_bytes);
+            bulk_load(smem_u32(sB + static_cast<size_t>(rb.slot) * b_bytes), p.wt + wt * b_bytes,
+                      b_bytes, bar_bfull(rb.slot));
+          }
+          __syncwarp();
+        }
+      }
+    }
+  } else if (warp == W_MMA) {
+    // ============================ MMA issuer ==============================
+    const uint32_t idesc = BF16 ? idesc_bf16(BN) : idesc_i8(BN, p.b_signed != 0);
+    const int nk = (p.dbg_flags & 2) ? 0 : KSTAGE / 32;
+    Ring ra(SA), rb(SB);
+    int lt = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += tile_step, ++lt) {
+      const int ab = nacc == 2 ? (lt & 1) : 0;
+      const int use = nacc == 2 ? (lt >> 1) : lt;
+      // the accumulator must have been drained by the epilogue of its last tile
+      mbar_wait(bar_accempty(ab), (use & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t dacc = tmem + static_cast<uint32_t>(ab) * BNa;
+      bool first = true;
+      for (int g = g0; g < g1; ++g) {
+        const int nsp = min(C::GS, p.n_spline_stages - g * C::GS);
+        for (int s = 0; s < nsp + (SILU ? 1 : 0); ++s, ra.next(), rb.next()) {
+          mbar_wait(bar_afull(ra.slot), ra.phase);
+          mbar_wait(bar_bfull(rb.slot), rb.phase);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t a_tmem = tmem + acol0 + acols * static_cast<uint32_t>(ra.slot);
+            const uint32_t b_addr = smem_u32(sB + static_cast<size_t>(rb.slot) * b_bytes);
+            for (int kk = 0; kk < nk; ++kk) {
+              // K step kk: SW128 block kk/4 of the stage's weight tile, 32 bytes in
+              const uint64_t bd = umma_desc_sw128(b_addr + (kk >> 2) * BN * 128 + 32 * (kk & 3));
+              const uint32_t acc = (first && kk == 0) ? 0u : 1u;
+              if (BF16)
+                mma_f16_ts(dacc, a_tmem + 8 * kk, bd, idesc, acc);
+              else
+                mma_i8_ts(dacc, a_tmem + 8 * kk, bd, idesc, acc);
+            }
+            tc_commit(bar_aempty(ra.slot));
+            tc_commit(bar_bempty(rb.slot));
+          }
+          __syncwarp();
+          first = false;
+        }
+      }
+      if (lane == 0) tc_commit(bar_accfull(ab));
+      __syncwarp();
+    }
+  } else if (warp < NPW) {
+    // ============================ producers ===============================
+    const int quarter = warp & 3;
+    const int h = warp >> 2;  // K-quarter of each stage this thread fills
+    const int r = quarter * 32 + lane;
+    const uint32_t t_lane = static_cast<uint32_t>(quarter * 32) << 16;
+    if (tab_bytes > 0) mbar_wait(bar_tab, 0);
+    if (threadIdx.x == 0) stamp(1);
+    const uint32_t* vals = reinterpret_cast<const uint32_t*>(sT);
+    const float* thr = reinterpret_cast<const float*>(sT + p.off_thr);
+    const uint8_t* silu_tab = sT + p.off_silu;
+    const uint2* c64 = reinterpret_cast<const uint2*>(sT + p.off_c64);
+    constexpr int H = C::Q;
+    const int xoff = h * H * static_cast<int>(xesz);  // this thread's bytes in the x row
+    uint32_t* sil_row = s_sil + (h * 8 * 128 + r) * 2;  // + wp*256 words: word pair wp
+    // conv: this row's position within its M tile
+    int yy = 0, ox = 0;
+    if (p.conv) {
+      const int pix = r % p.pimg;
+      yy = pix / p.Wo;
+      ox = pix - yy * p.Wo;
+    }
+    Ring ra(SA), rx(SX);
+    int idx = 0, lt = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += tile_step, ++lt) {
+      const Tile tl = tile_of(t);
+      const int oy = tl.y0 + yy;
+      TapWalk tw(p, g0 * C::GS);
+      uint32_t rsum = 0;
+      for (int g = g0; g < g1; ++g) {
+        const int nsp = min(C::GS, p.n_spline_stages - g * C::GS);
+        for (int s = 0; s < nsp + (SILU ? 1 : 0); ++s, ++idx, ra.next()) {
+          uint32_t w[16];
+          if (s < nsp) {
+            // 1. this thread's activations of the stage -> registers; free the slot
+            mbar_wait(bar_xfull(rx.slot), rx.phase);
+            const uint8_t* xt = sX + static_cast<size_t>(rx.slot) * x_bytes;
+            const int i0 = (p.conv ? tw.cc * C::IPS : (g * C::GS + s) * C::IPS) + h * H;
+            // padded conv taps read level(0.0) (layers.hpp:146-147 leaves them 0.0)
+            bool padtap = false;
+            if (p.conv) {
+              const int iy = oy * p.cstride + tw.ky - p.pad, ix = ox * p.cstride + tw.kx - p.pad;
+              padtap = static_cast<unsigned>(iy) >= static_cast<unsigned>(p.H) ||
+                       static_cast<unsigned>(ix) >= static_cast<unsigned>(p.W);
+            }
+            tw.next(p);
+            uint32_t nw[C::SW];
+            if constexpr (BF16) {
+              uint32_t xr[H];
+              load_x<4 * H>(xt, r, xoff, x_row_bytes, xr);
+              __syncwarp();
+              if (lane == 0) mbar_arrive(bar_xempty(rx.slot));
+              rx.next();
+              float x[H];
+#pragma unroll
+              for (int e = 0; e < H; ++e) x[e] = __uint_as_float(xr[e]);
+              bf16_row<NBP, MODE>(p, x, w, nw);
+            } else {
+              int a[H];
+              if (p.x_kind == X_F32) {
+                uint32_t xr[H];
+                load_x<4 * H>(xt, r, xoff, x_row_bytes, xr);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(bar_xempty(rx.slot));
+#pragma unroll
+                for (int e = 0; e < H; ++e) a[e] = lattice_level_x(__uint_as_float(xr[e]), p, thr);
+              } else {
+                uint32_t xr[H / 2];
+                load_x<2 * H>(xt, r, xoff, x_row_bytes, xr);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(bar_xempty(rx.slot));
+#pragma unroll
+                for (int q = 0; q < H / 2; ++q) {
+                  a[2 * q] = padtap ? p.lvl0 : static_cast<int>(xr[q] & 0xFFFF);
+                  a[2 * q + 1] = padtap ? p.lvl0 : static_cast<int>(xr[q] >> 16);
+                }
+              }
+              rx.next();
+              lut_row<NBP, MODE>(p, vals, c64, silu_tab, a, i0, w, rsum, nw);
+            }
+            if constexpr (SILU) {
+              // stage s's SiLU words are words s*SW.. of this thread's 64-byte base row
+              if constexpr (C::SW == 2) {
+                *reinterpret_cast<uint2*>(sil_row + s * 256) = make_uint2(nw[0], nw[1]);
+              } else {
+                sil_row[(s >> 1) * 256 + (s & 1)] = nw[0];
+              }
+            }
+          } else {
+            // base (SiLU) stage: this thread's 64 bytes of codes staged above;
+            // words of stages a short last group lacks are zeroed (stale bf16
+            // words could be NaN, and NaN * 0 is not 0)
+            const int valid = nsp * C::SW;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const uint2 v = *reinterpret_cast<const uint2*>(sil_row + q * 256);
+              w[2 * q] = 2 * q < valid ? v.x : 0u;
+              w[2 * q + 1] = 2 * q + 1 < valid ? v.y : 0u;
+            }
+          }
+          // 2. the A slot must be free (its previous MMAs retired), then store
+          mbar_wait(bar_aempty(ra.slot), ra.phase ^ 1);
+          tc_fence_after();
+          tmem_st16(tmem + t_lane + acol0 + acols * static_cast<uint32_t>(ra.slot) + 16u * h, w);
+          tmem_wait_st();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(bar_afull(ra.slot));
+          if (threadIdx.x == 0 && idx == 0) stamp(2);
+        }
+      }
+      if constexpr (MODE == MODE_ZP) {
+        // this K-quarter's row sums of the tile's codes, for the zero-point term
+        const int rb2 = lt & 1;
+        mbar_wait(bar_rsempty(rb2), ((lt >> 1) & 1) ^ 1);
+        s_rowsum[(rb2 * 4 + h) * 128 + r] = static_cast<int32_t>(rsum);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_rsfull(rb2));
+      }
+    }
+    if (threadIdx.x == 0) stamp(3);
+    if (!persistent) {
+      // split-K: dump this CTA's partial accumulators into its smem (the B/x
+      // rings are idle once the accumulator is complete); reduced below
+      const int rstride = BN + 4;  // words per row (+4 breaks bank conflicts)
+      uint32_t* red = reinterpret_cast<uint32_t*>(sB);
+      const uint32_t t_row = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
       if (has_work) {
-        mbar_wait(bar_tmem_full, 0);
+        mbar_wait(bar_accfull(0), 0);
         tc_fence_after();
       }
       if (threadIdx.x == 0) stamp(4);
 #pragma unroll 1
-      for (int gq = wh; gq < ngroups; gq += NPW / 4) {
+      for (int gq = h; gq < BN / 4; gq += 4) {
         uint32_t ra[4] = {0, 0, 0, 0};
         if (has_work) {
           tmem_ld4(t_row + gq * 4, ra);
           tmem_wait_ld();
         }
-        *reinterpret_cast<uint4*>(red + rloc * rstride + gq * 4) = make_uint4(ra[0], ra[1], ra[2], ra[3]);
+        *reinterpret_cast<uint4*>(red + r * rstride + gq * 4) = make_uint4(ra[0], ra[1], ra[2], ra[3]);
       }
     }
+  } else {
+    // ============================ epilogue ================================
+    // One warp per TMEM lane quarter; each thread finishes its row of the
+    // tile, 4 columns at a time (rolled: the epilogue code stays small).
+    const int wq = warp & 3;
+    const int rloc = wq * 32 + lane;
+    const uint32_t t_row = tmem + (static_cast<uint32_t>(wq * 32) << 16);
+    const int ngroups = BN / 4;
+    auto row_sum = [&](int b) {
+      int32_t rs = 0;
+      if constexpr (MODE == MODE_ZP) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) rs += s_rowsum[(b * 4 + q) * 128 + rloc];
+      }
+      return rs;
+    };
+
+    if (persistent) {
+      int lt = 0;
+      for (int t = blockIdx.x; t < n_tiles; t += tile_step, ++lt) {
+        const Tile tl = tile_of(t);
+        const int ab = nacc == 2 ? (lt & 1) : 0;
+        const int use = nacc == 2 ? (lt >> 1) : lt;
+        mbar_wait(bar_accfull(ab), use & 1);
+        tc_fence_after();
+        if (threadIdx.x == 32 * W_EPI && lt == 0) stamp(4);
+        int32_t rs = 0;
+        if constexpr (MODE == MODE_ZP) {
+          const int rb2 = lt & 1;
+          mbar_wait(bar_rsfull(rb2), (lt >> 1) & 1);
+          rs = row_sum(rb2);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(bar_rsempty(rb2));
+        }
+        const uint32_t tacc = t_row + static_cast<uint32_t>(ab) * BNa;
+#pragma unroll 1
+        for (int gq = 0; gq < ngroups; ++gq) {
+          uint32_t ra[4];
+          tmem_ld4(tacc + gq * 4, ra);
+          tmem_wait_ld();
+          finish4(tl.m0 + rloc, tl.n_tile * BN + gq * 4, ra, rs);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_accempty(ab));
+      }
+    } else if constexpr (MODE == MODE_ZP) {
+      // split-K: this CTA's row sums for the reduction below
+      int32_t rs = 0;
+      if (has_work) {
+        mbar_wait(bar_rsfull(0), 0);
+        rs = row_sum(0);
+      }
+      __syncwarp();
+      asm volatile("bar.sync 2, 128;" ::: "memory");  // all epilogue warps read slot 0 first
+      s_rowsum[rloc] = rs;
+    }
+  }
+
+  if (!persistent) {
+    // split-K across the cluster: every CTA reduces a slice of the tile's rows
+    // over all peers through distributed shared memory
     cluster_sync_all();
     if (threadIdx.x == 0) stamp(5);
     if (warp < NPW) {
+      const Tile tl = tile_of(blockIdx.x);
+      const int rstride = BN + 4;
+      const uint32_t* red = reinterpret_cast<const uint32_t*>(sB);
+      const int ngroups = BN / 4;
       const int S = p.splits;
       const uint32_t rank = cluster_rank();
       const int rows_per = 128 / S;
@@ -845,7 +941,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             ra[3] += wa.w;
           }
         }
-        finish4(m0 + rl, n_tile * BN + gq * 4, ra, rs);
+        finish4(tl.m0 + rl, tl.n_tile * BN + gq * 4, ra, rs);
       }
     }
     if (threadIdx.x == 0) stamp(7);
@@ -855,7 +951,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
   tc_fence_before();
   __syncthreads();
-  if (warp == NPW + 1) {
+  if (warp == W_MMA) {
     tc_fence_after();
     tmem_dealloc(tmem, tmem_cols);
   }
@@ -874,8 +970,18 @@ static cudaError_t launch_impl(const CUtensorMap& xmap, const GemmParams& p, siz
     if (e != cudaSuccess) return e;
     configured = smem;
   }
+  static int n_sm = 0;
+  if (n_sm == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    if (n_sm <= 0) n_sm = 148;
+  }
+  const int tiles = p.n_tiles_n * p.m_tiles;
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(p.n_tiles_n, p.m_tiles, p.splits);
+  // splits == 1: persistent CTAs (one per SM) loop over the tiles
+  cfg.gridDim = dim3(static_cast<unsigned>(p.splits == 1 ? (tiles < n_sm ? tiles : n_sm) : tiles), 1,
+                     p.splits);
   cfg.blockDim = dim3(GEMM_THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
@@ -894,19 +1000,26 @@ static cudaError_t launch_impl(const CUtensorMap& xmap, const GemmParams& p, siz
 int gemm_ips(bool bf16, int nbp) { return KSTAGE / (nbp * (bf16 ? 2 : 1)); }
 int gemm_gs(bool bf16, int nbp) { return KSTAGE / (bf16 ? 2 : 1) / gemm_ips(bf16, nbp); }
 int gemm_threads() { return GEMM_THREADS; }
-// TMEM A-ring depth: KSTAGE/4-column slots after the BN accumulator columns
-int gemm_tmem_slots(int BN) {
-  const int acol0 = (BN + 31) / 32 * 32;
+// TMEM accumulators: two (double-buffered across persistent tiles) when they
+// leave room for at least two A-ring slots
+int gemm_tmem_accs(int BN, int splits) {
+  const int bna = (BN + 31) / 32 * 32;
+  return (splits == 1 && 2 * bna + 2 * (KSTAGE / 4) <= 512) ? 2 : 1;
+}
+// TMEM A-ring depth: KSTAGE/4-column slots after the accumulator columns
+int gemm_tmem_slots(int BN, int nacc) {
+  const int acol0 = nacc * ((BN + 31) / 32 * 32);
   const int n = (512 - acol0) / (KSTAGE / 4);
   return n < 8 ? n : 8;
 }
 
 size_t gemm_smem_bytes(bool bf16, int nbp, int BN, int SA, int SB, int SX, int x_kind,
-                       int tab_bytes) {
+                       int tab_bytes, bool silu) {
   const size_t b = static_cast<size_t>(BN) * KSTAGE;
   const size_t x = 128u * gemm_ips(bf16, nbp) * (x_kind == X_F32 ? 4 : 2);
   const size_t t = (bf16 ? 0 : static_cast<size_t>(tab_bytes)) +
-                   (2 * SA + 2 * SB + 2 * SX + 2) * 8 + 128 * 4 + 2 * BN * 8 + 16;
+                   (2 * SA + 2 * SB + 2 * SX + 9) * 8 + 2 * 4 * 128 * 4 + 16 + 16 +
+                   (silu ? 4 * 8 * 128 * 8 : 0);  // SiLU code staging
   return 1024 + SB * b + SX * x + t;
 }
 

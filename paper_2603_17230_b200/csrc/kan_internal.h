@@ -17,7 +17,8 @@ enum XKind : int { X_F32 = 0, X_U16 = 1 };
 // K-steps; the stage's weight tile is two 128-byte-wide SW128 blocks.
 constexpr int KSTAGE = 256;
 constexpr int GEMM_PRODUCER_WARPS = 16;
-constexpr int GEMM_THREADS = 32 * (GEMM_PRODUCER_WARPS + 3);
+// producers + activation loader + MMA issuer + weight loader + 4 epilogue warps
+constexpr int GEMM_THREADS = 32 * (GEMM_PRODUCER_WARPS + 7);
 
 // One fused gather + tcgen05 GEMM launch (one KAN layer, linear form).
 struct GemmParams {
@@ -26,6 +27,7 @@ struct GemmParams {
   int SA;  // A ring stages (released by the MMA)
   int SB;  // weight-tile ring stages (released by the MMA)
   int SX;  // activation ring stages (released by the producers)
+  int nacc;  // TMEM accumulators (2: the epilogue overlaps the next tile)
   // stage schedule
   int IPS, GS;
   int n_spline_stages, n_groups, silu;
@@ -37,8 +39,13 @@ struct GemmParams {
   //   thr[L+2] (f32) at off_thr: thr[n] = smallest fp32 with level >= n
   //     (thr[0] = -inf, thr[L+1] = NaN), consulted only near rounding ties
   //   SiLU codes [L+1] (u8) at off_silu
+  //   NBP = 8: c64[L+1] (u64) at off_c64: the level's full 8-byte code row,
+  //     vals[frac] << 8*jj truncated to the row
+  // rep = 1 (NBP = 8 where smem allows): lane-private copies instead, so
+  //   every table read is one conflict-free wavefront: vals as [2^k][32 lanes]
+  //   words, SiLU codes packed 4 per word as [(L+4)/4][32 lanes]; no c64
   const uint8_t* tab;
-  int tab_bytes, off_thr, off_silu;
+  int tab_bytes, off_thr, off_silu, off_c64, rep;
   int L, k;
   float lo_f, inv_step_f;  // LUT path: lo_f = -lo/step (fp32), inv_step_f = 1/step
   // float basis (bf16 path)

@@ -51,7 +51,7 @@ def main():
                 e.model_forward(x, out=out, stream=st)
         g.replay()
     torch.cuda.synchronize()
-    for li in range(len(wl.dims) - 1):
+    for li in range(wl.n_kan):
         ms, n = e.layer_time_ms(li)
         print(f"layer {li}: {ms / max(n, 1) * 1e3:.2f} us avg over {n}")
 

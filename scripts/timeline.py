@@ -39,7 +39,7 @@ def main():
     for _ in range(3):
         e.model_forward(x)
     torch.cuda.synchronize()
-    for li in range(len(wl.dims) - 1):
+    for li in range(wl.n_kan):
         t = e.layer_timeline(li).astype(np.int64)
         if t.size == 0:
             continue
@@ -54,6 +54,10 @@ def main():
             print(f"   {n:9s} min {np.nanmin(col):8.2f}  med {np.nanmedian(col):8.2f}  max {np.nanmax(col):8.2f}")
         d = rel[:, 3] - rel[:, 2]
         print(f"   mainloop (stage0->lastA) med {np.nanmedian(d):.2f} us")
+        own = rel - rel[:, :1]  # each CTA relative to its own start
+        print("   per-CTA (from own start) medians: " + ", ".join(
+            f"{n} {np.nanmedian(own[:, k]):.2f}" for k, n in enumerate(NAMES)
+            if not np.all(np.isnan(own[:, k]))))
 
 
 if __name__ == "__main__":
