@@ -41,6 +41,8 @@ cudaError_t launch_levels(const float* x, int64_t n, const float* thr, float lo,
 cudaError_t launch_argmax(const float* logits, int64_t M, int N, int ld, int32_t* out,
                           cudaStream_t st);
 cudaError_t launch_fp32_layer(const Fp32Params& p, cudaStream_t st);
+cudaError_t launch_small_layer(const SmallParams& p, cudaStream_t st);
+size_t small_smem_bytes(const SmallParams& p);
 cudaError_t launch_nchw_to_nhwc(bool levels, const float* in, int64_t n_img, int C, int HW,
                                 void* out, int ldc, const float* thr, float lo, float inv_step,
                                 int L, cudaStream_t st);
@@ -130,6 +132,11 @@ struct PreparedLayer {
   int layer_index = 0;
   int n_in = 0, N = 0, BN = 0, n_tiles_n = 0, nbp = 8;
   int cps = 0;  // conv: IPS-wide channel chunks per tap
+  // small-N CUDA-core path (LUT, NBP = 8, N <= 16, per-channel weights)
+  bool small = false;
+  int n_in8 = 0;
+  DevBuf<unsigned long long> swq;  // [n_in][N] 8 basis weights per (input, output)
+  DevBuf<int8_t> swqb;             // [N][n_in8] SiLU base weights
   int IPS = 0, GS = 0, n_spline_stages = 0, n_groups = 0, total_stages = 0, silu = 0;
   DevBuf<uint8_t> wt;       // tcgen05 paths: pre-tiled weights
   DevBuf<float> w32, wb32;  // fp32 path
@@ -678,6 +685,34 @@ void prepare_gemm_layer(kan_engine* e, const Layer& l, PreparedLayer& pl, bool b
   }
   pl.wt.upload(wt);
 
+  // small-N layers run on CUDA cores (kan_small_layer_kernel): same integer
+  // weights, laid out per (input, output) in the GEMM input order
+  pl.small = !bf16 && nbp == 8 && N <= 16 && l.type == L_LINEAR && pl.b_signed &&
+             static_cast<size_t>(n_in) * N * 8 <= 96 * 1024;
+  if (pl.small) {
+    pl.n_in8 = (n_in + 63) / 64 * 64;  // 8 threads per row x a multiple of 8 inputs each
+    const int per = pl.n_in8 / 8;
+    std::vector<unsigned long long> swq(static_cast<size_t>(n_in) * N, 0ull);
+    std::vector<int8_t> swqb(static_cast<size_t>(N) * pl.n_in8, 0);
+    for (int i = 0; i < n_in; ++i) {
+      const int ir = perm[static_cast<size_t>(i)];
+      if (ir < 0) continue;
+      for (int j = 0; j < N; ++j) {
+        unsigned long long v = 0;
+        for (int b = 0; b < nb; ++b)
+          v |= static_cast<unsigned long long>(static_cast<uint8_t>(qw_s8[(static_cast<size_t>(ir) * nb + b) * N + j]))
+               << (8 * b);
+        swq[static_cast<size_t>(i) * N + j] = v;
+        // thread t = i % 8 of a row handles inputs t, t+8, ...: [j][t][e]
+        if (pl.silu)
+          swqb[(static_cast<size_t>(j) * 8 + i % 8) * per + i / 8] = qwb[static_cast<size_t>(ir) * N + j];
+      }
+    }
+    swq.resize(swq.size() + 1, 0ull);  // bulk copies move whole 16-byte units
+    pl.swq.upload(swq);
+    pl.swqb.upload(swqb);
+  }
+
   if (!bf16) {
     const QParams vq = quant_params(0.0, 1.0, cfg.lut_h);  // s_b = value_qp.scale (lut.hpp:112)
     const double s_b = vq.scale;
@@ -1132,6 +1167,44 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
   e->last_launches += 1;
 }
 
+void run_small_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& io, cudaStream_t st) {
+  const auto& ts = e->tabs[0];
+  SmallParams p{};
+  p.M = static_cast<int>(M);
+  p.n_in = pl.n_in;
+  p.N = pl.N;
+  p.x_kind = io.x_kind;
+  p.ld_x = static_cast<int>(io.ld_x);
+  p.k = e->lat.k;
+  p.L = static_cast<int>(e->lat.L);
+  p.mode = pl.silu ? 2 : 0;
+  p.x = io.x;
+  p.tab = ts.buf.p;
+  p.tab_bytes = ts.off_c64;  // vals, thresholds, SiLU codes (no code rows needed)
+  p.off_thr = ts.off_thr;
+  p.off_silu = ts.off_silu;
+  p.lo_f = static_cast<float>(e->grid.lo);
+  p.inv_step_f = static_cast<float>(1.0 / e->lat.step);
+  p.wq = pl.swq.p;
+  p.wqb = pl.swqb.p;
+  p.n_in8 = pl.n_in8;
+  p.epi = io.epi;
+  p.out = io.out;
+  p.ld_out = static_cast<int>(io.ld_out);
+  p.fs = pl.fs.p;
+  p.corr_b = pl.corr_b.p;
+  p.n_lo = e->grid.lo;
+  p.n_hi_open = e->grid.hi_open();
+  p.n_step = e->lat.step;
+  p.n_inv_step = 1.0 / e->lat.step;
+  p.n_L = static_cast<int>(e->lat.L);
+  p.out_scale = e->cfg.out_scale;
+  p.inv_out_scale = 1.0 / e->cfg.out_scale;
+  if (small_smem_bytes(p) > 227 * 1024) throw Unsupported("small layer exceeds shared memory");
+  ck(launch_small_layer(p, st), "small layer launch");
+  e->last_launches += 1;
+}
+
 void run_fp32_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const float* x, int64_t ld_x,
                     float* out, int64_t ld_out, cudaStream_t st) {
   Fp32Params p{};
@@ -1208,7 +1281,8 @@ void forward(kan_engine* e, const float* x, int64_t M, void* out, cudaStream_t s
       const int64_t ldc = pitch16(C, isz);
       e->xnhwc.alloc(static_cast<size_t>(M * HW * ldc * isz));
       ck(launch_nchw_to_nhwc(levels, x, M, C, HW, e->xnhwc.p, static_cast<int>(ldc),
-                             levels ? e->d_thr.p : nullptr, static_cast<float>(e->grid.lo),
+                             levels ? e->d_thr.p : nullptr,
+                             levels ? static_cast<float>(-e->grid.lo / e->lat.step) : 0.f,
                              levels ? static_cast<float>(1.0 / e->lat.step) : 0.f,
                              levels ? static_cast<int>(e->lat.L) : 0, st),
          "input transpose");
@@ -1311,6 +1385,8 @@ void forward(kan_engine* e, const float* x, int64_t M, void* out, cudaStream_t s
     if (fp32)
       run_fp32_layer(e, pl, M, static_cast<const float*>(src.p), src.ld, static_cast<float*>(o),
                      io.ld_out, st);
+    else if (pl.small && !conv)
+      run_small_layer(e, pl, rows, io, st);
     else
       run_gemm_layer(e, pl, rows, io, st);
     if (e->profiling) {
@@ -1552,7 +1628,10 @@ kan_status kan_engine_layer_accumulators(kan_engine* e, int layer, const uint16_
     io.out2 = acc_b_dev;
     io.epi = EPI_RAW;
     io.ld_out = pl.N;
-    run_gemm_layer(e, pl, batch, io, static_cast<cudaStream_t>(stream));
+    if (pl.small)
+      run_small_layer(e, pl, batch, io, static_cast<cudaStream_t>(stream));
+    else
+      run_gemm_layer(e, pl, batch, io, static_cast<cudaStream_t>(stream));
   });
 }
 

@@ -277,9 +277,10 @@ __device__ __forceinline__ void load_x(const uint8_t* xt, int r, int off, int ro
 // rint(t) is the reference's llround(RN((clamp(x)-lo)/step)) unless t lies
 // within 2e-3 of a half-integer; only then (p ~ 4e-3) is the threshold table
 // thr[n] = min{x : level(x) >= n} consulted.
-__device__ __forceinline__ int lattice_level_x(float x, const GemmParams& p, const float* thr) {
-  float t = fmaf(x, p.inv_step_f, p.lo_f);  // p.lo_f holds -lo/step on this path
-  t = fminf(fmaxf(t, 0.0f), static_cast<float>(p.L));
+__device__ __forceinline__ int lattice_level_tie(float x, float inv_step, float nlo_step, int L,
+                                                 const float* thr) {
+  float t = fmaf(x, inv_step, nlo_step);  // nlo_step = -lo/step
+  t = fminf(fmaxf(t, 0.0f), static_cast<float>(L));
   const float tr = rintf(t);
   int g = static_cast<int>(tr);
   if (fabsf(fabsf(t - tr) - 0.5f) < 2e-3f) {
@@ -287,6 +288,9 @@ __device__ __forceinline__ int lattice_level_x(float x, const GemmParams& p, con
     g += (x >= thr[g + 1]) ? 1 : 0;
   }
   return g;
+}
+__device__ __forceinline__ int lattice_level_x(float x, const GemmParams& p, const float* thr) {
+  return lattice_level_tie(x, p.inv_step_f, p.lo_f, p.L, thr);  // p.lo_f holds -lo/step
 }
 
 // 64 bytes of one A row (this thread's K-quarter of a stage) on the LUT path,
@@ -1069,6 +1073,141 @@ cudaError_t launch_levels(const float* x, int64_t n, const float* thr, float lo,
 }
 
 // ---------------------------------------------------------------------------
+// Small-N LUT layer on CUDA cores (engine's choice for N <= 16, NBP = 8, e.g.
+// the 64 -> 10 classifier of C1/C2).  Same integer restatement as the GEMM:
+// acc[j] = sum_i sum_r code_r(a_i) * q[i, jj_i + r, j] (+ SiLU codes * q_b),
+// here as one mixed-sign dp4a per (input, output) -- the 4 codes against the
+// 4 weights at bytes jj..jj+3 of the input's 8 basis weights -- so results
+// are identical to the tensor-core path.  TPR threads share a row (8
+// consecutive inputs each) and reduce by shuffles (integer sums: exact).
+__device__ __forceinline__ int dp4a_us(uint32_t a, uint32_t b, int c) {
+  int d;
+  asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
+template <int NMAX, int TPR, bool SILU>
+__global__ void __launch_bounds__(256) kan_small_layer_kernel(const SmallParams p) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const int n_in = p.n_in, N = p.N;
+  const int per = p.n_in8 / TPR;  // inputs per thread (multiple of 8)
+  const int tabb = (p.tab_bytes + 15) & ~15;
+  const int wqb_bytes = SILU ? N * p.n_in8 : 0;
+  const int wq_bytes = (n_in * N * 8 + 15) & ~15;
+  unsigned long long* s_wq = reinterpret_cast<unsigned long long*>(sm + tabb);
+  int8_t* s_wqb = reinterpret_cast<int8_t*>(sm + tabb + wq_bytes);
+  __shared__ uint64_t fill_bar;
+  // tables + weights: three bulk copies on one mbarrier (one memory round trip)
+  if (threadIdx.x == 0) {
+    mbar_init(smem_u32(&fill_bar), 1);
+    mbar_fence_init();
+    mbar_arrive_tx(smem_u32(&fill_bar), static_cast<uint32_t>(tabb + wq_bytes + wqb_bytes));
+    bulk_load(smem_u32(sm), p.tab, static_cast<uint32_t>(tabb), smem_u32(&fill_bar));
+    bulk_load(smem_u32(s_wq), p.wq, static_cast<uint32_t>(wq_bytes), smem_u32(&fill_bar));
+    if (wqb_bytes > 0)
+      bulk_load(smem_u32(s_wqb), p.wqb, static_cast<uint32_t>(wqb_bytes), smem_u32(&fill_bar));
+  }
+  __syncthreads();
+  mbar_wait(smem_u32(&fill_bar), 0);
+  const uint32_t* vals = reinterpret_cast<const uint32_t*>(sm);
+  const float* thr = reinterpret_cast<const float*>(sm + p.off_thr);
+  const uint8_t* silu_tab = sm + p.off_silu;
+  const uint32_t mask = (1u << p.k) - 1u;
+
+  const int64_t gt = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t row = gt / TPR;
+  const int t = static_cast<int>(gt % TPR);
+  int acc[NMAX];
+#pragma unroll
+  for (int j = 0; j < NMAX; ++j) acc[j] = 0;
+  if (row < p.M) {
+    // this thread's inputs: i = t + TPR*e (the row's threads read neighbouring
+    // inputs, so their weight rows fall in distinct banks; rows broadcast)
+    for (int e0 = 0; e0 < per; e0 += 8) {
+      uint32_t sw[2] = {0u, 0u};
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int i = t + TPR * (e0 + e);
+        if (i < n_in) {
+          int a;
+          if (p.x_kind == X_U16)
+            a = static_cast<const uint16_t*>(p.x)[row * p.ld_x + i];
+          else
+            a = lattice_level_f32(static_cast<const float*>(p.x)[row * p.ld_x + i], thr, p.lo_f,
+                                  p.inv_step_f, p.L);
+          const uint32_t v = vals[static_cast<uint32_t>(a) & mask];
+          const uint32_t sft = 8u * static_cast<uint32_t>(a >> p.k);
+          const unsigned long long* wrow = s_wq + i * N;
+#pragma unroll
+          for (int j = 0; j < NMAX; ++j)
+            if (j < N) acc[j] = dp4a_us(v, static_cast<uint32_t>(wrow[j] >> sft), acc[j]);
+          if constexpr (SILU) sw[e >> 2] |= static_cast<uint32_t>(silu_tab[a]) << (8 * (e & 3));
+        }
+      }
+      if constexpr (SILU) {
+#pragma unroll
+        for (int j = 0; j < NMAX; ++j) {
+          if (j < N) {
+            // SiLU weights of this thread's inputs, in its order: [j][t][e]
+            const uint2 wb = *reinterpret_cast<const uint2*>(s_wqb + (j * TPR + t) * per + e0);
+            acc[j] = dp4a_us(sw[1], wb.y, dp4a_us(sw[0], wb.x, acc[j]));
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < NMAX; ++j)
+#pragma unroll
+    for (int off = TPR / 2; off > 0; off >>= 1) acc[j] += __shfl_down_sync(0xffffffffu, acc[j], off, TPR);
+  if (t != 0 || row >= p.M) return;
+#pragma unroll
+  for (int j = 0; j < NMAX; ++j) {
+    if (j >= N) break;
+    const size_t o = static_cast<size_t>(row) * p.ld_out + j;
+    if (p.epi == EPI_RAW) {
+      static_cast<int32_t*>(p.out)[o] = acc[j];
+      continue;
+    }
+    const long long v = static_cast<long long>(acc[j]) - (SILU ? p.corr_b[j] : 0ll);
+    const double y = __dmul_rn(static_cast<double>(v), p.fs[j]);
+    if (p.epi == EPI_F32)
+      static_cast<float*>(p.out)[o] = __double2float_rn(y);
+    else if (p.epi == EPI_LEVEL)
+      static_cast<uint16_t*>(p.out)[o] =
+          static_cast<uint16_t>(lattice_level_fast(y, p.n_lo, p.n_hi_open, p.n_step, p.n_inv_step, p.n_L));
+    else
+      static_cast<int8_t*>(p.out)[o] = static_cast<int8_t>(requant_i8(y, p.out_scale, p.inv_out_scale));
+  }
+}
+
+size_t small_smem_bytes(const SmallParams& p) {
+  return static_cast<size_t>((p.tab_bytes + 15) & ~15) +
+         static_cast<size_t>((p.n_in * p.N * 8 + 15) & ~15) +
+         static_cast<size_t>(p.mode == MODE_SILU ? p.N * p.n_in8 : 0) + 16;
+}
+
+cudaError_t launch_small_layer(const SmallParams& p, cudaStream_t st) {
+  if (p.M == 0) return cudaSuccess;
+  constexpr int TPR = 8, THREADS = 256;
+  const size_t smem = small_smem_bytes(p);
+  const unsigned blocks = static_cast<unsigned>((static_cast<int64_t>(p.M) * TPR + THREADS - 1) / THREADS);
+  auto go = [&](auto kfn) -> cudaError_t {
+    static size_t configured = 0;
+    if (smem > configured) {
+      cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(smem));
+      if (e != cudaSuccess) return e;
+      configured = smem;
+    }
+    kfn<<<blocks, THREADS, smem, st>>>(p);
+    return cudaGetLastError();
+  };
+  if (p.mode == MODE_SILU) return go(kan_small_layer_kernel<16, TPR, true>);
+  return go(kan_small_layer_kernel<16, TPR, false>);
+}
+
+// ---------------------------------------------------------------------------
 // Pooling over stored activations (NHWC; u16 lattice levels on the LUT path,
 // fp32 on the float paths).
 //
@@ -1144,7 +1283,8 @@ cudaError_t launch_avgpool(const void* in, int64_t n_img, int HW, int C, int ld_
 // NCHW fp32 model input -> NHWC (lattice levels on the LUT path, fp32 on the
 // float paths) for the conv layers' TMA, which needs the innermost (channel)
 // box start 16-byte aligned.  32x32 (pixel x channel) tiles through smem;
-// levels as lattice_level_f32 (exact ActivationLattice::quantize of clamp(x)).
+// levels as lattice_level_tie (exact ActivationLattice::quantize of clamp(x));
+// `lo` here is -lo/step.
 template <bool LEVELS>
 __global__ void kan_nchw_to_nhwc_kernel(const float* __restrict__ in, int C, int HW,
                                         void* __restrict__ out, int ldc,
@@ -1165,7 +1305,7 @@ __global__ void kan_nchw_to_nhwc_kernel(const float* __restrict__ in, int C, int
       const float v = tile[threadIdx.x][py];
       const int64_t o = (n * HW + q) * ldc + c;
       if constexpr (LEVELS)
-        static_cast<uint16_t*>(out)[o] = static_cast<uint16_t>(lattice_level_f32(v, thr, lo, inv_step, L));
+        static_cast<uint16_t*>(out)[o] = static_cast<uint16_t>(lattice_level_tie(v, inv_step, lo, L, thr));
       else
         static_cast<float*>(out)[o] = v;
     }

@@ -91,6 +91,29 @@ struct GemmParams {
   int dbg_flags;  // tuning only: bit0 producers write zeros, bit1 skip the MMAs
 };
 
+// Small-N LUT layer on CUDA cores (N <= 16, NBP = 8): the per-input 4-code
+// dot products as mixed-sign dp4a against the 4 weights selected at byte jj.
+struct SmallParams {
+  int M, n_in, N, x_kind, ld_x, k, L, mode;  // mode: MODE_PLAIN / MODE_ZP / MODE_SILU
+  const void* x;
+  const uint8_t* tab;  // standard blob: vals at 0, thr at off_thr, SiLU codes at off_silu
+  int tab_bytes, off_thr, off_silu;
+  float lo_f, inv_step_f;
+  const unsigned long long* wq;  // [n_in][N] 8 basis weights (int8 bytes b = 0..7)
+  const int8_t* wqb;             // [N][8][n_in8/8] SiLU base weights (int8) in thread order, n_in8 = roundup(n_in, 64)
+  int n_in8;
+  int epi;
+  void* out;
+  int ld_out;
+  double f_tensor;
+  long long z_w;
+  const double* fs;
+  const long long* corr_b;
+  double n_lo, n_hi_open, n_step, n_inv_step;
+  int n_L;
+  double out_scale, inv_out_scale;
+};
+
 // fp32 SIMT Cox-de Boor layer (accuracy baseline).
 struct Fp32Params {
   int M, n_in, N, NBP, Npad;
