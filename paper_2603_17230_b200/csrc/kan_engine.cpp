@@ -576,6 +576,7 @@ void prepare_gemm_layer(kan_engine* e, const Layer& l, PreparedLayer& pl, bool b
   if (nb > 16) throw Unsupported("G + P > 16 is not supported by the tcgen05 path");
   if (g.P > 3) throw Unsupported("degree > 3 is not supported by the tcgen05 path");
   const int n_ref = l.n_in;  // reference inputs (conv: kernel^2 * c_in)
+  if (l.type == L_CONV && l.kernel > 5) throw Unsupported("conv kernels larger than 5x5 are not supported");
   const int N = l.type == L_LINEAR ? l.n_out : l.c_out;
   pl.IPS = gemm_ips(bf16, nbp);
   pl.GS = gemm_gs(bf16, nbp);

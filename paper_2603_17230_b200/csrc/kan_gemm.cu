@@ -26,6 +26,7 @@
 //                weight (B) tiles (ring released by the MMA).
 // The int32 (LUT) or fp32 (bf16) accumulator lives in TMEM columns [0, BN).
 #include <cuda.h>
+#include <utility>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -405,18 +406,19 @@ __device__ __forceinline__ void bf16_row(const GemmParams& p, const float (&x)[3
 // Walk over the conv taps in spline-stage order (tap-major, channel chunk
 // minor), without divisions in the loop.
 struct TapWalk {
-  int cc = 0, kx = 0, ky = 0;
+  int cc = 0, kx = 0, ky = 0, tap = 0;
   __device__ TapWalk(const GemmParams& p, int sp0) {
     if (p.conv) {
-      const int t = sp0 / p.cps;
-      cc = sp0 - t * p.cps;
-      ky = t / p.ksz;
-      kx = t - ky * p.ksz;
+      tap = sp0 / p.cps;
+      cc = sp0 - tap * p.cps;
+      ky = tap / p.ksz;
+      kx = tap - ky * p.ksz;
     }
   }
   __device__ __forceinline__ void next(const GemmParams& p) {
     if (++cc == p.cps) {
       cc = 0;
+      ++tap;
       if (++kx == p.ksz) {
         kx = 0;
         ++ky;
@@ -463,6 +465,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     if (dbg) dbg[i] = globaltimer();
   };
   if (threadIdx.x == 0) stamp(0);
+  pdl_trigger();
 
   // Tiles: 1D index, N tile fastest (CTAs sharing an activation tile run
   // together).  splits == 1: persistent, this CTA takes tiles blockIdx.x,
@@ -615,6 +618,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   // stay converged for the aligned barriers and tcgen05 ops that follow.
   if (warp == W_X) {
     // ========================= activation loader ==========================
+    // the activations are the previous kernel's output: everything the other
+    // roles read before the first x tile lands is constant (tables, weights)
+    pdl_wait();
     Ring rx(SX);
     for (int t = blockIdx.x; t < n_tiles; t += tile_step) {
       const Tile tl = tile_of(t);
@@ -733,6 +739,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const Tile tl = tile_of(t);
       const int oy = tl.y0 + yy;
       TapWalk tw(p, g0 * C::GS);
+      // conv: bit (ky*K + kx) set when that tap of this row's pixel is padding
+      uint32_t padmask = 0;
+      if (p.conv) {
+        for (int ky = 0; ky < p.ksz; ++ky)
+          for (int kx = 0; kx < p.ksz; ++kx) {
+            const int iy = oy * p.cstride + ky - p.pad, ix = ox * p.cstride + kx - p.pad;
+            if (static_cast<unsigned>(iy) >= static_cast<unsigned>(p.H) ||
+                static_cast<unsigned>(ix) >= static_cast<unsigned>(p.W))
+              padmask |= 1u << (ky * p.ksz + kx);
+          }
+      }
       uint32_t rsum = 0;
       for (int g = g0; g < g1; ++g) {
         const int nsp = min(C::GS, p.n_spline_stages - g * C::GS);
@@ -744,12 +761,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             const uint8_t* xt = sX + static_cast<size_t>(rx.slot) * x_bytes;
             const int i0 = (p.conv ? tw.cc * C::IPS : (g * C::GS + s) * C::IPS) + h * H;
             // padded conv taps read level(0.0) (layers.hpp:146-147 leaves them 0.0)
-            bool padtap = false;
-            if (p.conv) {
-              const int iy = oy * p.cstride + tw.ky - p.pad, ix = ox * p.cstride + tw.kx - p.pad;
-              padtap = static_cast<unsigned>(iy) >= static_cast<unsigned>(p.H) ||
-                       static_cast<unsigned>(ix) >= static_cast<unsigned>(p.W);
-            }
+            const bool padtap = (padmask >> tw.tap) & 1u;
             tw.next(p);
             uint32_t nw[C::SW];
             if constexpr (BF16) {
@@ -963,6 +975,26 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
 // ---------------------------------------------------------------------------
 // host-side launch helpers (called from kan_engine.cpp)
+
+// cudaLaunchKernelEx with programmatic stream serialization (PDL), so the
+// kernel's prologue overlaps its predecessor's tail (see pdl_wait/pdl_trigger).
+template <class... KArgs, class... Args>
+static cudaError_t launch_pdl(void (*kfn)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kfn, std::forward<Args>(args)...);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
 template <bool BF16, int NBP, int MODE>
 static cudaError_t launch_impl(const CUtensorMap& xmap, const GemmParams& p, size_t smem,
                                cudaStream_t st) {
@@ -989,13 +1021,15 @@ static cudaError_t launch_impl(const CUtensorMap& xmap, const GemmParams& p, siz
   cfg.blockDim = dim3(GEMM_THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 1;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = p.splits;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = 1;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = p.splits;
   cfg.attrs = attr;
-  cfg.numAttrs = p.splits > 1 ? 1 : 0;
+  cfg.numAttrs = p.splits > 1 ? 2 : 1;
   cudaError_t e = cudaLaunchKernelEx(&cfg, kfn, xmap, p);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
@@ -1054,6 +1088,8 @@ cudaError_t launch_gather_gemm(bool bf16, int nbp, int mode, const CUtensorMap& 
 __global__ void kan_levels_kernel(const float* __restrict__ x, int64_t n,
                                   const float* __restrict__ thr, float lo, float inv_step, int L,
                                   uint16_t* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ float s_thr[];
   for (int i = threadIdx.x; i < L + 2; i += blockDim.x) s_thr[i] = thr[i];
   __syncthreads();
@@ -1067,9 +1103,8 @@ cudaError_t launch_levels(const float* x, int64_t n, const float* thr, float lo,
   const int64_t nb = (n + 255) / 256;
   int blocks = static_cast<int>(nb < 148 * 8 ? nb : 148 * 8);
   if (blocks < 1) blocks = 1;
-  kan_levels_kernel<<<blocks, 256, (L + 2) * sizeof(float), st>>>(x, n, thr, lo, inv_step, L,
-                                                                   out);
-  return cudaGetLastError();
+  return launch_pdl(kan_levels_kernel, dim3(blocks), dim3(256), (L + 2) * sizeof(float), st, x, n, thr, lo,
+                    inv_step, L, out);
 }
 
 // ---------------------------------------------------------------------------
@@ -1107,8 +1142,10 @@ __global__ void __launch_bounds__(256) kan_small_layer_kernel(const SmallParams 
     if (wqb_bytes > 0)
       bulk_load(smem_u32(s_wqb), p.wqb, static_cast<uint32_t>(wqb_bytes), smem_u32(&fill_bar));
   }
+  pdl_trigger();
   __syncthreads();
   mbar_wait(smem_u32(&fill_bar), 0);
+  pdl_wait();  // the activations are the previous kernel's output
   const uint32_t* vals = reinterpret_cast<const uint32_t*>(sm);
   const float* thr = reinterpret_cast<const float*>(sm + p.off_thr);
   const uint8_t* silu_tab = sm + p.off_silu;
@@ -1200,8 +1237,7 @@ cudaError_t launch_small_layer(const SmallParams& p, cudaStream_t st) {
       if (e != cudaSuccess) return e;
       configured = smem;
     }
-    kfn<<<blocks, THREADS, smem, st>>>(p);
-    return cudaGetLastError();
+    return launch_pdl(kfn, dim3(blocks), dim3(THREADS), smem, st, p);
   };
   if (p.mode == MODE_SILU) return go(kan_small_layer_kernel<16, TPR, true>);
   return go(kan_small_layer_kernel<16, TPR, false>);
@@ -1217,6 +1253,8 @@ cudaError_t launch_small_layer(const SmallParams& p, cudaStream_t st) {
 template <class T>
 __global__ void kan_maxpool_kernel(const T* __restrict__ in, int64_t n_img, int H, int W, int C,
                                    int ld_in, int win, T* __restrict__ out, int ld_out) {
+  pdl_wait();
+  pdl_trigger();
   const int Ho = H / win, Wo = W / win;
   const int64_t total = n_img * Ho * Wo * C;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
@@ -1241,6 +1279,8 @@ __global__ void kan_maxpool_kernel(const T* __restrict__ in, int64_t n_img, int 
 // in fp64, rounded to fp32.
 __global__ void kan_avgpool_f32_kernel(const float* __restrict__ in, int64_t n_img, int HW, int C,
                                        int ld_in, float* __restrict__ out, int ld_out) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t total = n_img * C;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -1263,21 +1303,19 @@ cudaError_t launch_maxpool(bool levels, const void* in, int64_t n_img, int H, in
   const int64_t total = n_img * (H / win) * (W / win) * C;
   if (total == 0) return cudaSuccess;
   if (levels)
-    kan_maxpool_kernel<uint16_t><<<pool_blocks(total), 256, 0, st>>>(
-        static_cast<const uint16_t*>(in), n_img, H, W, C, ld_in, win, static_cast<uint16_t*>(out), ld_out);
-  else
-    kan_maxpool_kernel<float><<<pool_blocks(total), 256, 0, st>>>(
-        static_cast<const float*>(in), n_img, H, W, C, ld_in, win, static_cast<float*>(out), ld_out);
-  return cudaGetLastError();
+    return launch_pdl(kan_maxpool_kernel<uint16_t>, dim3(pool_blocks(total)), dim3(256), 0, st,
+                      static_cast<const uint16_t*>(in), n_img, H, W, C, ld_in, win, static_cast<uint16_t*>(out),
+                      ld_out);
+  return launch_pdl(kan_maxpool_kernel<float>, dim3(pool_blocks(total)), dim3(256), 0, st,
+                    static_cast<const float*>(in), n_img, H, W, C, ld_in, win, static_cast<float*>(out), ld_out);
 }
 
 cudaError_t launch_avgpool(const void* in, int64_t n_img, int HW, int C, int ld_in, void* out,
                            int ld_out, cudaStream_t st) {
   const int64_t total = n_img * C;
   if (total == 0) return cudaSuccess;
-  kan_avgpool_f32_kernel<<<pool_blocks(total), 256, 0, st>>>(
-      static_cast<const float*>(in), n_img, HW, C, ld_in, static_cast<float*>(out), ld_out);
-  return cudaGetLastError();
+  return launch_pdl(kan_avgpool_f32_kernel, dim3(pool_blocks(total)), dim3(256), 0, st,
+                    static_cast<const float*>(in), n_img, HW, C, ld_in, static_cast<float*>(out), ld_out);
 }
 
 // NCHW fp32 model input -> NHWC (lattice levels on the LUT path, fp32 on the
@@ -1286,28 +1324,45 @@ cudaError_t launch_avgpool(const void* in, int64_t n_img, int HW, int C, int ld_
 // levels as lattice_level_tie (exact ActivationLattice::quantize of clamp(x));
 // `lo` here is -lo/step.
 template <bool LEVELS>
-__global__ void kan_nchw_to_nhwc_kernel(const float* __restrict__ in, int C, int HW,
-                                        void* __restrict__ out, int ldc,
-                                        const float* __restrict__ thr, float lo, float inv_step,
-                                        int L) {
-  __shared__ float tile[32][33];
+__global__ void __launch_bounds__(256) kan_nchw_to_nhwc_kernel(const float* __restrict__ in, int C, int HW,
+                                                                void* __restrict__ out, int ldc,
+                                                                const float* __restrict__ thr, float lo,
+                                                                float inv_step, int L) {
+  pdl_wait();
+  pdl_trigger();
+  // tile: 64 channels x 32 pixels; loads coalesced along pixels, stores of a
+  // pixel's 64 channels as one 128-byte (levels) / 256-byte (fp32) warp row
+  __shared__ float tile[64][33];
   const int64_t n = blockIdx.z;
-  const int p0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+  const int p0 = blockIdx.x * 32, c0 = blockIdx.y * 64;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 warps
   const float* src = in + n * C * HW;
-  for (int cy = threadIdx.y; cy < 32; cy += 8) {
-    const int c = c0 + cy, q = p0 + threadIdx.x;
-    tile[cy][threadIdx.x] = (c < C && q < HW) ? src[static_cast<int64_t>(c) * HW + q] : 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int cy = ty + 8 * k, c = c0 + cy, q = p0 + tx;
+    tile[cy][tx] = (c < C && q < HW) ? src[static_cast<int64_t>(c) * HW + q] : 0.f;
   }
   __syncthreads();
-  for (int py = threadIdx.y; py < 32; py += 8) {
-    const int q = p0 + py, c = c0 + threadIdx.x;
-    if (q < HW && c < C) {
-      const float v = tile[threadIdx.x][py];
-      const int64_t o = (n * HW + q) * ldc + c;
-      if constexpr (LEVELS)
-        static_cast<uint16_t*>(out)[o] = static_cast<uint16_t>(lattice_level_tie(v, inv_step, lo, L, thr));
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int py = ty + 8 * k, q = p0 + py;
+    const int c = c0 + 2 * tx;  // lane -> channel pair
+    if (q >= HW || c >= C) continue;
+    const float v0 = tile[2 * tx][py];
+    const float v1 = tile[2 * tx + 1][py];
+    const int64_t o = (n * HW + q) * ldc + c;
+    if constexpr (LEVELS) {
+      const uint32_t a0 = static_cast<uint32_t>(lattice_level_tie(v0, inv_step, lo, L, thr));
+      const uint32_t a1 = static_cast<uint32_t>(lattice_level_tie(v1, inv_step, lo, L, thr));
+      if (c + 1 < C)
+        *reinterpret_cast<uint32_t*>(static_cast<uint16_t*>(out) + o) = a0 | (a1 << 16);
       else
-        static_cast<float*>(out)[o] = v;
+        static_cast<uint16_t*>(out)[o] = static_cast<uint16_t>(a0);
+    } else {
+      if (c + 1 < C)
+        *reinterpret_cast<float2*>(static_cast<float*>(out) + o) = make_float2(v0, v1);
+      else
+        static_cast<float*>(out)[o] = v0;
     }
   }
 }
@@ -1316,18 +1371,19 @@ cudaError_t launch_nchw_to_nhwc(bool levels, const float* in, int64_t n_img, int
                                 void* out, int ldc, const float* thr, float lo, float inv_step,
                                 int L, cudaStream_t st) {
   if (n_img == 0) return cudaSuccess;
-  const dim3 grid((HW + 31) / 32, (C + 31) / 32, static_cast<unsigned>(n_img));
-  const dim3 block(32, 8);
+  const dim3 grid((HW + 31) / 32, (C + 63) / 64, static_cast<unsigned>(n_img));
   if (levels)
-    kan_nchw_to_nhwc_kernel<true><<<grid, block, 0, st>>>(in, C, HW, out, ldc, thr, lo, inv_step, L);
-  else
-    kan_nchw_to_nhwc_kernel<false><<<grid, block, 0, st>>>(in, C, HW, out, ldc, thr, lo, inv_step, L);
-  return cudaGetLastError();
+    return launch_pdl(kan_nchw_to_nhwc_kernel<true>, grid, dim3(256), 0, st, in, C, HW, out, ldc, thr, lo,
+                      inv_step, L);
+  return launch_pdl(kan_nchw_to_nhwc_kernel<false>, grid, dim3(256), 0, st, in, C, HW, out, ldc, thr, lo,
+                    inv_step, L);
 }
 
 // argmax over logits rows (predict, eval.hpp:268-272: first maximum wins)
 __global__ void kan_argmax_kernel(const float* __restrict__ logits, int64_t M, int N, int ld,
                                   int32_t* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t m = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (m >= M) return;
   const float* r = logits + m * ld;
@@ -1340,9 +1396,8 @@ __global__ void kan_argmax_kernel(const float* __restrict__ logits, int64_t M, i
 cudaError_t launch_argmax(const float* logits, int64_t M, int N, int ld, int32_t* out,
                           cudaStream_t st) {
   if (M == 0) return cudaSuccess;
-  kan_argmax_kernel<<<static_cast<unsigned>((M + 255) / 256), 256, 0, st>>>(logits, M, N, ld,
-                                                                            out);
-  return cudaGetLastError();
+  return launch_pdl(kan_argmax_kernel, dim3(static_cast<unsigned>((M + 255) / 256)), dim3(256), 0, st, logits,
+                    M, N, ld, out);
 }
 
 }  // namespace kan
