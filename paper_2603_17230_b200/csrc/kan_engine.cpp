@@ -222,7 +222,7 @@ struct kan_engine {
   struct TabSet {
     DevBuf<uint8_t> buf;
     int bytes = 0, off_thr = 0, off_silu = 0, off_c64 = 0;
-  } tabs[2];
+  } tabs[3];
   double s_s = 1.0;
   int64_t z_s = 0;
   // workspaces: activation buffer slot of each layer's stored output (-1:
@@ -878,13 +878,13 @@ void configure(kan_engine* e, const kan_config* c) {
     std::vector<uint32_t> vals(nfrac);
     for (size_t f = 0; f < nfrac; ++f)
       vals[f] = lut_pack(g, cfg.lut_k, e->lut, static_cast<int64_t>(f));  // jj = 0
-    for (int variant = 0; variant < 2; ++variant) {
+    for (int variant = 0; variant < 3; ++variant) {
       auto& ts = e->tabs[variant];
-      if (variant == 1 && g.nb() > 8) {
+      if (variant >= 1 && g.nb() > 8) {
         ts.bytes = 0;
         continue;
       }
-      const size_t rep = variant == 1 ? 32 : 1;  // copies, interleaved by lane
+      const size_t rep = variant >= 1 ? 32 : 1;  // copies, interleaved by lane
       std::vector<uint8_t> blob(a16(nfrac * 4 * rep), 0);
       for (size_t f = 0; f < nfrac; ++f)
         for (size_t l = 0; l < rep; ++l) std::memcpy(&blob[(f * rep + l) * 4], &vals[f], 4);
@@ -893,7 +893,7 @@ void configure(kan_engine* e, const kan_config* c) {
       std::memcpy(&blob[static_cast<size_t>(ts.off_thr)], thr.data(), thr.size() * 4);
       ts.off_silu = static_cast<int>(blob.size());
       if (!codes.empty()) {
-        if (variant == 0) {
+        if (variant != 1) {
           blob.insert(blob.end(), codes.begin(), codes.end());
         } else {  // 4 codes per word, word w of lane l at (w*32 + l)*4
           const size_t words = (codes.size() + 3) / 4;
@@ -1058,10 +1058,11 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
   // table variant: the lane-private copies when they leave deep enough rings
   int SA = 2, SB = 2, SX = 2;
   int variant = 0;
-  if (!bf16 && e->tabs[1].bytes > 0) {
+  const int want_tab = e->force_tab >= 0 ? e->force_tab : 2;
+  if (!bf16 && want_tab > 0 && e->tabs[want_tab].bytes > 0) {
     try {
-      pick_stages(bf16, pl.nbp, pl.BN, io.x_kind, e->tabs[1].bytes, pl.silu != 0, 1, SA, SB, SX);
-      if (SB >= 3 && SX >= 4 && e->force_tab != 0) variant = 1;
+      pick_stages(bf16, pl.nbp, pl.BN, io.x_kind, e->tabs[want_tab].bytes, pl.silu != 0, 1, SA, SB, SX);
+      if (SB >= 3 && SX >= 4) variant = want_tab;
     } catch (const Unsupported&) {
     }
   }

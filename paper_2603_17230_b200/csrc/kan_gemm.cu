@@ -342,7 +342,7 @@ __device__ __forceinline__ void lut_row(const GemmParams& p, const uint32_t* val
     }
   }
   if constexpr (MODE == MODE_SILU) {
-    if (NBP == 8 && p.rep) {
+    if (NBP == 8 && p.rep == 1) {
       // lane-private packed codes: word (a >> 2) of this lane, byte a & 3
       const uint32_t* srep = reinterpret_cast<const uint32_t*>(silu_tab);
 #pragma unroll
@@ -538,6 +538,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     mbar_init(bar_tab, 1);
     mbar_fence_init();
   }
+  if (p.dbg_flags & 4)  // tuning only (no activation loads): a zero activation ring
+    for (uint32_t q = threadIdx.x; q < static_cast<uint32_t>(SX) * x_bytes / 4; q += blockDim.x)
+      reinterpret_cast<uint32_t*>(sX)[q] = 0u;
   if (warp == W_X && lane == 0) tma_prefetch(&xmap);
   if (warp == W_MMA) tmem_alloc(smem_u32(s_tmem), tmem_cols);
   tc_fence_before();
@@ -631,6 +634,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           mbar_wait(bar_xempty(rx.slot), rx.phase ^ 1);
           if (lane == 0) {
             const uint32_t dst = smem_u32(sX + static_cast<size_t>(rx.slot) * x_bytes);
+            if (p.dbg_flags & 4) {  // tuning only: no activation load (stale tile)
+              mbar_arrive(bar_xfull(rx.slot));
+            } else {
             mbar_arrive_tx(bar_xfull(rx.slot), x_bytes);
             if (!p.conv) {
               tma_load_2d(dst, &xmap, (g * C::GS + s) * C::IPS, tl.m0, bar_xfull(rx.slot));
@@ -639,6 +645,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               // (element strides in the tensor map step by the conv stride)
               const int iy = tl.y0 * p.cstride + tw.ky - p.pad, ix = tw.kx - p.pad;
               tma_load_4d(dst, &xmap, tw.cc * C::IPS, ix, iy, tl.n0, bar_xfull(rx.slot));
+            }
             }
           }
           __syncwarp();

@@ -43,7 +43,8 @@ struct GemmParams {
   //     vals[frac] << 8*jj truncated to the row
   // rep = 1 (NBP = 8 where smem allows): lane-private copies instead, so
   //   every table read is one conflict-free wavefront: vals as [2^k][32 lanes]
-  //   words, SiLU codes packed 4 per word as [(L+4)/4][32 lanes]; no c64
+  //   words, SiLU codes packed 4 per word as [(L+4)/4][32 lanes]; no c64.
+  // rep = 2: lane-private vals, shared SiLU codes (fewer instructions)
   const uint8_t* tab;
   int tab_bytes, off_thr, off_silu, off_c64, rep;
   int L, k;
