@@ -31,7 +31,7 @@ namespace kan {
 cudaError_t launch_gather_gemm(bool bf16, int nbp, int mode, const CUtensorMap& xmap,
                                const GemmParams& p, size_t smem, cudaStream_t st);
 size_t gemm_smem_bytes(bool bf16, int nbp, int BN, int SA, int SB, int SX, int x_kind,
-                       int tab_bytes, bool silu);
+                       int tab_bytes, bool silu, int fused_bytes);
 int gemm_ips(bool bf16, int nbp);
 int gemm_gs(bool bf16, int nbp);
 int gemm_tmem_slots(int BN, int nacc);
@@ -137,6 +137,7 @@ struct PreparedLayer {
   int n_in8 = 0;
   DevBuf<unsigned long long> swq;  // [n_in][N] 8 basis weights per (input, output)
   DevBuf<int8_t> swqb;             // [N][n_in8] SiLU base weights
+  DevBuf<int8_t> swqb_plain;       // [N][n_in] SiLU base weights (fused tail layer), padded to 16 B
   int IPS = 0, GS = 0, n_spline_stages = 0, n_groups = 0, total_stages = 0, silu = 0;
   DevBuf<uint8_t> wt;       // tcgen05 paths: pre-tiled weights
   DevBuf<float> w32, wb32;  // fp32 path
@@ -711,6 +712,14 @@ void prepare_gemm_layer(kan_engine* e, const Layer& l, PreparedLayer& pl, bool b
     }
     swq.resize(swq.size() + 1, 0ull);  // bulk copies move whole 16-byte units
     pl.swq.upload(swq);
+    std::vector<int8_t> plain((static_cast<size_t>(N) * n_in + 15) / 16 * 16, 0);
+    if (pl.silu)
+      for (int i = 0; i < n_in; ++i) {
+        const int ir = perm[static_cast<size_t>(i)];
+        if (ir < 0) continue;
+        for (int j = 0; j < N; ++j) plain[static_cast<size_t>(j) * n_in + i] = qwb[static_cast<size_t>(ir) * N + j];
+      }
+    pl.swqb_plain.upload(plain);
     pl.swqb.upload(swqb);
   }
 
@@ -952,15 +961,15 @@ void configure(kan_engine* e, const kan_config* c) {
 // the MMA (2 slots); the weight and activation rings hide L2 / HBM latency, so
 // they get equal depth first and the activation ring takes what is left.
 void pick_stages(bool bf16, int nbp, int BN, int x_kind, int tab_bytes, bool silu, int nacc, int& SA,
-                 int& SB, int& SX) {
+                 int& SB, int& SX, int fused_bytes = 0) {
   const size_t budget = 232448;
   SA = gemm_tmem_slots(BN, nacc);  // the A ring lives in TMEM
   for (SB = 12; SB >= 2; --SB)
-    if (gemm_smem_bytes(bf16, nbp, BN, SA, SB, SB, x_kind, tab_bytes, silu) <= budget) break;
+    if (gemm_smem_bytes(bf16, nbp, BN, SA, SB, SB, x_kind, tab_bytes, silu, fused_bytes) <= budget) break;
   if (SB < 2) throw Unsupported("tile configuration exceeds shared memory");
   for (SX = 24; SX > SB; --SX)
-    if (gemm_smem_bytes(bf16, nbp, BN, SA, SB, SX, x_kind, tab_bytes, silu) <= budget) break;
-  if (gemm_smem_bytes(bf16, nbp, BN, SA, SB, SX, x_kind, tab_bytes, silu) > budget) SX = SB;
+    if (gemm_smem_bytes(bf16, nbp, BN, SA, SB, SX, x_kind, tab_bytes, silu, fused_bytes) <= budget) break;
+  if (gemm_smem_bytes(bf16, nbp, BN, SA, SB, SX, x_kind, tab_bytes, silu, fused_bytes) > budget) SX = SB;
 }
 
 struct LayerIO {
@@ -975,6 +984,12 @@ struct LayerIO {
   const Layer* conv = nullptr;
   int64_t n_img = 0;
   // residual add and NCHW output
+  // fused output layer (split-K launches): the next, small layer and where
+  // it writes; run_gemm_layer sets `fused` when it took the layer over
+  PreparedLayer* fuse = nullptr;
+  void* fuse_out = nullptr;
+  int fuse_epi = 0;
+  bool* fused = nullptr;
   int res_kind = 0;
   const void* res = nullptr;
   int64_t ld_res = 0;
@@ -1093,6 +1108,46 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
   const int gps = (pl.n_groups + splits - 1) / splits;
   p.splits = splits;
   p.groups_per_split = gps;
+  // fused output layer: only for split-K launches (each CTA reduces whole rows)
+  int fused_bytes = 0;
+  if (io.fuse && splits > 1 && pl.n_tiles_n == 1 && !io.conv && io.epi == EPI_LEVEL) {
+    const PreparedLayer& f = *io.fuse;
+    const int wq_b = (f.n_in * f.N * 8 + 15) / 16 * 16;
+    const int wqb_b = f.silu ? (f.N * f.n_in + 15) / 16 * 16 : 0;
+    const int fb = wq_b + wqb_b + 128 * pl.BN * 2;
+    int SA2 = SA, SB2 = SB, SX2 = SX;
+    bool ok = f.n_in == pl.N && f.N <= 16 && 128 / splits >= 8;
+    if (ok) {
+      try {
+        pick_stages(bf16, pl.nbp, pl.BN, io.x_kind, tb, pl.silu != 0, 1, SA2, SB2, SX2, fb);
+      } catch (const Unsupported&) {
+        ok = false;
+      }
+    }
+    // the split-K partials are exchanged through the (then idle) rings
+    if (ok && red_bytes > static_cast<size_t>(SB2) * pl.BN * KSTAGE +
+                              static_cast<size_t>(SX2) * 128 * pl.IPS * (io.x_kind == X_F32 ? 4 : 2))
+      ok = false;
+    if (ok) {
+      SA = SA2;
+      SB = SB2;
+      SX = SX2;
+      fused_bytes = fb;
+      p.f_on = 1;
+      p.f_N = f.N;
+      p.f_silu = f.silu;
+      p.f_epi = io.fuse_epi;
+      p.f_ld_out = f.N;
+      p.f_wq_bytes = wq_b;
+      p.f_wqb_bytes = wqb_b;
+      p.f_wq = f.swq.p;
+      p.f_wqb = f.silu ? f.swqb_plain.p : nullptr;
+      p.f_fs = f.fs.p;
+      p.f_corr = f.corr_b.p;
+      p.f_out = io.fuse_out;
+      if (io.fused) *io.fused = true;
+    }
+  }
   // persistent launches double-buffer the accumulator when TMEM allows
   p.nacc = gemm_tmem_accs(pl.BN, splits);
   SA = gemm_tmem_slots(pl.BN, p.nacc);
@@ -1162,7 +1217,7 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
   } else {
     xmap = make_xmap(io.x, io.x_kind, M, pl.n_in, io.ld_x, pl.IPS);
   }
-  const size_t smem = gemm_smem_bytes(bf16, pl.nbp, pl.BN, SA, SB, SX, io.x_kind, tb, pl.silu != 0);
+  const size_t smem = gemm_smem_bytes(bf16, pl.nbp, pl.BN, SA, SB, SX, io.x_kind, tb, pl.silu != 0, fused_bytes);
   // kernel variant: 0 plain, 1 per-tensor zero point (reference scheme), 2 SiLU base
   const int mode = pl.silu ? 2 : ((!bf16 && pl.wscheme == KAN_W_PER_TENSOR_ASYM) ? 1 : 0);
   ck(launch_gather_gemm(bf16, pl.nbp, mode, xmap, p, smem, st), "gather_gemm launch");
@@ -1372,6 +1427,18 @@ void forward(kan_engine* e, const float* x, int64_t M, void* out, cudaStream_t s
       io.epi = levels ? EPI_LEVEL : EPI_F32;
     }
     io.out = o;
+    // fuse a small last layer that reads only this layer's hidden levels
+    bool fused = false;
+    if (lut && !conv && !last && i + 2 == nl && io.epi == EPI_LEVEL && !(pl.small && !conv)) {
+      const Layer& nx = e->layers[static_cast<size_t>(i + 1)];
+      PreparedLayer& pn = e->prep[static_cast<size_t>(nx.kan_index)];
+      if (nx.type == L_LINEAR && nx.src == i && nx.res_src == -2 && pn.small) {
+        io.fuse = &pn;
+        io.fuse_out = out;
+        io.fuse_epi = e->cfg.out_kind == KAN_OUT_I8 ? EPI_I8 : EPI_F32;
+        io.fused = &fused;
+      }
+    }
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     unsigned ev_flags = cudaEventRecordDefault;
     if (e->profiling) {
@@ -1399,6 +1466,7 @@ void forward(kan_engine* e, const float* x, int64_t M, void* out, cudaStream_t s
     dst.kind = io.epi == EPI_LEVEL ? X_U16 : X_F32;
     dst.nchw = false;
     dst.ld = io.ld_out;
+    if (fused) break;  // the output layer ran inside this launch
   }
 }
 

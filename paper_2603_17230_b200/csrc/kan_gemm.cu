@@ -403,6 +403,13 @@ __device__ __forceinline__ void bf16_row(const GemmParams& p, const float (&x)[3
   }
 }
 
+// u8 x s8 dot product of 4 byte pairs (dp4a.u32.s32): LUT codes x int8 weights
+__device__ __forceinline__ int dp4a_us(uint32_t a, uint32_t b, int c) {
+  int d;
+  asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
 // Walk over the conv taps in spline-stage order (tap-major, channel chunk
 // minor), without divisions in the loop.
 struct TapWalk {
@@ -456,6 +463,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   // Offset arithmetic from smem keeps the compiler on shared-memory accesses.
   const uint32_t sil_off = ((static_cast<uint32_t>(reinterpret_cast<uint8_t*>(s_tmem + 4) - smem)) + 15u) & ~15u;
   uint32_t* s_sil = reinterpret_cast<uint32_t*>(smem + sil_off);
+  // fused output layer: its weights and the CTA's hidden-level rows [128][BN]
+  const uint32_t f_off = sil_off + (SILU ? 4u * 8u * 128u * 8u : 0u);
+  unsigned long long* f_wq = reinterpret_cast<unsigned long long*>(smem + f_off);
+  int8_t* f_wqb = reinterpret_cast<int8_t*>(smem + f_off + p.f_wq_bytes);
+  uint16_t* f_lv = reinterpret_cast<uint16_t*>(smem + f_off + p.f_wq_bytes + p.f_wqb_bytes);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -604,7 +616,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           if (e < nvalid) o[e] = __double2float_rn(y[e]);
       }
     } else if (p.epi == EPI_LEVEL) {
-      uint16_t* o = reinterpret_cast<uint16_t*>(p.out) + base;
+      // fused output layer: the levels stay in this CTA's smem row buffer
+      uint16_t* o = p.f_on ? f_lv + (row & 127) * BN + (col0 % BN) : reinterpret_cast<uint16_t*>(p.out) + base;
 #pragma unroll
       for (int e = 0; e < 4; ++e)
         if (e < nvalid)
@@ -655,8 +668,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   } else if (warp == W_B) {
     // ===================== table + weight-tile loader =====================
     if (lane == 0 && tab_bytes > 0) {
-      mbar_arrive_tx(bar_tab, static_cast<uint32_t>(tab_bytes));
+      const uint32_t fb = p.f_on ? static_cast<uint32_t>(p.f_wq_bytes + p.f_wqb_bytes) : 0u;
+      mbar_arrive_tx(bar_tab, static_cast<uint32_t>(tab_bytes) + fb);
       bulk_load(smem_u32(sT), p.tab, static_cast<uint32_t>(tab_bytes), bar_tab);
+      if (p.f_on) {
+        bulk_load(smem_u32(f_wq), p.f_wq, static_cast<uint32_t>(p.f_wq_bytes), bar_tab);
+        bulk_load(smem_u32(f_wqb), p.f_wqb, static_cast<uint32_t>(p.f_wqb_bytes), bar_tab);
+      }
     }
     __syncwarp();
     Ring rb(SB);
@@ -966,6 +984,54 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         }
         finish4(tl.m0 + rl, tl.n_tile * BN + gq * 4, ra, rs);
       }
+      if (p.f_on) {
+        // fused output layer over this CTA's rows: TPR threads per row, inputs
+        // i = sub + TPR*e, mixed-sign dp4a per (input, output), integer
+        // shuffle reduction, then the fp64 epilogue (kan_small_layer_kernel's math)
+        asm volatile("bar.sync 3, %0;" ::"r"(NP) : "memory");
+        const int TPR = NP / rows_per;  // 16 or 32: a row's threads share a warp
+        const int lr = threadIdx.x / TPR, sub = threadIdx.x % TPR;
+        const int rl = static_cast<int>(rank) * rows_per + lr;
+        const int n2 = p.f_N, n_in2 = p.N;
+        const uint32_t* vals = reinterpret_cast<const uint32_t*>(sT);
+        const uint8_t* silu_tab = sT + p.off_silu;
+        const uint32_t mask = (1u << p.k) - 1u;
+        int acc[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) acc[j] = 0;
+        for (int i = sub; i < n_in2; i += TPR) {
+          const int a = f_lv[rl * BN + i];
+          const uint32_t v = p.rep ? vals[((static_cast<uint32_t>(a) & mask) << 5) | static_cast<uint32_t>(lane)]
+                                   : vals[static_cast<uint32_t>(a) & mask];
+          const uint32_t sft = 8u * static_cast<uint32_t>(a >> p.k);
+          const int sc = p.f_silu ? static_cast<int>(silu_tab[a]) : 0;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            if (j < n2) {
+              acc[j] = dp4a_us(v, static_cast<uint32_t>(f_wq[i * n2 + j] >> sft), acc[j]);
+              if (p.f_silu) acc[j] += sc * static_cast<int>(f_wqb[j * n_in2 + i]);
+            }
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          for (int off = TPR / 2; off > 0; off >>= 1) acc[j] += __shfl_down_sync(0xffffffffu, acc[j], off, TPR);
+        const int row = tl.m0 + rl;
+        if (sub == 0 && row < p.M) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            if (j < n2) {
+              const size_t o = static_cast<size_t>(row) * p.f_ld_out + j;
+              const long long v = static_cast<long long>(acc[j]) - (p.f_silu ? p.f_corr[j] : 0ll);
+              const double y = __dmul_rn(static_cast<double>(v), p.f_fs[j]);
+              if (p.f_epi == EPI_F32)
+                static_cast<float*>(p.f_out)[o] = __double2float_rn(y);
+              else
+                static_cast<int8_t*>(p.f_out)[o] = static_cast<int8_t>(requant_i8(y, p.out_scale, p.inv_out_scale));
+            }
+          }
+        }
+      }
     }
     if (threadIdx.x == 0) stamp(7);
     cluster_sync_all();  // peers' smem must outlive every remote read
@@ -1059,12 +1125,13 @@ int gemm_tmem_slots(int BN, int nacc) {
 }
 
 size_t gemm_smem_bytes(bool bf16, int nbp, int BN, int SA, int SB, int SX, int x_kind,
-                       int tab_bytes, bool silu) {
+                       int tab_bytes, bool silu, int fused_bytes) {
   const size_t b = static_cast<size_t>(BN) * KSTAGE;
   const size_t x = 128u * gemm_ips(bf16, nbp) * (x_kind == X_F32 ? 4 : 2);
   const size_t t = (bf16 ? 0 : static_cast<size_t>(tab_bytes)) +
                    (2 * SA + 2 * SB + 2 * SX + 9) * 8 + 2 * 4 * 128 * 4 + 16 + 16 +
-                   (silu ? 4 * 8 * 128 * 8 : 0);  // SiLU code staging
+                   (silu ? 4 * 8 * 128 * 8 : 0) +  // SiLU code staging
+                   static_cast<size_t>(fused_bytes);
   return 1024 + SB * b + SX * x + t;
 }
 
@@ -1122,11 +1189,6 @@ cudaError_t launch_levels(const float* x, int64_t n, const float* thr, float lo,
 // 4 weights at bytes jj..jj+3 of the input's 8 basis weights -- so results
 // are identical to the tensor-core path.  TPR threads share a row (8
 // consecutive inputs each) and reduce by shuffles (integer sums: exact).
-__device__ __forceinline__ int dp4a_us(uint32_t a, uint32_t b, int c) {
-  int d;
-  asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
-  return d;
-}
 
 template <int NMAX, int TPR, bool SILU>
 __global__ void __launch_bounds__(256) kan_small_layer_kernel(const SmallParams p) {

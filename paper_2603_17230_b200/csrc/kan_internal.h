@@ -85,6 +85,17 @@ struct GemmParams {
   const void* res;
   int ld_res;
   int out_hw;  // EPI_F32: >0 writes NCHW (H*W per channel), 0 row-major
+  // fused output layer (split-K launches, LUT path): the reduced hidden levels
+  // of each CTA's rows stay in smem and feed the next, small KAN layer
+  // (N2 <= 16, NBP = 8, per-channel weights) inside this kernel, which writes
+  // the model output; f_wq [n_in2][N2] 8 basis weights per (input, output),
+  // f_wqb [N2][n_in2] SiLU base weights, both bulk-copied to smem
+  int f_on, f_N, f_silu, f_epi, f_ld_out, f_wq_bytes, f_wqb_bytes;
+  const unsigned long long* f_wq;
+  const int8_t* f_wqb;
+  const double* f_fs;
+  const long long* f_corr;
+  void* f_out;
   // optional per-CTA phase timestamps (%globaltimer ns) for tuning:
   // [cta][8] = start, tables ready, first A stage, last A stage, TMEM full,
   // partials exchanged, done

@@ -278,4 +278,24 @@ def test_forward_host_equals_device_path():
     e = build(dims, G, Ws, Bs, mode="bspline-lut", silu_base=True)
     x = np.random.default_rng(5).uniform(-1, 1, (1024, 784)).astype(np.float32)
     np.testing.assert_array_equal(e.forward_host(x), e.model_forward(to_dev(x)).cpu().numpy())
-    assert e.last_launches == 2
+    # the 64 -> 10 output layer runs inside layer 0's split-K launch
+    assert e.last_launches == 1
+
+
+@pytest.mark.parametrize("M", [4096, 1024, 300])
+def test_fused_output_layer_matches_separate_launches(oracle, M):
+    """Split-K launches fuse the small output layer into their reduction; a
+    persistent launch (split_k=1) runs it as its own kernel.  Both are the
+    same integer computation: bit-identical logits, and equal to the oracle."""
+    dims, G = [784, 64, 10], 5
+    Ws, Bs = make_weights(dims, G, seed=6, silu=True)
+    x = np.random.default_rng(M).uniform(-1, 1, (M, 784)).astype(np.float32)
+    fused = build(dims, G, Ws, Bs, mode="bspline-lut", silu_base=True)
+    yf = fused.model_forward(to_dev(x)).cpu().numpy()
+    assert fused.last_launches == 1
+    sep = build(dims, G, Ws, Bs, mode="bspline-lut", silu_base=True, split_k=1)
+    ys = sep.model_forward(to_dev(x)).cpu().numpy()
+    assert sep.last_launches == 2
+    np.testing.assert_array_equal(yf, ys)
+    yo = oracle_int_model(oracle, G, 8, 8, W_PER_CHANNEL_SYM, 8, Ws, Bs, x)[-1]
+    np.testing.assert_array_equal(yf, yo.astype(np.float32))
