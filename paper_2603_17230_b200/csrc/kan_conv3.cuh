@@ -1,0 +1,388 @@
+// kan_conv3.cuh -- ky-shared 3x3 / stride-1 / pad-1 KAN conv on the LUT path
+// (included by kan_gemm.cu, which provides the level, table and epilogue
+// helpers).  Same result as kan_gather_gemm_kernel on the same layer: the
+// int32 accumulator is the same sum of products, in another order.
+//
+// Replaces, for these layers, convkan_forward (layers.hpp:162-190) =
+// im2col (layers.hpp:126-154) + kan_linear_forward<LutBasis>.
+//
+// Why a second kernel: an output tile is bh rows x Wo columns of one image.
+// Its three ky taps read the same input pixels shifted by whole rows of Wo
+// pixels.  So the producers expand the (bh+2)-row input window of one (kx,
+// channel chunk) "super-stage" once -- codes into a K-major SW128 tile in
+// shared memory, SiLU codes into a 32-byte-row SW32 tile -- and the MMA warp
+// issues the three taps as SS-mode tcgen05.mma whose A descriptors start
+// ky*Wo rows in (Wo % 8 == 0 keeps every start on an 8-row swizzle atom).
+// The SiLU base term of a tap is one extra K=32 MMA against the SiLU tile.
+// This halves the producer work per tap, the bound of these layers.
+//
+// Warp roles as in kan_gather_gemm_kernel (persistent tiles, 16 producers,
+// activation TMA, MMA, weight loader, 4 epilogue warps, double-buffered TMEM
+// accumulators).
+
+template <int MODE>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    kan_conv3_kernel(const __grid_constant__ CUtensorMap xmap, const GemmParams p) {
+  constexpr int NBP = 8;
+  constexpr int IPS = KSTAGE / NBP;  // 32 channels per super-stage
+  constexpr int H = IPS / 4;         // inputs per producer thread quarter
+  constexpr int NPW = GEMM_PRODUCER_WARPS;
+  constexpr int W_X = NPW, W_MMA = NPW + 1, W_B = NPW + 2, W_EPI = NPW + 3;
+  constexpr bool SILU = (MODE == MODE_SILU);
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+
+  const int SA = p.SA, SB = p.SB, SX = p.SX;
+  const int BN = p.BN;
+  const int R = p.ext_rows;  // expanded rows per super-stage
+  const uint32_t b_slot = static_cast<uint32_t>(p.b_slot);
+  const uint32_t xesz = (p.x_kind == X_F32) ? 4u : 2u;
+  const int x_row_bytes = IPS * static_cast<int>(xesz);
+  const uint32_t x_bytes = static_cast<uint32_t>(R) * x_row_bytes;
+  const uint32_t a_code_bytes = static_cast<uint32_t>(R) * KSTAGE;  // [2 kblocks][R][128 B]
+  const uint32_t a_bytes = a_code_bytes + (SILU ? static_cast<uint32_t>(R) * 32u : 0u);
+  uint8_t* sB = smem;
+  uint8_t* sA = sB + static_cast<size_t>(SB) * b_slot;
+  uint8_t* sX = sA + static_cast<size_t>(SA) * a_bytes;
+  uint8_t* sT = sX + static_cast<size_t>(SX) * x_bytes;
+  const int tab_bytes = p.tab_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sT + tab_bytes);
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bars + 2 * SA + 2 * SB + 2 * SX + 9);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  pdl_trigger();
+
+  const int n_tiles = p.m_tiles * p.n_tiles_n;
+  const int tile_step = static_cast<int>(gridDim.x);
+  struct Tile {
+    int m0, n_tile, n0, y0;
+  };
+  auto tile_of = [&](int t) {
+    Tile r;
+    const int mt = t / p.n_tiles_n;
+    r.n_tile = t - mt * p.n_tiles_n;
+    r.m0 = mt * 128;
+    r.n0 = mt / p.tpi;
+    r.y0 = (mt % p.tpi) * p.bh;
+    return r;
+  };
+
+  auto bar_xfull = [&](int s) { return smem_u32(bars + s); };
+  auto bar_xempty = [&](int s) { return smem_u32(bars + SX + s); };
+  auto bar_afull = [&](int s) { return smem_u32(bars + 2 * SX + s); };
+  auto bar_aempty = [&](int s) { return smem_u32(bars + 2 * SX + SA + s); };
+  auto bar_bfull = [&](int s) { return smem_u32(bars + 2 * SX + 2 * SA + s); };
+  auto bar_bempty = [&](int s) { return smem_u32(bars + 2 * SX + 2 * SA + SB + s); };
+  uint64_t* bx = bars + 2 * SX + 2 * SA + 2 * SB;
+  auto bar_accfull = [&](int b) { return smem_u32(bx + b); };
+  auto bar_accempty = [&](int b) { return smem_u32(bx + 2 + b); };
+  const uint32_t bar_tab = smem_u32(bx + 8);
+
+  constexpr uint32_t tmem_cols = 512;
+  const uint32_t BNa = static_cast<uint32_t>((BN + 31) / 32 * 32);
+  const int nacc = p.nacc;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < SX; ++s) {
+      mbar_init(bar_xfull(s), 1);
+      mbar_init(bar_xempty(s), NPW);
+    }
+    for (int s = 0; s < SA; ++s) {
+      mbar_init(bar_afull(s), NPW);
+      mbar_init(bar_aempty(s), 1);
+    }
+    for (int s = 0; s < SB; ++s) {
+      mbar_init(bar_bfull(s), 1);
+      mbar_init(bar_bempty(s), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(bar_accfull(b), 1);
+      mbar_init(bar_accempty(b), 4);
+    }
+    mbar_init(bar_tab, 1);
+    mbar_fence_init();
+  }
+  if (warp == W_X && lane == 0) tma_prefetch(&xmap);
+  if (warp == W_MMA) tmem_alloc(smem_u32(s_tmem), tmem_cols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *s_tmem;
+
+  if (warp == W_X) {
+    // ================= activation loader: one window per super-stage ========
+    pdl_wait();
+    Ring rx(SX);
+    for (int t = blockIdx.x; t < n_tiles; t += tile_step) {
+      const Tile tl = tile_of(t);
+      for (int ss = 0; ss < p.n_ss; ++ss, rx.next()) {
+        const int kx = ss / p.cps, cc = ss - kx * p.cps;
+        mbar_wait(bar_xempty(rx.slot), rx.phase ^ 1);
+        if (lane == 0) {
+          mbar_arrive_tx(bar_xfull(rx.slot), x_bytes);
+          // rows y0-1 .. y0+bh, columns kx-1 .. kx-1+Wo-1 (zero outside)
+          tma_load_4d(smem_u32(sX + static_cast<size_t>(rx.slot) * x_bytes), &xmap, cc * IPS, kx - 1,
+                      tl.y0 - 1, tl.n0, bar_xfull(rx.slot));
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp == W_B) {
+    // ============== table + weight-tile loader: 3 taps per super-stage ======
+    if (lane == 0 && tab_bytes > 0) {
+      mbar_arrive_tx(bar_tab, static_cast<uint32_t>(tab_bytes));
+      bulk_load(smem_u32(sT), p.tab, static_cast<uint32_t>(tab_bytes), bar_tab);
+    }
+    __syncwarp();
+    Ring rb(SB);
+    for (int t = blockIdx.x; t < n_tiles; t += tile_step) {
+      const Tile tl = tile_of(t);
+      for (int q = 0; q < 3 * p.n_ss; ++q, rb.next()) {
+        mbar_wait(bar_bempty(rb.slot), rb.phase ^ 1);
+        if (lane == 0) {
+          const size_t wt = static_cast<size_t>(tl.n_tile) * 3 * p.n_ss + q;
+          mbar_arrive_tx(bar_bfull(rb.slot), b_slot);
+          bulk_load(smem_u32(sB + static_cast<size_t>(rb.slot) * b_slot), p.wt + wt * b_slot, b_slot,
+                    bar_bfull(rb.slot));
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp == W_MMA) {
+    // ============ MMA issuer: SS-mode, three row-shifted taps per stage ====
+    const uint32_t idesc = idesc_i8(BN, true);
+    Ring ra(SA), rb(SB);
+    int lt = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += tile_step, ++lt) {
+      const int ab = nacc == 2 ? (lt & 1) : 0;
+      const int use = nacc == 2 ? (lt >> 1) : lt;
+      mbar_wait(bar_accempty(ab), (use & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t dacc = tmem + static_cast<uint32_t>(ab) * BNa;
+      bool first = true;
+      for (int ss = 0; ss < p.n_ss; ++ss, ra.next()) {
+        mbar_wait(bar_afull(ra.slot), ra.phase);
+        tc_fence_after();
+        const uint32_t a_addr = smem_u32(sA + static_cast<size_t>(ra.slot) * a_bytes);
+        for (int ky = 0; ky < 3; ++ky, rb.next()) {
+          mbar_wait(bar_bfull(rb.slot), rb.phase);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t b_addr = smem_u32(sB + static_cast<size_t>(rb.slot) * b_slot);
+            const uint32_t row_off = static_cast<uint32_t>(ky * p.Wo / 8) * 1024u;  // whole SW128 atoms
+#pragma unroll
+            for (int kk = 0; kk < KSTAGE / 32; ++kk) {
+              const uint64_t ad =
+                  umma_desc_sw128(a_addr + (kk >> 2) * static_cast<uint32_t>(R) * 128u + row_off + 32 * (kk & 3));
+              const uint64_t bd = umma_desc_sw128(b_addr + (kk >> 2) * BN * 128 + 32 * (kk & 3));
+              mma_i8(dacc, ad, bd, idesc, (first && kk == 0) ? 0u : 1u);
+            }
+            if constexpr (SILU) {
+              // the tap's SiLU base term: K = 32 codes against the SW32 SiLU weights
+              const uint64_t ad = umma_desc_sw32(a_addr + a_code_bytes + static_cast<uint32_t>(ky * p.Wo / 8) * 256u);
+              const uint64_t bd = umma_desc_sw32(b_addr + BN * KSTAGE);
+              mma_i8(dacc, ad, bd, idesc, 1u);
+            }
+            tc_commit(bar_bempty(rb.slot));
+          }
+          __syncwarp();
+          first = false;
+        }
+        if (lane == 0) tc_commit(bar_aempty(ra.slot));
+        __syncwarp();
+      }
+      if (lane == 0) tc_commit(bar_accfull(ab));
+      __syncwarp();
+    }
+  } else if (warp < NPW) {
+    // ==================== producers: expand each window once ================
+    if (tab_bytes > 0) mbar_wait(bar_tab, 0);
+    const uint32_t* vals = reinterpret_cast<const uint32_t*>(sT);
+    const float* thr = reinterpret_cast<const float*>(sT + p.off_thr);
+    const uint8_t* silu_tab = sT + p.off_silu;
+    const uint2* c64 = reinterpret_cast<const uint2*>(sT + p.off_c64);
+    const int units = (R / 32) * 4;  // (32-row group, K quarter) pairs
+    Ring ra(SA), rx(SX);
+    for (int t = blockIdx.x; t < n_tiles; t += tile_step) {
+      const Tile tl = tile_of(t);
+      uint32_t rsum = 0;
+      for (int ss = 0; ss < p.n_ss; ++ss, ra.next(), rx.next()) {
+        const int kx = ss / p.cps;
+        mbar_wait(bar_xfull(rx.slot), rx.phase);
+        mbar_wait(bar_aempty(ra.slot), ra.phase ^ 1);
+        const uint8_t* xt = sX + static_cast<size_t>(rx.slot) * x_bytes;
+        uint8_t* at = sA + static_cast<size_t>(ra.slot) * a_bytes;
+        for (int u = warp; u < units; u += NPW) {
+          const int g = u >> 2, h = u & 3;
+          const int rr = 32 * g + lane;  // expanded row = input pixel of the window
+          const int wy = rr / p.Wo, wx = rr - wy * p.Wo;
+          const int iy = tl.y0 - 1 + wy, ix = wx + kx - 1;
+          const bool pad = static_cast<unsigned>(iy) >= static_cast<unsigned>(p.H) ||
+                           static_cast<unsigned>(ix) >= static_cast<unsigned>(p.W);
+          int a[H];
+          const int xoff = h * H * static_cast<int>(xesz);
+          if (p.x_kind == X_F32) {
+            uint32_t xr[H];
+            load_x<4 * H>(xt, rr, xoff, x_row_bytes, xr);
+#pragma unroll
+            for (int e = 0; e < H; ++e)
+              a[e] = pad ? p.lvl0 : lattice_level_tie(__uint_as_float(xr[e]), p.inv_step_f, p.lo_f, p.L, thr);
+          } else {
+            uint32_t xr[H / 2];
+            load_x<2 * H>(xt, rr, xoff, x_row_bytes, xr);
+#pragma unroll
+            for (int q = 0; q < H / 2; ++q) {
+              a[2 * q] = pad ? p.lvl0 : static_cast<int>(xr[q] & 0xFFFF);
+              a[2 * q + 1] = pad ? p.lvl0 : static_cast<int>(xr[q] >> 16);
+            }
+          }
+          uint32_t w[16], nw[2];
+          lut_row<NBP, MODE>(p, vals, c64, silu_tab, a, 0, w, rsum, nw);
+          // codes: row rr, K bytes [64h, 64h+64) of the SW128 tile
+          uint8_t* ab = at + (h >> 1) * R * 128 + (rr >> 3) * 1024 + (rr & 7) * 128;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int ch = (h & 1) * 4 + c;
+            *reinterpret_cast<uint4*>(ab + ((ch ^ (rr & 7)) << 4)) =
+                make_uint4(w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
+          }
+          if constexpr (SILU) {
+            // SiLU codes: row rr, bytes [8h, 8h+8) of the SW32 tile
+            uint8_t* sb = at + a_code_bytes + (rr >> 3) * 256 + (rr & 7) * 32 +
+                          ((((h >> 1) ^ ((rr >> 2) & 1))) << 4) + (h & 1) * 8;
+            *reinterpret_cast<uint2*>(sb) = make_uint2(nw[0], nw[1]);
+          }
+        }
+        // generic-proxy smem writes -> visible to the tensor core (async proxy)
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(bar_xempty(rx.slot));
+          mbar_arrive(bar_afull(ra.slot));
+        }
+      }
+    }
+  } else {
+    // ============================ epilogue ================================
+    if (tab_bytes > 0) mbar_wait(bar_tab, 0);
+    const int wq = warp & 3;
+    const int rloc = wq * 32 + lane;
+    const uint32_t t_row = tmem + (static_cast<uint32_t>(wq * 32) << 16);
+    int lt = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += tile_step, ++lt) {
+      const Tile tl = tile_of(t);
+      const int ab = nacc == 2 ? (lt & 1) : 0;
+      const int use = nacc == 2 ? (lt >> 1) : lt;
+      mbar_wait(bar_accfull(ab), use & 1);
+      tc_fence_after();
+      const uint32_t tacc = t_row + static_cast<uint32_t>(ab) * BNa;
+      const int row = tl.m0 + rloc;
+      float rv[32];  // residual prefetch: 32 columns in flight per thread
+#pragma unroll 1
+      for (int gq = 0; gq < BN / 4; ++gq) {
+        if (p.res_kind && (gq & 7) == 0) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int c = tl.n_tile * BN + (gq + q) * 4;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (row < p.M && c + 3 < p.N && gq + q < BN / 4)
+              v = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(p.res) +
+                                                   static_cast<size_t>(row) * p.ld_res + c);
+            else if (row < p.M && gq + q < BN / 4)
+              for (int e = 0; e < 4; ++e)
+                if (c + e < p.N)
+                  (&v.x)[e] = reinterpret_cast<const float*>(p.res)[static_cast<size_t>(row) * p.ld_res + c + e];
+            rv[4 * q] = v.x;
+            rv[4 * q + 1] = v.y;
+            rv[4 * q + 2] = v.z;
+            rv[4 * q + 3] = v.w;
+          }
+        }
+        uint32_t ra[4];
+        tmem_ld4(tacc + gq * 4, ra);
+        tmem_wait_ld();
+        const int col0 = tl.n_tile * BN + gq * 4;
+        if (row >= p.M) continue;
+        const size_t base = static_cast<size_t>(row) * p.ld_out + col0;
+        const int nvalid = min(4, p.N - col0);
+        if (p.epi == EPI_RAW) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (e < nvalid) reinterpret_cast<uint32_t*>(p.out)[base + e] = ra[e];
+          continue;
+        }
+        double y[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int j = min(col0 + e, p.N - 1);
+          const long long v = static_cast<long long>(static_cast<int32_t>(ra[e])) - (SILU ? p.corr_b[j] : 0ll);
+          y[e] = __dmul_rn(static_cast<double>(v), p.fs[j]);
+          if (p.res_kind && e < nvalid) y[e] = __dadd_rn(y[e], static_cast<double>(rv[(gq & 7) * 4 + e]));
+        }
+        if (p.epi == EPI_F32 && p.out_hw > 0) {
+          const int hw = p.out_hw;
+          const int img = row / hw;
+          float* o = reinterpret_cast<float*>(p.out) + static_cast<size_t>(img) * p.N * hw +
+                     static_cast<size_t>(col0) * hw + (row - img * hw);
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (e < nvalid) o[static_cast<size_t>(e) * hw] = __double2float_rn(y[e]);
+        } else if (p.epi == EPI_F32) {
+          float* o = reinterpret_cast<float*>(p.out) + base;
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (e < nvalid) o[e] = __double2float_rn(y[e]);
+        } else {  // EPI_LEVEL
+          uint16_t* o = reinterpret_cast<uint16_t*>(p.out) + base;
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (e < nvalid)
+              o[e] = static_cast<uint16_t>(
+                  lattice_level_fast(y[e], p.n_lo, p.n_hi_open, p.n_step, p.n_inv_step, p.n_L));
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_accempty(ab));
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == W_MMA) {
+    tc_fence_after();
+    tmem_dealloc(tmem, tmem_cols);
+  }
+}
+
+size_t conv3_smem_bytes(int BN, int R, int SA, int SB, int SX, int x_kind, int tab_bytes, bool silu) {
+  const size_t b_slot = (static_cast<size_t>(BN) * (KSTAGE + (silu ? 32 : 0)) + 1023) / 1024 * 1024;
+  const size_t a = static_cast<size_t>(R) * (KSTAGE + (silu ? 32 : 0));
+  const size_t x = static_cast<size_t>(R) * (KSTAGE / 8) * (x_kind == X_F32 ? 4 : 2);
+  return 1024 + SB * b_slot + SA * a + SX * x + static_cast<size_t>(tab_bytes) + (2 * SA + 2 * SB + 2 * SX + 9) * 8 +
+         16;
+}
+
+cudaError_t launch_conv3(int mode, const CUtensorMap& xmap, const GemmParams& p, size_t smem, cudaStream_t st) {
+  static size_t configured[3] = {0, 0, 0};  // per kernel variant (same function type)
+  auto go = [&](auto kfn) -> cudaError_t {
+    if (smem > configured[mode]) {
+      cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      if (e != cudaSuccess) return e;
+      configured[mode] = smem;
+    }
+    static int n_sm = 0;
+    if (n_sm == 0) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+      if (n_sm <= 0) n_sm = 148;
+    }
+    const int tiles = p.n_tiles_n * p.m_tiles;
+    return launch_pdl(kfn, dim3(static_cast<unsigned>(tiles < n_sm ? tiles : n_sm)), dim3(GEMM_THREADS), smem, st,
+                      xmap, p);
+  };
+  if (mode == MODE_SILU) return go(kan_conv3_kernel<MODE_SILU>);
+  return go(kan_conv3_kernel<MODE_PLAIN>);
+}

@@ -42,6 +42,8 @@ cudaError_t launch_argmax(const float* logits, int64_t M, int N, int ld, int32_t
                           cudaStream_t st);
 cudaError_t launch_fp32_layer(const Fp32Params& p, cudaStream_t st);
 cudaError_t launch_small_layer(const SmallParams& p, cudaStream_t st);
+cudaError_t launch_conv3(int mode, const CUtensorMap& xmap, const GemmParams& p, size_t smem, cudaStream_t st);
+size_t conv3_smem_bytes(int BN, int R, int SA, int SB, int SX, int x_kind, int tab_bytes, bool silu);
 size_t small_smem_bytes(const SmallParams& p);
 cudaError_t launch_nchw_to_nhwc(bool levels, const float* in, int64_t n_img, int C, int HW,
                                 void* out, int ldc, const float* thr, float lo, float inv_step,
@@ -138,6 +140,11 @@ struct PreparedLayer {
   DevBuf<unsigned long long> swq;  // [n_in][N] 8 basis weights per (input, output)
   DevBuf<int8_t> swqb;             // [N][n_in8] SiLU base weights
   DevBuf<int8_t> swqb_plain;       // [N][n_in] SiLU base weights (fused tail layer), padded to 16 B
+  // ky-shared 3x3 conv kernel: weights as [n_tile][(kx, chunk)][ky] tap slots
+  // of b_slot3 bytes (SW128 codes part + SW32 SiLU part)
+  bool conv3 = false;
+  int b_slot3 = 0;
+  DevBuf<uint8_t> wt3;
   int IPS = 0, GS = 0, n_spline_stages = 0, n_groups = 0, total_stages = 0, silu = 0;
   DevBuf<uint8_t> wt;       // tcgen05 paths: pre-tiled weights
   DevBuf<float> w32, wb32;  // fp32 path
@@ -687,6 +694,45 @@ void prepare_gemm_layer(kan_engine* e, const Layer& l, PreparedLayer& pl, bool b
   }
   pl.wt.upload(wt);
 
+  // ky-shared 3x3 stride-1 pad-1 conv kernel (kan_conv3.cuh), LUT path
+  pl.conv3 = false;
+  if (!bf16 && l.type == L_CONV && l.kernel == 3 && l.stride == 1 && l.padding == 1 && nbp == 8 &&
+      pl.b_signed && std::getenv("KAN_NO_CONV3") == nullptr) {
+    const int Wo = l.out.w, Ho = l.out.h;
+    if (Wo % 8 == 0 && 128 % Wo == 0 && Ho * Wo >= 128 && Ho % (128 / Wo) == 0) {
+      pl.conv3 = true;
+      const int cps = pl.cps;
+      const int slot_raw = BN * (KSTAGE + (pl.silu ? 32 : 0));
+      pl.b_slot3 = (slot_raw + 1023) / 1024 * 1024;
+      std::vector<uint8_t> w3(static_cast<size_t>(pl.n_tiles_n) * 3 * 3 * cps * pl.b_slot3, 0);
+      for (int nt = 0; nt < pl.n_tiles_n; ++nt)
+        for (int kx = 0; kx < 3; ++kx)
+          for (int cc = 0; cc < cps; ++cc)
+            for (int ky = 0; ky < 3; ++ky) {
+              const size_t q = (static_cast<size_t>(nt) * 3 * cps + (kx * cps + cc)) * 3 + ky;
+              uint8_t* tile = w3.data() + q * pl.b_slot3;
+              const int t = ky * 3 + kx;
+              for (int n = 0; n < BN; ++n) {
+                const int j = nt * BN + n;
+                if (j >= N) continue;
+                for (int ii = 0; ii < 32; ++ii) {
+                  const int c = cc * 32 + ii;
+                  if (c >= l.c_in) break;
+                  const int ir = c * 9 + t;  // reference im2col column (layers.hpp:140-149)
+                  for (int b = 0; b < nb; ++b)
+                    tile[tile_off(BN, n, ii * 8 + b)] = static_cast<uint8_t>(qw_s8[(static_cast<size_t>(ir) * nb + b) * N + j]);
+                  if (pl.silu) {
+                    const size_t off = static_cast<size_t>(BN) * KSTAGE + (n >> 3) * 256 + (n & 7) * 32 +
+                                       ((((ii >> 4) ^ ((n >> 2) & 1))) << 4) + (ii & 15);
+                    tile[off] = static_cast<uint8_t>(qwb[static_cast<size_t>(ir) * N + j]);
+                  }
+                }
+              }
+            }
+      pl.wt3.upload(w3);
+    }
+  }
+
   // small-N layers run on CUDA cores (kan_small_layer_kernel): same integer
   // weights, laid out per (input, output) in the GEMM input order
   pl.small = !bf16 && nbp == 8 && N <= 16 && l.type == L_LINEAR && pl.b_signed &&
@@ -1070,6 +1116,80 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
   p.m_tiles = static_cast<int>((M + 127) / 128);
   p.dbg = nullptr;
   p.dbg_flags = e->dbg_flags;
+  // ky-shared 3x3 conv kernel: full tile grids (persistent), no zero point
+  // (it pays off on stored-level inputs with full channel chunks; fp32 inputs
+  // and the few-channel stem stay on the general kernel, measured faster there)
+  if (pl.conv3 && io.conv && io.epi != EPI_RAW && !io.fuse && io.x_kind == X_U16 && io.conv->c_in >= 32) {
+    const Layer& l = *io.conv;
+    const int Wo = l.out.w, bh = 128 / Wo;
+    const int tiles3 = static_cast<int>((M + 127) / 128) * pl.n_tiles_n;
+    if (tiles3 >= 148) {
+      const int R = (bh + 2) * Wo;
+      const bool silu = pl.silu != 0;
+      int variant = -1, SA = 2, SB = 0, SX = 2;
+      for (int v : {2, 0}) {  // lane-private vals if it leaves >= 3 tap slots
+        if (e->tabs[v].bytes == 0) continue;
+        for (SB = 4; SB >= 2; --SB)
+          if (conv3_smem_bytes(pl.BN, R, SA, SB, SX, io.x_kind, e->tabs[v].bytes, silu) <= 232448) break;
+        if (SB >= (v == 2 ? 3 : 2)) {
+          variant = v;
+          break;
+        }
+      }
+      if (variant >= 0) {
+        const auto& ts = e->tabs[variant];
+        p.SA = SA;
+        p.SB = SB;
+        p.SX = SX;
+        p.nacc = 2;
+        p.splits = 1;
+        p.tab = ts.buf.p;
+        p.tab_bytes = ts.bytes;
+        p.off_thr = ts.off_thr;
+        p.off_silu = ts.off_silu;
+        p.off_c64 = ts.off_c64;
+        p.rep = variant;
+        p.wt = pl.wt3.p;
+        p.ext_rows = R;
+        p.n_ss = 3 * pl.cps;
+        p.b_slot = pl.b_slot3;
+        p.conv = 1;
+        p.ksz = 3;
+        p.cstride = 1;
+        p.pad = 1;
+        p.cps = pl.cps;
+        p.H = l.in.h;
+        p.W = l.in.w;
+        p.Ho = l.out.h;
+        p.Wo = Wo;
+        p.bh = bh;
+        p.bn_img = 1;
+        p.tpi = l.out.h / bh;
+        p.pimg = 128;
+        p.lvl0 = static_cast<int>(e->lat.quantize(0.0));
+        p.epi = io.epi;
+        p.out = io.out;
+        p.ld_out = static_cast<int>(io.ld_out);
+        p.fs = pl.fs.p;
+        p.corr_b = pl.corr_b.p;
+        p.n_lo = e->grid.lo;
+        p.n_hi_open = e->grid.hi_open();
+        p.n_step = e->lat.step;
+        p.n_inv_step = 1.0 / e->lat.step;
+        p.n_L = static_cast<int>(e->lat.L);
+        p.res_kind = io.res_kind;
+        p.res = io.res;
+        p.ld_res = static_cast<int>(io.ld_res);
+        p.out_hw = io.out_hw;
+        // the (bh+2)-row window of one (kx, chunk): box rows bh+2, one image
+        const CUtensorMap xmap3 = make_conv_xmap(io, l, pl.IPS, bh + 2, 1);
+        const size_t smem = conv3_smem_bytes(pl.BN, R, SA, SB, SX, io.x_kind, ts.bytes, silu);
+        ck(launch_conv3(silu ? 2 : 0, xmap3, p, smem, st), "conv3 launch");
+        e->last_launches += 1;
+        return;
+      }
+    }
+  }
   // table variant: the lane-private copies when they leave deep enough rings
   int SA = 2, SB = 2, SX = 2;
   int variant = 0;

@@ -563,7 +563,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   // Epilogue of 4 accumulator columns of one output row (fp64, then the
   // requested output: raw, fp32, next-layer level, int8), shared by the
   // persistent epilogue warps and the split-K reduction.
-  auto finish4 = [&](int row, int col0, const uint32_t(&ra)[4], int32_t rs) {
+  auto finish4 = [&](int row, int col0, const uint32_t(&ra)[4], int32_t rs, const float* rpre = nullptr) {
     if (row >= p.M) return;
     const size_t base = static_cast<size_t>(row) * p.ld_out + col0;
     const int nvalid = min(4, p.N - col0);
@@ -590,8 +590,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
     }
     if (p.res_kind) {
-      // residual add of a stored fp32 tensor (engine extension, GemmParams::res_kind)
-      const float* rr = reinterpret_cast<const float*>(p.res) + static_cast<size_t>(row) * p.ld_res + col0;
+      // residual add of a stored fp32 tensor (engine extension, GemmParams::res_kind);
+      // rpre: values the persistent epilogue prefetched
+      const float* rr = rpre ? rpre : reinterpret_cast<const float*>(p.res) + static_cast<size_t>(row) * p.ld_res + col0;
 #pragma unroll
       for (int e = 0; e < 4; ++e)
         if (e < nvalid) y[e] = __dadd_rn(y[e], static_cast<double>(rr[e]));
@@ -919,12 +920,25 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           if (lane == 0) mbar_arrive(bar_rsempty(rb2));
         }
         const uint32_t tacc = t_row + static_cast<uint32_t>(ab) * BNa;
+        const int row = tl.m0 + rloc;
+        float rv[32];  // residual prefetch: 32 columns in flight per thread
 #pragma unroll 1
         for (int gq = 0; gq < ngroups; ++gq) {
+          if (p.res_kind && (gq & 7) == 0) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const int c = tl.n_tile * BN + (gq + q) * 4;
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                rv[4 * q + e] = (row < p.M && gq + q < ngroups && c + e < p.N)
+                                    ? reinterpret_cast<const float*>(p.res)[static_cast<size_t>(row) * p.ld_res + c + e]
+                                    : 0.f;
+            }
+          }
           uint32_t ra[4];
           tmem_ld4(tacc + gq * 4, ra);
           tmem_wait_ld();
-          finish4(tl.m0 + rloc, tl.n_tile * BN + gq * 4, ra, rs);
+          finish4(row, tl.n_tile * BN + gq * 4, ra, rs, p.res_kind ? rv + (gq & 7) * 4 : nullptr);
         }
         tc_fence_before();
         __syncwarp();
@@ -999,8 +1013,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         int acc[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) acc[j] = 0;
+        const bool valid_row = tl.m0 + rl < p.M;  // rows past M were never written
         for (int i = sub; i < n_in2; i += TPR) {
-          const int a = f_lv[rl * BN + i];
+          const int a = valid_row ? f_lv[rl * BN + i] : 0;
           const uint32_t v = p.rep ? vals[((static_cast<uint32_t>(a) & mask) << 5) | static_cast<uint32_t>(lane)]
                                    : vals[static_cast<uint32_t>(a) & mask];
           const uint32_t sft = 8u * static_cast<uint32_t>(a >> p.k);
@@ -1107,6 +1122,8 @@ static cudaError_t launch_impl(const CUtensorMap& xmap, const GemmParams& p, siz
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
+
+#include "kan_conv3.cuh"
 
 int gemm_ips(bool bf16, int nbp) { return KSTAGE / (nbp * (bf16 ? 2 : 1)); }
 int gemm_gs(bool bf16, int nbp) { return KSTAGE / (bf16 ? 2 : 1) / gemm_ips(bf16, nbp); }
@@ -1298,13 +1315,13 @@ cudaError_t launch_small_layer(const SmallParams& p, cudaStream_t st) {
   constexpr int TPR = 8, THREADS = 256;
   const size_t smem = small_smem_bytes(p);
   const unsigned blocks = static_cast<unsigned>((static_cast<int64_t>(p.M) * TPR + THREADS - 1) / THREADS);
+  static size_t configured[3] = {0, 0, 0};  // per kernel variant (same function type)
   auto go = [&](auto kfn) -> cudaError_t {
-    static size_t configured = 0;
-    if (smem > configured) {
+    if (smem > configured[p.mode]) {
       cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            static_cast<int>(smem));
       if (e != cudaSuccess) return e;
-      configured = smem;
+      configured[p.mode] = smem;
     }
     return launch_pdl(kfn, dim3(blocks), dim3(THREADS), smem, st, p);
   };

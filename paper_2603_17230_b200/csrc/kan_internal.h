@@ -85,6 +85,11 @@ struct GemmParams {
   const void* res;
   int ld_res;
   int out_hw;  // EPI_F32: >0 writes NCHW (H*W per channel), 0 row-major
+  // ky-shared 3x3 conv kernel (kan_conv3_kernel): ext_rows = (bh+2)*Wo input
+  // pixels expanded once per (kx, channel chunk) "super-stage" and read by the
+  // three ky taps through descriptors offset by ky*Wo rows; n_ss super-stages
+  // per tile; b_slot = bytes of one tap's weight tile (spline + SiLU parts)
+  int ext_rows, n_ss, b_slot;
   // fused output layer (split-K launches, LUT path): the reduced hidden levels
   // of each CTA's rows stay in smem and feed the next, small KAN layer
   // (N2 <= 16, NBP = 8, per-channel weights) inside this kernel, which writes

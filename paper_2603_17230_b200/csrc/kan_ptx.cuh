@@ -177,6 +177,18 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr) {
   return d;
 }
 
+// UMMA shared-memory descriptor, K-major 32-byte swizzle: 8-row x 32-byte
+// atoms (SBO = 256 B), 16-byte chunk ^= row bit 2 (the TMA SWIZZLE_32B layout).
+__device__ __forceinline__ uint64_t umma_desc_sw32(uint32_t smem_addr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((smem_addr & 0x3FFFF) >> 4);  // start address
+  d |= static_cast<uint64_t>(1) << 16;                      // LBO (single atom along K)
+  d |= static_cast<uint64_t>(256 >> 4) << 32;               // SBO
+  d |= static_cast<uint64_t>(1) << 46;                      // version
+  d |= static_cast<uint64_t>(6) << 61;                      // SWIZZLE_32B
+  return d;
+}
+
 // Instruction descriptors (M = 128, both operands K-major).
 __host__ __device__ constexpr uint32_t idesc_i8(int n, bool b_signed) {
   return (2u << 4)                             // D = s32

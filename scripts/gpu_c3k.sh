@@ -1,0 +1,5 @@
+cd $GRAFT_REPO_ROOT
+timeout -s KILL 600 python -m pytest tests -m gpu -q -x --timeout 60 --timeout-method=thread -p no:cacheprovider > /tmp/tall.log 2>&1; echo PYTEST $?; tail -1 /tmp/tall.log | cut -c1-200
+timeout -s KILL 300 python bench.py --config c4 --steps 1000 --warmup 20 --no-cpu-baseline > /tmp/b.json 2>/tmp/b.err; echo "BENCH c4 $?"; tail -2 /tmp/b.err
+python -c "import json;d=json.load(open('/tmp/b.json'));r=d['roofline'];print(round(d['value']),round(d['ms_per_step']*1e3,1),'us',r['bound'],round(r['frac'],3),[round(v*1e3,1) for v in r['layer_avg_ms']])"
+timeout -s KILL 120 python scripts/prof_layer.py --config c5 --iters 3 > /tmp/p5.log 2>&1; tail -21 /tmp/p5.log | awk '{s+=$3; printf "%s ", $3} END {print " total", s}'

@@ -5,6 +5,8 @@ adds, pooling, flatten), through the C ABI, against the CPU oracle
 
 Bar: bit-exact on the integer LUT path; 1e-2 norm-relative on the bf16 path.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -149,3 +151,44 @@ def test_bf16_conv_vs_reference(ref):
     r = np.stack([ref.conv_forward(5, 3, x[n].reshape(16, 8, 8).astype(np.float64), Ws[0], 16, 3,
                                    1, 1) for n in range(2)])
     assert rel_err(y, r) < 1e-2
+
+
+# ky-shared 3x3 kernel (kan_conv3.cuh): taken for 3x3/s1/p1 convs whose tile
+# grid fills the GPU (>= 148 tiles); smaller grids use the general kernel.
+CONV3_CASES = [
+    # C, H, W, c_out, silu, batch
+    (64, 32, 32, 64, True, 20),    # C4 shape, 160 tiles
+    (40, 16, 16, 48, False, 80),   # partial channel chunk, 16x16 maps
+    (32, 32, 32, 24, True, 19),    # one chunk
+]
+
+
+@pytest.mark.parametrize("C,H,W,co,silu,batch", CONV3_CASES)
+def test_conv3_kernel_bit_exact(oracle, C, H, W, co, silu, batch):
+    desc = conv_desc(C, H, W, co, 3, 1, 1)
+    Ws, Bs = weights_for(desc, seed=C + batch, silu=silu)
+    x = np.random.default_rng(C + co).uniform(-1.05, 1.05, (batch, C * H * W)).astype(np.float32)
+    e = build(desc, Ws, Bs, mode="bspline-lut", lut_k=8, lut_h=8, bits_w=8, w_scheme=W_PER_CHANNEL_SYM,
+              silu_base=silu)
+    y = e.model_forward(to_dev(x)).cpu().numpy()
+    yo = oracle.int_model_forward(desc, Ws, Bs, x, 8, 8, W_PER_CHANNEL_SYM, 8)
+    np.testing.assert_array_equal(y, yo.astype(np.float32).reshape(batch, -1))
+
+
+def test_conv3_matches_general_kernel_in_a_residual_stage():
+    """Stage-1 blocks at 32x32 take the ky-shared kernel (fp32-stored block
+    inputs and level inputs); the result is bit-identical to the general
+    gather-GEMM kernel (KAN_NO_CONV3)."""
+    layers = configs.reskan18_layers(width=(16, 32), n_classes=10, in_ch=3)
+    desc = {"name": "r", "grid": {"intervals": 5, "degree": 3}, "input": [3, 32, 32],
+            "conv_output": "floor", "layers": layers}
+    Ws, Bs = weights_for(desc, seed=21)
+    x = np.random.default_rng(21).uniform(-1, 1, (20, 3 * 1024)).astype(np.float32)
+    opts = dict(mode="bspline-lut", lut_k=8, lut_h=3, bits_w=8, w_scheme=W_PER_CHANNEL_SYM, silu_base=True)
+    y3 = build(desc, Ws, Bs, **opts).model_forward(to_dev(x)).cpu().numpy()
+    os.environ["KAN_NO_CONV3"] = "1"
+    try:
+        yg = build(desc, Ws, Bs, **opts).model_forward(to_dev(x)).cpu().numpy()
+    finally:
+        del os.environ["KAN_NO_CONV3"]
+    np.testing.assert_array_equal(y3, yg)
