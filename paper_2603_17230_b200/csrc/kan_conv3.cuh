@@ -47,7 +47,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   uint8_t* sT = sX + static_cast<size_t>(SX) * x_bytes;
   const int tab_bytes = p.tab_bytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sT + tab_bytes);
-  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bars + 2 * SA + 2 * SB + 2 * SX + 9);
+  double* s_cols = reinterpret_cast<double*>(bars + 2 * SA + 2 * SB + 2 * SX + 9);  // [2][BN] per tile
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(s_cols + 2 * BN);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -276,6 +277,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int use = nacc == 2 ? (lt >> 1) : lt;
       mbar_wait(bar_accfull(ab), use & 1);
       tc_fence_after();
+      // the tile's column constants, staged in smem (see kan_gather_gemm_kernel)
+      asm volatile("bar.sync 4, 128;" ::: "memory");
+      for (int i = static_cast<int>(threadIdx.x) - 32 * W_EPI; i < BN; i += 128) {
+        const int j = min(tl.n_tile * BN + i, p.N - 1);
+        s_cols[i] = p.fs[j];
+        s_cols[BN + i] = SILU ? static_cast<double>(p.corr_b[j]) : 0.0;
+      }
+      asm volatile("bar.sync 4, 128;" ::: "memory");
       const uint32_t tacc = t_row + static_cast<uint32_t>(ab) * BNa;
       const int row = tl.m0 + rloc;
       float rv[32];  // residual prefetch: 32 columns in flight per thread
@@ -315,9 +324,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         double y[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const int j = min(col0 + e, p.N - 1);
-          const long long v = static_cast<long long>(static_cast<int32_t>(ra[e])) - (SILU ? p.corr_b[j] : 0ll);
-          y[e] = __dmul_rn(static_cast<double>(v), p.fs[j]);
+          const int jl = gq * 4 + e;
+          const long long v = static_cast<long long>(static_cast<int32_t>(ra[e])) -
+                              (SILU ? static_cast<long long>(s_cols[BN + jl]) : 0ll);
+          y[e] = __dmul_rn(static_cast<double>(v), s_cols[jl]);
           if (p.res_kind && e < nvalid) y[e] = __dadd_rn(y[e], static_cast<double>(rv[(gq & 7) * 4 + e]));
         }
         if (p.epi == EPI_F32 && p.out_hw > 0) {
@@ -361,7 +371,7 @@ size_t conv3_smem_bytes(int BN, int R, int SA, int SB, int SX, int x_kind, int t
   const size_t a = static_cast<size_t>(R) * (KSTAGE + (silu ? 32 : 0));
   const size_t x = static_cast<size_t>(R) * (KSTAGE / 8) * (x_kind == X_F32 ? 4 : 2);
   return 1024 + SB * b_slot + SA * a + SX * x + static_cast<size_t>(tab_bytes) + (2 * SA + 2 * SB + 2 * SX + 9) * 8 +
-         16;
+         2 * static_cast<size_t>(BN) * 8 + 16;
 }
 
 cudaError_t launch_conv3(int mode, const CUtensorMap& xmap, const GemmParams& p, size_t smem, cudaStream_t st) {

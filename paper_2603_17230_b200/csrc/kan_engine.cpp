@@ -17,6 +17,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <limits>
 #include <memory>
 #include <string>
 #include <vector>
@@ -42,6 +43,8 @@ cudaError_t launch_argmax(const float* logits, int64_t M, int N, int ld, int32_t
                           cudaStream_t st);
 cudaError_t launch_fp32_layer(const Fp32Params& p, cudaStream_t st);
 cudaError_t launch_small_layer(const SmallParams& p, cudaStream_t st);
+cudaError_t launch_rows_to_levels(const float* x, int64_t M, int n, int ld_x, uint16_t* out, int ld_o,
+                                  const float* thr, float nlo_step, float inv_step, int L, cudaStream_t st);
 cudaError_t launch_conv3(int mode, const CUtensorMap& xmap, const GemmParams& p, size_t smem, cudaStream_t st);
 size_t conv3_smem_bytes(int BN, int R, int SA, int SB, int SX, int x_kind, int tab_bytes, bool silu);
 size_t small_smem_bytes(const SmallParams& p);
@@ -240,13 +243,17 @@ struct kan_engine {
   std::vector<DevBuf<uint8_t>> slots;
   DevBuf<float> xstage;
   DevBuf<uint8_t> xnhwc;  // NHWC copy of an image model's input
+  DevBuf<uint16_t> xlev;  // level prepass of a large fp32-input dense layer
   DevBuf<float> logits_tmp;
   DevBuf<uint8_t> io_in, io_out;
   int last_launches = 0;
   // optional per-CTA phase timestamps of each layer's last launch (tuning aid)
   bool timeline = false;
   int dbg_flags = 0;  // KAN_DBG_FLAGS (tuning experiments only)
-  int force_tab = -1;  // KAN_TABLES=0/1 forces the table variant (tuning only)
+  int force_tab = -1;  // KAN_TABLES=0/1/2 forces the table variant (tuning only)
+  // fp32-input dense layers with at least this many activations get the level
+  // prepass (KAN_LEVEL_PREPASS_MIN; tests lower it to exercise the path)
+  int64_t prepass_min = std::numeric_limits<int64_t>::max();
   std::vector<DevBuf<unsigned long long>> timeline_buf;
   std::vector<int64_t> timeline_ctas;
   // per-layer kernel timing (kan_engine_set_profiling)
@@ -983,6 +990,10 @@ void configure(kan_engine* e, const kan_config* c) {
   e->timeline = std::getenv("KAN_TIMELINE") != nullptr;
   e->dbg_flags = std::getenv("KAN_DBG_FLAGS") ? std::atoi(std::getenv("KAN_DBG_FLAGS")) : 0;
   e->force_tab = std::getenv("KAN_TABLES") ? std::atoi(std::getenv("KAN_TABLES")) : -1;
+  // off by default: on C3 the prepass saves layer 0 ~50 us but costs ~260 us
+  // itself (measured); the path stays available and tested
+  e->prepass_min = std::getenv("KAN_LEVEL_PREPASS_MIN") ? std::atoll(std::getenv("KAN_LEVEL_PREPASS_MIN"))
+                                                        : std::numeric_limits<int64_t>::max();
   e->timeline_buf.clear();
   e->timeline_buf.resize(static_cast<size_t>(e->n_kan));
   e->timeline_ctas.assign(static_cast<size_t>(e->n_kan), 0);
@@ -1520,6 +1531,23 @@ void forward(kan_engine* e, const float* x, int64_t M, void* out, cudaStream_t s
     io.x = src.p;
     io.x_kind = src.kind;
     io.ld_x = src.ld;
+    // large fp32-input dense layers: levels first (HBM-bound prepass), so the
+    // gather GEMM reads 2-byte levels and its producers skip the level
+    // arithmetic (small layers keep the in-kernel path: their steps are
+    // latency-bound)
+    if (lut && !conv && src.kind == X_F32 && !src.nchw && !(pl.small) &&
+        rows * static_cast<int64_t>(pl.n_in) >= e->prepass_min) {
+      const int64_t ldl = pitch16(pl.n_in, 2);
+      e->xlev.alloc(static_cast<size_t>(rows * ldl));
+      ck(launch_rows_to_levels(static_cast<const float*>(src.p), rows, pl.n_in, static_cast<int>(src.ld), e->xlev.p,
+                               static_cast<int>(ldl), e->d_thr.p, static_cast<float>(-e->grid.lo / e->lat.step),
+                               static_cast<float>(1.0 / e->lat.step), static_cast<int>(e->lat.L), st),
+         "level prepass");
+      e->last_launches += 1;
+      io.x = e->xlev.p;
+      io.x_kind = X_U16;
+      io.ld_x = ldl;
+    }
     if (conv) {
       if (src.nchw) throw LogicError("conv input must be stored NHWC");
       io.conv = &l;

@@ -456,7 +456,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int tab_bytes = BF16 ? 0 : p.tab_bytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sT + tab_bytes);
   int32_t* s_rowsum = reinterpret_cast<int32_t*>(bars + 2 * SA + 2 * SB + 2 * SX + 9);  // [2][4][128]
-  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(s_rowsum + 2 * 4 * 128);
+  // the current tile's column constants: scale fs[j] and SiLU correction (as double)
+  double* s_cols = reinterpret_cast<double*>(s_rowsum + 2 * 4 * 128);  // [2][BN]
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(s_cols + 2 * BN);
   // SiLU code staging (MODE_SILU): word wd of K-quarter h of row r at
   // ((h*8 + wd/2)*128 + r)*2 + (wd&1) -- written once per spline stage, read
   // back by the same thread for the group's base stage (conflict-free).
@@ -560,6 +562,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *s_tmem;
 
+  // Stage tile n_tile's column constants (fs, SiLU correction) in smem: the
+  // epilogue reads them per element, and global loads there would serialize
+  // one memory latency per column.  Threads [t0, t0 + nt) of the caller.
+  auto load_cols = [&](int n_tile, int t0, int nt) {
+    if constexpr (!BF16 && MODE != MODE_ZP) {
+      for (int i = static_cast<int>(threadIdx.x) - t0; i < BN; i += nt) {
+        const int j = min(n_tile * BN + i, p.N - 1);
+        s_cols[i] = p.fs[j];
+        s_cols[BN + i] = SILU ? static_cast<double>(p.corr_b[j]) : 0.0;
+      }
+    }
+  };
   // Epilogue of 4 accumulator columns of one output row (fp64, then the
   // requested output: raw, fp32, next-layer level, int8), shared by the
   // persistent epilogue warps and the split-K reduction.
@@ -585,8 +599,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             static_cast<long long>(static_cast<int32_t>(ra[e])) - p.z_w * static_cast<long long>(rs);
         y[e] = __dmul_rn(static_cast<double>(v), p.f_tensor);
       } else {
-        const long long v = static_cast<long long>(static_cast<int32_t>(ra[e])) - (SILU ? p.corr_b[j] : 0ll);
-        y[e] = __dmul_rn(static_cast<double>(v), p.fs[j]);
+        // column constants staged in smem for the tile (load_cols)
+        const int jl = j - (j / BN) * BN;
+        const long long v = static_cast<long long>(static_cast<int32_t>(ra[e])) -
+                            (SILU ? static_cast<long long>(s_cols[BN + jl]) : 0ll);
+        y[e] = __dmul_rn(static_cast<double>(v), s_cols[jl]);
       }
     }
     if (p.res_kind) {
@@ -619,16 +636,29 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     } else if (p.epi == EPI_LEVEL) {
       // fused output layer: the levels stay in this CTA's smem row buffer
       uint16_t* o = p.f_on ? f_lv + (row & 127) * BN + (col0 % BN) : reinterpret_cast<uint16_t*>(p.out) + base;
+      uint32_t a[4];
 #pragma unroll
       for (int e = 0; e < 4; ++e)
-        if (e < nvalid)
-          o[e] = static_cast<uint16_t>(
-              lattice_level_fast(y[e], p.n_lo, p.n_hi_open, p.n_step, p.n_inv_step, p.n_L));
+        a[e] = static_cast<uint32_t>(lattice_level_fast(y[e], p.n_lo, p.n_hi_open, p.n_step, p.n_inv_step, p.n_L));
+      if (nvalid == 4 && (reinterpret_cast<uintptr_t>(o) & 7) == 0) {
+        *reinterpret_cast<uint2*>(o) = make_uint2(a[0] | (a[1] << 16), a[2] | (a[3] << 16));  // one 8-byte store
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (e < nvalid) o[e] = static_cast<uint16_t>(a[e]);
+      }
     } else {  // EPI_I8
       int8_t* o = reinterpret_cast<int8_t*>(p.out) + base;
+      uint32_t q[4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e)
-        if (e < nvalid) o[e] = static_cast<int8_t>(requant_i8(y[e], p.out_scale, p.inv_out_scale));
+      for (int e = 0; e < 4; ++e) q[e] = static_cast<uint32_t>(requant_i8(y[e], p.out_scale, p.inv_out_scale)) & 0xFFu;
+      if (nvalid == 4 && (reinterpret_cast<uintptr_t>(o) & 3) == 0) {
+        *reinterpret_cast<uint32_t*>(o) = q[0] | (q[1] << 8) | (q[2] << 16) | (q[3] << 24);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (e < nvalid) o[e] = static_cast<int8_t>(q[e]);
+      }
     }
   };
   // Role loops run on whole warps (all lanes wait, lane 0 issues) so the warps
@@ -911,6 +941,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         mbar_wait(bar_accfull(ab), use & 1);
         tc_fence_after();
         if (threadIdx.x == 32 * W_EPI && lt == 0) stamp(4);
+        // all epilogue warps are past the previous tile: restage the columns
+        asm volatile("bar.sync 4, 128;" ::: "memory");
+        load_cols(tl.n_tile, 32 * W_EPI, 128);
+        asm volatile("bar.sync 4, 128;" ::: "memory");
         int32_t rs = 0;
         if constexpr (MODE == MODE_ZP) {
           const int rb2 = lt & 1;
@@ -922,23 +956,30 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const uint32_t tacc = t_row + static_cast<uint32_t>(ab) * BNa;
         const int row = tl.m0 + rloc;
         float rv[32];  // residual prefetch: 32 columns in flight per thread
+        const int ng = (p.dbg_flags & 8) ? 0 : ngroups;  // tuning only: skip the epilogue math
+        // 16 columns per TMEM load (BN is a multiple of 16)
 #pragma unroll 1
-        for (int gq = 0; gq < ngroups; ++gq) {
-          if (p.res_kind && (gq & 7) == 0) {
+        for (int g16 = 0; g16 < ng / 4; ++g16) {
+          if (p.res_kind && (g16 & 1) == 0) {
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-              const int c = tl.n_tile * BN + (gq + q) * 4;
+              const int c = tl.n_tile * BN + (4 * g16 + q) * 4;
 #pragma unroll
               for (int e = 0; e < 4; ++e)
-                rv[4 * q + e] = (row < p.M && gq + q < ngroups && c + e < p.N)
+                rv[4 * q + e] = (row < p.M && 4 * g16 + q < ngroups && c + e < p.N)
                                     ? reinterpret_cast<const float*>(p.res)[static_cast<size_t>(row) * p.ld_res + c + e]
                                     : 0.f;
             }
           }
-          uint32_t ra[4];
-          tmem_ld4(tacc + gq * 4, ra);
+          uint32_t r16[16];
+          tmem_ld16(tacc + g16 * 16, r16);
           tmem_wait_ld();
-          finish4(row, tl.n_tile * BN + gq * 4, ra, rs, p.res_kind ? rv + (gq & 7) * 4 : nullptr);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint32_t ra[4] = {r16[4 * q], r16[4 * q + 1], r16[4 * q + 2], r16[4 * q + 3]};
+            finish4(row, tl.n_tile * BN + (4 * g16 + q) * 4, ra, rs,
+                    p.res_kind ? rv + ((g16 & 1) * 4 + q) * 4 : nullptr);
+          }
         }
         tc_fence_before();
         __syncwarp();
@@ -964,6 +1005,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     if (threadIdx.x == 0) stamp(5);
     if (warp < NPW) {
       const Tile tl = tile_of(blockIdx.x);
+      load_cols(tl.n_tile, 0, NP);
+      asm volatile("bar.sync 3, %0;" ::"r"(NP) : "memory");
       const int rstride = BN + 4;
       const uint32_t* red = reinterpret_cast<const uint32_t*>(sB);
       const int ngroups = BN / 4;
@@ -1146,7 +1189,7 @@ size_t gemm_smem_bytes(bool bf16, int nbp, int BN, int SA, int SB, int SX, int x
   const size_t b = static_cast<size_t>(BN) * KSTAGE;
   const size_t x = 128u * gemm_ips(bf16, nbp) * (x_kind == X_F32 ? 4 : 2);
   const size_t t = (bf16 ? 0 : static_cast<size_t>(tab_bytes)) +
-                   (2 * SA + 2 * SB + 2 * SX + 9) * 8 + 2 * 4 * 128 * 4 + 16 + 16 +
+                   (2 * SA + 2 * SB + 2 * SX + 9) * 8 + 2 * 4 * 128 * 4 + 2 * BN * 8 + 16 + 16 +
                    (silu ? 4 * 8 * 128 * 8 : 0) +  // SiLU code staging
                    static_cast<size_t>(fused_bytes);
   return 1024 + SB * b + SX * x + t;
@@ -1463,6 +1506,53 @@ cudaError_t launch_nchw_to_nhwc(bool levels, const float* in, int64_t n_img, int
                       inv_step, L);
   return launch_pdl(kan_nchw_to_nhwc_kernel<false>, grid, dim3(256), 0, st, in, C, HW, out, ldc, thr, lo,
                     inv_step, L);
+}
+
+// Lattice levels of fp32 activation rows [M, n] (pitch ld_x) into u16 rows
+// (pitch ld_o): the level prepass of large fp32-input layers, so their GEMM
+// reads 2-byte levels and its producers skip the level arithmetic.
+__global__ void __launch_bounds__(256) kan_rows_to_levels_kernel(const float* __restrict__ x, int64_t M, int n,
+                                                                 int ld_x, uint16_t* __restrict__ out, int ld_o,
+                                                                 const float* __restrict__ thr, float nlo_step,
+                                                                 float inv_step, int L) {
+  pdl_wait();
+  pdl_trigger();
+  const int q4 = (n + 3) / 4;  // float4 groups per row
+  const int64_t total = M * q4;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / q4;
+    const int c = static_cast<int>(i - r * q4) * 4;
+    const float* src = x + r * ld_x + c;
+    float v[4];
+    if (c + 3 < n && (ld_x & 3) == 0) {
+      const float4 f = *reinterpret_cast<const float4*>(src);
+      v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) v[e] = c + e < n ? src[e] : 0.f;
+    }
+    uint32_t a[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) a[e] = static_cast<uint32_t>(lattice_level_tie(v[e], inv_step, nlo_step, L, thr));
+    uint16_t* dst = out + r * ld_o + c;
+    if (c + 3 < n) {
+      *reinterpret_cast<uint2*>(dst) = make_uint2(a[0] | (a[1] << 16), a[2] | (a[3] << 16));
+    } else {
+      for (int e = 0; e < 4; ++e)
+        if (c + e < n) dst[e] = static_cast<uint16_t>(a[e]);
+    }
+  }
+}
+
+cudaError_t launch_rows_to_levels(const float* x, int64_t M, int n, int ld_x, uint16_t* out, int ld_o,
+                                  const float* thr, float nlo_step, float inv_step, int L, cudaStream_t st) {
+  const int64_t total = M * ((n + 3) / 4);
+  if (total == 0) return cudaSuccess;
+  const int64_t nb = (total + 255) / 256;
+  const unsigned blocks = static_cast<unsigned>(nb < 148 * 32 ? nb : 148 * 32);
+  return launch_pdl(kan_rows_to_levels_kernel, dim3(blocks), dim3(256), 0, st, x, M, n, ld_x, out, ld_o, thr,
+                    nlo_step, inv_step, L);
 }
 
 // argmax over logits rows (predict, eval.hpp:268-272: first maximum wins)

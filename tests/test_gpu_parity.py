@@ -299,3 +299,24 @@ def test_fused_output_layer_matches_separate_launches(oracle, M):
     np.testing.assert_array_equal(yf, ys)
     yo = oracle_int_model(oracle, G, 8, 8, W_PER_CHANNEL_SYM, 8, Ws, Bs, x)[-1]
     np.testing.assert_array_equal(yf, yo.astype(np.float32))
+
+
+def test_level_prepass_matches_in_kernel_levels(oracle):
+    """Large fp32-input layers take an HBM-bound level prepass and the GEMM
+    reads u16 levels; the result is bit-identical to computing the levels in
+    the producers (threshold lowered here to exercise it at test size)."""
+    dims, G = [300, 100, 10], 10
+    Ws, Bs = make_weights(dims, G, seed=8, silu=True)
+    x = np.random.default_rng(8).uniform(-1.1, 1.1, (1000, 300)).astype(np.float32)
+    opts = dict(mode="bspline-lut", lut_k=8, lut_h=8, silu_base=True, split_k=1)
+    y0 = build(dims, G, Ws, Bs, **opts).model_forward(to_dev(x)).cpu().numpy()
+    os.environ["KAN_LEVEL_PREPASS_MIN"] = "0"
+    try:
+        e = build(dims, G, Ws, Bs, **opts)
+        y1 = e.model_forward(to_dev(x)).cpu().numpy()
+        assert e.last_launches == 3  # prepass + layer 0 + small output layer
+    finally:
+        del os.environ["KAN_LEVEL_PREPASS_MIN"]
+    np.testing.assert_array_equal(y0, y1)
+    yo = oracle_int_model(oracle, G, 8, 8, W_PER_CHANNEL_SYM, 8, Ws, Bs, x)[-1]
+    np.testing.assert_array_equal(y1, yo.astype(np.float32))
