@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(bar_accfull(b), 1);
-      mbar_init(bar_accempty(b), 4);
+      mbar_init(bar_accempty(b), GEMM_EPI_WARPS);
     }
     mbar_init(bar_tab, 1);
     mbar_fence_init();
@@ -278,18 +278,19 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       mbar_wait(bar_accfull(ab), use & 1);
       tc_fence_after();
       // the tile's column constants, staged in smem (see kan_gather_gemm_kernel)
-      asm volatile("bar.sync 4, 128;" ::: "memory");
-      for (int i = static_cast<int>(threadIdx.x) - 32 * W_EPI; i < BN; i += 128) {
+      asm volatile("bar.sync 4, %0;" ::"r"(32 * GEMM_EPI_WARPS) : "memory");
+      for (int i = static_cast<int>(threadIdx.x) - 32 * W_EPI; i < BN; i += 32 * GEMM_EPI_WARPS) {
         const int j = min(tl.n_tile * BN + i, p.N - 1);
         s_cols[i] = p.fs[j];
         s_cols[BN + i] = SILU ? static_cast<double>(p.corr_b[j]) : 0.0;
       }
-      asm volatile("bar.sync 4, 128;" ::: "memory");
+      asm volatile("bar.sync 4, %0;" ::"r"(32 * GEMM_EPI_WARPS) : "memory");
       const uint32_t tacc = t_row + static_cast<uint32_t>(ab) * BNa;
       const int row = tl.m0 + rloc;
       float rv[32];  // residual prefetch: 32 columns in flight per thread
+      const int half = (warp - W_EPI) >> 2;  // the two warps of a lane quarter take alternate 32-column blocks
 #pragma unroll 1
-      for (int gq = 0; gq < BN / 4; ++gq) {
+      for (int gq = 8 * half; gq < BN / 4; gq += ((gq & 7) == 7) ? 9 : 1) {
         if (p.res_kind && (gq & 7) == 0) {
 #pragma unroll
           for (int q = 0; q < 8; ++q) {

@@ -545,9 +545,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(bar_accfull(b), 1);
-      mbar_init(bar_accempty(b), 4);
+      mbar_init(bar_accempty(b), GEMM_EPI_WARPS);
       mbar_init(bar_rsfull(b), NPW);
-      mbar_init(bar_rsempty(b), 4);
+      mbar_init(bar_rsempty(b), GEMM_EPI_WARPS);
     }
     mbar_init(bar_tab, 1);
     mbar_fence_init();
@@ -942,9 +942,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         tc_fence_after();
         if (threadIdx.x == 32 * W_EPI && lt == 0) stamp(4);
         // all epilogue warps are past the previous tile: restage the columns
-        asm volatile("bar.sync 4, 128;" ::: "memory");
-        load_cols(tl.n_tile, 32 * W_EPI, 128);
-        asm volatile("bar.sync 4, 128;" ::: "memory");
+        asm volatile("bar.sync 4, %0;" ::"r"(32 * GEMM_EPI_WARPS) : "memory");
+        load_cols(tl.n_tile, 32 * W_EPI, 32 * GEMM_EPI_WARPS);
+        asm volatile("bar.sync 4, %0;" ::"r"(32 * GEMM_EPI_WARPS) : "memory");
         int32_t rs = 0;
         if constexpr (MODE == MODE_ZP) {
           const int rb2 = lt & 1;
@@ -957,16 +957,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const int row = tl.m0 + rloc;
         float rv[32];  // residual prefetch: 32 columns in flight per thread
         const int ng = (p.dbg_flags & 8) ? 0 : ngroups;  // tuning only: skip the epilogue math
-        // 16 columns per TMEM load (BN is a multiple of 16)
+        // 16 columns per TMEM load (BN is a multiple of 16); the two warps of
+        // a lane quarter take alternate 16-column groups
+        const int half = (warp - W_EPI) >> 2;
 #pragma unroll 1
-        for (int g16 = 0; g16 < ng / 4; ++g16) {
-          if (p.res_kind && (g16 & 1) == 0) {
+        for (int g16 = half; g16 < ng / 4; g16 += 2) {
+          if (p.res_kind && (g16 & 3) == half) {
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-              const int c = tl.n_tile * BN + (4 * g16 + q) * 4;
+              // this warp's next two 16-column groups: g16 and g16 + 2
+              const int gg = 4 * (g16 + 2 * (q >> 2)) + (q & 3);
+              const int c = tl.n_tile * BN + gg * 4;
 #pragma unroll
               for (int e = 0; e < 4; ++e)
-                rv[4 * q + e] = (row < p.M && 4 * g16 + q < ngroups && c + e < p.N)
+                rv[4 * q + e] = (row < p.M && gg < ngroups && c + e < p.N)
                                     ? reinterpret_cast<const float*>(p.res)[static_cast<size_t>(row) * p.ld_res + c + e]
                                     : 0.f;
             }
@@ -978,7 +982,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           for (int q = 0; q < 4; ++q) {
             const uint32_t ra[4] = {r16[4 * q], r16[4 * q + 1], r16[4 * q + 2], r16[4 * q + 3]};
             finish4(row, tl.n_tile * BN + (4 * g16 + q) * 4, ra, rs,
-                    p.res_kind ? rv + ((g16 & 1) * 4 + q) * 4 : nullptr);
+                    p.res_kind ? rv + (((g16 >> 1) & 1) * 4 + q) * 4 : nullptr);
           }
         }
         tc_fence_before();
@@ -993,7 +997,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         rs = row_sum(0);
       }
       __syncwarp();
-      asm volatile("bar.sync 2, 128;" ::: "memory");  // all epilogue warps read slot 0 first
+      asm volatile("bar.sync 2, %0;" ::"r"(32 * GEMM_EPI_WARPS) : "memory");  // all epilogue warps read slot 0 first
       s_rowsum[rloc] = rs;
     }
   }

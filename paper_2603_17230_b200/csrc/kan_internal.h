@@ -17,8 +17,10 @@ enum XKind : int { X_F32 = 0, X_U16 = 1 };
 // K-steps; the stage's weight tile is two 128-byte-wide SW128 blocks.
 constexpr int KSTAGE = 256;
 constexpr int GEMM_PRODUCER_WARPS = 16;
-// producers + activation loader + MMA issuer + weight loader + 4 epilogue warps
-constexpr int GEMM_THREADS = 32 * (GEMM_PRODUCER_WARPS + 7);
+// producers + activation loader + MMA issuer + weight loader + epilogue warps
+// (two per TMEM lane quarter, each on every other 16-column group)
+constexpr int GEMM_EPI_WARPS = 8;
+constexpr int GEMM_THREADS = 32 * (GEMM_PRODUCER_WARPS + 3 + GEMM_EPI_WARPS);
 
 // One fused gather + tcgen05 GEMM launch (one KAN layer, linear form).
 struct GemmParams {
