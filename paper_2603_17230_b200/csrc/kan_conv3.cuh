@@ -341,16 +341,42 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             if (e < nvalid) o[static_cast<size_t>(e) * hw] = __double2float_rn(y[e]);
         } else if (p.epi == EPI_F32) {
           float* o = reinterpret_cast<float*>(p.out) + base;
+          if (nvalid == 4 && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
+            *reinterpret_cast<float4*>(o) = make_float4(__double2float_rn(y[0]), __double2float_rn(y[1]),
+                                                        __double2float_rn(y[2]), __double2float_rn(y[3]));
+          } else {
 #pragma unroll
-          for (int e = 0; e < 4; ++e)
-            if (e < nvalid) o[e] = __double2float_rn(y[e]);
+            for (int e = 0; e < 4; ++e)
+              if (e < nvalid) o[e] = __double2float_rn(y[e]);
+          }
+          if (p.out_lv) {  // levels sidecar (see kan_gather_gemm_kernel), one 8-byte store
+            const float* thr = reinterpret_cast<const float*>(sT + p.off_thr);
+            uint16_t* ol = p.out_lv + static_cast<size_t>(row) * p.ld_lv + col0;
+            uint32_t a[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              a[e] = static_cast<uint32_t>(lattice_level_tie(__double2float_rn(y[e]), p.inv_step_f, p.lo_f, p.L, thr));
+            if (nvalid == 4 && (reinterpret_cast<uintptr_t>(ol) & 7) == 0) {
+              *reinterpret_cast<uint2*>(ol) = make_uint2(a[0] | (a[1] << 16), a[2] | (a[3] << 16));
+            } else {
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                if (e < nvalid) ol[e] = static_cast<uint16_t>(a[e]);
+            }
+          }
         } else {  // EPI_LEVEL
           uint16_t* o = reinterpret_cast<uint16_t*>(p.out) + base;
+          uint32_t a[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e)
-            if (e < nvalid)
-              o[e] = static_cast<uint16_t>(
-                  lattice_level_fast(y[e], p.n_lo, p.n_hi_open, p.n_step, p.n_inv_step, p.n_L));
+            a[e] = static_cast<uint32_t>(lattice_level_fast(y[e], p.n_lo, p.n_hi_open, p.n_step, p.n_inv_step, p.n_L));
+          if (nvalid == 4 && (reinterpret_cast<uintptr_t>(o) & 7) == 0) {
+            *reinterpret_cast<uint2*>(o) = make_uint2(a[0] | (a[1] << 16), a[2] | (a[3] << 16));
+          } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if (e < nvalid) o[e] = static_cast<uint16_t>(a[e]);
+          }
         }
       }
       tc_fence_before();

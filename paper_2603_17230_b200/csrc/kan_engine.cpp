@@ -240,7 +240,11 @@ struct kan_engine {
   // none -- views, the last layer, or the model input); slots are reused
   // once every consumer of their tensor has run
   std::vector<int> slot_of;
-  std::vector<DevBuf<uint8_t>> slots;
+  struct Slot {
+    DevBuf<uint8_t> main;
+    DevBuf<uint16_t> lv;  // levels sidecar of an fp32-stored tensor
+  };
+  std::vector<Slot> slots;
   DevBuf<float> xstage;
   DevBuf<uint8_t> xnhwc;  // NHWC copy of an image model's input
   DevBuf<uint16_t> xlev;  // level prepass of a large fp32-input dense layer
@@ -254,6 +258,7 @@ struct kan_engine {
   // fp32-input dense layers with at least this many activations get the level
   // prepass (KAN_LEVEL_PREPASS_MIN; tests lower it to exercise the path)
   int64_t prepass_min = std::numeric_limits<int64_t>::max();
+  bool lv_sidecar = true;  // KAN_LV_SIDECAR=0 disables the levels sidecar (tuning)
   std::vector<DevBuf<unsigned long long>> timeline_buf;
   std::vector<int64_t> timeline_ctas;
   // per-layer kernel timing (kan_engine_set_profiling)
@@ -992,6 +997,7 @@ void configure(kan_engine* e, const kan_config* c) {
   e->force_tab = std::getenv("KAN_TABLES") ? std::atoi(std::getenv("KAN_TABLES")) : -1;
   // off by default: on C3 the prepass saves layer 0 ~50 us but costs ~260 us
   // itself (measured); the path stays available and tested
+  e->lv_sidecar = !(std::getenv("KAN_LV_SIDECAR") && std::atoi(std::getenv("KAN_LV_SIDECAR")) == 0);
   e->prepass_min = std::getenv("KAN_LEVEL_PREPASS_MIN") ? std::atoll(std::getenv("KAN_LEVEL_PREPASS_MIN"))
                                                         : std::numeric_limits<int64_t>::max();
   e->timeline_buf.clear();
@@ -1047,6 +1053,7 @@ struct LayerIO {
   void* fuse_out = nullptr;
   int fuse_epi = 0;
   bool* fused = nullptr;
+  uint16_t* out_lv = nullptr;  // levels sidecar to write (EPI_F32 hidden outputs)
   int res_kind = 0;
   const void* res = nullptr;
   int64_t ld_res = 0;
@@ -1192,6 +1199,8 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
         p.res = io.res;
         p.ld_res = static_cast<int>(io.ld_res);
         p.out_hw = io.out_hw;
+        p.out_lv = io.out_lv;
+        p.ld_lv = static_cast<int>(io.ld_out);
         // the (bh+2)-row window of one (kx, chunk): box rows bh+2, one image
         const CUtensorMap xmap3 = make_conv_xmap(io, l, pl.IPS, bh + 2, 1);
         const size_t smem = conv3_smem_bytes(pl.BN, R, SA, SB, SX, io.x_kind, ts.bytes, silu);
@@ -1309,6 +1318,8 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
   p.out_scale = e->cfg.out_scale;
   p.inv_out_scale = 1.0 / e->cfg.out_scale;
   p.n_ch = pl.n_in;
+  p.out_lv = io.out_lv;
+  p.ld_lv = static_cast<int>(io.ld_out);
   p.res_kind = io.res_kind;
   p.res = io.res;
   p.ld_res = static_cast<int>(io.ld_res);
@@ -1423,6 +1434,7 @@ struct Act {
   int kind = X_F32;
   bool nchw = false;
   int64_t ld = 0;
+  const uint16_t* lv = nullptr;  // levels sidecar of an fp32-stored tensor (pitch ld)
 };
 
 // model_forward (eval.hpp:200-253): run the layer graph on the caller's stream.
@@ -1483,8 +1495,13 @@ void forward(kan_engine* e, const float* x, int64_t M, void* out, cudaStream_t s
   }
   std::vector<Act> acts(static_cast<size_t>(nl));
   auto slot = [&](int i, size_t bytes) -> void* {
-    auto& b = e->slots[static_cast<size_t>(e->slot_of[static_cast<size_t>(i)])];
+    auto& b = e->slots[static_cast<size_t>(e->slot_of[static_cast<size_t>(i)])].main;
     b.alloc(bytes);
+    return b.p;
+  };
+  auto slot_lv = [&](int i, size_t elems) -> uint16_t* {
+    auto& b = e->slots[static_cast<size_t>(e->slot_of[static_cast<size_t>(i)])].lv;
+    b.alloc(elems);
     return b.p;
   };
   for (int i = 0; i < nl; ++i) {
@@ -1494,6 +1511,7 @@ void forward(kan_engine* e, const float* x, int64_t M, void* out, cudaStream_t s
     Act& dst = acts[static_cast<size_t>(i)];
     if (l.type == L_FLATTEN) {
       dst = src;
+      dst.lv = nullptr;
       dst.ld = src.nchw ? static_cast<int64_t>(l.in.c) * l.in.h * l.in.w
                         : static_cast<int64_t>(l.in.h) * l.in.w * src.ld;
       dst.nchw = false;
@@ -1531,6 +1549,10 @@ void forward(kan_engine* e, const float* x, int64_t M, void* out, cudaStream_t s
     io.x = src.p;
     io.x_kind = src.kind;
     io.ld_x = src.ld;
+    if (lut && src.lv && src.kind == X_F32) {  // the producer stored levels beside the values
+      io.x = src.lv;
+      io.x_kind = X_U16;
+    }
     // large fp32-input dense layers: levels first (HBM-bound prepass), so the
     // gather GEMM reads 2-byte levels and its producers skip the level
     // arithmetic (small layers keep the in-kernel path: their steps are
@@ -1573,6 +1595,14 @@ void forward(kan_engine* e, const float* x, int64_t M, void* out, cudaStream_t s
       io.ld_out = pitch16(pl.N, osz);
       o = slot(i, static_cast<size_t>(rows * io.ld_out * osz));
       io.epi = levels ? EPI_LEVEL : EPI_F32;
+      // fp32-stored (residual) tensors also get their levels when a KAN layer reads them
+      // (at the fp32 pitch, which must also be a 16-byte pitch for u16 rows)
+      if (lut && l.store_f32 && !(pl.small && !conv) && e->lv_sidecar && pitch16(pl.N, 2) == io.ld_out) {
+        bool kan_consumer = false;
+        for (const auto& c : e->layers)
+          kan_consumer = kan_consumer || (c.src == i && (c.type == L_CONV || c.type == L_LINEAR));
+        if (kan_consumer) io.out_lv = slot_lv(i, static_cast<size_t>(rows * io.ld_out));
+      }
     }
     io.out = o;
     // fuse a small last layer that reads only this layer's hidden levels
@@ -1614,6 +1644,7 @@ void forward(kan_engine* e, const float* x, int64_t M, void* out, cudaStream_t s
     dst.kind = io.epi == EPI_LEVEL ? X_U16 : X_F32;
     dst.nchw = false;
     dst.ld = io.ld_out;
+    dst.lv = io.out_lv;
     if (fused) break;  // the output layer ran inside this launch
   }
 }

@@ -633,6 +633,24 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         for (int e = 0; e < 4; ++e)
           if (e < nvalid) o[e] = __double2float_rn(y[e]);
       }
+      if constexpr (!BF16) {
+        if (p.out_lv) {
+          // levels sidecar: what the consuming KAN layer would compute from these values
+          const float* thr = reinterpret_cast<const float*>(sT + p.off_thr);
+          uint32_t a[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            a[e] = static_cast<uint32_t>(lattice_level_tie(__double2float_rn(y[e]), p.inv_step_f, p.lo_f, p.L, thr));
+          uint16_t* ol = p.out_lv + static_cast<size_t>(row) * p.ld_lv + col0;
+          if (nvalid == 4 && (reinterpret_cast<uintptr_t>(ol) & 7) == 0) {
+            *reinterpret_cast<uint2*>(ol) = make_uint2(a[0] | (a[1] << 16), a[2] | (a[3] << 16));
+          } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if (e < nvalid) ol[e] = static_cast<uint16_t>(a[e]);
+          }
+        }
+      }
     } else if (p.epi == EPI_LEVEL) {
       // fused output layer: the levels stay in this CTA's smem row buffer
       uint16_t* o = p.f_on ? f_lv + (row & 127) * BN + (col0 % BN) : reinterpret_cast<uint16_t*>(p.out) + base;
@@ -919,6 +937,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     // ============================ epilogue ================================
     // One warp per TMEM lane quarter; each thread finishes its row of the
     // tile, 4 columns at a time (rolled: the epilogue code stays small).
+    if (tab_bytes > 0) mbar_wait(bar_tab, 0);  // the levels sidecar reads the thresholds
     const int wq = warp & 3;
     const int rloc = wq * 32 + lane;
     const uint32_t t_row = tmem + (static_cast<uint32_t>(wq * 32) << 16);

@@ -87,6 +87,10 @@ struct GemmParams {
   const void* res;
   int ld_res;
   int out_hw;  // EPI_F32: >0 writes NCHW (H*W per channel), 0 row-major
+  // EPI_F32 hidden outputs (LUT path): also the next layer's lattice levels of
+  // the stored fp32 values (null when no KAN layer consumes the tensor)
+  uint16_t* out_lv;
+  int ld_lv;
   // ky-shared 3x3 conv kernel (kan_conv3_kernel): ext_rows = (bh+2)*Wo input
   // pixels expanded once per (kx, channel chunk) "super-stage" and read by the
   // three ky taps through descriptors offset by ky*Wo rows; n_ss super-stages
