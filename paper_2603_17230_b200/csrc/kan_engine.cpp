@@ -48,6 +48,9 @@ cudaError_t launch_rows_to_levels(const float* x, int64_t M, int n, int ld_x, ui
 cudaError_t launch_conv3(int mode, const CUtensorMap& xmap, const GemmParams& p, size_t smem, cudaStream_t st);
 size_t conv3_smem_bytes(int BN, int R, int SA, int SB, int SX, int x_kind, int tab_bytes, bool silu);
 size_t small_smem_bytes(const SmallParams& p);
+cudaError_t launch_im2col_levels(const float* x, int64_t n_img, int C, int H, int W, int K, int stride, int pad,
+                                 int Ho, int Wo, uint16_t* out, int ld_o, const float* thr, float nlo_step,
+                                 float inv_step, int L, int lvl0, cudaStream_t st);
 cudaError_t launch_nchw_to_nhwc(bool levels, const float* in, int64_t n_img, int C, int HW,
                                 void* out, int ldc, const float* thr, float lo, float inv_step,
                                 int L, cudaStream_t st);
@@ -128,6 +131,10 @@ struct Layer {
   // LUT path storage of this layer's output: fp32 values when some consumer
   // needs values (a residual add, average pooling), else exact lattice levels
   bool store_f32 = false;
+  // LUT path: a conv on the model input with fewer channels than one IPS chunk
+  // (the ResKAN stem, c_in = 3) runs as a dense GEMM over an explicit level
+  // im2col of the NCHW input (c_in*k*k inputs instead of k*k padded chunks)
+  bool im2col = false;
   std::vector<double> coeffs;  // reference layout [n_in*nb, n_out]
   std::vector<double> base_w;  // [n_in, n_out]
 };
@@ -248,6 +255,7 @@ struct kan_engine {
   DevBuf<float> xstage;
   DevBuf<uint8_t> xnhwc;  // NHWC copy of an image model's input
   DevBuf<uint16_t> xlev;  // level prepass of a large fp32-input dense layer
+  DevBuf<uint16_t> xcol;  // level im2col of the model input (stem convs)
   DevBuf<float> logits_tmp;
   DevBuf<uint8_t> io_in, io_out;
   int last_launches = 0;
@@ -569,14 +577,14 @@ int act_esz(const kan_engine* e) { return e->cfg.mode == KAN_MODE_BSPLINE_LUT ? 
 std::vector<int> input_perm(const kan_engine* e, const Layer& l, int ips, int& cps) {
   std::vector<int> perm;
   cps = 0;
-  if (l.type == L_CONV) {
+  if (l.type == L_CONV && !l.im2col) {
     const int KK = l.kernel * l.kernel;
     cps = (l.c_in + ips - 1) / ips;
     const int cin_pad = cps * ips;
     perm.assign(static_cast<size_t>(KK) * cin_pad, -1);
     for (int t = 0; t < KK; ++t)
       for (int c = 0; c < l.c_in; ++c) perm[static_cast<size_t>(t) * cin_pad + c] = c * KK + t;
-  } else if (l.in.hw > 0) {
+  } else if (l.type != L_CONV && l.in.hw > 0) {
     const int ldc = static_cast<int>(pitch16(l.in.fc, act_esz(e)));
     perm.assign(static_cast<size_t>(l.in.hw) * ldc, -1);
     for (int q = 0; q < l.in.hw; ++q)
@@ -708,7 +716,7 @@ void prepare_gemm_layer(kan_engine* e, const Layer& l, PreparedLayer& pl, bool b
 
   // ky-shared 3x3 stride-1 pad-1 conv kernel (kan_conv3.cuh), LUT path
   pl.conv3 = false;
-  if (!bf16 && l.type == L_CONV && l.kernel == 3 && l.stride == 1 && l.padding == 1 && nbp == 8 &&
+  if (!bf16 && l.type == L_CONV && !l.im2col && l.kernel == 3 && l.stride == 1 && l.padding == 1 && nbp == 8 &&
       pl.b_signed && std::getenv("KAN_NO_CONV3") == nullptr) {
     const int Wo = l.out.w, Ho = l.out.h;
     if (Wo % 8 == 0 && 128 % Wo == 0 && Ho * Wo >= 128 && Ho % (128 / Wo) == 0) {
@@ -989,6 +997,11 @@ void configure(kan_engine* e, const kan_config* c) {
   } else {
     if (cfg.mode == KAN_MODE_FP32 && cfg.out_kind != KAN_OUT_F32)
       throw InvalidArgument("int8 outputs are only produced on the LUT path");
+  }
+  for (auto& l : e->layers) {
+    const int ncol = l.c_in * l.kernel * l.kernel;
+    l.im2col = cfg.mode == KAN_MODE_BSPLINE_LUT && l.type == L_CONV && l.src == -1 && l.c_in < 16 &&
+               ncol <= 64 && e->input_shape.size() == 3 && std::getenv("KAN_NO_IM2COL") == nullptr;
   }
   e->prep.clear();
   e->prep.resize(static_cast<size_t>(e->n_kan));
@@ -1470,7 +1483,7 @@ void forward(kan_engine* e, const float* x, int64_t M, void* out, cudaStream_t s
   if (in.nchw) {
     bool used_as_image = false;
     for (const auto& l : e->layers)
-      used_as_image = used_as_image || (l.src < 0 && l.type != L_FLATTEN);
+      used_as_image = used_as_image || (l.src < 0 && l.type != L_FLATTEN && !l.im2col);
     if (used_as_image) {
       for (const auto& l : e->layers)
         if (l.src < 0 && l.type == L_FLATTEN)
@@ -1570,7 +1583,20 @@ void forward(kan_engine* e, const float* x, int64_t M, void* out, cudaStream_t s
       io.x_kind = X_U16;
       io.ld_x = ldl;
     }
-    if (conv) {
+    if (conv && l.im2col) {  // explicit level im2col of the NCHW model input
+      const int ncol = l.c_in * l.kernel * l.kernel;
+      const int64_t ldc = pitch16(ncol, 2);
+      e->xcol.alloc(static_cast<size_t>(rows * ldc));
+      ck(launch_im2col_levels(x, M, l.c_in, l.in.h, l.in.w, l.kernel, l.stride, l.padding, l.out.h, l.out.w,
+                              e->xcol.p, static_cast<int>(ldc), e->d_thr.p,
+                              static_cast<float>(-e->grid.lo / e->lat.step), static_cast<float>(1.0 / e->lat.step),
+                              static_cast<int>(e->lat.L), static_cast<int>(e->lat.quantize(0.0)), st),
+         "input im2col");
+      e->last_launches += 1;
+      io.x = e->xcol.p;
+      io.x_kind = X_U16;
+      io.ld_x = ldc;
+    } else if (conv) {
       if (src.nchw) throw LogicError("conv input must be stored NHWC");
       io.conv = &l;
       io.n_img = M;

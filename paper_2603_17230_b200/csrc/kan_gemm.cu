@@ -1578,6 +1578,48 @@ cudaError_t launch_rows_to_levels(const float* x, int64_t M, int n, int ld_x, ui
                     nlo_step, inv_step, L);
 }
 
+// Explicit im2col over the NCHW fp32 model input into lattice levels, for convs
+// whose c_in is far below one channel chunk (the ResKAN stem, c_in = 3): one
+// row per output pixel (n, oy, ox), columns in the reference's channel-major
+// order c*K*K + ky*K + kx (layers.hpp:140-149), padded taps at level(0.0).
+// The layer then runs as a dense (c_in*K*K)-input GEMM.
+__global__ void __launch_bounds__(256) kan_im2col_levels_kernel(const float* __restrict__ x, int64_t n_img, int C,
+                                                                int H, int W, int K, int stride, int pad, int Ho,
+                                                                int Wo, uint16_t* __restrict__ out, int ld_o,
+                                                                const float* __restrict__ thr, float nlo_step,
+                                                                float inv_step, int L, int lvl0) {
+  pdl_wait();
+  pdl_trigger();
+  const int ncol = C * K * K;
+  const int64_t total = n_img * Ho * Wo * ncol;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int col = static_cast<int>(i % ncol);
+    const int64_t r = i / ncol;  // output pixel row
+    const int ox = static_cast<int>(r % Wo);
+    const int oy = static_cast<int>((r / Wo) % Ho);
+    const int64_t n = r / (static_cast<int64_t>(Wo) * Ho);
+    const int c = col / (K * K), t = col - c * K * K;
+    const int ky = t / K, kx = t - ky * K;
+    const int iy = oy * stride + ky - pad, ix = ox * stride + kx - pad;
+    int a = lvl0;
+    if (static_cast<unsigned>(iy) < static_cast<unsigned>(H) && static_cast<unsigned>(ix) < static_cast<unsigned>(W))
+      a = lattice_level_tie(x[((n * C + c) * H + iy) * W + ix], inv_step, nlo_step, L, thr);
+    out[r * ld_o + col] = static_cast<uint16_t>(a);
+  }
+}
+
+cudaError_t launch_im2col_levels(const float* x, int64_t n_img, int C, int H, int W, int K, int stride, int pad,
+                                 int Ho, int Wo, uint16_t* out, int ld_o, const float* thr, float nlo_step,
+                                 float inv_step, int L, int lvl0, cudaStream_t st) {
+  const int64_t total = n_img * Ho * Wo * C * K * K;
+  if (total == 0) return cudaSuccess;
+  const int64_t nb = (total + 255) / 256;
+  const unsigned blocks = static_cast<unsigned>(nb < 148 * 32 ? nb : 148 * 32);
+  return launch_pdl(kan_im2col_levels_kernel, dim3(blocks), dim3(256), 0, st, x, n_img, C, H, W, K, stride, pad, Ho,
+                    Wo, out, ld_o, thr, nlo_step, inv_step, L, lvl0);
+}
+
 // argmax over logits rows (predict, eval.hpp:268-272: first maximum wins)
 __global__ void kan_argmax_kernel(const float* __restrict__ logits, int64_t M, int N, int ld,
                                   int32_t* __restrict__ out) {

@@ -59,6 +59,7 @@ CONV_CASES = [
     (64, 16, 16, 32, 3, 1, 1, True, W_PER_CHANNEL_SYM, 2, 2),   # split-K over a cluster
     (32, 4, 4, 300, 3, 1, 1, True, W_PER_CHANNEL_SYM, 9, 0),    # 8 images per tile, 2 N tiles
     (5, 8, 8, 7, 1, 1, 0, True, W_PER_CHANNEL_SYM, 4, 0),       # 1x1
+    (2, 9, 11, 20, 5, 2, 2, True, W_PER_CHANNEL_SYM, 3, 0),     # 5x5 s2 stem (explicit im2col)
 ]
 
 
@@ -192,3 +193,22 @@ def test_conv3_matches_general_kernel_in_a_residual_stage():
     finally:
         del os.environ["KAN_NO_CONV3"]
     np.testing.assert_array_equal(y3, yg)
+
+
+@pytest.mark.parametrize("k,s,p", [(3, 1, 1), (3, 2, 1), (1, 1, 0)])
+def test_stem_im2col_matches_implicit_conv(k, s, p):
+    """Stem convs (model input, c_in < 16) run as a dense GEMM over an explicit
+    level im2col; the result is bit-identical to the implicit-im2col conv
+    kernel over the transposed input (KAN_NO_IM2COL)."""
+    desc = conv_desc(3, 16, 16, 32, k, s, p, floor=True)
+    desc["layers"].append({"type": "conv", "c_in": 32, "c_out": 8, "kernel": 1, "stride": 1, "padding": 0})
+    Ws, Bs = weights_for(desc, seed=k + s)
+    x = np.random.default_rng(k * s).uniform(-1.05, 1.05, (5, 3 * 256)).astype(np.float32)
+    opts = dict(mode="bspline-lut", lut_k=8, lut_h=8, bits_w=8, w_scheme=W_PER_CHANNEL_SYM, silu_base=True)
+    yi = build(desc, Ws, Bs, **opts).model_forward(to_dev(x)).cpu().numpy()
+    os.environ["KAN_NO_IM2COL"] = "1"
+    try:
+        yc = build(desc, Ws, Bs, **opts).model_forward(to_dev(x)).cpu().numpy()
+    finally:
+        del os.environ["KAN_NO_IM2COL"]
+    np.testing.assert_array_equal(yi, yc)
