@@ -54,15 +54,27 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int lane = threadIdx.x & 31;
   pdl_trigger();
 
-  const int n_tiles = p.m_tiles * p.n_tiles_n;
-  const int tile_step = static_cast<int>(gridDim.x);
+  // Work units: with p.mc == 2 the two CTAs of a cluster take the two M tiles
+  // of a unit (same N tile) and each issues half of the unit's weight-tile
+  // loads, multicast into both CTAs' rings -- half the L2 weight traffic.
+  // Every CTA walks every unit of its cluster (an odd last M tile leaves the
+  // second CTA a unit without a tile: it only releases its weight slots).
+  const int MC = p.mc > 1 ? p.mc : 1;
+  const uint32_t crank = MC > 1 ? cluster_rank() : 0u;
+  const int unit0 = MC > 1 ? static_cast<int>(cluster_id_x()) : static_cast<int>(blockIdx.x);
+  const int unit_step = MC > 1 ? static_cast<int>(n_clusters_x()) : static_cast<int>(gridDim.x);
+  const int n_units = (p.m_tiles + MC - 1) / MC * p.n_tiles_n;
+  const uint16_t mc_mask = static_cast<uint16_t>((1u << MC) - 1u);
   struct Tile {
     int m0, n_tile, n0, y0;
+    bool valid;
   };
-  auto tile_of = [&](int t) {
+  auto tile_of = [&](int u) {
     Tile r;
-    const int mt = t / p.n_tiles_n;
-    r.n_tile = t - mt * p.n_tiles_n;
+    const int mu = u / p.n_tiles_n;
+    r.n_tile = u - mu * p.n_tiles_n;
+    const int mt = mu * MC + static_cast<int>(crank);
+    r.valid = mt < p.m_tiles;
     r.m0 = mt * 128;
     r.n0 = mt / p.tpi;
     r.y0 = (mt % p.tpi) * p.bh;
@@ -95,7 +107,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     for (int s = 0; s < SB; ++s) {
       mbar_init(bar_bfull(s), 1);
-      mbar_init(bar_bempty(s), 1);
+      mbar_init(bar_bempty(s), MC);  // every CTA of the cluster releases the slot
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(bar_accfull(b), 1);
@@ -108,6 +120,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   if (warp == W_MMA) tmem_alloc(smem_u32(s_tmem), tmem_cols);
   tc_fence_before();
   __syncthreads();
+  if (MC > 1) cluster_sync_all();  // peers' barriers initialised before any multicast
   tc_fence_after();
   const uint32_t tmem = *s_tmem;
 
@@ -115,12 +128,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     // ================= activation loader: one window per super-stage ========
     pdl_wait();
     Ring rx(SX);
-    for (int t = blockIdx.x; t < n_tiles; t += tile_step) {
-      const Tile tl = tile_of(t);
+    for (int u = unit0; u < n_units; u += unit_step) {
+      const Tile tl = tile_of(u);
+      if (!tl.valid) continue;
       for (int ss = 0; ss < p.n_ss; ++ss, rx.next()) {
         const int kx = ss / p.cps, cc = ss - kx * p.cps;
         mbar_wait(bar_xempty(rx.slot), rx.phase ^ 1);
-        if (lane == 0) {
+        if (lane == 0 && (p.dbg_flags & 4)) {  // tuning only: no activation load (stale window)
+          mbar_arrive(bar_xfull(rx.slot));
+        } else if (lane == 0) {
           mbar_arrive_tx(bar_xfull(rx.slot), x_bytes);
           // rows y0-1 .. y0+bh, columns kx-1 .. kx-1+Wo-1 (zero outside)
           tma_load_4d(smem_u32(sX + static_cast<size_t>(rx.slot) * x_bytes), &xmap, cc * IPS, kx - 1,
@@ -137,64 +153,96 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     __syncwarp();
     Ring rb(SB);
-    for (int t = blockIdx.x; t < n_tiles; t += tile_step) {
-      const Tile tl = tile_of(t);
-      for (int q = 0; q < 3 * p.n_ss; ++q, rb.next()) {
+    uint32_t fill = 0;
+    for (int u = unit0; u < n_units; u += unit_step) {
+      const Tile tl = tile_of(u);
+      for (int q = 0; q < 3 * p.n_ss; ++q, rb.next(), ++fill) {
+        // released by every CTA of the cluster: safe to refill everywhere
         mbar_wait(bar_bempty(rb.slot), rb.phase ^ 1);
         if (lane == 0) {
           const size_t wt = static_cast<size_t>(tl.n_tile) * 3 * p.n_ss + q;
-          mbar_arrive_tx(bar_bfull(rb.slot), b_slot);
-          bulk_load(smem_u32(sB + static_cast<size_t>(rb.slot) * b_slot), p.wt + wt * b_slot, b_slot,
-                    bar_bfull(rb.slot));
+          const uint32_t dst = smem_u32(sB + static_cast<size_t>(rb.slot) * b_slot);
+          if (p.dbg_flags & 32)  // tuning only: no weight loads (stale slots)
+            mbar_arrive(bar_bfull(rb.slot));
+          else
+            mbar_arrive_tx(bar_bfull(rb.slot), b_slot);
+          if (p.dbg_flags & 32) {
+          } else if (MC == 1)
+            bulk_load(dst, p.wt + wt * b_slot, b_slot, bar_bfull(rb.slot));
+          else if (fill % MC == crank)
+            bulk_load_mc(dst, p.wt + wt * b_slot, b_slot, bar_bfull(rb.slot), mc_mask);
         }
         __syncwarp();
       }
     }
+    // drain: every peer's release of our slots has landed before the CTA exits
+    for (int s = 0; s < SB; ++s, rb.next()) mbar_wait(bar_bempty(rb.slot), rb.phase ^ 1);
   } else if (warp == W_MMA) {
     // ============ MMA issuer: SS-mode, three row-shifted taps per stage ====
+    // Warp-uniform waits and descriptors, one elected lane issues: at N = 64
+    // a tap is only ~300 tensor cycles, so the issue path must stay short.
     const uint32_t idesc = idesc_i8(BN, true);
+    const uint32_t a_kstep = static_cast<uint32_t>(R) * 8u;   // next 128-byte K block of A (x16 B)
+    const uint32_t b_kstep = static_cast<uint32_t>(BN) * 8u;  // next 128-byte K block of B (x16 B)
     Ring ra(SA), rb(SB);
     int lt = 0;
-    for (int t = blockIdx.x; t < n_tiles; t += tile_step, ++lt) {
+    auto release_b = [&](uint32_t bar) {
+      if (MC == 1)
+        tc_commit(bar);
+      else
+        tc_commit_mc(bar, mc_mask);
+    };
+    for (int u = unit0; u < n_units; u += unit_step) {
+      if (!tile_of(u).valid) {  // no tile here: release the unit's weight slots
+        for (int q = 0; q < 3 * p.n_ss; ++q, rb.next()) {
+          mbar_wait_warp(bar_bfull(rb.slot), rb.phase);
+          if (elect_one()) release_b(bar_bempty(rb.slot));
+          __syncwarp();
+        }
+        continue;
+      }
       const int ab = nacc == 2 ? (lt & 1) : 0;
       const int use = nacc == 2 ? (lt >> 1) : lt;
-      mbar_wait(bar_accempty(ab), (use & 1) ^ 1);
+      mbar_wait_warp(bar_accempty(ab), (use & 1) ^ 1);
       tc_fence_after();
       const uint32_t dacc = tmem + static_cast<uint32_t>(ab) * BNa;
-      bool first = true;
+      uint32_t acc = 0u;
       for (int ss = 0; ss < p.n_ss; ++ss, ra.next()) {
-        mbar_wait(bar_afull(ra.slot), ra.phase);
+        mbar_wait_warp(bar_afull(ra.slot), ra.phase);
         tc_fence_after();
         const uint32_t a_addr = smem_u32(sA + static_cast<size_t>(ra.slot) * a_bytes);
         for (int ky = 0; ky < 3; ++ky, rb.next()) {
-          mbar_wait(bar_bfull(rb.slot), rb.phase);
+          mbar_wait_warp(bar_bfull(rb.slot), rb.phase);
           tc_fence_after();
-          if (lane == 0) {
-            const uint32_t b_addr = smem_u32(sB + static_cast<size_t>(rb.slot) * b_slot);
-            const uint32_t row_off = static_cast<uint32_t>(ky * p.Wo / 8) * 1024u;  // whole SW128 atoms
+          const uint32_t b_addr = smem_u32(sB + static_cast<size_t>(rb.slot) * b_slot);
+          const uint32_t row_off = static_cast<uint32_t>(ky * p.Wo / 8) * 1024u;  // whole SW128 atoms
+          const uint64_t ad0 = umma_desc_sw128(a_addr + row_off);
+          const uint64_t bd0 = umma_desc_sw128(b_addr);
+          const uint64_t sd_a = umma_desc_sw32(a_addr + a_code_bytes + static_cast<uint32_t>(ky * p.Wo / 8) * 256u);
+          const uint64_t sd_b = umma_desc_sw32(b_addr + BN * KSTAGE);
+          if (elect_one()) {
+            if (!(p.dbg_flags & 2)) {  // (tuning only: flag 2 skips the MMAs)
 #pragma unroll
-            for (int kk = 0; kk < KSTAGE / 32; ++kk) {
-              const uint64_t ad =
-                  umma_desc_sw128(a_addr + (kk >> 2) * static_cast<uint32_t>(R) * 128u + row_off + 32 * (kk & 3));
-              const uint64_t bd = umma_desc_sw128(b_addr + (kk >> 2) * BN * 128 + 32 * (kk & 3));
-              mma_i8(dacc, ad, bd, idesc, (first && kk == 0) ? 0u : 1u);
-            }
-            if constexpr (SILU) {
+              for (int kk = 0; kk < KSTAGE / 32; ++kk) {
+                // descriptor start addresses advance in 16-byte units (no carry: smem < 256 KB)
+                const uint64_t ad = ad0 + (kk >> 2) * a_kstep + 2 * (kk & 3);
+                const uint64_t bd = bd0 + (kk >> 2) * b_kstep + 2 * (kk & 3);
+                mma_i8(dacc, ad, bd, idesc, kk == 0 ? acc : 1u);
+              }
               // the tap's SiLU base term: K = 32 codes against the SW32 SiLU weights
-              const uint64_t ad = umma_desc_sw32(a_addr + a_code_bytes + static_cast<uint32_t>(ky * p.Wo / 8) * 256u);
-              const uint64_t bd = umma_desc_sw32(b_addr + BN * KSTAGE);
-              mma_i8(dacc, ad, bd, idesc, 1u);
+              if (SILU) mma_i8(dacc, sd_a, sd_b, idesc, 1u);
             }
-            tc_commit(bar_bempty(rb.slot));
+            release_b(bar_bempty(rb.slot));
           }
           __syncwarp();
-          first = false;
+          acc = 1u;
         }
-        if (lane == 0) tc_commit(bar_aempty(ra.slot));
+        if (elect_one()) tc_commit(bar_aempty(ra.slot));
         __syncwarp();
       }
-      if (lane == 0) tc_commit(bar_accfull(ab));
+      if (elect_one()) tc_commit(bar_accfull(ab));
       __syncwarp();
+      ++lt;
     }
   } else if (warp < NPW) {
     // ==================== producers: expand each window once ================
@@ -205,8 +253,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const uint2* c64 = reinterpret_cast<const uint2*>(sT + p.off_c64);
     const int units = (R / 32) * 4;  // (32-row group, K quarter) pairs
     Ring ra(SA), rx(SX);
-    for (int t = blockIdx.x; t < n_tiles; t += tile_step) {
-      const Tile tl = tile_of(t);
+    for (int u = unit0; u < n_units; u += unit_step) {
+      const Tile tl = tile_of(u);
+      if (!tl.valid) continue;
       uint32_t rsum = 0;
       for (int ss = 0; ss < p.n_ss; ++ss, ra.next(), rx.next()) {
         const int kx = ss / p.cps;
@@ -214,7 +263,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         mbar_wait(bar_aempty(ra.slot), ra.phase ^ 1);
         const uint8_t* xt = sX + static_cast<size_t>(rx.slot) * x_bytes;
         uint8_t* at = sA + static_cast<size_t>(ra.slot) * a_bytes;
-        for (int u = warp; u < units; u += NPW) {
+        for (int u = (p.dbg_flags & 16) ? units : warp; u < units; u += NPW) {  // (flag 16: no expansion)
           const int g = u >> 2, h = u & 3;
           const int rr = 32 * g + lane;  // expanded row = input pixel of the window
           const int wy = rr / p.Wo, wx = rr - wy * p.Wo;
@@ -271,10 +320,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const int rloc = wq * 32 + lane;
     const uint32_t t_row = tmem + (static_cast<uint32_t>(wq * 32) << 16);
     int lt = 0;
-    for (int t = blockIdx.x; t < n_tiles; t += tile_step, ++lt) {
-      const Tile tl = tile_of(t);
+    for (int u = unit0; u < n_units; u += unit_step) {
+      const Tile tl = tile_of(u);
+      if (!tl.valid) continue;
       const int ab = nacc == 2 ? (lt & 1) : 0;
       const int use = nacc == 2 ? (lt >> 1) : lt;
+      ++lt;
       mbar_wait(bar_accfull(ab), use & 1);
       tc_fence_after();
       // the tile's column constants, staged in smem (see kan_gather_gemm_kernel)
@@ -290,7 +341,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       float rv[32];  // residual prefetch: 32 columns in flight per thread
       const int half = (warp - W_EPI) >> 2;  // the two warps of a lane quarter take alternate 32-column blocks
 #pragma unroll 1
-      for (int gq = 8 * half; gq < BN / 4; gq += ((gq & 7) == 7) ? 9 : 1) {
+      for (int gq = 8 * half; gq < ((p.dbg_flags & 8) ? 0 : BN / 4); gq += ((gq & 7) == 7) ? 9 : 1) {
         if (p.res_kind && (gq & 7) == 0) {
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
@@ -387,6 +438,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
   tc_fence_before();
   __syncthreads();
+  if (MC > 1) cluster_sync_all();  // no multicast into / release of an exited CTA
   if (warp == W_MMA) {
     tc_fence_after();
     tmem_dealloc(tmem, tmem_cols);
@@ -416,9 +468,24 @@ cudaError_t launch_conv3(int mode, const CUtensorMap& xmap, const GemmParams& p,
       cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
       if (n_sm <= 0) n_sm = 148;
     }
-    const int tiles = p.n_tiles_n * p.m_tiles;
-    return launch_pdl(kfn, dim3(static_cast<unsigned>(tiles < n_sm ? tiles : n_sm)), dim3(GEMM_THREADS), smem, st,
-                      xmap, p);
+    const int mc = p.mc > 1 ? p.mc : 1;
+    const int units = (p.m_tiles + mc - 1) / mc * p.n_tiles_n;
+    const int clusters = units < n_sm / mc ? units : n_sm / mc;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(clusters * mc));
+    cfg.blockDim = dim3(GEMM_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = static_cast<unsigned>(mc);
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    return cudaLaunchKernelEx(&cfg, kfn, xmap, p);
   };
   if (mode == MODE_SILU) return go(kan_conv3_kernel<MODE_SILU>);
   return go(kan_conv3_kernel<MODE_PLAIN>);

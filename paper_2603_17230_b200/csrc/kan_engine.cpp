@@ -266,6 +266,7 @@ struct kan_engine {
   // fp32-input dense layers with at least this many activations get the level
   // prepass (KAN_LEVEL_PREPASS_MIN; tests lower it to exercise the path)
   int64_t prepass_min = std::numeric_limits<int64_t>::max();
+  int conv3_mc = 2;  // conv3: CTAs per weight-multicast cluster (KAN_CONV3_MC)
   bool lv_sidecar = true;  // KAN_LV_SIDECAR=0 disables the levels sidecar (tuning)
   std::vector<DevBuf<unsigned long long>> timeline_buf;
   std::vector<int64_t> timeline_ctas;
@@ -1010,6 +1011,7 @@ void configure(kan_engine* e, const kan_config* c) {
   e->force_tab = std::getenv("KAN_TABLES") ? std::atoi(std::getenv("KAN_TABLES")) : -1;
   // off by default: on C3 the prepass saves layer 0 ~50 us but costs ~260 us
   // itself (measured); the path stays available and tested
+  e->conv3_mc = std::getenv("KAN_CONV3_MC") ? std::max(1, std::min(2, std::atoi(std::getenv("KAN_CONV3_MC")))) : 2;
   e->lv_sidecar = !(std::getenv("KAN_LV_SIDECAR") && std::atoi(std::getenv("KAN_LV_SIDECAR")) == 0);
   e->prepass_min = std::getenv("KAN_LEVEL_PREPASS_MIN") ? std::atoll(std::getenv("KAN_LEVEL_PREPASS_MIN"))
                                                         : std::numeric_limits<int64_t>::max();
@@ -1159,7 +1161,7 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
       const bool silu = pl.silu != 0;
       int variant = -1, SA = 2, SB = 0, SX = 2;
       for (int v : {2, 0}) {  // lane-private vals if it leaves >= 3 tap slots
-        if (e->tabs[v].bytes == 0) continue;
+        if (e->tabs[v].bytes == 0 || (e->force_tab >= 0 && v != e->force_tab)) continue;
         for (SB = 4; SB >= 2; --SB)
           if (conv3_smem_bytes(pl.BN, R, SA, SB, SX, io.x_kind, e->tabs[v].bytes, silu) <= 232448) break;
         if (SB >= (v == 2 ? 3 : 2)) {
@@ -1174,6 +1176,7 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
         p.SX = SX;
         p.nacc = 2;
         p.splits = 1;
+        p.mc = e->conv3_mc;
         p.tab = ts.buf.p;
         p.tab_bytes = ts.bytes;
         p.off_thr = ts.off_thr;

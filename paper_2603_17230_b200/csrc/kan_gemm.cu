@@ -162,6 +162,16 @@ __device__ __forceinline__ uint32_t cluster_rank() {
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
   return r;
 }
+__device__ __forceinline__ uint32_t cluster_id_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t n_clusters_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+  return r;
+}
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
   asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -745,44 +755,50 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
   } else if (warp == W_MMA) {
     // ============================ MMA issuer ==============================
+    // Warp-uniform waits and operands, one elected lane issues (operands stay
+    // in uniform registers: no per-MMA R2UR waterfall; it matters at small N).
     const uint32_t idesc = BF16 ? idesc_bf16(BN) : idesc_i8(BN, p.b_signed != 0);
-    const int nk = (p.dbg_flags & 2) ? 0 : KSTAGE / 32;
+    const bool no_mma = (p.dbg_flags & 2) != 0;
+    const uint32_t b_kstep = static_cast<uint32_t>(BN) * 8u;  // next 128-byte K block (x16 B)
     Ring ra(SA), rb(SB);
     int lt = 0;
     for (int t = blockIdx.x; t < n_tiles; t += tile_step, ++lt) {
       const int ab = nacc == 2 ? (lt & 1) : 0;
       const int use = nacc == 2 ? (lt >> 1) : lt;
       // the accumulator must have been drained by the epilogue of its last tile
-      mbar_wait(bar_accempty(ab), (use & 1) ^ 1);
+      mbar_wait_warp(bar_accempty(ab), (use & 1) ^ 1);
       tc_fence_after();
       const uint32_t dacc = tmem + static_cast<uint32_t>(ab) * BNa;
-      bool first = true;
+      uint32_t acc = 0u;
       for (int g = g0; g < g1; ++g) {
         const int nsp = min(C::GS, p.n_spline_stages - g * C::GS);
         for (int s = 0; s < nsp + (SILU ? 1 : 0); ++s, ra.next(), rb.next()) {
-          mbar_wait(bar_afull(ra.slot), ra.phase);
-          mbar_wait(bar_bfull(rb.slot), rb.phase);
+          mbar_wait_warp(bar_afull(ra.slot), ra.phase);
+          mbar_wait_warp(bar_bfull(rb.slot), rb.phase);
           tc_fence_after();
-          if (lane == 0) {
-            const uint32_t a_tmem = tmem + acol0 + acols * static_cast<uint32_t>(ra.slot);
-            const uint32_t b_addr = smem_u32(sB + static_cast<size_t>(rb.slot) * b_bytes);
-            for (int kk = 0; kk < nk; ++kk) {
-              // K step kk: SW128 block kk/4 of the stage's weight tile, 32 bytes in
-              const uint64_t bd = umma_desc_sw128(b_addr + (kk >> 2) * BN * 128 + 32 * (kk & 3));
-              const uint32_t acc = (first && kk == 0) ? 0u : 1u;
-              if (BF16)
-                mma_f16_ts(dacc, a_tmem + 8 * kk, bd, idesc, acc);
-              else
-                mma_i8_ts(dacc, a_tmem + 8 * kk, bd, idesc, acc);
+          const uint32_t a_tmem = tmem + acol0 + acols * static_cast<uint32_t>(ra.slot);
+          const uint64_t bd0 = umma_desc_sw128(smem_u32(sB + static_cast<size_t>(rb.slot) * b_bytes));
+          if (elect_one()) {
+            if (!no_mma) {
+#pragma unroll
+              for (int kk = 0; kk < KSTAGE / 32; ++kk) {
+                // K step kk: SW128 block kk/4 of the stage's weight tile, 32 bytes in
+                const uint64_t bd = bd0 + (kk >> 2) * b_kstep + 2 * (kk & 3);
+                const uint32_t a = kk == 0 ? acc : 1u;
+                if (BF16)
+                  mma_f16_ts(dacc, a_tmem + 8 * kk, bd, idesc, a);
+                else
+                  mma_i8_ts(dacc, a_tmem + 8 * kk, bd, idesc, a);
+              }
             }
             tc_commit(bar_aempty(ra.slot));
             tc_commit(bar_bempty(rb.slot));
           }
           __syncwarp();
-          first = false;
+          acc = 1u;
         }
       }
-      if (lane == 0) tc_commit(bar_accfull(ab));
+      if (elect_one()) tc_commit(bar_accfull(ab));
       __syncwarp();
     }
   } else if (warp < NPW) {

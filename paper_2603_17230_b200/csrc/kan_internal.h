@@ -30,6 +30,7 @@ struct GemmParams {
   int SB;  // weight-tile ring stages (released by the MMA)
   int SX;  // activation ring stages (released by the producers)
   int nacc;  // TMEM accumulators (2: the epilogue overlaps the next tile)
+  int mc;    // conv3: CTAs per cluster sharing (multicasting) the weight tiles
   // stage schedule
   int IPS, GS;
   int n_spline_stages, n_groups, silu;

@@ -161,6 +161,7 @@ CONV3_CASES = [
     (64, 32, 32, 64, True, 20),    # C4 shape, 160 tiles
     (40, 16, 16, 48, False, 80),   # partial channel chunk, 16x16 maps
     (32, 32, 32, 24, True, 19),    # one chunk
+    (32, 20, 32, 40, True, 31),    # 155 tiles: odd, the last weight-multicast pair has one tile
 ]
 
 
