@@ -534,3 +534,130 @@ int kor_im2col(const double* in, int C, int H, int W, int kernel, int stride, in
     }
   return 0;
 }
+
+/* ------------------------------------------------------------------------ */
+/* spline_table.hpp: spline-table mode                                       */
+/* ------------------------------------------------------------------------ */
+
+/* detail::build_tables, spline_table.hpp:38-85.  values [n_in][n_out][2^bits_a]
+ * (SplineTableSet::at, :31-33).  Input levels sit on the grid bounds
+ * (compute_quant_params(lo, hi, bits_a), :51); each spline is sampled at the
+ * dequantized level with basis_at_coord(knot_coord(x)) and the coefficient
+ * column dotted in k order (:59-71); one zero-spanning output range over the
+ * whole layer (RangeCalibrator + range(true) + zero_spanning, :73-76,
+ * quant.hpp:79-123) gives the shared h-bit output quantizer (:77-82). */
+int kor_spline_tables_build(const kor_grid* g, const double* coeffs, int n_in, int n_out,
+                            int bits_a, int h, uint8_t* values, double* qp_d, int64_t* qp_i) {
+  if (bits_a < 1 || bits_a > 8 || h < 2 || h > 8) return -1;
+  double in_s, out_s;
+  int64_t in_z, in_qhi, out_z, out_qhi;
+  if (kor_quant_params(g->lo, g->hi, bits_a, &in_s, &in_z, &in_qhi)) return -1;
+  const int64_t levels = (int64_t)1 << bits_a;
+  const int nb = g->intervals + g->degree;
+  const size_t n_tab = (size_t)n_in * (size_t)n_out;
+  double* sampled = (double*)malloc(sizeof(double) * n_tab * (size_t)levels);
+  double* basis = (double*)malloc(sizeof(double) * (size_t)nb * (size_t)levels);
+  if (!sampled || !basis) {
+    free(sampled);
+    free(basis);
+    return -1;
+  }
+  for (int64_t m = 0; m < levels; ++m) {
+    const double x = kor_dequantize(m, in_s, in_z);
+    kor_basis_at_coord(g, kor_knot_coord(g, x), basis + m * nb);
+  }
+  int seen = 0;
+  double lo = 0.0, hi = 0.0;
+  for (int i = 0; i < n_in; ++i)
+    for (int j = 0; j < n_out; ++j)
+      for (int64_t m = 0; m < levels; ++m) {
+        double acc = 0.0;
+        for (int k = 0; k < nb; ++k)
+          acc += basis[m * nb + k] * coeffs[((size_t)i * nb + k) * (size_t)n_out + j];
+        sampled[((size_t)i * n_out + j) * (size_t)levels + m] = acc;
+      }
+  /* RangeCalibrator::observe over sampled.flat() in row-major order */
+  for (size_t t = 0; t < n_tab * (size_t)levels; ++t) {
+    const double v = sampled[t];
+    if (!seen) {
+      lo = hi = v;
+      seen = 1;
+    } else {
+      lo = (v < lo) ? v : lo; /* std::min(lo, v) */
+      hi = (hi < v) ? v : hi; /* std::max(hi, v) */
+    }
+  }
+  if (!seen) { /* calibrate_range: empty stream */
+    free(sampled);
+    free(basis);
+    return -1;
+  }
+  if (lo == hi) { /* range(true): symmetric widening, quant.hpp:98-104 */
+    const double a = fabs(lo) > 1.0 ? fabs(lo) : 1.0;
+    const double pad = a * 2.220446049250313e-16 * 4.0;
+    lo = lo - pad;
+    hi = hi + pad;
+  }
+  lo = (0.0 < lo) ? 0.0 : lo; /* zero_spanning, quant.hpp:118-120 */
+  hi = (hi < 0.0) ? 0.0 : hi;
+  if (kor_quant_params(lo, hi, h, &out_s, &out_z, &out_qhi)) {
+    free(sampled);
+    free(basis);
+    return -1;
+  }
+  for (size_t t = 0; t < n_tab * (size_t)levels; ++t)
+    values[t] = (uint8_t)kor_quantize(sampled[t], out_s, out_z, 0, out_qhi);
+  free(sampled);
+  free(basis);
+  qp_d[0] = in_s;
+  qp_d[1] = out_s;
+  qp_i[0] = in_z;
+  qp_i[1] = in_qhi;
+  qp_i[2] = out_z;
+  qp_i[3] = out_qhi;
+  return 0;
+}
+
+/* Input level of one activation: quantize_value(x, in_qp), quant.hpp:51-54
+ * (no domain clamp: the level clamps, spline_table.hpp:98). */
+int64_t kor_spline_level(double x, double in_s, int64_t in_z, int64_t in_qhi) {
+  return kor_quantize(x, in_s, in_z, 0, in_qhi);
+}
+
+/* Integer form of spline_table_forward (spline_table.hpp:90-107): levels
+ * [M, n_in] -> acc[m, j] = sum_i (table[i][j][level] - z_out), the int64 sum
+ * the reference dequantizes once per output (out = s_out * acc). */
+int kor_spline_table_accumulate(const uint8_t* values, int n_in, int n_out, int bits_a,
+                                int64_t out_z, int64_t M, const uint8_t* levels, int64_t* acc) {
+  const int64_t E = (int64_t)1 << bits_a;
+  for (int64_t m = 0; m < M; ++m)
+    for (int j = 0; j < n_out; ++j) {
+      int64_t a = 0;
+      for (int i = 0; i < n_in; ++i)
+        a += (int64_t)values[((size_t)i * n_out + j) * (size_t)E + levels[m * n_in + i]] - out_z;
+      acc[m * n_out + j] = a;
+    }
+  return 0;
+}
+
+/* spline_table_forward, spline_table.hpp:90-107: fp64 activations -> outputs */
+int kor_spline_table_forward(const uint8_t* values, int n_in, int n_out, int bits_a,
+                             const double* qp_d, const int64_t* qp_i, int64_t M,
+                             const double* acts, double* out) {
+  uint8_t* lv = (uint8_t*)malloc((size_t)(n_in > 0 ? n_in : 1));
+  int64_t* acc = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n_out > 0 ? n_out : 1));
+  if (!lv || !acc) {
+    free(lv);
+    free(acc);
+    return -1;
+  }
+  for (int64_t m = 0; m < M; ++m) {
+    for (int i = 0; i < n_in; ++i)
+      lv[i] = (uint8_t)kor_spline_level(acts[m * n_in + i], qp_d[0], qp_i[0], qp_i[1]);
+    kor_spline_table_accumulate(values, n_in, n_out, bits_a, qp_i[2], 1, lv, acc);
+    for (int j = 0; j < n_out; ++j) out[m * n_out + j] = qp_d[1] * (double)acc[j];
+  }
+  free(lv);
+  free(acc);
+  return 0;
+}

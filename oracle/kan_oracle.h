@@ -137,6 +137,22 @@ int8_t kor_requant_i8(double y, double s_out);
 int kor_im2col(const double* in, int C, int H, int W, int kernel, int stride, int padding,
                double* out /* [Ho*Wo, K*K*C] */);
 
+
+/* ---- spline_table.hpp: spline-table mode -------------------------------- */
+/* build_spline_tables (spline_table.hpp:38-85): values [n_in][n_out][2^bits_a];
+ * qp_d = {in_scale, out_scale}; qp_i = {in_zp, in_qhi, out_zp, out_qhi}. */
+int kor_spline_tables_build(const kor_grid* g, const double* coeffs, int n_in, int n_out,
+                            int bits_a, int h, uint8_t* values, double* qp_d, int64_t* qp_i);
+/* quantize_value(x, in_qp) (quant.hpp:51-54) */
+int64_t kor_spline_level(double x, double in_s, int64_t in_z, int64_t in_qhi);
+/* integer sums sum_i (table[i][j][level] - z_out), levels [M, n_in] u8 */
+int kor_spline_table_accumulate(const uint8_t* values, int n_in, int n_out, int bits_a,
+                                int64_t out_z, int64_t M, const uint8_t* levels, int64_t* acc);
+/* spline_table_forward (spline_table.hpp:90-107) */
+int kor_spline_table_forward(const uint8_t* values, int n_in, int n_out, int bits_a,
+                             const double* qp_d, const int64_t* qp_i, int64_t M,
+                             const double* acts, double* out);
+
 #ifdef __cplusplus
 }
 #endif

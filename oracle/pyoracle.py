@@ -92,6 +92,14 @@ class Oracle:
         L.kor_requant_i8.argtypes = [C.c_double, C.c_double]
         L.kor_requant_i8.restype = C.c_int8
         L.kor_im2col.argtypes = [_dp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _dp]
+        L.kor_spline_tables_build.argtypes = [G, _dp, C.c_int, C.c_int, C.c_int, C.c_int, _u8p,
+                                              _dp, _i64p]
+        L.kor_spline_level.argtypes = [C.c_double, C.c_double, C.c_int64, C.c_int64]
+        L.kor_spline_level.restype = C.c_int64
+        L.kor_spline_table_accumulate.argtypes = [_u8p, C.c_int, C.c_int, C.c_int, C.c_int64,
+                                                  C.c_int64, _u8p, _i64p]
+        L.kor_spline_table_forward.argtypes = [_u8p, C.c_int, C.c_int, C.c_int, _dp, _i64p,
+                                               C.c_int64, _dp, _dp]
 
     # -- grid / quant ---------------------------------------------------------
     def grid(self, G, P, lo=-1.0, hi=1.0):
@@ -302,6 +310,88 @@ class Oracle:
         return np.ascontiguousarray(t.transpose(0, 3, 4, 1, 2)).reshape(M * Ho * Wo,
                                                                         Cc * kernel * kernel)
 
+    # -- spline-table mode (spline_table.hpp) ------------------------------------
+    def spline_tables(self, g, coeffs, n_in, n_out, bits_a, h):
+        """build_spline_tables: dict(values [n_in, n_out, 2^bits_a] u8, qp_d, qp_i)."""
+        coeffs = np.ascontiguousarray(coeffs, dtype=np.float64)
+        vals = np.zeros(n_in * n_out << bits_a, dtype=np.uint8)
+        qd, qi = np.zeros(2), np.zeros(4, dtype=np.int64)
+        if self.lib.kor_spline_tables_build(C.byref(g), coeffs.ravel(), n_in, n_out, bits_a, h,
+                                            vals, qd, qi):
+            raise ValueError("build_spline_tables: invalid arguments")
+        return {"values": vals.reshape(n_in, n_out, 1 << bits_a), "qp_d": qd, "qp_i": qi,
+                "bits_a": bits_a, "h": h, "n_in": n_in, "n_out": n_out}
+
+    def spline_levels(self, t, x):
+        """quantize_value(x, in_qp) per element (u8)."""
+        x = np.asarray(x, dtype=np.float64)
+        s, z, qh = t["qp_d"][0], int(t["qp_i"][0]), int(t["qp_i"][1])
+        f = np.vectorize(lambda v: self.lib.kor_spline_level(float(v), s, z, qh), otypes=[np.uint8])
+        return f(x) if x.size else x.astype(np.uint8)
+
+    def spline_accumulate(self, t, levels):
+        lv = np.ascontiguousarray(levels, dtype=np.uint8)
+        M = lv.shape[0]
+        acc = np.zeros((M, t["n_out"]), dtype=np.int64)
+        self.lib.kor_spline_table_accumulate(np.ascontiguousarray(t["values"]).ravel(), t["n_in"],
+                                             t["n_out"], t["bits_a"], int(t["qp_i"][2]), M,
+                                             lv.ravel(), acc)
+        return acc
+
+    def spline_forward(self, t, acts):
+        acts = np.ascontiguousarray(acts, dtype=np.float64)
+        out = np.zeros((acts.shape[0], t["n_out"]))
+        self.lib.kor_spline_table_forward(np.ascontiguousarray(t["values"]).ravel(), t["n_in"],
+                                          t["n_out"], t["bits_a"], t["qp_d"], t["qp_i"],
+                                          acts.shape[0], acts, out)
+        return out
+
+    def spline_model_tables(self, desc, Ws, bits_a, h):
+        G, P = desc["grid"]["intervals"], desc["grid"]["degree"]
+        lo, hi = desc.get("domain", [-1.0, 1.0])
+        g = self.grid(G, P, lo, hi)
+        tabs, ki, shape = [], 0, list(desc["input"])
+        for l in desc["layers"]:
+            if l["type"] == "linear":
+                tabs.append(self.spline_tables(g, Ws[ki], l["n_in"], l["n_out"], bits_a, h))
+                ki += 1
+            elif l["type"] == "conv":
+                kk = l["kernel"]
+                tabs.append(self.spline_tables(g, Ws[ki], l["c_in"] * kk * kk, l["c_out"], bits_a, h))
+                ki += 1
+        return tabs
+
+    def spline_model_forward(self, desc, tabs, x):
+        """model_forward in spline-table mode (eval.hpp:135-193, 200-253): fp64
+        values flow between layers; each KAN layer quantizes its input with
+        quantize_value and sums table entries; conv layers go through im2col
+        (layers.hpp:126-154); maxpool2 / flatten act on values."""
+        M = x.shape[0]
+        v = np.asarray(x, dtype=np.float64).reshape(M, *desc["input"])
+        ki = 0
+        for l in desc["layers"]:
+            typ = l["type"]
+            if typ == "linear":
+                v = self.spline_forward(tabs[ki], v.reshape(M, -1))
+                ki += 1
+            elif typ == "conv":
+                kk, s_, p_ = l["kernel"], l.get("stride", 1), l.get("padding", 0)
+                Ho = (v.shape[2] + 2 * p_ - kk) // s_ + 1
+                Wo = (v.shape[3] + 2 * p_ - kk) // s_ + 1
+                cols = np.concatenate([self.im2col(v[m], kk, s_, p_) for m in range(M)])
+                y = self.spline_forward(tabs[ki], cols)
+                v = y.reshape(M, Ho, Wo, -1).transpose(0, 3, 1, 2)
+                ki += 1
+            elif typ == "maxpool":
+                w = l.get("window", 2)
+                Ho, Wo = v.shape[2] // w, v.shape[3] // w
+                v = v[:, :, :Ho * w, :Wo * w].reshape(M, v.shape[1], Ho, w, Wo, w).max(axis=(3, 5))
+            elif typ == "flatten":
+                v = v.reshape(M, -1)
+            else:
+                raise ValueError(typ)
+        return v
+
     @staticmethod
     def storage_kinds(desc):
         """Engine storage rule (kan_engine.cpp plan_buffers): a stored tensor keeps
@@ -441,6 +531,12 @@ class Ref:
         L.ref_validate_descriptor.argtypes = [C.c_char_p]
         L.ref_graph_forward.argtypes = [C.c_char_p, C.POINTER(C.c_void_p), C.c_int, C.c_int,
                                         C.c_int, C.c_int64, _dp, C.c_int64, _dp, C.c_int]
+        L.ref_spline_tables.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int,
+                                        C.c_int, C.c_int, C.c_int, _dp, C.c_int, C.c_int, _u8p,
+                                        C.c_int64, _dp, _i64p]
+        L.ref_spline_tables.restype = C.c_int64
+        L.ref_spline_table_forward.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _u8p, _dp, _i64p,
+                                               C.c_int64, _dp, _dp]
         L.ref_model_forward.argtypes = [C.c_char_p, C.POINTER(C.c_void_p), C.c_int, C.c_int,
                                         C.c_int, C.c_int, C.c_int64, C.c_int64, _dp, C.c_int64,
                                         _dp, C.c_int, C.c_int64]
@@ -549,6 +645,30 @@ class Ref:
         out = np.zeros((inputs.shape[0], n_out))
         if self.lib.ref_graph_forward(text.encode(), ptrs, k, h, bits_w, inputs.shape[0], inputs,
                                       n_out, out, threads):
+            raise ValueError(self.err())
+        return out
+
+    def spline_tables(self, G, P, coeffs, n_in, n_out, bits_a, h, kernel=0, stride=1, padding=0,
+                      lo=-1.0, hi=1.0):
+        """build_spline_tables for a linear (kernel=0; n_in inputs) or conv layer
+        (n_in = c_in); returns the same dict as Oracle.spline_tables plus bits."""
+        coeffs = np.ascontiguousarray(coeffs, dtype=np.float64)
+        rows = n_in * (kernel * kernel if kernel else 1)
+        vals = np.zeros(rows * n_out << bits_a, dtype=np.uint8)
+        qd, qi = np.zeros(2), np.zeros(4, dtype=np.int64)
+        bits = self.lib.ref_spline_tables(G, P, lo, hi, n_in, n_out, kernel, stride, padding,
+                                          coeffs.ravel(), bits_a, h, vals, vals.size, qd, qi)
+        if bits < 0:
+            raise ValueError(self.err())
+        return {"values": vals.reshape(rows, n_out, 1 << bits_a), "qp_d": qd, "qp_i": qi,
+                "bits_a": bits_a, "h": h, "n_in": rows, "n_out": n_out, "stored_bits": bits}
+
+    def spline_forward(self, t, acts):
+        acts = np.ascontiguousarray(acts, dtype=np.float64)
+        out = np.zeros((acts.shape[0], t["n_out"]))
+        if self.lib.ref_spline_table_forward(t["n_in"], t["n_out"], t["bits_a"], t["h"],
+                                             np.ascontiguousarray(t["values"]).ravel(), t["qp_d"],
+                                             t["qp_i"], acts.shape[0], acts, out):
             raise ValueError(self.err())
         return out
 

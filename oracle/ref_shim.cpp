@@ -19,6 +19,7 @@
 #include <kantize/lut.hpp>
 #include <kantize/quant.hpp>
 #include <kantize/cost.hpp>
+#include <kantize/spline_table.hpp>
 
 #include <algorithm>
 #include <cstdint>
@@ -211,6 +212,66 @@ int ref_conv_forward(int G, int P, double lo, double hi, int mode, int k, int h,
   return fail(e);
 }
 
+// build_spline_tables (spline_table.hpp:87-95) for a linear layer (kernel == 0)
+// or a conv layer (c_in = n_in, c_out = n_out, kernel/stride/padding); values
+// [table_count * 2^bits_a]; qp_d = {in_scale, out_scale}; qp_i = {in_zp,
+// in_qhi, out_zp, out_qhi}.  Returns stored_bits(), or -1.
+int64_t ref_spline_tables(int G, int P, double lo, double hi, int n_in, int n_out, int kernel,
+                          int stride, int padding, const double* coeffs, int bits_a, int h,
+                          uint8_t* values, int64_t cap, double* qp_d, int64_t* qp_i) try {
+  const GridSpec g = build_grid(G, P, lo, hi);
+  SplineTableSet set;
+  if (kernel == 0) {
+    KanLinearLayer l = KanLinearLayer::zeros(n_in, n_out, g);
+    std::copy(coeffs, coeffs + l.coeffs.size(), l.coeffs.flat().begin());
+    set = build_spline_tables(l, bits_a, h);
+  } else {
+    ConvKanLayer c = ConvKanLayer::zeros(n_in, n_out, kernel, stride, padding, g);
+    std::copy(coeffs, coeffs + c.coeffs.size(), c.coeffs.flat().begin());
+    set = build_spline_tables(c, bits_a, h);
+  }
+  if (static_cast<int64_t>(set.values.size()) > cap) {
+    g_err = "ref_spline_tables: capacity";
+    return -1;
+  }
+  std::copy(set.values.begin(), set.values.end(), values);
+  qp_d[0] = set.in_qp.scale;
+  qp_d[1] = set.out_qp.scale;
+  qp_i[0] = set.in_qp.zero_point;
+  qp_i[1] = set.in_qp.q_hi;
+  qp_i[2] = set.out_qp.zero_point;
+  qp_i[3] = set.out_qp.q_hi;
+  return set.stored_bits();
+} catch (const std::exception& e) {
+  return fail(e);
+}
+
+// spline_table_forward (spline_table.hpp:90-107) over a table set rebuilt
+// from its parts (values [n_in][n_out][2^bits_a], quantizers as above)
+int ref_spline_table_forward(int n_in, int n_out, int bits_a, int h, const uint8_t* values,
+                             const double* qp_d, const int64_t* qp_i, int64_t M,
+                             const double* acts, double* out) try {
+  SplineTableSet set;
+  set.n_in = n_in;
+  set.n_out = n_out;
+  set.bits_a = bits_a;
+  set.value_bits = h;
+  set.in_qp = compute_quant_params(-1.0, 1.0, bits_a);
+  set.in_qp.scale = qp_d[0];
+  set.in_qp.zero_point = qp_i[0];
+  set.in_qp.q_hi = qp_i[1];
+  set.out_qp = compute_quant_params(-1.0, 1.0, h);
+  set.out_qp.scale = qp_d[1];
+  set.out_qp.zero_point = qp_i[2];
+  set.out_qp.q_hi = qp_i[3];
+  set.values.assign(values, values + set.table_count() * set.entries_per_table());
+  const Matrix r = spline_table_forward(make_matrix(M, n_in, acts), set);
+  std::copy(r.flat().begin(), r.flat().end(), out);
+  return 0;
+} catch (const std::exception& e) {
+  return fail(e);
+}
+
 // cost.hpp:68-74 mul_counts_layer().matmul via a descriptor (algorithmic work)
 int ref_validate_descriptor(const char* json_text) try {
   const Model m = model_from_descriptor(nlohmann::json::parse(json_text));
@@ -221,7 +282,8 @@ int ref_validate_descriptor(const char* json_text) try {
 
 // model_forward / predict (eval.hpp:200-276) over a descriptor-built model
 // (io.hpp:357-386).  coeff_ptrs[i] = coefficients of the i-th KAN layer.
-// mode: 0 fp32 (EvalMode::kFp32), 2 bspline-lut (EvalMode::kBsplineLut).
+// mode: 0 fp32 (EvalMode::kFp32), 2 bspline-lut (EvalMode::kBsplineLut),
+// 3 spline-table (EvalMode::kSplineTable; bits_a = k, value bits = h).
 // The batch is sharded over `threads` std::threads in chunks of `chunk`
 // rows (the forward is reentrant).
 int ref_model_forward(const char* json_text, const double* const* coeff_ptrs, int mode, int k,
@@ -239,11 +301,22 @@ int ref_model_forward(const char* json_text, const double* const* coeff_ptrs, in
       ++li;
     }
   }
-  const BsplineLut lut = build_bspline_lut(model.grid().degree(), k, h);
+  const BsplineLut lut = build_bspline_lut(model.grid().degree(), mode == 3 ? 8 : k, h);
+  // spline-table mode: one table set per KAN layer at (bits_a = k, h), as
+  // run_sweep builds them (sweep.hpp:239-256)
+  std::vector<SplineTableSet> tables;
+  if (mode == 3)
+    for (const auto& layer : model.layers) {
+      if (const auto* lin = std::get_if<KanLinearLayer>(&layer))
+        tables.push_back(build_spline_tables(*lin, k, h));
+      else if (const auto* conv = std::get_if<ConvKanLayer>(&layer))
+        tables.push_back(build_spline_tables(*conv, k, h));
+    }
   EvalOptions opts;
-  opts.mode = mode == 2 ? EvalMode::kBsplineLut : EvalMode::kFp32;
+  opts.mode = mode == 2 ? EvalMode::kBsplineLut : (mode == 3 ? EvalMode::kSplineTable : EvalMode::kFp32);
   opts.qcfg.bits_w = mode == 2 ? bits_w : kPassthroughBits;
   opts.lut = &lut;
+  opts.tables = &tables;
   if (threads < 1) threads = 1;
   if (chunk < 1) chunk = 256;
   std::vector<std::thread> pool;
