@@ -21,6 +21,9 @@
  *   kan_engine_layer_accumulators  the int32 form of the contraction behind
  *                               tabulated_kan_forward               lut.hpp:217-231
  *   kan_lut_build               build_bspline_lut                   lut.hpp:103-131
+ *   kan_engine_set_spline_tables  EvalOptions::tables (SplineTableSet) eval.hpp:41,
+ *                               spline_table.hpp:19-34
+ *   kan_engine_spline_table     build_spline_tables (probe)         spline_table.hpp:38-95
  *
  * Error mapping (reference exception -> status):
  *   std::invalid_argument (bits, LUT params, mode)  -> KAN_ERR_INVALID_ARGUMENT
@@ -63,11 +66,14 @@ typedef enum {
 } kan_status;
 
 /* Forward datapaths (EvalMode, eval.hpp:17; BF16 is new, FP32 = kFp32,
- * BSPLINE_LUT = kBsplineLut). */
+ * BSPLINE_LUT = kBsplineLut, SPLINE_TABLE = kSplineTable). */
 typedef enum {
-  KAN_MODE_FP32 = 0,        /* fp32 Cox-de Boor basis + fp32 FFMA contraction */
-  KAN_MODE_BF16 = 1,        /* fp32 basis -> bf16, tcgen05 kind::f16, fp32 accumulate */
-  KAN_MODE_BSPLINE_LUT = 2  /* lattice + quantized LUT, tcgen05 kind::i8, int32 accumulate */
+  KAN_MODE_FP32 = 0,         /* fp32 Cox-de Boor basis + fp32 FFMA contraction */
+  KAN_MODE_BF16 = 1,         /* fp32 basis -> bf16, tcgen05 kind::f16, fp32 accumulate */
+  KAN_MODE_BSPLINE_LUT = 2,  /* lattice + quantized LUT, tcgen05 kind::i8, int32 accumulate */
+  KAN_MODE_SPLINE_TABLE = 3  /* per-connection spline tables, gather + integer add
+                                (spline_table.hpp:19-123); lut_k = input bits bits_a,
+                                lut_h = value bits h */
 } kan_mode;
 
 /* Weight quantization on the LUT path. */
@@ -83,8 +89,9 @@ typedef enum {
 
 typedef struct {
   int mode;         /* kan_mode */
-  int lut_k;        /* LUT address bits per knot interval, 1..8 (lut.hpp:22) */
-  int lut_h;        /* LUT value bits, 2..8 (lut.hpp:75) */
+  int lut_k;        /* LUT address bits per knot interval, 1..8 (lut.hpp:22);
+                       spline-table mode: input address bits bits_a, 1..8 */
+  int lut_h;        /* LUT value bits, 2..8 (lut.hpp:75); spline-table mode: h */
   int bits_w;       /* weight bits: 1..8 per-tensor, 2..8 per-channel (8 and 4 tested) */
   int w_scheme;     /* kan_wscheme */
   int silu_base;    /* 1: add SiLU(x) . w_base (needs kan_engine_set_coeffs base weights) */
@@ -129,15 +136,32 @@ kan_status kan_engine_predict(kan_engine* e, const float* x_dev, int64_t batch,
                               int32_t* labels_dev, void* stream);
 
 /* Parity probes ------------------------------------------------------------ */
-/* Lattice levels of fp32 activations under layer `layer`'s grid and lut_k. */
+/* Lattice levels of fp32 activations under layer `layer`'s grid and lut_k
+ * (spline-table mode: quantize_value on the grid bounds at bits_a). */
 kan_status kan_engine_layer_levels(kan_engine* e, int layer, const float* x_dev, int64_t n,
                                    uint16_t* levels_dev, void* stream);
-/* Raw int32 accumulators of one LUT layer given its input levels [batch, n_in]:
+/* Raw int32 accumulators of one LUT layer given its input levels [batch, n_in]
+ * (spline-table mode: acc_s = sum_i (table[i][j][level] - z_out), acc_b unused):
  * acc_s [batch, n_out] (spline part), acc_b [batch, n_out] (SiLU base part;
  * may be NULL). */
 kan_status kan_engine_layer_accumulators(kan_engine* e, int layer, const uint16_t* levels_dev,
                                          int64_t batch, int32_t* acc_s_dev, int32_t* acc_b_dev,
                                          void* stream);
+/* Spline-table mode ------------------------------------------------------- */
+/* Supply the tables of KAN layer `layer` (SplineTableSet, spline_table.hpp:19-34;
+ * EvalOptions::tables, eval.hpp:41), e.g. read from a .kant container
+ * (io.hpp:335-344), instead of building them from the coefficients at configure:
+ * values [n_in][n_out][2^bits_a] (n_in = patch size for conv layers),
+ * qp_d = {in_scale, out_scale}, qp_i = {in_zero_point, in_q_hi, out_zero_point,
+ * out_q_hi}.  n = 0 clears them. */
+kan_status kan_engine_set_spline_tables(kan_engine* e, int layer, const uint8_t* values, int64_t n,
+                                        int bits_a, int h, const double* qp_d, const int64_t* qp_i);
+/* Host copy of the configured tables of KAN layer `layer` in the reference
+ * layout [n_in][n_out][2^bits_a] (SplineTableSet::values) and its quantizers
+ * (as above).  Returns the entry count, or a negative status. */
+int64_t kan_engine_spline_table(kan_engine* e, int layer, uint8_t* out, int64_t cap, double* qp_d,
+                                int64_t* qp_i);
+
 /* Host copy of the configured table (BsplineLut::entries). Returns entry count. */
 int64_t kan_engine_lut(const kan_engine* e, uint8_t* out, int64_t cap);
 /* Kernels launched by the most recent forward call. */
@@ -164,6 +188,14 @@ int64_t kan_lut_build(int degree, int k, int h, uint8_t* out, int64_t cap);
  * (lut.hpp:44-47, grid.hpp:49-56).  `out` holds L+2 floats.  Returns L+2. */
 int64_t kan_lattice_thresholds(int intervals, int degree, double lo, double hi, int k,
                                float* out, int64_t cap);
+
+/* Host utility: the spline-table input level thresholds the GPU uses,
+ * thr[n] = smallest fp32 x with quantize_value(x, in_qp) >= n for n = 1..2^bits_a-1
+ * (thr[0] = -inf), in_qp = compute_quant_params(lo, hi, bits_a) (quant.hpp:33-54,
+ * spline_table.hpp:51); thr[2^bits_a] = the smallest fp32 x whose llround
+ * overflows (level 0 there, as for NaN, on the reference's x86-64 build).
+ * Returns 2^bits_a + 1, or -KAN_ERR_INVALID_ARGUMENT. */
+int64_t kan_spline_thresholds(double lo, double hi, int bits_a, float* out, int64_t cap);
 
 #ifdef __cplusplus
 }

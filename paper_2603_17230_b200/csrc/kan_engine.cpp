@@ -58,6 +58,17 @@ cudaError_t launch_maxpool(bool levels, const void* in, int64_t n_img, int H, in
                            int ld_in, int win, void* out, int ld_out, cudaStream_t st);
 cudaError_t launch_avgpool(const void* in, int64_t n_img, int HW, int C, int ld_in, void* out,
                            int ld_out, cudaStream_t st);
+// spline-table mode (kan_spline_table.cu)
+cudaError_t launch_st_sample(const double* basis, const double* coeffs, int n_in, int n_out, int nb, int Lv,
+                             int pass, unsigned long long* mm, uint8_t* T, int Np, double s, double zd,
+                             long long qhi, cudaStream_t st);
+cudaError_t launch_st_layer(const StParams& p, cudaStream_t st);
+size_t st_layer_smem(const StParams& p);
+cudaError_t launch_st_levels(const float* x, int64_t n, const float* thr, float inv_s, float zf, int qhi,
+                             void* out, int out_u16, cudaStream_t st);
+cudaError_t launch_u16_to_u8(const uint16_t* in, int64_t n, uint8_t* out, cudaStream_t st);
+cudaError_t launch_st_maxpool(const uint8_t* in, int64_t planes, int H, int W, int win, uint8_t* out,
+                              cudaStream_t st);
 
 struct CudaError : std::runtime_error {
   using std::runtime_error::runtime_error;
@@ -137,6 +148,22 @@ struct Layer {
   bool im2col = false;
   std::vector<double> coeffs;  // reference layout [n_in*nb, n_out]
   std::vector<double> base_w;  // [n_in, n_out]
+  // spline-table mode: tables supplied by the caller (EvalOptions::tables,
+  // eval.hpp:41; e.g. loaded from a .kant container) instead of built from
+  // the coefficients; values in the reference layout [n_in][n_out][2^bits_a]
+  std::vector<uint8_t> st_values;
+  int st_bits_a = 0, st_h = 0;
+  double st_qd[2] = {0, 0};
+  int64_t st_qi[4] = {0, 0, 0, 0};
+};
+
+// Device state of one spline-table layer (SplineTableSet, spline_table.hpp:19-34)
+struct StLayer {
+  DevBuf<uint8_t> T;  // [n_in][Lv][Np]
+  int n_in = 0, n_out = 0, Np = 0, lpr = 1, col_tiles = 1;
+  int bits_a = 0, h = 0;
+  double in_s = 1.0, out_s = 1.0;
+  int64_t in_z = 0, in_qhi = 0, out_z = 0, out_qhi = 0;
 };
 
 // Device-side state of one configured KAN layer.
@@ -257,6 +284,12 @@ struct kan_engine {
   DevBuf<uint16_t> xlev;  // level prepass of a large fp32-input dense layer
   DevBuf<uint16_t> xcol;  // level im2col of the model input (stem convs)
   DevBuf<float> logits_tmp;
+  // spline-table mode
+  std::vector<StLayer> st;
+  QParams st_in;            // input quantizer on the grid bounds (spline_table.hpp:51)
+  DevBuf<float> st_thr;     // its exact fp32 thresholds
+  DevBuf<uint8_t> st_xlev;  // u8 levels of an image model input
+  DevBuf<uint8_t> st_probe;
   DevBuf<uint8_t> io_in, io_out;
   int last_launches = 0;
   // optional per-CTA phase timestamps of each layer's last launch (tuning aid)
@@ -902,11 +935,274 @@ void plan_buffers(kan_engine* e) {
   e->input_f32 = need_in;
 }
 
+// ---------------------------------------------------------------------------
+// Spline-table mode (EvalMode::kSplineTable, eval.hpp:17, 121-127, 137, 168):
+// every KAN layer is replaced by its per-connection tables and the forward is
+// table lookups + integer additions (spline_table.hpp:90-123).
+
+static double key_to_double(unsigned long long k) {
+  const unsigned long long u = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  double d;
+  std::memcpy(&d, &u, 8);
+  return d;
+}
+
+static void st_geometry(StLayer& sl) {
+  sl.Np = (sl.n_out + 15) / 16 * 16;
+  const int lanes = sl.Np / 16;
+  int lpr = 1;
+  while (lpr < lanes && lpr < 32) lpr *= 2;
+  sl.lpr = lpr;
+  sl.col_tiles = (lanes + lpr - 1) / lpr;
+}
+
+// build_spline_tables (spline_table.hpp:38-95) on the device: fp64 samples in
+// the reference's order, min/max fold, zero-spanning h-bit quantizer
+// (RangeCalibrator + range(true) + zero_spanning, quant.hpp:79-123), quantized
+// entries written straight into the gather layout.
+static void st_build_layer(kan_engine* e, const Layer& l, StLayer& sl, int bits_a, int h) {
+  const Grid& g = e->grid;
+  const int nb = g.nb();
+  const int64_t Lv = int64_t{1} << bits_a;
+  std::vector<double> basis(static_cast<size_t>(Lv * nb));
+  for (int64_t m = 0; m < Lv; ++m) {
+    const double x = e->st_in.scale * static_cast<double>(m - e->st_in.zp);  // dequantize_value
+    g.basis_at_coord(g.knot_coord(x), &basis[static_cast<size_t>(m * nb)]);
+  }
+  DevBuf<double> d_basis, d_coeffs;
+  d_basis.upload(basis);
+  d_coeffs.upload(l.coeffs);
+  DevBuf<unsigned long long> mm;
+  const std::vector<unsigned long long> init = {~0ull, 0ull};
+  mm.upload(init);
+  ck(launch_st_sample(d_basis.p, d_coeffs.p, sl.n_in, sl.n_out, nb, static_cast<int>(Lv), 0, mm.p, nullptr,
+                      sl.Np, 1.0, 0.0, 0, nullptr),
+     "spline table sampling");
+  unsigned long long keys[2];
+  ck(cudaMemcpy(keys, mm.p, sizeof(keys), cudaMemcpyDeviceToHost), "spline table range");
+  if (keys[0] == ~0ull) throw InvalidArgument("calibrate_range: empty stream");
+  double lo = key_to_double(keys[0]), hi = key_to_double(keys[1]);
+  if (lo == hi) {  // RangeCalibrator::range(true): symmetric widening
+    const double pad = std::max(std::abs(lo), 1.0) * std::numeric_limits<double>::epsilon() * 4.0;
+    lo = lo - pad;
+    hi = hi + pad;
+  }
+  lo = std::min(lo, 0.0);  // zero_spanning
+  hi = std::max(hi, 0.0);
+  const QParams oq = quant_params(lo, hi, h);
+  sl.out_s = oq.scale;
+  sl.out_z = oq.zp;
+  sl.out_qhi = oq.qhi;
+  sl.T.alloc(static_cast<size_t>(sl.n_in) * static_cast<size_t>(Lv) * sl.Np, true);
+  ck(launch_st_sample(d_basis.p, d_coeffs.p, sl.n_in, sl.n_out, nb, static_cast<int>(Lv), 1, mm.p, sl.T.p,
+                      sl.Np, oq.scale, static_cast<double>(oq.zp), oq.qhi, nullptr),
+     "spline table quantization");
+  ck(cudaDeviceSynchronize(), "spline table build");
+}
+
+// tables supplied by the caller: reference layout [n_in][n_out][2^bits_a] ->
+// gather layout [n_in][2^bits_a][Np]
+static void st_import_layer(const Layer& l, StLayer& sl) {
+  const int64_t Lv = int64_t{1} << l.st_bits_a;
+  std::vector<uint8_t> t(static_cast<size_t>(sl.n_in) * static_cast<size_t>(Lv) * sl.Np, 0);
+  for (int i = 0; i < sl.n_in; ++i)
+    for (int j = 0; j < sl.n_out; ++j)
+      for (int64_t m = 0; m < Lv; ++m)
+        t[(static_cast<size_t>(i) * Lv + m) * sl.Np + j] =
+            l.st_values[(static_cast<size_t>(i) * sl.n_out + j) * Lv + m];
+  sl.T.upload(t);
+  sl.out_s = l.st_qd[1];
+  sl.out_z = l.st_qi[2];
+  sl.out_qhi = l.st_qi[3];
+}
+
+void configure_st(kan_engine* e, const kan_config& cfg) {
+  const int bits_a = cfg.lut_k, h = cfg.lut_h;
+  // argument checks in build_tables order (spline_table.hpp:40-43)
+  if (bits_a < 1 || bits_a > 8) throw InvalidArgument("build_spline_tables: input bits must be in [1,8]");
+  if (h < 2 || h > 8) throw InvalidArgument("build_spline_tables: value bits must be in [2,8]");
+  if (cfg.out_kind != KAN_OUT_F32) throw InvalidArgument("int8 outputs are only produced on the LUT path");
+  if (cfg.silu_base) throw InvalidArgument("spline-table mode has no SiLU base term (spline_table.hpp:14-18)");
+  if (e->grid.nb() > 32) throw Unsupported("spline-table mode supports G+P <= 32");
+  for (const auto& l : e->layers) {
+    if (l.res_src != -2 || l.type == L_AVGPOOL)
+      throw Unsupported("spline-table mode runs the reference layer set (linear, conv, maxpool, flatten)");
+  }
+  e->st_in = quant_params(e->grid.lo, e->grid.hi, bits_a);  // spline_table.hpp:51
+  e->st_thr.upload(quant_thresholds(e->st_in));
+  e->st.clear();
+  e->st.resize(static_cast<size_t>(e->n_kan));
+  for (const auto& l : e->layers) {
+    if (l.type != L_LINEAR && l.type != L_CONV) continue;
+    StLayer& sl = e->st[static_cast<size_t>(l.kan_index)];
+    sl.n_in = l.type == L_LINEAR ? l.n_in : l.kernel * l.kernel * l.c_in;  // patch_size for conv
+    sl.n_out = l.type == L_LINEAR ? l.n_out : l.c_out;
+    sl.bits_a = bits_a;
+    sl.h = h;
+    sl.in_s = e->st_in.scale;
+    sl.in_z = e->st_in.zp;
+    sl.in_qhi = e->st_in.qhi;
+    st_geometry(sl);
+    if (!l.st_values.empty()) {
+      if (l.st_bits_a != bits_a)
+        throw InvalidArgument("spline tables of KAN layer " + std::to_string(l.kan_index) +
+                              " were supplied for " + std::to_string(l.st_bits_a) + " input bits");
+      st_import_layer(l, sl);
+    } else {
+      if (l.coeffs.size() != static_cast<size_t>(sl.n_in) * e->grid.nb() * sl.n_out)
+        throw InvalidArgument("coefficients of KAN layer " + std::to_string(l.kan_index) + " not set");
+      st_build_layer(e, l, sl, bits_a, h);
+    }
+  }
+}
+
+static StParams st_params(const kan_engine* e, const StLayer& sl) {
+  StParams p{};
+  p.n_in = sl.n_in;
+  p.n_out = sl.n_out;
+  p.Np = sl.Np;
+  p.Lv = 1 << sl.bits_a;
+  p.lpr = sl.lpr;
+  p.col_tiles = sl.col_tiles;
+  const int RP = 256 / sl.lpr;
+  int ic = std::min(256, (49152 / RP - 4) / 8 * 8);
+  ic = std::min(ic, (sl.n_in + 7) / 8 * 8);
+  p.ic = std::max(ic, 8);
+  p.T = sl.T.p;
+  p.thr = e->st_thr.p;
+  p.inv_s = static_cast<float>(1.0 / sl.in_s);
+  p.zf = static_cast<float>(sl.in_z);
+  p.lvl0 = static_cast<int>(quantize(0.0, e->st_in));
+  p.corr = static_cast<long long>(sl.n_in) * sl.out_z;
+  p.out_s = sl.out_s;
+  p.in_s = e->st_in.scale;
+  p.in_zd = static_cast<double>(e->st_in.zp);
+  p.in_qhi = e->st_in.qhi;
+  return p;
+}
+
+struct StAct {
+  const void* p = nullptr;
+  bool f32 = false;  // fp32 values (the model input) or u8 levels
+  int64_t ld = 0;    // dense rows: row pitch in elements (image tensors: dense NCHW)
+};
+
+// model_forward in spline-table mode (eval.hpp:200-253): u8 input levels flow
+// between layers in the reference's layouts (flat rows, NCHW images); the
+// model output leaves as fp32 values.
+void forward_st(kan_engine* e, const float* x, int64_t M, void* out, cudaStream_t st) {
+  const int nl = static_cast<int>(e->layers.size());
+  StAct in;
+  in.p = x;
+  in.f32 = true;
+  in.ld = e->input_size();
+  if (e->input_shape.size() == 3) {
+    bool image_use = false;
+    for (const auto& l : e->layers) image_use = image_use || (l.src < 0 && l.type != L_FLATTEN);
+    if (image_use) {  // conv / maxpool read u8 NCHW levels
+      const int64_t n = M * e->input_size();
+      e->st_xlev.alloc(static_cast<size_t>(n));
+      ck(launch_st_levels(x, n, e->st_thr.p, static_cast<float>(1.0 / e->st_in.scale),
+                          static_cast<float>(e->st_in.zp), static_cast<int>(e->st_in.qhi), e->st_xlev.p, 0, st),
+         "input levels");
+      e->last_launches += 1;
+      bool flat_use = false;
+      for (const auto& l : e->layers) flat_use = flat_use || (l.src < 0 && l.type == L_FLATTEN);
+      if (!flat_use) {
+        in.p = e->st_xlev.p;
+        in.f32 = false;
+      } else {
+        throw Unsupported("the model input cannot feed both a flatten and an image layer");
+      }
+    }
+  }
+  std::vector<StAct> acts(static_cast<size_t>(nl));
+  auto slot = [&](int i, size_t bytes) -> void* {
+    auto& b = e->slots[static_cast<size_t>(e->slot_of[static_cast<size_t>(i)])].main;
+    b.alloc(bytes);
+    return b.p;
+  };
+  for (int i = 0; i < nl; ++i) {
+    const Layer& l = e->layers[static_cast<size_t>(i)];
+    const StAct src = l.src < 0 ? in : acts[static_cast<size_t>(l.src)];
+    const bool last = i + 1 == nl;
+    StAct& dst = acts[static_cast<size_t>(i)];
+    if (l.type == L_FLATTEN) {  // NCHW is already the reference's flatten order
+      dst = src;
+      dst.ld = static_cast<int64_t>(l.in.c) * l.in.h * l.in.w;
+      continue;
+    }
+    if (l.type == L_MAXPOOL) {
+      if (src.f32) throw LogicError("maxpool reads u8 levels");
+      const int64_t planes = M * l.in.c;
+      uint8_t* o = static_cast<uint8_t*>(slot(i, static_cast<size_t>(planes) * l.out.h * l.out.w));
+      ck(launch_st_maxpool(static_cast<const uint8_t*>(src.p), planes, l.in.h, l.in.w, l.window, o, st),
+         "maxpool launch");
+      e->last_launches += 1;
+      dst.p = o;
+      dst.f32 = false;
+      continue;
+    }
+    const StLayer& sl = e->st[static_cast<size_t>(l.kan_index)];
+    StParams p = st_params(e, sl);
+    const bool conv = l.type == L_CONV;
+    if (conv) {
+      if (src.f32) throw LogicError("conv reads u8 levels");
+      p.conv = 1;
+      p.rows = M * l.out.h * l.out.w;
+      p.C = l.c_in;
+      p.H = l.in.h;
+      p.W = l.in.w;
+      p.K = l.kernel;
+      p.cstride = l.stride;
+      p.pad = l.padding;
+      p.Ho = l.out.h;
+      p.Wo = l.out.w;
+      p.in_kind = ST_IN_U8;
+    } else {
+      p.rows = M;
+      p.in_kind = src.f32 ? ST_IN_F32 : ST_IN_U8;
+      p.ld_x = src.ld;
+    }
+    p.x = src.p;
+    if (last) {
+      p.epi = EPI_F32;
+      p.out = out;
+      p.ld_out = sl.n_out;
+    } else {
+      p.epi = EPI_LEVEL;
+      p.ld_out = conv ? 0 : (sl.n_out + 15) / 16 * 16;
+      const size_t bytes = conv ? static_cast<size_t>(p.rows) * sl.n_out : static_cast<size_t>(M * p.ld_out);
+      p.out = slot(i, bytes);
+      dst.p = p.out;
+      dst.f32 = false;
+      dst.ld = conv ? 0 : p.ld_out;
+    }
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    unsigned ev_flags = cudaEventRecordDefault;
+    if (e->profiling) {
+      ck(cudaEventCreate(&ev0), "cudaEventCreate");
+      ck(cudaEventCreate(&ev1), "cudaEventCreate");
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      ck(cudaStreamIsCapturing(st, &cs), "cudaStreamIsCapturing");
+      ev_flags = cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault;
+      ck(cudaEventRecordWithFlags(ev0, st, ev_flags), "cudaEventRecord");
+    }
+    ck(launch_st_layer(p, st), "spline-table layer launch");
+    e->last_launches += 1;
+    if (e->profiling) {
+      ck(cudaEventRecordWithFlags(ev1, st, ev_flags), "cudaEventRecord");
+      e->pending.push_back({l.kan_index, ev0, ev1});
+    }
+  }
+}
+
 void configure(kan_engine* e, const kan_config* c) {
   if (!c) throw InvalidArgument("configure: null config");
   DeviceGuard dg(e->device);
   const kan_config cfg = *c;
-  if (cfg.mode != KAN_MODE_FP32 && cfg.mode != KAN_MODE_BF16 && cfg.mode != KAN_MODE_BSPLINE_LUT)
+  if (cfg.mode != KAN_MODE_FP32 && cfg.mode != KAN_MODE_BF16 && cfg.mode != KAN_MODE_BSPLINE_LUT &&
+      cfg.mode != KAN_MODE_SPLINE_TABLE)
     throw InvalidArgument("unknown evaluation mode");
   e->cfg = cfg;
   e->configured = false;
@@ -922,6 +1218,13 @@ void configure(kan_engine* e, const kan_config* c) {
   if (lastl.type == L_CONV && cfg.out_kind == KAN_OUT_I8)
     throw InvalidArgument("int8 outputs are produced by linear output layers only");
   plan_buffers(e);
+  if (cfg.mode == KAN_MODE_SPLINE_TABLE) {
+    e->prep.clear();
+    configure_st(e, cfg);
+    e->configured = true;
+    return;
+  }
+  e->st.clear();
   const Grid& g = e->grid;
   if (cfg.mode == KAN_MODE_BSPLINE_LUT) {
     e->lut = build_lut(g.P, cfg.lut_k, cfg.lut_h);  // validates P, k, h like the reference
@@ -1463,6 +1766,10 @@ void forward(kan_engine* e, const float* x, int64_t M, void* out, cudaStream_t s
   DeviceGuard dg(e->device);
   e->last_launches = 0;
   if (M == 0) return;
+  if (e->cfg.mode == KAN_MODE_SPLINE_TABLE) {
+    forward_st(e, x, M, out, st);
+    return;
+  }
   const bool lut = e->cfg.mode == KAN_MODE_BSPLINE_LUT;
   const bool fp32 = e->cfg.mode == KAN_MODE_FP32;
   const int esz = act_esz(e);
@@ -1862,12 +2169,20 @@ kan_status kan_engine_layer_levels(kan_engine* e, int layer, const float* x_dev,
                                    uint16_t* levels_dev, void* stream) {
   if (!e) return KAN_ERR_INVALID_ARGUMENT;
   return guarded(e, [&] {
-    if (!e->configured || e->cfg.mode != KAN_MODE_BSPLINE_LUT)
+    if (!e->configured || (e->cfg.mode != KAN_MODE_BSPLINE_LUT && e->cfg.mode != KAN_MODE_SPLINE_TABLE))
       throw LogicError("layer_levels: engine not configured for bspline-lut");
     (void)e->kan_layer(layer);  // one grid per model (Model::grid, layers.hpp:224-230)
     DeviceGuard dg(e->device);
     e->last_launches = 0;
     if (n == 0) return;
+    if (e->cfg.mode == KAN_MODE_SPLINE_TABLE) {
+      ck(launch_st_levels(x_dev, n, e->st_thr.p, static_cast<float>(1.0 / e->st_in.scale),
+                          static_cast<float>(e->st_in.zp), static_cast<int>(e->st_in.qhi), levels_dev, 1,
+                          static_cast<cudaStream_t>(stream)),
+         "levels launch");
+      e->last_launches = 1;
+      return;
+    }
     ck(launch_levels(x_dev, n, e->d_thr.p, static_cast<float>(e->grid.lo),
                      static_cast<float>(1.0 / e->lat.step), static_cast<int>(e->lat.L), levels_dev,
                      static_cast<cudaStream_t>(stream)),
@@ -1881,8 +2196,29 @@ kan_status kan_engine_layer_accumulators(kan_engine* e, int layer, const uint16_
                                          void* stream) {
   if (!e) return KAN_ERR_INVALID_ARGUMENT;
   return guarded(e, [&] {
-    if (!e->configured || e->cfg.mode != KAN_MODE_BSPLINE_LUT)
+    if (!e->configured || (e->cfg.mode != KAN_MODE_BSPLINE_LUT && e->cfg.mode != KAN_MODE_SPLINE_TABLE))
       throw LogicError("layer_accumulators: engine not configured for bspline-lut");
+    if (e->cfg.mode == KAN_MODE_SPLINE_TABLE) {  // any KAN layer, as dense (im2col'd) level rows
+      (void)e->kan_layer(layer);
+      DeviceGuard dg(e->device);
+      e->last_launches = 0;
+      if (batch == 0) return;
+      const StLayer& sl = e->st[static_cast<size_t>(layer)];
+      cudaStream_t st = static_cast<cudaStream_t>(stream);
+      e->st_probe.alloc(static_cast<size_t>(batch) * sl.n_in);
+      ck(launch_u16_to_u8(levels_dev, batch * sl.n_in, e->st_probe.p, st), "levels to u8");
+      StParams p = st_params(e, sl);
+      p.rows = batch;
+      p.in_kind = ST_IN_U8;
+      p.x = e->st_probe.p;
+      p.ld_x = sl.n_in;
+      p.epi = EPI_RAW;
+      p.out = acc_s_dev;
+      p.ld_out = sl.n_out;
+      ck(launch_st_layer(p, st), "spline-table layer launch");
+      e->last_launches = 2;
+      return;
+    }
     Layer& l = e->kan_layer(layer);
     if (l.type != L_LINEAR) throw Unsupported("layer_accumulators: linear layers only");
     DeviceGuard dg(e->device);
@@ -1911,6 +2247,69 @@ kan_status kan_engine_layer_accumulators(kan_engine* e, int layer, const uint16_
     else
       run_gemm_layer(e, pl, batch, io, static_cast<cudaStream_t>(stream));
   });
+}
+
+kan_status kan_engine_set_spline_tables(kan_engine* e, int layer, const uint8_t* values, int64_t n,
+                                        int bits_a, int h, const double* qp_d, const int64_t* qp_i) {
+  if (!e) return KAN_ERR_INVALID_ARGUMENT;
+  return guarded(e, [&] {
+    Layer& l = e->kan_layer(layer);
+    if (n == 0) {
+      l.st_values.clear();
+      l.st_bits_a = 0;
+      return;
+    }
+    if (bits_a < 1 || bits_a > 8) throw InvalidArgument("build_spline_tables: input bits must be in [1,8]");
+    if (h < 2 || h > 8) throw InvalidArgument("build_spline_tables: value bits must be in [2,8]");
+    if (!values || !qp_d || !qp_i) throw InvalidArgument("set_spline_tables: null buffer");
+    const int64_t n_in = l.type == L_LINEAR ? l.n_in : static_cast<int64_t>(l.kernel) * l.kernel * l.c_in;
+    const int64_t n_out = l.type == L_LINEAR ? l.n_out : l.c_out;
+    if (n != (n_in * n_out) << bits_a)
+      throw ShapeMismatch("set_spline_tables: expected " + std::to_string((n_in * n_out) << bits_a) +
+                          " entries, got " + std::to_string(n));
+    if (!(qp_d[1] > 0.0) || qp_i[3] != (int64_t{1} << h) - 1)
+      throw InvalidArgument("set_spline_tables: output quantizer does not match the value bits");
+    l.st_values.assign(values, values + n);
+    l.st_bits_a = bits_a;
+    l.st_h = h;
+    l.st_qd[0] = qp_d[0];
+    l.st_qd[1] = qp_d[1];
+    for (int t = 0; t < 4; ++t) l.st_qi[t] = qp_i[t];
+    e->configured = false;
+  });
+}
+
+int64_t kan_engine_spline_table(kan_engine* e, int layer, uint8_t* out, int64_t cap, double* qp_d,
+                                int64_t* qp_i) {
+  if (!e) return -KAN_ERR_INVALID_ARGUMENT;
+  int64_t count = 0;
+  const kan_status s = guarded(e, [&] {
+    if (!e->configured || e->cfg.mode != KAN_MODE_SPLINE_TABLE)
+      throw LogicError("spline_table: engine not configured for spline-table mode");
+    (void)e->kan_layer(layer);
+    const StLayer& sl = e->st[static_cast<size_t>(layer)];
+    const int64_t Lv = int64_t{1} << sl.bits_a;
+    count = static_cast<int64_t>(sl.n_in) * sl.n_out * Lv;
+    if (qp_d) {
+      qp_d[0] = sl.in_s;
+      qp_d[1] = sl.out_s;
+    }
+    if (qp_i) {
+      qp_i[0] = sl.in_z;
+      qp_i[1] = sl.in_qhi;
+      qp_i[2] = sl.out_z;
+      qp_i[3] = sl.out_qhi;
+    }
+    if (!out || cap < count) return;
+    DeviceGuard dg(e->device);
+    std::vector<uint8_t> t(static_cast<size_t>(sl.n_in) * Lv * sl.Np);
+    ck(cudaMemcpy(t.data(), sl.T.p, t.size(), cudaMemcpyDeviceToHost), "spline table D2H");
+    for (int i = 0; i < sl.n_in; ++i)
+      for (int j = 0; j < sl.n_out; ++j)
+        for (int64_t m = 0; m < Lv; ++m)
+          out[(static_cast<int64_t>(i) * sl.n_out + j) * Lv + m] = t[(static_cast<size_t>(i) * Lv + m) * sl.Np + j];
+  });
+  return s == KAN_OK ? count : -static_cast<int64_t>(s);
 }
 
 int64_t kan_engine_lut(const kan_engine* e, uint8_t* out, int64_t cap) {
@@ -1961,6 +2360,18 @@ int64_t kan_lut_build(int degree, int k, int h, uint8_t* out, int64_t cap) {
     const auto lut = build_lut(degree, k, h);
     const int64_t n = static_cast<int64_t>(lut.size());
     if (out && cap >= n) std::memcpy(out, lut.data(), static_cast<size_t>(n));
+    return n;
+  } catch (...) {
+    return -KAN_ERR_INVALID_ARGUMENT;
+  }
+}
+
+int64_t kan_spline_thresholds(double lo, double hi, int bits_a, float* out, int64_t cap) {
+  try {
+    if (bits_a < 1 || bits_a > 8) return -KAN_ERR_INVALID_ARGUMENT;
+    const auto thr = quant_thresholds(quant_params(lo, hi, bits_a));
+    const int64_t n = static_cast<int64_t>(thr.size());
+    if (out && cap >= n) std::memcpy(out, thr.data(), static_cast<size_t>(n) * sizeof(float));
     return n;
   } catch (...) {
     return -KAN_ERR_INVALID_ARGUMENT;

@@ -187,4 +187,48 @@ inline std::vector<float> level_thresholds(const Grid& g, const Lattice& lat) {
   return thr;
 }
 
+// Spline-table input levels (spline_table.hpp:98, quantize_value on the grid
+// bounds, no domain clamp): thr[n] = smallest fp32 x with level >= n for
+// n = 1..qhi, thr[0] = -inf; the same bisection over ordered fp32 patterns.
+// thr[qhi+1] = ovf, the smallest fp32 x with x/s + z >= 2^63: there (and at
+// NaN) the reference's llround overflows to LLONG_MIN, which clamps to level 0
+// on its x86-64 build, so the level is 0 for x >= ovf.
+inline std::vector<float> quant_thresholds(const QParams& q) {
+  auto key_to_float = [](int64_t key) {
+    uint32_t bits = key >= 0 ? static_cast<uint32_t>(key)
+                             : (static_cast<uint32_t>(-key) | 0x80000000u);
+    float f;
+    std::memcpy(&f, &bits, 4);
+    return f;
+  };
+  const int64_t kmin = -static_cast<int64_t>(0x7F800000u);
+  auto overflows = [&](float f) {
+    return !(static_cast<double>(f) / q.scale + static_cast<double>(q.zp) < 9223372036854775808.0);
+  };
+  int64_t ovf = 0, top = 0x7F800000;  // smallest key that overflows (+inf does)
+  while (ovf < top) {
+    const int64_t mid = ovf + (top - ovf) / 2;
+    if (overflows(key_to_float(mid)))
+      top = mid;
+    else
+      ovf = mid + 1;
+  }
+  const int64_t kmax = ovf - 1;  // quantize is monotone below the overflow
+  std::vector<float> thr(static_cast<size_t>(q.qhi) + 2);
+  thr[0] = -INFINITY;
+  thr[static_cast<size_t>(q.qhi) + 1] = key_to_float(ovf);
+  for (int64_t n = 1; n <= q.qhi; ++n) {
+    int64_t lo = kmin, hi = kmax;
+    while (lo < hi) {
+      const int64_t mid = lo + (hi - lo) / 2;
+      if (quantize(static_cast<double>(key_to_float(mid)), q) >= n)
+        hi = mid;
+      else
+        lo = mid + 1;
+    }
+    thr[static_cast<size_t>(n)] = key_to_float(lo);
+  }
+  return thr;
+}
+
 }  // namespace kan

@@ -151,4 +151,29 @@ struct Fp32Params {
   int G, P;
 };
 
+// Spline-table layer (spline_table.hpp:90-123): out = s_out * sum_i (T - z_out).
+enum StInKind : int { ST_IN_U8 = 0, ST_IN_F32 = 1 };
+struct StParams {
+  int64_t rows;  // dense: M; conv: n_img * Ho * Wo (rows ordered (img, oy, ox))
+  int n_in, n_out, Np, Lv;
+  int lpr, col_tiles, ic;  // lanes per row (16 columns each), column tiles, staged inputs per chunk
+  const uint8_t* T;        // [n_in][Lv][Np]
+  // input: dense rows [rows][ld_x] (u8 levels or fp32 values), or conv u8 NCHW
+  int in_kind;
+  const void* x;
+  int64_t ld_x;
+  const float* thr;  // fp32 input: thr[n] = smallest x with level >= n, n = 1..Lv-1
+  float inv_s, zf;
+  int conv, C, H, W, K, cstride, pad, Ho, Wo, lvl0;
+  // epilogue: EPI_F32 (row-major, or NCHW for conv), EPI_LEVEL (u8 levels of
+  // the consumer), EPI_RAW (int32 sums minus corr)
+  int epi;
+  void* out;
+  int64_t ld_out;
+  long long corr;  // n_in * z_out
+  double out_s;
+  double in_s, in_zd;  // the consumer's input quantizer (EPI_LEVEL; also the fp32 input's)
+  long long in_qhi;
+};
+
 }  // namespace kan

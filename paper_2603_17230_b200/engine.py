@@ -8,6 +8,8 @@ The reference (proj/include/kantize/) exposes
   tabulated_kan_forward(acts, layer, lut, bits_w)      lut.hpp:217-231
   kan_linear_forward(acts, layer)                      layers.hpp:118-121
   build_bspline_lut(P, k, h)                           lut.hpp:103-131
+  build_spline_tables(layer, bits_a, h)                spline_table.hpp:87-95
+  spline_table_forward(acts, tables)                   spline_table.hpp:90-107
   eval_mode_from_string("fp32" | "bspline-lut" ...)    eval.hpp:19-25
 
 This module keeps those names and argument meanings, but every forward runs in
@@ -44,7 +46,7 @@ STATUS_NAMES = {0: "OK", 1: "INVALID_ARGUMENT", 2: "SHAPE_MISMATCH", 3: "OUT_OF_
                 4: "CUDA", 5: "NCCL", 6: "IO", 7: "FORMAT", 8: "CHECKSUM", 9: "UNSUPPORTED",
                 10: "LOGIC"}
 
-MODE_FP32, MODE_BF16, MODE_BSPLINE_LUT = 0, 1, 2
+MODE_FP32, MODE_BF16, MODE_BSPLINE_LUT, MODE_SPLINE_TABLE = 0, 1, 2, 3
 W_PER_TENSOR_ASYM, W_PER_CHANNEL_SYM = 0, 1
 OUT_F32, OUT_I8 = 0, 1
 PASSTHROUGH_BITS = 32  # quant.hpp:15
@@ -87,11 +89,16 @@ _lib.kan_engine_layer_time_ms.argtypes = [_vp, C.c_int, C.POINTER(C.c_double),
                                           C.POINTER(C.c_int64)]
 _lib.kan_engine_layer_timeline.argtypes = [_vp, C.c_int, _vp, C.c_int64]
 _lib.kan_engine_layer_timeline.restype = C.c_int64
+_lib.kan_engine_set_spline_tables.argtypes = [_vp, C.c_int, _vp, C.c_int64, C.c_int, C.c_int, _vp, _vp]
+_lib.kan_engine_spline_table.argtypes = [_vp, C.c_int, _vp, C.c_int64, _vp, _vp]
+_lib.kan_engine_spline_table.restype = C.c_int64
 _lib.kan_lut_build.argtypes = [C.c_int, C.c_int, C.c_int, _vp, C.c_int64]
 _lib.kan_lut_build.restype = C.c_int64
 _lib.kan_lattice_thresholds.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, _vp,
                                         C.c_int64]
 _lib.kan_lattice_thresholds.restype = C.c_int64
+_lib.kan_spline_thresholds.argtypes = [C.c_double, C.c_double, C.c_int, _vp, C.c_int64]
+_lib.kan_spline_thresholds.restype = C.c_int64
 
 # exported symbols declared in include/kan_b200.h (checked by the CPU tests)
 EXPORTED = [
@@ -102,6 +109,7 @@ EXPORTED = [
     "kan_engine_layer_levels", "kan_engine_layer_accumulators", "kan_engine_lut",
     "kan_engine_last_launches", "kan_lut_build", "kan_lattice_thresholds",
     "kan_engine_set_profiling", "kan_engine_layer_time_ms", "kan_engine_layer_timeline",
+    "kan_engine_set_spline_tables", "kan_engine_spline_table", "kan_spline_thresholds",
 ]
 
 
@@ -115,9 +123,20 @@ def lattice_thresholds(G: int, P: int, k: int, lo: float = -1.0, hi: float = 1.0
     return out
 
 
+def spline_thresholds(bits_a: int, lo: float = -1.0, hi: float = 1.0) -> np.ndarray:
+    """The engine's exact fp32 spline-table input level thresholds (host utility)."""
+    n = _lib.kan_spline_thresholds(lo, hi, bits_a, None, 0)
+    if n < 0:
+        raise ValueError("spline_thresholds: bad arguments")
+    out = np.zeros(n, dtype=np.float32)
+    _lib.kan_spline_thresholds(lo, hi, bits_a, out.ctypes.data, n)
+    return out
+
+
 def eval_mode_from_string(s: str) -> int:
     """eval.hpp:19-25, plus the engine's bf16 datapath."""
-    table = {"fp32": MODE_FP32, "bf16": MODE_BF16, "bspline-lut": MODE_BSPLINE_LUT}
+    table = {"fp32": MODE_FP32, "bf16": MODE_BF16, "bspline-lut": MODE_BSPLINE_LUT,
+             "spline-table": MODE_SPLINE_TABLE}
     if s not in table:
         raise ValueError(f"unknown evaluation mode '{s}'")
     return table[s]
@@ -135,7 +154,10 @@ def build_bspline_lut(degree: int, k: int, h: int) -> np.ndarray:
 
 @dataclass
 class EvalOptions:
-    """EvalOptions (eval.hpp:37-45) extended with the engine's choices."""
+    """EvalOptions (eval.hpp:37-45) extended with the engine's choices.
+
+    spline-table mode reads lut_k as the tables' input bits (bits_a) and lut_h as
+    their value bits (h), as run_sweep passes (bits_a, bits_b) (sweep.hpp:247-253)."""
     mode: str = "fp32"
     lut_k: int = 8
     lut_h: int = 8
@@ -280,6 +302,36 @@ class Engine:
                                                        self._stream(stream)))
         return acc_s, acc_b
 
+    def set_spline_tables(self, layer: int, tables):
+        """Supply a layer's SplineTableSet (dict with values [n_in, n_out, 2^bits_a] u8,
+        bits_a, h, qp_d = (in_scale, out_scale), qp_i = (in_zp, in_qhi, out_zp,
+        out_qhi)) instead of building it from the coefficients; None clears."""
+        if tables is None:
+            self._check(_lib.kan_engine_set_spline_tables(self._h, layer, None, 0, 0, 0, None, None))
+            return
+        v = np.ascontiguousarray(tables["values"], dtype=np.uint8)
+        qd = np.ascontiguousarray(tables["qp_d"], dtype=np.float64)
+        qi = np.ascontiguousarray(tables["qp_i"], dtype=np.int64)
+        self._check(_lib.kan_engine_set_spline_tables(self._h, layer, v.ctypes.data, v.size,
+                                                      int(tables["bits_a"]), int(tables["h"]),
+                                                      qd.ctypes.data, qi.ctypes.data))
+
+    def spline_table(self, layer: int):
+        """The configured SplineTableSet of one KAN layer (reference layout)."""
+        qd = np.zeros(2)
+        qi = np.zeros(4, dtype=np.int64)
+        n = _lib.kan_engine_spline_table(self._h, layer, None, 0, qd.ctypes.data, qi.ctypes.data)
+        if n < 0:
+            self._check(int(-n))
+        n_in, n_out = self.layer_shape(layer)
+        out = np.zeros(n, dtype=np.uint8)
+        n2 = _lib.kan_engine_spline_table(self._h, layer, out.ctypes.data, n, None, None)
+        if n2 < 0:
+            self._check(int(-n2))
+        bits_a = int(n // (n_in * n_out)).bit_length() - 1 if n_in * n_out else 0
+        return {"values": out.reshape(n_in, n_out, -1), "qp_d": qd, "qp_i": qi, "bits_a": bits_a,
+                "h": int(qi[3] + 1).bit_length() - 1, "n_in": n_in, "n_out": n_out}
+
     def lut(self) -> np.ndarray:
         n = _lib.kan_engine_lut(self._h, None, 0)
         out = np.zeros(n, dtype=np.uint8)
@@ -334,4 +386,25 @@ def kan_linear_forward(acts, coeffs, G: int, P: int, mode: str = "fp32", lo=-1.0
     e = Engine(_linear_descriptor(n_in, n_out, G, P, lo, hi), device)
     e.set_coeffs(0, coeffs)
     e.configure(EvalOptions(mode=mode))
+    return e.model_forward(acts)
+
+
+def build_spline_tables(coeffs, n_in: int, n_out: int, G: int, P: int, bits_a: int, h: int,
+                        lo=-1.0, hi=1.0, device=0):
+    """build_spline_tables (spline_table.hpp:87-95) for a linear layer, built on the GPU."""
+    e = Engine(_linear_descriptor(n_in, n_out, G, P, lo, hi), device)
+    e.set_coeffs(0, coeffs)
+    e.configure(EvalOptions(mode="spline-table", lut_k=bits_a, lut_h=h))
+    return e.spline_table(0)
+
+
+def spline_table_forward(acts, tables, G: int = 5, P: int = 3, lo=-1.0, hi=1.0, device=0):
+    """spline_table_forward (spline_table.hpp:90-107) over a SplineTableSet dict, on the GPU."""
+    n_in, n_out = tables["n_in"], tables["n_out"]
+    if acts.shape[1] != n_in:
+        raise ValueError(f"spline_table_forward: shape mismatch: got {acts.shape[1]} inputs, "
+                         f"tables expect {n_in}")
+    e = Engine(_linear_descriptor(n_in, n_out, G, P, lo, hi), device)
+    e.set_spline_tables(0, tables)
+    e.configure(EvalOptions(mode="spline-table", lut_k=tables["bits_a"], lut_h=tables["h"]))
     return e.model_forward(acts)
