@@ -203,6 +203,21 @@ def cpu_baseline(wl, seconds: float):
     cores = os.cpu_count() or 1
     rows = cpu_rows(wl, cores)
     x = wl.inputs(rows, seed=99).astype(np.float64)
+    if Ref.available and wl.mode == "spline-table":
+        if not wl.reference_expressible:
+            raise RuntimeError("spline-table CPU baseline needs a reference-expressible model")
+        ref = Ref()
+        text = json.dumps(wl.descriptor())
+        n, dt = 0, 0.0
+        while dt < seconds:
+            _, sec = ref.st_model_forward(text, Ws, x, wl.out_size, wl.lut_k, wl.lut_h,
+                                          threads=cores, chunk=256)
+            n += rows
+            dt += sec
+        return {"value": n / dt, "unit": "samples/s", "cores": cores, "kind": "reference",
+                "sample": f"{n} samples ({rows}-row calls) of {wl.key} through the reference "
+                          f"model_forward in spline-table mode (bits_a={wl.lut_k}, h={wl.lut_h}, "
+                          f"tables built once, untimed), {cores} threads, {dt:.1f} s"}
     if Ref.available:
         ref = Ref()
         n = 0
@@ -253,29 +268,43 @@ def run_reference(args):
         return
     ref = Ref()
 
+    st_mode = wl.mode == "spline-table"
+    if st_mode:  # tables built once per call outside the timed forwards
+        if not wl.reference_expressible:
+            print(json.dumps({"impl": "reference", "unavailable": "the reference's model_forward "
+                              "cannot run this model in spline-table mode"}))
+            return
+        text = json.dumps(wl.descriptor())
+
     def step():
+        if st_mode:
+            return ref.st_model_forward(text, Ws, x, wl.out_size, wl.lut_k, wl.lut_h,
+                                        threads=cores, chunk=256)[1]
+        t = time.perf_counter()
         ref_forward(ref, wl, Ws, x, cores)
-    t0 = time.perf_counter()
-    step()  # first warm-up step also sizes the run (whole run within ~2 minutes)
-    t_step = time.perf_counter() - t0
+        return time.perf_counter() - t
+    t_step = step()  # first warm-up step also sizes the run (whole run within ~2 minutes)
     steps = max(1, min(args.steps, 50, int(120.0 / max(t_step, 1e-3))))
     for _ in range(min(args.warmup, 3) - 1):
         step()
-    t0 = time.perf_counter()
+    dt = 0.0
     for _ in range(steps):
-        step()
-    dt = time.perf_counter() - t0
+        dt += step()
     v = rows * steps / dt
     print(json.dumps({
-        "impl": "reference", "metric": "KAN samples/sec (int8-LUT path)", "value": v,
+        "impl": "reference",
+        "metric": "KAN samples/sec (spline-table path)" if st_mode else "KAN samples/sec (int8-LUT path)",
+        "value": v,
         "unit": "samples/s", "n_gpus": args.gpus, "steps": steps, "warmup": min(args.warmup, 3),
         "ms_per_step": dt / steps * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": wl.key + ": " + wl.title, "batch_per_step": rows,
                    "note": "reference CPU path: " + (
-                       "model_forward" if wl.reference_expressible else
-                       "composition of convkan_forward / kan_linear_forward (ref_graph_forward)")
-                   + f" bspline-lut k{wl.lut_k} h{wl.lut_h}, per-tensor u8 W, no SiLU"},
+                       f"model_forward in spline-table mode, bits_a={wl.lut_k} h={wl.lut_h}, "
+                       "tables built once outside the timed forwards" if st_mode else (
+                           ("model_forward" if wl.reference_expressible else
+                            "composition of convkan_forward / kan_linear_forward (ref_graph_forward)")
+                           + f" bspline-lut k{wl.lut_k} h{wl.lut_h}, per-tensor u8 W, no SiLU"))},
         "cpu_baseline": {"value": v, "unit": "samples/s", "cores": cores, "kind": "reference",
                          "sample": f"{steps} steps x {rows} rows, {cores} threads"},
         "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -398,6 +427,7 @@ def main():
         layer_ms.append(tot / max(cnt, 1))
     eng.set_profiling(False)
     lut = wl.mode == "bspline-lut"
+    st_mode = wl.mode == "spline-table"
     peaks, peak_src = measured_peaks()
     # bound of the dominant (largest-time) layer
     dom = int(np.argmax(layer_ms))
@@ -424,7 +454,7 @@ def main():
     ai = ops_l / bytes_l
     tensor_peak = int8_peak_tops * 1e12 if lut else peaks.get("bf16_tflops", 1677.7) * 1e12
     hbm_peak = peaks["hbm_gbs"] * 1e9
-    if ai < tensor_peak / hbm_peak:
+    if st_mode or ai < tensor_peak / hbm_peak:  # spline tables: gather + integer add, no tensor work
         roof = {"bound": "hbm", "achieved": bytes_l / t_l / 1e9, "peak": peaks["hbm_gbs"],
                 "unit": "GB/s"}
     else:
@@ -433,7 +463,8 @@ def main():
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["traffic"] = committed_traffic(wl.key)
     kl = wl.kan_layers()[dom]
-    roof["kernel"] = (f"kan_gather_gemm KAN layer {dom} ({kl['n_in']}->{kl['n_out']}"
+    roof["kernel"] = (("kan_st_layer" if st_mode else "kan_gather_gemm")
+                      + f" KAN layer {dom} ({kl['n_in']}->{kl['n_out']}"
                       + (f", {kl['pix']} px/sample)" if kl["pix"] > 1 else ")"))
     if launches_per_step == 1 and wl.n_kan > 1:
         roof["kernel"] += f" with the {wl.n_kan - 1} following layer(s) fused in"
@@ -478,10 +509,12 @@ def main():
         paper = PAPER_SAMPLES_PER_S.get(wl.key)
         line = {
             "metric": "KAN samples/sec (int8-LUT path)" if lut else f"KAN samples/sec ({wl.mode} path)",
+            # spline-table lines: roofline.per_launch.algorithmic_ops counts table
+            # lookups + integer adds (one per connection), not multiply-adds
             "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": (value / paper) if paper else None,
-            "dtype": "u8" if lut else wl.mode, "data": "synthetic",
+            "dtype": "u8" if (lut or st_mode) else wl.mode, "data": "synthetic",
             "config": {"workload": wl.key + ": " + wl.title, "batch_per_gpu": B,
                        "global_batch": B * world, "parallelism": f"dp{world}",
                        "l2": f"inputs rotate over {R} resident batches "

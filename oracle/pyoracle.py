@@ -537,6 +537,9 @@ class Ref:
         L.ref_spline_tables.restype = C.c_int64
         L.ref_spline_table_forward.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _u8p, _dp, _i64p,
                                                C.c_int64, _dp, _dp]
+        L.ref_st_model_forward.argtypes = [C.c_char_p, C.POINTER(C.c_void_p), C.c_int, C.c_int,
+                                           C.c_int64, C.c_int64, _dp, C.c_int64, _dp, C.c_int,
+                                           C.c_int64, C.c_int, C.POINTER(C.c_double)]
         L.ref_model_forward.argtypes = [C.c_char_p, C.POINTER(C.c_void_p), C.c_int, C.c_int,
                                         C.c_int, C.c_int, C.c_int64, C.c_int64, _dp, C.c_int64,
                                         _dp, C.c_int, C.c_int64]
@@ -671,6 +674,21 @@ class Ref:
                                              t["qp_i"], acts.shape[0], acts, out):
             raise ValueError(self.err())
         return out
+
+    def st_model_forward(self, text, coeffs, inputs, n_out, bits_a, h, threads=1, chunk=256,
+                         reps=1):
+        """model_forward in spline-table mode with the tables built once; returns
+        (logits, seconds of the `reps` forwards alone)."""
+        inputs = np.ascontiguousarray(inputs, dtype=np.float64)
+        cs = [np.ascontiguousarray(c, dtype=np.float64) for c in coeffs]
+        ptrs = (C.c_void_p * len(cs))(*[c.ctypes.data for c in cs])
+        out = np.zeros((inputs.shape[0], n_out))
+        sec = C.c_double()
+        if self.lib.ref_st_model_forward(text.encode(), ptrs, bits_a, h, inputs.shape[0],
+                                         inputs.shape[1], inputs, n_out, out, threads, chunk, reps,
+                                         C.byref(sec)):
+            raise ValueError(self.err())
+        return out, sec.value
 
     def validate_descriptor(self, text: str) -> int:
         n = self.lib.ref_validate_descriptor(text.encode())

@@ -22,6 +22,7 @@
 #include <kantize/spline_table.hpp>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -337,6 +338,66 @@ int ref_model_forward(const char* json_text, const double* const* coeff_ptrs, in
     });
   }
   for (auto& th : pool) th.join();
+  for (auto& e : errs)
+    if (!e.empty()) {
+      g_err = e;
+      return -1;
+    }
+  return 0;
+} catch (const std::exception& e) {
+  return fail(e);
+}
+
+// spline-table model_forward with the tables built ONCE up front (as run_sweep
+// does, sweep.hpp:239-256, and as a caller passing EvalOptions::tables does);
+// the batch runs `reps` times sharded over `threads` std::threads in `chunk`
+// rows; *seconds = wall time of the forwards alone (the CPU baseline of the
+// spline-table bench lines).
+int ref_st_model_forward(const char* json_text, const double* const* coeff_ptrs, int bits_a, int h,
+                         int64_t M, int64_t D, const double* inputs, int64_t n_out, double* out,
+                         int threads, int64_t chunk, int reps, double* seconds) try {
+  Model model = model_from_descriptor(nlohmann::json::parse(json_text));
+  int li = 0;
+  std::vector<SplineTableSet> tables;
+  for (auto& layer : model.layers) {
+    if (auto* lin = std::get_if<KanLinearLayer>(&layer)) {
+      std::copy(coeff_ptrs[li], coeff_ptrs[li] + lin->coeffs.size(), lin->coeffs.flat().begin());
+      tables.push_back(build_spline_tables(*lin, bits_a, h));
+      ++li;
+    } else if (auto* conv = std::get_if<ConvKanLayer>(&layer)) {
+      std::copy(coeff_ptrs[li], coeff_ptrs[li] + conv->coeffs.size(), conv->coeffs.flat().begin());
+      tables.push_back(build_spline_tables(*conv, bits_a, h));
+      ++li;
+    }
+  }
+  EvalOptions opts;
+  opts.mode = EvalMode::kSplineTable;
+  opts.tables = &tables;
+  if (threads < 1) threads = 1;
+  if (chunk < 1) chunk = 256;
+  if (reps < 1) reps = 1;
+  std::vector<std::string> errs(static_cast<std::size_t>(threads));
+  const int64_t per = (M + threads - 1) / threads;
+  const auto t0 = std::chrono::steady_clock::now();
+  for (int r = 0; r < reps; ++r) {
+    std::vector<std::thread> pool;
+    for (int t = 0; t < threads; ++t) {
+      pool.emplace_back([&, t] {
+        try {
+          const int64_t r0 = t * per, r1 = std::min(M, r0 + per);
+          for (int64_t s = r0; s < r1; s += chunk) {
+            const int64_t rows = std::min(chunk, r1 - s);
+            const Matrix logits = model_forward(model, make_matrix(rows, D, inputs + s * D), opts);
+            std::copy(logits.flat().begin(), logits.flat().end(), out + s * n_out);
+          }
+        } catch (const std::exception& e) {
+          errs[static_cast<std::size_t>(t)] = e.what();
+        }
+      });
+    }
+    for (auto& th : pool) th.join();
+  }
+  *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   for (auto& e : errs)
     if (!e.empty()) {
       g_err = e;

@@ -174,6 +174,8 @@ class Workload:
     def weight_bytes(self, layer: int) -> int:
         kl = self.kan_layers()[layer]
         a, b = kl["n_in"], kl["n_out"]
+        if self.mode == "spline-table":  # u8 tables [n_in][2^bits_a][n_out]
+            return a * b << self.lut_k
         nb = self.G + self.P
         esz = 2 if self.mode == "bf16" else (4 if self.mode == "fp32" else 1)
         return a * nb * b * esz + (a * b * esz if self.silu else 0)
@@ -183,15 +185,18 @@ class Workload:
         weights once.  Inputs are fp32 for layer 0; hidden activations are u16
         lattice levels on the LUT path and fp32 on the float paths."""
         lut = self.mode == "bspline-lut"
+        st = self.mode == "spline-table"  # hidden tensors are u8 input levels
         kls = self.kan_layers()
         kl = kls[layer]
-        in_b = 4 if layer == 0 else (2 if lut else 4)
+        in_b = 4 if layer == 0 else (1 if st else (2 if lut else 4))
         last = layer == len(kls) - 1
-        out_b = (1 if self.int8_out else 4) if last else (2 if lut else 4)
+        out_b = (1 if self.int8_out else 4) if last else (1 if st else (2 if lut else 4))
         return batch * (kl["in_elems"] * in_b + kl["out_elems"] * out_b) + self.weight_bytes(layer)
 
     def layer_ops_per_launch(self, layer: int, batch: int) -> int:
         kl = self.kan_layers()[layer]
+        if self.mode == "spline-table":  # one table lookup + one integer add per connection
+            return batch * kl["pix"] * kl["n_in"] * kl["n_out"]
         return 2 * batch * kl["pix"] * kl["n_in"] * (self.G + self.P) * kl["n_out"]
 
 
@@ -219,6 +224,22 @@ WORKLOADS = {
                          "LUT k8/h3 (3-bit table) + int8 W",
                    [3 * 32 * 32], 5, 3, 8192, 0.05, lut_h=3, input_shape=[3, 32, 32],
                    layers=reskan18_layers(), extra={"descriptor": {"conv_output": "floor"}}),
+    # spline-table mode (spline_table.hpp) on the C1/C2/C4
+    # shapes, 256-entry 8-bit tables (bits_a = 8, h = 8), no SiLU term (the
+    # reference's tables replace the whole activation phi_{i,j})
+    "c1st": Workload("c1st", "KAN MLP [784,64,10] G=5 P=3 batch 1024, spline tables bits_a=8 h=8",
+                     [784, 64, 10], 5, 3, 1024, 0.1, mode="spline-table", silu=False),
+    "c2st": Workload("c2st", "KAN MLP [784,64,10] G=5 P=3 batch 4096, spline tables bits_a=8 h=8",
+                     [784, 64, 10], 5, 3, 4096, 0.1, mode="spline-table", silu=False),
+    "c2st4": Workload("c2st4", "KAN MLP [784,64,10] G=5 P=3 batch 4096, spline tables bits_a=4 h=4",
+                      [784, 64, 10], 5, 3, 4096, 0.1, mode="spline-table", lut_k=4, lut_h=4,
+                      silu=False),
+    "c4st": Workload("c4st", "KAN conv 3x3 s1 p1 64->64 on 32x32, G=5 P=3 batch 256, spline tables "
+                             "bits_a=8 h=8 (implicit im2col)",
+                     [64 * 32 * 32], 5, 3, 256, 0.05, mode="spline-table", silu=False,
+                     input_shape=[64, 32, 32],
+                     layers=[{"type": "conv", "c_in": 64, "c_out": 64, "kernel": 3, "stride": 1,
+                              "padding": 1}]),
 }
 
 

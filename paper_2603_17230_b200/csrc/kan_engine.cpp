@@ -159,7 +159,8 @@ struct Layer {
 
 // Device state of one spline-table layer (SplineTableSet, spline_table.hpp:19-34)
 struct StLayer {
-  DevBuf<uint8_t> T;  // [n_in][Lv][Np]
+  DevBuf<uint8_t> T;  // [roundup4(n_in)][Lv][Np]
+  DevBuf<int> vthr;   // next-layer level thresholds on the integer sums (StParams::vthr)
   int n_in = 0, n_out = 0, Np = 0, lpr = 1, col_tiles = 1;
   int bits_a = 0, h = 0;
   double in_s = 1.0, out_s = 1.0;
@@ -993,7 +994,7 @@ static void st_build_layer(kan_engine* e, const Layer& l, StLayer& sl, int bits_
   sl.out_s = oq.scale;
   sl.out_z = oq.zp;
   sl.out_qhi = oq.qhi;
-  sl.T.alloc(static_cast<size_t>(sl.n_in) * static_cast<size_t>(Lv) * sl.Np, true);
+  sl.T.alloc(static_cast<size_t>((sl.n_in + 3) / 4 * 4) * static_cast<size_t>(Lv) * sl.Np, true);
   ck(launch_st_sample(d_basis.p, d_coeffs.p, sl.n_in, sl.n_out, nb, static_cast<int>(Lv), 1, mm.p, sl.T.p,
                       sl.Np, oq.scale, static_cast<double>(oq.zp), oq.qhi, nullptr),
      "spline table quantization");
@@ -1004,7 +1005,7 @@ static void st_build_layer(kan_engine* e, const Layer& l, StLayer& sl, int bits_
 // gather layout [n_in][2^bits_a][Np]
 static void st_import_layer(const Layer& l, StLayer& sl) {
   const int64_t Lv = int64_t{1} << l.st_bits_a;
-  std::vector<uint8_t> t(static_cast<size_t>(sl.n_in) * static_cast<size_t>(Lv) * sl.Np, 0);
+  std::vector<uint8_t> t(static_cast<size_t>((sl.n_in + 3) / 4 * 4) * static_cast<size_t>(Lv) * sl.Np, 0);
   for (int i = 0; i < sl.n_in; ++i)
     for (int j = 0; j < sl.n_out; ++j)
       for (int64_t m = 0; m < Lv; ++m)
@@ -1014,6 +1015,33 @@ static void st_import_layer(const Layer& l, StLayer& sl) {
   sl.out_s = l.st_qd[1];
   sl.out_z = l.st_qi[2];
   sl.out_qhi = l.st_qi[3];
+}
+
+// vthr[n] = smallest integer sum v whose output s_out * v quantizes to an input
+// level >= n under the consumer's quantizer (quantize_value is monotone in v);
+// INT_MAX when no attainable sum reaches n.
+static void st_sum_thresholds(const kan_engine* e, StLayer& sl) {
+  const int64_t vmin = -static_cast<int64_t>(sl.n_in) * sl.out_z;
+  const int64_t vmax = static_cast<int64_t>(sl.n_in) * (sl.out_qhi - sl.out_z);
+  auto level = [&](int64_t v) { return quantize(sl.out_s * static_cast<double>(v), e->st_in); };
+  std::vector<int> vt(static_cast<size_t>(e->st_in.qhi) + 1);
+  vt[0] = std::numeric_limits<int>::min();
+  for (int64_t n = 1; n <= e->st_in.qhi; ++n) {
+    if (level(vmax) < n) {
+      vt[static_cast<size_t>(n)] = std::numeric_limits<int>::max();
+      continue;
+    }
+    int64_t lo = vmin, hi = vmax;
+    while (lo < hi) {
+      const int64_t mid = lo + (hi - lo) / 2;
+      if (level(mid) >= n)
+        hi = mid;
+      else
+        lo = mid + 1;
+    }
+    vt[static_cast<size_t>(n)] = static_cast<int>(lo);
+  }
+  sl.vthr.upload(vt);
 }
 
 void configure_st(kan_engine* e, const kan_config& cfg) {
@@ -1053,10 +1081,14 @@ void configure_st(kan_engine* e, const kan_config& cfg) {
         throw InvalidArgument("coefficients of KAN layer " + std::to_string(l.kan_index) + " not set");
       st_build_layer(e, l, sl, bits_a, h);
     }
+    st_sum_thresholds(e, sl);
   }
 }
 
-static StParams st_params(const kan_engine* e, const StLayer& sl) {
+// Launch geometry of one spline-table launch over `rows` rows: input slices
+// per row until the grid has ~3 CTAs per SM (or a slice would own fewer than
+// one 4-input quad / channel), then the staged-level chunk that fits 32 KB.
+static StParams st_params(const kan_engine* e, const StLayer& sl, int64_t rows = 0, int conv_c = 0) {
   StParams p{};
   p.n_in = sl.n_in;
   p.n_out = sl.n_out;
@@ -1064,8 +1096,13 @@ static StParams st_params(const kan_engine* e, const StLayer& sl) {
   p.Lv = 1 << sl.bits_a;
   p.lpr = sl.lpr;
   p.col_tiles = sl.col_tiles;
-  const int RP = 256 / sl.lpr;
-  int ic = std::min(256, (49152 / RP - 4) / 8 * 8);
+  const int units = conv_c > 0 ? conv_c : (sl.n_in + 3) / 4;  // what slices split
+  int S = 1;
+  auto blocks = [&](int s_) { return (rows + 256 / (sl.lpr * s_) - 1) / (256 / (sl.lpr * s_)) * sl.col_tiles; };
+  while (S * sl.lpr < 256 && 2 * S <= units && blocks(S) < 148 * 3) S *= 2;
+  p.slices = S;
+  const int RP = 256 / (sl.lpr * S);
+  int ic = (32768 / RP - 8) / 8 * 8;
   ic = std::min(ic, (sl.n_in + 7) / 8 * 8);
   p.ic = std::max(ic, 8);
   p.T = sl.T.p;
@@ -1078,6 +1115,8 @@ static StParams st_params(const kan_engine* e, const StLayer& sl) {
   p.in_s = e->st_in.scale;
   p.in_zd = static_cast<double>(e->st_in.zp);
   p.in_qhi = e->st_in.qhi;
+  p.vthr = sl.vthr.p;
+  p.ratio_f = static_cast<float>(sl.out_s / e->st_in.scale);
   return p;
 }
 
@@ -1144,8 +1183,30 @@ void forward_st(kan_engine* e, const float* x, int64_t M, void* out, cudaStream_
       continue;
     }
     const StLayer& sl = e->st[static_cast<size_t>(l.kan_index)];
-    StParams p = st_params(e, sl);
     const bool conv = l.type == L_CONV;
+    StParams p = st_params(e, sl, conv ? M * l.out.h * l.out.w : M, conv ? l.c_in : 0);
+    // a small last layer reading only this dense layer's levels runs fused:
+    // one warp per row, the hidden levels never leave shared memory
+    bool fused = false;
+    if (!conv && i + 2 == nl && sl.col_tiles == 1 && sl.n_out <= 512) {
+      const Layer& nx = e->layers[static_cast<size_t>(i + 1)];
+      if (nx.type == L_LINEAR && nx.src == i) {
+        const StLayer& sn = e->st[static_cast<size_t>(nx.kan_index)];
+        if (sn.n_out <= 16) {
+          fused = true;
+          p.slices = std::max(p.slices, 32 / sl.lpr);  // at least one warp per row
+          p.f_on = 1;
+          p.f_n_in = sn.n_in;
+          p.f_n_out = sn.n_out;
+          p.f_Lv = 1 << sn.bits_a;
+          p.f_T = sn.T.p;
+          p.f_corr = static_cast<long long>(sn.n_in) * sn.out_z;
+          p.f_out_s = sn.out_s;
+          p.f_out = static_cast<float*>(out);
+          p.f_ld_out = sn.n_out;
+        }
+      }
+    }
     if (conv) {
       if (src.f32) throw LogicError("conv reads u8 levels");
       p.conv = 1;
@@ -1194,6 +1255,7 @@ void forward_st(kan_engine* e, const float* x, int64_t M, void* out, cudaStream_
       ck(cudaEventRecordWithFlags(ev1, st, ev_flags), "cudaEventRecord");
       e->pending.push_back({l.kan_index, ev0, ev1});
     }
+    if (fused) break;  // the output layer ran inside this launch
   }
 }
 
@@ -2207,7 +2269,7 @@ kan_status kan_engine_layer_accumulators(kan_engine* e, int layer, const uint16_
       cudaStream_t st = static_cast<cudaStream_t>(stream);
       e->st_probe.alloc(static_cast<size_t>(batch) * sl.n_in);
       ck(launch_u16_to_u8(levels_dev, batch * sl.n_in, e->st_probe.p, st), "levels to u8");
-      StParams p = st_params(e, sl);
+      StParams p = st_params(e, sl, batch);
       p.rows = batch;
       p.in_kind = ST_IN_U8;
       p.x = e->st_probe.p;

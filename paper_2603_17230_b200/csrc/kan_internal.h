@@ -157,7 +157,8 @@ struct StParams {
   int64_t rows;  // dense: M; conv: n_img * Ho * Wo (rows ordered (img, oy, ox))
   int n_in, n_out, Np, Lv;
   int lpr, col_tiles, ic;  // lanes per row (16 columns each), column tiles, staged inputs per chunk
-  const uint8_t* T;        // [n_in][Lv][Np]
+  int slices;              // input slices per row (partial sums meet in smem)
+  const uint8_t* T;        // [roundup4(n_in)][Lv][Np]; padded inputs are all-zero slices
   // input: dense rows [rows][ld_x] (u8 levels or fp32 values), or conv u8 NCHW
   int in_kind;
   const void* x;
@@ -174,6 +175,19 @@ struct StParams {
   double out_s;
   double in_s, in_zd;  // the consumer's input quantizer (EPI_LEVEL; also the fp32 input's)
   long long in_qhi;
+  // EPI_LEVEL: vthr[n] = smallest sum v (minus corr) whose output s_out * v has
+  // level >= n (n = 1..in_qhi), ratio_f = s_out / in_s for the fp32 estimate
+  const int* vthr;
+  float ratio_f;
+  // fused output layer (dense rows, one warp per row): the hidden levels of
+  // each row stay in smem and the next, last layer (n_out <= 16, tables
+  // [n_in][Lv][16]) runs in the same warp; f_out gets its fp32 outputs
+  int f_on, f_n_in, f_n_out, f_Lv;
+  const uint8_t* f_T;
+  long long f_corr;
+  double f_out_s;
+  float* f_out;
+  int64_t f_ld_out;
 };
 
 }  // namespace kan

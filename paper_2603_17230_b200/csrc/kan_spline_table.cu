@@ -145,8 +145,46 @@ struct Acc16 {
   }
 };
 
-__device__ __forceinline__ uint4 ldg_row(const uint8_t* p) {
-  return __ldg(reinterpret_cast<const uint4*>(p));
+// L2 eviction-priority policies: the tables are re-read by every row and
+// should stay L2-resident while the activation stream passes through
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+// one 16-byte table row slice; L1 is bypassed (rows are rarely re-hit there)
+__device__ __forceinline__ uint4 ldg_row(const uint8_t* p, uint64_t pol) {
+  uint4 v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+      : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+      : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ float4 ldg_stream_f4(const float4* p, uint64_t pol) {
+  float4 v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+      : "l"(p), "l"(pol));
+  return v;
+}
+
+// Next-layer level of an integer sum v (v = sum - corr): quantize_value of
+// s_out * v is monotone in v, so the host's exact integer thresholds
+// vthr[n] = smallest v with level >= n settle an fp32 estimate (no fp64 divide).
+__device__ __forceinline__ uint8_t st_level_of_sum(const StParams& p, int v) {
+  int n = __float2int_rn(fmaf(static_cast<float>(v), p.ratio_f, p.zf));
+  n = n < 0 ? 0 : (n > p.in_qhi ? static_cast<int>(p.in_qhi) : n);
+  if (n > 0 && v < __ldg(p.vthr + n))
+    --n;
+  else if (n < p.in_qhi && v >= __ldg(p.vthr + n + 1))
+    ++n;
+  return static_cast<uint8_t>(n);
 }
 
 // Epilogue of one row's 16 columns.
@@ -163,11 +201,10 @@ __device__ __forceinline__ void st_epilogue(const StParams& p, int64_t r, int c0
       if (p.epi == EPI_RAW) {
         static_cast<int*>(p.out)[o] = static_cast<int>(v);
       } else {
-        const double y = __dmul_rn(p.out_s, static_cast<double>(v));
         if (p.epi == EPI_LEVEL)
-          static_cast<uint8_t*>(p.out)[o] = st_level_f64(y, p.in_s, p.in_zd, p.in_qhi);
+          static_cast<uint8_t*>(p.out)[o] = st_level_of_sum(p, static_cast<int>(v));
         else
-          static_cast<float*>(p.out)[o] = static_cast<float>(y);
+          static_cast<float*>(p.out)[o] = static_cast<float>(__dmul_rn(p.out_s, static_cast<double>(v)));
       }
     }
     return;
@@ -177,8 +214,7 @@ __device__ __forceinline__ void st_epilogue(const StParams& p, int64_t r, int c0
     uint8_t q[16];
 #pragma unroll
     for (int t = 0; t < 16; ++t) {
-      const long long v = static_cast<long long>(a[t]) - p.corr;
-      q[t] = st_level_f64(__dmul_rn(p.out_s, static_cast<double>(v)), p.in_s, p.in_zd, p.in_qhi);
+      q[t] = st_level_of_sum(p, static_cast<int>(static_cast<long long>(a[t]) - p.corr));
     }
     uint8_t* dst = static_cast<uint8_t*>(p.out) + o;
     if (c0 + 16 <= p.n_out && (p.ld_out & 15) == 0) {
@@ -216,26 +252,93 @@ __device__ __forceinline__ void st_epilogue(const StParams& p, int64_t r, int c0
   }
 }
 
-// One spline-table layer.  A CTA of 256 threads runs RP = 256 / lpr rows at a
-// time, lpr lanes per row, each lane 16 columns of column tile blockIdx.y.
-// Dense rows stage their input levels (u8 rows, or fp32 rows quantized on the
-// way in) in shared memory, IC inputs at a time; conv rows read the u8 NCHW
-// input levels directly (implicit im2col, padded taps = level of 0.0).
-__global__ void __launch_bounds__(256) kan_st_layer_kernel(const StParams p) {
+// One spline-table layer.  A CTA of 256 threads runs RP rows at a time; each
+// row is split over S input slices x lpr lanes (16 columns each, column tile
+// blockIdx.y), so even a few thousand rows fill the GPU with independent
+// gathers.  Dense rows: slice s owns the 4-input quads q = s mod S; its lanes
+// read the quad's levels straight from the input row (one u32 of u8 levels, or
+// one float4 of fp32 values whose levels the group's lanes split and exchange
+// by shuffles) and issue eight 16-byte gathers per step (two quads).  Conv
+// rows read the u8 NCHW input levels directly (implicit im2col, padded taps =
+// level of 0.0); slice s owns channels c = s mod S.  The S partial sums of a
+// row meet by warp shuffles when the row's lpr*S threads share a warp, else in
+// shared memory.
+// Raw input of one 4-input quad: fp32 values, or u8 levels in .x
+template <bool F32>
+__device__ __forceinline__ float4 st_quad_raw(const StParams& p, const void* xrow, int q) {
+  if (!F32) {
+    const uint8_t* xr = static_cast<const uint8_t*>(xrow);
+    uint32_t w = 0;
+    if (4 * q + 3 < p.n_in && (p.ld_x & 3) == 0) {
+      w = __ldg(reinterpret_cast<const uint32_t*>(xr) + q);
+    } else {
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        if (4 * q + t < p.n_in) w |= static_cast<uint32_t>(__ldg(xr + 4 * q + t)) << (8 * t);
+    }
+    return make_float4(__uint_as_float(w), 0.f, 0.f, 0.f);
+  }
+  const float* xr = static_cast<const float*>(xrow);
+  if (4 * q + 3 < p.n_in && (p.ld_x & 3) == 0)
+    return ldg_stream_f4(reinterpret_cast<const float4*>(xr) + q, l2_policy_evict_first());
+  float v[4];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) v[t] = 4 * q + t < p.n_in ? __ldg(xr + 4 * q + t) : 0.f;
+  return make_float4(v[0], v[1], v[2], v[3]);
+}
+
+// The quad's four levels packed in a u32.  fp32 inputs: element t is
+// quantized by lane t % lpr of the group (slot t / lpr) and exchanged by
+// shuffles among the group's lanes (which share row, slice and trip count).
+template <int LPR, bool F32>
+__device__ __forceinline__ uint32_t st_quad_levels(const StParams& p, float4 f, int q, int lane,
+                                                   const float* thr) {
+  if (!F32) return __float_as_uint(f.x);
+  constexpr int lpr = LPR;
+  const float v[4] = {f.x, f.y, f.z, f.w};
+  const int l = lane % lpr;
+  int mine[4] = {0, 0, 0, 0};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int t = l + k * lpr;
+    const float vt = t == 0 ? v[0] : (t == 1 ? v[1] : (t == 2 ? v[2] : v[3]));
+    mine[k] = (t < 4 && 4 * q + t < p.n_in) ? st_level_f32(vt, thr, p.inv_s, p.zf, p.in_qhi) : 0;
+    if (k * lpr + lpr >= 4) break;
+  }
+  if constexpr (lpr == 1) return mine[0] | (mine[1] << 8) | (mine[2] << 16) | (static_cast<uint32_t>(mine[3]) << 24);
+  const int base = lane - l;
+  const unsigned mask = (lpr == 32) ? 0xffffffffu : (((1u << lpr) - 1u) << base);
+  uint32_t w = 0;
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const int src = base + (t % lpr);
+    const int mv = lpr >= 4 ? mine[0] : (t / lpr == 0 ? mine[0] : mine[1]);  // lpr == 2: slots 0, 1
+    const int lv = __shfl_sync(mask, mv, src);
+    w |= static_cast<uint32_t>(lv) << (8 * t);
+  }
+  return w;
+}
+
+template <int LPR, int KIND>  // KIND: 0 dense u8 levels, 1 dense fp32 values, 2 conv u8 NCHW
+__global__ void __launch_bounds__(256, 3) kan_st_layer_kernel(const StParams p) {
   extern __shared__ __align__(16) uint8_t st_smem[];
   pdl_trigger();
-  const int lpr = p.lpr;
-  const int RP = 256 / lpr;
-  const int g = threadIdx.x / lpr, l = threadIdx.x % lpr;
+  constexpr int lpr = LPR;
+  constexpr bool F32 = KIND == 1;
+  const int S = p.slices;
+  const int RP = 256 / (lpr * S);
+  const int lane = threadIdx.x & 31;
+  const int l = threadIdx.x % lpr, s = (threadIdx.x / lpr) % S, g = threadIdx.x / (lpr * S);
   const int c0 = (static_cast<int>(blockIdx.y) * lpr + l) * 16;
   const bool col_ok = c0 < p.Np;
-  const int IC = p.ic;
-  const int lds = IC + 4;  // staged row pitch (odd word count: conflict-free)
-  float* thr = reinterpret_cast<float*>(st_smem + RP * lds);
-  if (p.in_kind == ST_IN_F32)
+  int* red = reinterpret_cast<int*>(st_smem);                    // [8 warps][32][16] partial sums (S*lpr > 32)
+  float* thr = reinterpret_cast<float*>(st_smem + 256 * 16 * 4);  // [qhi + 2]
+  if (F32)
     for (int t = threadIdx.x; t <= p.in_qhi + 1; t += blockDim.x) thr[t] = p.thr[t];
+  __syncthreads();
   const uint8_t* T = p.T + (col_ok ? c0 : 0);
   const int64_t row_stride = static_cast<int64_t>(p.Lv) * p.Np;  // bytes per input
+  const uint64_t pol_t = l2_policy_evict_last();
   pdl_wait();
   for (int64_t rb = blockIdx.x; rb * RP < p.rows; rb += gridDim.x) {
     const int64_t r = rb * RP + g;
@@ -244,79 +347,165 @@ __global__ void __launch_bounds__(256) kan_st_layer_kernel(const StParams p) {
     acc.clear_pk();
 #pragma unroll
     for (int t = 0; t < 16; ++t) acc.a[t] = 0;
-    if (!p.conv) {
-      for (int i0 = 0; i0 < p.n_in; i0 += IC) {
-        const int cnt = min(IC, p.n_in - i0);
-        __syncthreads();  // the previous chunk's levels are consumed
-        if (p.in_kind == ST_IN_F32) {
-          const float* x = static_cast<const float*>(p.x);
-          for (int t = threadIdx.x; t < RP * IC; t += blockDim.x) {
-            const int rr = t / IC, ii = t % IC;
-            const int64_t row = rb * RP + rr;
-            int lv = 0;
-            if (ii < cnt && row < p.rows)
-              lv = st_level_f32(x[row * p.ld_x + i0 + ii], thr, p.inv_s, p.zf, p.in_qhi);
-            st_smem[rr * lds + ii] = static_cast<uint8_t>(lv);
+    if constexpr (KIND != 2) {
+      if (row_ok) {  // group-uniform: the lpr lanes of a (row, slice) share the trip count
+        constexpr int esz = F32 ? 4 : 1;
+        const uint8_t* xrow = static_cast<const uint8_t*>(p.x) + r * p.ld_x * esz;
+        const int nq = (p.n_in + 3) >> 2;
+        int q = s, since = 0;
+        // the next step's inputs are loaded while this step's gathers are in flight
+        float4 ra = q < nq ? st_quad_raw<F32>(p, xrow, q) : make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 rb2 = q + S < nq ? st_quad_raw<F32>(p, xrow, q + S) : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (; q + S < nq; q += 2 * S) {  // two quads in flight: eight 16-byte gathers
+          const uint32_t la = st_quad_levels<LPR, F32>(p, ra, q, lane, thr);
+          const uint32_t lb = st_quad_levels<LPR, F32>(p, rb2, q + S, lane, thr);
+          if (q + 2 * S < nq) ra = st_quad_raw<F32>(p, xrow, q + 2 * S);
+          if (q + 3 * S < nq) rb2 = st_quad_raw<F32>(p, xrow, q + 3 * S);
+          const uint8_t* Ta = T + static_cast<int64_t>(4 * q) * row_stride;
+          const uint8_t* Tb = T + static_cast<int64_t>(4 * (q + S)) * row_stride;
+          uint4 w[8];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            w[t] = ldg_row(Ta + t * row_stride + ((la >> (8 * t)) & 0xffu) * p.Np, pol_t);
+            w[4 + t] = ldg_row(Tb + t * row_stride + ((lb >> (8 * t)) & 0xffu) * p.Np, pol_t);
           }
-        } else {
-          const uint8_t* x = static_cast<const uint8_t*>(p.x);
-          for (int t = threadIdx.x; t < RP * IC; t += blockDim.x) {
-            const int rr = t / IC, ii = t % IC;
-            const int64_t row = rb * RP + rr;
-            st_smem[rr * lds + ii] = (ii < cnt && row < p.rows) ? x[row * p.ld_x + i0 + ii] : 0;
+#pragma unroll
+          for (int t = 0; t < 8; ++t) acc.add(w[t]);
+          since += 2;
+          if (since >= 62) {  // <= 256 inputs per flush: the 16-bit pairs cannot overflow
+            acc.flush();
+            since = 0;
           }
         }
-        __syncthreads();
-        if (row_ok && col_ok) {
-          const uint8_t* lv = st_smem + g * lds;
-          const uint8_t* Ti = T + static_cast<int64_t>(i0) * row_stride;
-          int ii = 0;
-          for (; ii + 4 <= cnt; ii += 4) {
-            const uint32_t l4 = *reinterpret_cast<const uint32_t*>(lv + ii);
-            const uint4 w0 = ldg_row(Ti + (l4 & 0xffu) * p.Np);
-            const uint4 w1 = ldg_row(Ti + row_stride + ((l4 >> 8) & 0xffu) * p.Np);
-            const uint4 w2 = ldg_row(Ti + 2 * row_stride + ((l4 >> 16) & 0xffu) * p.Np);
-            const uint4 w3 = ldg_row(Ti + 3 * row_stride + (l4 >> 24) * p.Np);
-            acc.add(w0);
-            acc.add(w1);
-            acc.add(w2);
-            acc.add(w3);
-            Ti += 4 * row_stride;
-          }
-          for (; ii < cnt; ++ii) {
-            acc.add(ldg_row(Ti + lv[ii] * p.Np));
-            Ti += row_stride;
-          }
-          acc.flush();  // IC <= 256 inputs per chunk
+        if (q < nq) {
+          const uint32_t la = st_quad_levels<LPR, F32>(p, ra, q, lane, thr);
+          const uint8_t* Ta = T + static_cast<int64_t>(4 * q) * row_stride;
+          uint4 w[4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) w[t] = ldg_row(Ta + t * row_stride + ((la >> (8 * t)) & 0xffu) * p.Np, pol_t);
+#pragma unroll
+          for (int t = 0; t < 4; ++t) acc.add(w[t]);
         }
+        acc.flush();
       }
-    } else if (row_ok && col_ok) {
+    } else if (row_ok) {
       const int64_t hw = static_cast<int64_t>(p.Ho) * p.Wo;
       const int64_t img = r / hw, pp = r % hw;
       const int oy = static_cast<int>(pp / p.Wo), ox = static_cast<int>(pp % p.Wo);
       const int iy0 = oy * p.cstride - p.pad, ix0 = ox * p.cstride - p.pad;
       const uint8_t* xin = static_cast<const uint8_t*>(p.x) + img * p.C * static_cast<int64_t>(p.H) * p.W;
-      const uint8_t* Ti = T;
       const int kk = p.K * p.K;
-      const int cpf = max(1, 256 / kk);  // channels between flushes (<= 256 inputs)
-      for (int c = 0; c < p.C; ++c) {
-        const uint8_t* xc = xin + static_cast<int64_t>(c) * p.H * p.W;
-        for (int ky = 0; ky < p.K; ++ky) {
-          const int iy = iy0 + ky;
-          const bool yok = iy >= 0 && iy < p.H;
-          for (int kx = 0; kx < p.K; ++kx) {
-            const int ix = ix0 + kx;
-            const int lv = (yok && ix >= 0 && ix < p.W) ? __ldg(xc + iy * p.W + ix) : p.lvl0;
-            acc.add(ldg_row(Ti + lv * p.Np));
-            Ti += row_stride;
-          }
-          if (kk > 256) acc.flush();  // very large kernels: one flush per kernel row
+      const int cpf = max(1, 256 / kk);  // own channels between flushes (<= 256 inputs)
+      int since = 0;
+      if (p.K == 3) {  // 3x3: tap offsets / padding masks hoisted, nine gathers in flight
+        int off[9];
+        bool ok[9];
+#pragma unroll
+        for (int t = 0; t < 9; ++t) {
+          const int iy = iy0 + t / 3, ix = ix0 + t % 3;
+          ok[t] = iy >= 0 && iy < p.H && ix >= 0 && ix < p.W;
+          off[t] = ok[t] ? iy * p.W + ix : 0;
         }
-        if ((c + 1) % cpf == 0) acc.flush();
+        const int64_t plane = static_cast<int64_t>(p.H) * p.W;
+        for (int c = s; c < p.C; c += S) {
+          const uint8_t* xc = xin + c * plane;
+          const uint8_t* Ti = T + static_cast<int64_t>(c) * 9 * row_stride;
+          int lv[9];
+#pragma unroll
+          for (int t = 0; t < 9; ++t) lv[t] = ok[t] ? __ldg(xc + off[t]) : p.lvl0;
+          uint4 w[9];
+#pragma unroll
+          for (int t = 0; t < 9; ++t) w[t] = ldg_row(Ti + t * row_stride + lv[t] * p.Np, pol_t);
+#pragma unroll
+          for (int t = 0; t < 9; ++t) acc.add(w[t]);
+          if (++since == 28) {  // 252 inputs per flush
+            acc.flush();
+            since = 0;
+          }
+        }
+      } else {
+        for (int c = s; c < p.C; c += S) {
+          const uint8_t* xc = xin + static_cast<int64_t>(c) * p.H * p.W;
+          const uint8_t* Ti = T + static_cast<int64_t>(c) * kk * row_stride;
+          for (int ky = 0; ky < p.K; ++ky) {
+            const int iy = iy0 + ky;
+            const bool yok = iy >= 0 && iy < p.H;
+            for (int kx = 0; kx < p.K; ++kx) {
+              const int ix = ix0 + kx;
+              const int lv = (yok && ix >= 0 && ix < p.W) ? __ldg(xc + iy * p.W + ix) : p.lvl0;
+              acc.add(ldg_row(Ti + lv * p.Np, pol_t));
+              Ti += row_stride;
+            }
+            if (kk > 256) acc.flush();  // very large kernels: one flush per kernel row
+          }
+          if (++since == cpf) {
+            acc.flush();
+            since = 0;
+          }
+        }
       }
       acc.flush();
     }
-    if (row_ok && col_ok) st_epilogue(p, r, c0, acc.a);
+    // the S slices of a row meet: warp shuffles over the slices inside a warp,
+    // then (rows wider than a warp) shared memory across the row's warps
+    if (S > 1) {
+      const int span = lpr * S < 32 ? lpr * S : 32;
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1)
+        if (o >= lpr && o < span)
+#pragma unroll
+          for (int t = 0; t < 16; ++t) acc.a[t] += __shfl_xor_sync(0xffffffffu, acc.a[t], o);
+      if (lpr * S > 32) {
+        const int wpr = lpr * S / 32;  // warps per row
+        __syncthreads();
+        if (lane < lpr) {
+#pragma unroll
+          for (int t = 0; t < 16; ++t) red[((threadIdx.x >> 5) * 32 + lane) * 16 + ((t + lane) & 15)] = acc.a[t];
+        }
+        __syncthreads();
+        if (s == 0) {
+          for (int o = 1; o < wpr; ++o) {
+            const int src = ((threadIdx.x >> 5) + o) * 32 + lane;
+#pragma unroll
+            for (int t = 0; t < 16; ++t) acc.a[t] += red[src * 16 + ((t + lane) & 15)];
+          }
+        }
+      }
+    }
+    if constexpr (KIND != 2) {
+      if (p.f_on) {  // fused output layer: the row's first warp (lpr * S >= 32) runs it
+        if ((threadIdx.x % (lpr * S)) >= 32) continue;  // warp-uniform
+        uint8_t* hid = st_smem + 256 * 16 * 4 + 258 * 4 + g * 512;
+        if (s == 0 && col_ok) {
+#pragma unroll
+          for (int t = 0; t < 16; ++t)
+            if (c0 + t < p.n_out) hid[c0 + t] = st_level_of_sum(p, static_cast<int>(acc.a[t] - p.corr));
+        }
+        __syncwarp();
+        Acc16 acc2;
+        acc2.clear_pk();
+#pragma unroll
+        for (int t = 0; t < 16; ++t) acc2.a[t] = 0;
+        if (row_ok)
+          for (int j = lane; j < p.f_n_in; j += 32)
+            acc2.add(ldg_row(p.f_T + (static_cast<int64_t>(j) * p.f_Lv + hid[j]) * 16, pol_t));
+        acc2.flush();  // <= 16 inputs per lane for n_in <= 512
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1)
+#pragma unroll
+          for (int t = 0; t < 16; ++t) acc2.a[t] += __shfl_xor_sync(0xffffffffu, acc2.a[t], o);
+        if (lane < p.f_n_out && row_ok) {
+          int v = acc2.a[0];
+#pragma unroll
+          for (int t = 1; t < 16; ++t) v = lane == t ? acc2.a[t] : v;
+          p.f_out[r * p.f_ld_out + lane] =
+              static_cast<float>(__dmul_rn(p.f_out_s, static_cast<double>(static_cast<long long>(v) - p.f_corr)));
+        }
+        __syncwarp();
+        continue;
+      }
+    }
+    if (s == 0 && row_ok && col_ok) st_epilogue(p, r, c0, acc.a);
   }
 }
 
@@ -426,25 +615,43 @@ cudaError_t launch_st_sample(const double* basis, const double* coeffs, int n_in
 }
 
 size_t st_layer_smem(const StParams& p) {
-  const int RP = 256 / p.lpr;
-  return static_cast<size_t>(RP) * (p.ic + 4) + 258 * sizeof(float);
+  return 256 * 16 * sizeof(int) + 258 * sizeof(float) + (p.f_on ? 8 * 512 : 0);
+}
+
+template <int LPR, int KIND>
+static cudaError_t launch_st_layer_t(const StParams& p, dim3 grid, size_t smem, cudaStream_t st) {
+  auto kfn = kan_st_layer_kernel<LPR, KIND>;
+  static size_t configured = 0;
+  if (smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  return st_launch(kfn, grid, dim3(256), smem, st, p);
+}
+
+template <int KIND>
+static cudaError_t launch_st_kind(const StParams& p, dim3 grid, size_t smem, cudaStream_t st) {
+  switch (p.lpr) {
+    case 1: return launch_st_layer_t<1, KIND>(p, grid, smem, st);
+    case 2: return launch_st_layer_t<2, KIND>(p, grid, smem, st);
+    case 4: return launch_st_layer_t<4, KIND>(p, grid, smem, st);
+    case 8: return launch_st_layer_t<8, KIND>(p, grid, smem, st);
+    case 16: return launch_st_layer_t<16, KIND>(p, grid, smem, st);
+    case 32: return launch_st_layer_t<32, KIND>(p, grid, smem, st);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 cudaError_t launch_st_layer(const StParams& p, cudaStream_t st) {
   if (p.rows == 0) return cudaSuccess;
   const size_t smem = st_layer_smem(p);
-  static size_t configured = 0;
-  if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(kan_st_layer_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-    configured = smem;
-  }
-  const int RP = 256 / p.lpr;
+  const int RP = 256 / (p.lpr * p.slices);
   const int64_t blocks = (p.rows + RP - 1) / RP;
   const int64_t cap = static_cast<int64_t>(st_sm_count()) * 8;
   const dim3 grid(static_cast<unsigned>(blocks < cap ? blocks : cap), static_cast<unsigned>(p.col_tiles));
-  return st_launch(kan_st_layer_kernel, grid, dim3(256), smem, st, p);
+  if (p.conv) return launch_st_kind<2>(p, grid, smem, st);
+  return p.in_kind == ST_IN_F32 ? launch_st_kind<1>(p, grid, smem, st) : launch_st_kind<0>(p, grid, smem, st);
 }
 
 cudaError_t launch_st_levels(const float* x, int64_t n, const float* thr, float inv_s, float zf, int qhi,

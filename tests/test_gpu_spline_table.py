@@ -90,7 +90,8 @@ def test_mlp_forward_bit_exact(oracle, dims, M, bits_a, h):
     want = oracle.spline_model_forward(desc, tabs, x.astype(np.float64)).astype(np.float32)
     np.testing.assert_array_equal(y, want)
     np.testing.assert_array_equal(e.forward_host(x), want)
-    assert e.last_launches == len(Ws)
+    fused = len(Ws) >= 2 and dims[-1] <= 16 and dims[-2] <= 512  # output layer runs fused
+    assert e.last_launches == len(Ws) - int(fused)
 
 
 def test_conv_models_bit_exact(oracle):
