@@ -24,6 +24,8 @@
  *   kan_engine_set_spline_tables  EvalOptions::tables (SplineTableSet) eval.hpp:41,
  *                               spline_table.hpp:19-34
  *   kan_engine_spline_table     build_spline_tables (probe)         spline_table.hpp:38-95
+ *   kan_container_load / _save  load_container / save_container     io.hpp:99-350
+ *   kan_engine_load             load_model / load_container + engine io.hpp:217-352
  *
  * Error mapping (reference exception -> status):
  *   std::invalid_argument (bits, LUT params, mode)  -> KAN_ERR_INVALID_ARGUMENT
@@ -188,6 +190,44 @@ int64_t kan_lut_build(int degree, int k, int h, uint8_t* out, int64_t cap);
  * (lut.hpp:44-47, grid.hpp:49-56).  `out` holds L+2 floats.  Returns L+2. */
 int64_t kan_lattice_thresholds(int intervals, int degree, double lo, double hi, int k,
                                float* out, int64_t cap);
+
+/* .kant model container (io.hpp:99-350) --------------------------------- */
+/* Host-side reader: load_container (io.hpp:217-350).  Errors: missing file ->
+ * KAN_ERR_IO, bad magic / unsupported version (named in the message) /
+ * truncation -> KAN_ERR_FORMAT, payload CRC mismatch -> KAN_ERR_CHECKSUM.  On
+ * error *out still holds a handle carrying the message (destroy it). */
+typedef struct kan_container kan_container;
+kan_status kan_container_load(const char* path, kan_container** out);
+void kan_container_destroy(kan_container* c);
+const char* kan_container_last_error(const kan_container* c);
+/* the stored model in the descriptor schema kan_engine_create takes */
+const char* kan_container_descriptor(const kan_container* c);
+int kan_container_num_kan_layers(const kan_container* c);
+/* coefficients of KAN layer `layer` (f32 in the file, widened to fp64), reference
+ * row layout [n_in*(G+P), n_out]; returns the count */
+int64_t kan_container_coeffs(const kan_container* c, int layer, double* out, int64_t cap);
+/* the embedded BsplineLut entries (0 if none) and its degree / k / h */
+int64_t kan_container_lut(const kan_container* c, uint8_t* out, int64_t cap, int* degree, int* k, int* h);
+/* embedded SplineTableSets (one per KAN layer when present), as for
+ * kan_engine_set_spline_tables */
+int kan_container_num_spline_tables(const kan_container* c);
+int64_t kan_container_spline_table(const kan_container* c, int t, uint8_t* out, int64_t cap, int* bits_a,
+                                   int* h, double* qp_d, int64_t* qp_i);
+/* save_container (io.hpp:108-211) of a descriptor-schema model: coeffs[i] =
+ * KAN layer i's coefficients (stored as f32); optional LUT entries (lut == NULL:
+ * none) and per-KAN-layer spline tables (st_values == NULL: none; qp arrays
+ * [n_kan][2] / [n_kan][4] as above).  Byte-identical to the reference's file. */
+kan_status kan_container_save(const char* path, const char* descriptor_json, const double* const* coeffs,
+                              const uint8_t* lut, int64_t lut_n, int lut_k, int lut_h,
+                              const uint8_t* const* st_values, int st_bits_a, int st_h, const double* st_qp_d,
+                              const int64_t* st_qp_i);
+const char* kan_container_save_error(void);
+/* crc32 of io.hpp:31-45 (host utility) */
+uint32_t kan_crc32(const uint8_t* data, size_t len);
+/* load_model + engine: create from the container's model, set its coefficients,
+ * its spline tables (if present) and its LUT (used by configure when lut_k /
+ * lut_h match the stored table). */
+kan_status kan_engine_load(const char* path, int device, kan_engine** out);
 
 /* Host utility: the spline-table input level thresholds the GPU uses,
  * thr[n] = smallest fp32 x with quantize_value(x, in_qp) >= n for n = 1..2^bits_a-1

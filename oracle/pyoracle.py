@@ -540,6 +540,9 @@ class Ref:
         L.ref_st_model_forward.argtypes = [C.c_char_p, C.POINTER(C.c_void_p), C.c_int, C.c_int,
                                            C.c_int64, C.c_int64, _dp, C.c_int64, _dp, C.c_int,
                                            C.c_int64, C.c_int, C.POINTER(C.c_double)]
+        L.ref_save_container.argtypes = [C.c_char_p, C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_int,
+                                         C.c_int, C.c_char_p]
+        L.ref_load_container.argtypes = [C.c_char_p]
         L.ref_model_forward.argtypes = [C.c_char_p, C.POINTER(C.c_void_p), C.c_int, C.c_int,
                                         C.c_int, C.c_int, C.c_int64, C.c_int64, _dp, C.c_int64,
                                         _dp, C.c_int, C.c_int64]
@@ -689,6 +692,19 @@ class Ref:
                                          C.byref(sec)):
             raise ValueError(self.err())
         return out, sec.value
+
+    def save_container(self, text, coeffs, path, lut_k=0, lut_h=0, st_bits_a=0, st_h=0):
+        """save_container of a descriptor-built model (io.hpp:108-211)."""
+        cs = [np.ascontiguousarray(c, dtype=np.float64) for c in coeffs]
+        ptrs = (C.c_void_p * len(cs))(*[c.ctypes.data for c in cs])
+        if self.lib.ref_save_container(text.encode(), ptrs, lut_k, lut_h, st_bits_a, st_h,
+                                       str(path).encode()):
+            raise ValueError(self.err())
+
+    def load_container(self, path):
+        """load_container: (layer count or -6 io / -7 format / -8 checksum, message)."""
+        n = self.lib.ref_load_container(str(path).encode())
+        return n, (self.err() if n < 0 else "")
 
     def validate_descriptor(self, text: str) -> int:
         n = self.lib.ref_validate_descriptor(text.encode())

@@ -20,6 +20,7 @@
 #include <kantize/quant.hpp>
 #include <kantize/cost.hpp>
 #include <kantize/spline_table.hpp>
+#include <optional>
 
 #include <algorithm>
 #include <chrono>
@@ -406,6 +407,52 @@ int ref_st_model_forward(const char* json_text, const double* const* coeff_ptrs,
   return 0;
 } catch (const std::exception& e) {
   return fail(e);
+}
+
+// save_container (io.hpp:108-211) of a descriptor-built model with its
+// coefficients; lut_k > 0 adds build_bspline_lut(P, lut_k, lut_h); st_bits_a > 0
+// adds build_spline_tables(layer, st_bits_a, st_h) for every KAN layer.
+int ref_save_container(const char* json_text, const double* const* coeff_ptrs, int lut_k, int lut_h,
+                       int st_bits_a, int st_h, const char* path) try {
+  Model model = model_from_descriptor(nlohmann::json::parse(json_text));
+  int li = 0;
+  std::vector<SplineTableSet> tables;
+  for (auto& layer : model.layers) {
+    if (auto* lin = std::get_if<KanLinearLayer>(&layer)) {
+      std::copy(coeff_ptrs[li], coeff_ptrs[li] + lin->coeffs.size(), lin->coeffs.flat().begin());
+      if (st_bits_a > 0) tables.push_back(build_spline_tables(*lin, st_bits_a, st_h));
+      ++li;
+    } else if (auto* conv = std::get_if<ConvKanLayer>(&layer)) {
+      std::copy(coeff_ptrs[li], coeff_ptrs[li] + conv->coeffs.size(), conv->coeffs.flat().begin());
+      if (st_bits_a > 0) tables.push_back(build_spline_tables(*conv, st_bits_a, st_h));
+      ++li;
+    }
+  }
+  std::optional<BsplineLut> lut;
+  if (lut_k > 0) lut = build_bspline_lut(model.grid().degree(), lut_k, lut_h);
+  save_container(model, path, lut ? &*lut : nullptr, st_bits_a > 0 ? &tables : nullptr);
+  return 0;
+} catch (const std::exception& e) {
+  return fail(e);
+}
+
+// load_container (io.hpp:217-350): number of layers, or -6 io_error,
+// -7 format_error, -8 checksum_error, -1 other
+int ref_load_container(const char* path) {
+  try {
+    return static_cast<int>(load_container(path).model.layers.size());
+  } catch (const io_error& e) {
+    g_err = e.what();
+    return -6;
+  } catch (const format_error& e) {
+    g_err = e.what();
+    return -7;
+  } catch (const checksum_error& e) {
+    g_err = e.what();
+    return -8;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
 }
 
 // Harness composition for descriptors the reference cannot express (the

@@ -8,5 +8,6 @@ from .engine import (  # noqa: F401
     Engine, EvalOptions, KanError, build_bspline_lut, eval_mode_from_string,
     kan_linear_forward, tabulated_kan_forward, lattice_thresholds, MODE_FP32, MODE_BF16, MODE_BSPLINE_LUT,
     MODE_SPLINE_TABLE, build_spline_tables, spline_table_forward, spline_thresholds,
+    load_container, save_container, crc32,
     W_PER_TENSOR_ASYM, W_PER_CHANNEL_SYM, OUT_F32, OUT_I8, PASSTHROUGH_BITS, LIB_PATH,
 )

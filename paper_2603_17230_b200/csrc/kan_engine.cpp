@@ -285,6 +285,10 @@ struct kan_engine {
   DevBuf<uint16_t> xlev;  // level prepass of a large fp32-input dense layer
   DevBuf<uint16_t> xcol;  // level im2col of the model input (stem convs)
   DevBuf<float> logits_tmp;
+  // LUT entries read from a .kant container (kan_engine_load): configure uses
+  // them when lut_k / lut_h match (EvalOptions::lut, eval.hpp:40)
+  std::vector<uint8_t> c_lut;
+  int c_lut_k = 0, c_lut_h = 0;
   // spline-table mode
   std::vector<StLayer> st;
   QParams st_in;            // input quantizer on the grid bounds (spline_table.hpp:51)
@@ -1290,6 +1294,12 @@ void configure(kan_engine* e, const kan_config* c) {
   const Grid& g = e->grid;
   if (cfg.mode == KAN_MODE_BSPLINE_LUT) {
     e->lut = build_lut(g.P, cfg.lut_k, cfg.lut_h);  // validates P, k, h like the reference
+    if (!e->c_lut.empty() && e->c_lut_k == cfg.lut_k && e->c_lut_h == cfg.lut_h) {
+      if (e->c_lut.size() != e->lut.size())
+        throw FormatError("configure: the container's LUT has " + std::to_string(e->c_lut.size()) +
+                          " entries, expected " + std::to_string(e->lut.size()));
+      e->lut = e->c_lut;  // the caller's table (eval.hpp:40 EvalOptions::lut)
+    }
     e->lat = Lattice::of(g, cfg.lut_k);
     const int64_t L = e->lat.L;
     const std::vector<float> thr = level_thresholds(g, e->lat);
@@ -2309,6 +2319,53 @@ kan_status kan_engine_layer_accumulators(kan_engine* e, int layer, const uint16_
     else
       run_gemm_layer(e, pl, batch, io, static_cast<cudaStream_t>(stream));
   });
+}
+
+kan_status kan_engine_load(const char* path, int device, kan_engine** out) {
+  if (!out || !path) return KAN_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  kan_container* c = nullptr;
+  kan_status st = kan_container_load(path, &c);
+  if (st != KAN_OK) {
+    // surface the container's message through a handle the caller can read
+    auto e = std::make_unique<kan_engine>();
+    e->err = kan_container_last_error(c);
+    kan_container_destroy(c);
+    *out = e.release();
+    return st;
+  }
+  st = kan_engine_create(kan_container_descriptor(c), device, out);
+  if (st == KAN_OK) {
+    kan_engine* e = *out;
+    for (int i = 0; i < kan_container_num_kan_layers(c) && st == KAN_OK; ++i) {
+      std::vector<double> w(static_cast<size_t>(kan_container_coeffs(c, i, nullptr, 0)));
+      kan_container_coeffs(c, i, w.data(), static_cast<int64_t>(w.size()));
+      st = kan_engine_set_coeffs(e, i, w.data(), static_cast<int64_t>(w.size()), nullptr, 0);
+    }
+    for (int t = 0; t < kan_container_num_spline_tables(c) && st == KAN_OK; ++t) {
+      int bits_a = 0, h = 0;
+      double qd[2];
+      int64_t qi[4];
+      std::vector<uint8_t> v(static_cast<size_t>(kan_container_spline_table(c, t, nullptr, 0, nullptr, nullptr,
+                                                                           nullptr, nullptr)));
+      kan_container_spline_table(c, t, v.data(), static_cast<int64_t>(v.size()), &bits_a, &h, qd, qi);
+      st = kan_engine_set_spline_tables(e, t, v.data(), static_cast<int64_t>(v.size()), bits_a, h, qd, qi);
+    }
+    int deg = 0, k = 0, h = 0;
+    const int64_t nl = kan_container_lut(c, nullptr, 0, &deg, &k, &h);
+    if (st == KAN_OK && nl > 0) {
+      e->c_lut.resize(static_cast<size_t>(nl));
+      kan_container_lut(c, e->c_lut.data(), nl, nullptr, nullptr, nullptr);
+      e->c_lut_k = k;
+      e->c_lut_h = h;
+      if (deg != e->grid.P) {
+        e->err = "load_container: LUT degree " + std::to_string(deg) + " does not match the model's degree";
+        st = KAN_ERR_FORMAT;
+      }
+    }
+  }
+  kan_container_destroy(c);
+  return st;
 }
 
 kan_status kan_engine_set_spline_tables(kan_engine* e, int layer, const uint8_t* values, int64_t n,

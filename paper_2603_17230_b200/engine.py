@@ -92,6 +92,28 @@ _lib.kan_engine_layer_timeline.restype = C.c_int64
 _lib.kan_engine_set_spline_tables.argtypes = [_vp, C.c_int, _vp, C.c_int64, C.c_int, C.c_int, _vp, _vp]
 _lib.kan_engine_spline_table.argtypes = [_vp, C.c_int, _vp, C.c_int64, _vp, _vp]
 _lib.kan_engine_spline_table.restype = C.c_int64
+_lib.kan_container_load.argtypes = [C.c_char_p, C.POINTER(_vp)]
+_lib.kan_container_destroy.argtypes = [_vp]
+_lib.kan_container_last_error.argtypes = [_vp]
+_lib.kan_container_last_error.restype = C.c_char_p
+_lib.kan_container_descriptor.argtypes = [_vp]
+_lib.kan_container_descriptor.restype = C.c_char_p
+_lib.kan_container_num_kan_layers.argtypes = [_vp]
+_lib.kan_container_coeffs.argtypes = [_vp, C.c_int, _vp, C.c_int64]
+_lib.kan_container_coeffs.restype = C.c_int64
+_lib.kan_container_lut.argtypes = [_vp, _vp, C.c_int64, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                   C.POINTER(C.c_int)]
+_lib.kan_container_lut.restype = C.c_int64
+_lib.kan_container_num_spline_tables.argtypes = [_vp]
+_lib.kan_container_spline_table.argtypes = [_vp, C.c_int, _vp, C.c_int64, C.POINTER(C.c_int),
+                                            C.POINTER(C.c_int), _vp, _vp]
+_lib.kan_container_spline_table.restype = C.c_int64
+_lib.kan_container_save.argtypes = [C.c_char_p, C.c_char_p, _vp, _vp, C.c_int64, C.c_int, C.c_int,
+                                    _vp, C.c_int, C.c_int, _vp, _vp]
+_lib.kan_container_save_error.restype = C.c_char_p
+_lib.kan_crc32.argtypes = [_vp, C.c_size_t]
+_lib.kan_crc32.restype = C.c_uint32
+_lib.kan_engine_load.argtypes = [C.c_char_p, C.c_int, C.POINTER(_vp)]
 _lib.kan_lut_build.argtypes = [C.c_int, C.c_int, C.c_int, _vp, C.c_int64]
 _lib.kan_lut_build.restype = C.c_int64
 _lib.kan_lattice_thresholds.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, _vp,
@@ -110,6 +132,10 @@ EXPORTED = [
     "kan_engine_last_launches", "kan_lut_build", "kan_lattice_thresholds",
     "kan_engine_set_profiling", "kan_engine_layer_time_ms", "kan_engine_layer_timeline",
     "kan_engine_set_spline_tables", "kan_engine_spline_table", "kan_spline_thresholds",
+    "kan_container_load", "kan_container_destroy", "kan_container_last_error",
+    "kan_container_descriptor", "kan_container_num_kan_layers", "kan_container_coeffs",
+    "kan_container_lut", "kan_container_num_spline_tables", "kan_container_spline_table",
+    "kan_container_save", "kan_container_save_error", "kan_crc32", "kan_engine_load",
 ]
 
 
@@ -131,6 +157,76 @@ def spline_thresholds(bits_a: int, lo: float = -1.0, hi: float = 1.0) -> np.ndar
     out = np.zeros(n, dtype=np.float32)
     _lib.kan_spline_thresholds(lo, hi, bits_a, out.ctypes.data, n)
     return out
+
+
+def crc32(data: bytes) -> int:
+    """crc32 of io.hpp:31-45."""
+    buf = (C.c_uint8 * max(len(data), 1)).from_buffer_copy(data or b"\0")
+    return _lib.kan_crc32(C.addressof(buf), len(data))
+
+
+def load_container(path: str) -> dict:
+    """load_container (io.hpp:217-350): the model as a descriptor, its coefficients,
+    and the LUT / spline tables stored with it.  Raises OSError (io_error),
+    ValueError (format_error / checksum_error; KanError.status tells which)."""
+    h = _vp()
+    st = _lib.kan_container_load(str(path).encode(), C.byref(h))
+    try:
+        if st != KAN_OK:
+            msg = _lib.kan_container_last_error(h).decode()
+            raise _STATUS.get(st, RuntimeError)(KanError(st, msg))
+        out = {"descriptor": json.loads(_lib.kan_container_descriptor(h).decode()), "coeffs": [],
+               "lut": None, "spline_tables": []}
+        for i in range(_lib.kan_container_num_kan_layers(h)):
+            n = _lib.kan_container_coeffs(h, i, None, 0)
+            w = np.zeros(n)
+            _lib.kan_container_coeffs(h, i, w.ctypes.data, n)
+            out["coeffs"].append(w)
+        deg, k, hb = C.c_int(), C.c_int(), C.c_int()
+        n = _lib.kan_container_lut(h, None, 0, C.byref(deg), C.byref(k), C.byref(hb))
+        if n > 0:
+            e = np.zeros(n, dtype=np.uint8)
+            _lib.kan_container_lut(h, e.ctypes.data, n, None, None, None)
+            out["lut"] = {"entries": e, "degree": deg.value, "k": k.value, "h": hb.value}
+        for t in range(_lib.kan_container_num_spline_tables(h)):
+            ba, hv = C.c_int(), C.c_int()
+            qd, qi = np.zeros(2), np.zeros(4, dtype=np.int64)
+            n = _lib.kan_container_spline_table(h, t, None, 0, None, None, None, None)
+            v = np.zeros(n, dtype=np.uint8)
+            _lib.kan_container_spline_table(h, t, v.ctypes.data, n, C.byref(ba), C.byref(hv),
+                                            qd.ctypes.data, qi.ctypes.data)
+            out["spline_tables"].append({"values": v, "bits_a": ba.value, "h": hv.value,
+                                         "qp_d": qd, "qp_i": qi})
+        return out
+    finally:
+        _lib.kan_container_destroy(h)
+
+
+def save_container(path: str, descriptor, coeffs, lut=None, spline_tables=None):
+    """save_container (io.hpp:108-211): lut = dict(entries, k, h) or None;
+    spline_tables = one dict per KAN layer (values, bits_a, h, qp_d, qp_i) or None."""
+    text = descriptor if isinstance(descriptor, str) else json.dumps(descriptor)
+    cs = [np.ascontiguousarray(c, dtype=np.float64) for c in coeffs]
+    cp = (_vp * len(cs))(*[c.ctypes.data for c in cs])
+    le = None if lut is None else np.ascontiguousarray(lut["entries"], dtype=np.uint8)
+    sv = sp = sqd = sqi = None
+    ba = hv = 0
+    if spline_tables:
+        vals = [np.ascontiguousarray(t["values"], dtype=np.uint8).ravel() for t in spline_tables]
+        sv = (_vp * len(vals))(*[v.ctypes.data for v in vals])
+        sqd = np.ascontiguousarray(np.stack([t["qp_d"] for t in spline_tables]), dtype=np.float64)
+        sqi = np.ascontiguousarray(np.stack([t["qp_i"] for t in spline_tables]), dtype=np.int64)
+        ba, hv = int(spline_tables[0]["bits_a"]), int(spline_tables[0]["h"])
+        sp = vals
+    st = _lib.kan_container_save(str(path).encode(), text.encode(), cp,
+                                 None if le is None else le.ctypes.data,
+                                 0 if le is None else le.size,
+                                 0 if lut is None else int(lut["k"]), 0 if lut is None else int(lut["h"]),
+                                 sv, ba, hv, None if sqd is None else sqd.ctypes.data,
+                                 None if sqi is None else sqi.ctypes.data)
+    del sp
+    if st != KAN_OK:
+        raise _STATUS.get(st, RuntimeError)(KanError(st, _lib.kan_container_save_error().decode()))
 
 
 def eval_mode_from_string(s: str) -> int:
@@ -192,6 +288,23 @@ class Engine:
             raise _STATUS.get(st, RuntimeError)(KanError(st, msg))
         self.device = device
         self.opts: Optional[EvalOptions] = None
+
+    @classmethod
+    def load(cls, path: str, device: int = 0) -> "Engine":
+        """load_model (io.hpp:352) into an engine: the container's model,
+        coefficients, spline tables and LUT."""
+        self = cls.__new__(cls)
+        h = _vp()
+        st = _lib.kan_engine_load(str(path).encode(), device, C.byref(h))
+        self._h = h
+        if st != KAN_OK:
+            msg = _lib.kan_engine_last_error(h).decode() if h else ""
+            self.close()
+            raise _STATUS.get(st, RuntimeError)(KanError(st, msg))
+        self.descriptor = load_container(path)["descriptor"]
+        self.device = device
+        self.opts = None
+        return self
 
     # -- lifetime ---------------------------------------------------------------
     def close(self):
