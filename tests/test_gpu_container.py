@@ -49,7 +49,7 @@ def test_reference_container_with_tables_drives_both_table_paths(ref, oracle, tm
     e.configure(EvalOptions(mode="spline-table", lut_k=6, lut_h=7))
     y = e.model_forward(xd).cpu().numpy()
     ws32 = [w.astype(np.float32).astype(np.float64) for w in ws]
-    tabs = oracle.spline_model_tables(DESC, ws32, 6, 7)
+    tabs = oracle.spline_model_tables(DESC, ws, 6, 7)  # the reference tabulated its fp64 coefficients
     want = oracle.spline_model_forward(DESC, tabs, x.astype(np.float64)).astype(np.float32)
     np.testing.assert_array_equal(y, want)
     # LUT mode with the stored (k=4, h=6) table: the reference's model_forward
