@@ -1062,10 +1062,21 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         uint32_t ra[4] = {0, 0, 0, 0};
         int32_t rs = 0;
         const uint32_t off = red_addr + static_cast<uint32_t>((rl * rstride + gq * 4) * 4);
-#pragma unroll 1
-        for (int q = 0; q < S; ++q) {
-          const uint4 wa = ld_cluster_v4(mapa(off, q));
-          if constexpr (MODE == MODE_ZP) rs += static_cast<int32_t>(ld_cluster_u32(mapa(rs_addr + rl * 4, q)));
+        // all S remote loads first (cluster <= 8 CTAs), then the sums
+        uint4 wq8[8];
+        int32_t rq8[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (q < S) {
+            wq8[q] = ld_cluster_v4(mapa(off, q));
+            if constexpr (MODE == MODE_ZP) rq8[q] = static_cast<int32_t>(ld_cluster_u32(mapa(rs_addr + rl * 4, q)));
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (q >= S) break;
+          const uint4 wa = wq8[q];
+          if constexpr (MODE == MODE_ZP) rs += rq8[q];
           if constexpr (BF16) {
             ra[0] = __float_as_uint(__uint_as_float(ra[0]) + __uint_as_float(wa.x));
             ra[1] = __float_as_uint(__uint_as_float(ra[1]) + __uint_as_float(wa.y));
@@ -1082,51 +1093,74 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
       if (p.f_on) {
         // fused output layer over this CTA's rows: TPR threads per row, inputs
-        // i = sub + TPR*e, mixed-sign dp4a per (input, output), integer
-        // shuffle reduction, then the fp64 epilogue (kan_small_layer_kernel's math)
+        // i = sub + TPR*e (all loads issued up front: shared-memory latency
+        // here is ~100 cycles, so dependent chains are what costs), mixed-sign
+        // dp4a per (input, output), xor-shuffle reduction over the row's
+        // threads (offset-outer, so the outputs' shuffles overlap), then thread
+        // sub == j runs output j's fp64 epilogue
         asm volatile("bar.sync 3, %0;" ::"r"(NP) : "memory");
-        const int TPR = NP / rows_per;  // 16 or 32: a row's threads share a warp
+        const int TPR = NP / rows_per;  // 8, 16 or 32: a row's threads share a warp
         const int lr = threadIdx.x / TPR, sub = threadIdx.x % TPR;
         const int rl = static_cast<int>(rank) * rows_per + lr;
         const int n2 = p.f_N, n_in2 = p.N;
+        const int row = tl.m0 + rl;
+        const bool valid_row = row < p.M;  // rows past M were never written
+        double fs_j = 0.0;
+        long long corr_j = 0;
+        if (sub < n2) {  // epilogue constants in flight during the contraction
+          fs_j = p.f_fs[sub];
+          if (p.f_silu) corr_j = p.f_corr[sub];
+        }
         const uint32_t* vals = reinterpret_cast<const uint32_t*>(sT);
         const uint8_t* silu_tab = sT + p.off_silu;
         const uint32_t mask = (1u << p.k) - 1u;
+        const uint16_t* lvr = f_lv + rl * BN;
         int acc[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) acc[j] = 0;
-        const bool valid_row = tl.m0 + rl < p.M;  // rows past M were never written
-        for (int i = sub; i < n_in2; i += TPR) {
-          const int a = valid_row ? f_lv[rl * BN + i] : 0;
-          const uint32_t v = p.rep ? vals[((static_cast<uint32_t>(a) & mask) << 5) | static_cast<uint32_t>(lane)]
-                                   : vals[static_cast<uint32_t>(a) & mask];
-          const uint32_t sft = 8u * static_cast<uint32_t>(a >> p.k);
-          const int sc = p.f_silu ? static_cast<int>(silu_tab[a]) : 0;
+        for (int i0 = 0; i0 < n_in2; i0 += 8 * TPR) {
+          int av[8];
+          uint32_t vv[8];
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            if (j < n2) {
-              acc[j] = dp4a_us(v, static_cast<uint32_t>(f_wq[i * n2 + j] >> sft), acc[j]);
-              if (p.f_silu) acc[j] += sc * static_cast<int>(f_wqb[j * n_in2 + i]);
+          for (int e = 0; e < 8; ++e) {
+            const int i = i0 + sub + e * TPR;
+            av[e] = (valid_row && i < n_in2) ? lvr[i] : 0;
+          }
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            vv[e] = p.rep ? vals[((static_cast<uint32_t>(av[e]) & mask) << 5) | static_cast<uint32_t>(lane)]
+                          : vals[static_cast<uint32_t>(av[e]) & mask];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int i = i0 + sub + e * TPR;
+            if (i < n_in2) {
+              const uint32_t sft = 8u * static_cast<uint32_t>(av[e] >> p.k);
+              const int sc = p.f_silu ? static_cast<int>(silu_tab[av[e]]) : 0;
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                if (j < n2) {
+                  acc[j] = dp4a_us(vv[e], static_cast<uint32_t>(f_wq[i * n2 + j] >> sft), acc[j]);
+                  if (p.f_silu) acc[j] += sc * static_cast<int>(f_wqb[j * n_in2 + i]);
+                }
+              }
             }
           }
         }
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
-          for (int off = TPR / 2; off > 0; off >>= 1) acc[j] += __shfl_down_sync(0xffffffffu, acc[j], off, TPR);
-        const int row = tl.m0 + rl;
-        if (sub == 0 && row < p.M) {
+        for (int off = 16; off >= 1; off >>= 1)
+          if (off < TPR)
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            if (j < n2) {
-              const size_t o = static_cast<size_t>(row) * p.f_ld_out + j;
-              const long long v = static_cast<long long>(acc[j]) - (p.f_silu ? p.f_corr[j] : 0ll);
-              const double y = __dmul_rn(static_cast<double>(v), p.f_fs[j]);
-              if (p.f_epi == EPI_F32)
-                static_cast<float*>(p.f_out)[o] = __double2float_rn(y);
-              else
-                static_cast<int8_t*>(p.f_out)[o] = static_cast<int8_t>(requant_i8(y, p.out_scale, p.inv_out_scale));
-            }
-          }
+            for (int j = 0; j < 16; ++j) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], off);
+        if (sub < n2 && valid_row) {
+          int v32 = acc[0];
+#pragma unroll
+          for (int j = 1; j < 16; ++j) v32 = sub == j ? acc[j] : v32;
+          const size_t o = static_cast<size_t>(row) * p.f_ld_out + sub;
+          const double y = __dmul_rn(static_cast<double>(static_cast<long long>(v32) - corr_j), fs_j);
+          if (p.f_epi == EPI_F32)
+            static_cast<float*>(p.f_out)[o] = __double2float_rn(y);
+          else
+            static_cast<int8_t*>(p.f_out)[o] = static_cast<int8_t>(requant_i8(y, p.out_scale, p.inv_out_scale));
         }
       }
     }
