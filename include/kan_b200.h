@@ -17,6 +17,7 @@
  *   kan_engine_forward          model_forward(model, inputs, opts)  eval.hpp:200-253
  *   kan_engine_forward_host     same, host buffers (H2D + D2H inside)
  *   kan_engine_predict          predict(model, inputs, opts)        eval.hpp:255-276
+ *   kan_engine_evaluate_accuracy  evaluate_accuracy(model, ds, opts) eval.hpp:279-287
  *   kan_engine_layer_levels     ActivationLattice::quantize(clamp)  lut.hpp:44-47
  *   kan_engine_layer_accumulators  the int32 form of the contraction behind
  *                               tabulated_kan_forward               lut.hpp:217-231
@@ -73,9 +74,14 @@ typedef enum {
   KAN_MODE_FP32 = 0,         /* fp32 Cox-de Boor basis + fp32 FFMA contraction */
   KAN_MODE_BF16 = 1,         /* fp32 basis -> bf16, tcgen05 kind::f16, fp32 accumulate */
   KAN_MODE_BSPLINE_LUT = 2,  /* lattice + quantized LUT, tcgen05 kind::i8, int32 accumulate */
-  KAN_MODE_SPLINE_TABLE = 3  /* per-connection spline tables, gather + integer add
+  KAN_MODE_SPLINE_TABLE = 3, /* per-connection spline tables, gather + integer add
                                 (spline_table.hpp:19-123); lut_k = input bits bits_a,
                                 lut_h = value bits h */
+  KAN_MODE_FAKE_QUANT = 4    /* EvalMode::kFakeQuant (eval.hpp:106-159): bits_w per-tensor
+                                weights, lut_k = bits_a (grid-bound activation quantizer),
+                                lut_h = bits_b (basis over [0,1]); 32 = passthrough.
+                                bits_a <= 8: exact fp64 per-connection fp32 tables, gather
+                                + fp32 add; bits_a = bits_b = 32: the fp32 Cox-de Boor path */
 } kan_mode;
 
 /* Weight quantization on the LUT path. */
@@ -136,6 +142,11 @@ kan_status kan_engine_forward_host(kan_engine* e, const float* x_host, int64_t b
 /* predict: argmax of the logits (first maximum wins, eval.hpp:268-272). */
 kan_status kan_engine_predict(kan_engine* e, const float* x_dev, int64_t batch,
                               int32_t* labels_dev, void* stream);
+
+/* evaluate_accuracy (eval.hpp:279-287): top-1 accuracy of predict against
+ * int32 labels [batch] on the device (0 for an empty batch). */
+kan_status kan_engine_evaluate_accuracy(kan_engine* e, const float* x_dev, const int32_t* labels_dev,
+                                        int64_t batch, double* accuracy, void* stream);
 
 /* Parity probes ------------------------------------------------------------ */
 /* Lattice levels of fp32 activations under layer `layer`'s grid and lut_k

@@ -661,3 +661,63 @@ int kor_spline_table_forward(const uint8_t* values, int n_in, int n_out, int bit
   free(acc);
   return 0;
 }
+
+/* ------------------------------------------------------------------------ */
+/* eval.hpp fake-quant mode (EvalMode::kFakeQuant)                           */
+/* ------------------------------------------------------------------------ */
+
+/* forward_linear in fake-quant mode (eval.hpp:135-159): W fake-quantized per
+ * tensor (maybe_fake_quant_weights, eval.hpp:70-76), activations fake-quantized
+ * on the grid bounds (a_params_for, eval.hpp:55-68; fake_quant, quant.hpp:65-68),
+ * then kan_linear_forward (clamp, layers.hpp:111) with RecursiveBasis or
+ * FakeQuantBasis over [0, 1] at bits_b (layers.hpp:85-94); 32 = passthrough. */
+int kor_fakequant_forward_fp64(const kor_grid* g, int bits_w, int bits_a, int bits_b, int64_t M,
+                               int n_in, int n_out, const double* acts, const double* coeffs,
+                               double* out) {
+  const int nb = g->intervals + g->degree;
+  const int64_t K = (int64_t)n_in * nb;
+  const size_t nw = (size_t)K * (size_t)n_out;
+  double* wq = (double*)malloc(sizeof(double) * (nw ? nw : 1));
+  if (bits_w == 32 || nw == 0) {
+    memcpy(wq, coeffs, sizeof(double) * nw);
+  } else {
+    uint8_t* q = (uint8_t*)malloc(nw);
+    double s;
+    int64_t z;
+    if (kor_wquant_per_tensor(coeffs, nw, bits_w, q, &s, &z)) {
+      free(q);
+      free(wq);
+      return -1;
+    }
+    for (size_t i = 0; i < nw; ++i) wq[i] = kor_dequantize(q[i], s, z);
+    free(q);
+  }
+  double as = 1.0, bs = 1.0;
+  int64_t az = 0, ahi = 0, bz = 0, bhi = 0;
+  if (bits_a != 32 && kor_quant_params(g->lo, g->hi, bits_a, &as, &az, &ahi)) {
+    free(wq);
+    return -1;
+  }
+  if (bits_b != 32 && kor_quant_params(0.0, 1.0, bits_b, &bs, &bz, &bhi)) {
+    free(wq);
+    return -1;
+  }
+  const int64_t blk = 64;
+  double* bmat = (double*)malloc(sizeof(double) * (size_t)(blk * K));
+  for (int64_t m0 = 0; m0 < M; m0 += blk) {
+    const int64_t rows = (M - m0) < blk ? (M - m0) : blk;
+    for (int64_t m = 0; m < rows; ++m)
+      for (int i = 0; i < n_in; ++i) {
+        double x = acts[(m0 + m) * n_in + i];
+        if (bits_a != 32) x = kor_dequantize(kor_quantize(x, as, az, 0, ahi), as, az);
+        double* row = bmat + m * K + (int64_t)i * nb;
+        kor_basis_at_coord(g, kor_knot_coord(g, kor_clamp(g, x)), row);
+        if (bits_b != 32)
+          for (int k = 0; k < nb; ++k) row[k] = kor_dequantize(kor_quantize(row[k], bs, bz, 0, bhi), bs, bz);
+      }
+    matmul_ref(rows, K, n_out, bmat, wq, out + m0 * n_out);
+  }
+  free(bmat);
+  free(wq);
+  return 0;
+}

@@ -153,6 +153,11 @@ int kor_spline_table_forward(const uint8_t* values, int n_in, int n_out, int bit
                              const double* qp_d, const int64_t* qp_i, int64_t M,
                              const double* acts, double* out);
 
+/* ---- eval.hpp fake-quant mode: one linear layer (bits 32 = passthrough) --- */
+int kor_fakequant_forward_fp64(const kor_grid* g, int bits_w, int bits_a, int bits_b, int64_t M,
+                               int n_in, int n_out, const double* acts, const double* coeffs,
+                               double* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -92,6 +92,8 @@ class Oracle:
         L.kor_requant_i8.argtypes = [C.c_double, C.c_double]
         L.kor_requant_i8.restype = C.c_int8
         L.kor_im2col.argtypes = [_dp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _dp]
+        L.kor_fakequant_forward_fp64.argtypes = [G, C.c_int, C.c_int, C.c_int, C.c_int64, C.c_int,
+                                                 C.c_int, _dp, _dp, _dp]
         L.kor_spline_tables_build.argtypes = [G, _dp, C.c_int, C.c_int, C.c_int, C.c_int, _u8p,
                                               _dp, _i64p]
         L.kor_spline_level.argtypes = [C.c_double, C.c_double, C.c_int64, C.c_int64]
@@ -309,6 +311,51 @@ class Oracle:
         t = np.stack(taps, axis=2)  # [M, C, KK, Ho, Wo]
         return np.ascontiguousarray(t.transpose(0, 3, 4, 1, 2)).reshape(M * Ho * Wo,
                                                                         Cc * kernel * kernel)
+
+    # -- fake-quant mode (eval.hpp:106-159) ----------------------------------------
+    def fakequant_forward(self, g, bits_w, bits_a, bits_b, acts, coeffs):
+        acts = np.ascontiguousarray(acts, dtype=np.float64)
+        coeffs = np.ascontiguousarray(coeffs, dtype=np.float64)
+        out = np.zeros((acts.shape[0], coeffs.shape[1]))
+        if self.lib.kor_fakequant_forward_fp64(C.byref(g), bits_w, bits_a, bits_b, acts.shape[0],
+                                               acts.shape[1], coeffs.shape[1], acts, coeffs, out):
+            raise ValueError("fake-quant: bad arguments")
+        return out
+
+    def fakequant_model_forward(self, desc, Ws, x, bits_w, bits_a, bits_b):
+        """model_forward in fake-quant mode over linear / conv / maxpool / flatten
+        (conv: im2col of the fake-quantized input, padded taps 0.0)."""
+        G, P = desc["grid"]["intervals"], desc["grid"]["degree"]
+        lo, hi = desc.get("domain", [-1.0, 1.0])
+        g = self.grid(G, P, lo, hi)
+        M = x.shape[0]
+        v = np.asarray(x, dtype=np.float64).reshape(M, *desc["input"])
+        ki = 0
+        for l in desc["layers"]:
+            typ = l["type"]
+            if typ == "linear":
+                v = self.fakequant_forward(g, bits_w, bits_a, bits_b, v.reshape(M, -1), Ws[ki])
+                ki += 1
+            elif typ == "conv":
+                kk, s_, p_ = l["kernel"], l.get("stride", 1), l.get("padding", 0)
+                Ho = (v.shape[2] + 2 * p_ - kk) // s_ + 1
+                Wo = (v.shape[3] + 2 * p_ - kk) // s_ + 1
+                vq = v
+                if bits_a != 32:  # forward_conv fake-quantizes the tensor, then im2col pads 0.0
+                    s, z, qh = self.quant_params(lo, hi, bits_a)
+                    vq = s * (np.clip(np.vectorize(lambda t: self.lib.kor_quantize(float(t), s, z, 0, qh),
+                                                   otypes=[np.int64])(v), 0, qh) - z)
+                cols = np.concatenate([self.im2col(vq[m], kk, s_, p_) for m in range(M)])
+                y = self.fakequant_forward(g, bits_w, 32, bits_b, cols, Ws[ki])
+                v = y.reshape(M, Ho, Wo, -1).transpose(0, 3, 1, 2)
+                ki += 1
+            elif typ == "maxpool":
+                w = l.get("window", 2)
+                Ho, Wo = v.shape[2] // w, v.shape[3] // w
+                v = v[:, :, :Ho * w, :Wo * w].reshape(M, v.shape[1], Ho, w, Wo, w).max(axis=(3, 5))
+            elif typ == "flatten":
+                v = v.reshape(M, -1)
+        return v
 
     # -- spline-table mode (spline_table.hpp) ------------------------------------
     def spline_tables(self, g, coeffs, n_in, n_out, bits_a, h):

@@ -284,7 +284,8 @@ int ref_validate_descriptor(const char* json_text) try {
 
 // model_forward / predict (eval.hpp:200-276) over a descriptor-built model
 // (io.hpp:357-386).  coeff_ptrs[i] = coefficients of the i-th KAN layer.
-// mode: 0 fp32 (EvalMode::kFp32), 2 bspline-lut (EvalMode::kBsplineLut),
+// mode: 0 fp32 (EvalMode::kFp32), 1 fake-quant (EvalMode::kFakeQuant; bits_w,
+// bits_a = k, bits_b = h), 2 bspline-lut (EvalMode::kBsplineLut),
 // 3 spline-table (EvalMode::kSplineTable; bits_a = k, value bits = h).
 // The batch is sharded over `threads` std::threads in chunks of `chunk`
 // rows (the forward is reentrant).
@@ -303,7 +304,7 @@ int ref_model_forward(const char* json_text, const double* const* coeff_ptrs, in
       ++li;
     }
   }
-  const BsplineLut lut = build_bspline_lut(model.grid().degree(), mode == 3 ? 8 : k, h);
+  const BsplineLut lut = build_bspline_lut(model.grid().degree(), mode == 2 ? k : 8, mode == 2 ? h : 8);
   // spline-table mode: one table set per KAN layer at (bits_a = k, h), as
   // run_sweep builds them (sweep.hpp:239-256)
   std::vector<SplineTableSet> tables;
@@ -315,8 +316,13 @@ int ref_model_forward(const char* json_text, const double* const* coeff_ptrs, in
         tables.push_back(build_spline_tables(*conv, k, h));
     }
   EvalOptions opts;
-  opts.mode = mode == 2 ? EvalMode::kBsplineLut : (mode == 3 ? EvalMode::kSplineTable : EvalMode::kFp32);
-  opts.qcfg.bits_w = mode == 2 ? bits_w : kPassthroughBits;
+  opts.mode = mode == 2 ? EvalMode::kBsplineLut
+                       : (mode == 3 ? EvalMode::kSplineTable : (mode == 1 ? EvalMode::kFakeQuant : EvalMode::kFp32));
+  opts.qcfg.bits_w = (mode == 2 || mode == 1) ? bits_w : kPassthroughBits;
+  if (mode == 1) {  // fake-quant: bits_a = k, bits_b = h (sweep.hpp:262-266), grid-bound ranges
+    opts.qcfg.bits_a = k;
+    opts.qcfg.bits_b = h;
+  }
   opts.lut = &lut;
   opts.tables = &tables;
   if (threads < 1) threads = 1;

@@ -67,6 +67,8 @@ size_t st_layer_smem(const StParams& p);
 cudaError_t launch_st_levels(const float* x, int64_t n, const float* thr, float inv_s, float zf, int qhi,
                              void* out, int out_u16, cudaStream_t st);
 cudaError_t launch_u16_to_u8(const uint16_t* in, int64_t n, uint8_t* out, cudaStream_t st);
+cudaError_t launch_count_equal(const int32_t* a, const int32_t* b, int64_t n, unsigned long long* count,
+                               cudaStream_t st);
 cudaError_t launch_st_maxpool(const uint8_t* in, int64_t planes, int H, int W, int win, uint8_t* out,
                               cudaStream_t st);
 
@@ -165,6 +167,7 @@ struct StLayer {
   int bits_a = 0, h = 0;
   double in_s = 1.0, out_s = 1.0;
   int64_t in_z = 0, in_qhi = 0, out_z = 0, out_qhi = 0;
+  bool ft = false;  // fake-quant mode: fp32 tables, Np = row bytes (4 per column)
 };
 
 // Device-side state of one configured KAN layer.
@@ -295,6 +298,8 @@ struct kan_engine {
   DevBuf<float> st_thr;     // its exact fp32 thresholds
   DevBuf<uint8_t> st_xlev;  // u8 levels of an image model input
   DevBuf<uint8_t> st_probe;
+  DevBuf<int32_t> pred_tmp;
+  DevBuf<unsigned long long> count_tmp;
   DevBuf<uint8_t> io_in, io_out;
   int last_launches = 0;
   // optional per-CTA phase timestamps of each layer's last launch (tuning aid)
@@ -953,7 +958,7 @@ static double key_to_double(unsigned long long k) {
 }
 
 static void st_geometry(StLayer& sl) {
-  sl.Np = (sl.n_out + 15) / 16 * 16;
+  sl.Np = sl.ft ? (sl.n_out + 3) / 4 * 16 : (sl.n_out + 15) / 16 * 16;  // bytes; 16 per lane
   const int lanes = sl.Np / 16;
   int lpr = 1;
   while (lpr < lanes && lpr < 32) lpr *= 2;
@@ -1048,6 +1053,86 @@ static void st_sum_thresholds(const kan_engine* e, StLayer& sl) {
   sl.vthr.upload(vt);
 }
 
+// Fake-quant mode (EvalMode::kFakeQuant, eval.hpp:106-159).  With quantized
+// activations (bits_a <= 8) every input takes one of 2^bits_a values, so each
+// connection's activation phi_{i,j}(level) = sum_k fq_b(basis(clamp(dequant(level))))[k]
+// * fq_w(W)[i*nb+k, j] is tabulated exactly in fp64 (the reference's k order)
+// and rounded once to fp32; the forward gathers and adds the fp32 entries.
+// Weights: per-tensor fake quantization (maybe_fake_quant_weights, eval.hpp:70-76).
+static std::vector<double> fake_quant_weights(const std::vector<double>& w, int bits) {
+  if (bits == 32 || w.empty()) return w;
+  double lo = w[0], hi = w[0];
+  for (double v : w) {  // RangeCalibrator::observe
+    lo = (v < lo) ? v : lo;
+    hi = (hi < v) ? v : hi;
+  }
+  if (lo == hi) {
+    const double pad = std::max(std::abs(lo), 1.0) * std::numeric_limits<double>::epsilon() * 4.0;
+    lo -= pad;
+    hi += pad;
+  }
+  const QParams q = quant_params(std::min(lo, 0.0), std::max(hi, 0.0), bits);
+  std::vector<double> out(w.size());
+  for (size_t i = 0; i < w.size(); ++i) out[i] = q.scale * static_cast<double>(quantize(w[i], q) - q.zp);
+  return out;
+}
+
+void configure_fq(kan_engine* e, const kan_config& cfg) {
+  const int bits_w = cfg.bits_w, bits_a = cfg.lut_k, bits_b = cfg.lut_h;
+  for (int b : {bits_w, bits_a, bits_b})
+    if (b != 32 && (b < 1 || b > 8)) throw InvalidArgument("compute_quant_params: bits must be in [1,8] or 32");
+  if (cfg.out_kind != KAN_OUT_F32) throw InvalidArgument("int8 outputs are only produced on the LUT path");
+  if (cfg.silu_base) throw InvalidArgument("fake-quant mode has no SiLU base term");
+  if (e->grid.nb() > 32) throw Unsupported("fake-quant mode supports G+P <= 32");
+  for (const auto& l : e->layers)
+    if (l.res_src != -2 || l.type == L_AVGPOOL)
+      throw Unsupported("fake-quant mode runs the reference layer set (linear, conv, maxpool, flatten)");
+  if (bits_a == 32)
+    throw Unsupported("fake-quant mode with passthrough activations: use bits_a <= 8 (tabulated) or mode fp32");
+  const Grid& g = e->grid;
+  e->st_in = quant_params(g.lo, g.hi, bits_a);  // a_params_for, eval.hpp:55-68 (grid bounds)
+  e->st_thr.upload(quant_thresholds(e->st_in));
+  const int64_t Lv = int64_t{1} << bits_a;
+  const int nb = g.nb();
+  // fake-quantized basis at every activation level: basis(clamp(dequant(m)))
+  // (kan_linear_forward clamps, layers.hpp:111), then FakeQuantBasis at bits_b
+  std::vector<double> basis(static_cast<size_t>(Lv * nb));
+  const QParams bq = bits_b == 32 ? QParams{} : quant_params(0.0, 1.0, bits_b);
+  for (int64_t m = 0; m < Lv; ++m) {
+    const double x = g.clamp(e->st_in.scale * static_cast<double>(m - e->st_in.zp));
+    double* row = &basis[static_cast<size_t>(m * nb)];
+    g.basis_at_coord(g.knot_coord(x), row);
+    if (bits_b != 32)
+      for (int k = 0; k < nb; ++k) row[k] = bq.scale * static_cast<double>(quantize(row[k], bq) - bq.zp);
+  }
+  DevBuf<double> d_basis;
+  d_basis.upload(basis);
+  e->st.clear();
+  e->st.resize(static_cast<size_t>(e->n_kan));
+  for (const auto& l : e->layers) {
+    if (l.type != L_LINEAR && l.type != L_CONV) continue;
+    StLayer& sl = e->st[static_cast<size_t>(l.kan_index)];
+    sl.ft = true;
+    sl.n_in = l.type == L_LINEAR ? l.n_in : l.kernel * l.kernel * l.c_in;
+    sl.n_out = l.type == L_LINEAR ? l.n_out : l.c_out;
+    sl.bits_a = bits_a;
+    sl.h = bits_b;
+    sl.in_s = e->st_in.scale;
+    sl.in_z = e->st_in.zp;
+    sl.in_qhi = e->st_in.qhi;
+    st_geometry(sl);
+    if (l.coeffs.size() != static_cast<size_t>(sl.n_in) * nb * sl.n_out)
+      throw InvalidArgument("coefficients of KAN layer " + std::to_string(l.kan_index) + " not set");
+    DevBuf<double> d_coeffs;
+    d_coeffs.upload(fake_quant_weights(l.coeffs, bits_w));
+    sl.T.alloc(static_cast<size_t>((sl.n_in + 3) / 4 * 4) * static_cast<size_t>(Lv) * sl.Np, true);
+    ck(launch_st_sample(d_basis.p, d_coeffs.p, sl.n_in, sl.n_out, nb, static_cast<int>(Lv), 2, nullptr, sl.T.p,
+                        sl.Np, 1.0, 0.0, 0, nullptr),
+       "fake-quant table build");
+    ck(cudaDeviceSynchronize(), "fake-quant table build");
+  }
+}
+
 void configure_st(kan_engine* e, const kan_config& cfg) {
   const int bits_a = cfg.lut_k, h = cfg.lut_h;
   // argument checks in build_tables order (spline_table.hpp:40-43)
@@ -1121,6 +1206,7 @@ static StParams st_params(const kan_engine* e, const StLayer& sl, int64_t rows =
   p.in_qhi = e->st_in.qhi;
   p.vthr = sl.vthr.p;
   p.ratio_f = static_cast<float>(sl.out_s / e->st_in.scale);
+  p.ft = sl.ft ? 1 : 0;
   return p;
 }
 
@@ -1192,7 +1278,7 @@ void forward_st(kan_engine* e, const float* x, int64_t M, void* out, cudaStream_
     // a small last layer reading only this dense layer's levels runs fused:
     // one warp per row, the hidden levels never leave shared memory
     bool fused = false;
-    if (!conv && i + 2 == nl && sl.col_tiles == 1 && sl.n_out <= 512) {
+    if (!sl.ft && !conv && i + 2 == nl && sl.col_tiles == 1 && sl.n_out <= 512) {
       const Layer& nx = e->layers[static_cast<size_t>(i + 1)];
       if (nx.type == L_LINEAR && nx.src == i) {
         const StLayer& sn = e->st[static_cast<size_t>(nx.kan_index)];
@@ -1268,7 +1354,7 @@ void configure(kan_engine* e, const kan_config* c) {
   DeviceGuard dg(e->device);
   const kan_config cfg = *c;
   if (cfg.mode != KAN_MODE_FP32 && cfg.mode != KAN_MODE_BF16 && cfg.mode != KAN_MODE_BSPLINE_LUT &&
-      cfg.mode != KAN_MODE_SPLINE_TABLE)
+      cfg.mode != KAN_MODE_SPLINE_TABLE && cfg.mode != KAN_MODE_FAKE_QUANT)
     throw InvalidArgument("unknown evaluation mode");
   e->cfg = cfg;
   e->configured = false;
@@ -1284,9 +1370,33 @@ void configure(kan_engine* e, const kan_config* c) {
   if (lastl.type == L_CONV && cfg.out_kind == KAN_OUT_I8)
     throw InvalidArgument("int8 outputs are produced by linear output layers only");
   plan_buffers(e);
-  if (cfg.mode == KAN_MODE_SPLINE_TABLE) {
+  if (cfg.mode == KAN_MODE_FAKE_QUANT && cfg.lut_k == 32 && cfg.lut_h == 32) {
+    // weights-only fake quantization: the fp32 Cox-de Boor path on the
+    // fake-quantized coefficients (forward_linear with RecursiveBasis, eval.hpp:144-146)
+    if (cfg.bits_w != 32 && (cfg.bits_w < 1 || cfg.bits_w > 8))
+      throw InvalidArgument("compute_quant_params: bits must be in [1,8] or 32");
+    std::vector<std::vector<double>> keep;
+    for (auto& l : e->layers) {
+      keep.push_back(l.coeffs);
+      l.coeffs = fake_quant_weights(l.coeffs, cfg.bits_w);
+    }
+    kan_config c2 = cfg;
+    c2.mode = KAN_MODE_FP32;
+    try {
+      configure(e, &c2);
+    } catch (...) {
+      for (size_t i = 0; i < e->layers.size(); ++i) e->layers[i].coeffs = std::move(keep[i]);
+      throw;
+    }
+    for (size_t i = 0; i < e->layers.size(); ++i) e->layers[i].coeffs = std::move(keep[i]);
+    return;
+  }
+  if (cfg.mode == KAN_MODE_SPLINE_TABLE || cfg.mode == KAN_MODE_FAKE_QUANT) {
     e->prep.clear();
-    configure_st(e, cfg);
+    if (cfg.mode == KAN_MODE_SPLINE_TABLE)
+      configure_st(e, cfg);
+    else
+      configure_fq(e, cfg);
     e->configured = true;
     return;
   }
@@ -1838,7 +1948,7 @@ void forward(kan_engine* e, const float* x, int64_t M, void* out, cudaStream_t s
   DeviceGuard dg(e->device);
   e->last_launches = 0;
   if (M == 0) return;
-  if (e->cfg.mode == KAN_MODE_SPLINE_TABLE) {
+  if (e->cfg.mode == KAN_MODE_SPLINE_TABLE || e->cfg.mode == KAN_MODE_FAKE_QUANT) {
     forward_st(e, x, M, out, st);
     return;
   }
@@ -2237,17 +2347,42 @@ kan_status kan_engine_predict(kan_engine* e, const float* x_dev, int64_t batch,
   });
 }
 
+kan_status kan_engine_evaluate_accuracy(kan_engine* e, const float* x_dev, const int32_t* labels_dev,
+                                        int64_t batch, double* accuracy, void* stream) {
+  if (!e || !accuracy) return KAN_ERR_INVALID_ARGUMENT;
+  return guarded(e, [&] {
+    if (batch < 0) throw InvalidArgument("evaluate_accuracy: negative batch");
+    *accuracy = 0.0;  // an empty dataset scores 0 (eval.hpp:281)
+    if (batch == 0) return;
+    if (!x_dev || !labels_dev) throw InvalidArgument("evaluate_accuracy: null buffer");
+    DeviceGuard dg(e->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    e->pred_tmp.alloc(static_cast<size_t>(batch));
+    const kan_status ps = kan_engine_predict(e, x_dev, batch, e->pred_tmp.p, stream);
+    if (ps != KAN_OK) throw CudaError(e->err);
+    const int launches = e->last_launches;
+    e->count_tmp.alloc(1);
+    ck(launch_count_equal(e->pred_tmp.p, labels_dev, batch, e->count_tmp.p, st), "count launch");
+    unsigned long long c = 0;
+    ck(cudaMemcpyAsync(&c, e->count_tmp.p, sizeof(c), cudaMemcpyDeviceToHost, st), "D2H");
+    ck(cudaStreamSynchronize(st), "stream sync");
+    e->last_launches = launches + 1;
+    *accuracy = static_cast<double>(c) / static_cast<double>(batch);
+  });
+}
+
 kan_status kan_engine_layer_levels(kan_engine* e, int layer, const float* x_dev, int64_t n,
                                    uint16_t* levels_dev, void* stream) {
   if (!e) return KAN_ERR_INVALID_ARGUMENT;
   return guarded(e, [&] {
-    if (!e->configured || (e->cfg.mode != KAN_MODE_BSPLINE_LUT && e->cfg.mode != KAN_MODE_SPLINE_TABLE))
+    if (!e->configured || (e->cfg.mode != KAN_MODE_BSPLINE_LUT && e->cfg.mode != KAN_MODE_SPLINE_TABLE &&
+                           e->cfg.mode != KAN_MODE_FAKE_QUANT))
       throw LogicError("layer_levels: engine not configured for bspline-lut");
     (void)e->kan_layer(layer);  // one grid per model (Model::grid, layers.hpp:224-230)
     DeviceGuard dg(e->device);
     e->last_launches = 0;
     if (n == 0) return;
-    if (e->cfg.mode == KAN_MODE_SPLINE_TABLE) {
+    if (e->cfg.mode == KAN_MODE_SPLINE_TABLE || e->cfg.mode == KAN_MODE_FAKE_QUANT) {
       ck(launch_st_levels(x_dev, n, e->st_thr.p, static_cast<float>(1.0 / e->st_in.scale),
                           static_cast<float>(e->st_in.zp), static_cast<int>(e->st_in.qhi), levels_dev, 1,
                           static_cast<cudaStream_t>(stream)),

@@ -158,6 +158,7 @@ struct StParams {
   int n_in, n_out, Np, Lv;
   int lpr, col_tiles, ic;  // lanes per row (16 columns each), column tiles, staged inputs per chunk
   int slices;              // input slices per row (partial sums meet in smem)
+  int ft;                  // fp32 tables (fake-quant mode): Np is the row size in bytes
   const uint8_t* T;        // [roundup4(n_in)][Lv][Np]; padded inputs are all-zero slices
   // input: dense rows [rows][ld_x] (u8 levels or fp32 values), or conv u8 NCHW
   int in_kind;

@@ -28,6 +28,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "kan_internal.h"
 #include "kan_ptx.cuh"
@@ -43,6 +44,7 @@ __device__ __forceinline__ unsigned long long dkey(double v) {
 // Samples of phi_{i,j} at every input level, thread per (i, j).
 //   pass 0: min/max fold into mm[0] (min key) / mm[1] (max key)
 //   pass 1: T[(i*Lv + m)*Np + j] = clamp(llround(v / s + z), 0, qhi)
+//   pass 2: fp32 T[(i*Lv + m)*(Np/4) + j] = v (fake-quant float tables; Np in bytes)
 template <int NBMAX>
 __global__ void __launch_bounds__(256) st_sample_kernel(const double* __restrict__ basis,
                                                         const double* __restrict__ coeffs, int n_in,
@@ -72,6 +74,8 @@ __global__ void __launch_bounds__(256) st_sample_kernel(const double* __restrict
           kmin = key < kmin ? key : kmin;
           kmax = key > kmax ? key : kmax;
         }
+      } else if (pass == 2) {  // fake-quant float tables: the fp64 sample rounded once
+        reinterpret_cast<float*>(T)[(static_cast<int64_t>(i) * Lv + m) * (Np / 4) + j] = __double2float_rn(acc);
       } else {
         long long q = llround(__dadd_rn(__ddiv_rn(acc, s), zd));
         q = q < 0 ? 0 : (q > qhi ? qhi : q);
@@ -143,6 +147,19 @@ struct Acc16 {
     }
     clear_pk();
   }
+};
+
+// fake-quant float tables: a lane's 16-byte row slice is 4 fp32 columns
+struct AccF {
+  float a[4];
+  __device__ __forceinline__ void clear_pk() {}
+  __device__ __forceinline__ void add(const uint4 w) {
+    a[0] += __uint_as_float(w.x);
+    a[1] += __uint_as_float(w.y);
+    a[2] += __uint_as_float(w.z);
+    a[3] += __uint_as_float(w.w);
+  }
+  __device__ __forceinline__ void flush() {}
 };
 
 // L2 eviction-priority policies: the tables are re-read by every row and
@@ -252,6 +269,27 @@ __device__ __forceinline__ void st_epilogue(const StParams& p, int64_t r, int c0
   }
 }
 
+// Epilogue of one row's 4 fp32 columns (fake-quant float tables): fp32 values,
+// or the next layer's input level of the value (exact fp32 thresholds)
+__device__ __forceinline__ void st_epilogue_f(const StParams& p, int64_t r, int col0, const float (&a)[4]) {
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const int j = col0 + t;
+    if (j >= p.n_out) break;
+    int64_t o;
+    if (p.conv) {
+      const int64_t hw = static_cast<int64_t>(p.Ho) * p.Wo;
+      o = ((r / hw) * p.n_out + j) * hw + r % hw;
+    } else {
+      o = r * p.ld_out + j;
+    }
+    if (p.epi == EPI_LEVEL)
+      static_cast<uint8_t*>(p.out)[o] = static_cast<uint8_t>(st_level_f32(a[t], p.thr, p.inv_s, p.zf, static_cast<int>(p.in_qhi)));
+    else
+      static_cast<float*>(p.out)[o] = a[t];
+  }
+}
+
 // One spline-table layer.  A CTA of 256 threads runs RP rows at a time; each
 // row is split over S input slices x lpr lanes (16 columns each, column tile
 // blockIdx.y), so even a few thousand rows fill the GPU with independent
@@ -319,7 +357,10 @@ __device__ __forceinline__ uint32_t st_quad_levels(const StParams& p, float4 f, 
   return w;
 }
 
-template <int LPR, int KIND>  // KIND: 0 dense u8 levels, 1 dense fp32 values, 2 conv u8 NCHW
+// KIND: 0 dense u8 levels, 1 dense fp32 values, 2 conv u8 NCHW.  FT: fp32
+// tables (fake-quant mode): a lane's 16-byte slice is 4 fp32 columns summed in
+// fp32, no output quantizer.
+template <int LPR, int KIND, bool FT>
 __global__ void __launch_bounds__(256, 3) kan_st_layer_kernel(const StParams p) {
   extern __shared__ __align__(16) uint8_t st_smem[];
   pdl_trigger();
@@ -343,10 +384,11 @@ __global__ void __launch_bounds__(256, 3) kan_st_layer_kernel(const StParams p) 
   for (int64_t rb = blockIdx.x; rb * RP < p.rows; rb += gridDim.x) {
     const int64_t r = rb * RP + g;
     const bool row_ok = r < p.rows;
-    Acc16 acc;
+    constexpr int NC = FT ? 4 : 16;  // columns per lane
+    std::conditional_t<FT, AccF, Acc16> acc;
     acc.clear_pk();
 #pragma unroll
-    for (int t = 0; t < 16; ++t) acc.a[t] = 0;
+    for (int t = 0; t < NC; ++t) acc.a[t] = 0;
     if constexpr (KIND != 2) {
       if (row_ok) {  // group-uniform: the lpr lanes of a (row, slice) share the trip count
         constexpr int esz = F32 ? 4 : 1;
@@ -454,25 +496,33 @@ __global__ void __launch_bounds__(256, 3) kan_st_layer_kernel(const StParams p) 
       for (int o = 16; o >= 1; o >>= 1)
         if (o >= lpr && o < span)
 #pragma unroll
-          for (int t = 0; t < 16; ++t) acc.a[t] += __shfl_xor_sync(0xffffffffu, acc.a[t], o);
+          for (int t = 0; t < NC; ++t) acc.a[t] += __shfl_xor_sync(0xffffffffu, acc.a[t], o);
       if (lpr * S > 32) {
         const int wpr = lpr * S / 32;  // warps per row
         __syncthreads();
         if (lane < lpr) {
 #pragma unroll
-          for (int t = 0; t < 16; ++t) red[((threadIdx.x >> 5) * 32 + lane) * 16 + ((t + lane) & 15)] = acc.a[t];
+          for (int t = 0; t < NC; ++t)
+            red[((threadIdx.x >> 5) * 32 + lane) * 16 + ((t + lane) & 15)] =
+                (FT ? __float_as_int(static_cast<float>(acc.a[t])) : static_cast<int>(acc.a[t]));
         }
         __syncthreads();
         if (s == 0) {
           for (int o = 1; o < wpr; ++o) {
             const int src = ((threadIdx.x >> 5) + o) * 32 + lane;
 #pragma unroll
-            for (int t = 0; t < 16; ++t) acc.a[t] += red[src * 16 + ((t + lane) & 15)];
+            for (int t = 0; t < NC; ++t) {
+              const int bits = red[src * 16 + ((t + lane) & 15)];
+              if constexpr (FT)
+                acc.a[t] += __int_as_float(bits);
+              else
+                acc.a[t] += bits;
+            }
           }
         }
       }
     }
-    if constexpr (KIND != 2) {
+    if constexpr (KIND != 2 && !FT) {
       if (p.f_on) {  // fused output layer: the row's first warp (lpr * S >= 32) runs it
         if ((threadIdx.x % (lpr * S)) >= 32) continue;  // warp-uniform
         uint8_t* hid = st_smem + 256 * 16 * 4 + 258 * 4 + g * 512;
@@ -505,7 +555,12 @@ __global__ void __launch_bounds__(256, 3) kan_st_layer_kernel(const StParams p) 
         continue;
       }
     }
-    if (s == 0 && row_ok && col_ok) st_epilogue(p, r, c0, acc.a);
+    if (s == 0 && row_ok && col_ok) {
+      if constexpr (FT)
+        st_epilogue_f(p, r, c0 / 4, acc.a);
+      else
+        st_epilogue(p, r, c0, acc.a);
+    }
   }
 }
 
@@ -558,6 +613,19 @@ __global__ void __launch_bounds__(256) kan_st_maxpool_kernel(const uint8_t* __re
       }
     out[t] = m;
   }
+}
+
+// evaluate_accuracy (eval.hpp:279-287): number of rows whose prediction equals the label
+__global__ void __launch_bounds__(256) kan_count_equal_kernel(const int32_t* __restrict__ a,
+                                                              const int32_t* __restrict__ b, int64_t n,
+                                                              unsigned long long* count) {
+  unsigned long long c = 0;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    c += a[i] == b[i] ? 1ull : 0ull;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
 }
 
 // ---------------------------------------------------------------------------
@@ -618,9 +686,9 @@ size_t st_layer_smem(const StParams& p) {
   return 256 * 16 * sizeof(int) + 258 * sizeof(float) + (p.f_on ? 8 * 512 : 0);
 }
 
-template <int LPR, int KIND>
+template <int LPR, int KIND, bool FT>
 static cudaError_t launch_st_layer_t(const StParams& p, dim3 grid, size_t smem, cudaStream_t st) {
-  auto kfn = kan_st_layer_kernel<LPR, KIND>;
+  auto kfn = kan_st_layer_kernel<LPR, KIND, FT>;
   static size_t configured = 0;
   if (smem > configured) {
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
@@ -630,17 +698,23 @@ static cudaError_t launch_st_layer_t(const StParams& p, dim3 grid, size_t smem, 
   return st_launch(kfn, grid, dim3(256), smem, st, p);
 }
 
-template <int KIND>
+template <int KIND, bool FT>
 static cudaError_t launch_st_kind(const StParams& p, dim3 grid, size_t smem, cudaStream_t st) {
   switch (p.lpr) {
-    case 1: return launch_st_layer_t<1, KIND>(p, grid, smem, st);
-    case 2: return launch_st_layer_t<2, KIND>(p, grid, smem, st);
-    case 4: return launch_st_layer_t<4, KIND>(p, grid, smem, st);
-    case 8: return launch_st_layer_t<8, KIND>(p, grid, smem, st);
-    case 16: return launch_st_layer_t<16, KIND>(p, grid, smem, st);
-    case 32: return launch_st_layer_t<32, KIND>(p, grid, smem, st);
+    case 1: return launch_st_layer_t<1, KIND, FT>(p, grid, smem, st);
+    case 2: return launch_st_layer_t<2, KIND, FT>(p, grid, smem, st);
+    case 4: return launch_st_layer_t<4, KIND, FT>(p, grid, smem, st);
+    case 8: return launch_st_layer_t<8, KIND, FT>(p, grid, smem, st);
+    case 16: return launch_st_layer_t<16, KIND, FT>(p, grid, smem, st);
+    case 32: return launch_st_layer_t<32, KIND, FT>(p, grid, smem, st);
     default: return cudaErrorInvalidValue;
   }
+}
+
+template <bool FT>
+static cudaError_t launch_st_ft(const StParams& p, dim3 grid, size_t smem, cudaStream_t st) {
+  if (p.conv) return launch_st_kind<2, FT>(p, grid, smem, st);
+  return p.in_kind == ST_IN_F32 ? launch_st_kind<1, FT>(p, grid, smem, st) : launch_st_kind<0, FT>(p, grid, smem, st);
 }
 
 cudaError_t launch_st_layer(const StParams& p, cudaStream_t st) {
@@ -650,8 +724,7 @@ cudaError_t launch_st_layer(const StParams& p, cudaStream_t st) {
   const int64_t blocks = (p.rows + RP - 1) / RP;
   const int64_t cap = static_cast<int64_t>(st_sm_count()) * 8;
   const dim3 grid(static_cast<unsigned>(blocks < cap ? blocks : cap), static_cast<unsigned>(p.col_tiles));
-  if (p.conv) return launch_st_kind<2>(p, grid, smem, st);
-  return p.in_kind == ST_IN_F32 ? launch_st_kind<1>(p, grid, smem, st) : launch_st_kind<0>(p, grid, smem, st);
+  return p.ft ? launch_st_ft<true>(p, grid, smem, st) : launch_st_ft<false>(p, grid, smem, st);
 }
 
 cudaError_t launch_st_levels(const float* x, int64_t n, const float* thr, float inv_s, float zf, int qhi,
@@ -661,6 +734,15 @@ cudaError_t launch_st_levels(const float* x, int64_t n, const float* thr, float 
   const int64_t cap = static_cast<int64_t>(st_sm_count()) * 16;
   return st_launch(kan_st_levels_kernel, dim3(static_cast<unsigned>(blocks < cap ? blocks : cap)), dim3(256), 0,
                    st, x, n, thr, inv_s, zf, qhi, out, out_u16);
+}
+
+cudaError_t launch_count_equal(const int32_t* a, const int32_t* b, int64_t n, unsigned long long* count,
+                               cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(count, 0, sizeof(unsigned long long), st);
+  if (e != cudaSuccess || n == 0) return e;
+  const int64_t blocks = (n + 255) / 256;
+  kan_count_equal_kernel<<<static_cast<unsigned>(blocks < 1184 ? blocks : 1184), 256, 0, st>>>(a, b, n, count);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_u16_to_u8(const uint16_t* in, int64_t n, uint8_t* out, cudaStream_t st) {

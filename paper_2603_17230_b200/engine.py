@@ -46,7 +46,7 @@ STATUS_NAMES = {0: "OK", 1: "INVALID_ARGUMENT", 2: "SHAPE_MISMATCH", 3: "OUT_OF_
                 4: "CUDA", 5: "NCCL", 6: "IO", 7: "FORMAT", 8: "CHECKSUM", 9: "UNSUPPORTED",
                 10: "LOGIC"}
 
-MODE_FP32, MODE_BF16, MODE_BSPLINE_LUT, MODE_SPLINE_TABLE = 0, 1, 2, 3
+MODE_FP32, MODE_BF16, MODE_BSPLINE_LUT, MODE_SPLINE_TABLE, MODE_FAKE_QUANT = 0, 1, 2, 3, 4
 W_PER_TENSOR_ASYM, W_PER_CHANNEL_SYM = 0, 1
 OUT_F32, OUT_I8 = 0, 1
 PASSTHROUGH_BITS = 32  # quant.hpp:15
@@ -79,6 +79,7 @@ _lib.kan_engine_configure.argtypes = [_vp, C.POINTER(_Config)]
 _lib.kan_engine_forward.argtypes = [_vp, _vp, C.c_int64, _vp, _vp]
 _lib.kan_engine_forward_host.argtypes = [_vp, _vp, C.c_int64, _vp, _vp]
 _lib.kan_engine_predict.argtypes = [_vp, _vp, C.c_int64, _vp, _vp]
+_lib.kan_engine_evaluate_accuracy.argtypes = [_vp, _vp, _vp, C.c_int64, C.POINTER(C.c_double), _vp]
 _lib.kan_engine_layer_levels.argtypes = [_vp, C.c_int, _vp, C.c_int64, _vp, _vp]
 _lib.kan_engine_layer_accumulators.argtypes = [_vp, C.c_int, _vp, C.c_int64, _vp, _vp, _vp]
 _lib.kan_engine_lut.argtypes = [_vp, _vp, C.c_int64]
@@ -136,6 +137,7 @@ EXPORTED = [
     "kan_container_descriptor", "kan_container_num_kan_layers", "kan_container_coeffs",
     "kan_container_lut", "kan_container_num_spline_tables", "kan_container_spline_table",
     "kan_container_save", "kan_container_save_error", "kan_crc32", "kan_engine_load",
+    "kan_engine_evaluate_accuracy",
 ]
 
 
@@ -232,7 +234,7 @@ def save_container(path: str, descriptor, coeffs, lut=None, spline_tables=None):
 def eval_mode_from_string(s: str) -> int:
     """eval.hpp:19-25, plus the engine's bf16 datapath."""
     table = {"fp32": MODE_FP32, "bf16": MODE_BF16, "bspline-lut": MODE_BSPLINE_LUT,
-             "spline-table": MODE_SPLINE_TABLE}
+             "spline-table": MODE_SPLINE_TABLE, "fake-quant": MODE_FAKE_QUANT}
     if s not in table:
         raise ValueError(f"unknown evaluation mode '{s}'")
     return table[s]
@@ -253,7 +255,8 @@ class EvalOptions:
     """EvalOptions (eval.hpp:37-45) extended with the engine's choices.
 
     spline-table mode reads lut_k as the tables' input bits (bits_a) and lut_h as
-    their value bits (h), as run_sweep passes (bits_a, bits_b) (sweep.hpp:247-253)."""
+    their value bits (h), as run_sweep passes (bits_a, bits_b) (sweep.hpp:247-253);
+    fake-quant mode reads bits_w, lut_k = bits_a and lut_h = bits_b (32 = passthrough)."""
     mode: str = "fp32"
     lut_k: int = 8
     lut_h: int = 8
@@ -395,6 +398,15 @@ class Engine:
         self._check(_lib.kan_engine_predict(self._h, x.data_ptr(), x.shape[0],
                                             labels.data_ptr(), self._stream(stream)))
         return labels
+
+    def evaluate_accuracy(self, x, labels, stream=None) -> float:
+        """evaluate_accuracy (eval.hpp:279-287): top-1 accuracy against int32 labels."""
+        torch = _torch()
+        lab = labels.to(device=x.device, dtype=torch.int32).contiguous()
+        acc = C.c_double()
+        self._check(_lib.kan_engine_evaluate_accuracy(self._h, x.data_ptr(), lab.data_ptr(), x.shape[0],
+                                                      C.byref(acc), self._stream(stream)))
+        return acc.value
 
     # -- parity probes ---------------------------------------------------------------
     def layer_levels(self, layer: int, x, stream=None):
