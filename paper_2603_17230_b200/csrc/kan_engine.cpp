@@ -296,7 +296,8 @@ struct kan_engine {
   std::vector<StLayer> st;
   QParams st_in;            // input quantizer on the grid bounds (spline_table.hpp:51)
   DevBuf<float> st_thr;     // its exact fp32 thresholds
-  DevBuf<uint8_t> st_xlev;  // u8 levels of an image model input
+  DevBuf<uint8_t> st_xlev;  // u8 levels of the model input (image models; dense prepass)
+  bool st_prepass = true;   // KAN_ST_PREPASS=0: quantize fp32 rows inside the gather kernel
   DevBuf<uint8_t> st_probe;
   DevBuf<int32_t> pred_tmp;
   DevBuf<unsigned long long> count_tmp;
@@ -1090,6 +1091,7 @@ void configure_fq(kan_engine* e, const kan_config& cfg) {
   if (bits_a == 32)
     throw Unsupported("fake-quant mode with passthrough activations: use bits_a <= 8 (tabulated) or mode fp32");
   const Grid& g = e->grid;
+  e->st_prepass = !(std::getenv("KAN_ST_PREPASS") && std::atoi(std::getenv("KAN_ST_PREPASS")) == 0);
   e->st_in = quant_params(g.lo, g.hi, bits_a);  // a_params_for, eval.hpp:55-68 (grid bounds)
   e->st_thr.upload(quant_thresholds(e->st_in));
   const int64_t Lv = int64_t{1} << bits_a;
@@ -1145,6 +1147,7 @@ void configure_st(kan_engine* e, const kan_config& cfg) {
     if (l.res_src != -2 || l.type == L_AVGPOOL)
       throw Unsupported("spline-table mode runs the reference layer set (linear, conv, maxpool, flatten)");
   }
+  e->st_prepass = !(std::getenv("KAN_ST_PREPASS") && std::atoi(std::getenv("KAN_ST_PREPASS")) == 0);
   e->st_in = quant_params(e->grid.lo, e->grid.hi, bits_a);  // spline_table.hpp:51
   e->st_thr.upload(quant_thresholds(e->st_in));
   e->st.clear();
@@ -1175,7 +1178,7 @@ void configure_st(kan_engine* e, const kan_config& cfg) {
 }
 
 // Launch geometry of one spline-table launch over `rows` rows: input slices
-// per row until the grid has ~3 CTAs per SM (or a slice would own fewer than
+// per row until the grid has ~1.5 CTAs per SM (measured best on C1/C2 shapes; or a slice would own fewer than
 // one 4-input quad / channel), then the staged-level chunk that fits 32 KB.
 static StParams st_params(const kan_engine* e, const StLayer& sl, int64_t rows = 0, int conv_c = 0) {
   StParams p{};
@@ -1188,7 +1191,11 @@ static StParams st_params(const kan_engine* e, const StLayer& sl, int64_t rows =
   const int units = conv_c > 0 ? conv_c : (sl.n_in + 3) / 4;  // what slices split
   int S = 1;
   auto blocks = [&](int s_) { return (rows + 256 / (sl.lpr * s_) - 1) / (256 / (sl.lpr * s_)) * sl.col_tiles; };
-  while (S * sl.lpr < 256 && 2 * S <= units && blocks(S) < 148 * 3) S *= 2;
+  while (S * sl.lpr < 256 && 2 * S <= units && blocks(S) < 148 * 3 / 2) S *= 2;
+  if (const char* ev = std::getenv("KAN_ST_SLICES")) {  // tuning only
+    const int want = std::atoi(ev);
+    if (want >= 1 && (want & (want - 1)) == 0 && want * sl.lpr <= 256) S = want;
+  }
   p.slices = S;
   const int RP = 256 / (sl.lpr * S);
   int ic = (32768 / RP - 8) / 8 * 8;
@@ -1316,6 +1323,20 @@ void forward_st(kan_engine* e, const float* x, int64_t M, void* out, cudaStream_
       p.ld_x = src.ld;
     }
     p.x = src.p;
+    // fp32 dense rows: quantize them once in an HBM-bound prepass (u8 levels),
+    // so the gather loop reads one u32 of levels per quad instead of running
+    // the threshold math and level shuffles in every lane group
+    if (!conv && src.f32 && e->st_prepass && src.ld == sl.n_in) {
+      const int64_t n = M * static_cast<int64_t>(sl.n_in);
+      e->st_xlev.alloc(static_cast<size_t>(n));
+      ck(launch_st_levels(static_cast<const float*>(src.p), n, e->st_thr.p, static_cast<float>(1.0 / e->st_in.scale),
+                          static_cast<float>(e->st_in.zp), static_cast<int>(e->st_in.qhi), e->st_xlev.p, 0, st),
+         "input levels");
+      e->last_launches += 1;
+      p.in_kind = ST_IN_U8;
+      p.x = e->st_xlev.p;
+      p.ld_x = sl.n_in;
+    }
     if (last) {
       p.epi = EPI_F32;
       p.out = out;
