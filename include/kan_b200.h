@@ -160,6 +160,12 @@ kan_status kan_engine_layer_levels(kan_engine* e, int layer, const float* x_dev,
 kan_status kan_engine_layer_accumulators(kan_engine* e, int layer, const uint16_t* levels_dev,
                                          int64_t batch, int32_t* acc_s_dev, int32_t* acc_b_dev,
                                          void* stream);
+/* Fake-quant calibrated activation policy (QuantConfig::ARangePolicy::kCalibrated,
+ * EvalOptions::a_ranges, eval.hpp:43-68): ranges [n][2] = (lo, hi) per KAN layer,
+ * as calibrate_activation_ranges returns them (eval.hpp:289-341); n = 0 restores
+ * the grid-bound policy.  Takes effect at the next kan_engine_configure. */
+kan_status kan_engine_set_activation_ranges(kan_engine* e, const double* ranges, int n);
+
 /* Spline-table mode ------------------------------------------------------- */
 /* Supply the tables of KAN layer `layer` (SplineTableSet, spline_table.hpp:19-34;
  * EvalOptions::tables, eval.hpp:41), e.g. read from a .kant container

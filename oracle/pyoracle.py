@@ -590,6 +590,9 @@ class Ref:
         L.ref_save_container.argtypes = [C.c_char_p, C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_int,
                                          C.c_int, C.c_char_p]
         L.ref_load_container.argtypes = [C.c_char_p]
+        L.ref_calibrate_ranges.argtypes = [C.c_char_p, C.POINTER(C.c_void_p), C.c_int64, C.c_int64, _dp, _dp]
+        L.ref_fakequant_calibrated_forward.argtypes = [C.c_char_p, C.POINTER(C.c_void_p), C.c_int, C.c_int,
+                                                       C.c_int, _dp, C.c_int64, C.c_int64, _dp, C.c_int64, _dp]
         L.ref_model_forward.argtypes = [C.c_char_p, C.POINTER(C.c_void_p), C.c_int, C.c_int,
                                         C.c_int, C.c_int, C.c_int64, C.c_int64, _dp, C.c_int64,
                                         _dp, C.c_int, C.c_int64]
@@ -752,6 +755,28 @@ class Ref:
         """load_container: (layer count or -6 io / -7 format / -8 checksum, message)."""
         n = self.lib.ref_load_container(str(path).encode())
         return n, (self.err() if n < 0 else "")
+
+    def calibrate_ranges(self, text, coeffs, inputs, n_kan):
+        """calibrate_activation_ranges (eval.hpp:289-341): [n_kan, 2] (lo, hi)."""
+        inputs = np.ascontiguousarray(inputs, dtype=np.float64)
+        cs = [np.ascontiguousarray(c, dtype=np.float64) for c in coeffs]
+        ptrs = (C.c_void_p * len(cs))(*[c.ctypes.data for c in cs])
+        out = np.zeros((n_kan, 2))
+        if self.lib.ref_calibrate_ranges(text.encode(), ptrs, inputs.shape[0], inputs.shape[1], inputs,
+                                         out) < 0:
+            raise ValueError(self.err())
+        return out
+
+    def fakequant_calibrated_forward(self, text, coeffs, inputs, n_out, bits_w, bits_a, bits_b, ranges):
+        inputs = np.ascontiguousarray(inputs, dtype=np.float64)
+        cs = [np.ascontiguousarray(c, dtype=np.float64) for c in coeffs]
+        ptrs = (C.c_void_p * len(cs))(*[c.ctypes.data for c in cs])
+        rg = np.ascontiguousarray(ranges, dtype=np.float64)
+        out = np.zeros((inputs.shape[0], n_out))
+        if self.lib.ref_fakequant_calibrated_forward(text.encode(), ptrs, bits_w, bits_a, bits_b, rg,
+                                                     inputs.shape[0], inputs.shape[1], inputs, n_out, out):
+            raise ValueError(self.err())
+        return out
 
     def validate_descriptor(self, text: str) -> int:
         n = self.lib.ref_validate_descriptor(text.encode())

@@ -461,6 +461,65 @@ int ref_load_container(const char* path) {
   }
 }
 
+// calibrate_activation_ranges (eval.hpp:289-341) of a descriptor-built model:
+// ranges [n_kan][2] (lo, hi)
+int ref_calibrate_ranges(const char* json_text, const double* const* coeff_ptrs, int64_t M, int64_t D,
+                         const double* inputs, double* ranges) try {
+  Model model = model_from_descriptor(nlohmann::json::parse(json_text));
+  int li = 0;
+  for (auto& layer : model.layers) {
+    if (auto* lin = std::get_if<KanLinearLayer>(&layer)) {
+      std::copy(coeff_ptrs[li], coeff_ptrs[li] + lin->coeffs.size(), lin->coeffs.flat().begin());
+      ++li;
+    } else if (auto* conv = std::get_if<ConvKanLayer>(&layer)) {
+      std::copy(coeff_ptrs[li], coeff_ptrs[li] + conv->coeffs.size(), conv->coeffs.flat().begin());
+      ++li;
+    }
+  }
+  const auto r = calibrate_activation_ranges(model, make_matrix(M, D, inputs));
+  for (std::size_t i = 0; i < r.size(); ++i) {
+    ranges[2 * i] = r[i].first;
+    ranges[2 * i + 1] = r[i].second;
+  }
+  return static_cast<int>(r.size());
+} catch (const std::exception& e) {
+  return fail(e);
+}
+
+// model_forward in fake-quant mode with the calibrated activation policy
+// (QuantConfig::ARangePolicy::kCalibrated, eval.hpp:55-68): ranges [n_kan][2]
+int ref_fakequant_calibrated_forward(const char* json_text, const double* const* coeff_ptrs, int bits_w,
+                                     int bits_a, int bits_b, const double* ranges, int64_t M, int64_t D,
+                                     const double* inputs, int64_t n_out, double* out) try {
+  Model model = model_from_descriptor(nlohmann::json::parse(json_text));
+  int li = 0;
+  for (auto& layer : model.layers) {
+    if (auto* lin = std::get_if<KanLinearLayer>(&layer)) {
+      std::copy(coeff_ptrs[li], coeff_ptrs[li] + lin->coeffs.size(), lin->coeffs.flat().begin());
+      ++li;
+    } else if (auto* conv = std::get_if<ConvKanLayer>(&layer)) {
+      std::copy(coeff_ptrs[li], coeff_ptrs[li] + conv->coeffs.size(), conv->coeffs.flat().begin());
+      ++li;
+    }
+  }
+  EvalOptions opts;
+  opts.mode = EvalMode::kFakeQuant;
+  opts.qcfg.bits_w = bits_w;
+  opts.qcfg.bits_a = bits_a;
+  opts.qcfg.bits_b = bits_b;
+  opts.qcfg.a_range_policy = QuantConfig::ARangePolicy::kCalibrated;
+  for (int i = 0; i < li; ++i) opts.a_ranges.emplace_back(ranges[2 * i], ranges[2 * i + 1]);
+  const Matrix r = model_forward(model, make_matrix(M, D, inputs), opts);
+  if (static_cast<int64_t>(r.cols()) != n_out) {
+    g_err = "ref_fakequant_calibrated_forward: output width";
+    return -1;
+  }
+  std::copy(r.flat().begin(), r.flat().end(), out);
+  return 0;
+} catch (const std::exception& e) {
+  return fail(e);
+}
+
 // Harness composition for descriptors the reference cannot express (the
 // engine's additive extension: named tensors id / input_from / residual,
 // global_avgpool, "conv_output": "floor"), built ONLY from reference

@@ -168,6 +168,8 @@ struct StLayer {
   double in_s = 1.0, out_s = 1.0;
   int64_t in_z = 0, in_qhi = 0, out_z = 0, out_qhi = 0;
   bool ft = false;  // fake-quant mode: fp32 tables, Np = row bytes (4 per column)
+  QParams aq;         // this layer's input quantizer (a_params_for, eval.hpp:55-68)
+  DevBuf<float> athr; // its exact fp32 thresholds (empty: the engine-wide st_thr)
 };
 
 // Device-side state of one configured KAN layer.
@@ -292,6 +294,9 @@ struct kan_engine {
   // them when lut_k / lut_h match (EvalOptions::lut, eval.hpp:40)
   std::vector<uint8_t> c_lut;
   int c_lut_k = 0, c_lut_h = 0;
+  // fake-quant calibrated activation ranges, one (lo, hi) per KAN layer
+  // (EvalOptions::a_ranges, eval.hpp:43-44); empty: the grid bounds
+  std::vector<std::pair<double, double>> a_ranges;
   // spline-table mode
   std::vector<StLayer> st;
   QParams st_in;            // input quantizer on the grid bounds (spline_table.hpp:51)
@@ -1092,23 +1097,13 @@ void configure_fq(kan_engine* e, const kan_config& cfg) {
     throw Unsupported("fake-quant mode with passthrough activations: use bits_a <= 8 (tabulated) or mode fp32");
   const Grid& g = e->grid;
   e->st_prepass = !(std::getenv("KAN_ST_PREPASS") && std::atoi(std::getenv("KAN_ST_PREPASS")) == 0);
+  if (!e->a_ranges.empty() && static_cast<int>(e->a_ranges.size()) != e->n_kan)
+    throw InvalidArgument("model_forward: calibrated activation policy needs a range per KAN layer");
   e->st_in = quant_params(g.lo, g.hi, bits_a);  // a_params_for, eval.hpp:55-68 (grid bounds)
   e->st_thr.upload(quant_thresholds(e->st_in));
   const int64_t Lv = int64_t{1} << bits_a;
   const int nb = g.nb();
-  // fake-quantized basis at every activation level: basis(clamp(dequant(m)))
-  // (kan_linear_forward clamps, layers.hpp:111), then FakeQuantBasis at bits_b
-  std::vector<double> basis(static_cast<size_t>(Lv * nb));
   const QParams bq = bits_b == 32 ? QParams{} : quant_params(0.0, 1.0, bits_b);
-  for (int64_t m = 0; m < Lv; ++m) {
-    const double x = g.clamp(e->st_in.scale * static_cast<double>(m - e->st_in.zp));
-    double* row = &basis[static_cast<size_t>(m * nb)];
-    g.basis_at_coord(g.knot_coord(x), row);
-    if (bits_b != 32)
-      for (int k = 0; k < nb; ++k) row[k] = bq.scale * static_cast<double>(quantize(row[k], bq) - bq.zp);
-  }
-  DevBuf<double> d_basis;
-  d_basis.upload(basis);
   e->st.clear();
   e->st.resize(static_cast<size_t>(e->n_kan));
   for (const auto& l : e->layers) {
@@ -1119,12 +1114,30 @@ void configure_fq(kan_engine* e, const kan_config& cfg) {
     sl.n_out = l.type == L_LINEAR ? l.n_out : l.c_out;
     sl.bits_a = bits_a;
     sl.h = bits_b;
-    sl.in_s = e->st_in.scale;
-    sl.in_z = e->st_in.zp;
-    sl.in_qhi = e->st_in.qhi;
+    // this layer's activation quantizer: grid bounds, or its calibrated range
+    sl.aq = e->a_ranges.empty()
+                ? e->st_in
+                : quant_params(e->a_ranges[static_cast<size_t>(l.kan_index)].first,
+                               e->a_ranges[static_cast<size_t>(l.kan_index)].second, bits_a);
+    sl.athr.upload(quant_thresholds(sl.aq));
+    sl.in_s = sl.aq.scale;
+    sl.in_z = sl.aq.zp;
+    sl.in_qhi = sl.aq.qhi;
     st_geometry(sl);
     if (l.coeffs.size() != static_cast<size_t>(sl.n_in) * nb * sl.n_out)
       throw InvalidArgument("coefficients of KAN layer " + std::to_string(l.kan_index) + " not set");
+    // fake-quantized basis at every activation level: basis(clamp(dequant(m)))
+    // (kan_linear_forward clamps, layers.hpp:111), then FakeQuantBasis at bits_b
+    std::vector<double> basis(static_cast<size_t>(Lv * nb));
+    for (int64_t m = 0; m < Lv; ++m) {
+      const double x = g.clamp(sl.aq.scale * static_cast<double>(m - sl.aq.zp));
+      double* row = &basis[static_cast<size_t>(m * nb)];
+      g.basis_at_coord(g.knot_coord(x), row);
+      if (bits_b != 32)
+        for (int k = 0; k < nb; ++k) row[k] = bq.scale * static_cast<double>(quantize(row[k], bq) - bq.zp);
+    }
+    DevBuf<double> d_basis;
+    d_basis.upload(basis);
     DevBuf<double> d_coeffs;
     d_coeffs.upload(fake_quant_weights(l.coeffs, bits_w));
     sl.T.alloc(static_cast<size_t>((sl.n_in + 3) / 4 * 4) * static_cast<size_t>(Lv) * sl.Np, true);
@@ -1162,6 +1175,7 @@ void configure_st(kan_engine* e, const kan_config& cfg) {
     sl.in_s = e->st_in.scale;
     sl.in_z = e->st_in.zp;
     sl.in_qhi = e->st_in.qhi;
+    sl.aq = e->st_in;
     st_geometry(sl);
     if (!l.st_values.empty()) {
       if (l.st_bits_a != bits_a)
@@ -1202,15 +1216,15 @@ static StParams st_params(const kan_engine* e, const StLayer& sl, int64_t rows =
   ic = std::min(ic, (sl.n_in + 7) / 8 * 8);
   p.ic = std::max(ic, 8);
   p.T = sl.T.p;
-  p.thr = e->st_thr.p;
+  p.thr = sl.athr.p ? sl.athr.p : e->st_thr.p;
   p.inv_s = static_cast<float>(1.0 / sl.in_s);
   p.zf = static_cast<float>(sl.in_z);
-  p.lvl0 = static_cast<int>(quantize(0.0, e->st_in));
+  p.lvl0 = static_cast<int>(quantize(0.0, sl.aq));
   p.corr = static_cast<long long>(sl.n_in) * sl.out_z;
   p.out_s = sl.out_s;
   p.in_s = e->st_in.scale;
   p.in_zd = static_cast<double>(e->st_in.zp);
-  p.in_qhi = e->st_in.qhi;
+  p.in_qhi = sl.aq.qhi;
   p.vthr = sl.vthr.p;
   p.ratio_f = static_cast<float>(sl.out_s / e->st_in.scale);
   p.ft = sl.ft ? 1 : 0;
@@ -1238,8 +1252,9 @@ void forward_st(kan_engine* e, const float* x, int64_t M, void* out, cudaStream_
     if (image_use) {  // conv / maxpool read u8 NCHW levels
       const int64_t n = M * e->input_size();
       e->st_xlev.alloc(static_cast<size_t>(n));
-      ck(launch_st_levels(x, n, e->st_thr.p, static_cast<float>(1.0 / e->st_in.scale),
-                          static_cast<float>(e->st_in.zp), static_cast<int>(e->st_in.qhi), e->st_xlev.p, 0, st),
+      const StLayer& s0 = e->st[0];  // the first KAN layer quantizes the model input
+      ck(launch_st_levels(x, n, s0.athr.p ? s0.athr.p : e->st_thr.p, static_cast<float>(1.0 / s0.aq.scale),
+                          static_cast<float>(s0.aq.zp), static_cast<int>(s0.aq.qhi), e->st_xlev.p, 0, st),
          "input levels");
       e->last_launches += 1;
       bool flat_use = false;
@@ -1329,8 +1344,8 @@ void forward_st(kan_engine* e, const float* x, int64_t M, void* out, cudaStream_
     if (!conv && src.f32 && e->st_prepass && src.ld == sl.n_in) {
       const int64_t n = M * static_cast<int64_t>(sl.n_in);
       e->st_xlev.alloc(static_cast<size_t>(n));
-      ck(launch_st_levels(static_cast<const float*>(src.p), n, e->st_thr.p, static_cast<float>(1.0 / e->st_in.scale),
-                          static_cast<float>(e->st_in.zp), static_cast<int>(e->st_in.qhi), e->st_xlev.p, 0, st),
+      ck(launch_st_levels(static_cast<const float*>(src.p), n, p.thr, p.inv_s, p.zf, static_cast<int>(sl.aq.qhi),
+                          e->st_xlev.p, 0, st),
          "input levels");
       e->last_launches += 1;
       p.in_kind = ST_IN_U8;
@@ -1343,6 +1358,17 @@ void forward_st(kan_engine* e, const float* x, int64_t M, void* out, cudaStream_
       p.ld_out = sl.n_out;
     } else {
       p.epi = EPI_LEVEL;
+      // levels for the consuming KAN layer's quantizer (maxpool / flatten keep them)
+      for (int j = i + 1; j < nl; ++j) {
+        const Layer& lc = e->layers[static_cast<size_t>(j)];
+        if (lc.type != L_LINEAR && lc.type != L_CONV) continue;
+        const StLayer& sc = e->st[static_cast<size_t>(lc.kan_index)];
+        p.o_thr = sc.athr.p ? sc.athr.p : e->st_thr.p;
+        p.o_inv_s = static_cast<float>(1.0 / sc.aq.scale);
+        p.o_zf = static_cast<float>(sc.aq.zp);
+        p.o_qhi = static_cast<int>(sc.aq.qhi);
+        break;
+      }
       p.ld_out = conv ? 0 : (sl.n_out + 15) / 16 * 16;
       const size_t bytes = conv ? static_cast<size_t>(p.rows) * sl.n_out : static_cast<size_t>(M * p.ld_out);
       p.out = slot(i, bytes);
@@ -2522,6 +2548,21 @@ kan_status kan_engine_load(const char* path, int device, kan_engine** out) {
   }
   kan_container_destroy(c);
   return st;
+}
+
+kan_status kan_engine_set_activation_ranges(kan_engine* e, const double* ranges, int n) {
+  if (!e) return KAN_ERR_INVALID_ARGUMENT;
+  return guarded(e, [&] {
+    if (n == 0) {
+      e->a_ranges.clear();
+    } else {
+      if (n != e->n_kan || !ranges)
+        throw InvalidArgument("model_forward: calibrated activation policy needs a range per KAN layer");
+      e->a_ranges.clear();
+      for (int i = 0; i < n; ++i) e->a_ranges.emplace_back(ranges[2 * i], ranges[2 * i + 1]);
+    }
+    e->configured = false;
+  });
 }
 
 kan_status kan_engine_set_spline_tables(kan_engine* e, int layer, const uint8_t* values, int64_t n,

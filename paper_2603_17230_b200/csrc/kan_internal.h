@@ -180,6 +180,11 @@ struct StParams {
   // level >= n (n = 1..in_qhi), ratio_f = s_out / in_s for the fp32 estimate
   const int* vthr;
   float ratio_f;
+  // fake-quant EPI_LEVEL: the consuming layer's input quantizer (calibrated
+  // ranges give every KAN layer its own): thresholds, 1/s, z, q_hi
+  const float* o_thr;
+  float o_inv_s, o_zf;
+  int o_qhi;
   // fused output layer (dense rows, one warp per row): the hidden levels of
   // each row stay in smem and the next, last layer (n_out <= 16, tables
   // [n_in][Lv][16]) runs in the same warp; f_out gets its fp32 outputs

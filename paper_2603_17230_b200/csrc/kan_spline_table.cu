@@ -284,7 +284,7 @@ __device__ __forceinline__ void st_epilogue_f(const StParams& p, int64_t r, int 
       o = r * p.ld_out + j;
     }
     if (p.epi == EPI_LEVEL)
-      static_cast<uint8_t*>(p.out)[o] = static_cast<uint8_t>(st_level_f32(a[t], p.thr, p.inv_s, p.zf, static_cast<int>(p.in_qhi)));
+      static_cast<uint8_t*>(p.out)[o] = static_cast<uint8_t>(st_level_f32(a[t], p.o_thr, p.o_inv_s, p.o_zf, p.o_qhi));
     else
       static_cast<float*>(p.out)[o] = a[t];
   }

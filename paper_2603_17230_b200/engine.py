@@ -90,6 +90,7 @@ _lib.kan_engine_layer_time_ms.argtypes = [_vp, C.c_int, C.POINTER(C.c_double),
                                           C.POINTER(C.c_int64)]
 _lib.kan_engine_layer_timeline.argtypes = [_vp, C.c_int, _vp, C.c_int64]
 _lib.kan_engine_layer_timeline.restype = C.c_int64
+_lib.kan_engine_set_activation_ranges.argtypes = [_vp, _vp, C.c_int]
 _lib.kan_engine_set_spline_tables.argtypes = [_vp, C.c_int, _vp, C.c_int64, C.c_int, C.c_int, _vp, _vp]
 _lib.kan_engine_spline_table.argtypes = [_vp, C.c_int, _vp, C.c_int64, _vp, _vp]
 _lib.kan_engine_spline_table.restype = C.c_int64
@@ -137,7 +138,7 @@ EXPORTED = [
     "kan_container_descriptor", "kan_container_num_kan_layers", "kan_container_coeffs",
     "kan_container_lut", "kan_container_num_spline_tables", "kan_container_spline_table",
     "kan_container_save", "kan_container_save_error", "kan_crc32", "kan_engine_load",
-    "kan_engine_evaluate_accuracy",
+    "kan_engine_evaluate_accuracy", "kan_engine_set_activation_ranges",
 ]
 
 
@@ -266,6 +267,8 @@ class EvalOptions:
     out_kind: int = OUT_F32
     out_scale: float = 1.0
     split_k: int = 0
+    # fake-quant calibrated policy: one (lo, hi) per KAN layer (EvalOptions::a_ranges)
+    a_ranges: Optional[Sequence] = None
 
 
 def _torch():
@@ -353,6 +356,11 @@ class Engine:
                                                0 if b is None else b.size))
 
     def configure(self, opts: EvalOptions):
+        if opts.a_ranges is None:
+            self._check(_lib.kan_engine_set_activation_ranges(self._h, None, 0))
+        else:
+            rg = np.ascontiguousarray(opts.a_ranges, dtype=np.float64).reshape(-1, 2)
+            self._check(_lib.kan_engine_set_activation_ranges(self._h, rg.ctypes.data, rg.shape[0]))
         cfg = _Config(eval_mode_from_string(opts.mode), opts.lut_k, opts.lut_h, opts.bits_w,
                       opts.w_scheme, int(bool(opts.silu_base)), opts.out_kind,
                       float(opts.out_scale), opts.split_k)

@@ -103,3 +103,25 @@ def test_sweep_matches_reference_accuracy(ref):
             assert p.accuracy == want, (c, p.accuracy, want)  # bit-exact path
         else:
             assert abs(p.accuracy - want) <= 0.005, (c, p.accuracy, want)
+
+
+@pytest.mark.parametrize("desc", [MLP, LEKAN])
+def test_fake_quant_calibrated_ranges(ref, desc):
+    """QuantConfig::ARangePolicy::kCalibrated: per-layer activation quantizers
+    from the reference's calibrate_activation_ranges (eval.hpp:289-341)."""
+    ws = _ws(desc, 7)
+    e = _engine(desc, ws)
+    D = int(np.prod(desc["input"]))
+    rng = np.random.default_rng(3)
+    calib = rng.uniform(-1, 1, (64, D))
+    x = rng.uniform(-1, 1, (200 if D < 100 else 12, D)).astype(np.float32)
+    text = json.dumps(desc)
+    nk = sum(l["type"] in ("linear", "conv") for l in desc["layers"])
+    ranges = ref.calibrate_ranges(text, ws, calib, nk)
+    for bw, ba, bb in ((8, 8, 8), (6, 5, 4)):
+        e.configure(EvalOptions(mode="fake-quant", bits_w=bw, lut_k=ba, lut_h=bb, a_ranges=ranges))
+        y = e.model_forward(torch.from_numpy(x).cuda()).cpu().numpy().astype(np.float64)
+        r = ref.fakequant_calibrated_forward(text, ws, x.astype(np.float64), 10, bw, ba, bb, ranges)
+        assert _rel(y, r) < TOL
+    with pytest.raises(ValueError):
+        e.configure(EvalOptions(mode="fake-quant", bits_w=8, lut_k=8, lut_h=8, a_ranges=ranges[:1]))
