@@ -3,6 +3,7 @@
 "KAN samples/sec (int8-LUT path) and % of roofline at 1/2/4/8 B200").
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+                  [--streams S] [--split-k K]
 
 A step = one forward pass of the workload over one batch of synthetic input.
 Default workload = BASELINE.json configs[1] (C2): KAN MLP [784,64,10], G=5,
@@ -11,6 +12,11 @@ SiLU base term, hidden outputs requantized to the next layer's lattice, int8
 logits.  For N > 1 (torchrun, one process per GPU, NCCL) every rank runs the
 same per-GPU batch (weak scaling); logits are gathered to rank 0 over NCCL
 once per 16-batch replay.  Rank 0 prints ONE JSON line.
+
+C1/C2 keep several independent batches in flight per GPU (one engine and CUDA
+stream each, STREAMS_DEFAULT): a single C2 forward is a latency-bound launch
+on a fraction of the SMs, so batches overlap; every batch is still one full
+forward, and the timed region covers all K of them.
 
 Timing: W untimed warm-up steps, then exactly K steps bracketed by a barrier
 and cudaDeviceSynchronize on both sides, device-timed with CUDA events on the
@@ -35,6 +41,14 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 L2_BYTES = 126 * 1024 * 1024
+# independent batches in flight per GPU (one engine + CUDA stream each): the
+# C1/C2 forwards are single latency-bound launches that leave SMs idle in their
+# split-K reduction tail, so two batches in flight overlap one's tail with the
+# other's main loop (measured; bench.py --streams overrides)
+STREAMS_DEFAULT = {"c1": 4, "c2": 6}
+# K splits per launch (0 = the engine's choice): C2 runs unsplit (32 persistent
+# CTAs per batch, 2 launches) so six batches share the GPU without a split-K tail
+SPLIT_DEFAULT = {"c2": 1}
 PAPER_SAMPLES_PER_S = {  # PAPER.md:603, KANMLP2 G=5 8-bit LUT on RTX 3090
     "c1": 10000 / 5.9e-3, "c2": 10000 / 5.9e-3,
 }
@@ -50,6 +64,9 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
                     help="wall time of the bounded CPU-baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--streams", type=int, default=0,
+                    help="independent batches in flight (one engine + stream each); 0 = per-config default")
+    ap.add_argument("--split-k", type=int, default=0, help="force the K splits of split-K launches")
     return ap.parse_args()
 
 
@@ -335,12 +352,19 @@ def main():
     B = wl.batch  # per-GPU batch (weak scaling)
 
     Ws, Bs = wl.weights()
-    eng = Engine(wl.descriptor(), local)
-    for i, (w, b) in enumerate(zip(Ws, Bs)):
-        eng.set_coeffs(i, w, b)
+    n_streams = args.streams or STREAMS_DEFAULT.get(wl.key, 1)
+    engines = []
+    for _ in range(n_streams):  # one engine per stream: independent workspaces
+        e_ = Engine(wl.descriptor(), local)
+        for i, (w, b) in enumerate(zip(Ws, Bs)):
+            e_.set_coeffs(i, w, b)
+        engines.append(e_)
+    eng = engines[0]
     opts = EvalOptions(mode=wl.mode, lut_k=wl.lut_k, lut_h=wl.lut_h, bits_w=wl.bits_w,
-                       w_scheme=W_PER_CHANNEL_SYM, silu_base=wl.silu, out_kind=OUT_F32)
-    eng.configure(opts)
+                       w_scheme=W_PER_CHANNEL_SYM, silu_base=wl.silu, out_kind=OUT_F32,
+                       split_k=args.split_k or SPLIT_DEFAULT.get(wl.key, 0))
+    for e_ in engines:
+        e_.configure(opts)
 
     # rotating resident input batches, total > L2
     in_bytes = B * wl.input_size * 4
@@ -351,22 +375,33 @@ def main():
         y = eng.model_forward(xs[0]).float()
         s_out = float(y.abs().max().item()) / 127.0
         opts.out_kind, opts.out_scale = OUT_I8, s_out
-        eng.configure(opts)
+        for e_ in engines:
+            e_.configure(opts)
     out_dtype = torch.int8 if wl.int8_out else torch.float32
     outs = torch.empty((R, B, wl.out_size), device=dev, dtype=out_dtype)
     st = torch.cuda.Stream(dev)
+    aux = [torch.cuda.Stream(dev) for _ in range(n_streams - 1)]
+    streams = [st] + aux
     torch.cuda.synchronize()
-    # warm the engine (allocations happen outside graph capture)
-    with torch.cuda.stream(st):
-        for r in range(R):
-            eng.model_forward(xs[r], out=outs[r], stream=st)
+    # warm the engines (allocations happen outside graph capture)
+    for k, e_ in enumerate(engines):
+        with torch.cuda.stream(streams[k]):
+            for r in range(R):
+                e_.model_forward(xs[r], out=outs[r], stream=streams[k])
     torch.cuda.synchronize()
     launches_per_step = eng.last_launches
 
+    # the R-forward graph: batch r runs on stream r % n_streams (its own engine),
+    # forked from and joined back into the capture stream
     big = torch.cuda.CUDAGraph()
     with torch.cuda.graph(big, stream=st):
+        for s_ in aux:
+            s_.wait_stream(st)
         for r in range(R):
-            eng.model_forward(xs[r], out=outs[r], stream=st)
+            k = r % n_streams
+            engines[k].model_forward(xs[r], out=outs[r], stream=streams[k])
+        for s_ in aux:
+            st.wait_stream(s_)
     singles = []
     for r in range(R):
         g = torch.cuda.CUDAGraph()
@@ -520,6 +555,11 @@ def main():
                        "l2": f"inputs rotate over {R} resident batches "
                              f"({R * in_bytes / 2**20:.0f} MiB > 126 MiB L2)",
                        "launch": f"CUDA graphs ({R}-forward graph + single-forward graphs)",
+                       "streams": n_streams,
+                       "split_k": opts.split_k or "auto",
+                       "concurrency": (f"{n_streams} independent batches in flight (one engine + CUDA "
+                                       "stream each); ms_per_step = timed region / steps"
+                                       if n_streams > 1 else "one batch at a time"),
                        "vs_baseline_ref": "PAPER.md:603 KANMLP2 G=5 8-bit LUT, RTX 3090, "
                                           "1.69M samples/s" if paper else None},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
