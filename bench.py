@@ -468,10 +468,12 @@ def main():
     dom = int(np.argmax(layer_ms))
     bytes_l = wl.layer_bytes_per_launch(dom, B)
     ops_l = wl.layer_ops_per_launch(dom, B)
-    if launches_per_step == 1:
-        # the whole forward is one launch (fused output layer): model input in,
-        # model output out, every layer's weights once; the hidden activations
-        # never leave the chip
+    whole = launches_per_step == 1 or n_streams > 1
+    if whole:
+        # the whole forward is one launch (fused output layer), or several
+        # batches are in flight (per-launch event brackets cannot isolate one
+        # launch): model input in, model output out, every layer's weights
+        # once per batch, over the effective time per batch
         bytes_l = (B * wl.input_size * 4 + B * wl.out_size * (1 if wl.int8_out else 4)
                    + sum(wl.weight_bytes(li) for li in range(wl.n_kan)))
         ops_l = wl.ops_per_sample() * B
@@ -483,7 +485,7 @@ def main():
     # a step that is a single launch (C1/C2: the output layer runs fused):
     # the kernel's live average over the timed region is the step time (the
     # profiling pass's event nodes would break the overlap between steps)
-    if launches_per_step == 1:
+    if whole:
         layer_ms[dom] = ms / args.steps
     t_l = layer_ms[dom] / 1e3
     ai = ops_l / bytes_l
@@ -503,9 +505,13 @@ def main():
                       + (f", {kl['pix']} px/sample)" if kl["pix"] > 1 else ")"))
     if launches_per_step == 1 and wl.n_kan > 1:
         roof["kernel"] += f" with the {wl.n_kan - 1} following layer(s) fused in"
+    if n_streams > 1:
+        roof["kernel"] = (f"whole forward ({launches_per_step} launch(es) per batch, "
+                          f"{n_streams} batches in flight)")
     roof["per_launch"] = {"algorithmic_bytes": bytes_l, "algorithmic_ops": ops_l,
                           "avg_ms": layer_ms[dom], "launches_timed": prof_steps,
-                          "timing": ("timed region / steps (one launch per step)" if launches_per_step == 1
+                          "timing": (f"timed region / steps ({n_streams} batches in flight)" if n_streams > 1
+                                     else "timed region / steps (one launch per step)" if launches_per_step == 1
                                      else "CUDA event pair around the kernel node, graph replay")}
     roof["peak_source"] = peak_src + (
         "" if not lut or "int8_tops" in peaks else "; int8 peak = datasheet 4.5 POPS dense")
