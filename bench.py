@@ -519,18 +519,27 @@ def main():
     roof["share_of_step"] = layer_ms[dom] / (ms / args.steps)
 
     # ---- e2e through the public API: host buffers, H2D + forward + D2H every step
-    # (with batches in flight, two host threads each drive their own engine and
-    # stream, so one call's host->device copy overlaps the other's forward; the
-    # C ABI call releases the GIL)
+    # (two host threads each drive their own engine and stream, so one call's
+    # host->device copy overlaps the other's forward; the C ABI call releases
+    # the GIL)
     e2e_steps = max(10, min(args.steps, 300))
-    n_e2e = 2 if n_streams > 1 else 1
+    n_e2e = 2
     e2e_steps -= e2e_steps % n_e2e
+    e2e_engines, e2e_streams = list(engines[:n_e2e]), list(streams[:n_e2e])
+    while len(e2e_engines) < n_e2e:  # a second engine / stream for the overlap
+        e_ = Engine(wl.descriptor(), local)
+        for i, (w, b) in enumerate(zip(Ws, Bs)):
+            e_.set_coeffs(i, w, b)
+        e_.configure(opts)
+        e2e_engines.append(e_)
+        e2e_streams.append(torch.cuda.Stream(dev))
     hx = [torch.from_numpy(wl.inputs(B, seed=500 + r)).pin_memory() for r in range(4)]
     houts = [torch.empty((B, wl.out_size), dtype=out_dtype).pin_memory() for _ in range(n_e2e)]
 
     def e2e_worker(k, n):
         for i in range(n):
-            engines[k].forward_host_ptr(hx[(i + k) % 4].data_ptr(), B, houts[k].data_ptr(), stream=streams[k])
+            e2e_engines[k].forward_host_ptr(hx[(i + k) % 4].data_ptr(), B, houts[k].data_ptr(),
+                                            stream=e2e_streams[k])
     for k in range(n_e2e):
         e2e_worker(k, 3)
     if world > 1:

@@ -666,6 +666,10 @@ void prepare_gemm_layer(kan_engine* e, const Layer& l, PreparedLayer& pl, bool b
   pl.N = N;
   pl.nbp = nbp;
   pl.BN = N > 256 ? 256 : std::max(16, (N + 15) / 16 * 16);
+  if (const char* ev = std::getenv("KAN_FORCE_BN")) {  // tuning only
+    const int bn = std::atoi(ev);
+    if (bn >= 16 && bn <= 256 && bn % 16 == 0 && bn < pl.BN) pl.BN = bn;
+  }
   pl.n_tiles_n = (N + pl.BN - 1) / pl.BN;
   pl.silu = cfg.silu_base ? 1 : 0;
   if (pl.silu && l.base_w.size() != static_cast<size_t>(n_ref) * N)
@@ -1838,6 +1842,7 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
   }
   // persistent launches double-buffer the accumulator when TMEM allows
   p.nacc = gemm_tmem_accs(pl.BN, splits);
+  if (std::getenv("KAN_FORCE_NACC1")) p.nacc = 1;  // tuning only: deeper A ring
   SA = gemm_tmem_slots(pl.BN, p.nacc);
   p.SA = SA;
   p.SB = SB;

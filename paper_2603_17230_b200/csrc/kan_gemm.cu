@@ -384,20 +384,36 @@ __device__ __forceinline__ void bf16_row(const GemmParams& p, const float (&x)[3
 #pragma unroll
   for (int e = 0; e < H; ++e) {
     float Nv[PMAX + 1];
-    const int jj = basis_f32<PMAX>(x[e], p.flo, p.fhi_open, p.finv_delta, p.G, p.P, Nv);
-#pragma unroll
-    for (int q = 0; q < NBP / 2; ++q) {
-      float v2[2];
-#pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        const int rr = 2 * q + t - jj;
-        float val = 0.f;
-#pragma unroll
-        for (int m = 0; m <= PMAX; ++m) val = (rr == m) ? Nv[m] : val;
-        v2[t] = val;
-      }
-      w[e * (NBP / 2) + q] = pack_bf16(v2[0], v2[1]);
+    int jj;
+    if (p.P == 3) {
+      // uniform cubic: the local Cox-de Boor triangle in closed form (same
+      // basis; fp32 rounding differs by ~1e-7, far inside the bf16 bar)
+      const float xc = fminf(fmaxf(x[e], p.flo), p.fhi_open);
+      const float xi = (xc - p.flo) * p.finv_delta + 3.0f;
+      int j = static_cast<int>(floorf(xi));
+      j = min(max(j, 3), p.G + 2);
+      const float u = xi - static_cast<float>(j), v = 1.0f - u;
+      const float u2 = u * u, u3 = u2 * u;
+      constexpr float s6 = 1.0f / 6.0f;
+      Nv[0] = v * v * v * s6;
+      Nv[1] = fmaf(3.0f, u3, fmaf(-6.0f, u2, 4.0f)) * s6;
+      Nv[2] = fmaf(-3.0f, u3, fmaf(3.0f, u2, fmaf(3.0f, u, 1.0f))) * s6;
+      Nv[3] = u3 * s6;
+      jj = j - 3;
+    } else {
+      jj = basis_f32<PMAX>(x[e], p.flo, p.fhi_open, p.finv_delta, p.G, p.P, Nv);
     }
+    // the P+1 values as bf16 at slots jj.. of the NBP-slot row: pack them into
+    // up to three words (shifted by half a word when jj is odd), then place
+    const uint32_t lo = pack_bf16(Nv[0], Nv[1]), hi = pack_bf16(Nv[2], Nv[3]);
+    const bool odd = (jj & 1) != 0;
+    const uint32_t A = odd ? (lo << 16) : lo;
+    const uint32_t B = odd ? __funnelshift_l(lo, hi, 16) : hi;
+    const uint32_t Cw = odd ? (hi >> 16) : 0u;
+    const int w0 = jj >> 1;
+#pragma unroll
+    for (int q = 0; q < NBP / 2; ++q)
+      w[e * (NBP / 2) + q] = q == w0 ? A : (q == w0 + 1 ? B : (q == w0 + 2 ? Cw : 0u));
   }
   if constexpr (MODE == MODE_SILU) {
 #pragma unroll
@@ -406,7 +422,7 @@ __device__ __forceinline__ void bf16_row(const GemmParams& p, const float (&x)[3
 #pragma unroll
       for (int t = 0; t < 2; ++t) {
         const float xc = fminf(fmaxf(x[2 * q + t], p.flo), p.fhi_open);
-        s2[t] = xc / (1.0f + __expf(-xc));
+        s2[t] = __fdividef(xc, 1.0f + __expf(-xc));
       }
       nw[q] = pack_bf16(s2[0], s2[1]);
     }
