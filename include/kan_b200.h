@@ -27,6 +27,8 @@
  *   kan_engine_spline_table     build_spline_tables (probe)         spline_table.hpp:38-95
  *   kan_container_load / _save  load_container / save_container     io.hpp:99-350
  *   kan_engine_load             load_model / load_container + engine io.hpp:217-352
+ *   kan_engine_linear_backward  kan_linear_backward                 train.hpp:84-136
+ *   kan_softmax_cross_entropy   softmax_cross_entropy               train.hpp:139-160
  *
  * Error mapping (reference exception -> status):
  *   std::invalid_argument (bits, LUT params, mode)  -> KAN_ERR_INVALID_ARGUMENT
@@ -160,6 +162,19 @@ kan_status kan_engine_layer_levels(kan_engine* e, int layer, const float* x_dev,
 kan_status kan_engine_layer_accumulators(kan_engine* e, int layer, const uint16_t* levels_dev,
                                          int64_t batch, int32_t* acc_s_dev, int32_t* acc_b_dev,
                                          void* stream);
+/* Training backward (train.hpp:84-160), fp32 ----------------------------- */
+/* kan_linear_backward of linear KAN layer `layer` with its current
+ * coefficients: x [batch, n_in] (the layer's inputs), dout [batch, n_out] ->
+ * dcoeffs [n_in*(G+P), n_out] (reference row layout) and, if dinputs is not
+ * NULL, dinputs [batch, n_in] (zero where clamp_to_domain moved x). */
+kan_status kan_engine_linear_backward(kan_engine* e, int layer, const float* x_dev, int64_t batch,
+                                      const float* dout_dev, float* dcoeffs_dev, float* dinputs_dev,
+                                      void* stream);
+/* softmax_cross_entropy (train.hpp:139-160): per-row loss [batch] (the mean is
+ * their average) and dL/dlogits [batch, n] = (softmax - onehot) / batch. */
+kan_status kan_softmax_cross_entropy(const float* logits_dev, const int32_t* labels_dev, int64_t batch, int n,
+                                     float* loss_rows_dev, float* dlogits_dev, void* stream);
+
 /* Fake-quant calibrated activation policy (QuantConfig::ARangePolicy::kCalibrated,
  * EvalOptions::a_ranges, eval.hpp:43-68): ranges [n][2] = (lo, hi) per KAN layer,
  * as calibrate_activation_ranges returns them (eval.hpp:289-341); n = 0 restores

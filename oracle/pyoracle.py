@@ -593,6 +593,9 @@ class Ref:
         L.ref_calibrate_ranges.argtypes = [C.c_char_p, C.POINTER(C.c_void_p), C.c_int64, C.c_int64, _dp, _dp]
         L.ref_fakequant_calibrated_forward.argtypes = [C.c_char_p, C.POINTER(C.c_void_p), C.c_int, C.c_int,
                                                        C.c_int, _dp, C.c_int64, C.c_int64, _dp, C.c_int64, _dp]
+        L.ref_linear_backward.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_int64, C.c_int,
+                                          C.c_int, _dp, _dp, _dp, _dp, _dp]
+        L.ref_softmax_ce.argtypes = [C.c_int64, C.c_int, _dp, _i32p, _dp, C.POINTER(C.c_double)]
         L.ref_model_forward.argtypes = [C.c_char_p, C.POINTER(C.c_void_p), C.c_int, C.c_int,
                                         C.c_int, C.c_int, C.c_int64, C.c_int64, _dp, C.c_int64,
                                         _dp, C.c_int, C.c_int64]
@@ -777,6 +780,27 @@ class Ref:
                                                      inputs.shape[0], inputs.shape[1], inputs, n_out, out):
             raise ValueError(self.err())
         return out
+
+    def linear_backward(self, G, P, acts, coeffs, dout, lo=-1.0, hi=1.0):
+        """kan_linear_backward (train.hpp:131-136): (dcoeffs, dinputs)."""
+        acts = np.ascontiguousarray(acts, dtype=np.float64)
+        coeffs = np.ascontiguousarray(coeffs, dtype=np.float64)
+        dout = np.ascontiguousarray(dout, dtype=np.float64)
+        dc = np.zeros(coeffs.shape)
+        di = np.zeros(acts.shape)
+        if self.lib.ref_linear_backward(G, P, lo, hi, acts.shape[0], acts.shape[1], coeffs.shape[1], acts,
+                                        coeffs, dout, dc, di):
+            raise ValueError(self.err())
+        return dc, di
+
+    def softmax_ce(self, logits, labels):
+        logits = np.ascontiguousarray(logits, dtype=np.float64)
+        labels = np.ascontiguousarray(labels, dtype=np.int32)
+        d = np.zeros(logits.shape)
+        loss = C.c_double()
+        if self.lib.ref_softmax_ce(logits.shape[0], logits.shape[1], logits, labels, d, C.byref(loss)):
+            raise ValueError(self.err())
+        return loss.value, d
 
     def validate_descriptor(self, text: str) -> int:
         n = self.lib.ref_validate_descriptor(text.encode())

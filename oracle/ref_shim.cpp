@@ -20,6 +20,7 @@
 #include <kantize/quant.hpp>
 #include <kantize/cost.hpp>
 #include <kantize/spline_table.hpp>
+#include <kantize/train.hpp>
 #include <optional>
 
 #include <algorithm>
@@ -515,6 +516,30 @@ int ref_fakequant_calibrated_forward(const char* json_text, const double* const*
     return -1;
   }
   std::copy(r.flat().begin(), r.flat().end(), out);
+  return 0;
+} catch (const std::exception& e) {
+  return fail(e);
+}
+
+// kan_linear_backward (train.hpp:131-136): dcoeffs [n_in*nb, n_out], dinputs [M, n_in]
+int ref_linear_backward(int G, int P, double lo, double hi, int64_t M, int n_in, int n_out, const double* acts,
+                        const double* coeffs, const double* dout, double* dcoeffs, double* dinputs) try {
+  const KanLinearLayer l = make_linear(G, P, lo, hi, n_in, n_out, coeffs);
+  const LayerGrads g = kan_linear_backward(make_matrix(M, n_in, acts), l, make_matrix(M, n_out, dout));
+  std::copy(g.d_coeffs.flat().begin(), g.d_coeffs.flat().end(), dcoeffs);
+  std::copy(g.d_inputs.flat().begin(), g.d_inputs.flat().end(), dinputs);
+  return 0;
+} catch (const std::exception& e) {
+  return fail(e);
+}
+
+// softmax_cross_entropy (train.hpp:139-160): returns the mean loss in *loss
+int ref_softmax_ce(int64_t M, int n, const double* logits, const int32_t* labels, double* dlogits,
+                   double* loss) try {
+  std::vector<int> lab(labels, labels + M);
+  Matrix d;
+  *loss = softmax_cross_entropy(make_matrix(M, n, logits), lab, d);
+  std::copy(d.flat().begin(), d.flat().end(), dlogits);
   return 0;
 } catch (const std::exception& e) {
   return fail(e);

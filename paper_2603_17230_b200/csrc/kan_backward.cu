@@ -1,0 +1,164 @@
+// kan_backward.cu -- training backward of a linear KAN layer, fp32.
+//
+// Replaces the reference's training math (proj/include/kantize/train.hpp):
+//   kan_linear_backward_with (:84-129)  -> kan_bw_dcoeffs_kernel, kan_bw_dinputs_kernel
+//   basis_derivative_at_coord (:24-51)  -> bw_basis (degree P-1 triangle, differenced)
+//   softmax_cross_entropy (:139-160)    -> kan_softmax_ce_kernel
+// d_coeffs = B^T dY over the clamped activations' basis rows; d_inputs[m,i] =
+// sum_k b'_k(x) (dY[m] . W[i*nb+k]), zero where clamp_to_domain moved x.  The
+// basis is local (P+1 non-zeros), so both are scatter/gather loops over the
+// support instead of dense GEMMs; fp32 throughout (held to 1e-4 of the fp64
+// reference).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace kan {
+
+struct BwParams {
+  int64_t M;
+  int n_in, n_out, G, P;
+  const float* x;  // [M][ld_x]
+  int64_t ld_x;
+  const float* dy;  // [M][n_out]
+  const float* w;   // [n_in*nb][n_out] (reference layout)
+  float* dcoeffs;   // [n_in*nb][n_out]
+  float* dinputs;   // [M][n_in] or null
+  float lo, hi_open, inv_delta;
+};
+
+// Local basis of degree P at x (already clamped): N[r] = B_{j-P+r}, returns
+// jj = j - P (first supported basis); with deriv, D[r] = B'_{j-P+r} in x units
+// (degree P-1 triangle, (B_{i,P-1} - B_{i+1,P-1}) / delta, train.hpp:46-50).
+__device__ __forceinline__ int bw_basis(float x, const BwParams& p, float (&N)[4], float (&D)[4], bool deriv) {
+  const float xi = (x - p.lo) * p.inv_delta + static_cast<float>(p.P);
+  int j = static_cast<int>(floorf(xi));
+  j = min(max(j, p.P), p.G + p.P - 1);
+  // triangle: T[q] at degree d holds B_{j-d+q}, q = 0..d
+  float T[4] = {1.f, 0.f, 0.f, 0.f};
+  float M[4] = {0.f, 0.f, 0.f, 0.f};  // degree P-1 values B_{j-P+1+q}
+  for (int d = 1; d <= p.P; ++d) {
+    if (d == p.P) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) M[q] = T[q];
+    }
+    const float rd = 1.0f / static_cast<float>(d);
+    float U[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (q > d) break;
+      const int i = j - d + q;
+      const float left = q == 0 ? 0.f : T[q - 1];
+      const float right = q == d ? 0.f : T[q];
+      U[q] = ((xi - static_cast<float>(i)) * rd) * left + ((static_cast<float>(i + d + 1) - xi) * rd) * right;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) T[q] = U[q];
+  }
+  if (p.P == 0) M[0] = 0.f;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) N[r] = r <= p.P ? T[r] : 0.f;
+  if (deriv) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      // B'_{j-P+r} = (B_{j-P+r,P-1} - B_{j-P+r+1,P-1}) / delta, with M[q] = B_{j-P+1+q,P-1}
+      const float a = (r >= 1 && r - 1 < p.P) ? M[r - 1] : 0.f;
+      const float b = (r < p.P) ? M[r] : 0.f;
+      D[r] = r <= p.P ? (a - b) * p.inv_delta : 0.f;
+    }
+  }
+  return j - p.P;
+}
+
+// d_coeffs: CTA (input i, 128 outputs), thread j sums over the batch rows
+__global__ void __launch_bounds__(128) kan_bw_dcoeffs_kernel(const BwParams p) {
+  const int i = blockIdx.x;
+  const int j = blockIdx.y * 128 + threadIdx.x;
+  const int nb = p.G + p.P;
+  float acc[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) acc[k] = 0.f;
+  for (int64_t m = 0; m < p.M; ++m) {
+    const float x = fminf(fmaxf(__ldg(p.x + m * p.ld_x + i), p.lo), p.hi_open);
+    float N[4], D[4];
+    const int jj = bw_basis(x, p, N, D, false);
+    const float g = j < p.n_out ? __ldg(p.dy + m * p.n_out + j) : 0.f;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const int r = k - jj;
+      const float b = r == 0 ? N[0] : (r == 1 ? N[1] : (r == 2 ? N[2] : (r == 3 ? N[3] : 0.f)));
+      acc[k] = fmaf(b, g, acc[k]);
+    }
+  }
+  if (j < p.n_out)
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+      if (k < nb) p.dcoeffs[(static_cast<int64_t>(i) * nb + k) * p.n_out + j] = acc[k];
+}
+
+// d_inputs: thread per (m, i)
+__global__ void __launch_bounds__(256) kan_bw_dinputs_kernel(const BwParams p) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= p.M * p.n_in) return;
+  const int64_t m = t / p.n_in;
+  const int i = static_cast<int>(t % p.n_in);
+  const int nb = p.G + p.P;
+  const float x = __ldg(p.x + m * p.ld_x + i);
+  const float cx = fminf(fmaxf(x, p.lo), p.hi_open);
+  if (cx != x) {  // the clamp blocks the gradient (train.hpp:113)
+    p.dinputs[m * p.n_in + i] = 0.f;
+    return;
+  }
+  float N[4], D[4];
+  const int jj = bw_basis(cx, p, N, D, true);
+  const float* g = p.dy + m * p.n_out;
+  float acc = 0.f;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    if (r > p.P || jj + r >= nb || D[r] == 0.f) continue;
+    const float* wr = p.w + (static_cast<int64_t>(i) * nb + jj + r) * p.n_out;
+    float dot = 0.f;
+    for (int j = 0; j < p.n_out; ++j) dot = fmaf(__ldg(wr + j), __ldg(g + j), dot);
+    acc = fmaf(D[r], dot, acc);
+  }
+  p.dinputs[m * p.n_in + i] = acc;
+}
+
+// softmax_cross_entropy: per row loss (log-sum-exp) and dL/dlogits = (p - y) / M
+__global__ void __launch_bounds__(256) kan_softmax_ce_kernel(const float* __restrict__ logits,
+                                                             const int32_t* __restrict__ labels, int64_t M,
+                                                             int n, float* __restrict__ loss_rows,
+                                                             float* __restrict__ dlogits) {
+  const int64_t m = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (m >= M) return;
+  const float* row = logits + m * n;
+  float mx = row[0];
+  for (int j = 1; j < n; ++j) mx = fmaxf(mx, row[j]);
+  float den = 0.f;
+  for (int j = 0; j < n; ++j) den += expf(row[j] - mx);
+  const int y = labels[m];
+  loss_rows[m] = logf(den) - (row[y] - mx);
+  const float inv_m = 1.0f / static_cast<float>(M);
+  for (int j = 0; j < n; ++j) dlogits[m * n + j] = (expf(row[j] - mx) / den - (j == y ? 1.f : 0.f)) * inv_m;
+}
+
+cudaError_t launch_linear_backward(const BwParams& p, cudaStream_t st) {
+  if (p.M == 0) return cudaSuccess;
+  kan_bw_dcoeffs_kernel<<<dim3(static_cast<unsigned>(p.n_in), static_cast<unsigned>((p.n_out + 127) / 128)), 128, 0,
+                          st>>>(p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || !p.dinputs) return e;
+  const int64_t n = p.M * p.n_in;
+  kan_bw_dinputs_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_softmax_ce(const float* logits, const int32_t* labels, int64_t M, int n, float* loss_rows,
+                              float* dlogits, cudaStream_t st) {
+  if (M == 0) return cudaSuccess;
+  kan_softmax_ce_kernel<<<static_cast<unsigned>((M + 255) / 256), 256, 0, st>>>(logits, labels, M, n, loss_rows,
+                                                                                  dlogits);
+  return cudaGetLastError();
+}
+
+}  // namespace kan

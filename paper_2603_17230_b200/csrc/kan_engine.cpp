@@ -58,6 +58,21 @@ cudaError_t launch_maxpool(bool levels, const void* in, int64_t n_img, int H, in
                            int ld_in, int win, void* out, int ld_out, cudaStream_t st);
 cudaError_t launch_avgpool(const void* in, int64_t n_img, int HW, int C, int ld_in, void* out,
                            int ld_out, cudaStream_t st);
+// training backward (kan_backward.cu)
+struct BwParams {
+  int64_t M;
+  int n_in, n_out, G, P;
+  const float* x;
+  int64_t ld_x;
+  const float* dy;
+  const float* w;
+  float* dcoeffs;
+  float* dinputs;
+  float lo, hi_open, inv_delta;
+};
+cudaError_t launch_linear_backward(const BwParams& p, cudaStream_t st);
+cudaError_t launch_softmax_ce(const float* logits, const int32_t* labels, int64_t M, int n, float* loss_rows,
+                              float* dlogits, cudaStream_t st);
 // spline-table mode (kan_spline_table.cu)
 cudaError_t launch_st_sample(const double* basis, const double* coeffs, int n_in, int n_out, int nb, int Lv,
                              int pass, unsigned long long* mm, uint8_t* T, int Np, double s, double zd,
@@ -150,6 +165,9 @@ struct Layer {
   bool im2col = false;
   std::vector<double> coeffs;  // reference layout [n_in*nb, n_out]
   std::vector<double> base_w;  // [n_in, n_out]
+  // fp32 copy of coeffs for the training backward (uploaded on first use after
+  // set_coeffs)
+  std::shared_ptr<DevBuf<float>> w_bw;
   // spline-table mode: tables supplied by the caller (EvalOptions::tables,
   // eval.hpp:41; e.g. loaded from a .kant container) instead of built from
   // the coefficients; values in the reference layout [n_in][n_out][2^bits_a]
@@ -2335,6 +2353,7 @@ kan_status kan_engine_set_coeffs(kan_engine* e, int layer, const double* coeffs,
       throw ShapeMismatch("set_coeffs: expected " + std::to_string(want) + " coefficients, got " +
                           std::to_string(n));
     l.coeffs.assign(coeffs, coeffs + n);
+    l.w_bw.reset();
     if (base_w) {
       if (n_base != static_cast<int64_t>(l.n_in) * l.n_out)
         throw ShapeMismatch("set_coeffs: base weights must be [n_in, n_out]");
@@ -2553,6 +2572,57 @@ kan_status kan_engine_load(const char* path, int device, kan_engine** out) {
   }
   kan_container_destroy(c);
   return st;
+}
+
+kan_status kan_engine_linear_backward(kan_engine* e, int layer, const float* x_dev, int64_t batch,
+                                      const float* dout_dev, float* dcoeffs_dev, float* dinputs_dev, void* stream) {
+  if (!e) return KAN_ERR_INVALID_ARGUMENT;
+  return guarded(e, [&] {
+    Layer& l = e->kan_layer(layer);
+    if (l.type != L_LINEAR) throw Unsupported("linear_backward: linear KAN layers only");
+    if (batch < 0) throw InvalidArgument("linear_backward: negative batch");
+    const int nb = e->grid.nb();
+    if (l.coeffs.size() != static_cast<size_t>(l.n_in) * nb * l.n_out)
+      throw InvalidArgument("coefficients of KAN layer " + std::to_string(layer) + " not set");
+    if (nb > 16 || e->grid.P > 3) throw Unsupported("linear_backward supports G+P <= 16 and degree <= 3");
+    if (batch > 0 && (!x_dev || !dout_dev || !dcoeffs_dev)) throw InvalidArgument("linear_backward: null buffer");
+    DeviceGuard dg(e->device);
+    if (!l.w_bw) {
+      l.w_bw = std::make_shared<DevBuf<float>>();
+      std::vector<float> w32(l.coeffs.begin(), l.coeffs.end());
+      l.w_bw->upload(w32);
+    }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (batch == 0) {  // d_coeffs of an empty batch is zero (train.hpp:95)
+      ck(cudaMemsetAsync(dcoeffs_dev, 0, l.coeffs.size() * sizeof(float), st), "memset");
+      return;
+    }
+    BwParams p{};
+    p.M = batch;
+    p.n_in = l.n_in;
+    p.n_out = l.n_out;
+    p.G = e->grid.G;
+    p.P = e->grid.P;
+    p.x = x_dev;
+    p.ld_x = l.n_in;
+    p.dy = dout_dev;
+    p.w = l.w_bw->p;
+    p.dcoeffs = dcoeffs_dev;
+    p.dinputs = dinputs_dev;
+    p.lo = static_cast<float>(e->grid.lo);
+    p.hi_open = std::nextafter(static_cast<float>(e->grid.hi), static_cast<float>(e->grid.lo));
+    p.inv_delta = static_cast<float>(1.0 / e->grid.delta);
+    ck(launch_linear_backward(p, st), "backward launch");
+  });
+}
+
+kan_status kan_softmax_cross_entropy(const float* logits_dev, const int32_t* labels_dev, int64_t batch, int n,
+                                     float* loss_rows_dev, float* dlogits_dev, void* stream) {
+  if (batch < 0 || n < 1) return KAN_ERR_INVALID_ARGUMENT;
+  if (batch > 0 && (!logits_dev || !labels_dev || !loss_rows_dev || !dlogits_dev)) return KAN_ERR_INVALID_ARGUMENT;
+  const cudaError_t e = launch_softmax_ce(logits_dev, labels_dev, batch, n, loss_rows_dev, dlogits_dev,
+                                          static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? KAN_OK : KAN_ERR_CUDA;
 }
 
 kan_status kan_engine_set_activation_ranges(kan_engine* e, const double* ranges, int n) {

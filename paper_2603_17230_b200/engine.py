@@ -91,6 +91,8 @@ _lib.kan_engine_layer_time_ms.argtypes = [_vp, C.c_int, C.POINTER(C.c_double),
 _lib.kan_engine_layer_timeline.argtypes = [_vp, C.c_int, _vp, C.c_int64]
 _lib.kan_engine_layer_timeline.restype = C.c_int64
 _lib.kan_engine_set_activation_ranges.argtypes = [_vp, _vp, C.c_int]
+_lib.kan_engine_linear_backward.argtypes = [_vp, C.c_int, _vp, C.c_int64, _vp, _vp, _vp, _vp]
+_lib.kan_softmax_cross_entropy.argtypes = [_vp, _vp, C.c_int64, C.c_int, _vp, _vp, _vp]
 _lib.kan_engine_set_spline_tables.argtypes = [_vp, C.c_int, _vp, C.c_int64, C.c_int, C.c_int, _vp, _vp]
 _lib.kan_engine_spline_table.argtypes = [_vp, C.c_int, _vp, C.c_int64, _vp, _vp]
 _lib.kan_engine_spline_table.restype = C.c_int64
@@ -139,6 +141,7 @@ EXPORTED = [
     "kan_container_lut", "kan_container_num_spline_tables", "kan_container_spline_table",
     "kan_container_save", "kan_container_save_error", "kan_crc32", "kan_engine_load",
     "kan_engine_evaluate_accuracy", "kan_engine_set_activation_ranges",
+    "kan_engine_linear_backward", "kan_softmax_cross_entropy",
 ]
 
 
@@ -416,6 +419,22 @@ class Engine:
                                                       C.byref(acc), self._stream(stream)))
         return acc.value
 
+    # -- training (train.hpp) -----------------------------------------------------------
+    def linear_backward(self, layer: int, x, dout, want_inputs: bool = True, stream=None):
+        """kan_linear_backward (train.hpp:84-136) on CUDA fp32 tensors: (dcoeffs
+        [n_in*(G+P), n_out], dinputs [batch, n_in] or None)."""
+        torch = _torch()
+        n_in, n_out = self.layer_shape(layer)
+        nb = self.descriptor["grid"]["intervals"] + self.descriptor["grid"]["degree"]
+        x = x.contiguous()
+        dout = dout.contiguous()
+        dc = torch.empty((n_in * nb, n_out), device=x.device, dtype=torch.float32)
+        di = torch.empty((x.shape[0], n_in), device=x.device, dtype=torch.float32) if want_inputs else None
+        self._check(_lib.kan_engine_linear_backward(self._h, layer, x.data_ptr(), x.shape[0], dout.data_ptr(),
+                                                    dc.data_ptr(), None if di is None else di.data_ptr(),
+                                                    self._stream(stream)))
+        return dc, di
+
     # -- parity probes ---------------------------------------------------------------
     def layer_levels(self, layer: int, x, stream=None):
         torch = _torch()
@@ -541,3 +560,19 @@ def spline_table_forward(acts, tables, G: int = 5, P: int = 3, lo=-1.0, hi=1.0, 
     e.set_spline_tables(0, tables)
     e.configure(EvalOptions(mode="spline-table", lut_k=tables["bits_a"], lut_h=tables["h"]))
     return e.model_forward(acts)
+
+
+def softmax_cross_entropy(logits, labels, stream=None):
+    """softmax_cross_entropy (train.hpp:139-160) on the GPU: (mean loss, dlogits)."""
+    torch = _torch()
+    logits = logits.contiguous()
+    lab = labels.to(device=logits.device, dtype=torch.int32).contiguous()
+    M, n = logits.shape
+    rows = torch.empty(M, device=logits.device, dtype=torch.float32)
+    d = torch.empty_like(logits)
+    s = stream if stream is not None else torch.cuda.current_stream(logits.device)
+    st = _lib.kan_softmax_cross_entropy(logits.data_ptr(), lab.data_ptr(), M, n, rows.data_ptr(), d.data_ptr(),
+                                        C.c_void_p(s.cuda_stream))
+    if st != KAN_OK:
+        raise _STATUS.get(st, RuntimeError)(KanError(st, "softmax_cross_entropy"))
+    return float(rows.double().mean().item()) if M else 0.0, d
