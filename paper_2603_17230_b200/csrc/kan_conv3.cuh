@@ -340,17 +340,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int row = tl.m0 + rloc;
       float rv[32];  // residual prefetch: 32 columns in flight per thread
       const int half = (warp - W_EPI) >> 2;  // the two warps of a lane quarter take alternate 32-column blocks
+      // 32-column blocks (the two warps of a lane quarter alternate), read as
+      // two 16-column TMEM loads: 2 round trips per block instead of 8
 #pragma unroll 1
-      for (int gq = 8 * half; gq < ((p.dbg_flags & 8) ? 0 : BN / 4); gq += ((gq & 7) == 7) ? 9 : 1) {
-        if (p.res_kind && (gq & 7) == 0) {
+      for (int blk = half; blk < ((p.dbg_flags & 8) ? 0 : (BN + 31) / 32); blk += 2) {
+        const int gq0 = blk * 8;
+        if (p.res_kind) {
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
-            const int c = tl.n_tile * BN + (gq + q) * 4;
+            const int c = tl.n_tile * BN + (gq0 + q) * 4;
             float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (row < p.M && c + 3 < p.N && gq + q < BN / 4)
+            if (row < p.M && c + 3 < p.N && gq0 + q < BN / 4)
               v = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(p.res) +
                                                    static_cast<size_t>(row) * p.ld_res + c);
-            else if (row < p.M && gq + q < BN / 4)
+            else if (row < p.M && gq0 + q < BN / 4)
               for (int e = 0; e < 4; ++e)
                 if (c + e < p.N)
                   (&v.x)[e] = reinterpret_cast<const float*>(p.res)[static_cast<size_t>(row) * p.ld_res + c + e];
@@ -360,9 +363,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             rv[4 * q + 3] = v.w;
           }
         }
-        uint32_t ra[4];
-        tmem_ld4(tacc + gq * 4, ra);
+#pragma unroll 1
+        for (int sub = 0; sub < 2; ++sub) {
+        uint32_t r16[16];
+        tmem_ld16(tacc + blk * 32 + sub * 16, r16);
         tmem_wait_ld();
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+        const int q = sub * 4 + q4;
+        const int gq = gq0 + q;
+        if (gq >= BN / 4) break;
+        const uint32_t ra[4] = {r16[4 * q4], r16[4 * q4 + 1], r16[4 * q4 + 2], r16[4 * q4 + 3]};
         const int col0 = tl.n_tile * BN + gq * 4;
         if (row >= p.M) continue;
         const size_t base = static_cast<size_t>(row) * p.ld_out + col0;
@@ -428,6 +439,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             for (int e = 0; e < 4; ++e)
               if (e < nvalid) o[e] = static_cast<uint16_t>(a[e]);
           }
+        }
+        }
         }
       }
       tc_fence_before();
