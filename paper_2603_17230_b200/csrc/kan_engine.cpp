@@ -42,6 +42,10 @@ cudaError_t launch_levels(const float* x, int64_t n, const float* thr, float lo,
 cudaError_t launch_argmax(const float* logits, int64_t M, int N, int ld, int32_t* out,
                           cudaStream_t st);
 cudaError_t launch_fp32_layer(const Fp32Params& p, cudaStream_t st);
+cudaError_t launch_im2col_f32(const float* in, int64_t n_img, int C, int H, int W, int K, int stride, int pad, int Ho,
+                              int Wo, float* out, cudaStream_t st);
+cudaError_t launch_rows_to_nchw(const float* rows, int64_t n_img, int HW, int N, float* out, cudaStream_t st);
+cudaError_t launch_maxpool_f32(const float* in, int64_t planes, int H, int W, int win, float* out, cudaStream_t st);
 cudaError_t launch_small_layer(const SmallParams& p, cudaStream_t st);
 cudaError_t launch_rows_to_levels(const float* x, int64_t M, int n, int ld_x, uint16_t* out, int ld_o,
                                   const float* thr, float nlo_step, float inv_step, int L, cudaStream_t st);
@@ -308,6 +312,7 @@ struct kan_engine {
   DevBuf<uint16_t> xlev;  // level prepass of a large fp32-input dense layer
   DevBuf<uint16_t> xcol;  // level im2col of the model input (stem convs)
   DevBuf<float> logits_tmp;
+  DevBuf<float> fp_col, fp_rows;  // fp32 conv models: patch rows, layer output rows
   // LUT entries read from a .kant container (kan_engine_load): configure uses
   // them when lut_k / lut_h match (EvalOptions::lut, eval.hpp:40)
   std::vector<uint8_t> c_lut;
@@ -1432,9 +1437,9 @@ void configure(kan_engine* e, const kan_config* c) {
     throw Unsupported("the last layer must be a KAN layer");
   if (cfg.mode == KAN_MODE_FP32) {
     for (auto& l : e->layers)
-      if (l.type != L_LINEAR || l.src != static_cast<int>(&l - e->layers.data()) - 1 || l.res_src != -2)
-        throw Unsupported("fp32 mode runs dense layer stacks; conv, pooling and residual layers run "
-                          "on the bf16 and bspline-lut paths");
+      if (l.type == L_AVGPOOL || l.src != static_cast<int>(&l - e->layers.data()) - 1 || l.res_src != -2)
+        throw Unsupported("fp32 mode runs the reference layer set (linear, conv, maxpool, flatten); "
+                          "residual blocks and global pooling run on the bf16 and bspline-lut paths");
   }
   if (lastl.type == L_CONV && cfg.out_kind == KAN_OUT_I8)
     throw InvalidArgument("int8 outputs are produced by linear output layers only");
@@ -2008,6 +2013,59 @@ struct Act {
   const uint16_t* lv = nullptr;  // levels sidecar of an fp32-stored tensor (pitch ld)
 };
 
+// model_forward in fp32 mode over conv / maxpool / flatten stacks
+// (convkan_forward = im2col + kan_linear_forward, layers.hpp:126-190): NCHW
+// fp32 activations, explicit im2col rows through the fp32 Cox-de Boor layer
+// kernel, rows reshaped back to NCHW.
+void forward_fp32_nchw(kan_engine* e, const float* x, int64_t M, void* out, cudaStream_t st) {
+  const int nl = static_cast<int>(e->layers.size());
+  const float* cur = x;
+  int64_t ld = e->input_size();  // dense rows: pitch; images: dense NCHW per sample
+  for (int i = 0; i < nl; ++i) {
+    const Layer& l = e->layers[static_cast<size_t>(i)];
+    const bool last = i + 1 == nl;
+    if (l.type == L_FLATTEN) {
+      ld = static_cast<int64_t>(l.in.c) * l.in.h * l.in.w;
+      continue;
+    }
+    auto dst = [&](size_t elems) -> float* {
+      if (last) return static_cast<float*>(out);
+      auto& b = e->slots[static_cast<size_t>(e->slot_of[static_cast<size_t>(i)])].main;
+      b.alloc(elems * sizeof(float));
+      return reinterpret_cast<float*>(b.p);
+    };
+    if (l.type == L_MAXPOOL) {
+      const int64_t planes = M * l.in.c;
+      float* o = dst(static_cast<size_t>(planes) * l.out.h * l.out.w);
+      ck(launch_maxpool_f32(cur, planes, l.in.h, l.in.w, l.window, o, st), "maxpool launch");
+      e->last_launches += 1;
+      cur = o;
+      continue;
+    }
+    PreparedLayer& pl = e->prep[static_cast<size_t>(l.kan_index)];
+    if (l.type == L_LINEAR) {
+      float* o = dst(static_cast<size_t>(M) * pl.N);
+      run_fp32_layer(e, pl, M, cur, ld, o, pl.N, st);
+      cur = o;
+      ld = pl.N;
+      continue;
+    }
+    // conv: patch rows, the dense layer, NCHW output
+    const int hw = l.out.h * l.out.w;
+    const int64_t rows = M * hw;
+    e->fp_col.alloc(static_cast<size_t>(rows) * pl.n_in);
+    ck(launch_im2col_f32(cur, M, l.c_in, l.in.h, l.in.w, l.kernel, l.stride, l.padding, l.out.h, l.out.w,
+                         e->fp_col.p, st),
+       "im2col launch");
+    e->fp_rows.alloc(static_cast<size_t>(rows) * pl.N);
+    run_fp32_layer(e, pl, rows, e->fp_col.p, pl.n_in, e->fp_rows.p, pl.N, st);
+    float* o = dst(static_cast<size_t>(rows) * pl.N);
+    ck(launch_rows_to_nchw(e->fp_rows.p, M, hw, pl.N, o, st), "reshape launch");
+    e->last_launches += 2;
+    cur = o;
+  }
+}
+
 // model_forward (eval.hpp:200-253): run the layer graph on the caller's stream.
 // KAN layers are one fused gather-GEMM launch each; pooling layers are small
 // elementwise kernels; flatten is a view (the consuming linear layer's
@@ -2024,6 +2082,14 @@ void forward(kan_engine* e, const float* x, int64_t M, void* out, cudaStream_t s
   }
   const bool lut = e->cfg.mode == KAN_MODE_BSPLINE_LUT;
   const bool fp32 = e->cfg.mode == KAN_MODE_FP32;
+  if (fp32) {
+    bool dense = true;
+    for (const auto& l : e->layers) dense = dense && l.type == L_LINEAR;
+    if (!dense || e->input_shape.size() == 3) {
+      forward_fp32_nchw(e, x, M, out, st);
+      return;
+    }
+  }
   const int esz = act_esz(e);
   // the model input: dense rows need a 16-byte pitch for TMA
   Act in;

@@ -158,3 +158,89 @@ cudaError_t launch_fp32_layer(const Fp32Params& p, cudaStream_t st) {
 }
 
 }  // namespace kan
+
+// ---------------------------------------------------------------------------
+// fp32 conv models (EvalMode::kFp32 on conv / maxpool / flatten stacks): the
+// reference's convkan_forward = im2col (layers.hpp:126-154) + the dense layer
+// on the patch rows, NCHW activations throughout (flatten is a view).
+namespace kan {
+
+// rows [n_img*Ho*Wo][C*K*K], column c*K*K + ky*K + kx; out-of-image taps 0.0
+__global__ void __launch_bounds__(256) kan_im2col_f32_kernel(const float* __restrict__ in, int64_t n_img, int C,
+                                                             int H, int W, int K, int stride, int pad, int Ho,
+                                                             int Wo, float* __restrict__ out) {
+  const int ncol = C * K * K;
+  const int64_t total = n_img * Ho * Wo * static_cast<int64_t>(ncol);
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int col = static_cast<int>(t % ncol);
+    const int64_t rowi = t / ncol;
+    const int ox = static_cast<int>(rowi % Wo);
+    const int oy = static_cast<int>((rowi / Wo) % Ho);
+    const int64_t img = rowi / (static_cast<int64_t>(Wo) * Ho);
+    const int c = col / (K * K), kk = col % (K * K), ky = kk / K, kx = kk % K;
+    const int iy = oy * stride + ky - pad, ix = ox * stride + kx - pad;
+    out[t] = (iy >= 0 && iy < H && ix >= 0 && ix < W) ? in[((img * C + c) * H + iy) * W + ix] : 0.f;
+  }
+}
+
+// rows [n_img*HW][N] -> NCHW [n_img][N][HW] (convkan_forward's reshape, layers.hpp:179-184)
+__global__ void __launch_bounds__(256) kan_rows_to_nchw_kernel(const float* __restrict__ rows, int64_t n_img,
+                                                               int HW, int N, float* __restrict__ out) {
+  const int64_t total = n_img * HW * static_cast<int64_t>(N);
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int p = static_cast<int>(t % HW);
+    const int64_t q = t / HW;
+    const int j = static_cast<int>(q % N);
+    const int64_t img = q / N;
+    out[t] = rows[(img * HW + p) * N + j];
+  }
+}
+
+// maxpool2 (layers.hpp:193-205) on NCHW fp32 planes
+__global__ void __launch_bounds__(256) kan_maxpool_f32_kernel(const float* __restrict__ in, int64_t planes, int H,
+                                                              int W, int win, float* __restrict__ out) {
+  const int Ho = H / win, Wo = W / win;
+  const int64_t total = planes * Ho * Wo;
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t pl = t / (Ho * Wo);
+    const int q = static_cast<int>(t % (Ho * Wo));
+    const int oy = q / Wo, ox = q % Wo;
+    const float* src = in + pl * H * W + static_cast<int64_t>(oy * win) * W + ox * win;
+    float m = src[0];
+    for (int dy = 0; dy < win; ++dy)
+      for (int dx = 0; dx < win; ++dx) m = fmaxf(m, src[dy * W + dx]);
+    out[t] = m;
+  }
+}
+
+static unsigned fp_blocks(int64_t n) {
+  const int64_t b = (n + 255) / 256;
+  return static_cast<unsigned>(b < 148 * 32 ? b : 148 * 32);
+}
+
+cudaError_t launch_im2col_f32(const float* in, int64_t n_img, int C, int H, int W, int K, int stride, int pad, int Ho,
+                              int Wo, float* out, cudaStream_t st) {
+  const int64_t n = n_img * Ho * Wo * static_cast<int64_t>(C) * K * K;
+  if (n == 0) return cudaSuccess;
+  kan_im2col_f32_kernel<<<fp_blocks(n), 256, 0, st>>>(in, n_img, C, H, W, K, stride, pad, Ho, Wo, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rows_to_nchw(const float* rows, int64_t n_img, int HW, int N, float* out, cudaStream_t st) {
+  const int64_t n = n_img * HW * static_cast<int64_t>(N);
+  if (n == 0) return cudaSuccess;
+  kan_rows_to_nchw_kernel<<<fp_blocks(n), 256, 0, st>>>(rows, n_img, HW, N, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_maxpool_f32(const float* in, int64_t planes, int H, int W, int win, float* out, cudaStream_t st) {
+  const int64_t n = planes * (H / win) * (W / win);
+  if (n == 0) return cudaSuccess;
+  kan_maxpool_f32_kernel<<<fp_blocks(n), 256, 0, st>>>(in, planes, H, W, win, out);
+  return cudaGetLastError();
+}
+
+}  // namespace kan

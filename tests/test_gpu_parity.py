@@ -320,3 +320,40 @@ def test_level_prepass_matches_in_kernel_levels(oracle):
     np.testing.assert_array_equal(y0, y1)
     yo = oracle_int_model(oracle, G, 8, 8, W_PER_CHANNEL_SYM, 8, Ws, Bs, x)[-1]
     np.testing.assert_array_equal(y1, yo.astype(np.float32))
+
+
+@pytest.mark.parametrize("name", ["lekan", "cnn3"])
+def test_fp32_conv_models_match_reference(ref, name):
+    """EvalMode::kFp32 on the reference's conv descriptors (convkan_forward with
+    RecursiveBasis, maxpool2, flatten): fp32 im2col rows through the fp32
+    Cox-de Boor kernel, within the fp32 bar."""
+    import json as _json
+    desc = {"lekan": {"name": "LeKAN", "grid": {"intervals": 3, "degree": 3}, "input": [1, 28, 28],
+                      "layers": [{"type": "conv", "c_in": 1, "c_out": 6, "kernel": 5, "stride": 1, "padding": 0},
+                                 {"type": "maxpool", "window": 2},
+                                 {"type": "conv", "c_in": 6, "c_out": 16, "kernel": 5, "stride": 1, "padding": 2},
+                                 {"type": "maxpool", "window": 2}, {"type": "flatten"},
+                                 {"type": "linear", "n_in": 576, "n_out": 10}]},
+            "cnn3": {"name": "c", "grid": {"intervals": 5, "degree": 3}, "input": [3, 17, 17],
+                     "layers": [{"type": "conv", "c_in": 3, "c_out": 8, "kernel": 3, "stride": 1, "padding": 1},
+                                {"type": "conv", "c_in": 8, "c_out": 12, "kernel": 3, "stride": 2, "padding": 1},
+                                {"type": "maxpool", "window": 2}, {"type": "flatten"},
+                                {"type": "linear", "n_in": 192, "n_out": 10}]}}[name]
+    nb = desc["grid"]["intervals"] + desc["grid"]["degree"]
+    rng = np.random.default_rng(7)
+    Ws = []
+    for l in desc["layers"]:
+        if l["type"] == "conv":
+            Ws.append(rng.normal(0, 0.1, (l["c_in"] * l["kernel"] ** 2 * nb, l["c_out"])))
+        elif l["type"] == "linear":
+            Ws.append(rng.normal(0, 0.1, (l["n_in"] * nb, l["n_out"])))
+    e = Engine(desc, 0)
+    for i, w in enumerate(Ws):
+        e.set_coeffs(i, w)
+    e.configure(EvalOptions(mode="fp32"))
+    D = int(np.prod(desc["input"]))
+    x = rng.uniform(-1, 1, (9, D)).astype(np.float32)
+    y = e.model_forward(torch.from_numpy(x).cuda()).cpu().numpy().astype(np.float64)
+    r = ref.model_forward(_json.dumps(desc), Ws, x.astype(np.float64), 10, mode=0)
+    assert np.linalg.norm(y - r) / np.linalg.norm(r) < FP32_TOL
+    assert np.array_equal(e.predict(torch.from_numpy(x).cuda()).cpu().numpy(), r.argmax(1))
