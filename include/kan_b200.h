@@ -170,6 +170,19 @@ kan_status kan_engine_layer_accumulators(kan_engine* e, int layer, const uint16_
 kan_status kan_engine_linear_backward(kan_engine* e, int layer, const float* x_dev, int64_t batch,
                                       const float* dout_dev, float* dcoeffs_dev, float* dinputs_dev,
                                       void* stream);
+/* conv layer backward (train.hpp:367-399): x [batch, c_in, H, W] (NCHW, the
+ * layer's input), dout [batch, c_out, Ho, Wo] -> dcoeffs [c_in*K*K*(G+P), c_out]
+ * and, if dinputs is not NULL, dinputs [batch, c_in, H, W] (col2im_add of the
+ * patch gradients). */
+kan_status kan_engine_conv_backward(kan_engine* e, int layer, const float* x_dev, int64_t batch,
+                                    const float* dout_dev, float* dcoeffs_dev, float* dinputs_dev, void* stream);
+/* maxpool2 (layers.hpp:193-205) forward and its backward (train.hpp:407-431:
+ * the gradient goes to the first strict maximum of each window) on NCHW fp32
+ * planes [planes, H, W]. */
+kan_status kan_maxpool2_f32(const float* in_dev, int64_t planes, int H, int W, int window, float* out_dev,
+                            void* stream);
+kan_status kan_maxpool2_backward_f32(const float* in_dev, int64_t planes, int H, int W, int window,
+                                     const float* dout_dev, float* din_dev, void* stream);
 /* softmax_cross_entropy (train.hpp:139-160): per-row loss [batch] (the mean is
  * their average) and dL/dlogits [batch, n] = (softmax - onehot) / batch. */
 kan_status kan_softmax_cross_entropy(const float* logits_dev, const int32_t* labels_dev, int64_t batch, int n,

@@ -595,6 +595,9 @@ class Ref:
                                                        C.c_int, _dp, C.c_int64, C.c_int64, _dp, C.c_int64, _dp]
         L.ref_linear_backward.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_int64, C.c_int,
                                           C.c_int, _dp, _dp, _dp, _dp, _dp]
+        L.ref_train.argtypes = [C.c_char_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.c_int64, C.c_int64,
+                                _dp, _i32p, C.c_double, C.c_double, C.c_int, C.c_int, C.c_uint64,
+                                C.POINTER(C.c_double)]
         L.ref_softmax_ce.argtypes = [C.c_int64, C.c_int, _dp, _i32p, _dp, C.POINTER(C.c_double)]
         L.ref_model_forward.argtypes = [C.c_char_p, C.POINTER(C.c_void_p), C.c_int, C.c_int,
                                         C.c_int, C.c_int, C.c_int64, C.c_int64, _dp, C.c_int64,
@@ -792,6 +795,20 @@ class Ref:
                                         coeffs, dout, dc, di):
             raise ValueError(self.err())
         return dc, di
+
+    def train(self, text, coeffs, inputs, labels, lr, momentum, epochs, batch, seed=0):
+        """train (train.hpp:247-462): (updated coefficients, last epoch loss)."""
+        inputs = np.ascontiguousarray(inputs, dtype=np.float64)
+        labels = np.ascontiguousarray(labels, dtype=np.int32)
+        cs = [np.ascontiguousarray(c, dtype=np.float64) for c in coeffs]
+        outs = [np.zeros_like(c) for c in cs]
+        pin = (C.c_void_p * len(cs))(*[c.ctypes.data for c in cs])
+        pout = (C.c_void_p * len(outs))(*[o.ctypes.data for o in outs])
+        loss = C.c_double()
+        if self.lib.ref_train(text.encode(), pin, pout, inputs.shape[0], inputs.shape[1], inputs, labels, lr,
+                              momentum, epochs, batch, seed, C.byref(loss)):
+            raise ValueError(self.err())
+        return outs, loss.value
 
     def softmax_ce(self, logits, labels):
         logits = np.ascontiguousarray(logits, dtype=np.float64)

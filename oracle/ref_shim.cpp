@@ -545,6 +545,48 @@ int ref_softmax_ce(int64_t M, int n, const double* logits, const int32_t* labels
   return fail(e);
 }
 
+// train (train.hpp:247-462) of a descriptor-built model on (inputs, labels):
+// SGD with momentum, `epochs` epochs of `batch` rows; coefficients updated in
+// place in coeff_out (same layout as coeff_ptrs); returns the last epoch loss
+// in *loss
+int ref_train(const char* json_text, const double* const* coeff_ptrs, double* const* coeff_out, int64_t M,
+              int64_t D, const double* inputs, const int32_t* labels, double lr, double momentum, int epochs,
+              int batch, uint64_t seed, double* loss) try {
+  Model model = model_from_descriptor(nlohmann::json::parse(json_text));
+  int li = 0;
+  for (auto& layer : model.layers) {
+    if (auto* lin = std::get_if<KanLinearLayer>(&layer)) {
+      std::copy(coeff_ptrs[li], coeff_ptrs[li] + lin->coeffs.size(), lin->coeffs.flat().begin());
+      ++li;
+    } else if (auto* conv = std::get_if<ConvKanLayer>(&layer)) {
+      std::copy(coeff_ptrs[li], coeff_ptrs[li] + conv->coeffs.size(), conv->coeffs.flat().begin());
+      ++li;
+    }
+  }
+  Dataset ds;
+  ds.inputs = make_matrix(M, D, inputs);
+  ds.labels.assign(labels, labels + M);
+  TrainConfig cfg;
+  cfg.lr = lr;
+  cfg.momentum = momentum;
+  cfg.epochs = epochs;
+  cfg.batch = batch;
+  cfg.seed = seed;
+  const TrainResult r = train(model, ds, cfg);
+  *loss = r.epoch_losses.empty() ? 0.0 : r.epoch_losses.back();
+  li = 0;
+  for (auto& layer : model.layers) {
+    if (auto* lin = std::get_if<KanLinearLayer>(&layer)) {
+      std::copy(lin->coeffs.flat().begin(), lin->coeffs.flat().end(), coeff_out[li++]);
+    } else if (auto* conv = std::get_if<ConvKanLayer>(&layer)) {
+      std::copy(conv->coeffs.flat().begin(), conv->coeffs.flat().end(), coeff_out[li++]);
+    }
+  }
+  return 0;
+} catch (const std::exception& e) {
+  return fail(e);
+}
+
 // Harness composition for descriptors the reference cannot express (the
 // engine's additive extension: named tensors id / input_from / residual,
 // global_avgpool, "conv_output": "floor"), built ONLY from reference

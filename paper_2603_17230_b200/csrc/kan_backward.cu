@@ -162,3 +162,112 @@ cudaError_t launch_softmax_ce(const float* logits, const int32_t* labels, int64_
 }
 
 }  // namespace kan
+
+// ---------------------------------------------------------------------------
+// conv / pooling backward (train.hpp:367-431)
+namespace kan {
+
+// NCHW [n_img][N][HW] -> rows [n_img*HW][N]
+__global__ void __launch_bounds__(256) kan_nchw_to_rows_kernel(const float* __restrict__ in, int64_t n_img, int HW,
+                                                               int N, float* __restrict__ rows) {
+  const int64_t total = n_img * HW * static_cast<int64_t>(N);
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int j = static_cast<int>(t % N);
+    const int64_t r = t / N;
+    const int p = static_cast<int>(r % HW);
+    const int64_t img = r / HW;
+    rows[t] = in[(img * N + j) * HW + p];
+  }
+}
+
+// col2im_add (train.hpp:221-243) as a gather: every input pixel sums the
+// patch-gradient entries that read it (deterministic, no atomics)
+__global__ void __launch_bounds__(256) kan_col2im_kernel(const float* __restrict__ dpatch, int64_t n_img, int C,
+                                                         int H, int W, int K, int stride, int pad, int Ho, int Wo,
+                                                         float* __restrict__ din) {
+  const int64_t total = n_img * C * static_cast<int64_t>(H) * W;
+  const int ncol = C * K * K;
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int ix = static_cast<int>(t % W);
+    const int iy = static_cast<int>((t / W) % H);
+    const int c = static_cast<int>((t / (static_cast<int64_t>(W) * H)) % C);
+    const int64_t img = t / (static_cast<int64_t>(W) * H * C);
+    float acc = 0.f;
+    for (int ky = 0; ky < K; ++ky) {
+      const int ny = iy + pad - ky;
+      if (ny < 0 || ny % stride) continue;
+      const int oy = ny / stride;
+      if (oy >= Ho) continue;
+      for (int kx = 0; kx < K; ++kx) {
+        const int nx = ix + pad - kx;
+        if (nx < 0 || nx % stride) continue;
+        const int ox = nx / stride;
+        if (ox >= Wo) continue;
+        acc += dpatch[((img * Ho + oy) * Wo + ox) * ncol + (c * K + ky) * K + kx];
+      }
+    }
+    din[t] = acc;
+  }
+}
+
+// maxpool2 backward (train.hpp:407-431): each output's gradient goes to the
+// first strict maximum of its window (row-major scan); windows do not overlap
+__global__ void __launch_bounds__(256) kan_maxpool_bw_kernel(const float* __restrict__ in, int64_t planes, int H,
+                                                             int W, int win, const float* __restrict__ dout,
+                                                             float* __restrict__ din) {
+  const int Ho = H / win, Wo = W / win;
+  const int64_t total = planes * Ho * Wo;
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t pl = t / (Ho * Wo);
+    const int q = static_cast<int>(t % (Ho * Wo));
+    const int y = q / Wo, x = q % Wo;
+    const float* src = in + pl * H * W;
+    int by = y * win, bx = x * win;
+    float best = src[by * W + bx];
+    for (int dy = 0; dy < win; ++dy)
+      for (int dx = 0; dx < win; ++dx) {
+        const float v = src[(y * win + dy) * W + x * win + dx];
+        if (v > best) {
+          best = v;
+          by = y * win + dy;
+          bx = x * win + dx;
+        }
+      }
+    din[pl * H * W + by * W + bx] = dout[t];  // din zeroed by the launcher
+  }
+}
+
+static unsigned bw_blocks(int64_t n) {
+  const int64_t b = (n + 255) / 256;
+  return static_cast<unsigned>(b < 148 * 32 ? b : 148 * 32);
+}
+
+cudaError_t launch_nchw_to_rows(const float* in, int64_t n_img, int HW, int N, float* rows, cudaStream_t st) {
+  const int64_t n = n_img * HW * static_cast<int64_t>(N);
+  if (n == 0) return cudaSuccess;
+  kan_nchw_to_rows_kernel<<<bw_blocks(n), 256, 0, st>>>(in, n_img, HW, N, rows);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_col2im(const float* dpatch, int64_t n_img, int C, int H, int W, int K, int stride, int pad, int Ho,
+                          int Wo, float* din, cudaStream_t st) {
+  const int64_t n = n_img * C * static_cast<int64_t>(H) * W;
+  if (n == 0) return cudaSuccess;
+  kan_col2im_kernel<<<bw_blocks(n), 256, 0, st>>>(dpatch, n_img, C, H, W, K, stride, pad, Ho, Wo, din);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_maxpool_bw(const float* in, int64_t planes, int H, int W, int win, const float* dout, float* din,
+                              cudaStream_t st) {
+  const int64_t n_in = planes * H * static_cast<int64_t>(W);
+  cudaError_t e = cudaMemsetAsync(din, 0, static_cast<size_t>(n_in) * sizeof(float), st);
+  const int64_t n = planes * (H / win) * (W / win);
+  if (e != cudaSuccess || n == 0) return e;
+  kan_maxpool_bw_kernel<<<bw_blocks(n), 256, 0, st>>>(in, planes, H, W, win, dout, din);
+  return cudaGetLastError();
+}
+
+}  // namespace kan

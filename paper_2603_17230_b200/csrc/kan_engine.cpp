@@ -77,6 +77,11 @@ struct BwParams {
 cudaError_t launch_linear_backward(const BwParams& p, cudaStream_t st);
 cudaError_t launch_softmax_ce(const float* logits, const int32_t* labels, int64_t M, int n, float* loss_rows,
                               float* dlogits, cudaStream_t st);
+cudaError_t launch_nchw_to_rows(const float* in, int64_t n_img, int HW, int N, float* rows, cudaStream_t st);
+cudaError_t launch_col2im(const float* dpatch, int64_t n_img, int C, int H, int W, int K, int stride, int pad, int Ho,
+                          int Wo, float* din, cudaStream_t st);
+cudaError_t launch_maxpool_bw(const float* in, int64_t planes, int H, int W, int win, const float* dout, float* din,
+                              cudaStream_t st);
 // spline-table mode (kan_spline_table.cu)
 cudaError_t launch_st_sample(const double* basis, const double* coeffs, int n_in, int n_out, int nb, int Lv,
                              int pass, unsigned long long* mm, uint8_t* T, int Np, double s, double zd,
@@ -313,6 +318,7 @@ struct kan_engine {
   DevBuf<uint16_t> xcol;  // level im2col of the model input (stem convs)
   DevBuf<float> logits_tmp;
   DevBuf<float> fp_col, fp_rows;  // fp32 conv models: patch rows, layer output rows
+  DevBuf<float> bw_drows, bw_dpatch;  // conv backward: dY rows, patch gradients
   // LUT entries read from a .kant container (kan_engine_load): configure uses
   // them when lut_k / lut_h match (EvalOptions::lut, eval.hpp:40)
   std::vector<uint8_t> c_lut;
@@ -2680,6 +2686,82 @@ kan_status kan_engine_linear_backward(kan_engine* e, int layer, const float* x_d
     p.inv_delta = static_cast<float>(1.0 / e->grid.delta);
     ck(launch_linear_backward(p, st), "backward launch");
   });
+}
+
+kan_status kan_engine_conv_backward(kan_engine* e, int layer, const float* x_dev, int64_t batch,
+                                    const float* dout_dev, float* dcoeffs_dev, float* dinputs_dev, void* stream) {
+  if (!e) return KAN_ERR_INVALID_ARGUMENT;
+  return guarded(e, [&] {
+    Layer& l = e->kan_layer(layer);
+    if (l.type != L_CONV) throw Unsupported("conv_backward: conv KAN layers only");
+    if (batch < 0) throw InvalidArgument("conv_backward: negative batch");
+    const int nb = e->grid.nb();
+    const int n_in = l.kernel * l.kernel * l.c_in;
+    if (l.coeffs.size() != static_cast<size_t>(n_in) * nb * l.c_out)
+      throw InvalidArgument("coefficients of KAN layer " + std::to_string(layer) + " not set");
+    if (nb > 16 || e->grid.P > 3) throw Unsupported("conv_backward supports G+P <= 16 and degree <= 3");
+    if (batch > 0 && (!x_dev || !dout_dev || !dcoeffs_dev)) throw InvalidArgument("conv_backward: null buffer");
+    DeviceGuard dg(e->device);
+    if (!l.w_bw) {
+      l.w_bw = std::make_shared<DevBuf<float>>();
+      std::vector<float> w32(l.coeffs.begin(), l.coeffs.end());
+      l.w_bw->upload(w32);
+    }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (batch == 0) {
+      ck(cudaMemsetAsync(dcoeffs_dev, 0, l.coeffs.size() * sizeof(float), st), "memset");
+      return;
+    }
+    // the reference's conv backward: im2col patches of the input, the linear
+    // backward on the patch rows, col2im_add of the patch gradients
+    // (train.hpp:367-399)
+    const int hw = l.out.h * l.out.w;
+    const int64_t rows = batch * hw;
+    e->fp_col.alloc(static_cast<size_t>(rows) * n_in);
+    ck(launch_im2col_f32(x_dev, batch, l.c_in, l.in.h, l.in.w, l.kernel, l.stride, l.padding, l.out.h, l.out.w,
+                         e->fp_col.p, st),
+       "im2col launch");
+    e->bw_drows.alloc(static_cast<size_t>(rows) * l.c_out);
+    ck(launch_nchw_to_rows(dout_dev, batch, hw, l.c_out, e->bw_drows.p, st), "gradient rows");
+    if (dinputs_dev) e->bw_dpatch.alloc(static_cast<size_t>(rows) * n_in);
+    BwParams p{};
+    p.M = rows;
+    p.n_in = n_in;
+    p.n_out = l.c_out;
+    p.G = e->grid.G;
+    p.P = e->grid.P;
+    p.x = e->fp_col.p;
+    p.ld_x = n_in;
+    p.dy = e->bw_drows.p;
+    p.w = l.w_bw->p;
+    p.dcoeffs = dcoeffs_dev;
+    p.dinputs = dinputs_dev ? e->bw_dpatch.p : nullptr;
+    p.lo = static_cast<float>(e->grid.lo);
+    p.hi_open = std::nextafter(static_cast<float>(e->grid.hi), static_cast<float>(e->grid.lo));
+    p.inv_delta = static_cast<float>(1.0 / e->grid.delta);
+    ck(launch_linear_backward(p, st), "backward launch");
+    if (dinputs_dev)
+      ck(launch_col2im(e->bw_dpatch.p, batch, l.c_in, l.in.h, l.in.w, l.kernel, l.stride, l.padding, l.out.h,
+                       l.out.w, dinputs_dev, st),
+         "col2im launch");
+  });
+}
+
+kan_status kan_maxpool2_f32(const float* in_dev, int64_t planes, int H, int W, int window, float* out_dev,
+                            void* stream) {
+  if (planes < 0 || window < 1 || H < window || W < window) return KAN_ERR_INVALID_ARGUMENT;
+  return launch_maxpool_f32(in_dev, planes, H, W, window, out_dev, static_cast<cudaStream_t>(stream)) == cudaSuccess
+             ? KAN_OK
+             : KAN_ERR_CUDA;
+}
+
+kan_status kan_maxpool2_backward_f32(const float* in_dev, int64_t planes, int H, int W, int window,
+                                     const float* dout_dev, float* din_dev, void* stream) {
+  if (planes < 0 || window < 1 || H < window || W < window) return KAN_ERR_INVALID_ARGUMENT;
+  return launch_maxpool_bw(in_dev, planes, H, W, window, dout_dev, din_dev, static_cast<cudaStream_t>(stream)) ==
+                 cudaSuccess
+             ? KAN_OK
+             : KAN_ERR_CUDA;
 }
 
 kan_status kan_softmax_cross_entropy(const float* logits_dev, const int32_t* labels_dev, int64_t batch, int n,

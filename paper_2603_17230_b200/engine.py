@@ -93,6 +93,9 @@ _lib.kan_engine_layer_timeline.restype = C.c_int64
 _lib.kan_engine_set_activation_ranges.argtypes = [_vp, _vp, C.c_int]
 _lib.kan_engine_linear_backward.argtypes = [_vp, C.c_int, _vp, C.c_int64, _vp, _vp, _vp, _vp]
 _lib.kan_softmax_cross_entropy.argtypes = [_vp, _vp, C.c_int64, C.c_int, _vp, _vp, _vp]
+_lib.kan_engine_conv_backward.argtypes = [_vp, C.c_int, _vp, C.c_int64, _vp, _vp, _vp, _vp]
+_lib.kan_maxpool2_f32.argtypes = [_vp, C.c_int64, C.c_int, C.c_int, C.c_int, _vp, _vp]
+_lib.kan_maxpool2_backward_f32.argtypes = [_vp, C.c_int64, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp]
 _lib.kan_engine_set_spline_tables.argtypes = [_vp, C.c_int, _vp, C.c_int64, C.c_int, C.c_int, _vp, _vp]
 _lib.kan_engine_spline_table.argtypes = [_vp, C.c_int, _vp, C.c_int64, _vp, _vp]
 _lib.kan_engine_spline_table.restype = C.c_int64
@@ -141,7 +144,8 @@ EXPORTED = [
     "kan_container_lut", "kan_container_num_spline_tables", "kan_container_spline_table",
     "kan_container_save", "kan_container_save_error", "kan_crc32", "kan_engine_load",
     "kan_engine_evaluate_accuracy", "kan_engine_set_activation_ranges",
-    "kan_engine_linear_backward", "kan_softmax_cross_entropy",
+    "kan_engine_linear_backward", "kan_softmax_cross_entropy", "kan_engine_conv_backward",
+    "kan_maxpool2_f32", "kan_maxpool2_backward_f32",
 ]
 
 
@@ -435,6 +439,22 @@ class Engine:
                                                     self._stream(stream)))
         return dc, di
 
+    def conv_backward(self, layer: int, x, dout, want_inputs: bool = True, stream=None):
+        """The conv-layer backward of train() (train.hpp:367-399): x [batch, c_in, H, W]
+        and dout [batch, c_out, Ho, Wo] as contiguous CUDA fp32 tensors (any 2-D view);
+        returns (dcoeffs [c_in*K*K*(G+P), c_out], dinputs shaped like x or None)."""
+        torch = _torch()
+        n_in, n_out = self.layer_shape(layer)
+        nb = self.descriptor["grid"]["intervals"] + self.descriptor["grid"]["degree"]
+        x = x.contiguous()
+        dout = dout.contiguous()
+        dc = torch.empty((n_in * nb, n_out), device=x.device, dtype=torch.float32)
+        di = torch.empty_like(x) if want_inputs else None
+        self._check(_lib.kan_engine_conv_backward(self._h, layer, x.data_ptr(), x.shape[0], dout.data_ptr(),
+                                                  dc.data_ptr(), None if di is None else di.data_ptr(),
+                                                  self._stream(stream)))
+        return dc, di
+
     # -- parity probes ---------------------------------------------------------------
     def layer_levels(self, layer: int, x, stream=None):
         torch = _torch()
@@ -576,3 +596,30 @@ def softmax_cross_entropy(logits, labels, stream=None):
     if st != KAN_OK:
         raise _STATUS.get(st, RuntimeError)(KanError(st, "softmax_cross_entropy"))
     return float(rows.double().mean().item()) if M else 0.0, d
+
+
+def maxpool2(x, channels: int, H: int, W: int, window: int = 2, stream=None):
+    """maxpool2 (layers.hpp:193-205) on NCHW fp32 rows [batch, C*H*W] -> [batch, C*Ho*Wo]."""
+    torch = _torch()
+    x = x.contiguous()
+    M = x.shape[0]
+    out = torch.empty((M, channels * (H // window) * (W // window)), device=x.device, dtype=torch.float32)
+    s = stream if stream is not None else torch.cuda.current_stream(x.device)
+    st = _lib.kan_maxpool2_f32(x.data_ptr(), M * channels, H, W, window, out.data_ptr(), C.c_void_p(s.cuda_stream))
+    if st != KAN_OK:
+        raise _STATUS.get(st, RuntimeError)(KanError(st, "maxpool2"))
+    return out
+
+
+def maxpool2_backward(x, dout, channels: int, H: int, W: int, window: int = 2, stream=None):
+    """The pooling backward of train() (train.hpp:407-431)."""
+    torch = _torch()
+    x = x.contiguous()
+    dout = dout.contiguous()
+    din = torch.empty_like(x)
+    s = stream if stream is not None else torch.cuda.current_stream(x.device)
+    st = _lib.kan_maxpool2_backward_f32(x.data_ptr(), x.shape[0] * channels, H, W, window, dout.data_ptr(),
+                                        din.data_ptr(), C.c_void_p(s.cuda_stream))
+    if st != KAN_OK:
+        raise _STATUS.get(st, RuntimeError)(KanError(st, "maxpool2_backward"))
+    return din

@@ -1,23 +1,25 @@
-"""GPU training of KAN MLPs, mirroring the reference's train() for linear
-stacks (train.hpp:162-410): minibatch SGD with momentum on softmax
-cross-entropy.
+"""GPU training of KAN models, mirroring the reference's train()
+(train.hpp:162-462): minibatch SGD with momentum on softmax cross-entropy,
+over the reference layer set (linear, conv, maxpool, flatten).
 
-Forward: each layer is its own fp32 engine (the Cox-de Boor datapath), so the
-layer inputs the backward needs stay on the device.  Backward:
-kan_engine_linear_backward per layer (d_coeffs, d_inputs; the bottom layer
-skips d_inputs, train.hpp:358), softmax_cross_entropy on the GPU.  Update
-(train.hpp:361-366): v = momentum * v - lr * g; w += v, applied in fp64 on
-the host copy and pushed back with set_coeffs (one upload per layer per step).
-Conv layers (train.hpp:367-400, col2im) are not covered.
+Forward: each KAN layer is its own fp32 engine (the Cox-de Boor datapath; conv
+layers through fp32 im2col rows), maxpool2 a GPU kernel, flatten a view; the
+layer inputs the backward needs stay on the device.  Backward, last layer
+first: kan_engine_linear_backward / kan_engine_conv_backward (d_coeffs,
+d_inputs; the bottom layer skips d_inputs, train.hpp:358, 392), the pooling
+backward (train.hpp:407-431), softmax_cross_entropy on the GPU.  Update
+(train.hpp:361-366, 401-404): v = momentum * v - lr * g; w += v, in fp64 on
+the host copy, pushed back with set_coeffs (one upload per layer per step).
 """
 from __future__ import annotations
 
 from dataclasses import dataclass
-from typing import List, Optional
+from typing import List
 
 import numpy as np
 
-from .engine import Engine, EvalOptions, softmax_cross_entropy
+from . import configs as _configs
+from .engine import Engine, EvalOptions, maxpool2, maxpool2_backward, softmax_cross_entropy
 
 
 @dataclass
@@ -29,42 +31,76 @@ class TrainConfig:
     seed: int = 0
 
 
-class MlpTrainer:
+class Trainer:
     def __init__(self, descriptor: dict, coeffs: List[np.ndarray], cfg: TrainConfig, device: int = 0):
-        if any(l["type"] != "linear" for l in descriptor["layers"]):
-            raise NotImplementedError("MlpTrainer trains linear KAN stacks (no conv / pooling)")
+        for l in descriptor["layers"]:
+            if l["type"] not in ("linear", "conv", "maxpool", "flatten") or \
+                    {"id", "input_from", "residual"} & set(l):
+                raise NotImplementedError("train() covers the reference layer set (linear, conv, maxpool, flatten)")
         self.cfg = cfg
         self.desc = descriptor
+        self.shapes = _configs.walk_shapes(descriptor)
         self.coeffs = [np.array(c, dtype=np.float64) for c in coeffs]
         self.vel = [np.zeros_like(c) for c in self.coeffs]
-        g = descriptor["grid"]
-        self.engines = []
-        for l, c in zip(descriptor["layers"], self.coeffs):
-            d = {"name": "layer", "grid": g, "input": [l["n_in"]], "layers": [l]}
-            if "domain" in descriptor:
-                d["domain"] = descriptor["domain"]
-            e = Engine(d, device)
-            e.set_coeffs(0, c)
-            e.configure(EvalOptions(mode="fp32"))
-            self.engines.append(e)
+        self.engines = []  # per layer: an fp32 single-layer engine, or None
+        ki = 0
+        for s in self.shapes:
+            if s["type"] in ("linear", "conv"):
+                d = {"name": "layer", "grid": descriptor["grid"], "input": list(s["in"]), "layers": [s["layer"]]}
+                if "domain" in descriptor:
+                    d["domain"] = descriptor["domain"]
+                e = Engine(d, device)
+                e.set_coeffs(0, self.coeffs[ki])
+                e.configure(EvalOptions(mode="fp32"))
+                self.engines.append(e)
+                ki += 1
+            else:
+                self.engines.append(None)
 
     def forward(self, x):
+        """Per-layer inputs and the logits (rows [batch, values])."""
         acts = [x]
-        for e in self.engines:
-            acts.append(e.model_forward(acts[-1]))
+        for s, e in zip(self.shapes, self.engines):
+            cur = acts[-1]
+            if s["type"] in ("linear", "conv"):
+                acts.append(e.model_forward(cur.contiguous()))
+            elif s["type"] == "maxpool":
+                c, h, w = s["in"]
+                acts.append(maxpool2(cur, c, h, w, s["layer"].get("window", 2)))
+            else:  # flatten: NCHW rows are already the reference's flat order
+                acts.append(cur)
         return acts
 
     def step(self, x, labels) -> float:
         """One minibatch: forward, loss, backward, momentum update; returns the loss."""
         acts = self.forward(x)
         loss, d = softmax_cross_entropy(acts[-1], labels)
-        for li in range(len(self.engines) - 1, -1, -1):
-            dc, di = self.engines[li].linear_backward(0, acts[li], d, want_inputs=li > 0)
+        ki = sum(1 for e in self.engines if e is not None)
+        for li in range(len(self.shapes) - 1, -1, -1):
+            s, e = self.shapes[li], self.engines[li]
+            want = li > 0
+            if s["type"] == "linear":
+                ki -= 1
+                dc, d = e.linear_backward(0, acts[li], d, want_inputs=want)
+            elif s["type"] == "conv":
+                ki -= 1
+                dc, d = e.conv_backward(0, acts[li], d, want_inputs=want)
+            elif s["type"] == "maxpool":
+                c, h, w = s["in"]
+                d = maxpool2_backward(acts[li], d, c, h, w, s["layer"].get("window", 2))
+                continue
+            else:
+                continue
             g = dc.double().cpu().numpy()
-            self.vel[li] = self.cfg.momentum * self.vel[li] - self.cfg.lr * g
-            self.coeffs[li] += self.vel[li]
-            d = di
-        for e, c in zip(self.engines, self.coeffs):
-            e.set_coeffs(0, c)
-            e.configure(EvalOptions(mode="fp32"))
+            self.vel[ki] = self.cfg.momentum * self.vel[ki] - self.cfg.lr * g
+            self.coeffs[ki] += self.vel[ki]
+        ki = 0
+        for e in self.engines:
+            if e is not None:
+                e.set_coeffs(0, self.coeffs[ki])
+                e.configure(EvalOptions(mode="fp32"))
+                ki += 1
         return loss
+
+
+MlpTrainer = Trainer  # the linear-stack case

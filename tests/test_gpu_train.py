@@ -79,3 +79,85 @@ def test_mlp_sgd_momentum_steps_track_reference(ref):
         assert abs(loss - rloss) <= 1e-4 * max(1.0, abs(rloss)), (step, loss, rloss)
         for a, b, w0 in zip(tr.coeffs, rW, Ws):
             assert _rel(a - w0, b - w0) < 1e-3  # the accumulated updates agree
+
+
+CNN = {"name": "cnn", "grid": {"intervals": 3, "degree": 3}, "input": [2, 11, 11],
+       "layers": [{"type": "conv", "c_in": 2, "c_out": 4, "kernel": 3, "stride": 1, "padding": 1},
+                  {"type": "maxpool", "window": 2},
+                  {"type": "conv", "c_in": 4, "c_out": 5, "kernel": 3, "stride": 2, "padding": 1},
+                  {"type": "flatten"},
+                  {"type": "linear", "n_in": 45, "n_out": 10}]}
+
+
+def _cnn_ws(seed):
+    rng = np.random.default_rng(seed)
+    nb = 6
+    return [rng.normal(0, 0.3, (2 * 9 * nb, 4)), rng.normal(0, 0.3, (4 * 9 * nb, 5)),
+            rng.normal(0, 0.3, (45 * nb, 10))]
+
+
+@pytest.mark.parametrize("desc_ws", ["mlp", "cnn"])
+def test_training_tracks_reference_train(ref, desc_ws):
+    """Two full-batch epochs of the reference's own train() (train.hpp:247-462)
+    vs the GPU Trainer: updated coefficients and loss."""
+    import json
+    from paper_2603_17230_b200.train import Trainer
+    if desc_ws == "mlp":
+        desc = {"name": "m", "grid": {"intervals": 5, "degree": 3}, "input": [30],
+                "layers": [{"type": "linear", "n_in": 30, "n_out": 16},
+                           {"type": "linear", "n_in": 16, "n_out": 10}]}
+        rng = np.random.default_rng(8)
+        Ws = [rng.normal(0, 0.2, (30 * 8, 16)), rng.normal(0, 0.2, (16 * 8, 10))]
+    else:
+        desc, Ws = CNN, _cnn_ws(9)
+    D = int(np.prod(desc["input"]))
+    rng = np.random.default_rng(11)
+    x = rng.uniform(-1, 1, (48, D)).astype(np.float32)
+    y = rng.integers(0, 10, 48).astype(np.int32)
+    cfg = TrainConfig(lr=0.05, momentum=0.9)
+    tr = Trainer(desc, Ws, cfg)
+    xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+    for _ in range(2):
+        loss = tr.step(xd, yd)
+    rW, rloss = ref.train(json.dumps(desc), Ws, x.astype(np.float64), y, cfg.lr, cfg.momentum, 2, 48)
+    assert abs(loss - rloss) <= 1e-4 * max(1.0, abs(rloss)), (loss, rloss)
+    for a, b, w0 in zip(tr.coeffs, rW, Ws):
+        assert _rel(a - w0, b - w0) < 1e-3
+
+
+def test_conv_backward_matches_reference_composition(ref):
+    """kan_engine_conv_backward vs the reference's conv step: im2col patches,
+    kan_linear_backward on the patch rows, col2im_add (train.hpp:367-399)."""
+    G, P = 3, 3
+    rng = np.random.default_rng(3)
+    c_in, c_out, H, W = 3, 6, 7, 7
+    desc = {"name": "c", "grid": {"intervals": G, "degree": P}, "input": [c_in, H, W],
+            "layers": [{"type": "conv", "c_in": c_in, "c_out": c_out, "kernel": 3, "stride": 2, "padding": 1}]}
+    Wt = rng.normal(0, 0.3, (c_in * 9 * (G + P), c_out))
+    e = Engine(desc)
+    e.set_coeffs(0, Wt)
+    M = 5
+    x = rng.uniform(-1.1, 1.1, (M, c_in, H, W)).astype(np.float32)
+    Ho = (H + 2 - 3) // 2 + 1
+    dout = rng.normal(0, 1, (M, c_out, Ho, Ho)).astype(np.float32)
+    dc, di = e.conv_backward(0, torch.from_numpy(x).cuda(), torch.from_numpy(dout).cuda())
+    rdc = np.zeros_like(Wt)
+    rdi = np.zeros(x.shape)
+    for m in range(M):
+        patches = ref.im2col(x[m].astype(np.float64), 3, 2, 1)
+        drows = dout[m].reshape(c_out, -1).T.astype(np.float64)
+        gc, gi = ref.linear_backward(G, P, patches, Wt, drows)
+        rdc += gc
+        for oy in range(Ho):
+            for ox in range(Ho):
+                row = gi[oy * Ho + ox]
+                col = 0
+                for c in range(c_in):
+                    for ky in range(3):
+                        for kx in range(3):
+                            iy, ix = oy * 2 + ky - 1, ox * 2 + kx - 1
+                            if 0 <= iy < H and 0 <= ix < W:
+                                rdi[m, c, iy, ix] += row[col]
+                            col += 1
+    assert _rel(dc.cpu().numpy().astype(np.float64), rdc) < TOL
+    assert _rel(di.cpu().numpy().astype(np.float64), rdi) < TOL
