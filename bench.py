@@ -45,10 +45,11 @@ L2_BYTES = 126 * 1024 * 1024
 # C1/C2 forwards are single latency-bound launches that leave SMs idle in their
 # split-K reduction tail, so two batches in flight overlap one's tail with the
 # other's main loop (measured; bench.py --streams overrides)
-STREAMS_DEFAULT = {"c1": 4, "c2": 6}
+STREAMS_DEFAULT = {"c1": 8, "c2": 12}
 # K splits per launch (0 = the engine's choice): C2 runs unsplit (32 persistent
-# CTAs per batch, 2 launches) so six batches share the GPU without a split-K tail
-SPLIT_DEFAULT = {"c2": 1}
+# CTAs per batch, 2 launches) so many batches share the GPU without a split-K
+# tail; C1 runs 2-way split (16 CTAs per batch, fused output layer)
+SPLIT_DEFAULT = {"c1": 2, "c2": 1}
 PAPER_SAMPLES_PER_S = {  # PAPER.md:603, KANMLP2 G=5 8-bit LUT on RTX 3090
     "c1": 10000 / 5.9e-3, "c2": 10000 / 5.9e-3,
 }
