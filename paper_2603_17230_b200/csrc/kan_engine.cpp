@@ -341,6 +341,7 @@ struct kan_engine {
   bool timeline = false;
   int dbg_flags = 0;  // KAN_DBG_FLAGS (tuning experiments only)
   int force_tab = -1;  // KAN_TABLES=0/1/2 forces the table variant (tuning only)
+  bool epi_stage = true;  // KAN_EPI_STAGE=0 disables the staged fp32 epilogue (tuning only)
   // fp32-input dense layers with at least this many activations get the level
   // prepass (KAN_LEVEL_PREPASS_MIN; tests lower it to exercise the path)
   int64_t prepass_min = std::numeric_limits<int64_t>::max();
@@ -1574,6 +1575,7 @@ void configure(kan_engine* e, const kan_config* c) {
   e->timeline = std::getenv("KAN_TIMELINE") != nullptr;
   e->dbg_flags = std::getenv("KAN_DBG_FLAGS") ? std::atoi(std::getenv("KAN_DBG_FLAGS")) : 0;
   e->force_tab = std::getenv("KAN_TABLES") ? std::atoi(std::getenv("KAN_TABLES")) : -1;
+  e->epi_stage = !(std::getenv("KAN_EPI_STAGE") && std::atoi(std::getenv("KAN_EPI_STAGE")) == 0);
   // off by default: on C3 the prepass saves layer 0 ~50 us but costs ~260 us
   // itself (measured); the path stays available and tested
   e->conv3_mc = std::getenv("KAN_CONV3_MC") ? std::max(1, std::min(2, std::atoi(std::getenv("KAN_CONV3_MC")))) : 2;
@@ -1794,17 +1796,22 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
   // table variant: the lane-private copies when they leave deep enough rings
   int SA = 2, SB = 2, SX = 2;
   int variant = 0;
+  // fp32 row-major output: the epilogue stages 32x16 blocks in smem so each
+  // store instruction writes whole 64-byte row segments
+  const bool stg = !bf16 && e->epi_stage && io.epi == EPI_F32 && io.out_hw == 0 && !io.res_kind;
+  const int stg_bytes = stg ? GEMM_STG_BYTES : 0;
   const int want_tab = e->force_tab >= 0 ? e->force_tab : 2;
   if (!bf16 && want_tab > 0 && e->tabs[want_tab].bytes > 0) {
     try {
-      pick_stages(bf16, pl.nbp, pl.BN, io.x_kind, e->tabs[want_tab].bytes, pl.silu != 0, 1, SA, SB, SX);
+      pick_stages(bf16, pl.nbp, pl.BN, io.x_kind, e->tabs[want_tab].bytes, pl.silu != 0, 1, SA, SB, SX, stg_bytes);
       if (SB >= 3 && SX >= 4) variant = want_tab;
     } catch (const Unsupported&) {
     }
   }
   const auto& ts = e->tabs[variant];
   const int tb = bf16 ? 0 : ts.bytes;
-  pick_stages(bf16, pl.nbp, pl.BN, io.x_kind, tb, pl.silu != 0, 1, SA, SB, SX);
+  pick_stages(bf16, pl.nbp, pl.BN, io.x_kind, tb, pl.silu != 0, 1, SA, SB, SX, stg_bytes);
+  p.stg_on = stg ? 1 : 0;
   p.tab = ts.buf.p;
   p.tab_bytes = ts.bytes;
   p.off_thr = ts.off_thr;
@@ -1830,7 +1837,7 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
   p.splits = splits;
   p.groups_per_split = gps;
   // fused output layer: only for split-K launches (each CTA reduces whole rows)
-  int fused_bytes = 0;
+  int fused_bytes = stg_bytes;
   if (io.fuse && splits > 1 && pl.n_tiles_n == 1 && !io.conv && io.epi == EPI_LEVEL) {
     const PreparedLayer& f = *io.fuse;
     const int wq_b = (f.n_in * f.N * 8 + 15) / 16 * 16;

@@ -985,6 +985,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
     if (persistent) {
       int lt = 0;
+      int cur_n = -1;
       for (int t = blockIdx.x; t < n_tiles; t += tile_step, ++lt) {
         const Tile tl = tile_of(t);
         const int ab = nacc == 2 ? (lt & 1) : 0;
@@ -993,9 +994,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         tc_fence_after();
         if (threadIdx.x == 32 * W_EPI && lt == 0) stamp(4);
         // all epilogue warps are past the previous tile: restage the columns
-        asm volatile("bar.sync 4, %0;" ::"r"(32 * GEMM_EPI_WARPS) : "memory");
-        load_cols(tl.n_tile, 32 * W_EPI, 32 * GEMM_EPI_WARPS);
-        asm volatile("bar.sync 4, %0;" ::"r"(32 * GEMM_EPI_WARPS) : "memory");
+        // (only when the column tile changes; every epilogue warp walks the
+        // same tiles, so the branch is uniform)
+        if (tl.n_tile != cur_n) {
+          asm volatile("bar.sync 4, %0;" ::"r"(32 * GEMM_EPI_WARPS) : "memory");
+          load_cols(tl.n_tile, 32 * W_EPI, 32 * GEMM_EPI_WARPS);
+          asm volatile("bar.sync 4, %0;" ::"r"(32 * GEMM_EPI_WARPS) : "memory");
+          cur_n = tl.n_tile;
+        }
         int32_t rs = 0;
         if constexpr (MODE == MODE_ZP) {
           const int rb2 = lt & 1;
@@ -1011,6 +1017,105 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         // 16 columns per TMEM load (BN is a multiple of 16); the two warps of
         // a lane quarter take alternate 16-column groups
         const int half = (warp - W_EPI) >> 2;
+        if constexpr (!BF16 && MODE != MODE_ZP) {
+          // Straight-line epilogue for the common fp32 row-major output
+          // (+ levels sidecar) of a full-width tile: the same fp64 arithmetic
+          // as finish4 with the per-group checks hoisted.  (int32 acc - corr)
+          // is an integer below 2^53, so the fp64 subtraction is exact.
+          const int n0 = tl.n_tile * BN;
+          const bool fast = p.epi == EPI_F32 && p.out_hw == 0 && !p.res_kind && n0 + BN <= p.N &&
+                            (p.ld_out & 3) == 0 && (reinterpret_cast<uintptr_t>(p.out) & 15) == 0 &&
+                            (p.out_lv == nullptr ||
+                             ((p.ld_lv & 7) == 0 && (reinterpret_cast<uintptr_t>(p.out_lv) & 15) == 0)) &&
+                            !(p.dbg_flags & 8);
+          if (fast) {
+            const float* thr = reinterpret_cast<const float*>(sT + p.off_thr);
+#pragma unroll 1
+            for (int g16 = half; g16 < ngroups / 4; g16 += 2) {
+              uint32_t r16[16];
+              tmem_ld16(tacc + g16 * 16, r16);
+              tmem_wait_ld();
+              if (p.stg_on) {
+                // this warp's 32 rows x 16 columns through smem: each store
+                // instruction then writes 8 whole 64-byte row segments (levels:
+                // 16 whole 32-byte segments) instead of 32 half sectors
+                const int cl = g16 * 16;
+                uint8_t* sg = smem + f_off + static_cast<uint32_t>(warp - W_EPI) * (32u * GEMM_STG_PITCH);
+                float f[16];
+#pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                  const double v = __dsub_rn(static_cast<double>(static_cast<int32_t>(r16[e])), s_cols[BN + cl + e]);
+                  f[e] = __double2float_rn(__dmul_rn(v, s_cols[cl + e]));
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                  *reinterpret_cast<float4*>(sg + lane * GEMM_STG_PITCH + q * 16) =
+                      make_float4(f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]);
+                __syncwarp();
+                const int rb = tl.m0 + wq * 32;
+#pragma unroll
+                for (int s = 0; s < 4; ++s) {
+                  const int rl = s * 8 + (lane >> 2);
+                  const float4 v = *reinterpret_cast<const float4*>(sg + rl * GEMM_STG_PITCH + (lane & 3) * 16);
+                  if (rb + rl < p.M)
+                    *reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) + static_cast<size_t>(rb + rl) * p.ld_out +
+                                               n0 + cl + (lane & 3) * 4) = v;
+                }
+                if (p.out_lv) {
+                  uint32_t w[8];
+#pragma unroll
+                  for (int q = 0; q < 8; ++q) {
+                    const uint32_t a0 = static_cast<uint32_t>(lattice_level_tie(f[2 * q], p.inv_step_f, p.lo_f, p.L, thr));
+                    const uint32_t a1 = static_cast<uint32_t>(lattice_level_tie(f[2 * q + 1], p.inv_step_f, p.lo_f, p.L, thr));
+                    w[q] = a0 | (a1 << 16);
+                  }
+                  __syncwarp();
+                  // 48-byte pitch: conflict-free 16-byte stores
+                  *reinterpret_cast<uint4*>(sg + lane * 48) = make_uint4(w[0], w[1], w[2], w[3]);
+                  *reinterpret_cast<uint4*>(sg + lane * 48 + 16) = make_uint4(w[4], w[5], w[6], w[7]);
+                  __syncwarp();
+#pragma unroll
+                  for (int s = 0; s < 2; ++s) {
+                    const int rl = s * 16 + (lane >> 1);
+                    const uint4 v = *reinterpret_cast<const uint4*>(sg + rl * 48 + (lane & 1) * 16);
+                    if (rb + rl < p.M)
+                      *reinterpret_cast<uint4*>(p.out_lv + static_cast<size_t>(rb + rl) * p.ld_lv + n0 + cl +
+                                                (lane & 1) * 8) = v;
+                  }
+                }
+                __syncwarp();
+              } else if (row < p.M) {
+                const int cl = g16 * 16;
+                float f[16];
+#pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                  const double v = __dsub_rn(static_cast<double>(static_cast<int32_t>(r16[e])), s_cols[BN + cl + e]);
+                  f[e] = __double2float_rn(__dmul_rn(v, s_cols[cl + e]));
+                }
+                float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) +
+                                                      static_cast<size_t>(row) * p.ld_out + n0 + cl);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) o[q] = make_float4(f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]);
+                if (p.out_lv) {
+                  uint32_t w[8];
+#pragma unroll
+                  for (int q = 0; q < 8; ++q) {
+                    const uint32_t a0 = static_cast<uint32_t>(lattice_level_tie(f[2 * q], p.inv_step_f, p.lo_f, p.L, thr));
+                    const uint32_t a1 = static_cast<uint32_t>(lattice_level_tie(f[2 * q + 1], p.inv_step_f, p.lo_f, p.L, thr));
+                    w[q] = a0 | (a1 << 16);
+                  }
+                  uint4* ol = reinterpret_cast<uint4*>(p.out_lv + static_cast<size_t>(row) * p.ld_lv + n0 + cl);
+                  ol[0] = make_uint4(w[0], w[1], w[2], w[3]);
+                  ol[1] = make_uint4(w[4], w[5], w[6], w[7]);
+                }
+              }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar_accempty(ab));
+            continue;
+          }
+        }
 #pragma unroll 1
         for (int g16 = half; g16 < ng / 4; g16 += 2) {
           if (p.res_kind && (g16 & 3) == half) {

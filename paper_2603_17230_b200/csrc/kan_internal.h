@@ -20,6 +20,9 @@ constexpr int GEMM_PRODUCER_WARPS = 16;
 // producers + activation loader + MMA issuer + weight loader + epilogue warps
 // (two per TMEM lane quarter, each on every other 16-column group)
 constexpr int GEMM_EPI_WARPS = 8;
+// per epilogue warp: 32 rows x 16 fp32 columns at an 80-byte pitch (conflict-free 16-byte stores)
+constexpr int GEMM_STG_PITCH = 80;
+constexpr int GEMM_STG_BYTES = GEMM_EPI_WARPS * 32 * GEMM_STG_PITCH;
 constexpr int GEMM_THREADS = 32 * (GEMM_PRODUCER_WARPS + 3 + GEMM_EPI_WARPS);
 
 // One fused gather + tcgen05 GEMM launch (one KAN layer, linear form).
@@ -103,6 +106,7 @@ struct GemmParams {
   // the model output; f_wq [n_in2][N2] 8 basis weights per (input, output),
   // f_wqb [N2][n_in2] SiLU base weights, both bulk-copied to smem
   int f_on, f_N, f_silu, f_epi, f_ld_out, f_wq_bytes, f_wqb_bytes;
+  int stg_on;  // fp32 epilogue staged through smem (the fused-layer region) for row-coalesced stores
   const unsigned long long* f_wq;
   const int8_t* f_wqb;
   const double* f_fs;
