@@ -460,7 +460,9 @@ struct TapWalk {
   }
 };
 
-template <bool BF16, int NBP, int MODE>
+// FE: the fp32 row-major epilogue fast path is compiled in (a separate
+// instantiation, so the other variants keep their register allocation)
+template <bool BF16, int NBP, int MODE, bool FE = false>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     kan_gather_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const GemmParams p) {
   using C = Cfg<BF16, NBP>;
@@ -1017,7 +1019,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         // 16 columns per TMEM load (BN is a multiple of 16); the two warps of
         // a lane quarter take alternate 16-column groups
         const int half = (warp - W_EPI) >> 2;
-        if constexpr (!BF16 && MODE != MODE_ZP) {
+        if constexpr (FE) {
           // Straight-line epilogue for the common fp32 row-major output
           // (+ levels sidecar) of a full-width tile: the same fp64 arithmetic
           // as finish4 with the per-group checks hoisted.  (int32 acc - corr)
@@ -1320,10 +1322,10 @@ static cudaError_t launch_pdl(void (*kfn)(KArgs...), dim3 grid, dim3 block, size
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
-template <bool BF16, int NBP, int MODE>
+template <bool BF16, int NBP, int MODE, bool FE = false>
 static cudaError_t launch_impl(const CUtensorMap& xmap, const GemmParams& p, size_t smem,
                                cudaStream_t st) {
-  auto kfn = kan_gather_gemm_kernel<BF16, NBP, MODE>;
+  auto kfn = kan_gather_gemm_kernel<BF16, NBP, MODE, FE>;
   static size_t configured = 0;  // per instantiation: raise the smem limit once
   if (smem > configured) {
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1398,14 +1400,22 @@ cudaError_t launch_gather_gemm(bool bf16, int nbp, int mode, const CUtensorMap& 
     return nbp == 8 ? launch_impl<true, 8, MODE_PLAIN>(xmap, p, smem, st)
                     : launch_impl<true, 16, MODE_PLAIN>(xmap, p, smem, st);
   }
+  // fp32 row-major outputs take the instantiation with the fast epilogue
+  const bool fe = p.epi == EPI_F32 && p.out_hw == 0 && !p.res_kind && p.splits == 1;
   switch (mode) {
     case MODE_ZP:
       return nbp == 8 ? launch_impl<false, 8, MODE_ZP>(xmap, p, smem, st)
                       : launch_impl<false, 16, MODE_ZP>(xmap, p, smem, st);
     case MODE_SILU:
+      if (fe)
+        return nbp == 8 ? launch_impl<false, 8, MODE_SILU, true>(xmap, p, smem, st)
+                        : launch_impl<false, 16, MODE_SILU, true>(xmap, p, smem, st);
       return nbp == 8 ? launch_impl<false, 8, MODE_SILU>(xmap, p, smem, st)
                       : launch_impl<false, 16, MODE_SILU>(xmap, p, smem, st);
     default:
+      if (fe)
+        return nbp == 8 ? launch_impl<false, 8, MODE_PLAIN, true>(xmap, p, smem, st)
+                        : launch_impl<false, 16, MODE_PLAIN, true>(xmap, p, smem, st);
       return nbp == 8 ? launch_impl<false, 8, MODE_PLAIN>(xmap, p, smem, st)
                       : launch_impl<false, 16, MODE_PLAIN>(xmap, p, smem, st);
   }
