@@ -1798,18 +1798,27 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
   int variant = 0;
   // fp32 row-major output: the epilogue stages 32x16 blocks in smem so each
   // store instruction writes whole 64-byte row segments
-  const bool stg = !bf16 && e->epi_stage && io.epi == EPI_F32 && io.out_hw == 0 && !io.res_kind;
-  const int stg_bytes = stg ? GEMM_STG_BYTES : 0;
+  bool stg = !bf16 && e->epi_stage && io.epi == EPI_F32 && io.out_hw == 0 && !io.res_kind;
   const int want_tab = e->force_tab >= 0 ? e->force_tab : 2;
   if (!bf16 && want_tab > 0 && e->tabs[want_tab].bytes > 0) {
     try {
-      pick_stages(bf16, pl.nbp, pl.BN, io.x_kind, e->tabs[want_tab].bytes, pl.silu != 0, 1, SA, SB, SX, stg_bytes);
+      pick_stages(bf16, pl.nbp, pl.BN, io.x_kind, e->tabs[want_tab].bytes, pl.silu != 0, 1, SA, SB, SX);
       if (SB >= 3 && SX >= 4) variant = want_tab;
     } catch (const Unsupported&) {
     }
   }
   const auto& ts = e->tabs[variant];
   const int tb = bf16 ? 0 : ts.bytes;
+  // the staging buffer only when it leaves the table variant and rings intact
+  if (stg) {
+    try {
+      pick_stages(bf16, pl.nbp, pl.BN, io.x_kind, tb, pl.silu != 0, 1, SA, SB, SX, GEMM_STG_BYTES);
+      stg = SB >= 3 && (variant == 0 || SX >= 4);
+    } catch (const Unsupported&) {
+      stg = false;
+    }
+  }
+  const int stg_bytes = stg ? GEMM_STG_BYTES : 0;
   pick_stages(bf16, pl.nbp, pl.BN, io.x_kind, tb, pl.silu != 0, 1, SA, SB, SX, stg_bytes);
   p.stg_on = stg ? 1 : 0;
   p.tab = ts.buf.p;

@@ -357,3 +357,27 @@ def test_fp32_conv_models_match_reference(ref, name):
     r = ref.model_forward(_json.dumps(desc), Ws, x.astype(np.float64), 10, mode=0)
     assert np.linalg.norm(y - r) / np.linalg.norm(r) < FP32_TOL
     assert np.array_equal(e.predict(torch.from_numpy(x).cuda()).cpu().numpy(), r.argmax(1))
+
+
+@pytest.mark.parametrize("dims", [[200, 64], [120, 96, 128], [150, 80], [100, 300]])
+@pytest.mark.parametrize("silu", [False, True])
+@pytest.mark.parametrize("split", [1, 0])
+def test_fp32_output_epilogue_paths_bit_exact(oracle, dims, silu, split):
+    """fp32 row-major outputs: full-width column tiles take the straight-line
+    epilogue staged through shared memory (kan_gemm.cu, FE instantiation),
+    ragged ones (N = 300: a 256 + 44 column split) and split-K launches take
+    finish4.  M = 333 leaves a partial row tile.  All are bit-exact with the
+    oracle and identical with the staging switched off (KAN_EPI_STAGE=0)."""
+    G, M = 5, 333
+    Ws, Bs = make_weights(dims, G, seed=11, silu=silu)
+    x = np.random.default_rng(11).uniform(-1.05, 1.05, (M, dims[0])).astype(np.float32)
+    opts = dict(mode="bspline-lut", lut_k=8, lut_h=8, silu_base=silu, split_k=split)
+    y = build(dims, G, Ws, Bs, **opts).model_forward(to_dev(x)).cpu().numpy()
+    yo = oracle_int_model(oracle, G, 8, 8, W_PER_CHANNEL_SYM, 8, Ws, Bs, x)[-1]
+    np.testing.assert_array_equal(y, yo.astype(np.float32))
+    os.environ["KAN_EPI_STAGE"] = "0"
+    try:
+        y0 = build(dims, G, Ws, Bs, **opts).model_forward(to_dev(x)).cpu().numpy()
+    finally:
+        del os.environ["KAN_EPI_STAGE"]
+    np.testing.assert_array_equal(y0, y)
