@@ -20,7 +20,10 @@
 // activation TMA, MMA, weight loader, 4 epilogue warps, double-buffered TMEM
 // accumulators).
 
-template <int MODE>
+// LF: the straight-line next-layer-level epilogue is compiled in (its own
+// instantiation: adding it to the residual/fp32 variant costs that one
+// registers and measured 25 % on C5's residual convs)
+template <int MODE, bool LF = false>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     kan_conv3_kernel(const __grid_constant__ CUtensorMap xmap, const GemmParams p) {
   constexpr int NBP = 8;
@@ -340,6 +343,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int row = tl.m0 + rloc;
       float rv[32];  // residual prefetch: 32 columns in flight per thread
       const int half = (warp - W_EPI) >> 2;  // the two warps of a lane quarter take alternate 32-column blocks
+      const bool lvl_fast = LF && p.epi == EPI_LEVEL && !p.res_kind && tl.n_tile * BN + BN <= p.N &&
+                            (p.ld_out & 7) == 0 && (reinterpret_cast<uintptr_t>(p.out) & 15) == 0;
       // 32-column blocks (the two warps of a lane quarter alternate), read as
       // two 16-column TMEM loads: 2 round trips per block instead of 8
 #pragma unroll 1
@@ -368,6 +373,30 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         uint32_t r16[16];
         tmem_ld16(tacc + blk * 32 + sub * 16, r16);
         tmem_wait_ld();
+        if (LF && lvl_fast) {
+          // next-layer levels of 16 full columns, straight-line: the same fp64
+          // (acc - corr) * fs (the subtraction is exact in fp64: an integer
+          // below 2^53) and lattice_level_fast, then two 16-byte stores
+          const int cl = blk * 32 + sub * 16;
+          if (row < p.M && cl < BN) {
+            uint32_t w[8];
+#pragma unroll
+            for (int e = 0; e < 16; e += 2) {
+              const double y0 =
+                  __dmul_rn(__dsub_rn(static_cast<double>(static_cast<int32_t>(r16[e])), s_cols[BN + cl + e]), s_cols[cl + e]);
+              const double y1 = __dmul_rn(
+                  __dsub_rn(static_cast<double>(static_cast<int32_t>(r16[e + 1])), s_cols[BN + cl + e + 1]), s_cols[cl + e + 1]);
+              const uint32_t a0 = static_cast<uint32_t>(lattice_level_fast(y0, p.n_lo, p.n_hi_open, p.n_step, p.n_inv_step, p.n_L));
+              const uint32_t a1 = static_cast<uint32_t>(lattice_level_fast(y1, p.n_lo, p.n_hi_open, p.n_step, p.n_inv_step, p.n_L));
+              w[e >> 1] = a0 | (a1 << 16);
+            }
+            uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(p.out) + static_cast<size_t>(row) * p.ld_out +
+                                                tl.n_tile * BN + cl);
+            o[0] = make_uint4(w[0], w[1], w[2], w[3]);
+            o[1] = make_uint4(w[4], w[5], w[6], w[7]);
+          }
+          continue;
+        }
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4) {
         const int q = sub * 4 + q4;
@@ -467,12 +496,14 @@ size_t conv3_smem_bytes(int BN, int R, int SA, int SB, int SX, int x_kind, int t
 }
 
 cudaError_t launch_conv3(int mode, const CUtensorMap& xmap, const GemmParams& p, size_t smem, cudaStream_t st) {
-  static size_t configured[3] = {0, 0, 0};  // per kernel variant (same function type)
+  static size_t configured[6] = {0, 0, 0, 0, 0, 0};  // per kernel variant (same function type)
+  const bool lf = p.epi == EPI_LEVEL && !p.res_kind;
+  const int var = mode * 2 + (lf ? 1 : 0);
   auto go = [&](auto kfn) -> cudaError_t {
-    if (smem > configured[mode]) {
+    if (smem > configured[var]) {
       cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
       if (e != cudaSuccess) return e;
-      configured[mode] = smem;
+      configured[var] = smem;
     }
     static int n_sm = 0;
     if (n_sm == 0) {
@@ -500,6 +531,6 @@ cudaError_t launch_conv3(int mode, const CUtensorMap& xmap, const GemmParams& p,
     cfg.numAttrs = 2;
     return cudaLaunchKernelEx(&cfg, kfn, xmap, p);
   };
-  if (mode == MODE_SILU) return go(kan_conv3_kernel<MODE_SILU>);
-  return go(kan_conv3_kernel<MODE_PLAIN>);
+  if (mode == MODE_SILU) return lf ? go(kan_conv3_kernel<MODE_SILU, true>) : go(kan_conv3_kernel<MODE_SILU>);
+  return lf ? go(kan_conv3_kernel<MODE_PLAIN, true>) : go(kan_conv3_kernel<MODE_PLAIN>);
 }
