@@ -460,9 +460,10 @@ struct TapWalk {
   }
 };
 
-// FE: the fp32 row-major epilogue fast path is compiled in (a separate
-// instantiation, so the other variants keep their register allocation)
-template <bool BF16, int NBP, int MODE, bool FE = false>
+// FE: a straight-line epilogue is compiled in -- 1: fp32 row-major output
+// (+ levels sidecar), 2: next-layer levels.  Separate instantiations, so the
+// other variants keep their register allocation.
+template <bool BF16, int NBP, int MODE, int FE = 0>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     kan_gather_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const GemmParams p) {
   using C = Cfg<BF16, NBP>;
@@ -1019,7 +1020,47 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         // 16 columns per TMEM load (BN is a multiple of 16); the two warps of
         // a lane quarter take alternate 16-column groups
         const int half = (warp - W_EPI) >> 2;
-        if constexpr (FE) {
+        if constexpr (FE == 2) {
+          // next-layer levels of full-width tiles, 16 columns per TMEM load:
+          // finish4's fp64 (acc - corr) * fs (exact subtraction, as below) and
+          // lattice_level_fast, two 16-byte stores per row block
+          const int n0 = tl.n_tile * BN;
+          if (p.epi == EPI_LEVEL && !p.f_on && !p.res_kind && n0 + BN <= p.N && (p.ld_out & 7) == 0 &&
+              (reinterpret_cast<uintptr_t>(p.out) & 15) == 0 && !(p.dbg_flags & 8)) {
+#pragma unroll 1
+            for (int g16 = half; g16 < ngroups / 4; g16 += 2) {
+              uint32_t r16[16];
+              tmem_ld16(tacc + g16 * 16, r16);
+              tmem_wait_ld();
+              if (row < p.M) {
+                const int cl = g16 * 16;
+                uint32_t w[8];
+#pragma unroll
+                for (int e = 0; e < 16; e += 2) {
+                  const double y0 = __dmul_rn(
+                      __dsub_rn(static_cast<double>(static_cast<int32_t>(r16[e])), s_cols[BN + cl + e]), s_cols[cl + e]);
+                  const double y1 = __dmul_rn(
+                      __dsub_rn(static_cast<double>(static_cast<int32_t>(r16[e + 1])), s_cols[BN + cl + e + 1]),
+                      s_cols[cl + e + 1]);
+                  const uint32_t a0 =
+                      static_cast<uint32_t>(lattice_level_fast(y0, p.n_lo, p.n_hi_open, p.n_step, p.n_inv_step, p.n_L));
+                  const uint32_t a1 =
+                      static_cast<uint32_t>(lattice_level_fast(y1, p.n_lo, p.n_hi_open, p.n_step, p.n_inv_step, p.n_L));
+                  w[e >> 1] = a0 | (a1 << 16);
+                }
+                uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(p.out) +
+                                                    static_cast<size_t>(row) * p.ld_out + n0 + cl);
+                o[0] = make_uint4(w[0], w[1], w[2], w[3]);
+                o[1] = make_uint4(w[4], w[5], w[6], w[7]);
+              }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar_accempty(ab));
+            continue;
+          }
+        }
+        if constexpr (FE == 1) {
           // Straight-line epilogue for the common fp32 row-major output
           // (+ levels sidecar) of a full-width tile: the same fp64 arithmetic
           // as finish4 with the per-group checks hoisted.  (int32 acc - corr)
@@ -1322,7 +1363,7 @@ static cudaError_t launch_pdl(void (*kfn)(KArgs...), dim3 grid, dim3 block, size
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
-template <bool BF16, int NBP, int MODE, bool FE = false>
+template <bool BF16, int NBP, int MODE, int FE = 0>
 static cudaError_t launch_impl(const CUtensorMap& xmap, const GemmParams& p, size_t smem,
                                cudaStream_t st) {
   auto kfn = kan_gather_gemm_kernel<BF16, NBP, MODE, FE>;
@@ -1401,21 +1442,29 @@ cudaError_t launch_gather_gemm(bool bf16, int nbp, int mode, const CUtensorMap& 
                     : launch_impl<true, 16, MODE_PLAIN>(xmap, p, smem, st);
   }
   // fp32 row-major outputs take the instantiation with the fast epilogue
-  const bool fe = p.epi == EPI_F32 && p.out_hw == 0 && !p.res_kind && p.splits == 1;
+  const int fe = (p.splits != 1 || p.res_kind) ? 0
+                 : (p.epi == EPI_F32 && p.out_hw == 0) ? 1
+                 : (p.epi == EPI_LEVEL && !p.f_on) ? 2 : 0;
   switch (mode) {
     case MODE_ZP:
       return nbp == 8 ? launch_impl<false, 8, MODE_ZP>(xmap, p, smem, st)
                       : launch_impl<false, 16, MODE_ZP>(xmap, p, smem, st);
     case MODE_SILU:
-      if (fe)
-        return nbp == 8 ? launch_impl<false, 8, MODE_SILU, true>(xmap, p, smem, st)
-                        : launch_impl<false, 16, MODE_SILU, true>(xmap, p, smem, st);
+      if (fe == 1)
+        return nbp == 8 ? launch_impl<false, 8, MODE_SILU, 1>(xmap, p, smem, st)
+                        : launch_impl<false, 16, MODE_SILU, 1>(xmap, p, smem, st);
+      if (fe == 2)
+        return nbp == 8 ? launch_impl<false, 8, MODE_SILU, 2>(xmap, p, smem, st)
+                        : launch_impl<false, 16, MODE_SILU, 2>(xmap, p, smem, st);
       return nbp == 8 ? launch_impl<false, 8, MODE_SILU>(xmap, p, smem, st)
                       : launch_impl<false, 16, MODE_SILU>(xmap, p, smem, st);
     default:
-      if (fe)
-        return nbp == 8 ? launch_impl<false, 8, MODE_PLAIN, true>(xmap, p, smem, st)
-                        : launch_impl<false, 16, MODE_PLAIN, true>(xmap, p, smem, st);
+      if (fe == 1)
+        return nbp == 8 ? launch_impl<false, 8, MODE_PLAIN, 1>(xmap, p, smem, st)
+                        : launch_impl<false, 16, MODE_PLAIN, 1>(xmap, p, smem, st);
+      if (fe == 2)
+        return nbp == 8 ? launch_impl<false, 8, MODE_PLAIN, 2>(xmap, p, smem, st)
+                        : launch_impl<false, 16, MODE_PLAIN, 2>(xmap, p, smem, st);
       return nbp == 8 ? launch_impl<false, 8, MODE_PLAIN>(xmap, p, smem, st)
                       : launch_impl<false, 16, MODE_PLAIN>(xmap, p, smem, st);
   }

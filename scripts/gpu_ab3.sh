@@ -1,0 +1,13 @@
+# A/B of alt/libkan_b200_old.so vs the current build: C1/C2/C3 bench and C5 per-layer times
+cd $GRAFT_REPO_ROOT
+L=paper_2603_17230_b200/libkan_b200.so
+cp $L paper_2603_17230_b200/alt/libkan_b200_new.so
+for v in new old new old; do
+  cp paper_2603_17230_b200/alt/libkan_b200_$v.so $L
+  for c in c2 c1 c3; do
+   st=20000; [ $c = c3 ] && st=60
+   timeout -s KILL 300 python bench.py --config $c --steps $st --warmup 5 --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('$v $c', round(d['ms_per_step']*1e3,2), 'us', d['clocks']['sm_mhz'])"
+  done
+  timeout -s KILL 300 python scripts/prof_layer.py --config c5 --iters 2 2>&1 | grep -E "layer (6|8|11|13|16|18):" | tr '\n' ' ' | sed "s/^/$v c5: /"; echo
+done
+cp paper_2603_17230_b200/alt/libkan_b200_new.so $L
