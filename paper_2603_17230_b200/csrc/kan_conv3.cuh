@@ -20,10 +20,11 @@
 // activation TMA, MMA, weight loader, 4 epilogue warps, double-buffered TMEM
 // accumulators).
 
-// LF: the straight-line next-layer-level epilogue is compiled in (its own
-// instantiation: adding it to the residual/fp32 variant costs that one
-// registers and measured 25 % on C5's residual convs)
-template <int MODE, bool LF = false>
+// LF: a straight-line epilogue is compiled in -- 1: next-layer levels,
+// 2: fp32 row-major output (+ residual add, + levels sidecar).  Each is its
+// own instantiation: adding the level path to the residual variant cost that
+// one registers and measured 25 % on C5's residual convs.
+template <int MODE, int LF = 0>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     kan_conv3_kernel(const __grid_constant__ CUtensorMap xmap, const GemmParams p) {
   constexpr int NBP = 8;
@@ -343,10 +344,64 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int row = tl.m0 + rloc;
       float rv[32];  // residual prefetch: 32 columns in flight per thread
       const int half = (warp - W_EPI) >> 2;  // the two warps of a lane quarter take alternate 32-column blocks
-      const bool lvl_fast = LF && p.epi == EPI_LEVEL && !p.res_kind && tl.n_tile * BN + BN <= p.N &&
+      const bool lvl_fast = LF == 1 && p.epi == EPI_LEVEL && !p.res_kind && tl.n_tile * BN + BN <= p.N &&
                             (p.ld_out & 7) == 0 && (reinterpret_cast<uintptr_t>(p.out) & 15) == 0;
       // 32-column blocks (the two warps of a lane quarter alternate), read as
       // two 16-column TMEM loads: 2 round trips per block instead of 8
+      if constexpr (LF == 2) {
+        const int n0 = tl.n_tile * BN;
+        if (p.epi == EPI_F32 && p.out_hw == 0 && n0 + BN <= p.N && (p.ld_out & 3) == 0 &&
+            (reinterpret_cast<uintptr_t>(p.out) & 15) == 0 &&
+            (!p.res_kind || ((p.ld_res & 3) == 0 && (reinterpret_cast<uintptr_t>(p.res) & 15) == 0)) &&
+            (p.out_lv == nullptr || ((p.ld_lv & 7) == 0 && (reinterpret_cast<uintptr_t>(p.out_lv) & 15) == 0)) &&
+            !(p.dbg_flags & 8)) {
+          // 16 columns per step: residual loads issued before the TMEM load,
+          // then finish4's fp64 (acc - corr) * fs [+ residual] (exact
+          // subtraction), the fp32 row and its levels sidecar
+          const float* thr = reinterpret_cast<const float*>(sT + p.off_thr);
+#pragma unroll 1
+          for (int cl = half * 16; cl < BN; cl += 32) {
+            float4 rv4[4] = {};
+            if (p.res_kind && row < p.M) {
+              const float4* rp = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(p.res) +
+                                                                 static_cast<size_t>(row) * p.ld_res + n0 + cl);
+#pragma unroll
+              for (int q = 0; q < 4; ++q) rv4[q] = rp[q];
+            }
+            uint32_t r16[16];
+            tmem_ld16(tacc + cl, r16);
+            tmem_wait_ld();
+            if (row < p.M) {
+              float f[16];
+#pragma unroll
+              for (int e = 0; e < 16; ++e) {
+                double y = __dmul_rn(__dsub_rn(static_cast<double>(static_cast<int32_t>(r16[e])), s_cols[BN + cl + e]),
+                                     s_cols[cl + e]);
+                if (p.res_kind) y = __dadd_rn(y, static_cast<double>((&rv4[e >> 2].x)[e & 3]));
+                f[e] = __double2float_rn(y);
+              }
+              float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) +
+                                                    static_cast<size_t>(row) * p.ld_out + n0 + cl);
+#pragma unroll
+              for (int q = 0; q < 4; ++q) o[q] = make_float4(f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]);
+              if (p.out_lv) {
+                uint32_t w[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                  w[q] = static_cast<uint32_t>(lattice_level_tie(f[2 * q], p.inv_step_f, p.lo_f, p.L, thr)) |
+                         (static_cast<uint32_t>(lattice_level_tie(f[2 * q + 1], p.inv_step_f, p.lo_f, p.L, thr)) << 16);
+                uint4* ol = reinterpret_cast<uint4*>(p.out_lv + static_cast<size_t>(row) * p.ld_lv + n0 + cl);
+                ol[0] = make_uint4(w[0], w[1], w[2], w[3]);
+                ol[1] = make_uint4(w[4], w[5], w[6], w[7]);
+              }
+            }
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(bar_accempty(ab));
+          continue;
+        }
+      }
 #pragma unroll 1
       for (int blk = half; blk < ((p.dbg_flags & 8) ? 0 : (BN + 31) / 32); blk += 2) {
         const int gq0 = blk * 8;
@@ -373,7 +428,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         uint32_t r16[16];
         tmem_ld16(tacc + blk * 32 + sub * 16, r16);
         tmem_wait_ld();
-        if (LF && lvl_fast) {
+        if (LF == 1 && lvl_fast) {
           // next-layer levels of 16 full columns, straight-line: the same fp64
           // (acc - corr) * fs (the subtraction is exact in fp64: an integer
           // below 2^53) and lattice_level_fast, then two 16-byte stores
@@ -496,9 +551,9 @@ size_t conv3_smem_bytes(int BN, int R, int SA, int SB, int SX, int x_kind, int t
 }
 
 cudaError_t launch_conv3(int mode, const CUtensorMap& xmap, const GemmParams& p, size_t smem, cudaStream_t st) {
-  static size_t configured[6] = {0, 0, 0, 0, 0, 0};  // per kernel variant (same function type)
-  const bool lf = p.epi == EPI_LEVEL && !p.res_kind;
-  const int var = mode * 2 + (lf ? 1 : 0);
+  static size_t configured[9] = {};  // per kernel variant (same function type)
+  const int lf = (p.epi == EPI_LEVEL && !p.res_kind) ? 1 : (p.epi == EPI_F32 && p.out_hw == 0) ? 2 : 0;
+  const int var = mode * 3 + lf;
   auto go = [&](auto kfn) -> cudaError_t {
     if (smem > configured[var]) {
       cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
@@ -531,6 +586,9 @@ cudaError_t launch_conv3(int mode, const CUtensorMap& xmap, const GemmParams& p,
     cfg.numAttrs = 2;
     return cudaLaunchKernelEx(&cfg, kfn, xmap, p);
   };
-  if (mode == MODE_SILU) return lf ? go(kan_conv3_kernel<MODE_SILU, true>) : go(kan_conv3_kernel<MODE_SILU>);
-  return lf ? go(kan_conv3_kernel<MODE_PLAIN, true>) : go(kan_conv3_kernel<MODE_PLAIN>);
+  if (mode == MODE_SILU)
+    return lf == 1 ? go(kan_conv3_kernel<MODE_SILU, 1>)
+                   : (lf == 2 ? go(kan_conv3_kernel<MODE_SILU, 2>) : go(kan_conv3_kernel<MODE_SILU>));
+  return lf == 1 ? go(kan_conv3_kernel<MODE_PLAIN, 1>)
+                 : (lf == 2 ? go(kan_conv3_kernel<MODE_PLAIN, 2>) : go(kan_conv3_kernel<MODE_PLAIN>));
 }
