@@ -45,11 +45,13 @@ L2_BYTES = 126 * 1024 * 1024
 # C1/C2 forwards are single latency-bound launches that leave SMs idle in their
 # split-K reduction tail, so two batches in flight overlap one's tail with the
 # other's main loop (measured; bench.py --streams overrides)
-STREAMS_DEFAULT = {"c1": 8, "c2": 12}
-# K splits per launch (0 = the engine's choice): C2 runs unsplit (32 persistent
-# CTAs per batch, 2 launches) so many batches share the GPU without a split-K
-# tail; C1 runs 2-way split (16 CTAs per batch, fused output layer)
-SPLIT_DEFAULT = {"c1": 2, "c2": 1}
+STREAMS_DEFAULT = {"c1": 20, "c2": 12}
+# K splits per launch (0 = the engine's choice): both run unsplit -- persistent
+# CTAs per batch whose epilogue is the straight-line level instantiation, so
+# many batches share the GPU without a split-K tail (measured sweep,
+# scripts/gpu_splits.sh: C1 split 1 x 20 in flight 4.03 us/batch vs split 2 x 8
+# 5.06 us; C2 split 1 x 12 11.15 us vs split 2 14.8 us)
+SPLIT_DEFAULT = {"c1": 1, "c2": 1}
 PAPER_SAMPLES_PER_S = {  # PAPER.md:603, KANMLP2 G=5 8-bit LUT on RTX 3090
     "c1": 10000 / 5.9e-3, "c2": 10000 / 5.9e-3,
 }
