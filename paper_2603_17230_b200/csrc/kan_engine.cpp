@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <limits>
@@ -1787,6 +1788,11 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
         // the (bh+2)-row window of one (kx, chunk): box rows bh+2, one image
         const CUtensorMap xmap3 = make_conv_xmap(io, l, pl.IPS, bh + 2, 1);
         const size_t smem = conv3_smem_bytes(pl.BN, R, SA, SB, SX, io.x_kind, ts.bytes, silu);
+  if (std::getenv("KAN_TRACE_LAUNCH"))  // tuning only: the epilogue configuration of each launch
+    std::fprintf(stderr, "launch %s layer %d epi %d res %d out_hw %d lv %d N %d BN %d ld_out %d ld_res %d splits %d al %d%d%d\n", "conv3",
+                 pl.layer_index, p.epi, p.res_kind, p.out_hw, p.out_lv != nullptr, p.N, p.BN, p.ld_out, p.ld_res,
+                 p.splits, static_cast<int>(reinterpret_cast<uintptr_t>(p.out) & 15),
+                 static_cast<int>(reinterpret_cast<uintptr_t>(p.res) & 15), static_cast<int>(reinterpret_cast<uintptr_t>(p.out_lv) & 15));
         ck(launch_conv3(silu ? 2 : 0, xmap3, p, smem, st), "conv3 launch");
         e->last_launches += 1;
         return;
@@ -1960,6 +1966,11 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
   const size_t smem = gemm_smem_bytes(bf16, pl.nbp, pl.BN, SA, SB, SX, io.x_kind, tb, pl.silu != 0, fused_bytes);
   // kernel variant: 0 plain, 1 per-tensor zero point (reference scheme), 2 SiLU base
   const int mode = pl.silu ? 2 : ((!bf16 && pl.wscheme == KAN_W_PER_TENSOR_ASYM) ? 1 : 0);
+  if (std::getenv("KAN_TRACE_LAUNCH"))  // tuning only: the epilogue configuration of each launch
+    std::fprintf(stderr, "launch %s layer %d epi %d res %d out_hw %d lv %d N %d BN %d ld_out %d ld_res %d splits %d al %d%d%d\n", "gather",
+                 pl.layer_index, p.epi, p.res_kind, p.out_hw, p.out_lv != nullptr, p.N, p.BN, p.ld_out, p.ld_res,
+                 p.splits, static_cast<int>(reinterpret_cast<uintptr_t>(p.out) & 15),
+                 static_cast<int>(reinterpret_cast<uintptr_t>(p.res) & 15), static_cast<int>(reinterpret_cast<uintptr_t>(p.out_lv) & 15));
   ck(launch_gather_gemm(bf16, pl.nbp, mode, xmap, p, smem, st), "gather_gemm launch");
   e->last_launches += 1;
 }

@@ -461,7 +461,7 @@ struct TapWalk {
 };
 
 // FE: a straight-line epilogue is compiled in -- 1: fp32 row-major output
-// (+ levels sidecar), 2: next-layer levels.  Separate instantiations, so the
+// (+ levels sidecar), 2: next-layer levels, 3: residual add then levels.  Separate instantiations, so the
 // other variants keep their register allocation.
 template <bool BF16, int NBP, int MODE, int FE = 0>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
@@ -1020,15 +1020,24 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         // 16 columns per TMEM load (BN is a multiple of 16); the two warps of
         // a lane quarter take alternate 16-column groups
         const int half = (warp - W_EPI) >> 2;
-        if constexpr (FE == 2) {
+        if constexpr (FE == 2 || FE == 3) {
           // next-layer levels of full-width tiles, 16 columns per TMEM load:
           // finish4's fp64 (acc - corr) * fs (exact subtraction, as below) and
           // lattice_level_fast, two 16-byte stores per row block
           const int n0 = tl.n_tile * BN;
-          if (p.epi == EPI_LEVEL && !p.f_on && !p.res_kind && n0 + BN <= p.N && (p.ld_out & 7) == 0 &&
+          if (p.epi == EPI_LEVEL && !p.f_on && (FE == 3) == (p.res_kind != 0) &&
+              (FE == 2 || ((p.ld_res & 3) == 0 && (reinterpret_cast<uintptr_t>(p.res) & 15) == 0)) &&
+              n0 + BN <= p.N && (p.ld_out & 7) == 0 &&
               (reinterpret_cast<uintptr_t>(p.out) & 15) == 0 && !(p.dbg_flags & 8)) {
 #pragma unroll 1
             for (int g16 = half; g16 < ngroups / 4; g16 += 2) {
+              float4 rv4[4] = {};
+              if (FE == 3 && row < p.M) {  // residual row segment, loaded before the TMEM read
+                const float4* rp = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(p.res) +
+                                                                   static_cast<size_t>(row) * p.ld_res + n0 + g16 * 16);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) rv4[q] = rp[q];
+              }
               uint32_t r16[16];
               tmem_ld16(tacc + g16 * 16, r16);
               tmem_wait_ld();
@@ -1037,11 +1046,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 uint32_t w[8];
 #pragma unroll
                 for (int e = 0; e < 16; e += 2) {
-                  const double y0 = __dmul_rn(
+                  double y0 = __dmul_rn(
                       __dsub_rn(static_cast<double>(static_cast<int32_t>(r16[e])), s_cols[BN + cl + e]), s_cols[cl + e]);
-                  const double y1 = __dmul_rn(
+                  double y1 = __dmul_rn(
                       __dsub_rn(static_cast<double>(static_cast<int32_t>(r16[e + 1])), s_cols[BN + cl + e + 1]),
                       s_cols[cl + e + 1]);
+                  if constexpr (FE == 3) {
+                    y0 = __dadd_rn(y0, static_cast<double>((&rv4[e >> 2].x)[e & 3]));
+                    y1 = __dadd_rn(y1, static_cast<double>((&rv4[(e + 1) >> 2].x)[(e + 1) & 3]));
+                  }
                   const uint32_t a0 =
                       static_cast<uint32_t>(lattice_level_fast(y0, p.n_lo, p.n_hi_open, p.n_step, p.n_inv_step, p.n_L));
                   const uint32_t a1 =
@@ -1442,9 +1455,10 @@ cudaError_t launch_gather_gemm(bool bf16, int nbp, int mode, const CUtensorMap& 
                     : launch_impl<true, 16, MODE_PLAIN>(xmap, p, smem, st);
   }
   // fp32 row-major outputs take the instantiation with the fast epilogue
-  const int fe = (p.splits != 1 || p.res_kind) ? 0
-                 : (p.epi == EPI_F32 && p.out_hw == 0) ? 1
-                 : (p.epi == EPI_LEVEL && !p.f_on) ? 2 : 0;
+  const int fe = p.splits != 1                                      ? 0
+                 : (p.epi == EPI_F32 && p.out_hw == 0 && !p.res_kind) ? 1
+                 : (p.epi == EPI_LEVEL && !p.f_on)                    ? (p.res_kind ? 3 : 2)
+                                                                      : 0;
   switch (mode) {
     case MODE_ZP:
       return nbp == 8 ? launch_impl<false, 8, MODE_ZP>(xmap, p, smem, st)
@@ -1456,6 +1470,9 @@ cudaError_t launch_gather_gemm(bool bf16, int nbp, int mode, const CUtensorMap& 
       if (fe == 2)
         return nbp == 8 ? launch_impl<false, 8, MODE_SILU, 2>(xmap, p, smem, st)
                         : launch_impl<false, 16, MODE_SILU, 2>(xmap, p, smem, st);
+      if (fe == 3)
+        return nbp == 8 ? launch_impl<false, 8, MODE_SILU, 3>(xmap, p, smem, st)
+                        : launch_impl<false, 16, MODE_SILU, 3>(xmap, p, smem, st);
       return nbp == 8 ? launch_impl<false, 8, MODE_SILU>(xmap, p, smem, st)
                       : launch_impl<false, 16, MODE_SILU>(xmap, p, smem, st);
     default:
@@ -1465,6 +1482,9 @@ cudaError_t launch_gather_gemm(bool bf16, int nbp, int mode, const CUtensorMap& 
       if (fe == 2)
         return nbp == 8 ? launch_impl<false, 8, MODE_PLAIN, 2>(xmap, p, smem, st)
                         : launch_impl<false, 16, MODE_PLAIN, 2>(xmap, p, smem, st);
+      if (fe == 3)
+        return nbp == 8 ? launch_impl<false, 8, MODE_PLAIN, 3>(xmap, p, smem, st)
+                        : launch_impl<false, 16, MODE_PLAIN, 3>(xmap, p, smem, st);
       return nbp == 8 ? launch_impl<false, 8, MODE_PLAIN>(xmap, p, smem, st)
                       : launch_impl<false, 16, MODE_PLAIN>(xmap, p, smem, st);
   }

@@ -107,16 +107,19 @@ def test_strided_conv_on_levels_bit_exact(oracle, k, s, p):
 
 
 @pytest.mark.parametrize("h", [3, 8])
-def test_small_reskan_bit_exact(oracle, h):
+@pytest.mark.parametrize("split", [0, 1])
+def test_small_reskan_bit_exact(oracle, h, split):
     """ResKAN18 topology at reduced width / resolution: stem, identity and
-    projection residual blocks, stride 2, global average pool, linear head."""
+    projection residual blocks, stride 2, global average pool, linear head.
+    split_k=1 keeps every launch persistent, so the straight-line epilogue
+    instantiations (levels, residual + levels, fp32 + residual + sidecar) run."""
     layers = configs.reskan18_layers(width=(16, 32), n_classes=10, in_ch=3)
     desc = {"name": "reskan-small", "grid": {"intervals": 5, "degree": 3}, "input": [3, 16, 16],
             "conv_output": "floor", "layers": layers}
     Ws, Bs = weights_for(desc, seed=h)
     x = np.random.default_rng(h).uniform(-1, 1, (6, 3 * 256)).astype(np.float32)
     e = build(desc, Ws, Bs, mode="bspline-lut", lut_k=8, lut_h=h, bits_w=8,
-              w_scheme=W_PER_CHANNEL_SYM, silu_base=True)
+              w_scheme=W_PER_CHANNEL_SYM, silu_base=True, split_k=split)
     y = e.model_forward(to_dev(x)).cpu().numpy()
     yo = oracle.int_model_forward(desc, Ws, Bs, x, 8, h, W_PER_CHANNEL_SYM, 8)
     np.testing.assert_array_equal(y, yo.astype(np.float32))
