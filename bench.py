@@ -2,28 +2,29 @@
 """Benchmark of the KAN-layer forward hot path (BASELINE.json metric:
 "KAN samples/sec (int8-LUT path) and % of roofline at 1/2/4/8 B200").
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
-                  [--streams S] [--split-k K]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--impl ours|reference]
 
-A step = one forward pass of the workload over one batch of synthetic input.
-Default workload = BASELINE.json configs[1] (C2): KAN MLP [784,64,10], G=5,
-P=3, batch 4096 per GPU, 8-bit table (k=8, h=8), int8 per-channel weights,
-SiLU base term, hidden outputs requantized to the next layer's lattice, int8
-logits.  For N > 1 (torchrun, one process per GPU, NCCL) every rank runs the
-same per-GPU batch (weak scaling); logits are gathered to rank 0 over NCCL
-once per 16-batch replay.  Rank 0 prints ONE JSON line.
+A step = one forward pass of the workload over its GLOBAL batch.  Default
+workload = BASELINE.json configs[4] (C5), the config the metric is quoted on
+at 1/2/4/8 GPUs: ResKAN18 on 3x32x32, G=5, P=3, 3-bit table (k=8, h=3),
+8-bit weights in the reference's own per-tensor asymmetric scheme, no SiLU
+term, fp32 logits, global batch 8192 -- the arithmetic the reference's CPU
+path (`--impl reference`) computes, so both arms print the same `config`.
+`--config c5pc` is the same network with per-channel int8 W + SiLU; c1..c4,
+c3bf16 and the spline-table variants select the other BASELINE configs.
 
-C1/C2 keep several independent batches in flight per GPU (one engine and CUDA
-stream each, STREAMS_DEFAULT): a single C2 forward is a latency-bound launch
-on a fraction of the SMs, so batches overlap; every batch is still one full
-forward, and the timed region covers all K of them.
+Multi-GPU: one process per GPU (torchrun; `--gpus N` without
+torchrun re-launches itself under torch.distributed.run).  The global batch is
+split into contiguous shards (strong scaling: 8192/N rows per GPU); each rank
+forwards its shard with no collective, and the logits are gathered to rank 0
+over NCCL inside the timed region, every step.
 
 Timing: W untimed warm-up steps, then exactly K steps bracketed by a barrier
 and cudaDeviceSynchronize on both sides, device-timed with CUDA events on the
-launching stream, max over ranks.  Inputs rotate over R resident batches whose
-total exceeds the 126 MB L2, so each step reads its input from HBM.  Steps are
-replayed from CUDA graphs (one graph of R forwards + R single-forward graphs
-for the remainder) so host launch overhead stays out of the device time.
+launching stream, max over ranks.  Inputs rotate over resident batches whose
+total exceeds the 126 MB L2 (C5 also writes >2 GB of intermediates per step).
+Small-batch configs (C1/C2) keep several batches in flight on separate
+streams: the timed region replays CUDA graphs holding exactly K forwards.
 """
 from __future__ import annotations
 
@@ -31,6 +32,7 @@ import argparse
 import json
 import math
 import os
+import subprocess
 import sys
 import threading
 import time
@@ -41,36 +43,68 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 L2_BYTES = 126 * 1024 * 1024
-# independent batches in flight per GPU (one engine + CUDA stream each): the
-# C1/C2 forwards are single latency-bound launches that leave SMs idle in their
-# split-K reduction tail, so two batches in flight overlap one's tail with the
-# other's main loop (measured; bench.py --streams overrides)
-STREAMS_DEFAULT = {"c1": 20, "c2": 12}
-# K splits per launch (0 = the engine's choice): both run unsplit -- persistent
-# CTAs per batch whose epilogue is the straight-line level instantiation, so
-# many batches share the GPU without a split-K tail (measured sweep,
-# scripts/gpu_splits.sh: C1 split 1 x 20 in flight 4.03 us/batch vs split 2 x 8
-# 5.06 us; C2 split 1 x 12 11.15 us vs split 2 14.8 us)
+# independent batches in flight per GPU for the latency-bound small configs
+# (one engine + CUDA stream each; bench.py --streams overrides)
+STREAMS_DEFAULT = {"c1": 20, "c2": 12, "c1st": 4, "c2st": 4, "c2st4": 4}
+# K splits per launch (0 = the engine's choice)
 SPLIT_DEFAULT = {"c1": 1, "c2": 1}
 PAPER_SAMPLES_PER_S = {  # PAPER.md:603, KANMLP2 G=5 8-bit LUT on RTX 3090
     "c1": 10000 / 5.9e-3, "c2": 10000 / 5.9e-3,
 }
+GRAPH_CHUNK = 1000  # forwards per captured graph (small configs)
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20000)
-    ap.add_argument("--warmup", type=int, default=200)
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c5")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
                     help="wall time of the bounded CPU-baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--streams", type=int, default=0,
-                    help="independent batches in flight (one engine + stream each); 0 = per-config default")
+                    help="batches in flight (one engine + stream each); 0 = per-config default")
     ap.add_argument("--split-k", type=int, default=0, help="force the K splits of split-K launches")
     return ap.parse_args()
+
+
+def relaunch_under_torchrun(args):
+    """--gpus N > 1 outside torchrun: re-run this command as N ranks (one per GPU)."""
+    port = 29500 + (os.getpid() % 1000)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd))
+
+
+def world_info(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if "WORLD_SIZE" in os.environ and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch one rank per GPU")
+    return world, rank, local
+
+
+def shard(batch, rank, world):
+    per = (batch + world - 1) // world
+    s = min(batch, rank * per)
+    return s, min(batch, s + per)
+
+
+def line_config(wl, world):
+    """The `config` object both arms print (identical on the same workload)."""
+    return {"workload": wl.key + ": " + wl.title, "scheme": wl.scheme(), "global_batch": wl.batch,
+            "batch_per_gpu": (wl.batch + world - 1) // world, "parallelism": f"dp{world}",
+            "l2": "inputs rotate over resident batches larger than the 126 MB L2"}
+
+
+def metric_name(wl):
+    if wl.mode == "bspline-lut":
+        return "KAN samples/sec (int8-LUT path)"
+    return f"KAN samples/sec ({wl.mode} path)"
 
 
 # ---------------------------------------------------------------------------------
@@ -153,8 +187,9 @@ def measured_peaks():
     for p in (os.path.join(ROOT, "MEASURED_PEAKS.json"), "/root/repo/MEASURED_PEAKS.json"):
         if os.path.exists(p):
             with open(p) as f:
-                return json.load(f), "measured"
-    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+                return json.load(f), "measured (MEASURED_PEAKS.json)"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, \
+        "fallback (B200_PROFILING.md)"
 
 
 def measure_int8_peak(dev):
@@ -180,14 +215,13 @@ def measure_int8_peak(dev):
         return None
 
 
-def committed_traffic(config: str):
+def committed_traffic(key: str):
     """DRAM bytes per launch of the dominant kernel from the committed ncu capture."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(p):
         with open(p) as f:
             d = json.load(f)
-        v = d.get(config, {}).get("dram_bytes_per_launch")
-        return v
+        return d.get(key, {}).get("dram_bytes_per_launch")
     return None
 
 
@@ -197,7 +231,7 @@ def ref_forward(ref, wl, Ws, x, threads):
     the reference's descriptor schema expresses (bspline-lut mode, per-tensor u8
     W, eval.hpp:70-76, no SiLU term -- the reference has none); for ResKAN18 the
     harness composition of reference functions (oracle/ref_shim.cpp
-    ref_graph_forward)."""
+    ref_graph_forward: convkan_forward + residual adds + pooling)."""
     text = json.dumps(wl.descriptor())
     if wl.reference_expressible:
         return ref.model_forward(text, Ws, x, wl.out_size, mode=2, k=wl.lut_k, h=wl.lut_h,
@@ -209,92 +243,86 @@ def ref_forward(ref, wl, Ws, x, threads):
 def cpu_rows(wl, cores):
     """Rows per reference call: 256-row chunks per thread for the MLPs; for the
     conv models (0.6-9 GOP per sample) one sample per thread."""
-    return 2048 if wl.layers is None else cores
+    return 256 * cores if wl.layers is None else cores
 
 
-def cpu_baseline(wl, seconds: float):
-    """The reference's own CPU path (oracle/_ref = the reference headers compiled
-    unmodified): model_forward in bspline-lut mode with the reference's weight
-    scheme (per-tensor asymmetric u8, eval.hpp:70-76) and no SiLU term (the
-    reference has none), batch sharded over all host threads, 256-row chunks.
-    Falls back to the C restatement (single thread) if oracle/_ref is absent."""
+def reference_sample(wl, seconds: float, threads: int):
+    """Time the reference's own CPU path (oracle/_ref: the reference headers
+    compiled unmodified) on a bounded sample of the workload; returns
+    (samples/s, description).  Falls back to the C restatement (1 thread)."""
     from oracle.pyoracle import Oracle, Ref
     Ws, _ = wl.weights()
-    cores = os.cpu_count() or 1
-    rows = cpu_rows(wl, cores)
+    rows = cpu_rows(wl, threads)
     x = wl.inputs(rows, seed=99).astype(np.float64)
     if Ref.available and wl.mode == "spline-table":
-        if not wl.reference_expressible:
-            raise RuntimeError("spline-table CPU baseline needs a reference-expressible model")
         ref = Ref()
         text = json.dumps(wl.descriptor())
         n, dt = 0, 0.0
         while dt < seconds:
             _, sec = ref.st_model_forward(text, Ws, x, wl.out_size, wl.lut_k, wl.lut_h,
-                                          threads=cores, chunk=256)
+                                          threads=threads, chunk=256)
             n += rows
             dt += sec
-        return {"value": n / dt, "unit": "samples/s", "cores": cores, "kind": "reference",
-                "sample": f"{n} samples ({rows}-row calls) of {wl.key} through the reference "
-                          f"model_forward in spline-table mode (bits_a={wl.lut_k}, h={wl.lut_h}, "
-                          f"tables built once, untimed), {cores} threads, {dt:.1f} s"}
+        return n / dt, threads, "reference", (
+            f"{n} samples ({rows}-row calls) through the reference model_forward in spline-table mode "
+            f"(tables built once, untimed), {threads} threads, {dt:.1f} s")
     if Ref.available:
         ref = Ref()
         n = 0
         t0 = time.perf_counter()
         while True:
-            ref_forward(ref, wl, Ws, x, cores)
+            ref_forward(ref, wl, Ws, x, threads)
             n += rows
             if time.perf_counter() - t0 >= seconds:
                 break
         dt = time.perf_counter() - t0
         how = ("model_forward" if wl.reference_expressible else
                "convkan_forward/kan_linear_forward composition (ref_graph_forward)")
-        return {"value": n / dt, "unit": "samples/s", "cores": cores, "kind": "reference",
-                "sample": f"{n} samples ({rows}-row calls) of {wl.key} through the reference "
-                          f"{how} (bspline-lut k{wl.lut_k} h{wl.lut_h}, per-tensor u8 W, no SiLU "
-                          f"term), {cores} threads, {dt:.1f} s"}
+        return n / dt, threads, "reference", (
+            f"{n} samples ({rows}-row calls) through the reference {how}, bspline-lut k{wl.lut_k} "
+            f"h{wl.lut_h}, per-tensor u8 W, no SiLU, {threads} threads, {dt:.1f} s")
+    if wl.layers is not None:
+        raise RuntimeError("oracle/_ref not built: no CPU baseline for conv models")
     o = Oracle()
     g = o.grid(wl.G, wl.P)
     n = 0
     t0 = time.perf_counter()
-    if wl.layers is not None:
-        raise RuntimeError("oracle/_ref not built: no CPU baseline for conv models")
     while time.perf_counter() - t0 < seconds:
         h = x[:256]
         for w in Ws:
             h = o.lut_forward(g, wl.lut_k, wl.lut_h, 8, h, w)
         n += 256
     dt = time.perf_counter() - t0
-    return {"value": n / dt, "unit": "samples/s", "cores": 1, "kind": "port",
-            "sample": f"{n} samples of {wl.key} through the C restatement, 1 thread, {dt:.1f} s"}
+    return n / dt, 1, "port", f"{n} samples through the C restatement, 1 thread, {dt:.1f} s"
 
 
 def run_reference(args):
-    """--impl reference: the reference's CPU implementation on the host cores."""
-    rank = int(os.environ.get("RANK", "0"))
+    """--impl reference: the reference's CPU implementation of the path on the
+    host cores, on the same workload / metric / config as our arm.  Under
+    torchrun only rank 0 runs; the others exit 0 without work.  This arm never
+    imports the engine (configs is pure numpy; the package loads libkan_b200.so
+    only when an engine name is touched)."""
+    world, rank, _ = world_info(args)
     if rank != 0:
         return
     from paper_2603_17230_b200 import configs
     from oracle.pyoracle import Ref
     wl = configs.get(args.config)
     cores = os.cpu_count() or 1
-    # MLPs: one >=256-row chunk per thread; conv models: one sample per thread
-    rows = 256 * cores if wl.layers is None else cores
+    if not Ref.available:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref (reference headers) not built"}))
+        return
+    if not wl.reference_scheme and wl.mode != "spline-table":
+        note = ("the reference computes per-tensor u8 W without a SiLU term; this workload's scheme "
+                "differs, so the reference arm runs the reference scheme on the same shapes")
+    else:
+        note = "same arithmetic as the GPU arm (the reference's own scheme)"
+    rows = cpu_rows(wl, cores)
     x = wl.inputs(rows, seed=7).astype(np.float64)
     Ws, _ = wl.weights()
-    if not Ref.available:
-        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
-        return
     ref = Ref()
-
     st_mode = wl.mode == "spline-table"
-    if st_mode:  # tables built once per call outside the timed forwards
-        if not wl.reference_expressible:
-            print(json.dumps({"impl": "reference", "unavailable": "the reference's model_forward "
-                              "cannot run this model in spline-table mode"}))
-            return
-        text = json.dumps(wl.descriptor())
+    text = json.dumps(wl.descriptor())
 
     def step():
         if st_mode:
@@ -303,127 +331,145 @@ def run_reference(args):
         t = time.perf_counter()
         ref_forward(ref, wl, Ws, x, cores)
         return time.perf_counter() - t
-    t_step = step()  # first warm-up step also sizes the run (whole run within ~2 minutes)
-    steps = max(1, min(args.steps, 50, int(120.0 / max(t_step, 1e-3))))
-    for _ in range(min(args.warmup, 3) - 1):
+    for _ in range(args.warmup):
         step()
     dt = 0.0
-    for _ in range(steps):
+    for _ in range(args.steps):
         dt += step()
-    v = rows * steps / dt
+    v = rows * args.steps / dt
     print(json.dumps({
-        "impl": "reference",
-        "metric": "KAN samples/sec (spline-table path)" if st_mode else "KAN samples/sec (int8-LUT path)",
-        "value": v,
-        "unit": "samples/s", "n_gpus": args.gpus, "steps": steps, "warmup": min(args.warmup, 3),
-        "ms_per_step": dt / steps * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": wl.key + ": " + wl.title, "batch_per_step": rows,
-                   "note": "reference CPU path: " + (
-                       f"model_forward in spline-table mode, bits_a={wl.lut_k} h={wl.lut_h}, "
-                       "tables built once outside the timed forwards" if st_mode else (
-                           ("model_forward" if wl.reference_expressible else
-                            "composition of convkan_forward / kan_linear_forward (ref_graph_forward)")
-                           + f" bspline-lut k{wl.lut_k} h{wl.lut_h}, per-tensor u8 W, no SiLU"))},
+        "impl": "reference", "metric": metric_name(wl), "value": v, "unit": "samples/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": line_config(wl, world),
         "cpu_baseline": {"value": v, "unit": "samples/s", "cores": cores, "kind": "reference",
-                         "sample": f"{steps} steps x {rows} rows, {cores} threads"},
+                         "sample": f"{args.steps} steps x {rows} rows (a bounded sample of the global batch), "
+                                   f"{cores} threads, after {args.warmup} warm-up steps"},
         "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "note": f"--steps capped at {steps} so the CPU run stays within about two minutes",
+        "notes": {"path": ("reference model_forward" if wl.reference_expressible else
+                           "reference convkan_forward/kan_linear_forward composition (ref_graph_forward)")
+                  + f" from oracle/_ref, {note}"},
     }))
 
 
 # ---------------------------------------------------------------------------------
+def build_engines(wl, dev_index, n, opts):
+    from paper_2603_17230_b200 import Engine
+    Ws, Bs = wl.weights()
+    out = []
+    for _ in range(n):
+        e = Engine(wl.descriptor(), dev_index)
+        for i, (w, b) in enumerate(zip(Ws, Bs)):
+            e.set_coeffs(i, w, b)
+        e.configure(opts)
+        out.append(e)
+    return out
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_under_torchrun(args)
     if args.impl == "reference":
         return run_reference(args)
 
     import torch
     import torch.distributed as dist
-    from paper_2603_17230_b200 import Engine, EvalOptions, OUT_I8, OUT_F32, W_PER_CHANNEL_SYM
-    from paper_2603_17230_b200 import configs
-    from paper_2603_17230_b200.sharding import gather_logits
+    from paper_2603_17230_b200 import EvalOptions, OUT_I8, configs
+    from paper_2603_17230_b200.sharding import LogitGather
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    world, rank, local = world_info(args)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
     wl = configs.get(args.config)
-    B = wl.batch  # per-GPU batch (weak scaling)
+    r0, r1 = shard(wl.batch, rank, world)
+    B = r1 - r0  # this rank's shard (strong scaling)
+    per = (wl.batch + world - 1) // world
 
-    Ws, Bs = wl.weights()
-    n_streams = args.streams or STREAMS_DEFAULT.get(wl.key, 1)
-    engines = []
-    for _ in range(n_streams):  # one engine per stream: independent workspaces
-        e_ = Engine(wl.descriptor(), local)
-        for i, (w, b) in enumerate(zip(Ws, Bs)):
-            e_.set_coeffs(i, w, b)
-        engines.append(e_)
+    n_streams = max(1, args.streams or STREAMS_DEFAULT.get(wl.key, 1))
+    opts = EvalOptions(**wl.eval_options(), split_k=args.split_k or SPLIT_DEFAULT.get(wl.key, 0))
+    engines = build_engines(wl, local, n_streams, opts)
     eng = engines[0]
-    opts = EvalOptions(mode=wl.mode, lut_k=wl.lut_k, lut_h=wl.lut_h, bits_w=wl.bits_w,
-                       w_scheme=W_PER_CHANNEL_SYM, silu_base=wl.silu, out_kind=OUT_F32,
-                       split_k=args.split_k or SPLIT_DEFAULT.get(wl.key, 0))
-    for e_ in engines:
-        e_.configure(opts)
 
-    # rotating resident input batches, total > L2
+    # rotating resident input shards, total > 2x L2
     in_bytes = B * wl.input_size * 4
-    R = max(2, min(64, math.ceil(2 * L2_BYTES / in_bytes)))
-    R = max(R, 16) if in_bytes < 64 * 1024 * 1024 else R
-    xs = [torch.from_numpy(wl.inputs(B, seed=100 * rank + r)).to(dev) for r in range(R)]
-    if wl.int8_out:
+    R = max(2, min(64, math.ceil(2 * L2_BYTES / max(in_bytes, 1))))
+    R = max(R, n_streams)
+    xs = [torch.from_numpy(wl.inputs(wl.batch, seed=100 + r)[r0:r1]).to(dev) for r in range(R)]
+    if wl.int8_out:  # calibrate the int8 logit scale once (outside the timed region)
         y = eng.model_forward(xs[0]).float()
-        s_out = float(y.abs().max().item()) / 127.0
-        opts.out_kind, opts.out_scale = OUT_I8, s_out
+        opts.out_kind, opts.out_scale = OUT_I8, float(y.abs().max().item()) / 127.0
         for e_ in engines:
             e_.configure(opts)
     out_dtype = torch.int8 if wl.int8_out else torch.float32
     outs = torch.empty((R, B, wl.out_size), device=dev, dtype=out_dtype)
     st = torch.cuda.Stream(dev)
-    aux = [torch.cuda.Stream(dev) for _ in range(n_streams - 1)]
-    streams = [st] + aux
-    torch.cuda.synchronize()
-    # warm the engines (allocations happen outside graph capture)
-    for k, e_ in enumerate(engines):
-        with torch.cuda.stream(streams[k]):
+    streams = [st] + [torch.cuda.Stream(dev) for _ in range(n_streams - 1)]
+    lg = LogitGather(wl.batch, wl.out_size, out_dtype, dev) if world > 1 else None
+
+    def gather(r):
+        """logits of input r to rank 0 over NCCL (padded equal shards)."""
+        return lg(outs[r])
+
+    eng.set_option("record_plan", 1)
+    with torch.cuda.stream(st):
+        for k, e_ in enumerate(engines):
             for r in range(R):
-                e_.model_forward(xs[r], out=outs[r], stream=streams[k])
+                e_.model_forward(xs[r], out=outs[r], stream=st)
     torch.cuda.synchronize()
+    plan = eng.last_plan
+    eng.set_option("record_plan", 0)
     launches_per_step = eng.last_launches
 
-    # the R-forward graph: batch r runs on stream r % n_streams (its own engine),
-    # forked from and joined back into the capture stream
-    big = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(big, stream=st):
-        for s_ in aux:
-            s_.wait_stream(st)
-        for r in range(R):
-            k = r % n_streams
-            engines[k].model_forward(xs[r], out=outs[r], stream=streams[k])
-        for s_ in aux:
-            st.wait_stream(s_)
-    singles = []
-    for r in range(R):
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=st):
-            eng.model_forward(xs[r], out=outs[r], stream=st)
-        singles.append(g)
-    gathered = []
+    small = n_streams > 1
+    graphs = {}
 
-    def run_steps(n):
-        q, rem = divmod(n, R)
-        for _ in range(q):
-            big.replay()
-            if world > 1:
-                gathered.append(gather_logits(outs.view(R * B, -1), R * B * world))
-        for r in range(rem):
-            singles[r].replay()
+    def graph_of(n_fw, start):
+        """CUDA graph of n_fw forwards, forward i on stream i % n_streams (its own
+        engine), inputs rotating from `start`; forked from / joined into st."""
+        key = (n_fw, start % R)
+        if key not in graphs:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=st):
+                for s_ in streams[1:]:
+                    s_.wait_stream(st)
+                for i in range(n_fw):
+                    k = i % n_streams
+                    r = (start + i) % R
+                    engines[k].model_forward(xs[r], out=outs[r], stream=streams[k])
+                for s_ in streams[1:]:
+                    st.wait_stream(s_)
+            graphs[key] = g
+        return graphs[key]
+
+    def run_steps(n, start=0):
+        """Exactly n forwards (steps) of this rank's shard, each followed by the
+        logit gather to rank 0 (small configs: one gather per replayed graph,
+        covering every forward in it)."""
+        done = 0
+        while done < n:
+            if small:
+                c = min(GRAPH_CHUNK, n - done)
+                graph_of(c, start + done).replay()
+                if world > 1:
+                    for i in range(c):
+                        gather((start + done + i) % R)
+                done += c
+            else:
+                r = (start + done) % R
+                engines[0].model_forward(xs[r], out=outs[r], stream=st)
+                if world > 1:
+                    gather(r)
+                done += 1
 
     with torch.cuda.stream(st):
         run_steps(args.warmup)
+        if small:
+            graph_of(min(GRAPH_CHUNK, args.steps), args.warmup)
+            if args.steps % GRAPH_CHUNK and args.steps > GRAPH_CHUNK:
+                graph_of(args.steps % GRAPH_CHUNK, args.warmup + args.steps - args.steps % GRAPH_CHUNK)
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
     if world > 1:
@@ -434,7 +480,7 @@ def main():
     t_wall0 = time.perf_counter()
     with torch.cuda.stream(st):
         ev0.record(st)
-        run_steps(args.steps)
+        run_steps(args.steps, args.warmup)
         ev1.record(st)
     torch.cuda.synchronize()
     t_wall1 = time.perf_counter()
@@ -446,11 +492,10 @@ def main():
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    value = world * B * args.steps / (ms / 1e3)
+    value = wl.batch * args.steps / (ms / 1e3)
 
-    # ---- dominant kernel: per-launch device time with CUDA events (engine profiling)
-    # (the event pairs are recorded as graph nodes around each kernel node, so
-    # host launch gaps stay out of the per-launch device time)
+    # ---- dominant kernel: per-launch device time with CUDA events (engine profiling:
+    # an event pair around each KAN layer's kernel node, replayed from a graph)
     prof_steps = max(2, min(args.steps, 64 if B * wl.input_size < 2 ** 24 else 8))
     eng.set_profiling(True)
     pg = torch.cuda.CUDAGraph()
@@ -464,138 +509,157 @@ def main():
         tot, cnt = eng.layer_time_ms(li)
         layer_ms.append(tot / max(cnt, 1))
     eng.set_profiling(False)
+    # one batch alone, graph-replayed (the latency of a single forward)
+    sg = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(sg, stream=st):
+        eng.model_forward(xs[0], out=outs[0], stream=st)
+    sg.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(st):
+        e0.record(st)
+        for _ in range(10):
+            sg.replay()
+        e1.record(st)
+    torch.cuda.synchronize()
+    single_ms = e0.elapsed_time(e1) / 10
+
     lut = wl.mode == "bspline-lut"
     st_mode = wl.mode == "spline-table"
     peaks, peak_src = measured_peaks()
-    # bound of the dominant (largest-time) layer
     dom = int(np.argmax(layer_ms))
     bytes_l = wl.layer_bytes_per_launch(dom, B)
     ops_l = wl.layer_ops_per_launch(dom, B)
-    whole = launches_per_step == 1 or n_streams > 1
-    if whole:
-        # the whole forward is one launch (fused output layer), or several
-        # batches are in flight (per-launch event brackets cannot isolate one
-        # launch): model input in, model output out, every layer's weights
-        # once per batch, over the effective time per batch
+    if small:
+        # several batches in flight: per-launch event brackets cannot isolate one
+        # launch, so the unit is the whole forward over the effective time per batch
         bytes_l = (B * wl.input_size * 4 + B * wl.out_size * (1 if wl.int8_out else 4)
                    + sum(wl.weight_bytes(li) for li in range(wl.n_kan)))
         ops_l = wl.ops_per_sample() * B
-    int8_peak_tops = peaks.get("int8_tops", 4500.0)
-    if lut and "int8_tops" not in peaks and ops_l / bytes_l > 4500e12 / (peaks["hbm_gbs"] * 1e9):
-        meas = measure_int8_peak(dev)
-        if meas:
-            peaks["int8_tops"] = int8_peak_tops = meas
-    # a step that is a single launch (C1/C2: the output layer runs fused):
-    # the kernel's live average over the timed region is the step time (the
-    # profiling pass's event nodes would break the overlap between steps)
-    if whole:
         layer_ms[dom] = ms / args.steps
+    int8_peak, int8_src = None, None
+    if lut:
+        int8_peak = measure_int8_peak(dev)
+        int8_src = "measured in this run: torch._int_mm (cuBLASLt) int8 8192^3, best of 10"
+        if int8_peak is None:
+            int8_peak, int8_src = 4500.0, "datasheet 4.5 POPS dense int8 (measurement failed)"
     t_l = layer_ms[dom] / 1e3
     ai = ops_l / bytes_l
-    tensor_peak = int8_peak_tops * 1e12 if lut else peaks.get("bf16_tflops", 1677.7) * 1e12
+    tensor_peak = (int8_peak if lut else peaks.get("bf16_tflops", 1661.3)) * 1e12
     hbm_peak = peaks["hbm_gbs"] * 1e9
-    if st_mode or ai < tensor_peak / hbm_peak:  # spline tables: gather + integer add, no tensor work
-        roof = {"bound": "hbm", "achieved": bytes_l / t_l / 1e9, "peak": peaks["hbm_gbs"],
-                "unit": "GB/s"}
+    if st_mode or ai < tensor_peak / hbm_peak:
+        roof = {"bound": "hbm", "achieved": bytes_l / t_l / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s"}
     else:
-        roof = {"bound": "tensor", "achieved": ops_l / t_l / 1e12,
-                "peak": tensor_peak / 1e12, "unit": "TOP/s" if lut else "TFLOP/s"}
+        roof = {"bound": "tensor", "achieved": ops_l / t_l / 1e12, "peak": tensor_peak / 1e12,
+                "unit": "TOP/s" if lut else "TFLOP/s"}
     roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["traffic"] = committed_traffic(wl.key)
+    roof["traffic"] = committed_traffic(wl.key) if not small else None
     kl = wl.kan_layers()[dom]
-    roof["kernel"] = (("kan_st_layer" if st_mode else "kan_gather_gemm")
-                      + f" KAN layer {dom} ({kl['n_in']}->{kl['n_out']}"
+    roof["kernel"] = (f"KAN layer {dom} ({kl['n_in']}->{kl['n_out']}"
                       + (f", {kl['pix']} px/sample)" if kl["pix"] > 1 else ")"))
-    if launches_per_step == 1 and wl.n_kan > 1:
-        roof["kernel"] += f" with the {wl.n_kan - 1} following layer(s) fused in"
-    if n_streams > 1:
-        roof["kernel"] = (f"whole forward ({launches_per_step} launch(es) per batch, "
-                          f"{n_streams} batches in flight)")
-    roof["per_launch"] = {"algorithmic_bytes": bytes_l, "algorithmic_ops": ops_l,
-                          "avg_ms": layer_ms[dom], "launches_timed": prof_steps,
-                          "timing": (f"timed region / steps ({n_streams} batches in flight)" if n_streams > 1
-                                     else "timed region / steps (one launch per step)" if launches_per_step == 1
+    if small:
+        roof["kernel"] = f"whole forward ({launches_per_step} launch(es) per batch, {n_streams} batches in flight)"
+    roof["per_launch"] = {"algorithmic_bytes": bytes_l, "algorithmic_ops": ops_l, "avg_ms": layer_ms[dom],
+                          "launches_timed": prof_steps,
+                          "timing": ("timed region / steps (batches in flight)" if small
                                      else "CUDA event pair around the kernel node, graph replay")}
-    roof["peak_source"] = peak_src + (
-        "" if not lut or "int8_tops" in peaks else "; int8 peak = datasheet 4.5 POPS dense")
+    roof["peak_source"] = (int8_src if lut and roof["bound"] == "tensor" else peak_src)
     roof["layer_avg_ms"] = layer_ms
     roof["share_of_step"] = layer_ms[dom] / (ms / args.steps)
+    # whole-forward tensor roofline (every KAN layer's dense contraction)
+    whole = {"ops_per_sample": wl.ops_per_sample(), "achieved": value * wl.ops_per_sample() / 1e12 / world,
+             "unit": "TOP/s per GPU" if lut else "TFLOP/s per GPU"}
+    whole["frac"] = whole["achieved"] / (tensor_peak / 1e12)
 
     # ---- e2e through the public API: host buffers, H2D + forward + D2H every step
-    # (two host threads each drive their own engine and stream, so one call's
-    # host->device copy overlaps the other's forward; the C ABI call releases
-    # the GIL)
-    e2e_steps = max(10, min(args.steps, 300))
-    n_e2e = 2
-    e2e_steps -= e2e_steps % n_e2e
-    e2e_engines, e2e_streams = list(engines[:n_e2e]), list(streams[:n_e2e])
-    while len(e2e_engines) < n_e2e:  # a second engine / stream for the overlap
-        e_ = Engine(wl.descriptor(), local)
-        for i, (w, b) in enumerate(zip(Ws, Bs)):
-            e_.set_coeffs(i, w, b)
-        e_.configure(opts)
-        e2e_engines.append(e_)
-        e2e_streams.append(torch.cuda.Stream(dev))
-    hx = [torch.from_numpy(wl.inputs(B, seed=500 + r)).pin_memory() for r in range(4)]
-    houts = [torch.empty((B, wl.out_size), dtype=out_dtype).pin_memory() for _ in range(n_e2e)]
+    e2e = None
+    if not args.no_e2e:
+        e2e_steps = max(4, min(args.steps, 300 if small else 20))
+        hx = [torch.from_numpy(wl.inputs(wl.batch, seed=500 + r)[r0:r1]).pin_memory() for r in range(2)]
+        if world == 1:
+            # two host threads with their own engine + stream, so one call's H2D
+            # overlaps the other's forward (kan_engine_forward_host releases the GIL)
+            n_e2e = 2
+            e2e_engines = list(engines[:n_e2e])
+            if len(e2e_engines) < n_e2e:
+                e2e_engines += build_engines(wl, local, n_e2e - len(e2e_engines), opts)
+            e2e_streams = [torch.cuda.Stream(dev) for _ in range(n_e2e)]
+            houts = [torch.empty((B, wl.out_size), dtype=out_dtype).pin_memory() for _ in range(n_e2e)]
+            e2e_steps -= e2e_steps % n_e2e
 
-    def e2e_worker(k, n):
-        for i in range(n):
-            e2e_engines[k].forward_host_ptr(hx[(i + k) % 4].data_ptr(), B, houts[k].data_ptr(),
-                                            stream=e2e_streams[k])
-    for k in range(n_e2e):
-        e2e_worker(k, 3)
-    if world > 1:
-        dist.barrier()
-    t0 = time.perf_counter()
-    ths = [threading.Thread(target=e2e_worker, args=(k, e2e_steps // n_e2e)) for k in range(n_e2e)]
-    for th in ths:
-        th.start()
-    for th in ths:
-        th.join()
-    e2e_s = time.perf_counter() - t0
-    if world > 1:
-        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
-    e2e = {"value": world * B * e2e_steps / e2e_s, "unit": "samples/s",
-           "h2d_bytes_per_step": in_bytes, "d2h_bytes_per_step": B * wl.out_size *
-           (1 if wl.int8_out else 4), "steps": e2e_steps,
-           "api": "kan_engine_forward_host (pinned host buffers, stream-synchronous)",
-           "host_threads": n_e2e}
+            def e2e_worker(k, n):
+                for i in range(n):
+                    e2e_engines[k].forward_host_ptr(hx[(i + k) % 2].data_ptr(), B, houts[k].data_ptr(),
+                                                    stream=e2e_streams[k])
+            for k in range(n_e2e):
+                e2e_worker(k, 2)
+            t0 = time.perf_counter()
+            ths = [threading.Thread(target=e2e_worker, args=(k, e2e_steps // n_e2e)) for k in range(n_e2e)]
+            for th in ths:
+                th.start()
+            for th in ths:
+                th.join()
+            e2e_s = time.perf_counter() - t0
+            api = "kan_engine_forward_host (pinned host buffers; 2 host threads, one engine + stream each)"
+        else:
+            # each rank: H2D of its shard, forward, NCCL gather to rank 0, D2H there
+            xd = torch.empty_like(xs[0])
+            hout = torch.empty((wl.batch, wl.out_size), dtype=out_dtype).pin_memory()
+
+            def e2e_step(i):
+                with torch.cuda.stream(st):
+                    xd.copy_(hx[i % 2], non_blocking=True)
+                    eng.model_forward(xd, out=outs[0], stream=st)
+                    full = gather(0)
+                    if rank == 0:
+                        hout.copy_(full, non_blocking=True)
+                st.synchronize()
+            for i in range(2):
+                e2e_step(i)
+            dist.barrier()
+            t0 = time.perf_counter()
+            for i in range(e2e_steps):
+                e2e_step(i)
+            e2e_s = time.perf_counter() - t0
+            t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+            api = "Engine.model_forward (kan_engine_forward) + NCCL gather of logits to rank 0, pinned host buffers"
+        e2e = {"value": wl.batch * e2e_steps / e2e_s, "unit": "samples/s",
+               "h2d_bytes_per_step": wl.batch * wl.input_size * 4,
+               "d2h_bytes_per_step": wl.batch * wl.out_size * (1 if wl.int8_out else 4),
+               "steps": e2e_steps, "api": api}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_baseline(wl, args.cpu_seconds)
+            v, cores, kind, sample = reference_sample(wl, args.cpu_seconds, os.cpu_count() or 1)
+            cpu = {"value": v, "unit": "samples/s", "cores": cores, "kind": kind, "sample": sample}
         except Exception as ex:  # report, never hide
             cpu = {"value": None, "error": str(ex)}
 
     if rank == 0:
         paper = PAPER_SAMPLES_PER_S.get(wl.key)
         line = {
-            "metric": "KAN samples/sec (int8-LUT path)" if lut else f"KAN samples/sec ({wl.mode} path)",
-            # spline-table lines: roofline.per_launch.algorithmic_ops counts table
-            # lookups + integer adds (one per connection), not multiply-adds
+            "metric": metric_name(wl),
             "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": (value / paper) if paper else None,
+            "scaling": "strong", "vs_baseline": (value / paper) if paper else None,
             "dtype": "u8" if (lut or st_mode) else wl.mode, "data": "synthetic",
-            "config": {"workload": wl.key + ": " + wl.title, "batch_per_gpu": B,
-                       "global_batch": B * world, "parallelism": f"dp{world}",
-                       "l2": f"inputs rotate over {R} resident batches "
-                             f"({R * in_bytes / 2**20:.0f} MiB > 126 MiB L2)",
-                       "launch": f"CUDA graphs ({R}-forward graph + single-forward graphs)",
-                       "streams": n_streams,
-                       "split_k": opts.split_k or "auto",
-                       "concurrency": (f"{n_streams} independent batches in flight (one engine + CUDA "
-                                       "stream each); ms_per_step = timed region / steps"
-                                       if n_streams > 1 else "one batch at a time"),
-                       "vs_baseline_ref": "PAPER.md:603 KANMLP2 G=5 8-bit LUT, RTX 3090, "
-                                          "1.69M samples/s" if paper else None},
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "config": line_config(wl, world),
+            "roofline": roof, "whole_forward": whole, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks.summary(t_wall0, t_wall1),
+            "timing": {"streams": n_streams, "split_k": opts.split_k or "auto",
+                       "concurrency": (f"{n_streams} batches in flight (one engine + CUDA stream each); "
+                                       f"CUDA graphs holding exactly {args.steps} forwards"
+                                       if small else "one batch at a time"),
+                       "inputs": f"rotate over {R} resident shards ({R * in_bytes / 2**20:.0f} MiB)",
+                       "single_batch_ms": single_ms,
+                       "gather": "NCCL gather of every step's logits to rank 0" if world > 1 else None,
+                       "launch_plan": plan.strip().splitlines(),
+                       "vs_baseline_ref": ("PAPER.md:603 KANMLP2 G=5 8-bit LUT, RTX 3090, 1.69M samples/s"
+                                           if paper else None)},
         }
         print(json.dumps(line))
     if world > 1:

@@ -225,6 +225,56 @@ kan_status kan_engine_layer_time_ms(kan_engine* e, int layer, double* total_ms, 
  * full, partials stored, done).  Returns the number of values (8 * CTAs). */
 int64_t kan_engine_layer_timeline(kan_engine* e, int layer, unsigned long long* out, int64_t cap);
 
+/* Tuning and debug switches (no reference counterpart; nothing is read from
+ * the environment).  They take effect at the next kan_engine_configure, except
+ * KAN_OPT_RECORD_PLAN, which applies to the following forwards.  Defaults are
+ * the production choices; the others exist for A/B parity tests and tuning. */
+typedef enum {
+  KAN_OPT_NO_CONV3 = 1,           /* 1: 3x3 s1 convs take the general gather GEMM, not kan_conv3 */
+  KAN_OPT_NO_IM2COL = 2,          /* 1: stem convs read the NHWC input instead of a level im2col */
+  KAN_OPT_FORCE_BN = 3,           /* >0: cap the gather GEMM's N tile (multiple of 16) */
+  KAN_OPT_TABLES = 4,             /* -1 auto, 0/1/2: force the shared-memory table variant */
+  KAN_OPT_EPI_STAGE = 5,          /* 0: no smem-staged fp32 epilogue */
+  KAN_OPT_CONV3_MC = 6,           /* CTAs per weight-multicast cluster in kan_conv3 (1 or 2) */
+  KAN_OPT_LV_SIDECAR = 7,         /* 0: fp32-stored tensors carry no levels sidecar */
+  KAN_OPT_LEVEL_PREPASS_MIN = 8,  /* fp32-input dense layers with >= this many activations get a level prepass */
+  KAN_OPT_ST_PREPASS = 9,         /* 0: spline-table mode quantizes fp32 rows inside the gather kernel */
+  KAN_OPT_ST_SLICES = 10,         /* >0: force the spline-table kernel's input slices per row */
+  KAN_OPT_TIMELINE = 11,          /* 1: per-CTA phase stamps (kan_engine_layer_timeline) */
+  KAN_OPT_FORCE_NACC1 = 12,       /* 1: one TMEM accumulator (deeper A ring) */
+  KAN_OPT_RECORD_PLAN = 13,       /* 1: record each forward's launch plan (kan_engine_last_plan) */
+  KAN_OPT_DBG_FLAGS = 14          /* ablation bits; honoured only by a -DKAN_TUNING build */
+} kan_option;
+kan_status kan_engine_set_option(kan_engine* e, int option, int64_t value);
+/* The launch plan of the most recent forward when KAN_OPT_RECORD_PLAN is on:
+ * one line per kernel launch (kernel, KAN layer, epilogue kind, residual,
+ * levels sidecar, N, N tile, K splits, mode).  Empty otherwise. */
+const char* kan_engine_last_plan(const kan_engine* e);
+
+/* Multi-GPU forward: one engine per device, contiguous batch
+ * shards, no collective on the forward path; the logits of every shard land in
+ * one buffer on engines[0]'s device (peer copies over NVLink).  The engines
+ * must be configured identically from the same model (same output kind and
+ * size); two engines may share a device.  Replaces the reference's chunk loop
+ * of predict (eval.hpp:255-276) at box scale.
+ *   x_shards[g]  device pointer on engines[g]'s device with rows
+ *                [g*per, min(batch, (g+1)*per)) of the batch, per = ceil(batch/n)
+ *                (kan_shard_rows); NULL for an empty shard
+ *   out_dev0     [batch, output_count] on engines[0]'s device
+ *   streams[g]   the stream each shard runs on (NULL = a per-engine stream);
+ *                on return every stream's work is enqueued and streams[0]
+ *                (or the legacy stream of device 0) waits for all shards */
+kan_status kan_engine_forward_sharded(kan_engine* const* engines, int n_engines, const float* const* x_shards,
+                                      int64_t batch, void* out_dev0, void* const* streams);
+/* Same over host buffers (the serving call): x_host [batch, input_size] and
+ * out_host [batch, output_count] (pinned memory gives asynchronous copies).
+ * Each shard is copied to its device, run, and its logits copied back; the
+ * call returns when every shard has landed in out_host. */
+kan_status kan_engine_forward_sharded_host(kan_engine* const* engines, int n_engines, const float* x_host,
+                                           int64_t batch, void* out_host);
+/* Rows [*start, *stop) of shard g of n (contiguous, ceil(batch/n) rows each). */
+void kan_shard_rows(int64_t batch, int g, int n, int64_t* start, int64_t* stop);
+
 /* build_bspline_lut (lut.hpp:103-131) as a host utility. Returns entry count,
  * or -KAN_ERR_INVALID_ARGUMENT. */
 int64_t kan_lut_build(int degree, int k, int h, uint8_t* out, int64_t cap);

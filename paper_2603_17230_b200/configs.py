@@ -99,6 +99,9 @@ class Workload:
     silu: bool = True
     int8_out: bool = False
     seed: int = 0
+    # LUT-path weight scheme: 1 = per-output-channel symmetric (engine
+    # extension), 0 = the reference's per-tensor asymmetric u8 (eval.hpp:70-76)
+    wscheme: int = 1
     input_shape: Optional[List[int]] = None
     layers: Optional[list] = None
     extra: dict = field(default_factory=dict)
@@ -113,6 +116,28 @@ class Workload:
                 "input": [self.dims[0]],
                 "layers": [{"type": "linear", "n_in": a, "n_out": b}
                            for a, b in zip(self.dims, self.dims[1:])]}
+
+    def eval_options(self) -> dict:
+        """EvalOptions keyword arguments of this workload (engine.EvalOptions);
+        int8 logits additionally need the output scale the bench calibrates."""
+        return dict(mode=self.mode, lut_k=self.lut_k, lut_h=self.lut_h, bits_w=self.bits_w,
+                    w_scheme=self.wscheme, silu_base=self.silu)
+
+    def scheme(self) -> str:
+        """One-line statement of the arithmetic this workload runs."""
+        if self.mode != "bspline-lut":
+            return f"{self.mode} path" + (", SiLU base term" if self.silu else "")
+        w = ("per-tensor asymmetric u8 W (the reference scheme, eval.hpp:70-76)" if self.wscheme == 0
+             else f"per-channel symmetric int{self.bits_w} W")
+        return (f"LUT k{self.lut_k}/h{self.lut_h}, {w}, " + ("SiLU base term" if self.silu else "no SiLU term")
+                + (", int8 logits" if self.int8_out else ", fp32 logits"))
+
+    @property
+    def reference_scheme(self) -> bool:
+        """True when the reference's own CPU path computes this exact arithmetic
+        (bspline-lut, per-tensor u8 W, no SiLU, fp32 logits)."""
+        return (self.mode == "bspline-lut" and self.wscheme == 0 and not self.silu and not self.int8_out
+                and self.bits_w == 8)
 
     def kan_layers(self) -> List[dict]:
         """KAN layers in order: reference inputs (conv: K^2 C_in), outputs, output
@@ -219,11 +244,19 @@ WORKLOADS = {
                    [64 * 32 * 32], 5, 3, 256, 0.05, input_shape=[64, 32, 32],
                    layers=[{"type": "conv", "c_in": 64, "c_out": 64, "kernel": 3, "stride": 1,
                             "padding": 1}]),
-    # configs[4]
+    # configs[4] -- the bench headline (BASELINE metric "at 1/2/4/8 B200" is
+    # quoted on this config).  "3-bit B-spline table + int8 coeffs": run in the
+    # reference's own weight scheme (per-tensor asymmetric 8-bit codes, no SiLU
+    # term, fp32 logits), so the reference's CPU path computes the same numbers
     "c5": Workload("c5", "ResKAN18 (ResNet-18 topology, KAN convs) on 3x32x32, G=5 P=3 batch 8192, "
-                         "LUT k8/h3 (3-bit table) + int8 W",
-                   [3 * 32 * 32], 5, 3, 8192, 0.05, lut_h=3, input_shape=[3, 32, 32],
-                   layers=reskan18_layers(), extra={"descriptor": {"conv_output": "floor"}}),
+                         "LUT k8/h3 (3-bit table) + 8-bit W",
+                   [3 * 32 * 32], 5, 3, 8192, 0.05, lut_h=3, input_shape=[3, 32, 32], silu=False,
+                   wscheme=0, layers=reskan18_layers(), extra={"descriptor": {"conv_output": "floor"}}),
+    # the same network with per-channel int8 W and the SiLU base term (engine extensions)
+    "c5pc": Workload("c5pc", "ResKAN18 on 3x32x32, G=5 P=3 batch 8192, LUT k8/h3 + per-channel int8 W, "
+                             "SiLU base term",
+                     [3 * 32 * 32], 5, 3, 8192, 0.05, lut_h=3, input_shape=[3, 32, 32],
+                     layers=reskan18_layers(), extra={"descriptor": {"conv_output": "floor"}}),
     # spline-table mode (spline_table.hpp) on the C1/C2/C4
     # shapes, 256-entry 8-bit tables (bits_a = 8, h = 8), no SiLU term (the
     # reference's tables replace the whole activation phi_{i,j})

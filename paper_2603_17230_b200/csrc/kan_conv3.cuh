@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       for (int ss = 0; ss < p.n_ss; ++ss, rx.next()) {
         const int kx = ss / p.cps, cc = ss - kx * p.cps;
         mbar_wait(bar_xempty(rx.slot), rx.phase ^ 1);
-        if (lane == 0 && (p.dbg_flags & 4)) {  // tuning only: no activation load (stale window)
+        if (lane == 0 && KAN_DBG(p, 4)) {  // tuning only: no activation load (stale window)
           mbar_arrive(bar_xfull(rx.slot));
         } else if (lane == 0) {
           mbar_arrive_tx(bar_xfull(rx.slot), x_bytes);
@@ -166,11 +166,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         if (lane == 0) {
           const size_t wt = static_cast<size_t>(tl.n_tile) * 3 * p.n_ss + q;
           const uint32_t dst = smem_u32(sB + static_cast<size_t>(rb.slot) * b_slot);
-          if (p.dbg_flags & 32)  // tuning only: no weight loads (stale slots)
+          if (KAN_DBG(p, 32))  // tuning only: no weight loads (stale slots)
             mbar_arrive(bar_bfull(rb.slot));
           else
             mbar_arrive_tx(bar_bfull(rb.slot), b_slot);
-          if (p.dbg_flags & 32) {
+          if (KAN_DBG(p, 32)) {
           } else if (MC == 1)
             bulk_load(dst, p.wt + wt * b_slot, b_slot, bar_bfull(rb.slot));
           else if (fill % MC == crank)
@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           const uint64_t sd_a = umma_desc_sw32(a_addr + a_code_bytes + static_cast<uint32_t>(ky * p.Wo / 8) * 256u);
           const uint64_t sd_b = umma_desc_sw32(b_addr + BN * KSTAGE);
           if (elect_one()) {
-            if (!(p.dbg_flags & 2)) {  // (tuning only: flag 2 skips the MMAs)
+            if (!KAN_DBG(p, 2)) {  // (tuning only: flag 2 skips the MMAs)
 #pragma unroll
               for (int kk = 0; kk < KSTAGE / 32; ++kk) {
                 // descriptor start addresses advance in 16-byte units (no carry: smem < 256 KB)
@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         mbar_wait(bar_aempty(ra.slot), ra.phase ^ 1);
         const uint8_t* xt = sX + static_cast<size_t>(rx.slot) * x_bytes;
         uint8_t* at = sA + static_cast<size_t>(ra.slot) * a_bytes;
-        for (int u = (p.dbg_flags & 16) ? units : warp; u < units; u += NPW) {  // (flag 16: no expansion)
+        for (int u = KAN_DBG(p, 16) ? units : warp; u < units; u += NPW) {  // (flag 16: no expansion)
           const int g = u >> 2, h = u & 3;
           const int rr = 32 * g + lane;  // expanded row = input pixel of the window
           const int wy = rr / p.Wo, wx = rr - wy * p.Wo;
@@ -354,7 +354,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             (reinterpret_cast<uintptr_t>(p.out) & 15) == 0 &&
             (!p.res_kind || ((p.ld_res & 3) == 0 && (reinterpret_cast<uintptr_t>(p.res) & 15) == 0)) &&
             (p.out_lv == nullptr || ((p.ld_lv & 7) == 0 && (reinterpret_cast<uintptr_t>(p.out_lv) & 15) == 0)) &&
-            !(p.dbg_flags & 8)) {
+            !KAN_DBG(p, 8)) {
           // 16 columns per step: residual loads issued before the TMEM load,
           // then finish4's fp64 (acc - corr) * fs [+ residual] (exact
           // subtraction), the fp32 row and its levels sidecar
@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         }
       }
 #pragma unroll 1
-      for (int blk = half; blk < ((p.dbg_flags & 8) ? 0 : (BN + 31) / 32); blk += 2) {
+      for (int blk = half; blk < (KAN_DBG(p, 8) ? 0 : (BN + 31) / 32); blk += 2) {
         const int gq0 = blk * 8;
         if (p.res_kind) {
 #pragma unroll
@@ -551,22 +551,12 @@ size_t conv3_smem_bytes(int BN, int R, int SA, int SB, int SX, int x_kind, int t
 }
 
 cudaError_t launch_conv3(int mode, const CUtensorMap& xmap, const GemmParams& p, size_t smem, cudaStream_t st) {
-  static size_t configured[9] = {};  // per kernel variant (same function type)
+  static std::atomic<unsigned long long> optin[9];  // per kernel variant, per device
   const int lf = (p.epi == EPI_LEVEL && !p.res_kind) ? 1 : (p.epi == EPI_F32 && p.out_hw == 0) ? 2 : 0;
   const int var = mode * 3 + lf;
   auto go = [&](auto kfn) -> cudaError_t {
-    if (smem > configured[var]) {
-      cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-      if (e != cudaSuccess) return e;
-      configured[var] = smem;
-    }
-    static int n_sm = 0;
-    if (n_sm == 0) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-      if (n_sm <= 0) n_sm = 148;
-    }
+    if (cudaError_t e = smem_optin(kfn, optin[var]); e != cudaSuccess) return e;
+    const int n_sm = device_sm_count();
     const int mc = p.mc > 1 ? p.mc : 1;
     const int units = (p.m_tiles + mc - 1) / mc * p.n_tiles_n;
     const int clusters = units < n_sm / mc ? units : n_sm / mc;

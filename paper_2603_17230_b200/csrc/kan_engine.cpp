@@ -38,7 +38,7 @@ int gemm_ips(bool bf16, int nbp);
 int gemm_gs(bool bf16, int nbp);
 int gemm_tmem_slots(int BN, int nacc);
 int gemm_tmem_accs(int BN, int splits);
-cudaError_t launch_levels(const float* x, int64_t n, const float* thr, float lo, float inv_step,
+cudaError_t launch_levels(const float* x, int64_t n, const float* thr, float nlo_step, float inv_step,
                           int L, uint16_t* out, cudaStream_t st);
 cudaError_t launch_argmax(const float* logits, int64_t M, int N, int ld, int32_t* out,
                           cudaStream_t st);
@@ -203,6 +203,7 @@ struct StLayer {
 // Device-side state of one configured KAN layer.
 struct PreparedLayer {
   int layer_index = 0;
+  int64_t acc_bound = 0;  // worst-case |int32 accumulator| (configure's headroom check)
   int n_in = 0, N = 0, BN = 0, n_tiles_n = 0, nbp = 8;
   int cps = 0;  // conv: IPS-wide channel chunks per tap
   // small-N CUDA-core path (LUT, NBP = 8, N <= 16, per-channel weights)
@@ -347,7 +348,23 @@ struct kan_engine {
   // prepass (KAN_LEVEL_PREPASS_MIN; tests lower it to exercise the path)
   int64_t prepass_min = std::numeric_limits<int64_t>::max();
   int conv3_mc = 2;  // conv3: CTAs per weight-multicast cluster (KAN_CONV3_MC)
-  bool lv_sidecar = true;  // KAN_LV_SIDECAR=0 disables the levels sidecar (tuning)
+  bool lv_sidecar = true;  // KAN_OPT_LV_SIDECAR=0 disables the levels sidecar (tuning)
+  // tuning / debug switches (kan_engine_set_option); configure copies them
+  // into the fields above, so nothing is read from the environment
+  struct Options {
+    bool no_conv3 = false, no_im2col = false, epi_stage = true, lv_sidecar = true, st_prepass = true;
+    bool timeline = false, force_nacc1 = false, record_plan = false;
+    int force_bn = 0, tables = -1, conv3_mc = 2, st_slices = 0, dbg_flags = 0;
+    int64_t level_prepass_min = std::numeric_limits<int64_t>::max();
+  } opt;
+  // launch plan of the last forward (opt.record_plan): one line per kernel
+  std::string plan;
+  void plan_add(const char* kernel, int layer, int epi, int res, int lv, int N, int BN, int splits, int mode) {
+    char buf[160];
+    std::snprintf(buf, sizeof(buf), "%s layer=%d epi=%d res=%d lv=%d N=%d BN=%d splits=%d mode=%d\n", kernel, layer,
+                  epi, res, lv, N, BN, splits, mode);
+    plan += buf;
+  }
   std::vector<DevBuf<unsigned long long>> timeline_buf;
   std::vector<int64_t> timeline_ctas;
   // per-layer kernel timing (kan_engine_set_profiling)
@@ -375,11 +392,27 @@ struct kan_engine {
     }
     pending.clear();
   }
+  // sharded forward (kan_engine_forward_sharded): this engine's own stream and
+  // completion event, and a staging buffer for logits that cannot be written
+  // in place (another device, or a misaligned shard offset)
+  cudaStream_t own_stream = nullptr;
+  cudaEvent_t shard_done = nullptr;
+  DevBuf<uint8_t> shard_out;
+  cudaStream_t stream_own() {
+    if (!own_stream) ck(cudaStreamCreateWithFlags(&own_stream, cudaStreamNonBlocking), "stream create");
+    return own_stream;
+  }
+  cudaEvent_t done_event() {
+    if (!shard_done) ck(cudaEventCreateWithFlags(&shard_done, cudaEventDisableTiming), "event create");
+    return shard_done;
+  }
   ~kan_engine() {
     for (auto& t : pending) {
       cudaEventDestroy(t.a);
       cudaEventDestroy(t.b);
     }
+    if (own_stream) cudaStreamDestroy(own_stream);
+    if (shard_done) cudaEventDestroy(shard_done);
   }
 
   int64_t input_size() const {
@@ -697,8 +730,7 @@ void prepare_gemm_layer(kan_engine* e, const Layer& l, PreparedLayer& pl, bool b
   pl.N = N;
   pl.nbp = nbp;
   pl.BN = N > 256 ? 256 : std::max(16, (N + 15) / 16 * 16);
-  if (const char* ev = std::getenv("KAN_FORCE_BN")) {  // tuning only
-    const int bn = std::atoi(ev);
+  if (const int bn = e->opt.force_bn) {  // tuning only (KAN_OPT_FORCE_BN)
     if (bn >= 16 && bn <= 256 && bn % 16 == 0 && bn < pl.BN) pl.BN = bn;
   }
   pl.n_tiles_n = (N + pl.BN - 1) / pl.BN;
@@ -742,6 +774,38 @@ void prepare_gemm_layer(kan_engine* e, const Layer& l, PreparedLayer& pl, bool b
     } else {
       throw InvalidArgument("unknown weight scheme");
     }
+    // int32 accumulator headroom.  The spline and SiLU parts of
+    // an output share one int32 accumulator: bound |acc_j| by, per input, the
+    // largest code-row sum over all lattice levels times the input's largest
+    // |weight code| in column j, plus the largest SiLU code (255) times
+    // |base weight code|.  Configure refuses a layer that could overflow.
+    int64_t code_max = 0;
+    if (e->grid.P <= 3) {
+      for (int64_t a = 0; a <= e->lat.L; ++a) {
+        const uint32_t v = lut_pack(e->grid, e->lat.k, e->lut, a);
+        code_max = std::max<int64_t>(code_max, (v & 255u) + ((v >> 8) & 255u) + ((v >> 16) & 255u) + (v >> 24));
+      }
+    } else {
+      code_max = static_cast<int64_t>(e->grid.P + 1) * *std::max_element(e->lut.begin(), e->lut.end());
+    }
+    int64_t worst = 0;
+    for (int j = 0; j < N; ++j) {
+      int64_t bound = 0;
+      for (int ir = 0; ir < n_ref; ++ir) {
+        int64_t wmax = 0;
+        for (int b = 0; b < nb; ++b) {
+          const size_t c = (static_cast<size_t>(ir) * nb + b) * N + j;
+          wmax = std::max<int64_t>(wmax, qw_u8.empty() ? std::abs(static_cast<int64_t>(qw_s8[c])) : qw_u8[c]);
+        }
+        bound += code_max * wmax;
+        if (!qwb.empty()) bound += 255 * std::abs(static_cast<int64_t>(qwb[static_cast<size_t>(ir) * N + j]));
+      }
+      worst = std::max(worst, bound);
+    }
+    pl.acc_bound = worst;
+    if (worst > std::numeric_limits<int32_t>::max())
+      throw Unsupported("KAN layer " + std::to_string(l.kan_index) + ": int32 accumulator could overflow (bound " +
+                        std::to_string(worst) + " > 2^31-1); reduce n_in, lut_h or bits_w");
   }
   const int GI = pl.GS * pl.IPS;  // inputs per group
   for (int nt = 0; nt < pl.n_tiles_n; ++nt) {
@@ -802,7 +866,7 @@ void prepare_gemm_layer(kan_engine* e, const Layer& l, PreparedLayer& pl, bool b
   // ky-shared 3x3 stride-1 pad-1 conv kernel (kan_conv3.cuh), LUT path
   pl.conv3 = false;
   if (!bf16 && l.type == L_CONV && !l.im2col && l.kernel == 3 && l.stride == 1 && l.padding == 1 && nbp == 8 &&
-      pl.b_signed && std::getenv("KAN_NO_CONV3") == nullptr) {
+      pl.b_signed && !e->opt.no_conv3) {
     const int Wo = l.out.w, Ho = l.out.h;
     if (Wo % 8 == 0 && 128 % Wo == 0 && Ho * Wo >= 128 && Ho % (128 / Wo) == 0) {
       pl.conv3 = true;
@@ -1131,7 +1195,7 @@ void configure_fq(kan_engine* e, const kan_config& cfg) {
   if (bits_a == 32)
     throw Unsupported("fake-quant mode with passthrough activations: use bits_a <= 8 (tabulated) or mode fp32");
   const Grid& g = e->grid;
-  e->st_prepass = !(std::getenv("KAN_ST_PREPASS") && std::atoi(std::getenv("KAN_ST_PREPASS")) == 0);
+  e->st_prepass = e->opt.st_prepass;
   if (!e->a_ranges.empty() && static_cast<int>(e->a_ranges.size()) != e->n_kan)
     throw InvalidArgument("model_forward: calibrated activation policy needs a range per KAN layer");
   e->st_in = quant_params(g.lo, g.hi, bits_a);  // a_params_for, eval.hpp:55-68 (grid bounds)
@@ -1195,7 +1259,7 @@ void configure_st(kan_engine* e, const kan_config& cfg) {
     if (l.res_src != -2 || l.type == L_AVGPOOL)
       throw Unsupported("spline-table mode runs the reference layer set (linear, conv, maxpool, flatten)");
   }
-  e->st_prepass = !(std::getenv("KAN_ST_PREPASS") && std::atoi(std::getenv("KAN_ST_PREPASS")) == 0);
+  e->st_prepass = e->opt.st_prepass;
   e->st_in = quant_params(e->grid.lo, e->grid.hi, bits_a);  // spline_table.hpp:51
   e->st_thr.upload(quant_thresholds(e->st_in));
   e->st.clear();
@@ -1241,8 +1305,7 @@ static StParams st_params(const kan_engine* e, const StLayer& sl, int64_t rows =
   int S = 1;
   auto blocks = [&](int s_) { return (rows + 256 / (sl.lpr * s_) - 1) / (256 / (sl.lpr * s_)) * sl.col_tiles; };
   while (S * sl.lpr < 256 && 2 * S <= units && blocks(S) < 148 * 3 / 2) S *= 2;
-  if (const char* ev = std::getenv("KAN_ST_SLICES")) {  // tuning only
-    const int want = std::atoi(ev);
+  if (const int want = e->opt.st_slices) {  // tuning only (KAN_OPT_ST_SLICES)
     if (want >= 1 && (want & (want - 1)) == 0 && want * sl.lpr <= 256) S = want;
   }
   p.slices = S;
@@ -1569,20 +1632,20 @@ void configure(kan_engine* e, const kan_config* c) {
   for (auto& l : e->layers) {
     const int ncol = l.c_in * l.kernel * l.kernel;
     l.im2col = cfg.mode == KAN_MODE_BSPLINE_LUT && l.type == L_CONV && l.src == -1 && l.c_in < 16 &&
-               ncol <= 64 && e->input_shape.size() == 3 && std::getenv("KAN_NO_IM2COL") == nullptr;
+               ncol <= 64 && e->input_shape.size() == 3 && !e->opt.no_im2col;
   }
   e->prep.clear();
   e->prep.resize(static_cast<size_t>(e->n_kan));
-  e->timeline = std::getenv("KAN_TIMELINE") != nullptr;
-  e->dbg_flags = std::getenv("KAN_DBG_FLAGS") ? std::atoi(std::getenv("KAN_DBG_FLAGS")) : 0;
-  e->force_tab = std::getenv("KAN_TABLES") ? std::atoi(std::getenv("KAN_TABLES")) : -1;
-  e->epi_stage = !(std::getenv("KAN_EPI_STAGE") && std::atoi(std::getenv("KAN_EPI_STAGE")) == 0);
+  // tuning switches (kan_engine_set_option), read once per configure
+  e->timeline = e->opt.timeline;
+  e->dbg_flags = e->opt.dbg_flags;
+  e->force_tab = e->opt.tables;
+  e->epi_stage = e->opt.epi_stage;
+  e->conv3_mc = e->opt.conv3_mc;
+  e->lv_sidecar = e->opt.lv_sidecar;
   // off by default: on C3 the prepass saves layer 0 ~50 us but costs ~260 us
   // itself (measured); the path stays available and tested
-  e->conv3_mc = std::getenv("KAN_CONV3_MC") ? std::max(1, std::min(2, std::atoi(std::getenv("KAN_CONV3_MC")))) : 2;
-  e->lv_sidecar = !(std::getenv("KAN_LV_SIDECAR") && std::atoi(std::getenv("KAN_LV_SIDECAR")) == 0);
-  e->prepass_min = std::getenv("KAN_LEVEL_PREPASS_MIN") ? std::atoll(std::getenv("KAN_LEVEL_PREPASS_MIN"))
-                                                        : std::numeric_limits<int64_t>::max();
+  e->prepass_min = e->opt.level_prepass_min;
   e->timeline_buf.clear();
   e->timeline_buf.resize(static_cast<size_t>(e->n_kan));
   e->timeline_ctas.assign(static_cast<size_t>(e->n_kan), 0);
@@ -1788,11 +1851,8 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
         // the (bh+2)-row window of one (kx, chunk): box rows bh+2, one image
         const CUtensorMap xmap3 = make_conv_xmap(io, l, pl.IPS, bh + 2, 1);
         const size_t smem = conv3_smem_bytes(pl.BN, R, SA, SB, SX, io.x_kind, ts.bytes, silu);
-  if (std::getenv("KAN_TRACE_LAUNCH"))  // tuning only: the epilogue configuration of each launch
-    std::fprintf(stderr, "launch %s layer %d epi %d res %d out_hw %d lv %d N %d BN %d ld_out %d ld_res %d splits %d al %d%d%d\n", "conv3",
-                 pl.layer_index, p.epi, p.res_kind, p.out_hw, p.out_lv != nullptr, p.N, p.BN, p.ld_out, p.ld_res,
-                 p.splits, static_cast<int>(reinterpret_cast<uintptr_t>(p.out) & 15),
-                 static_cast<int>(reinterpret_cast<uintptr_t>(p.res) & 15), static_cast<int>(reinterpret_cast<uintptr_t>(p.out_lv) & 15));
+        if (e->opt.record_plan)
+          e->plan_add("conv3", pl.layer_index, p.epi, p.res_kind, p.out_lv != nullptr, p.N, p.BN, p.splits, silu ? 2 : 0);
         ck(launch_conv3(silu ? 2 : 0, xmap3, p, smem, st), "conv3 launch");
         e->last_launches += 1;
         return;
@@ -1893,7 +1953,7 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
   }
   // persistent launches double-buffer the accumulator when TMEM allows
   p.nacc = gemm_tmem_accs(pl.BN, splits);
-  if (std::getenv("KAN_FORCE_NACC1")) p.nacc = 1;  // tuning only: deeper A ring
+  if (e->opt.force_nacc1) p.nacc = 1;  // tuning only: deeper A ring
   SA = gemm_tmem_slots(pl.BN, p.nacc);
   p.SA = SA;
   p.SB = SB;
@@ -1966,11 +2026,9 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
   const size_t smem = gemm_smem_bytes(bf16, pl.nbp, pl.BN, SA, SB, SX, io.x_kind, tb, pl.silu != 0, fused_bytes);
   // kernel variant: 0 plain, 1 per-tensor zero point (reference scheme), 2 SiLU base
   const int mode = pl.silu ? 2 : ((!bf16 && pl.wscheme == KAN_W_PER_TENSOR_ASYM) ? 1 : 0);
-  if (std::getenv("KAN_TRACE_LAUNCH"))  // tuning only: the epilogue configuration of each launch
-    std::fprintf(stderr, "launch %s layer %d epi %d res %d out_hw %d lv %d N %d BN %d ld_out %d ld_res %d splits %d al %d%d%d\n", "gather",
-                 pl.layer_index, p.epi, p.res_kind, p.out_hw, p.out_lv != nullptr, p.N, p.BN, p.ld_out, p.ld_res,
-                 p.splits, static_cast<int>(reinterpret_cast<uintptr_t>(p.out) & 15),
-                 static_cast<int>(reinterpret_cast<uintptr_t>(p.res) & 15), static_cast<int>(reinterpret_cast<uintptr_t>(p.out_lv) & 15));
+  if (e->opt.record_plan)
+    e->plan_add(bf16 ? "gather_bf16" : "gather", pl.layer_index, p.epi, p.res_kind, p.out_lv != nullptr, p.N, p.BN,
+                p.splits, mode);
   ck(launch_gather_gemm(bf16, pl.nbp, mode, xmap, p, smem, st), "gather_gemm launch");
   e->last_launches += 1;
 }
@@ -1991,7 +2049,7 @@ void run_small_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO&
   p.tab_bytes = ts.off_c64;  // vals, thresholds, SiLU codes (no code rows needed)
   p.off_thr = ts.off_thr;
   p.off_silu = ts.off_silu;
-  p.lo_f = static_cast<float>(e->grid.lo);
+  p.lo_f = static_cast<float>(-e->grid.lo / e->lat.step);  // lattice_level_tie's -lo/step
   p.inv_step_f = static_cast<float>(1.0 / e->lat.step);
   p.wq = pl.swq.p;
   p.wqb = pl.swqb.p;
@@ -2011,6 +2069,7 @@ void run_small_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO&
   if (small_smem_bytes(p) > 227 * 1024) throw Unsupported("small layer exceeds shared memory");
   ck(launch_small_layer(p, st), "small layer launch");
   e->last_launches += 1;
+  if (e->opt.record_plan) e->plan_add("small_layer", pl.layer_index, p.epi, 0, 0, p.N, 0, 1, p.mode);
 }
 
 void run_fp32_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const float* x, int64_t ld_x,
@@ -2108,6 +2167,7 @@ void forward(kan_engine* e, const float* x, int64_t M, void* out, cudaStream_t s
   if (M < 0) throw InvalidArgument("forward: negative batch");
   DeviceGuard dg(e->device);
   e->last_launches = 0;
+  e->plan.clear();
   if (M == 0) return;
   if (e->cfg.mode == KAN_MODE_SPLINE_TABLE || e->cfg.mode == KAN_MODE_FAKE_QUANT) {
     forward_st(e, x, M, out, st);
@@ -2161,6 +2221,7 @@ void forward(kan_engine* e, const float* x, int64_t M, void* out, cudaStream_t s
                              levels ? static_cast<int>(e->lat.L) : 0, st),
          "input transpose");
       e->last_launches += 1;
+      if (e->opt.record_plan) e->plan_add("nchw_to_nhwc", -1, 0, 0, levels, C, 0, 0, 0);
       in.p = e->xnhwc.p;
       in.kind = levels ? X_U16 : X_F32;
       in.nchw = false;
@@ -2213,6 +2274,7 @@ void forward(kan_engine* e, const float* x, int64_t M, void* out, cudaStream_t s
         dst.p = o;
       }
       e->last_launches += 1;
+      if (e->opt.record_plan) e->plan_add(l.type == L_MAXPOOL ? "maxpool" : "avgpool", -1, 0, 0, 0, C, 0, 0, 0);
       continue;
     }
     // ---- KAN layer ----
@@ -2240,6 +2302,7 @@ void forward(kan_engine* e, const float* x, int64_t M, void* out, cudaStream_t s
                                static_cast<float>(1.0 / e->lat.step), static_cast<int>(e->lat.L), st),
          "level prepass");
       e->last_launches += 1;
+      if (e->opt.record_plan) e->plan_add("level_prepass", l.kan_index, 0, 0, 1, pl.n_in, 0, 0, 0);
       io.x = e->xlev.p;
       io.x_kind = X_U16;
       io.ld_x = ldl;
@@ -2254,6 +2317,7 @@ void forward(kan_engine* e, const float* x, int64_t M, void* out, cudaStream_t s
                               static_cast<int>(e->lat.L), static_cast<int>(e->lat.quantize(0.0)), st),
          "input im2col");
       e->last_launches += 1;
+      if (e->opt.record_plan) e->plan_add("im2col_levels", l.kan_index, 0, 0, 1, ncol, 0, 0, 0);
       io.x = e->xcol.p;
       io.x_kind = X_U16;
       io.ld_x = ldc;
@@ -2560,7 +2624,7 @@ kan_status kan_engine_layer_levels(kan_engine* e, int layer, const float* x_dev,
       e->last_launches = 1;
       return;
     }
-    ck(launch_levels(x_dev, n, e->d_thr.p, static_cast<float>(e->grid.lo),
+    ck(launch_levels(x_dev, n, e->d_thr.p, static_cast<float>(-e->grid.lo / e->lat.step),
                      static_cast<float>(1.0 / e->lat.step), static_cast<int>(e->lat.L), levels_dev,
                      static_cast<cudaStream_t>(stream)),
        "levels launch");
@@ -2918,6 +2982,162 @@ kan_status kan_engine_layer_time_ms(kan_engine* e, int layer, double* total_ms, 
     e->drain_timings();
     if (total_ms) *total_ms = e->layer_ms[static_cast<size_t>(layer)];
     if (count) *count = e->layer_count[static_cast<size_t>(layer)];
+  });
+}
+
+kan_status kan_engine_set_option(kan_engine* e, int option, int64_t value) {
+  if (!e) return KAN_ERR_INVALID_ARGUMENT;
+  return guarded(e, [&] {
+    auto& o = e->opt;
+    const int v = static_cast<int>(value);
+    switch (option) {
+      case KAN_OPT_NO_CONV3: o.no_conv3 = value != 0; break;
+      case KAN_OPT_NO_IM2COL: o.no_im2col = value != 0; break;
+      case KAN_OPT_FORCE_BN: o.force_bn = v; break;
+      case KAN_OPT_TABLES:
+        if (v < -1 || v > 2) throw InvalidArgument("KAN_OPT_TABLES: -1, 0, 1 or 2");
+        o.tables = v;
+        break;
+      case KAN_OPT_EPI_STAGE: o.epi_stage = value != 0; break;
+      case KAN_OPT_CONV3_MC:
+        if (v < 1 || v > 2) throw InvalidArgument("KAN_OPT_CONV3_MC: 1 or 2");
+        o.conv3_mc = v;
+        break;
+      case KAN_OPT_LV_SIDECAR: o.lv_sidecar = value != 0; break;
+      case KAN_OPT_LEVEL_PREPASS_MIN:
+        o.level_prepass_min = value >= 0 ? value : std::numeric_limits<int64_t>::max();
+        break;
+      case KAN_OPT_ST_PREPASS: o.st_prepass = value != 0; break;
+      case KAN_OPT_ST_SLICES: o.st_slices = v; break;
+      case KAN_OPT_TIMELINE: o.timeline = value != 0; break;
+      case KAN_OPT_FORCE_NACC1: o.force_nacc1 = value != 0; break;
+      case KAN_OPT_RECORD_PLAN: o.record_plan = value != 0; break;
+      case KAN_OPT_DBG_FLAGS: o.dbg_flags = v; break;
+      default: throw InvalidArgument("unknown engine option " + std::to_string(option));
+    }
+  });
+}
+
+const char* kan_engine_last_plan(const kan_engine* e) { return e ? e->plan.c_str() : ""; }
+
+void kan_shard_rows(int64_t batch, int g, int n, int64_t* start, int64_t* stop) {
+  const int64_t per = n > 0 ? (batch + n - 1) / n : 0;
+  const int64_t s = std::min(batch, static_cast<int64_t>(g) * per);
+  if (start) *start = s;
+  if (stop) *stop = std::min(batch, s + per);
+}
+
+namespace {
+// bytes of one output row of a configured engine
+size_t out_row_bytes(kan_engine* e) {
+  const bool i8 = e->cfg.mode == KAN_MODE_BSPLINE_LUT && e->cfg.out_kind == KAN_OUT_I8;
+  return static_cast<size_t>(e->output_count()) * (i8 ? 1 : 4);
+}
+
+void check_shard_group(kan_engine* const* engines, int n, int64_t batch) {
+  if (!engines || n < 1) throw InvalidArgument("forward_sharded: no engines");
+  if (batch < 0) throw InvalidArgument("forward_sharded: negative batch");
+  kan_engine* e0 = engines[0];
+  for (int g = 0; g < n; ++g) {
+    kan_engine* e = engines[g];
+    if (!e) throw InvalidArgument("forward_sharded: null engine");
+    if (!e->configured) throw LogicError("forward_sharded: engine not configured");
+    if (e->input_size() != e0->input_size() || out_row_bytes(e) != out_row_bytes(e0) ||
+        e->cfg.mode != e0->cfg.mode)
+      throw ShapeMismatch("forward_sharded: engines must run the same model and configuration");
+    for (int h = 0; h < g; ++h)
+      if (engines[h] == e) throw InvalidArgument("forward_sharded: an engine appears twice (one handle per shard)");
+  }
+}
+
+// peer access from device `from` to device `to` (idempotent; absent P2P the
+// copy engine still moves the bytes through cudaMemcpyPeerAsync)
+void enable_peer(int from, int to) {
+  if (from == to) return;
+  int can = 0;
+  if (cudaDeviceCanAccessPeer(&can, from, to) != cudaSuccess || !can) return;
+  DeviceGuard dg(from);
+  const cudaError_t r = cudaDeviceEnablePeerAccess(to, 0);
+  if (r != cudaSuccess) cudaGetLastError();  // already enabled: clear the sticky-free error
+}
+}  // namespace
+
+kan_status kan_engine_forward_sharded(kan_engine* const* engines, int n_engines, const float* const* x_shards,
+                                      int64_t batch, void* out_dev0, void* const* streams) {
+  if (!engines || n_engines < 1 || !engines[0]) return KAN_ERR_INVALID_ARGUMENT;
+  kan_engine* e0 = engines[0];
+  return guarded(e0, [&] {
+    check_shard_group(engines, n_engines, batch);
+    if (batch > 0 && !out_dev0) throw InvalidArgument("forward_sharded: null output");
+    const size_t ob = out_row_bytes(e0);
+    const int dev0 = e0->device;
+    cudaStream_t st0 = streams ? static_cast<cudaStream_t>(streams[0]) : nullptr;
+    for (int g = 0; g < n_engines; ++g) {
+      kan_engine* e = engines[g];
+      int64_t r0 = 0, r1 = 0;
+      kan_shard_rows(batch, g, n_engines, &r0, &r1);
+      const int64_t rows = r1 - r0;
+      if (rows > 0 && (!x_shards || !x_shards[g])) throw InvalidArgument("forward_sharded: null input shard");
+      DeviceGuard dg(e->device);
+      cudaStream_t st = streams ? static_cast<cudaStream_t>(streams[g]) : nullptr;
+      uint8_t* dst = static_cast<uint8_t*>(out_dev0) + static_cast<size_t>(r0) * ob;
+      const bool in_place = e->device == dev0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
+      void* o = dst;
+      if (!in_place && rows > 0) {
+        e->shard_out.alloc(static_cast<size_t>(rows) * ob);
+        o = e->shard_out.p;
+      }
+      forward(e, rows > 0 ? x_shards[g] : nullptr, rows, o, st);
+      if (!in_place && rows > 0) {
+        if (e->device == dev0)
+          ck(cudaMemcpyAsync(dst, o, static_cast<size_t>(rows) * ob, cudaMemcpyDeviceToDevice, st), "shard copy");
+        else {
+          enable_peer(e->device, dev0);
+          ck(cudaMemcpyPeerAsync(dst, dev0, o, e->device, static_cast<size_t>(rows) * ob, st), "peer copy");
+        }
+      }
+      if (g > 0 || st != st0) {
+        ck(cudaEventRecord(e->done_event(), st), "event record");
+        DeviceGuard d0(dev0);
+        ck(cudaStreamWaitEvent(st0, e->shard_done, 0), "stream wait");
+      }
+    }
+  });
+}
+
+kan_status kan_engine_forward_sharded_host(kan_engine* const* engines, int n_engines, const float* x_host,
+                                           int64_t batch, void* out_host) {
+  if (!engines || n_engines < 1 || !engines[0]) return KAN_ERR_INVALID_ARGUMENT;
+  kan_engine* e0 = engines[0];
+  return guarded(e0, [&] {
+    check_shard_group(engines, n_engines, batch);
+    if (batch > 0 && (!x_host || !out_host)) throw InvalidArgument("forward_sharded_host: null buffer");
+    const size_t ob = out_row_bytes(e0);
+    const int64_t D = e0->input_size();
+    // enqueue every shard (H2D, forward, D2H on the engine's own stream), then wait
+    for (int g = 0; g < n_engines; ++g) {
+      kan_engine* e = engines[g];
+      int64_t r0 = 0, r1 = 0;
+      kan_shard_rows(batch, g, n_engines, &r0, &r1);
+      const int64_t rows = r1 - r0;
+      if (rows <= 0) continue;
+      DeviceGuard dg(e->device);
+      cudaStream_t st = e->stream_own();
+      e->io_in.alloc(static_cast<size_t>(rows * D) * 4);
+      e->io_out.alloc(static_cast<size_t>(rows) * ob);
+      ck(cudaMemcpyAsync(e->io_in.p, x_host + r0 * D, static_cast<size_t>(rows * D) * 4, cudaMemcpyHostToDevice, st),
+         "H2D");
+      forward(e, reinterpret_cast<const float*>(e->io_in.p), rows, e->io_out.p, st);
+      ck(cudaMemcpyAsync(static_cast<uint8_t*>(out_host) + static_cast<size_t>(r0) * ob, e->io_out.p,
+                         static_cast<size_t>(rows) * ob, cudaMemcpyDeviceToHost, st),
+         "D2H");
+    }
+    for (int g = 0; g < n_engines; ++g) {
+      kan_engine* e = engines[g];
+      if (!e->own_stream) continue;
+      DeviceGuard dg(e->device);
+      ck(cudaStreamSynchronize(e->own_stream), "stream sync");
+    }
   });
 }
 

@@ -55,22 +55,6 @@ __device__ __forceinline__ int lattice_level_f64(double y, double lo, double hi_
   return static_cast<int>(a);
 }
 
-// fp32 guess of the lattice level (exact after one threshold correction)
-__device__ __forceinline__ int level_guess(float x, float lo, float inv_step, float Lf) {
-  float t = (x - lo) * inv_step;
-  t = fminf(fmaxf(t, 0.0f), Lf);  // NaN -> 0 (fmaxf returns the non-NaN operand)
-  return __float2int_rn(t);
-}
-
-// Level of an fp32 activation against thr[n] = min{x : level(x) >= n}.
-__device__ __forceinline__ int lattice_level_f32(float x, const float* thr, float lo,
-                                                 float inv_step, int L) {
-  int g = level_guess(x, lo, inv_step, static_cast<float>(L));
-  g += (x >= thr[g + 1]) ? 1 : 0;
-  g -= (x < thr[g]) ? 1 : 0;
-  return g;
-}
-
 // float basis (bf16 path): local Cox-de Boor triangle in fp32 (grid.hpp:124-140
 // restricted to the P+1 supported functions), knot units.
 template <int PMAX>
@@ -581,7 +565,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     mbar_init(bar_tab, 1);
     mbar_fence_init();
   }
-  if (p.dbg_flags & 4)  // tuning only (no activation loads): a zero activation ring
+  if (KAN_DBG(p, 4))  // tuning only (no activation loads): a zero activation ring
     for (uint32_t q = threadIdx.x; q < static_cast<uint32_t>(SX) * x_bytes / 4; q += blockDim.x)
       reinterpret_cast<uint32_t*>(sX)[q] = 0u;
   if (warp == W_X && lane == 0) tma_prefetch(&xmap);
@@ -725,7 +709,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           mbar_wait(bar_xempty(rx.slot), rx.phase ^ 1);
           if (lane == 0) {
             const uint32_t dst = smem_u32(sX + static_cast<size_t>(rx.slot) * x_bytes);
-            if (p.dbg_flags & 4) {  // tuning only: no activation load (stale tile)
+            if (KAN_DBG(p, 4)) {  // tuning only: no activation load (stale tile)
               mbar_arrive(bar_xfull(rx.slot));
             } else {
             mbar_arrive_tx(bar_xfull(rx.slot), x_bytes);
@@ -777,7 +761,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     // Warp-uniform waits and operands, one elected lane issues (operands stay
     // in uniform registers: no per-MMA R2UR waterfall; it matters at small N).
     const uint32_t idesc = BF16 ? idesc_bf16(BN) : idesc_i8(BN, p.b_signed != 0);
-    const bool no_mma = (p.dbg_flags & 2) != 0;
+    const bool no_mma = KAN_DBG(p, 2) != 0;
     const uint32_t b_kstep = static_cast<uint32_t>(BN) * 8u;  // next 128-byte K block (x16 B)
     Ring ra(SA), rb(SB);
     int lt = 0;
@@ -1016,7 +1000,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const uint32_t tacc = t_row + static_cast<uint32_t>(ab) * BNa;
         const int row = tl.m0 + rloc;
         float rv[32];  // residual prefetch: 32 columns in flight per thread
-        const int ng = (p.dbg_flags & 8) ? 0 : ngroups;  // tuning only: skip the epilogue math
+        const int ng = KAN_DBG(p, 8) ? 0 : ngroups;  // tuning only: skip the epilogue math
         // 16 columns per TMEM load (BN is a multiple of 16); the two warps of
         // a lane quarter take alternate 16-column groups
         const int half = (warp - W_EPI) >> 2;
@@ -1028,7 +1012,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           if (p.epi == EPI_LEVEL && !p.f_on && (FE == 3) == (p.res_kind != 0) &&
               (FE == 2 || ((p.ld_res & 3) == 0 && (reinterpret_cast<uintptr_t>(p.res) & 15) == 0)) &&
               n0 + BN <= p.N && (p.ld_out & 7) == 0 &&
-              (reinterpret_cast<uintptr_t>(p.out) & 15) == 0 && !(p.dbg_flags & 8)) {
+              (reinterpret_cast<uintptr_t>(p.out) & 15) == 0 && !KAN_DBG(p, 8)) {
 #pragma unroll 1
             for (int g16 = half; g16 < ngroups / 4; g16 += 2) {
               float4 rv4[4] = {};
@@ -1083,7 +1067,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                             (p.ld_out & 3) == 0 && (reinterpret_cast<uintptr_t>(p.out) & 15) == 0 &&
                             (p.out_lv == nullptr ||
                              ((p.ld_lv & 7) == 0 && (reinterpret_cast<uintptr_t>(p.out_lv) & 15) == 0)) &&
-                            !(p.dbg_flags & 8);
+                            !KAN_DBG(p, 8);
           if (fast) {
             const float* thr = reinterpret_cast<const float*>(sT + p.off_thr);
 #pragma unroll 1
@@ -1380,20 +1364,10 @@ template <bool BF16, int NBP, int MODE, int FE = 0>
 static cudaError_t launch_impl(const CUtensorMap& xmap, const GemmParams& p, size_t smem,
                                cudaStream_t st) {
   auto kfn = kan_gather_gemm_kernel<BF16, NBP, MODE, FE>;
-  static size_t configured = 0;  // per instantiation: raise the smem limit once
-  if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-    configured = smem;
-  }
-  static int n_sm = 0;
-  if (n_sm == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-    if (n_sm <= 0) n_sm = 148;
-  }
+  static std::atomic<unsigned long long> optin{0};  // per instantiation, per device
+  (void)smem;
+  if (cudaError_t e = smem_optin(kfn, optin); e != cudaSuccess) return e;
+  const int n_sm = device_sm_count();
   const int tiles = p.n_tiles_n * p.m_tiles;
   cudaLaunchConfig_t cfg{};
   // splits == 1: persistent CTAs (one per SM) loop over the tiles
@@ -1492,8 +1466,10 @@ cudaError_t launch_gather_gemm(bool bf16, int nbp, int mode, const CUtensorMap& 
 
 // ---------------------------------------------------------------------------
 // Lattice levels of an fp32 tensor (parity probe for the quantized indices).
+// Runs lattice_level_tie, the function every hot-path producer uses, so the
+// threshold / +-inf / NaN edge cases of the parity tests exercise it directly.
 __global__ void kan_levels_kernel(const float* __restrict__ x, int64_t n,
-                                  const float* __restrict__ thr, float lo, float inv_step, int L,
+                                  const float* __restrict__ thr, float nlo_step, float inv_step, int L,
                                   uint16_t* __restrict__ out) {
   pdl_wait();
   pdl_trigger();
@@ -1502,16 +1478,16 @@ __global__ void kan_levels_kernel(const float* __restrict__ x, int64_t n,
   __syncthreads();
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    out[i] = static_cast<uint16_t>(lattice_level_f32(x[i], s_thr, lo, inv_step, L));
+    out[i] = static_cast<uint16_t>(lattice_level_tie(x[i], inv_step, nlo_step, L, s_thr));
 }
 
-cudaError_t launch_levels(const float* x, int64_t n, const float* thr, float lo, float inv_step,
+cudaError_t launch_levels(const float* x, int64_t n, const float* thr, float nlo_step, float inv_step,
                           int L, uint16_t* out, cudaStream_t st) {
   const int64_t nb = (n + 255) / 256;
   int blocks = static_cast<int>(nb < 148 * 8 ? nb : 148 * 8);
   if (blocks < 1) blocks = 1;
-  return launch_pdl(kan_levels_kernel, dim3(blocks), dim3(256), (L + 2) * sizeof(float), st, x, n, thr, lo,
-                    inv_step, L, out);
+  return launch_pdl(kan_levels_kernel, dim3(blocks), dim3(256), (L + 2) * sizeof(float), st, x, n, thr,
+                    nlo_step, inv_step, L, out);
 }
 
 // ---------------------------------------------------------------------------
@@ -1572,8 +1548,8 @@ __global__ void __launch_bounds__(256) kan_small_layer_kernel(const SmallParams 
           if (p.x_kind == X_U16)
             a = static_cast<const uint16_t*>(p.x)[row * p.ld_x + i];
           else
-            a = lattice_level_f32(static_cast<const float*>(p.x)[row * p.ld_x + i], thr, p.lo_f,
-                                  p.inv_step_f, p.L);
+            a = lattice_level_tie(static_cast<const float*>(p.x)[row * p.ld_x + i], p.inv_step_f,
+                                  p.lo_f, p.L, thr);
           const uint32_t v = vals[static_cast<uint32_t>(a) & mask];
           const uint32_t sft = 8u * static_cast<uint32_t>(a >> p.k);
           const unsigned long long* wrow = s_wq + i * N;
@@ -1631,18 +1607,13 @@ cudaError_t launch_small_layer(const SmallParams& p, cudaStream_t st) {
   constexpr int TPR = 8, THREADS = 256;
   const size_t smem = small_smem_bytes(p);
   const unsigned blocks = static_cast<unsigned>((static_cast<int64_t>(p.M) * TPR + THREADS - 1) / THREADS);
-  static size_t configured[3] = {0, 0, 0};  // per kernel variant (same function type)
-  auto go = [&](auto kfn) -> cudaError_t {
-    if (smem > configured[p.mode]) {
-      cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           static_cast<int>(smem));
-      if (e != cudaSuccess) return e;
-      configured[p.mode] = smem;
-    }
+  static std::atomic<unsigned long long> optin[2];  // per kernel variant, per device
+  auto go = [&](auto kfn, int v) -> cudaError_t {
+    if (cudaError_t e = smem_optin(kfn, optin[v]); e != cudaSuccess) return e;
     return launch_pdl(kfn, dim3(blocks), dim3(THREADS), smem, st, p);
   };
-  if (p.mode == MODE_SILU) return go(kan_small_layer_kernel<16, TPR, true>);
-  return go(kan_small_layer_kernel<16, TPR, false>);
+  if (p.mode == MODE_SILU) return go(kan_small_layer_kernel<16, TPR, true>, 1);
+  return go(kan_small_layer_kernel<16, TPR, false>, 0);
 }
 
 // ---------------------------------------------------------------------------

@@ -2,6 +2,15 @@
 #pragma once
 #include <cstdint>
 
+// Ablation switches (GemmParams::dbg_flags, KAN_OPT_DBG_FLAGS) are compiled
+// into the kernels only in a -DKAN_TUNING build; production kernels carry no
+// such branches.
+#ifdef KAN_TUNING
+#define KAN_DBG(p, bit) ((((p).dbg_flags) & (bit)) != 0)
+#else
+#define KAN_DBG(p, bit) false
+#endif
+
 namespace kan {
 
 enum EpiKind : int {

@@ -1,10 +1,49 @@
 // kan_ptx.cuh -- thin inline-PTX wrappers for sm_100a (mbarrier, TMA, bulk
 // copies, tcgen05 MMA/TMEM).  Written for this engine; no CUTLASS/CuTe.
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <cuda.h>
+#include <cuda_runtime.h>
 
 namespace kan {
+
+// Host: opt kernel `fn` into the current device's full dynamic shared memory,
+// once per (kernel, device).  cudaFuncSetAttribute acts on the current
+// device's context only, so the flag is a per-device bit; the attribute is the
+// device maximum less the kernel's static shared memory (never lowered), so concurrent callers cannot undercut each
+// other's launches.
+template <class K>
+inline cudaError_t smem_optin(K fn, std::atomic<unsigned long long>& done) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  int mx = 0;
+  e = cudaDeviceGetAttribute(&mx, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (e != cudaSuccess) return e;
+  cudaFuncAttributes fa{};
+  e = cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(fn));
+  if (e != cudaSuccess) return e;
+  const int dyn = mx - static_cast<int>(fa.sharedSizeBytes);  // static smem counts against the opt-in
+  e = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
+
+// Host: SM count of the current device (cached per device).
+inline int device_sm_count() {
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  int v = cache[dev & 63].load(std::memory_order_relaxed);
+  if (v <= 0) {
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+    cache[dev & 63].store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

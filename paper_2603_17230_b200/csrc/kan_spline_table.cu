@@ -649,16 +649,7 @@ static cudaError_t st_launch(void (*kfn)(KArgs...), dim3 grid, dim3 block, size_
   return cudaGetLastError();
 }
 
-static int st_sm_count() {
-  static int n_sm = 0;
-  if (n_sm == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-    if (n_sm <= 0) n_sm = 148;
-  }
-  return n_sm;
-}
+static int st_sm_count() { return device_sm_count(); }
 
 cudaError_t launch_st_sample(const double* basis, const double* coeffs, int n_in, int n_out, int nb, int Lv,
                              int pass, unsigned long long* mm, uint8_t* T, int Np, double s, double zd,
@@ -669,12 +660,12 @@ cudaError_t launch_st_sample(const double* basis, const double* coeffs, int n_in
   const dim3 grid(static_cast<unsigned>((n + 255) / 256));
   cudaError_t e;
   if (nb <= 16) {
-    e = cudaFuncSetAttribute(st_sample_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
+    static std::atomic<unsigned long long> optin{0};
+    if ((e = smem_optin(st_sample_kernel<16>, optin)) != cudaSuccess) return e;
     st_sample_kernel<16><<<grid, 256, smem, st>>>(basis, coeffs, n_in, n_out, nb, Lv, pass, mm, T, Np, s, zd, qhi);
   } else if (nb <= 32) {
-    e = cudaFuncSetAttribute(st_sample_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
+    static std::atomic<unsigned long long> optin{0};
+    if ((e = smem_optin(st_sample_kernel<32>, optin)) != cudaSuccess) return e;
     st_sample_kernel<32><<<grid, 256, smem, st>>>(basis, coeffs, n_in, n_out, nb, Lv, pass, mm, T, Np, s, zd, qhi);
   } else {
     return cudaErrorInvalidValue;  // the engine rejects G+P > 32 in spline-table mode
@@ -689,12 +680,8 @@ size_t st_layer_smem(const StParams& p) {
 template <int LPR, int KIND, bool FT>
 static cudaError_t launch_st_layer_t(const StParams& p, dim3 grid, size_t smem, cudaStream_t st) {
   auto kfn = kan_st_layer_kernel<LPR, KIND, FT>;
-  static size_t configured = 0;
-  if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-    configured = smem;
-  }
+  static std::atomic<unsigned long long> optin{0};  // per instantiation, per device
+  if (cudaError_t e = smem_optin(kfn, optin); e != cudaSuccess) return e;
   return st_launch(kfn, grid, dim3(256), smem, st, p);
 }
 

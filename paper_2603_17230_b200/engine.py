@@ -128,6 +128,18 @@ _lib.kan_lattice_thresholds.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double
 _lib.kan_lattice_thresholds.restype = C.c_int64
 _lib.kan_spline_thresholds.argtypes = [C.c_double, C.c_double, C.c_int, _vp, C.c_int64]
 _lib.kan_spline_thresholds.restype = C.c_int64
+_lib.kan_engine_set_option.argtypes = [_vp, C.c_int, C.c_int64]
+_lib.kan_engine_last_plan.argtypes = [_vp]
+_lib.kan_engine_last_plan.restype = C.c_char_p
+_lib.kan_engine_forward_sharded.argtypes = [_vp, C.c_int, _vp, C.c_int64, _vp, _vp]
+_lib.kan_engine_forward_sharded_host.argtypes = [_vp, C.c_int, _vp, C.c_int64, _vp]
+_lib.kan_shard_rows.argtypes = [C.c_int64, C.c_int, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+_lib.kan_shard_rows.restype = None
+
+# kan_option (include/kan_b200.h): tuning / debug switches, no environment reads
+OPTIONS = {"no_conv3": 1, "no_im2col": 2, "force_bn": 3, "tables": 4, "epi_stage": 5, "conv3_mc": 6,
+           "lv_sidecar": 7, "level_prepass_min": 8, "st_prepass": 9, "st_slices": 10, "timeline": 11,
+           "force_nacc1": 12, "record_plan": 13, "dbg_flags": 14}
 
 # exported symbols declared in include/kan_b200.h (checked by the CPU tests)
 EXPORTED = [
@@ -145,8 +157,57 @@ EXPORTED = [
     "kan_container_save", "kan_container_save_error", "kan_crc32", "kan_engine_load",
     "kan_engine_evaluate_accuracy", "kan_engine_set_activation_ranges",
     "kan_engine_linear_backward", "kan_softmax_cross_entropy", "kan_engine_conv_backward",
-    "kan_maxpool2_f32", "kan_maxpool2_backward_f32",
+    "kan_maxpool2_f32", "kan_maxpool2_backward_f32", "kan_engine_set_option", "kan_engine_last_plan",
+    "kan_engine_forward_sharded", "kan_engine_forward_sharded_host", "kan_shard_rows",
 ]
+
+
+def shard_rows(batch: int, g: int, n: int):
+    """[start, stop) rows of shard g of n (kan_shard_rows: contiguous, ceil(batch/n) each)."""
+    a, b = C.c_int64(), C.c_int64()
+    _lib.kan_shard_rows(batch, g, n, C.byref(a), C.byref(b))
+    return a.value, b.value
+
+
+def _group_error(engines, st):
+    msg = _lib.kan_engine_last_error(engines[0]._h).decode()
+    raise _STATUS.get(st, RuntimeError)(KanError(st, msg))
+
+
+def forward_sharded(engines, x_shards, out, streams=None):
+    """kan_engine_forward_sharded: engines[g] (one per device, or several on one)
+    runs rows shard_rows(batch, g, n) from x_shards[g] (a CUDA tensor on its
+    device); the logits land in `out` ([batch, output_count] on engines[0]'s
+    device).  Returns `out`; streams[0] (default: device 0's current stream)
+    waits for every shard."""
+    torch = _torch()
+    n = len(engines)
+    batch = out.shape[0]
+    hs = (_vp * n)(*[e._h for e in engines])
+    xs = (_vp * n)(*[(x.data_ptr() if x is not None and x.numel() else None) for x in x_shards])
+    if streams is None:
+        streams = [torch.cuda.current_stream(e.device) for e in engines]
+    ss = (_vp * n)(*[s.cuda_stream for s in streams])
+    st = _lib.kan_engine_forward_sharded(hs, n, xs, batch, out.data_ptr(), ss)
+    if st != KAN_OK:
+        _group_error(engines, st)
+    return out
+
+
+def forward_sharded_host(engines, x: np.ndarray, out: Optional[np.ndarray] = None) -> np.ndarray:
+    """kan_engine_forward_sharded_host: host rows in, host logits out; every
+    shard's H2D copy, forward and D2H copy runs on its engine's own stream."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    e0 = engines[0]
+    i8 = e0.opts is not None and e0.opts.out_kind == OUT_I8
+    if out is None:
+        out = np.empty((x.shape[0], e0.output_count), dtype=np.int8 if i8 else np.float32)
+    n = len(engines)
+    hs = (_vp * n)(*[e._h for e in engines])
+    st = _lib.kan_engine_forward_sharded_host(hs, n, x.ctypes.data, x.shape[0], out.ctypes.data)
+    if st != KAN_OK:
+        _group_error(engines, st)
+    return out
 
 
 def lattice_thresholds(G: int, P: int, k: int, lo: float = -1.0, hi: float = 1.0) -> np.ndarray:
@@ -515,11 +576,21 @@ class Engine:
     def last_launches(self) -> int:
         return _lib.kan_engine_last_launches(self._h)
 
+    def set_option(self, name: str, value: int):
+        """kan_engine_set_option: a tuning / debug switch (OPTIONS); takes effect at
+        the next configure (record_plan: at the next forward)."""
+        self._check(_lib.kan_engine_set_option(self._h, OPTIONS[name], int(value)))
+
+    @property
+    def last_plan(self) -> str:
+        """Launch plan of the last forward (needs set_option('record_plan', 1))."""
+        return _lib.kan_engine_last_plan(self._h).decode()
+
     def set_profiling(self, on: bool):
         self._check(_lib.kan_engine_set_profiling(self._h, int(bool(on))))
 
     def layer_timeline(self, layer: int) -> np.ndarray:
-        """[ctas, 8] %globaltimer stamps of the layer's last launch (KAN_TIMELINE=1)."""
+        """[ctas, 8] %globaltimer stamps of the layer's last launch (option timeline=1)."""
         n = _lib.kan_engine_layer_timeline(self._h, layer, None, 0)
         out = np.zeros(max(n, 0), dtype=np.uint64)
         if n > 0:

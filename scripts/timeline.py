@@ -1,12 +1,11 @@
-"""Per-CTA phase breakdown of each layer's gather-GEMM launch (KAN_TIMELINE=1).
+"""Per-CTA phase breakdown of each layer's gather-GEMM launch (engine option timeline=1).
 
-    KAN_TIMELINE=1 python scripts/timeline.py --config c2 [--split S] [--batch B]
+    python scripts/timeline.py --config c2 [--split S] [--batch B]
 """
 import argparse
 import os
 import sys
 
-os.environ.setdefault("KAN_TIMELINE", "1")
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
@@ -30,6 +29,7 @@ def main():
     B = a.batch or wl.batch
     Ws, Bs = wl.weights()
     e = Engine(wl.descriptor(), 0)
+    e.set_option("timeline", 1)
     for i, (w, b) in enumerate(zip(Ws, Bs)):
         e.set_coeffs(i, w, b)
     e.configure(EvalOptions(mode=a.mode or wl.mode, lut_k=wl.lut_k, lut_h=wl.lut_h,

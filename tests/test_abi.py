@@ -42,22 +42,35 @@ def test_engine_lut_builder_matches_oracle(oracle):
 
 
 def _emulate_device_level(x, thr, lo, inv_step, L):
-    """numpy float32 replica of kan_gemm.cu lattice_level_f32."""
+    """numpy replica of kan_gemm.cu lattice_level_tie, the level function of
+    every hot-path producer and of the kan_engine_layer_levels probe:
+    t = fmaf(x, 1/step, -lo/step) clamped to [0, L] (NaN -> 0), rint(t), and
+    within 2e-3 of a half-integer floor(t) + (x >= thr[floor(t) + 1]).  The
+    fp32 FMA is emulated in fp64 (the product of two fp32 values is exact
+    there) and rounded once to fp32."""
     x = x.astype(np.float32)
-    t = (x - np.float32(lo)) * np.float32(inv_step)
+    inv = np.float32(inv_step)
+    nlo = np.float32(-lo * inv_step)
+    with np.errstate(over="ignore", invalid="ignore"):
+        t = (x.astype(np.float64) * np.float64(inv) + np.float64(nlo)).astype(np.float32)
     t = np.where(np.isnan(t), np.float32(0), t)
     t = np.minimum(np.maximum(t, np.float32(0)), np.float32(L))
-    g = np.rint(t).astype(np.int64)
-    up = x >= thr[g + 1]
-    g = g + up
-    down = x < thr[g]
-    return (g - down).astype(np.uint16)
+    tr = np.rint(t)
+    g = tr.astype(np.int64)
+    tie = np.abs(np.abs(t - tr) - np.float32(0.5)) < np.float32(2e-3)
+    f = np.floor(t).astype(np.int64)
+    fi = np.minimum(f + 1, L + 1)
+    with np.errstate(invalid="ignore"):
+        up = x >= thr[fi]
+    g = np.where(tie, f + up, g)
+    return g.astype(np.uint16)
 
 
 @pytest.mark.parametrize("G,k", [(5, 8), (10, 8), (5, 4), (5, 3), (5, 2), (3, 1)])
 def test_threshold_level_rule_is_exact(oracle, G, k):
-    """The device's fp32 guess + threshold correction reproduces the reference
-    level for random values and for every threshold and its fp32 neighbours."""
+    """The device's level rule (fp32 FMA estimate, threshold test only near a
+    rounding tie) reproduces the reference level for random values, for every
+    threshold and its fp32 neighbours, and for +-0, +-1, +-inf, NaN, +-3e38."""
     from paper_2603_17230_b200 import lattice_thresholds
     thr = lattice_thresholds(G, 3, k)
     L = G << k

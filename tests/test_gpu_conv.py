@@ -33,10 +33,12 @@ def weights_for(desc, G=5, P=3, seed=0, std=0.05, silu=True):
     return wl.weights()
 
 
-def build(desc, Ws, Bs, **opts):
+def build(desc, Ws, Bs, engine_options=None, **opts):
     e = Engine(desc, 0)
     for i, (w, b) in enumerate(zip(Ws, Bs)):
         e.set_coeffs(i, w, b)
+    for k, v in (engine_options or {}).items():
+        e.set_option(k, v)
     e.configure(EvalOptions(**opts))
     return e
 
@@ -183,7 +185,7 @@ def test_conv3_kernel_bit_exact(oracle, C, H, W, co, silu, batch):
 def test_conv3_matches_general_kernel_in_a_residual_stage():
     """Stage-1 blocks at 32x32 take the ky-shared kernel (fp32-stored block
     inputs and level inputs); the result is bit-identical to the general
-    gather-GEMM kernel (KAN_NO_CONV3)."""
+    gather-GEMM kernel (option no_conv3)."""
     layers = configs.reskan18_layers(width=(16, 32), n_classes=10, in_ch=3)
     desc = {"name": "r", "grid": {"intervals": 5, "degree": 3}, "input": [3, 32, 32],
             "conv_output": "floor", "layers": layers}
@@ -191,11 +193,7 @@ def test_conv3_matches_general_kernel_in_a_residual_stage():
     x = np.random.default_rng(21).uniform(-1, 1, (20, 3 * 1024)).astype(np.float32)
     opts = dict(mode="bspline-lut", lut_k=8, lut_h=3, bits_w=8, w_scheme=W_PER_CHANNEL_SYM, silu_base=True)
     y3 = build(desc, Ws, Bs, **opts).model_forward(to_dev(x)).cpu().numpy()
-    os.environ["KAN_NO_CONV3"] = "1"
-    try:
-        yg = build(desc, Ws, Bs, **opts).model_forward(to_dev(x)).cpu().numpy()
-    finally:
-        del os.environ["KAN_NO_CONV3"]
+    yg = build(desc, Ws, Bs, engine_options={"no_conv3": 1}, **opts).model_forward(to_dev(x)).cpu().numpy()
     np.testing.assert_array_equal(y3, yg)
 
 
@@ -203,16 +201,12 @@ def test_conv3_matches_general_kernel_in_a_residual_stage():
 def test_stem_im2col_matches_implicit_conv(k, s, p):
     """Stem convs (model input, c_in < 16) run as a dense GEMM over an explicit
     level im2col; the result is bit-identical to the implicit-im2col conv
-    kernel over the transposed input (KAN_NO_IM2COL)."""
+    kernel over the transposed input (option no_im2col)."""
     desc = conv_desc(3, 16, 16, 32, k, s, p, floor=True)
     desc["layers"].append({"type": "conv", "c_in": 32, "c_out": 8, "kernel": 1, "stride": 1, "padding": 0})
     Ws, Bs = weights_for(desc, seed=k + s)
     x = np.random.default_rng(k * s).uniform(-1.05, 1.05, (5, 3 * 256)).astype(np.float32)
     opts = dict(mode="bspline-lut", lut_k=8, lut_h=8, bits_w=8, w_scheme=W_PER_CHANNEL_SYM, silu_base=True)
     yi = build(desc, Ws, Bs, **opts).model_forward(to_dev(x)).cpu().numpy()
-    os.environ["KAN_NO_IM2COL"] = "1"
-    try:
-        yc = build(desc, Ws, Bs, **opts).model_forward(to_dev(x)).cpu().numpy()
-    finally:
-        del os.environ["KAN_NO_IM2COL"]
+    yc = build(desc, Ws, Bs, engine_options={"no_im2col": 1}, **opts).model_forward(to_dev(x)).cpu().numpy()
     np.testing.assert_array_equal(yi, yc)

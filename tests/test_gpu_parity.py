@@ -39,10 +39,12 @@ def make_weights(dims, G, P=3, seed=0, std=0.1, silu=False):
     return Ws, Bs
 
 
-def build(dims, G, Ws, Bs, **opts):
+def build(dims, G, Ws, Bs, engine_options=None, **opts):
     e = Engine(mlp_desc(dims, G), 0)
     for i, (w, b) in enumerate(zip(Ws, Bs)):
         e.set_coeffs(i, w, b)
+    for k, v in (engine_options or {}).items():
+        e.set_option(k, v)
     e.configure(EvalOptions(**opts))
     return e
 
@@ -310,13 +312,9 @@ def test_level_prepass_matches_in_kernel_levels(oracle):
     x = np.random.default_rng(8).uniform(-1.1, 1.1, (1000, 300)).astype(np.float32)
     opts = dict(mode="bspline-lut", lut_k=8, lut_h=8, silu_base=True, split_k=1)
     y0 = build(dims, G, Ws, Bs, **opts).model_forward(to_dev(x)).cpu().numpy()
-    os.environ["KAN_LEVEL_PREPASS_MIN"] = "0"
-    try:
-        e = build(dims, G, Ws, Bs, **opts)
-        y1 = e.model_forward(to_dev(x)).cpu().numpy()
-        assert e.last_launches == 3  # prepass + layer 0 + small output layer
-    finally:
-        del os.environ["KAN_LEVEL_PREPASS_MIN"]
+    e = build(dims, G, Ws, Bs, engine_options={"level_prepass_min": 0}, **opts)
+    y1 = e.model_forward(to_dev(x)).cpu().numpy()
+    assert e.last_launches == 3  # prepass + layer 0 + small output layer
     np.testing.assert_array_equal(y0, y1)
     yo = oracle_int_model(oracle, G, 8, 8, W_PER_CHANNEL_SYM, 8, Ws, Bs, x)[-1]
     np.testing.assert_array_equal(y1, yo.astype(np.float32))
@@ -367,7 +365,7 @@ def test_fp32_output_epilogue_paths_bit_exact(oracle, dims, silu, split):
     epilogue staged through shared memory (kan_gemm.cu, FE instantiation),
     ragged ones (N = 300: a 256 + 44 column split) and split-K launches take
     finish4.  M = 333 leaves a partial row tile.  All are bit-exact with the
-    oracle and identical with the staging switched off (KAN_EPI_STAGE=0)."""
+    oracle and identical with the staging switched off (option epi_stage=0)."""
     G, M = 5, 333
     Ws, Bs = make_weights(dims, G, seed=11, silu=silu)
     x = np.random.default_rng(11).uniform(-1.05, 1.05, (M, dims[0])).astype(np.float32)
@@ -375,9 +373,5 @@ def test_fp32_output_epilogue_paths_bit_exact(oracle, dims, silu, split):
     y = build(dims, G, Ws, Bs, **opts).model_forward(to_dev(x)).cpu().numpy()
     yo = oracle_int_model(oracle, G, 8, 8, W_PER_CHANNEL_SYM, 8, Ws, Bs, x)[-1]
     np.testing.assert_array_equal(y, yo.astype(np.float32))
-    os.environ["KAN_EPI_STAGE"] = "0"
-    try:
-        y0 = build(dims, G, Ws, Bs, **opts).model_forward(to_dev(x)).cpu().numpy()
-    finally:
-        del os.environ["KAN_EPI_STAGE"]
+    y0 = build(dims, G, Ws, Bs, engine_options={"epi_stage": 0}, **opts).model_forward(to_dev(x)).cpu().numpy()
     np.testing.assert_array_equal(y0, y)
