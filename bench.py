@@ -54,6 +54,11 @@ PAPER_SAMPLES_PER_S = {  # PAPER.md:603, KANMLP2 G=5 8-bit LUT on R
 GRAPH_CHUNK = 1000  # forwards per captured graph (small configs)
 
 
+def per_config(table, key, default):
+    """A per-config default; sweep variants (c2k4, c1fp32, ...) inherit their base config's."""
+    return table.get(key, table.get(key[:2], default))
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -388,8 +393,8 @@ def main():
     B = r1 - r0  # this rank's shard (strong scaling)
     per = (wl.batch + world - 1) // world
 
-    n_streams = max(1, args.streams or STREAMS_DEFAULT.get(wl.key, 1))
-    opts = EvalOptions(**wl.eval_options(), split_k=args.split_k or SPLIT_DEFAULT.get(wl.key, 0))
+    n_streams = max(1, args.streams or per_config(STREAMS_DEFAULT, wl.key, 1))
+    opts = EvalOptions(**wl.eval_options(), split_k=args.split_k or per_config(SPLIT_DEFAULT, wl.key, 0))
     engines = build_engines(wl, local, n_streams, opts)
     eng = engines[0]
 

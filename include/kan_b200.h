@@ -243,7 +243,9 @@ typedef enum {
   KAN_OPT_TIMELINE = 11,          /* 1: per-CTA phase stamps (kan_engine_layer_timeline) */
   KAN_OPT_FORCE_NACC1 = 12,       /* 1: one TMEM accumulator (deeper A ring) */
   KAN_OPT_RECORD_PLAN = 13,       /* 1: record each forward's launch plan (kan_engine_last_plan) */
-  KAN_OPT_DBG_FLAGS = 14          /* ablation bits; honoured only by a -DKAN_TUNING build */
+  KAN_OPT_DBG_FLAGS = 14,         /* ablation bits; honoured only by a -DKAN_TUNING build */
+  KAN_OPT_NO_CONVW = 15,          /* 1: 3x3 s1 convs skip the window-shared kan_convw kernel */
+  KAN_OPT_CONVW_RINGS = 16        /* kan_convw ring depths SA*100 + SB*10 + SX (0 = automatic) */
 } kan_option;
 kan_status kan_engine_set_option(kan_engine* e, int option, int64_t value);
 /* The launch plan of the most recent forward when KAN_OPT_RECORD_PLAN is on:

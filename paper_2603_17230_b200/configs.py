@@ -233,6 +233,24 @@ WORKLOADS = {
     "c2": Workload("c2", "KAN MLP [784,64,10] G=5 P=3 batch 4096, LUT k8/h8 + int8 per-channel W, "
                          "SiLU base, hidden outputs requantized to the lattice, int8 logits",
                    [784, 64, 10], 5, 3, 4096, 0.1, int8_out=True),
+    # configs[0], the float accuracy baseline on the same model: fp32 Cox-de Boor
+    # basis + fp32 FFMA contraction (the paper's LUT-vs-recursion comparison,
+    # PAPER.md:603)
+    "c1fp32": Workload("c1fp32", "KAN MLP [784,64,10] G=5 P=3 batch 1024, fp32 Cox-de Boor path",
+                       [784, 64, 10], 5, 3, 1024, 0.1, mode="fp32"),
+    # configs[1] sweep points (sweep.hpp:112-119 enumerates the k/h cross
+    # product; "no GPU benefit below 8 bits")
+    "c2k4": Workload("c2k4", "KAN MLP [784,64,10] G=5 P=3 batch 4096, LUT k4/h4 + int8 per-channel W, "
+                             "SiLU base, int8 logits", [784, 64, 10], 5, 3, 4096, 0.1, lut_k=4, lut_h=4,
+                     int8_out=True),
+    "c2k3": Workload("c2k3", "KAN MLP [784,64,10] G=5 P=3 batch 4096, LUT k3/h3 + int8 per-channel W, "
+                             "SiLU base, int8 logits", [784, 64, 10], 5, 3, 4096, 0.1, lut_k=3, lut_h=3,
+                     int8_out=True),
+    "c2k2": Workload("c2k2", "KAN MLP [784,64,10] G=5 P=3 batch 4096, LUT k2/h2 + int8 per-channel W, "
+                             "SiLU base, int8 logits", [784, 64, 10], 5, 3, 4096, 0.1, lut_k=2, lut_h=2,
+                     int8_out=True),
+    "c2w4": Workload("c2w4", "KAN MLP [784,64,10] G=5 P=3 batch 4096, LUT k8/h8 + int4 per-channel W, "
+                             "SiLU base, int8 logits", [784, 64, 10], 5, 3, 4096, 0.1, bits_w=4, int8_out=True),
     # configs[2]
     "c3": Workload("c3", "Wide KAN MLP [3072,1024,1024,10] G=10 P=3 batch 65536, LUT k8/h8 + int8 W",
                    [3072, 1024, 1024, 10], 10, 3, 65536, 0.05),

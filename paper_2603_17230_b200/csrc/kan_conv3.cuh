@@ -279,9 +279,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           if (p.x_kind == X_F32) {
             uint32_t xr[H];
             load_x<4 * H>(xt, rr, xoff, x_row_bytes, xr);
+            levels8_f32<H>([&](int e) { return __uint_as_float(xr[e]); }, p.inv_step_f, p.lo_f, p.L, thr, a);
+            if (pad)
 #pragma unroll
-            for (int e = 0; e < H; ++e)
-              a[e] = pad ? p.lvl0 : lattice_level_tie(__uint_as_float(xr[e]), p.inv_step_f, p.lo_f, p.L, thr);
+              for (int e = 0; e < H; ++e) a[e] = p.lvl0;
           } else {
             uint32_t xr[H / 2];
             load_x<2 * H>(xt, rr, xoff, x_row_bytes, xr);
@@ -387,9 +388,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               if (p.out_lv) {
                 uint32_t w[8];
 #pragma unroll
-                for (int q = 0; q < 8; ++q)
-                  w[q] = static_cast<uint32_t>(lattice_level_tie(f[2 * q], p.inv_step_f, p.lo_f, p.L, thr)) |
-                         (static_cast<uint32_t>(lattice_level_tie(f[2 * q + 1], p.inv_step_f, p.lo_f, p.L, thr)) << 16);
+                for (int hh = 0; hh < 2; ++hh) {
+                  int lv[8];
+                  levels8_f32([&](int e8) { return f[8 * hh + e8]; }, p.inv_step_f, p.lo_f, p.L, thr, lv);
+#pragma unroll
+                  for (int q = 0; q < 4; ++q)
+                    w[4 * hh + q] = static_cast<uint32_t>(lv[2 * q]) | (static_cast<uint32_t>(lv[2 * q + 1]) << 16);
+                }
                 uint4* ol = reinterpret_cast<uint4*>(p.out_lv + static_cast<size_t>(row) * p.ld_lv + n0 + cl);
                 ol[0] = make_uint4(w[0], w[1], w[2], w[3]);
                 ol[1] = make_uint4(w[4], w[5], w[6], w[7]);
@@ -436,15 +441,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           if (row < p.M && cl < BN) {
             uint32_t w[8];
 #pragma unroll
-            for (int e = 0; e < 16; e += 2) {
-              const double y0 =
-                  __dmul_rn(__dsub_rn(static_cast<double>(static_cast<int32_t>(r16[e])), s_cols[BN + cl + e]), s_cols[cl + e]);
-              const double y1 = __dmul_rn(
-                  __dsub_rn(static_cast<double>(static_cast<int32_t>(r16[e + 1])), s_cols[BN + cl + e + 1]), s_cols[cl + e + 1]);
-              const uint32_t a0 = static_cast<uint32_t>(lattice_level_fast(y0, p.n_lo, p.n_hi_open, p.n_step, p.n_inv_step, p.n_L));
-              const uint32_t a1 = static_cast<uint32_t>(lattice_level_fast(y1, p.n_lo, p.n_hi_open, p.n_step, p.n_inv_step, p.n_L));
-              w[e >> 1] = a0 | (a1 << 16);
-            }
+            for (int hh = 0; hh < 2; ++hh)
+              levels8_f64(
+                  [&](int e8) {
+                    const int e = 8 * hh + e8;
+                    return __dmul_rn(__dsub_rn(static_cast<double>(static_cast<int32_t>(r16[e])), s_cols[BN + cl + e]),
+                                     s_cols[cl + e]);
+                  },
+                  p.n_lo, p.n_hi_open, p.n_step, p.n_inv_step, p.n_L, w + 4 * hh);
             uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(p.out) + static_cast<size_t>(row) * p.ld_out +
                                                 tl.n_tile * BN + cl);
             o[0] = make_uint4(w[0], w[1], w[2], w[3]);

@@ -23,21 +23,28 @@
 // Tile: 8 images x TR output rows x W columns (W = 16 or 32); NACC = TR*W/16
 // accumulators of 128 rows x BN columns, double-buffered in TMEM
 // (NACC * BN <= 256).  K: C_in / 4 blocks of 32 bytes (4 channels x NBP = 8
-// basis bytes); an activation load (8 channels, u16 levels) feeds two blocks.
+// basis bytes); an activation load (8 channels, u16 levels) feeds two blocks,
+// expanded one per producer step so the A ring runs SA - 1 blocks ahead.
 // MODE_ZP (the reference's per-tensor asymmetric weights): the producers sum
 // each window row's codes over all channels (wsum), and the epilogue forms
 // each output row's code sum from the 9 window rows it read.
 //
-// Warp roles as in kan_gather_gemm_kernel: 16 producers, activation TMA, MMA
-// issuer, weight loader, 8 epilogue warps (two per TMEM lane quarter).
+// Warp roles as in kan_gather_gemm_kernel (12 producers here), activation TMA,
+// MMA issuer, weight loader, 8 epilogue warps (two per TMEM lane quarter).
+
+// 12 producer warps (the window expansion is cheap here), so the epilogue's
+// 16-column fp64 chains get more registers than the 27-warp gather kernel's
+constexpr int CONVW_PRODUCER_WARPS = 12;
+constexpr int CONVW_THREADS = 32 * (CONVW_PRODUCER_WARPS + 3 + GEMM_EPI_WARPS);
+constexpr int CONVW_MAX_ROWS = 3 * 32 * CONVW_PRODUCER_WARPS;  // window rows: RPT rows per producer thread
 
 template <int MODE>
-__global__ void __launch_bounds__(GEMM_THREADS, 1)
+__global__ void __launch_bounds__(CONVW_THREADS, 1)
     kan_convw_kernel(const __grid_constant__ CUtensorMap xmap, const GemmParams p) {
-  constexpr int NPW = GEMM_PRODUCER_WARPS, NP = 32 * NPW;
+  constexpr int NPW = CONVW_PRODUCER_WARPS, NP = 32 * NPW;
   constexpr int W_X = NPW, W_MMA = NPW + 1, W_B = NPW + 2, W_EPI = NPW + 3;
   constexpr bool ZP = (MODE == MODE_ZP);
-  constexpr int RPT = 4;  // window rows per producer thread (max): WR <= RPT * NP
+  constexpr int RPT = CONVW_MAX_ROWS / NP;  // window rows per producer thread (max)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
 
@@ -163,7 +170,19 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   } else if (warp == W_MMA) {
     // ============ MMA issuer: 9 taps x NACC accumulators per K block ============
     const uint32_t idesc = idesc_i8(BN, p.b_signed != 0);
-    const uint32_t tap_b = static_cast<uint32_t>(BN) * 32u;  // bytes of one tap's weight tile
+    // descriptor start addresses advance in 16-byte units: one window row
+    // (32 B) is 2 units.  Row offsets of each accumulator's first pixel and of
+    // each tap, computed once (no divisions in the issue loop: at N = 64 a
+    // K block is 36 MMAs of ~34 tensor cycles each, so the loop must be short)
+    uint32_t acc_row[8], tap_row[9];
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+      const int py = (a * 16) / W, px = a * 16 - py * W;
+      acc_row[a] = static_cast<uint32_t>((py * WP + px) * 8 * 2);
+    }
+#pragma unroll
+    for (int tap = 0; tap < 9; ++tap) tap_row[tap] = static_cast<uint32_t>(((tap / 3) * WP + tap % 3) * 8 * 2);
+    const uint64_t b_tap = static_cast<uint64_t>(BN) * 2u;  // one tap's weight tile (BN x 32 B) in 16-byte units
     Ring ra(SA), rb(SB);
     int lt = 0;
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++lt) {
@@ -175,19 +194,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         mbar_wait_warp(bar_afull(ra.slot), ra.phase);
         mbar_wait_warp(bar_bfull(rb.slot), rb.phase);
         tc_fence_after();
-        const uint32_t a_addr = smem_u32(sA + static_cast<size_t>(ra.slot) * a_bytes);
-        const uint32_t b_addr = smem_u32(sB + static_cast<size_t>(rb.slot) * b_slot);
+        const uint64_t ad0 = umma_desc_sw32(smem_u32(sA + static_cast<size_t>(ra.slot) * a_bytes));
+        const uint64_t bd0 = umma_desc_sw32(smem_u32(sB + static_cast<size_t>(rb.slot) * b_slot));
         if (elect_one()) {
+#pragma unroll
           for (int tap = 0; tap < 9; ++tap) {
-            const int ky = tap / 3, kx = tap - 3 * (tap / 3);
-            const uint64_t bd = umma_desc_sw32(b_addr + static_cast<uint32_t>(tap) * tap_b);
-            for (int a = 0; a < NACC; ++a) {
-              // first output pixel of accumulator a: row a*16/W of the band, column (a*16) % W
-              const int py = (a * 16) / W, px = a * 16 - py * W;
-              const uint32_t wrow = static_cast<uint32_t>(((py + ky) * WP + px + kx) * 8);
-              mma_i8(dacc + static_cast<uint32_t>(a * BN), umma_desc_sw32(a_addr + wrow * 32u), bd, idesc,
-                     (kb | tap) != 0 ? 1u : 0u);
-            }
+            const uint64_t bd = bd0 + static_cast<uint64_t>(tap) * b_tap;
+            const uint32_t acc = (kb | tap) != 0 ? 1u : 0u;
+#pragma unroll
+            for (int a = 0; a < 8; ++a)
+              if (a < NACC && !KAN_DBG(p, 2))  // (tuning only: flag 2 skips the MMAs)
+                mma_i8(dacc + static_cast<uint32_t>(a * BN), ad0 + (acc_row[a] + tap_row[tap]), bd, idesc, acc);
           }
           tc_commit(bar_aempty(ra.slot));
           tc_commit(bar_bempty(rb.slot));
@@ -218,50 +235,42 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         pad[q] = static_cast<unsigned>(iy) >= static_cast<unsigned>(H) || static_cast<unsigned>(ix) >= static_cast<unsigned>(W);
         rs[q] = 0u;
       }
-      for (int kp = 0; kp < n_kb / 2; ++kp, rx.next()) {
-        mbar_wait(bar_xfull(rx.slot), rx.phase);
-        const uint8_t* xt = sX + static_cast<size_t>(rx.slot) * x_bytes;
-        // the pair of A slots this load fills (K blocks 2kp, 2kp+1)
-        Ring ra1 = ra;
-        ra1.next();
+      for (int kb = 0; kb < n_kb; ++kb, ra.next()) {
+        // one K block (4 channels) per step; an activation load covers two
+        const int xh = kb & 1;
+        if (xh == 0) mbar_wait(bar_xfull(rx.slot), rx.phase);
         mbar_wait(bar_aempty(ra.slot), ra.phase ^ 1);
-        mbar_wait(bar_aempty(ra1.slot), ra1.phase ^ 1);
-        uint8_t* at0 = sA + static_cast<size_t>(ra.slot) * a_bytes;
-        uint8_t* at1 = sA + static_cast<size_t>(ra1.slot) * a_bytes;
+        const uint8_t* xt = sX + static_cast<size_t>(rx.slot) * x_bytes + xh * 8;
+        uint8_t* at = sA + static_cast<size_t>(ra.slot) * a_bytes;
 #pragma unroll
         for (int q = 0; q < RPT; ++q) {
           const int r = tid + q * NP;
           if (r < WR) {
-            const uint4 lv = *reinterpret_cast<const uint4*>(xt + static_cast<size_t>(r) * 16);
-            const uint32_t lw[4] = {lv.x, lv.y, lv.z, lv.w};
-            uint32_t w[16];
+            const uint2 lv = *reinterpret_cast<const uint2*>(xt + static_cast<size_t>(r) * 16);
+            const uint32_t lw[2] = {lv.x, lv.y};
+            uint32_t w[8];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
+            for (int e = 0; e < 4; ++e) {
               const uint32_t a = pad[q] ? static_cast<uint32_t>(p.lvl0) : ((lw[e >> 1] >> (16 * (e & 1))) & 0xFFFFu);
-              const uint2 c = c64[a];
+              const uint2 c = c64[KAN_DBG(p, 64) ? lane : a];  // (tuning only: flag 64 = conflict-free fake lookups)
               w[2 * e] = c.x;
               w[2 * e + 1] = c.y;
               if constexpr (ZP) rs[q] = __dp4a(c.y, 0x01010101u, __dp4a(c.x, 0x01010101u, rs[q]));
             }
-            // row r of the two SW32 K-major windows: 16-byte chunk c at c ^ row bit 2
+            // row r of the SW32 K-major window: 16-byte chunk c at c ^ row bit 2
             const uint32_t sw = (static_cast<uint32_t>(r) >> 2) & 1u;
-            uint8_t* d0 = at0 + static_cast<size_t>(r) * 32;
-            uint8_t* d1 = at1 + static_cast<size_t>(r) * 32;
-            *reinterpret_cast<uint4*>(d0 + (sw << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
-            *reinterpret_cast<uint4*>(d0 + ((sw ^ 1u) << 4)) = make_uint4(w[4], w[5], w[6], w[7]);
-            *reinterpret_cast<uint4*>(d1 + (sw << 4)) = make_uint4(w[8], w[9], w[10], w[11]);
-            *reinterpret_cast<uint4*>(d1 + ((sw ^ 1u) << 4)) = make_uint4(w[12], w[13], w[14], w[15]);
+            uint8_t* d = at + static_cast<size_t>(r) * 32;
+            *reinterpret_cast<uint4*>(d + (sw << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+            *reinterpret_cast<uint4*>(d + ((sw ^ 1u) << 4)) = make_uint4(w[4], w[5], w[6], w[7]);
           }
         }
         fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
         __syncwarp();
         if (lane == 0) {
-          mbar_arrive(bar_xempty(rx.slot));
+          if (xh == 1) mbar_arrive(bar_xempty(rx.slot));
           mbar_arrive(bar_afull(ra.slot));
-          mbar_arrive(bar_afull(ra1.slot));
         }
-        ra.next();
-        ra.next();
+        if (xh == 1) rx.next();
       }
       if constexpr (ZP) {
         // the window rows' code sums for the epilogue's zero-point term
@@ -299,45 +308,42 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
       mbar_wait(bar_accfull(ab), (lt >> 1) & 1);
       tc_fence_after();
-      int32_t rsum[8];  // ZP: each accumulator row's code sum (up to 8 accumulators)
-      if constexpr (ZP) {
-        const int wb = lt & 1;
-        mbar_wait(bar_wsfull(wb), (lt >> 1) & 1);
-        const int32_t* ws = s_wsum + wb * WR;
-#pragma unroll
-        for (int a = 0; a < 8; ++a) {
-          rsum[a] = 0;
-          if (a < NACC) {
-            const int pix = a * 16 + pl_;
-            const int py = pix / W, px = pix - py * W;
-            int s = 0;
-#pragma unroll
-            for (int tap = 0; tap < 9; ++tap)
-              s += ws[(((py + tap / 3) * WP + px + tap % 3) << 3) + img_l];
-            rsum[a] = s;
-          }
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(bar_wsempty(wb));
-      }
+      const int32_t* ws = s_wsum + (lt & 1) * WR;
+      if constexpr (ZP) mbar_wait(bar_wsfull(lt & 1), (lt >> 1) & 1);
       const int img = tl.g * 8 + img_l;
       const bool valid = img < p.M;
       const int n0 = tl.nt * BN;
 #pragma unroll 1
       for (int a = 0; a < NACC; ++a) {
         const int pix = a * 16 + pl_;
-        const int oy = tl.oy0 + pix / W, ox = pix % W;
-        const size_t orow = (static_cast<size_t>(img) * H + oy) * W + ox;  // NHWC row
+        const int py = pix / W, px = pix - py * W;
+        const int oy = tl.oy0 + py;
+        const size_t orow = (static_cast<size_t>(img) * H + oy) * W + px;  // NHWC row
         long long zc = 0;
         if constexpr (ZP) {
+          // the row's code sum: the 9 window rows its taps read (zero-point term)
+          int s_ = 0;
 #pragma unroll
-          for (int q = 0; q < 8; ++q)
-            if (q == a) zc = p.z_w * static_cast<long long>(rsum[q]);
+          for (int tap = 0; tap < 9; ++tap) s_ += ws[(((py + tap / 3) * WP + px + tap % 3) << 3) + img_l];
+          zc = p.z_w * static_cast<long long>(s_);
         }
         const uint32_t tacc = t_row + static_cast<uint32_t>(ab) * 256u + static_cast<uint32_t>(a * BN);
 #pragma unroll 1
-        for (int cl = half * 16; cl < BN; cl += 32) {
+        for (int cl = half * 16; cl < (KAN_DBG(p, 8) ? 0 : BN); cl += 32) {  // (tuning: flag 8 skips the epilogue)
           const bool full = n0 + cl + 16 <= p.N;
+          if (p.res_kind && valid) {
+            // pull the NEXT group's residual segment into L1 while this one is processed
+            size_t nrow = orow;
+            int ncl = cl + 32;
+            if (ncl >= BN && a + 1 < NACC) {
+              const int npix = (a + 1) * 16 + pl_;
+              const int npy = npix / W;
+              nrow = (static_cast<size_t>(img) * H + tl.oy0 + npy) * W + (npix - npy * W);
+              ncl = half * 16;
+            }
+            if (ncl < BN && n0 + ncl < p.N)
+              asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const float*>(p.res) + nrow * p.ld_res + n0 + ncl));
+          }
           float4 rv4[4] = {};
           if (p.res_kind && valid && full) {
             const float4* rp =
@@ -349,54 +355,59 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           tmem_ld16(tacc + cl, r16);
           tmem_wait_ld();
           if (!valid) continue;
-          double y[16];
-#pragma unroll
-          for (int e = 0; e < 16; ++e) {
+          // y = (acc - z_w * rowsum) * f (ZP) or acc * fs[j]; + residual (fp64)
+          auto yval = [&](int e) -> double {
+            double y;
             if constexpr (ZP)
-              y[e] = __dmul_rn(static_cast<double>(static_cast<long long>(static_cast<int32_t>(r16[e])) - zc), p.f_tensor);
+              y = __dmul_rn(static_cast<double>(static_cast<long long>(static_cast<int32_t>(r16[e])) - zc), p.f_tensor);
             else
-              y[e] = __dmul_rn(static_cast<double>(static_cast<int32_t>(r16[e])), s_cols[cl + e]);
-          }
+              y = __dmul_rn(static_cast<double>(static_cast<int32_t>(r16[e])), s_cols[cl + e]);
+            if (p.res_kind) y = __dadd_rn(y, static_cast<double>((&rv4[e >> 2].x)[e & 3]));
+            return y;
+          };
           if (full) {
-            if (p.res_kind) {
-#pragma unroll
-              for (int e = 0; e < 16; ++e) y[e] = __dadd_rn(y[e], static_cast<double>((&rv4[e >> 2].x)[e & 3]));
-            }
             if (p.epi == EPI_LEVEL) {
+              // branch-free level estimates 8 at a time, then the (rare) tie fix-ups
               uint32_t w[8];
 #pragma unroll
-              for (int e = 0; e < 16; e += 2) {
-                const uint32_t a0 = static_cast<uint32_t>(lattice_level_fast(y[e], p.n_lo, p.n_hi_open, p.n_step, p.n_inv_step, p.n_L));
-                const uint32_t a1 = static_cast<uint32_t>(lattice_level_fast(y[e + 1], p.n_lo, p.n_hi_open, p.n_step, p.n_inv_step, p.n_L));
-                w[e >> 1] = a0 | (a1 << 16);
-              }
+              for (int hh = 0; hh < 2; ++hh)
+                levels8_f64([&](int e8) { return yval(8 * hh + e8); }, p.n_lo, p.n_hi_open, p.n_step, p.n_inv_step,
+                            p.n_L, w + 4 * hh);
               uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(p.out) + orow * p.ld_out + n0 + cl);
               o[0] = make_uint4(w[0], w[1], w[2], w[3]);
               o[1] = make_uint4(w[4], w[5], w[6], w[7]);
             } else {  // EPI_F32 row-major (+ levels sidecar)
               float f[16];
 #pragma unroll
-              for (int e = 0; e < 16; ++e) f[e] = __double2float_rn(y[e]);
+              for (int e = 0; e < 16; ++e) f[e] = __double2float_rn(yval(e));
               float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) + orow * p.ld_out + n0 + cl);
 #pragma unroll
               for (int q = 0; q < 4; ++q) o[q] = make_float4(f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]);
               if (p.out_lv) {
                 uint32_t w[8];
 #pragma unroll
-                for (int q = 0; q < 8; ++q)
-                  w[q] = static_cast<uint32_t>(lattice_level_tie(f[2 * q], p.inv_step_f, p.lo_f, p.L, thr)) |
-                         (static_cast<uint32_t>(lattice_level_tie(f[2 * q + 1], p.inv_step_f, p.lo_f, p.L, thr)) << 16);
+                for (int hh = 0; hh < 2; ++hh) {
+                  int lv[8];
+                  levels8_f32([&](int e8) { return f[8 * hh + e8]; }, p.inv_step_f, p.lo_f, p.L, thr, lv);
+#pragma unroll
+                  for (int q = 0; q < 4; ++q)
+                    w[4 * hh + q] = static_cast<uint32_t>(lv[2 * q]) | (static_cast<uint32_t>(lv[2 * q + 1]) << 16);
+                }
                 uint4* ol = reinterpret_cast<uint4*>(p.out_lv + orow * p.ld_lv + n0 + cl);
                 ol[0] = make_uint4(w[0], w[1], w[2], w[3]);
                 ol[1] = make_uint4(w[4], w[5], w[6], w[7]);
               }
             }
           } else {
-            // ragged last column group: element-wise
+            // ragged last column group: element-wise (the residual read here)
             for (int e = 0; e < 16; ++e) {
               const int j = n0 + cl + e;
               if (j >= p.N) break;
-              double v = y[e];
+              double v;
+              if constexpr (ZP)
+                v = __dmul_rn(static_cast<double>(static_cast<long long>(static_cast<int32_t>(r16[e])) - zc), p.f_tensor);
+              else
+                v = __dmul_rn(static_cast<double>(static_cast<int32_t>(r16[e])), s_cols[cl + e]);
               if (p.res_kind) v = __dadd_rn(v, static_cast<double>(reinterpret_cast<const float*>(p.res)[orow * p.ld_res + j]));
               if (p.epi == EPI_LEVEL) {
                 reinterpret_cast<uint16_t*>(p.out)[orow * p.ld_out + j] =
@@ -410,6 +421,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             }
           }
         }
+      }
+      if constexpr (ZP) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_wsempty(lt & 1));
       }
       tc_fence_before();
       __syncwarp();
@@ -440,7 +455,7 @@ cudaError_t launch_convw(int mode, const CUtensorMap& xmap, const GemmParams& p,
     const int tiles = (p.M + 7) / 8 * (p.H / p.bh) * p.n_tiles_n;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(tiles < n_sm ? tiles : n_sm));
-    cfg.blockDim = dim3(GEMM_THREADS);
+    cfg.blockDim = dim3(CONVW_THREADS);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];

@@ -52,6 +52,8 @@ cudaError_t launch_rows_to_levels(const float* x, int64_t M, int n, int ld_x, ui
                                   const float* thr, float nlo_step, float inv_step, int L, cudaStream_t st);
 cudaError_t launch_conv3(int mode, const CUtensorMap& xmap, const GemmParams& p, size_t smem, cudaStream_t st);
 size_t conv3_smem_bytes(int BN, int R, int SA, int SB, int SX, int x_kind, int tab_bytes, bool silu);
+cudaError_t launch_convw(int mode, const CUtensorMap& xmap, const GemmParams& p, size_t smem, cudaStream_t st);
+size_t convw_smem_bytes(int BN, int WR, int SA, int SB, int SX, int tab_bytes, bool zp);
 size_t small_smem_bytes(const SmallParams& p);
 cudaError_t launch_im2col_levels(const float* x, int64_t n_img, int C, int H, int W, int K, int stride, int pad,
                                  int Ho, int Wo, uint16_t* out, int ld_o, const float* thr, float nlo_step,
@@ -217,6 +219,11 @@ struct PreparedLayer {
   bool conv3 = false;
   int b_slot3 = 0;
   DevBuf<uint8_t> wt3;
+  // window-shared 3x3 conv kernel (kan_convw.cuh): weights as
+  // [n_tile][K block of 4 channels][9 taps][BNw rows][32 B] (SW32 K-major)
+  bool convw = false;
+  int bnw = 0, trw = 0, ntw = 0, b_slotw = 0;
+  DevBuf<uint8_t> wtw;
   int IPS = 0, GS = 0, n_spline_stages = 0, n_groups = 0, total_stages = 0, silu = 0;
   DevBuf<uint8_t> wt;       // tcgen05 paths: pre-tiled weights
   DevBuf<float> w32, wb32;  // fp32 path
@@ -352,6 +359,8 @@ struct kan_engine {
   // tuning / debug switches (kan_engine_set_option); configure copies them
   // into the fields above, so nothing is read from the environment
   struct Options {
+    bool no_convw = false;
+    int convw_rings = 0;
     bool no_conv3 = false, no_im2col = false, epi_stage = true, lv_sidecar = true, st_prepass = true;
     bool timeline = false, force_nacc1 = false, record_plan = false;
     int force_bn = 0, tables = -1, conv3_mc = 2, st_slices = 0, dbg_flags = 0;
@@ -899,6 +908,47 @@ void prepare_gemm_layer(kan_engine* e, const Layer& l, PreparedLayer& pl, bool b
               }
             }
       pl.wt3.upload(w3);
+    }
+  }
+
+  // window-shared 3x3 stride-1 pad-1 conv kernel (kan_convw.cuh): no SiLU
+  // term, 16- or 32-pixel-wide maps, whole 8-channel activation loads
+  pl.convw = false;
+  if (!bf16 && l.type == L_CONV && !l.im2col && l.kernel == 3 && l.stride == 1 && l.padding == 1 && nbp == 8 &&
+      !pl.silu && !e->opt.no_convw && l.c_in % 8 == 0 && (l.out.w == 16 || l.out.w == 32) && l.out.h == l.in.h &&
+      l.out.w == l.in.w) {
+    const int W = l.out.w;
+    const int bnw = N <= 256 ? (N + 15) / 16 * 16 : 256;
+    const int per_row = W / 16;  // accumulators per output row
+    int tr = 1;
+    while (2 * tr * per_row * bnw <= 256 && l.out.h % (2 * tr) == 0 && (2 * tr + 2) * (W + 2) * 8 <= 1152) tr *= 2;
+    if (tr * per_row * bnw <= 256 && l.out.h % tr == 0 && (tr + 2) * (W + 2) * 8 <= 1152) {  // CONVW_MAX_ROWS
+      pl.convw = true;
+      pl.bnw = bnw;
+      pl.trw = tr;
+      pl.ntw = (N + bnw - 1) / bnw;
+      pl.b_slotw = 9 * bnw * 32;
+      const int n_kb = l.c_in / 4;
+      std::vector<uint8_t> ww(static_cast<size_t>(pl.ntw) * n_kb * pl.b_slotw, 0);
+      for (int nt = 0; nt < pl.ntw; ++nt)
+        for (int kb = 0; kb < n_kb; ++kb)
+          for (int t = 0; t < 9; ++t) {
+            uint8_t* tile = ww.data() + (static_cast<size_t>(nt) * n_kb + kb) * pl.b_slotw + static_cast<size_t>(t) * bnw * 32;
+            for (int n = 0; n < bnw; ++n) {
+              const int j = nt * bnw + n;
+              if (j >= N) continue;
+              for (int kbyte = 0; kbyte < 32; ++kbyte) {
+                const int c = kb * 4 + kbyte / 8, b = kbyte % 8;
+                if (b >= nb) continue;
+                const int ir = c * 9 + t;  // reference im2col column (layers.hpp:140-149)
+                const size_t src = (static_cast<size_t>(ir) * nb + b) * N + j;
+                const uint8_t v = pl.b_signed ? static_cast<uint8_t>(qw_s8[src]) : qw_u8[src];
+                // SW32 K-major: 16-byte chunk c of row n at chunk c ^ (n bit 2)
+                tile[n * 32 + ((((kbyte >> 4) ^ ((n >> 2) & 1))) << 4) + (kbyte & 15)] = v;
+              }
+            }
+          }
+      pl.wtw.upload(ww);
     }
   }
 
@@ -1780,6 +1830,89 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
   p.m_tiles = static_cast<int>((M + 127) / 128);
   p.dbg = nullptr;
   p.dbg_flags = e->dbg_flags;
+  // window-shared 3x3 conv kernel: 8 images per tile, all nine taps from one
+  // expanded window (kan_convw.cuh)
+  if (pl.convw && io.conv && io.x_kind == X_U16 && !io.fuse &&
+      (io.epi == EPI_LEVEL || (io.epi == EPI_F32 && io.out_hw == 0)) && (io.ld_x & 7) == 0 &&
+      (io.ld_out & 7) == 0 && (!io.res_kind || (io.ld_res & 3) == 0) &&
+      (reinterpret_cast<uintptr_t>(io.out) & 15) == 0 && (reinterpret_cast<uintptr_t>(io.res) & 15) == 0 &&
+      (reinterpret_cast<uintptr_t>(io.out_lv) & 15) == 0) {
+    const Layer& l = *io.conv;
+    const int W = l.out.w, TR = pl.trw, BNw = pl.bnw;
+    const int WR = (TR + 2) * (W + 2) * 8;
+    const bool zp = pl.wscheme == KAN_W_PER_TENSOR_ASYM;
+    const auto& ts = e->tabs[0];
+    int SA = 3, SB = 3, SX = 2;
+    if (const int rings = e->opt.convw_rings) {  // tuning: SA*100 + SB*10 + SX
+      SA = rings / 100;
+      SB = rings / 10 % 10;
+      SX = rings % 10;
+    }
+    while (convw_smem_bytes(BNw, WR, SA, SB, SX, ts.bytes, zp) > 232448 && SB > 2) --SB;
+    while (convw_smem_bytes(BNw, WR, SA, SB, SX, ts.bytes, zp) > 232448 && SA > 2) --SA;
+    if (convw_smem_bytes(BNw, WR, SA, SB, SX, ts.bytes, zp) <= 232448) {
+      p.M = static_cast<int>(io.n_img);  // images
+      p.N = pl.N;
+      p.BN = BNw;
+      p.n_tiles_n = pl.ntw;
+      p.SA = SA;
+      p.SB = SB;
+      p.SX = SX;
+      p.nacc = TR * W / 16;
+      p.splits = 1;
+      p.tab = ts.buf.p;
+      p.tab_bytes = ts.bytes;
+      p.off_thr = ts.off_thr;
+      p.off_silu = ts.off_silu;
+      p.off_c64 = ts.off_c64;
+      p.rep = 0;
+      p.wt = pl.wtw.p;
+      p.ext_rows = WR;
+      p.n_ss = l.c_in / 4;
+      p.b_slot = pl.b_slotw;
+      p.conv = 1;
+      p.H = l.in.h;
+      p.W = l.in.w;
+      p.bh = TR;
+      p.lvl0 = static_cast<int>(e->lat.quantize(0.0));
+      p.epi = io.epi;
+      p.out = io.out;
+      p.ld_out = static_cast<int>(io.ld_out);
+      p.fs = pl.fs.p;
+      p.f_tensor = pl.f_tensor;
+      p.z_w = pl.z_w;
+      p.n_lo = e->grid.lo;
+      p.n_hi_open = e->grid.hi_open();
+      p.n_step = e->lat.step;
+      p.n_inv_step = 1.0 / e->lat.step;
+      p.n_L = static_cast<int>(e->lat.L);
+      p.res_kind = io.res_kind;
+      p.res = io.res;
+      p.ld_res = static_cast<int>(io.ld_res);
+      p.out_lv = io.out_lv;
+      p.ld_lv = static_cast<int>(io.ld_out);
+      // 4D map over the NHWC levels with the IMAGE dimension second fastest:
+      // dims (C, N, W, H), box (8 channels, 8 images, W + 2, TR + 2)
+      CUtensorMap xm;
+      std::memset(&xm, 0, sizeof xm);
+      const uint64_t ldb = static_cast<uint64_t>(io.ld_x) * 2;
+      cuuint64_t dims[4] = {static_cast<cuuint64_t>(l.c_in), static_cast<cuuint64_t>(io.n_img),
+                            static_cast<cuuint64_t>(l.in.w), static_cast<cuuint64_t>(l.in.h)};
+      cuuint64_t strides[3] = {ldb * l.in.w * l.in.h, ldb, ldb * l.in.w};
+      cuuint32_t box[4] = {8u, 8u, static_cast<cuuint32_t>(W + 2), static_cast<cuuint32_t>(TR + 2)};
+      cuuint32_t estr[4] = {1u, 1u, 1u, 1u};
+      CUresult r = get_encode_fn()(&xm, CU_TENSOR_MAP_DATA_TYPE_UINT16, 4, const_cast<void*>(io.x), dims, strides,
+                                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (convw) failed (" + std::to_string(r) + ")");
+      const size_t smem = convw_smem_bytes(BNw, WR, SA, SB, SX, ts.bytes, zp);
+      if (e->opt.record_plan)
+        e->plan_add("convw", pl.layer_index, p.epi, p.res_kind, p.out_lv != nullptr, p.N, BNw, 1, zp ? 1 : 0);
+      ck(launch_convw(zp ? 1 : 0, xm, p, smem, st), "convw launch");  // MODE_ZP / MODE_PLAIN
+      e->last_launches += 1;
+      return;
+    }
+  }
   // ky-shared 3x3 conv kernel: full tile grids (persistent), no zero point
   // (it pays off on stored-level inputs with full channel chunks; fp32 inputs
   // and the few-channel stem stay on the general kernel, measured faster there)
@@ -2992,6 +3125,8 @@ kan_status kan_engine_set_option(kan_engine* e, int option, int64_t value) {
     const int v = static_cast<int>(value);
     switch (option) {
       case KAN_OPT_NO_CONV3: o.no_conv3 = value != 0; break;
+      case KAN_OPT_NO_CONVW: o.no_convw = value != 0; break;
+      case KAN_OPT_CONVW_RINGS: o.convw_rings = v; break;
       case KAN_OPT_NO_IM2COL: o.no_im2col = value != 0; break;
       case KAN_OPT_FORCE_BN: o.force_bn = v; break;
       case KAN_OPT_TABLES:

@@ -118,24 +118,107 @@ __device__ __noinline__ double ddiv_rn_slow(double a, double b) { return __ddiv_
 // for every level range the engine supports (L <= 4096), so llround(q) equals
 // the reference's llround(RN((t-lo)/step)) unless q lies within 1e-7 of a
 // half-integer; only then is the correctly rounded division evaluated.
+// Branch-free part of lattice_level_fast: the level from the multiply, plus
+// whether q lies in the tie band (then the caller redoes it with
+// lattice_level_f64, the division form).  Epilogues evaluate 16 of these with
+// no branch in between, so the fp64 chains overlap instead of running one
+// after another behind a per-element branch; ties are fixed up afterwards.
+__device__ __forceinline__ int level_mul(double y, double lo, double hi_open, double inv_step, int L, bool& tie) {
+  double t = (y < lo) ? lo : y;
+  t = (hi_open < t) ? hi_open : t;
+  const double u = __dadd_rn(__dmul_rn(__dsub_rn(t, lo), inv_step), 0.5);
+  int a = __double2int_rz(u);
+  const double f = __dsub_rn(u, static_cast<double>(a));
+  tie = (f < 1e-7) || (f > 1.0 - 1e-7);
+  a = a < 0 ? 0 : a;  // NaN converts to INT_MIN: level 0, as llround's INT64_MIN clamps
+  return a > L ? L : a;
+}
+// Branch-free part of lattice_level_tie: rint of the fp32 estimate, plus
+// whether it lies near a rounding tie (then the threshold test decides).
+__device__ __forceinline__ int level_tie_est(float x, float inv_step, float nlo_step, int L, bool& tie) {
+  float t = fmaf(x, inv_step, nlo_step);
+  t = fminf(fmaxf(t, 0.0f), static_cast<float>(L));
+  const float tr = rintf(t);
+  tie = fabsf(fabsf(t - tr) - 0.5f) < 2e-3f;
+  return static_cast<int>(tr);
+}
+
+// out-of-line tie fix-ups (rare; kept out of the epilogues' hot code)
+__device__ __noinline__ int level_fixup_f64(double y, double lo, double hi_open, double step, int L) {
+  return lattice_level_f64(y, lo, hi_open, step, L);
+}
+__device__ __noinline__ int level_fixup_f32(float x, float inv_step, float nlo_step, int L, const float* thr) {
+  float t = fmaf(x, inv_step, nlo_step);
+  t = fminf(fmaxf(t, 0.0f), static_cast<float>(L));
+  const int g = static_cast<int>(floorf(t));
+  return g + ((x >= thr[g + 1]) ? 1 : 0);
+}
+
+// 8 next-layer levels of fp64 values yf(0..7), packed two per word: the
+// branch-free estimates first (their fp64 chains overlap), tie fix-ups after
+template <class YF>
+__device__ __forceinline__ void levels8_f64(YF yf, double lo, double hi_open, double step, double inv_step, int L,
+                                            uint32_t* w) {
+  int lv[8];
+  uint32_t ties = 0;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    bool t;
+    lv[e] = level_mul(yf(e), lo, hi_open, inv_step, L, t);
+    ties |= static_cast<uint32_t>(t) << e;
+  }
+  if (ties) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      if ((ties >> e) & 1u) lv[e] = level_fixup_f64(yf(e), lo, hi_open, step, L);
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) w[q] = static_cast<uint32_t>(lv[2 * q]) | (static_cast<uint32_t>(lv[2 * q + 1]) << 16);
+}
+// 8 lattice levels of fp32 values xf(0..7) (lattice_level_tie), same scheme
+template <int N = 8, class XF>
+__device__ __forceinline__ void levels8_f32(XF xf, float inv_step, float nlo_step, int L, const float* thr, int* lv) {
+  uint32_t ties = 0;
+#pragma unroll
+  for (int e = 0; e < N; ++e) {
+    bool t;
+    lv[e] = level_tie_est(xf(e), inv_step, nlo_step, L, t);
+    ties |= static_cast<uint32_t>(t) << e;
+  }
+  if (ties) {
+#pragma unroll
+    for (int e = 0; e < N; ++e)
+      if ((ties >> e) & 1u) lv[e] = level_fixup_f32(xf(e), inv_step, nlo_step, L, thr);
+  }
+}
+
 __device__ __forceinline__ int lattice_level_fast(double y, double lo, double hi_open, double step,
                                                   double inv_step, int L) {
   double t = (y < lo) ? lo : y;
   t = (hi_open < t) ? hi_open : t;
   const double d = __dsub_rn(t, lo);
-  double q = __dmul_rn(d, inv_step);
-  if (fabs(__dsub_rn(__dsub_rn(q, floor(q)), 0.5)) < 1e-7) q = ddiv_rn_slow(d, step);
-  long long a = llround_ref(q);
-  if (a < 0) a = 0;
-  if (a > L) a = L;
-  return static_cast<int>(a);
+  // q >= 0 (or NaN), q < L + 1: llround(q) = trunc(q + 0.5), and q + 0.5 is
+  // exact below 2^52; f = the fraction of q + 0.5, so q is within 1e-7 of a
+  // half-integer exactly when f < 1e-7 or f > 1 - 1e-7 (then divide)
+  const double u = __dadd_rn(__dmul_rn(d, inv_step), 0.5);
+  int a = __double2int_rz(u);
+  const double f = __dsub_rn(u, static_cast<double>(a));
+  if (f < 1e-7 || f > 1.0 - 1e-7) a = __double2int_rz(__dadd_rn(ddiv_rn_slow(d, step), 0.5));
+  a = a < 0 ? 0 : a;  // NaN converts to INT_MIN: level 0, as llround's INT64_MIN clamps
+  return a > L ? L : a;
 }
 
 // clamp(llround(y / s), -127, 127) with the same guarded-multiply rule
+// (llround = trunc(q +- 0.5), exact for |q| < 2^52)
 __device__ __forceinline__ int requant_i8(double y, double s, double inv_s) {
   double q = __dmul_rn(y, inv_s);
-  if (fabs(q) < 1024.0 && fabs(__dsub_rn(__dsub_rn(q, floor(q)), 0.5)) < 1e-7) q = ddiv_rn_slow(y, s);
-  long long v = llround_ref(q);
+  double u = __dadd_rn(q, q < 0.0 ? -0.5 : 0.5);
+  long long v = __double2ll_rz(u);
+  const double f = fabs(__dsub_rn(u, static_cast<double>(v)));
+  if (fabs(q) < 1024.0 && (f < 1e-7 || f > 1.0 - 1e-7)) {
+    q = ddiv_rn_slow(y, s);
+    v = __double2ll_rz(__dadd_rn(q, q < 0.0 ? -0.5 : 0.5));
+  }
   v = v < -127 ? -127 : (v > 127 ? 127 : v);
   return static_cast<int>(v);
 }
@@ -874,8 +957,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 load_x<4 * H>(xt, r, xoff, x_row_bytes, xr);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(bar_xempty(rx.slot));
-#pragma unroll
-                for (int e = 0; e < H; ++e) a[e] = lattice_level_x(__uint_as_float(xr[e]), p, thr);
+                levels8_f32<H>([&](int e) { return __uint_as_float(xr[e]); }, p.inv_step_f, p.lo_f, p.L, thr, a);
               } else {
                 uint32_t xr[H / 2];
                 load_x<2 * H>(xt, r, xoff, x_row_bytes, xr);
@@ -1029,22 +1111,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 const int cl = g16 * 16;
                 uint32_t w[8];
 #pragma unroll
-                for (int e = 0; e < 16; e += 2) {
-                  double y0 = __dmul_rn(
-                      __dsub_rn(static_cast<double>(static_cast<int32_t>(r16[e])), s_cols[BN + cl + e]), s_cols[cl + e]);
-                  double y1 = __dmul_rn(
-                      __dsub_rn(static_cast<double>(static_cast<int32_t>(r16[e + 1])), s_cols[BN + cl + e + 1]),
-                      s_cols[cl + e + 1]);
-                  if constexpr (FE == 3) {
-                    y0 = __dadd_rn(y0, static_cast<double>((&rv4[e >> 2].x)[e & 3]));
-                    y1 = __dadd_rn(y1, static_cast<double>((&rv4[(e + 1) >> 2].x)[(e + 1) & 3]));
-                  }
-                  const uint32_t a0 =
-                      static_cast<uint32_t>(lattice_level_fast(y0, p.n_lo, p.n_hi_open, p.n_step, p.n_inv_step, p.n_L));
-                  const uint32_t a1 =
-                      static_cast<uint32_t>(lattice_level_fast(y1, p.n_lo, p.n_hi_open, p.n_step, p.n_inv_step, p.n_L));
-                  w[e >> 1] = a0 | (a1 << 16);
-                }
+                for (int hh = 0; hh < 2; ++hh)
+                  levels8_f64(
+                      [&](int e8) {
+                        const int e = 8 * hh + e8;
+                        double y = __dmul_rn(
+                            __dsub_rn(static_cast<double>(static_cast<int32_t>(r16[e])), s_cols[BN + cl + e]), s_cols[cl + e]);
+                        if constexpr (FE == 3) y = __dadd_rn(y, static_cast<double>((&rv4[e >> 2].x)[e & 3]));
+                        return y;
+                      },
+                      p.n_lo, p.n_hi_open, p.n_step, p.n_inv_step, p.n_L, w + 4 * hh);
                 uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(p.out) +
                                                     static_cast<size_t>(row) * p.ld_out + n0 + cl);
                 o[0] = make_uint4(w[0], w[1], w[2], w[3]);
@@ -1104,10 +1180,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 if (p.out_lv) {
                   uint32_t w[8];
 #pragma unroll
-                  for (int q = 0; q < 8; ++q) {
-                    const uint32_t a0 = static_cast<uint32_t>(lattice_level_tie(f[2 * q], p.inv_step_f, p.lo_f, p.L, thr));
-                    const uint32_t a1 = static_cast<uint32_t>(lattice_level_tie(f[2 * q + 1], p.inv_step_f, p.lo_f, p.L, thr));
-                    w[q] = a0 | (a1 << 16);
+                  for (int hh = 0; hh < 2; ++hh) {
+                    int lv[8];
+                    levels8_f32([&](int e8) { return f[8 * hh + e8]; }, p.inv_step_f, p.lo_f, p.L, thr, lv);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                      w[4 * hh + q] = static_cast<uint32_t>(lv[2 * q]) | (static_cast<uint32_t>(lv[2 * q + 1]) << 16);
                   }
                   __syncwarp();
                   // 48-byte pitch: conflict-free 16-byte stores
@@ -1139,10 +1217,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 if (p.out_lv) {
                   uint32_t w[8];
 #pragma unroll
-                  for (int q = 0; q < 8; ++q) {
-                    const uint32_t a0 = static_cast<uint32_t>(lattice_level_tie(f[2 * q], p.inv_step_f, p.lo_f, p.L, thr));
-                    const uint32_t a1 = static_cast<uint32_t>(lattice_level_tie(f[2 * q + 1], p.inv_step_f, p.lo_f, p.L, thr));
-                    w[q] = a0 | (a1 << 16);
+                  for (int hh = 0; hh < 2; ++hh) {
+                    int lv[8];
+                    levels8_f32([&](int e8) { return f[8 * hh + e8]; }, p.inv_step_f, p.lo_f, p.L, thr, lv);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                      w[4 * hh + q] = static_cast<uint32_t>(lv[2 * q]) | (static_cast<uint32_t>(lv[2 * q + 1]) << 16);
                   }
                   uint4* ol = reinterpret_cast<uint4*>(p.out_lv + static_cast<size_t>(row) * p.ld_lv + n0 + cl);
                   ol[0] = make_uint4(w[0], w[1], w[2], w[3]);
@@ -1391,6 +1471,7 @@ static cudaError_t launch_impl(const CUtensorMap& xmap, const GemmParams& p, siz
 }
 
 #include "kan_conv3.cuh"
+#include "kan_convw.cuh"
 
 int gemm_ips(bool bf16, int nbp) { return KSTAGE / (nbp * (bf16 ? 2 : 1)); }
 int gemm_gs(bool bf16, int nbp) { return KSTAGE / (bf16 ? 2 : 1) / gemm_ips(bf16, nbp); }

@@ -109,8 +109,13 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 // warp-uniform, so tcgen05 operands computed there live in uniform registers
 // (no per-instruction R2UR waterfall in the MMA issue loop).
 __device__ __forceinline__ void mbar_wait_warp(uint32_t bar, uint32_t parity) {
+#ifdef KAN_NO_SLEEP_HINT
+  while (!__all_sync(0xffffffffu, mbar_try_wait(bar, parity))) {
+  }
+#else
   while (!__all_sync(0xffffffffu, mbar_try_wait_sleep(bar, parity))) {
   }
+#endif
 }
 // one lane of the (converged) warp
 __device__ __forceinline__ bool elect_one() {

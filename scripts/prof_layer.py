@@ -12,7 +12,7 @@ sys.path.insert(0, ROOT)
 
 import torch  # noqa: E402
 
-from paper_2603_17230_b200 import Engine, EvalOptions, W_PER_CHANNEL_SYM  # noqa: E402
+from paper_2603_17230_b200 import Engine, EvalOptions  # noqa: E402
 from paper_2603_17230_b200 import configs  # noqa: E402
 
 
@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--split", type=int, default=0)
     ap.add_argument("--nograph", action="store_true")
     ap.add_argument("--mode", default="")
+    ap.add_argument("--opt", action="append", default=[], help="engine option name=value (repeatable)")
     a = ap.parse_args()
     wl = configs.get(a.config)
     B = a.batch or wl.batch
@@ -31,9 +32,13 @@ def main():
     e = Engine(wl.descriptor(), 0)
     for i, (w, b) in enumerate(zip(Ws, Bs)):
         e.set_coeffs(i, w, b)
-    e.configure(EvalOptions(mode=a.mode or wl.mode, lut_k=wl.lut_k, lut_h=wl.lut_h,
-                            bits_w=wl.bits_w, w_scheme=W_PER_CHANNEL_SYM, silu_base=wl.silu,
-                            split_k=a.split))
+    for kv in a.opt:
+        k, v = kv.split("=")
+        e.set_option(k, int(v))
+    o = wl.eval_options()
+    if a.mode:
+        o["mode"] = a.mode
+    e.configure(EvalOptions(**o, split_k=a.split))
     x = torch.from_numpy(wl.inputs(B)).cuda()
     out = e.model_forward(x)  # warm-up: allocations, lazy module load
     torch.cuda.synchronize()

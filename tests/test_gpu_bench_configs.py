@@ -37,7 +37,7 @@ def bench_engine(wl, **over):
     e = Engine(wl.descriptor(), 0)
     for i, (w, b) in enumerate(zip(Ws, Bs)):
         e.set_coeffs(i, w, b)
-    opts = EvalOptions(**wl.eval_options(), split_k=bench.SPLIT_DEFAULT.get(wl.key, 0))
+    opts = EvalOptions(**wl.eval_options(), split_k=bench.per_config(bench.SPLIT_DEFAULT, wl.key, 0))
     for k, v in over.items():
         setattr(opts, k, v)
     e.configure(opts)

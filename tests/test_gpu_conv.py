@@ -210,3 +210,58 @@ def test_stem_im2col_matches_implicit_conv(k, s, p):
     yi = build(desc, Ws, Bs, **opts).model_forward(to_dev(x)).cpu().numpy()
     yc = build(desc, Ws, Bs, engine_options={"no_im2col": 1}, **opts).model_forward(to_dev(x)).cpu().numpy()
     np.testing.assert_array_equal(yi, yc)
+
+
+# window-shared 3x3 kernel (kan_convw.cuh): 8 images per tile, all nine taps
+# from one expanded window; taken for 3x3/s1/p1 convs on stored levels with
+# 16- or 32-wide maps and no SiLU term.  Inputs are stored levels, so the
+# layer under test follows a 1x1 conv (which writes the levels).
+CONVW_CASES = [
+    # C, H, W, c_out, wscheme, batch
+    (64, 32, 32, 64, W_PER_TENSOR_ASYM, 16),   # C5 stage 1, the reference scheme
+    (64, 32, 32, 64, W_PER_CHANNEL_SYM, 13),   # partial image group
+    (128, 16, 16, 128, W_PER_TENSOR_ASYM, 9),  # C5 stage 2
+    (32, 16, 16, 256, W_PER_CHANNEL_SYM, 8),   # BN 256, one output row per tile
+    (16, 16, 16, 40, W_PER_TENSOR_ASYM, 11),   # ragged 16-column group
+    (8, 16, 16, 300, W_PER_CHANNEL_SYM, 3),    # two N tiles, the second ragged
+]
+
+
+@pytest.mark.parametrize("C,H,W,co,ws,batch", CONVW_CASES)
+def test_convw_kernel_bit_exact(oracle, C, H, W, co, ws, batch):
+    desc = conv_desc(C, H, W, C, 1, 1, 0)
+    desc["layers"].append({"type": "conv", "c_in": C, "c_out": co, "kernel": 3, "stride": 1, "padding": 1})
+    # a 1x1 consumer, so the layer under test writes a stored (NHWC) tensor
+    desc["layers"].append({"type": "conv", "c_in": co, "c_out": 8, "kernel": 1, "stride": 1, "padding": 0})
+    Ws, Bs = weights_for(desc, seed=C + co, silu=False)
+    x = np.random.default_rng(C * co).uniform(-1.05, 1.05, (batch, C * H * W)).astype(np.float32)
+    opts = dict(mode="bspline-lut", lut_k=8, lut_h=3, bits_w=8, w_scheme=ws, silu_base=False)
+    e = build(desc, Ws, Bs, **opts)
+    e.set_option("record_plan", 1)
+    y = e.model_forward(to_dev(x)).cpu().numpy()
+    assert "convw layer=1" in e.last_plan
+    yg = build(desc, Ws, Bs, engine_options={"no_convw": 1, "no_conv3": 1}, **opts).model_forward(to_dev(x)).cpu().numpy()
+    np.testing.assert_array_equal(y, yg)
+    yo = oracle.int_model_forward(desc, Ws, Bs, x, 8, 3, ws, 8)
+    np.testing.assert_array_equal(y, yo.astype(np.float32).reshape(batch, -1))
+
+
+@pytest.mark.parametrize("ws", [W_PER_TENSOR_ASYM, W_PER_CHANNEL_SYM])
+def test_convw_in_residual_stages_bit_exact(oracle, ws):
+    """Reduced-width ResKAN18 at 32x32 without the SiLU term: the stage-1/2
+    stride-1 convs take kan_convw (levels out; fp32 + residual + levels
+    sidecar out; residual then levels), batch 21 (a partial image group)."""
+    layers = configs.reskan18_layers(width=(16, 32), n_classes=10, in_ch=3)
+    desc = {"name": "r", "grid": {"intervals": 5, "degree": 3}, "input": [3, 32, 32],
+            "conv_output": "floor", "layers": layers}
+    Ws, Bs = weights_for(desc, seed=23, silu=False)
+    x = np.random.default_rng(23).uniform(-1, 1, (21, 3 * 1024)).astype(np.float32)
+    opts = dict(mode="bspline-lut", lut_k=8, lut_h=3, bits_w=8, w_scheme=ws, silu_base=False)
+    e = build(desc, Ws, Bs, **opts)
+    e.set_option("record_plan", 1)
+    y = e.model_forward(to_dev(x)).cpu().numpy()
+    assert e.last_plan.count("convw") >= 6
+    yg = build(desc, Ws, Bs, engine_options={"no_convw": 1}, **opts).model_forward(to_dev(x)).cpu().numpy()
+    np.testing.assert_array_equal(y, yg)
+    yo = oracle.int_model_forward(desc, Ws, Bs, x, 8, 3, ws, 8)
+    np.testing.assert_array_equal(y, yo.astype(np.float32))

@@ -85,7 +85,7 @@ def test_options_and_launch_plan():
     plan = e.last_plan.strip().splitlines()
     assert len(plan) == e.last_launches
     assert plan[0].startswith("im2col_levels") or plan[0].startswith("nchw_to_nhwc")
-    assert sum(p.startswith(("gather", "conv3", "small_layer")) for p in plan) == wl.n_kan
+    assert sum(p.startswith(("gather", "conv3", "convw", "small_layer")) for p in plan) == wl.n_kan
     e.set_option("record_plan", 0)
     e.model_forward(x)
     assert e.last_plan == ""
