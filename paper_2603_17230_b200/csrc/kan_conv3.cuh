@@ -376,7 +376,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               float f[16];
 #pragma unroll
               for (int e = 0; e < 16; ++e) {
-                double y = __dmul_rn(__dsub_rn(static_cast<double>(static_cast<int32_t>(r16[e])), s_cols[BN + cl + e]),
+                double y = __dmul_rn(__dsub_rn(i32_to_f64(r16[e]), s_cols[BN + cl + e]),
                                      s_cols[cl + e]);
                 if (p.res_kind) y = __dadd_rn(y, static_cast<double>((&rv4[e >> 2].x)[e & 3]));
                 f[e] = __double2float_rn(y);
@@ -445,7 +445,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               levels8_f64(
                   [&](int e8) {
                     const int e = 8 * hh + e8;
-                    return __dmul_rn(__dsub_rn(static_cast<double>(static_cast<int32_t>(r16[e])), s_cols[BN + cl + e]),
+                    return __dmul_rn(__dsub_rn(i32_to_f64(r16[e]), s_cols[BN + cl + e]),
                                      s_cols[cl + e]);
                   },
                   p.n_lo, p.n_hi_open, p.n_step, p.n_inv_step, p.n_L, w + 4 * hh);

@@ -20,11 +20,16 @@
 // output instead of 9x).  Outputs go back to NHWC row by row (each thread one
 // row of BN channels), so neighbouring layers are unaffected.
 //
-// Tile: 8 images x TR output rows x W columns (W = 16 or 32); NACC = TR*W/16
-// accumulators of 128 rows x BN columns, double-buffered in TMEM
-// (NACC * BN <= 256).  K: C_in / 4 blocks of 32 bytes (4 channels x NBP = 8
-// basis bytes); an activation load (8 channels, u16 levels) feeds two blocks,
-// expanded one per producer step so the A ring runs SA - 1 blocks ahead.
+// Tile: G images x TR output rows x TW columns, TW = min(W, 16) and G = 128 /
+// TW (8 images for maps 16 or 32 wide, 16 for 8-wide, 32 for 4-wide maps);
+// NACC = TR accumulators of 128 rows (one output row of TW pixels x G images)
+// x BN columns, double-buffered in TMEM (NACC * BN <= 256).  The window is
+// (TR+2) rows x (TW+2) columns x G images; a one-pixel shift is G/8 core-matrix
+// groups.  K: C_in / 4 blocks of 32 bytes (4
+// channels x NBP = 8 basis bytes), expanded one per producer step; an
+// activation load brings CX = 8 / 16 / 32 channels of every window row (16 /
+// 32 / 64-byte rows, TMA swizzle none / 32B / 64B, so the producers' 8-byte
+// reads stay conflict-free) and feeds CX / 4 blocks.
 // MODE_ZP (the reference's per-tensor asymmetric weights): the producers sum
 // each window row's codes over all channels (wsum), and the epilogue forms
 // each output row's code sum from the 9 window rows it read.
@@ -38,7 +43,10 @@ constexpr int CONVW_PRODUCER_WARPS = 12;
 constexpr int CONVW_THREADS = 32 * (CONVW_PRODUCER_WARPS + 3 + GEMM_EPI_WARPS);
 constexpr int CONVW_MAX_ROWS = 3 * 32 * CONVW_PRODUCER_WARPS;  // window rows: RPT rows per producer thread
 
-template <int MODE>
+// OUT: the epilogue's output, EPI_LEVEL (next-layer levels) or EPI_F32
+// (fp32 rows + levels sidecar); a separate instantiation each keeps the code
+// small enough for the instruction cache.
+template <int MODE, int OUT, int LG>
 __global__ void __launch_bounds__(CONVW_THREADS, 1)
     kan_convw_kernel(const __grid_constant__ CUtensorMap xmap, const GemmParams p) {
   constexpr int NPW = CONVW_PRODUCER_WARPS, NP = 32 * NPW;
@@ -51,12 +59,17 @@ __global__ void __launch_bounds__(CONVW_THREADS, 1)
   const int SA = p.SA, SB = p.SB, SX = p.SX;
   const int BN = p.BN;
   const int W = p.W, H = p.H, TR = p.bh;
-  const int WP = W + 2;                // window pitch in pixels
-  const int WR = p.ext_rows;           // window rows = (TR + 2) * WP * 8
+  constexpr int G = 1 << LG;           // images per tile (8, 16, 32)
+  constexpr int TW = 128 / G, WP = TW + 2;  // tile width, window pitch in pixels
+  constexpr int lg = LG;
+  const int CX = p.cps;                // channels per activation load
+  const int KPX = CX / 4;              // K blocks per activation load
+  const int WR = p.ext_rows;           // window rows = (TR + 2) * WP * G
   const int NACC = p.nacc;             // accumulators per tile
   const int n_kb = p.n_ss;             // 32-byte K blocks (4 channels each)
-  const uint32_t a_bytes = static_cast<uint32_t>(WR) * 32u;
-  const uint32_t x_bytes = static_cast<uint32_t>(WR) * 16u;  // 8 channels of u16 levels per row
+  const uint32_t a_bytes = (static_cast<uint32_t>(WR) * 32u + 1023u) & ~1023u;  // 1 KB-aligned slots
+  const uint32_t x_row = static_cast<uint32_t>(CX) * 2u;      // bytes per window row of one load
+  const uint32_t x_bytes = ((static_cast<uint32_t>(WR) * x_row + 1023u) & ~1023u);
   const uint32_t b_slot = static_cast<uint32_t>(p.b_slot);  // 9 taps x BN rows x 32 B
   uint8_t* sB = smem;
   uint8_t* sA = sB + static_cast<size_t>(SB) * b_slot;
@@ -72,19 +85,35 @@ __global__ void __launch_bounds__(CONVW_THREADS, 1)
   const int lane = threadIdx.x & 31;
   pdl_trigger();
 
-  // tiles: (image group of 8, band of TR output rows, N tile), N tile fastest
-  const int bands = H / TR;
-  const int n_groups = (p.M + 7) / 8;  // p.M = images
-  const int n_tiles = n_groups * bands * p.n_tiles_n;
+  // Work units: (block of MC image groups, band of TR output rows, TW-column
+  // block, N tile), N tile fastest.  With p.mc = MC > 1 the MC CTAs of a
+  // cluster take the MC image groups of a unit and share its weight slots:
+  // each slot is fetched once (by one CTA, in turn) and multicast into every
+  // CTA's ring, so L2 serves the weights once per cluster; a CTA whose image
+  // group is past the batch only releases the unit's weight slots.
+  const int MC = p.mc > 1 ? p.mc : 1;
+  const uint32_t crank = MC > 1 ? cluster_rank() : 0u;
+  const int unit0 = MC > 1 ? static_cast<int>(cluster_id_x()) : static_cast<int>(blockIdx.x);
+  const int unit_step = MC > 1 ? static_cast<int>(n_clusters_x()) : static_cast<int>(gridDim.x);
+  const uint16_t mc_mask = static_cast<uint16_t>((1u << MC) - 1u);
+  const int bands = H / TR, cblocks = W / TW;
+  const int n_groups = (p.M + G - 1) / G;  // p.M = images
+  const int n_units = (n_groups + MC - 1) / MC * bands * cblocks * p.n_tiles_n;
   struct Tile {
-    int g, oy0, nt;
+    int g, oy0, x0, nt;
+    bool valid;
   };
-  auto tile_of = [&](int t) {
+  auto tile_of = [&](int u) {
     Tile r;
-    r.nt = t % p.n_tiles_n;
-    const int gb = t / p.n_tiles_n;
-    r.g = gb / bands;
-    r.oy0 = (gb - r.g * bands) * TR;
+    r.nt = u % p.n_tiles_n;
+    int q = u / p.n_tiles_n;
+    const int cb = q % cblocks;
+    q /= cblocks;
+    const int gb = q / bands;
+    r.oy0 = (q - gb * bands) * TR;
+    r.x0 = cb * TW;
+    r.g = gb * MC + static_cast<int>(crank);
+    r.valid = r.g < n_groups;
     return r;
   };
 
@@ -112,7 +141,7 @@ __global__ void __launch_bounds__(CONVW_THREADS, 1)
     }
     for (int s = 0; s < SB; ++s) {
       mbar_init(bar_bfull(s), 1);
-      mbar_init(bar_bempty(s), 1);
+      mbar_init(bar_bempty(s), MC);  // every CTA of the cluster releases the slot
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(bar_accfull(b), 1);
@@ -127,21 +156,25 @@ __global__ void __launch_bounds__(CONVW_THREADS, 1)
   if (warp == W_MMA) tmem_alloc(smem_u32(s_tmem), 512);
   tc_fence_before();
   __syncthreads();
+  if (MC > 1) cluster_sync_all();  // peers' barriers initialised before any multicast
   tc_fence_after();
   const uint32_t tmem = *s_tmem;
 
   if (warp == W_X) {
-    // ============ activation loader: the tile's window, 8 channels per load ======
+    // ============ activation loader: the tile's window, CX channels per load ====
     pdl_wait();
     Ring rx(SX);
-    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-      const Tile tl = tile_of(t);
-      for (int kp = 0; kp < n_kb / 2; ++kp, rx.next()) {
+    for (int u = unit0; u < n_units; u += unit_step) {
+      const Tile tl = tile_of(u);
+      if (!tl.valid) continue;
+      for (int kp = 0; kp < n_kb / KPX; ++kp, rx.next()) {
         mbar_wait(bar_xempty(rx.slot), rx.phase ^ 1);
-        if (lane == 0) {
-          mbar_arrive_tx(bar_xfull(rx.slot), x_bytes);
-          // box (8 channels, 8 images, W+2 columns, TR+2 rows) from (c, img, -1, oy0-1)
-          tma_load_4d(smem_u32(sX + static_cast<size_t>(rx.slot) * x_bytes), &xmap, kp * 8, tl.g * 8, -1,
+        if (lane == 0 && KAN_DBG(p, 4)) {  // tuning only: no activation loads (stale window)
+          mbar_arrive(bar_xfull(rx.slot));
+        } else if (lane == 0) {
+          mbar_arrive_tx(bar_xfull(rx.slot), static_cast<uint32_t>(WR) * x_row);
+          // box (CX channels, G images, TW+2 columns, TR+2 rows) from (c, img, x0-1, oy0-1)
+          tma_load_4d(smem_u32(sX + static_cast<size_t>(rx.slot) * x_bytes), &xmap, kp * CX, tl.g * G, tl.x0 - 1,
                       tl.oy0 - 1, bar_xfull(rx.slot));
         }
         __syncwarp();
@@ -155,18 +188,30 @@ __global__ void __launch_bounds__(CONVW_THREADS, 1)
     }
     __syncwarp();
     Ring rb(SB);
-    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-      const Tile tl = tile_of(t);
-      for (int kb = 0; kb < n_kb; ++kb, rb.next()) {
+    uint32_t fill = 0;
+    for (int u = unit0; u < n_units; u += unit_step) {
+      const Tile tl = tile_of(u);
+      for (int kb = 0; kb < n_kb; ++kb, rb.next(), ++fill) {
+        // released by every CTA of the cluster: safe to refill everywhere
         mbar_wait(bar_bempty(rb.slot), rb.phase ^ 1);
         if (lane == 0) {
+          const uint32_t dst = smem_u32(sB + static_cast<size_t>(rb.slot) * b_slot);
+          const uint8_t* src = p.wt + (static_cast<size_t>(tl.nt) * n_kb + kb) * b_slot;
+          if (KAN_DBG(p, 32)) {  // tuning only: no weight loads (stale slots)
+            mbar_arrive(bar_bfull(rb.slot));
+          } else {
           mbar_arrive_tx(bar_bfull(rb.slot), b_slot);
-          bulk_load(smem_u32(sB + static_cast<size_t>(rb.slot) * b_slot),
-                    p.wt + (static_cast<size_t>(tl.nt) * n_kb + kb) * b_slot, b_slot, bar_bfull(rb.slot));
+          if (MC == 1)
+            bulk_load(dst, src, b_slot, bar_bfull(rb.slot));
+          else if (fill % MC == crank)
+            bulk_load_mc(dst, src, b_slot, bar_bfull(rb.slot), mc_mask);
+          }
         }
         __syncwarp();
       }
     }
+    // drain: every peer's release of our slots has landed before the CTA exits
+    for (int s = 0; s < SB; ++s, rb.next()) mbar_wait(bar_bempty(rb.slot), rb.phase ^ 1);
   } else if (warp == W_MMA) {
     // ============ MMA issuer: 9 taps x NACC accumulators per K block ============
     const uint32_t idesc = idesc_i8(BN, p.b_signed != 0);
@@ -176,16 +221,27 @@ __global__ void __launch_bounds__(CONVW_THREADS, 1)
     // K block is 36 MMAs of ~34 tensor cycles each, so the loop must be short)
     uint32_t acc_row[8], tap_row[9];
 #pragma unroll
-    for (int a = 0; a < 8; ++a) {
-      const int py = (a * 16) / W, px = a * 16 - py * W;
-      acc_row[a] = static_cast<uint32_t>((py * WP + px) * 8 * 2);
-    }
+    for (int a = 0; a < 8; ++a) acc_row[a] = static_cast<uint32_t>(a * WP * G * 2);  // accumulator a = band row a
 #pragma unroll
-    for (int tap = 0; tap < 9; ++tap) tap_row[tap] = static_cast<uint32_t>(((tap / 3) * WP + tap % 3) * 8 * 2);
+    for (int tap = 0; tap < 9; ++tap) tap_row[tap] = static_cast<uint32_t>(((tap / 3) * WP + tap % 3) * G * 2);
     const uint64_t b_tap = static_cast<uint64_t>(BN) * 2u;  // one tap's weight tile (BN x 32 B) in 16-byte units
     Ring ra(SA), rb(SB);
+    auto release_b = [&](uint32_t bar) {
+      if (MC == 1)
+        tc_commit(bar);
+      else
+        tc_commit_mc(bar, mc_mask);
+    };
     int lt = 0;
-    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++lt) {
+    for (int u = unit0; u < n_units; u += unit_step) {
+      if (!tile_of(u).valid) {  // no tile here: release the unit's weight slots
+        for (int kb = 0; kb < n_kb; ++kb, rb.next()) {
+          mbar_wait_warp(bar_bfull(rb.slot), rb.phase);
+          if (elect_one()) release_b(bar_bempty(rb.slot));
+          __syncwarp();
+        }
+        continue;
+      }
       const int ab = lt & 1;
       mbar_wait_warp(bar_accempty(ab), ((lt >> 1) & 1) ^ 1);
       tc_fence_after();
@@ -207,12 +263,13 @@ __global__ void __launch_bounds__(CONVW_THREADS, 1)
                 mma_i8(dacc + static_cast<uint32_t>(a * BN), ad0 + (acc_row[a] + tap_row[tap]), bd, idesc, acc);
           }
           tc_commit(bar_aempty(ra.slot));
-          tc_commit(bar_bempty(rb.slot));
+          release_b(bar_bempty(rb.slot));
         }
         __syncwarp();
       }
       if (elect_one()) tc_commit(bar_accfull(ab));
       __syncwarp();
+      ++lt;
     }
   } else if (warp < NPW) {
     // ============ producers: expand the window once per K block =================
@@ -221,8 +278,9 @@ __global__ void __launch_bounds__(CONVW_THREADS, 1)
     const int tid = threadIdx.x;  // 0 .. NP-1
     Ring ra(SA), rx(SX);
     int lt = 0;
-    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++lt) {
-      const Tile tl = tile_of(t);
+    for (int u = unit0; u < n_units; u += unit_step) {
+      const Tile tl = tile_of(u);
+      if (!tl.valid) continue;
       // this thread's window rows r = tid + q*NP: spatial padding flags (taps
       // outside the map read level(0.0), as im2col's zero taps do)
       bool pad[RPT];
@@ -230,23 +288,28 @@ __global__ void __launch_bounds__(CONVW_THREADS, 1)
 #pragma unroll
       for (int q = 0; q < RPT; ++q) {
         const int r = tid + q * NP;
-        const int pix = r >> 3, wy = pix / WP, wx = pix - wy * WP;
-        const int iy = tl.oy0 - 1 + wy, ix = wx - 1;
+        const int pix = r >> lg, wy = pix / WP, wx = pix - wy * WP;
+        const int iy = tl.oy0 - 1 + wy, ix = tl.x0 - 1 + wx;
         pad[q] = static_cast<unsigned>(iy) >= static_cast<unsigned>(H) || static_cast<unsigned>(ix) >= static_cast<unsigned>(W);
         rs[q] = 0u;
       }
       for (int kb = 0; kb < n_kb; ++kb, ra.next()) {
-        // one K block (4 channels) per step; an activation load covers two
-        const int xh = kb & 1;
+        // one K block (4 channels) per step; an activation load covers KPX
+        const int xh = kb & (KPX - 1);  // KPX = 2, 4 or 8
         if (xh == 0) mbar_wait(bar_xfull(rx.slot), rx.phase);
         mbar_wait(bar_aempty(ra.slot), ra.phase ^ 1);
-        const uint8_t* xt = sX + static_cast<size_t>(rx.slot) * x_bytes + xh * 8;
+        const uint8_t* xt = sX + static_cast<size_t>(rx.slot) * x_bytes;
         uint8_t* at = sA + static_cast<size_t>(ra.slot) * a_bytes;
+        // this block's 8 bytes of a window row: 16-byte chunk xh/2 (swizzled
+        // with the row as the TMA wrote it), half xh&1
+        const uint32_t chunk = static_cast<uint32_t>(xh >> 1), off8 = static_cast<uint32_t>(xh & 1) * 8u;
 #pragma unroll
         for (int q = 0; q < RPT; ++q) {
           const int r = tid + q * NP;
           if (r < WR) {
-            const uint2 lv = *reinterpret_cast<const uint2*>(xt + static_cast<size_t>(r) * 16);
+            const uint32_t ur = static_cast<uint32_t>(r);
+            const uint32_t sw = CX == 32 ? ((ur >> 1) & 3u) : (CX == 16 ? ((ur >> 2) & 1u) : 0u);
+            const uint2 lv = *reinterpret_cast<const uint2*>(xt + ur * x_row + ((chunk ^ sw) << 4) + off8);
             const uint32_t lw[2] = {lv.x, lv.y};
             uint32_t w[8];
 #pragma unroll
@@ -258,19 +321,19 @@ __global__ void __launch_bounds__(CONVW_THREADS, 1)
               if constexpr (ZP) rs[q] = __dp4a(c.y, 0x01010101u, __dp4a(c.x, 0x01010101u, rs[q]));
             }
             // row r of the SW32 K-major window: 16-byte chunk c at c ^ row bit 2
-            const uint32_t sw = (static_cast<uint32_t>(r) >> 2) & 1u;
+            const uint32_t sa = (ur >> 2) & 1u;
             uint8_t* d = at + static_cast<size_t>(r) * 32;
-            *reinterpret_cast<uint4*>(d + (sw << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
-            *reinterpret_cast<uint4*>(d + ((sw ^ 1u) << 4)) = make_uint4(w[4], w[5], w[6], w[7]);
+            *reinterpret_cast<uint4*>(d + (sa << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+            *reinterpret_cast<uint4*>(d + ((sa ^ 1u) << 4)) = make_uint4(w[4], w[5], w[6], w[7]);
           }
         }
         fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
         __syncwarp();
         if (lane == 0) {
-          if (xh == 1) mbar_arrive(bar_xempty(rx.slot));
+          if (xh == KPX - 1) mbar_arrive(bar_xempty(rx.slot));
           mbar_arrive(bar_afull(ra.slot));
         }
-        if (xh == 1) rx.next();
+        if (xh == KPX - 1) rx.next();
       }
       if constexpr (ZP) {
         // the window rows' code sums for the epilogue's zero-point term
@@ -284,6 +347,7 @@ __global__ void __launch_bounds__(CONVW_THREADS, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_wsfull(wb));
       }
+      ++lt;
     }
   } else {
     // ============ epilogue: NACC accumulators x BN columns -> NHWC rows ==========
@@ -292,13 +356,14 @@ __global__ void __launch_bounds__(CONVW_THREADS, 1)
     const int wq = warp & 3;             // TMEM lane quarter
     const int half = (warp - W_EPI) >> 2;  // alternate 16-column groups
     const int rloc = wq * 32 + lane;     // row within an accumulator
-    const int img_l = rloc & 7, pl_ = rloc >> 3;
+    const int img_l = rloc & (G - 1), pl_ = rloc >> lg;
     const uint32_t t_row = tmem + (static_cast<uint32_t>(wq * 32) << 16);
     const int et = static_cast<int>(threadIdx.x) - 32 * W_EPI;
     int lt = 0;
     int staged_nt = -1;
-    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++lt) {
-      const Tile tl = tile_of(t);
+    for (int u = unit0; u < n_units; u += unit_step) {
+      const Tile tl = tile_of(u);
+      if (!tl.valid) continue;
       const int ab = lt & 1;
       if (!ZP && tl.nt != staged_nt) {  // per-column scales (restaged when the N tile changes)
         asm volatile("bar.sync 5, %0;" ::"r"(32 * GEMM_EPI_WARPS) : "memory");
@@ -310,22 +375,21 @@ __global__ void __launch_bounds__(CONVW_THREADS, 1)
       tc_fence_after();
       const int32_t* ws = s_wsum + (lt & 1) * WR;
       if constexpr (ZP) mbar_wait(bar_wsfull(lt & 1), (lt >> 1) & 1);
-      const int img = tl.g * 8 + img_l;
+      const int img = tl.g * G + img_l;
       const bool valid = img < p.M;
       const int n0 = tl.nt * BN;
 #pragma unroll 1
       for (int a = 0; a < NACC; ++a) {
-        const int pix = a * 16 + pl_;
-        const int py = pix / W, px = pix - py * W;
+        const int py = a, px = pl_;  // accumulator a = band row a; its rows = TW pixels x G images
         const int oy = tl.oy0 + py;
-        const size_t orow = (static_cast<size_t>(img) * H + oy) * W + px;  // NHWC row
-        long long zc = 0;
+        const size_t orow = (static_cast<size_t>(img) * H + oy) * W + tl.x0 + px;  // NHWC row
+        double zc = 0.0;
         if constexpr (ZP) {
           // the row's code sum: the 9 window rows its taps read (zero-point term)
           int s_ = 0;
 #pragma unroll
-          for (int tap = 0; tap < 9; ++tap) s_ += ws[(((py + tap / 3) * WP + px + tap % 3) << 3) + img_l];
-          zc = p.z_w * static_cast<long long>(s_);
+          for (int tap = 0; tap < 9; ++tap) s_ += ws[(((py + tap / 3) * WP + px + tap % 3) << lg) + img_l];
+          zc = static_cast<double>(p.z_w * static_cast<long long>(s_));  // exact below 2^53
         }
         const uint32_t tacc = t_row + static_cast<uint32_t>(ab) * 256u + static_cast<uint32_t>(a * BN);
 #pragma unroll 1
@@ -336,9 +400,7 @@ __global__ void __launch_bounds__(CONVW_THREADS, 1)
             size_t nrow = orow;
             int ncl = cl + 32;
             if (ncl >= BN && a + 1 < NACC) {
-              const int npix = (a + 1) * 16 + pl_;
-              const int npy = npix / W;
-              nrow = (static_cast<size_t>(img) * H + tl.oy0 + npy) * W + (npix - npy * W);
+              nrow = orow + static_cast<size_t>(W);  // the next band row, same pixel
               ncl = half * 16;
             }
             if (ncl < BN && n0 + ncl < p.N)
@@ -356,17 +418,18 @@ __global__ void __launch_bounds__(CONVW_THREADS, 1)
           tmem_wait_ld();
           if (!valid) continue;
           // y = (acc - z_w * rowsum) * f (ZP) or acc * fs[j]; + residual (fp64)
+          // (acc - z_w * rowsum) is exact in fp64, so converting first changes nothing
           auto yval = [&](int e) -> double {
             double y;
             if constexpr (ZP)
-              y = __dmul_rn(static_cast<double>(static_cast<long long>(static_cast<int32_t>(r16[e])) - zc), p.f_tensor);
+              y = __dmul_rn(__dsub_rn(i32_to_f64(r16[e]), zc), p.f_tensor);
             else
-              y = __dmul_rn(static_cast<double>(static_cast<int32_t>(r16[e])), s_cols[cl + e]);
+              y = __dmul_rn(i32_to_f64(r16[e]), s_cols[cl + e]);
             if (p.res_kind) y = __dadd_rn(y, static_cast<double>((&rv4[e >> 2].x)[e & 3]));
             return y;
           };
           if (full) {
-            if (p.epi == EPI_LEVEL) {
+            if constexpr (OUT == EPI_LEVEL) {
               // branch-free level estimates 8 at a time, then the (rare) tie fix-ups
               uint32_t w[8];
 #pragma unroll
@@ -405,11 +468,11 @@ __global__ void __launch_bounds__(CONVW_THREADS, 1)
               if (j >= p.N) break;
               double v;
               if constexpr (ZP)
-                v = __dmul_rn(static_cast<double>(static_cast<long long>(static_cast<int32_t>(r16[e])) - zc), p.f_tensor);
+                v = __dmul_rn(__dsub_rn(i32_to_f64(r16[e]), zc), p.f_tensor);
               else
-                v = __dmul_rn(static_cast<double>(static_cast<int32_t>(r16[e])), s_cols[cl + e]);
+                v = __dmul_rn(i32_to_f64(r16[e]), s_cols[cl + e]);
               if (p.res_kind) v = __dadd_rn(v, static_cast<double>(reinterpret_cast<const float*>(p.res)[orow * p.ld_res + j]));
-              if (p.epi == EPI_LEVEL) {
+              if constexpr (OUT == EPI_LEVEL) {
                 reinterpret_cast<uint16_t*>(p.out)[orow * p.ld_out + j] =
                     static_cast<uint16_t>(lattice_level_fast(v, p.n_lo, p.n_hi_open, p.n_step, p.n_inv_step, p.n_L));
               } else {
@@ -429,42 +492,60 @@ __global__ void __launch_bounds__(CONVW_THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(bar_accempty(ab));
+      ++lt;
     }
   }
 
   tc_fence_before();
   __syncthreads();
+  if (MC > 1) cluster_sync_all();  // no multicast into / release of an exited CTA
   if (warp == W_MMA) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
 }
 
-size_t convw_smem_bytes(int BN, int WR, int SA, int SB, int SX, int tab_bytes, bool zp) {
+size_t convw_smem_bytes(int BN, int WR, int CX, int SA, int SB, int SX, int tab_bytes, bool zp) {
   const size_t b = static_cast<size_t>(9) * BN * 32;
-  return 1024 + SB * b + SA * static_cast<size_t>(WR) * 32 + SX * static_cast<size_t>(WR) * 16 +
+  const size_t x = (static_cast<size_t>(WR) * CX * 2 + 1023) / 1024 * 1024;
+  return 1024 + SB * b + SA * ((static_cast<size_t>(WR) * 32 + 1023) / 1024 * 1024) + SX * x +
          ((static_cast<size_t>(tab_bytes) + 15) & ~static_cast<size_t>(15)) + (zp ? 2 * static_cast<size_t>(WR) * 4 : 0) +
          (2 * SA + 2 * SB + 2 * SX + 13) * 8 + static_cast<size_t>(BN) * 8 + 16;
 }
 
 cudaError_t launch_convw(int mode, const CUtensorMap& xmap, const GemmParams& p, size_t smem, cudaStream_t st) {
-  static std::atomic<unsigned long long> optin[2];
+  static std::atomic<unsigned long long> optin[12];
   auto go = [&](auto kfn, int v) -> cudaError_t {
     if (cudaError_t e = smem_optin(kfn, optin[v]); e != cudaSuccess) return e;
     const int n_sm = device_sm_count();
-    const int tiles = (p.M + 7) / 8 * (p.H / p.bh) * p.n_tiles_n;
+    const int mc = p.mc > 1 ? p.mc : 1;
+    const int units = ((p.M + p.bn_img - 1) / p.bn_img + mc - 1) / mc * (p.H / p.bh) * (p.W / p.Wo) * p.n_tiles_n;
+    const int clusters = units < n_sm / mc ? units : n_sm / mc;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(static_cast<unsigned>(tiles < n_sm ? tiles : n_sm));
+    cfg.gridDim = dim3(static_cast<unsigned>(clusters * mc));
     cfg.blockDim = dim3(CONVW_THREADS);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = static_cast<unsigned>(mc);
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = mc > 1 ? 2 : 1;  // a cluster launch only when the weights are multicast
     return cudaLaunchKernelEx(&cfg, kfn, xmap, p);
   };
-  if (mode == MODE_ZP) return go(kan_convw_kernel<MODE_ZP>, 1);
-  return go(kan_convw_kernel<MODE_PLAIN>, 0);
+  const bool lvl = p.epi == EPI_LEVEL;
+  auto pick = [&](auto lgc) -> cudaError_t {
+    constexpr int LG = decltype(lgc)::value;
+    const int v = 4 * (LG - 3);
+    if (mode == MODE_ZP)
+      return lvl ? go(kan_convw_kernel<MODE_ZP, EPI_LEVEL, LG>, v + 3) : go(kan_convw_kernel<MODE_ZP, EPI_F32, LG>, v + 2);
+    return lvl ? go(kan_convw_kernel<MODE_PLAIN, EPI_LEVEL, LG>, v + 1) : go(kan_convw_kernel<MODE_PLAIN, EPI_F32, LG>, v);
+  };
+  if (p.bn_img == 8) return pick(std::integral_constant<int, 3>{});
+  if (p.bn_img == 16) return pick(std::integral_constant<int, 4>{});
+  return pick(std::integral_constant<int, 5>{});
 }

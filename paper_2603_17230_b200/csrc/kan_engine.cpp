@@ -53,7 +53,7 @@ cudaError_t launch_rows_to_levels(const float* x, int64_t M, int n, int ld_x, ui
 cudaError_t launch_conv3(int mode, const CUtensorMap& xmap, const GemmParams& p, size_t smem, cudaStream_t st);
 size_t conv3_smem_bytes(int BN, int R, int SA, int SB, int SX, int x_kind, int tab_bytes, bool silu);
 cudaError_t launch_convw(int mode, const CUtensorMap& xmap, const GemmParams& p, size_t smem, cudaStream_t st);
-size_t convw_smem_bytes(int BN, int WR, int SA, int SB, int SX, int tab_bytes, bool zp);
+size_t convw_smem_bytes(int BN, int WR, int CX, int SA, int SB, int SX, int tab_bytes, bool zp);
 size_t small_smem_bytes(const SmallParams& p);
 cudaError_t launch_im2col_levels(const float* x, int64_t n_img, int C, int H, int W, int K, int stride, int pad,
                                  int Ho, int Wo, uint16_t* out, int ld_o, const float* thr, float nlo_step,
@@ -360,7 +360,7 @@ struct kan_engine {
   // into the fields above, so nothing is read from the environment
   struct Options {
     bool no_convw = false;
-    int convw_rings = 0;
+    int convw_rings = 0, convw_tr = 0, convw_mc = 0;
     bool no_conv3 = false, no_im2col = false, epi_stage = true, lv_sidecar = true, st_prepass = true;
     bool timeline = false, force_nacc1 = false, record_plan = false;
     int force_bn = 0, tables = -1, conv3_mc = 2, st_slices = 0, dbg_flags = 0;
@@ -912,17 +912,20 @@ void prepare_gemm_layer(kan_engine* e, const Layer& l, PreparedLayer& pl, bool b
   }
 
   // window-shared 3x3 stride-1 pad-1 conv kernel (kan_convw.cuh): no SiLU
-  // term, 16- or 32-pixel-wide maps, whole 8-channel activation loads
+  // term, maps a multiple of 16 wide, whole 8-channel activation loads
   pl.convw = false;
+  const int tw = std::min(16, l.out.w);  // tile width; 128 / tw images per tile
   if (!bf16 && l.type == L_CONV && !l.im2col && l.kernel == 3 && l.stride == 1 && l.padding == 1 && nbp == 8 &&
-      !pl.silu && !e->opt.no_convw && l.c_in % 8 == 0 && (l.out.w == 16 || l.out.w == 32) && l.out.h == l.in.h &&
-      l.out.w == l.in.w) {
-    const int W = l.out.w;
+      !pl.silu && !e->opt.no_convw && l.c_in % 8 == 0 && (tw == 16 || tw == 8 || tw == 4) && l.out.w % tw == 0 &&
+      l.out.h == l.in.h && l.out.w == l.in.w) {
     const int bnw = N <= 256 ? (N + 15) / 16 * 16 : 256;
-    const int per_row = W / 16;  // accumulators per output row
-    int tr = 1;
-    while (2 * tr * per_row * bnw <= 256 && l.out.h % (2 * tr) == 0 && (2 * tr + 2) * (W + 2) * 8 <= 1152) tr *= 2;
-    if (tr * per_row * bnw <= 256 && l.out.h % tr == 0 && (tr + 2) * (W + 2) * 8 <= 1152) {  // CONVW_MAX_ROWS
+    const int gimg = 128 / tw;
+    // output rows per tile: as many accumulators (one per row) as TMEM double-
+    // buffers and the producers' window rows allow, dividing the map height
+    int tr = 0;
+    for (int t = 1; t <= 6; ++t)
+      if (t * bnw <= 256 && l.out.h % t == 0 && (t + 2) * (tw + 2) * gimg <= 1152) tr = t;  // CONVW_MAX_ROWS
+    if (tr > 0) {
       pl.convw = true;
       pl.bnw = bnw;
       pl.trw = tr;
@@ -1838,19 +1841,35 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
       (reinterpret_cast<uintptr_t>(io.out) & 15) == 0 && (reinterpret_cast<uintptr_t>(io.res) & 15) == 0 &&
       (reinterpret_cast<uintptr_t>(io.out_lv) & 15) == 0) {
     const Layer& l = *io.conv;
-    const int W = l.out.w, TR = pl.trw, BNw = pl.bnw;
-    const int WR = (TR + 2) * (W + 2) * 8;
+    int TR = pl.trw;
+    const int BNw = pl.bnw;
+    if (const int t = e->opt.convw_tr; t > 0 && t < TR && l.out.h % t == 0) TR = t;  // tuning: fewer rows per tile
     const bool zp = pl.wscheme == KAN_W_PER_TENSOR_ASYM;
     const auto& ts = e->tabs[0];
-    int SA = 3, SB = 3, SX = 2;
-    if (const int rings = e->opt.convw_rings) {  // tuning: SA*100 + SB*10 + SX
-      SA = rings / 100;
-      SB = rings / 10 % 10;
-      SX = rings % 10;
+    // activation loads: CX channels (64-byte rows where the channels allow),
+    // and the deepest rings that fit, trading window height for them
+    int CX = l.c_in % 32 == 0 ? 32 : (l.c_in % 16 == 0 ? 16 : 8);
+    int SA = 4, SB = 3, SX = 2, WR = 0;
+    int TRu = TR;
+    const int TW = std::min(16, l.out.w), G = 128 / TW;
+    for (;;) {
+      WR = (TRu + 2) * (TW + 2) * G;
+      SA = 4, SB = 3, SX = 2;
+      if (const int rings = e->opt.convw_rings) {  // tuning: SA*100 + SB*10 + SX
+        SA = rings / 100;
+        SB = rings / 10 % 10;
+        SX = rings % 10;
+      }
+      auto fits = [&] { return convw_smem_bytes(BNw, WR, CX, SA, SB, SX, ts.bytes, zp) <= 232448; };
+      while (!fits() && SB > 2) --SB;
+      while (!fits() && SA > 3) --SA;
+      while (!fits() && CX > 16) CX /= 2;
+      while (!fits() && SA > 2) --SA;
+      while (!fits() && CX > 8) CX /= 2;
+      if (fits() || TRu == 1) break;
+      do { --TRu; } while (TRu > 1 && l.out.h % TRu != 0);
     }
-    while (convw_smem_bytes(BNw, WR, SA, SB, SX, ts.bytes, zp) > 232448 && SB > 2) --SB;
-    while (convw_smem_bytes(BNw, WR, SA, SB, SX, ts.bytes, zp) > 232448 && SA > 2) --SA;
-    if (convw_smem_bytes(BNw, WR, SA, SB, SX, ts.bytes, zp) <= 232448) {
+    if (convw_smem_bytes(BNw, WR, CX, SA, SB, SX, ts.bytes, zp) <= 232448) {
       p.M = static_cast<int>(io.n_img);  // images
       p.N = pl.N;
       p.BN = BNw;
@@ -1858,8 +1877,11 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
       p.SA = SA;
       p.SB = SB;
       p.SX = SX;
-      p.nacc = TR * W / 16;
+      p.nacc = TRu;
       p.splits = 1;
+      // weight slots shared by a cluster of image groups (multicast): the
+      // weights are re-streamed from L2 per tile, 9 taps x BN x 32 B per K block
+      p.mc = e->opt.convw_mc > 0 ? e->opt.convw_mc : 1;
       p.tab = ts.buf.p;
       p.tab_bytes = ts.bytes;
       p.off_thr = ts.off_thr;
@@ -1873,7 +1895,10 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
       p.conv = 1;
       p.H = l.in.h;
       p.W = l.in.w;
-      p.bh = TR;
+      p.bh = TRu;
+      p.Wo = TW;     // tile width
+      p.bn_img = G;  // images per tile
+      p.cps = CX;    // channels per activation load
       p.lvl0 = static_cast<int>(e->lat.quantize(0.0));
       p.epi = io.epi;
       p.out = io.out;
@@ -1892,20 +1917,23 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
       p.out_lv = io.out_lv;
       p.ld_lv = static_cast<int>(io.ld_out);
       // 4D map over the NHWC levels with the IMAGE dimension second fastest:
-      // dims (C, N, W, H), box (8 channels, 8 images, W + 2, TR + 2)
+      // dims (C, N, W, H), box (CX channels, 8 images, 18 columns, TR + 2 rows)
       CUtensorMap xm;
       std::memset(&xm, 0, sizeof xm);
       const uint64_t ldb = static_cast<uint64_t>(io.ld_x) * 2;
       cuuint64_t dims[4] = {static_cast<cuuint64_t>(l.c_in), static_cast<cuuint64_t>(io.n_img),
                             static_cast<cuuint64_t>(l.in.w), static_cast<cuuint64_t>(l.in.h)};
       cuuint64_t strides[3] = {ldb * l.in.w * l.in.h, ldb, ldb * l.in.w};
-      cuuint32_t box[4] = {8u, 8u, static_cast<cuuint32_t>(W + 2), static_cast<cuuint32_t>(TR + 2)};
+      cuuint32_t box[4] = {static_cast<cuuint32_t>(CX), static_cast<cuuint32_t>(G), static_cast<cuuint32_t>(TW + 2),
+                           static_cast<cuuint32_t>(TRu + 2)};
       cuuint32_t estr[4] = {1u, 1u, 1u, 1u};
+      const CUtensorMapSwizzle sw = CX == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                    : CX == 16 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE;
       CUresult r = get_encode_fn()(&xm, CU_TENSOR_MAP_DATA_TYPE_UINT16, 4, const_cast<void*>(io.x), dims, strides,
-                                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
       if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (convw) failed (" + std::to_string(r) + ")");
-      const size_t smem = convw_smem_bytes(BNw, WR, SA, SB, SX, ts.bytes, zp);
+      const size_t smem = convw_smem_bytes(BNw, WR, CX, SA, SB, SX, ts.bytes, zp);
       if (e->opt.record_plan)
         e->plan_add("convw", pl.layer_index, p.epi, p.res_kind, p.out_lv != nullptr, p.N, BNw, 1, zp ? 1 : 0);
       ck(launch_convw(zp ? 1 : 0, xm, p, smem, st), "convw launch");  // MODE_ZP / MODE_PLAIN
@@ -3127,6 +3155,11 @@ kan_status kan_engine_set_option(kan_engine* e, int option, int64_t value) {
       case KAN_OPT_NO_CONV3: o.no_conv3 = value != 0; break;
       case KAN_OPT_NO_CONVW: o.no_convw = value != 0; break;
       case KAN_OPT_CONVW_RINGS: o.convw_rings = v; break;
+      case KAN_OPT_CONVW_TR: o.convw_tr = v; break;
+      case KAN_OPT_CONVW_MC:
+        if (v < 0 || v > 4 || v == 3) throw InvalidArgument("KAN_OPT_CONVW_MC: 0 (auto), 1, 2 or 4");
+        o.convw_mc = v;
+        break;
       case KAN_OPT_NO_IM2COL: o.no_im2col = value != 0; break;
       case KAN_OPT_FORCE_BN: o.force_bn = v; break;
       case KAN_OPT_TABLES:

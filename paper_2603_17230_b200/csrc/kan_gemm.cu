@@ -126,21 +126,29 @@ __device__ __noinline__ double ddiv_rn_slow(double a, double b) { return __ddiv_
 __device__ __forceinline__ int level_mul(double y, double lo, double hi_open, double inv_step, int L, bool& tie) {
   double t = (y < lo) ? lo : y;
   t = (hi_open < t) ? hi_open : t;
-  const double u = __dadd_rn(__dmul_rn(__dsub_rn(t, lo), inv_step), 0.5);
-  int a = __double2int_rz(u);
-  const double f = __dsub_rn(u, static_cast<double>(a));
-  tie = (f < 1e-7) || (f > 1.0 - 1e-7);
-  a = a < 0 ? 0 : a;  // NaN converts to INT_MIN: level 0, as llround's INT64_MIN clamps
+  const double q = __dmul_rn(__dsub_rn(t, lo), inv_step);  // in [0, L + 1) (or NaN)
+  // round q to the nearest integer by the 2^52 shift (no conversion unit):
+  // the integer sits in the low word; it is llround(q) unless q is a tie, and
+  // ties lie in the band |q - rint(q)| > 0.5 - 1e-7 that is redone exactly.
+  // NaN leaves a zero low word: level 0, as llround's INT64_MIN clamps.
+  const double m = __dadd_rn(q, 4503599627370496.0);
+  const int a = __double2loint(m);
+  tie = fabs(__dsub_rn(q, __dsub_rn(m, 4503599627370496.0))) > 0.5 - 1e-7;
   return a > L ? L : a;
 }
-// Branch-free part of lattice_level_tie: rint of the fp32 estimate, plus
-// whether it lies near a rounding tie (then the threshold test decides).
+// Branch-free part of lattice_level_tie: the fp32 estimate rounded to the
+// nearest integer by the 1.5 * 2^23 shift, plus whether it lies near a
+// rounding tie (then the threshold test decides).
 __device__ __forceinline__ int level_tie_est(float x, float inv_step, float nlo_step, int L, bool& tie) {
   float t = fmaf(x, inv_step, nlo_step);
-  t = fminf(fmaxf(t, 0.0f), static_cast<float>(L));
-  const float tr = rintf(t);
-  tie = fabsf(fabsf(t - tr) - 0.5f) < 2e-3f;
-  return static_cast<int>(tr);
+  t = fminf(fmaxf(t, 0.0f), static_cast<float>(L));  // NaN -> 0
+  const float m = __fadd_rn(t, 12582912.0f);
+  tie = fabsf(fabsf(__fsub_rn(t, __fsub_rn(m, 12582912.0f))) - 0.5f) < 2e-3f;
+  return __float_as_int(m) - 0x4B400000;
+}
+// exact int32 -> fp64 without the conversion unit (2^52 + 2^31 shift)
+__device__ __forceinline__ double i32_to_f64(uint32_t v) {
+  return __dsub_rn(__hiloint2double(0x43300000, static_cast<int>(v ^ 0x80000000u)), 4503601774854144.0);
 }
 
 // out-of-line tie fix-ups (rare; kept out of the epilogues' hot code)
@@ -1116,7 +1124,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                       [&](int e8) {
                         const int e = 8 * hh + e8;
                         double y = __dmul_rn(
-                            __dsub_rn(static_cast<double>(static_cast<int32_t>(r16[e])), s_cols[BN + cl + e]), s_cols[cl + e]);
+                            __dsub_rn(i32_to_f64(r16[e]), s_cols[BN + cl + e]), s_cols[cl + e]);
                         if constexpr (FE == 3) y = __dadd_rn(y, static_cast<double>((&rv4[e >> 2].x)[e & 3]));
                         return y;
                       },
@@ -1160,7 +1168,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 float f[16];
 #pragma unroll
                 for (int e = 0; e < 16; ++e) {
-                  const double v = __dsub_rn(static_cast<double>(static_cast<int32_t>(r16[e])), s_cols[BN + cl + e]);
+                  const double v = __dsub_rn(i32_to_f64(r16[e]), s_cols[BN + cl + e]);
                   f[e] = __double2float_rn(__dmul_rn(v, s_cols[cl + e]));
                 }
 #pragma unroll
@@ -1207,7 +1215,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 float f[16];
 #pragma unroll
                 for (int e = 0; e < 16; ++e) {
-                  const double v = __dsub_rn(static_cast<double>(static_cast<int32_t>(r16[e])), s_cols[BN + cl + e]);
+                  const double v = __dsub_rn(i32_to_f64(r16[e]), s_cols[BN + cl + e]);
                   f[e] = __double2float_rn(__dmul_rn(v, s_cols[cl + e]));
                 }
                 float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) +

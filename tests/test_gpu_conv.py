@@ -224,6 +224,9 @@ CONVW_CASES = [
     (32, 16, 16, 256, W_PER_CHANNEL_SYM, 8),   # BN 256, one output row per tile
     (16, 16, 16, 40, W_PER_TENSOR_ASYM, 11),   # ragged 16-column group
     (8, 16, 16, 300, W_PER_CHANNEL_SYM, 3),    # two N tiles, the second ragged
+    (32, 8, 8, 256, W_PER_TENSOR_ASYM, 20),    # 8-wide maps: 16 images per tile, partial group
+    (64, 4, 4, 512, W_PER_CHANNEL_SYM, 40),    # 4-wide maps: 32 images per tile, two N tiles
+    (16, 8, 8, 24, W_PER_TENSOR_ASYM, 5),      # 8-wide, one partial group, ragged N
 ]
 
 
@@ -248,10 +251,11 @@ def test_convw_kernel_bit_exact(oracle, C, H, W, co, ws, batch):
 
 @pytest.mark.parametrize("ws", [W_PER_TENSOR_ASYM, W_PER_CHANNEL_SYM])
 def test_convw_in_residual_stages_bit_exact(oracle, ws):
-    """Reduced-width ResKAN18 at 32x32 without the SiLU term: the stage-1/2
-    stride-1 convs take kan_convw (levels out; fp32 + residual + levels
-    sidecar out; residual then levels), batch 21 (a partial image group)."""
-    layers = configs.reskan18_layers(width=(16, 32), n_classes=10, in_ch=3)
+    """Reduced-width ResKAN18 (all four stages: 32/16/8/4-wide maps) at
+    32x32 without the SiLU term: the stride-1 convs take kan_convw (levels
+    out; fp32 + residual + levels sidecar out; residual then levels), batch 21
+    (partial image groups of 8, 16 and 32)."""
+    layers = configs.reskan18_layers(width=(8, 16, 32, 64), n_classes=10, in_ch=3)
     desc = {"name": "r", "grid": {"intervals": 5, "degree": 3}, "input": [3, 32, 32],
             "conv_output": "floor", "layers": layers}
     Ws, Bs = weights_for(desc, seed=23, silu=False)
@@ -260,7 +264,7 @@ def test_convw_in_residual_stages_bit_exact(oracle, ws):
     e = build(desc, Ws, Bs, **opts)
     e.set_option("record_plan", 1)
     y = e.model_forward(to_dev(x)).cpu().numpy()
-    assert e.last_plan.count("convw") >= 6
+    assert e.last_plan.count("convw") >= 12
     yg = build(desc, Ws, Bs, engine_options={"no_convw": 1}, **opts).model_forward(to_dev(x)).cpu().numpy()
     np.testing.assert_array_equal(y, yg)
     yo = oracle.int_model_forward(desc, Ws, Bs, x, 8, 3, ws, 8)
