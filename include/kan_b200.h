@@ -247,7 +247,8 @@ typedef enum {
   KAN_OPT_NO_CONVW = 15,          /* 1: 3x3 s1 convs skip the window-shared kan_convw kernel */
   KAN_OPT_CONVW_RINGS = 16,       /* kan_convw ring depths SA*100 + SB*10 + SX (0 = automatic) */
   KAN_OPT_CONVW_TR = 17,          /* kan_convw output rows per tile cap (0 = automatic) */
-  KAN_OPT_CONVW_MC = 18           /* kan_convw CTAs per weight-multicast cluster: 1, 2, 4 (0 = automatic) */
+  KAN_OPT_CONVW_MC = 18,          /* kan_convw CTAs per weight-multicast cluster: 1, 2, 4 (0 = automatic) */
+  KAN_OPT_CONVW_BN = 19           /* kan_convw N tile cap, multiple of 16 (0 = automatic, 128) */
 } kan_option;
 kan_status kan_engine_set_option(kan_engine* e, int option, int64_t value);
 /* The launch plan of the most recent forward when KAN_OPT_RECORD_PLAN is on:

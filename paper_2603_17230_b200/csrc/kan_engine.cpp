@@ -360,7 +360,7 @@ struct kan_engine {
   // into the fields above, so nothing is read from the environment
   struct Options {
     bool no_convw = false;
-    int convw_rings = 0, convw_tr = 0, convw_mc = 0;
+    int convw_rings = 0, convw_tr = 0, convw_mc = 0, convw_bn = 0;
     bool no_conv3 = false, no_im2col = false, epi_stage = true, lv_sidecar = true, st_prepass = true;
     bool timeline = false, force_nacc1 = false, record_plan = false;
     int force_bn = 0, tables = -1, conv3_mc = 2, st_slices = 0, dbg_flags = 0;
@@ -918,7 +918,10 @@ void prepare_gemm_layer(kan_engine* e, const Layer& l, PreparedLayer& pl, bool b
   if (!bf16 && l.type == L_CONV && !l.im2col && l.kernel == 3 && l.stride == 1 && l.padding == 1 && nbp == 8 &&
       !pl.silu && !e->opt.no_convw && l.c_in % 8 == 0 && (tw == 16 || tw == 8 || tw == 4) && l.out.w % tw == 0 &&
       l.out.h == l.in.h && l.out.w == l.in.w) {
-    const int bnw = N <= 256 ? (N + 15) / 16 * 16 : 256;
+    // N tile: 128 columns at most by default (two MMA-rate N = 128 tiles per
+    // 256 channels keep the weight slots small enough for a 4-deep A ring)
+    const int bn_cap = e->opt.convw_bn > 0 ? e->opt.convw_bn : 128;
+    const int bnw = std::min((N + 15) / 16 * 16, bn_cap);
     const int gimg = 128 / tw;
     // output rows per tile: as many accumulators (one per row) as TMEM double-
     // buffers and the producers' window rows allow, dividing the map height
@@ -3156,6 +3159,10 @@ kan_status kan_engine_set_option(kan_engine* e, int option, int64_t value) {
       case KAN_OPT_NO_CONVW: o.no_convw = value != 0; break;
       case KAN_OPT_CONVW_RINGS: o.convw_rings = v; break;
       case KAN_OPT_CONVW_TR: o.convw_tr = v; break;
+      case KAN_OPT_CONVW_BN:
+        if (v != 0 && (v < 16 || v > 256 || v % 16)) throw InvalidArgument("KAN_OPT_CONVW_BN: 0 or a multiple of 16 in 16..256");
+        o.convw_bn = v;
+        break;
       case KAN_OPT_CONVW_MC:
         if (v < 0 || v > 4 || v == 3) throw InvalidArgument("KAN_OPT_CONVW_MC: 0 (auto), 1, 2 or 4");
         o.convw_mc = v;
