@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(CONVW_THREADS, 1)
       if (!tl.valid) continue;
       for (int kp = 0; kp < n_kb / KPX; ++kp, rx.next()) {
         mbar_wait(bar_xempty(rx.slot), rx.phase ^ 1);
-        if (lane == 0 && KAN_DBG(p, 4)) {  // tuning only: no activation loads (stale window)
+        if (lane == 0 && KAN_DBG(p, 128)) {  // tuning only (flag 128): no activation loads (stale window)
           mbar_arrive(bar_xfull(rx.slot));
         } else if (lane == 0) {
           mbar_arrive_tx(bar_xfull(rx.slot), static_cast<uint32_t>(WR) * x_row);
@@ -215,16 +215,14 @@ __global__ void __launch_bounds__(CONVW_THREADS, 1)
   } else if (warp == W_MMA) {
     // ============ MMA issuer: 9 taps x NACC accumulators per K block ============
     const uint32_t idesc = idesc_i8(BN, p.b_signed != 0);
-    // descriptor start addresses advance in 16-byte units: one window row
-    // (32 B) is 2 units.  Row offsets of each accumulator's first pixel and of
-    // each tap, computed once (no divisions in the issue loop: at N = 64 a
-    // K block is 36 MMAs of ~34 tensor cycles each, so the loop must be short)
-    uint32_t acc_row[8], tap_row[9];
-#pragma unroll
-    for (int a = 0; a < 8; ++a) acc_row[a] = static_cast<uint32_t>(a * WP * G * 2);  // accumulator a = band row a
-#pragma unroll
-    for (int tap = 0; tap < 9; ++tap) tap_row[tap] = static_cast<uint32_t>(((tap / 3) * WP + tap % 3) * G * 2);
-    const uint64_t b_tap = static_cast<uint64_t>(BN) * 2u;  // one tap's weight tile (BN x 32 B) in 16-byte units
+    // Descriptor start addresses advance in 16-byte units: one window row
+    // (32 B) is 2 units, and a start address below 256 KB never carries out of
+    // the low word, so the issue loop moves 32-bit low words only.  Per K
+    // block: NACC accumulators (runtime loop) x 9 taps (unrolled, the taps'
+    // row offsets are compile-time constants).
+    const uint32_t d_hi = static_cast<uint32_t>(umma_desc_sw32(0u) >> 32);
+    const uint32_t acc_step = static_cast<uint32_t>(WP * G * 2);  // next accumulator = next band row
+    const uint32_t b_tap = static_cast<uint32_t>(BN) * 2u;        // one tap's weight tile (BN x 32 B)
     Ring ra(SA), rb(SB);
     auto release_b = [&](uint32_t bar) {
       if (MC == 1)
@@ -250,20 +248,28 @@ __global__ void __launch_bounds__(CONVW_THREADS, 1)
         mbar_wait_warp(bar_afull(ra.slot), ra.phase);
         mbar_wait_warp(bar_bfull(rb.slot), rb.phase);
         tc_fence_after();
-        const uint64_t ad0 = umma_desc_sw32(smem_u32(sA + static_cast<size_t>(ra.slot) * a_bytes));
-        const uint64_t bd0 = umma_desc_sw32(smem_u32(sB + static_cast<size_t>(rb.slot) * b_slot));
+        const uint32_t a_lo = static_cast<uint32_t>(umma_desc_sw32(smem_u32(sA + static_cast<size_t>(ra.slot) * a_bytes)));
+        const uint32_t b_lo = static_cast<uint32_t>(umma_desc_sw32(smem_u32(sB + static_cast<size_t>(rb.slot) * b_slot)));
         if (elect_one()) {
+          if (!KAN_DBG(p, 2)) {  // (tuning only: flag 2 skips the MMAs)
+            for (int a = 0; a < NACC; ++a) {
+              const uint32_t arow = a_lo + static_cast<uint32_t>(a) * acc_step;
+              const uint32_t d = dacc + static_cast<uint32_t>(a * BN);
 #pragma unroll
-          for (int tap = 0; tap < 9; ++tap) {
-            const uint64_t bd = bd0 + static_cast<uint64_t>(tap) * b_tap;
-            const uint32_t acc = (kb | tap) != 0 ? 1u : 0u;
-#pragma unroll
-            for (int a = 0; a < 8; ++a)
-              if (a < NACC && !KAN_DBG(p, 2))  // (tuning only: flag 2 skips the MMAs)
-                mma_i8(dacc + static_cast<uint32_t>(a * BN), ad0 + (acc_row[a] + tap_row[tap]), bd, idesc, acc);
+              for (int tap = 0; tap < 9; ++tap) {
+                constexpr int TR9[9] = {0, 1, 2, WP, WP + 1, WP + 2, 2 * WP, 2 * WP + 1, 2 * WP + 2};
+                mma_i8_lh(d, arow + static_cast<uint32_t>(TR9[tap] * G * 2), d_hi, b_lo + static_cast<uint32_t>(tap) * b_tap,
+                          d_hi, idesc, (kb | tap) != 0 ? 1u : 0u);
+              }
+            }
           }
-          tc_commit(bar_aempty(ra.slot));
-          release_b(bar_bempty(rb.slot));
+          if (KAN_DBG(p, 512)) {  // (tuning only: plain arrivals instead of commits, no MMAs in flight)
+            mbar_arrive(bar_aempty(ra.slot));
+            mbar_arrive(bar_bempty(rb.slot));
+          } else {
+            tc_commit(bar_aempty(ra.slot));
+            release_b(bar_bempty(rb.slot));
+          }
         }
         __syncwarp();
       }
@@ -306,7 +312,7 @@ __global__ void __launch_bounds__(CONVW_THREADS, 1)
 #pragma unroll
         for (int q = 0; q < RPT; ++q) {
           const int r = tid + q * NP;
-          if (r < WR) {
+          if (r < WR && !KAN_DBG(p, 256)) {  // (tuning only: flag 256 skips the expansion)
             const uint32_t ur = static_cast<uint32_t>(r);
             const uint32_t sw = CX == 32 ? ((ur >> 1) & 3u) : (CX == 16 ? ((ur >> 2) & 1u) : 0u);
             const uint2 lv = *reinterpret_cast<const uint2*>(xt + ur * x_row + ((chunk ^ sw) << 4) + off8);
@@ -314,7 +320,8 @@ __global__ void __launch_bounds__(CONVW_THREADS, 1)
             uint32_t w[8];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              const uint32_t a = pad[q] ? static_cast<uint32_t>(p.lvl0) : ((lw[e >> 1] >> (16 * (e & 1))) & 0xFFFFu);
+              uint32_t a = pad[q] ? static_cast<uint32_t>(p.lvl0) : ((lw[e >> 1] >> (16 * (e & 1))) & 0xFFFFu);
+              if (KAN_DBG(p, 128)) a &= 1023u;  // (tuning only: stale windows hold garbage levels)
               const uint2 c = c64[KAN_DBG(p, 64) ? lane : a];  // (tuning only: flag 64 = conflict-free fake lookups)
               w[2 * e] = c.x;
               w[2 * e + 1] = c.y;
@@ -327,7 +334,7 @@ __global__ void __launch_bounds__(CONVW_THREADS, 1)
             *reinterpret_cast<uint4*>(d + ((sa ^ 1u) << 4)) = make_uint4(w[4], w[5], w[6], w[7]);
           }
         }
-        fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
+        if (!KAN_DBG(p, 1024)) fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
         __syncwarp();
         if (lane == 0) {
           if (xh == KPX - 1) mbar_arrive(bar_xempty(rx.slot));
