@@ -1089,6 +1089,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         }
         const uint32_t tacc = t_row + static_cast<uint32_t>(ab) * BNa;
         const int row = tl.m0 + rloc;
+        // the straight-line paths' fp64 value of accumulator r of tile column c:
+        // (acc - corr_c) * fs_c, or with the reference's zero point (acc - z_w *
+        // rowsum) * f -- finish4's arithmetic (the subtractions are exact in fp64)
+        const double zc_row = MODE == MODE_ZP ? static_cast<double>(p.z_w * static_cast<long long>(rs)) : 0.0;
+        auto ycol = [&](uint32_t r, int c) -> double {
+          if constexpr (MODE == MODE_ZP)
+            return __dmul_rn(__dsub_rn(i32_to_f64(r), zc_row), p.f_tensor);
+          else
+            return __dmul_rn(__dsub_rn(i32_to_f64(r), s_cols[BN + c]), s_cols[c]);
+        };
         float rv[32];  // residual prefetch: 32 columns in flight per thread
         const int ng = KAN_DBG(p, 8) ? 0 : ngroups;  // tuning only: skip the epilogue math
         // 16 columns per TMEM load (BN is a multiple of 16); the two warps of
@@ -1123,8 +1133,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                   levels8_f64(
                       [&](int e8) {
                         const int e = 8 * hh + e8;
-                        double y = __dmul_rn(
-                            __dsub_rn(i32_to_f64(r16[e]), s_cols[BN + cl + e]), s_cols[cl + e]);
+                        double y = ycol(r16[e], cl + e);
                         if constexpr (FE == 3) y = __dadd_rn(y, static_cast<double>((&rv4[e >> 2].x)[e & 3]));
                         return y;
                       },
@@ -1167,10 +1176,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 uint8_t* sg = smem + f_off + static_cast<uint32_t>(warp - W_EPI) * (32u * GEMM_STG_PITCH);
                 float f[16];
 #pragma unroll
-                for (int e = 0; e < 16; ++e) {
-                  const double v = __dsub_rn(i32_to_f64(r16[e]), s_cols[BN + cl + e]);
-                  f[e] = __double2float_rn(__dmul_rn(v, s_cols[cl + e]));
-                }
+                for (int e = 0; e < 16; ++e) f[e] = __double2float_rn(ycol(r16[e], cl + e));
 #pragma unroll
                 for (int q = 0; q < 4; ++q)
                   *reinterpret_cast<float4*>(sg + lane * GEMM_STG_PITCH + q * 16) =
@@ -1214,10 +1220,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 const int cl = g16 * 16;
                 float f[16];
 #pragma unroll
-                for (int e = 0; e < 16; ++e) {
-                  const double v = __dsub_rn(i32_to_f64(r16[e]), s_cols[BN + cl + e]);
-                  f[e] = __double2float_rn(__dmul_rn(v, s_cols[cl + e]));
-                }
+                for (int e = 0; e < 16; ++e) f[e] = __double2float_rn(ycol(r16[e], cl + e));
                 float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) +
                                                       static_cast<size_t>(row) * p.ld_out + n0 + cl);
 #pragma unroll
@@ -1524,6 +1527,15 @@ cudaError_t launch_gather_gemm(bool bf16, int nbp, int mode, const CUtensorMap& 
                                                                       : 0;
   switch (mode) {
     case MODE_ZP:
+      if (fe == 1)
+        return nbp == 8 ? launch_impl<false, 8, MODE_ZP, 1>(xmap, p, smem, st)
+                        : launch_impl<false, 16, MODE_ZP, 1>(xmap, p, smem, st);
+      if (fe == 2)
+        return nbp == 8 ? launch_impl<false, 8, MODE_ZP, 2>(xmap, p, smem, st)
+                        : launch_impl<false, 16, MODE_ZP, 2>(xmap, p, smem, st);
+      if (fe == 3)
+        return nbp == 8 ? launch_impl<false, 8, MODE_ZP, 3>(xmap, p, smem, st)
+                        : launch_impl<false, 16, MODE_ZP, 3>(xmap, p, smem, st);
       return nbp == 8 ? launch_impl<false, 8, MODE_ZP>(xmap, p, smem, st)
                       : launch_impl<false, 16, MODE_ZP>(xmap, p, smem, st);
     case MODE_SILU:
