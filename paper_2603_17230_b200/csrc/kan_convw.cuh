@@ -167,6 +167,18 @@ __global__ void __launch_bounds__(CONVW_THREADS, 1)
     for (int u = unit0; u < n_units; u += unit_step) {
       const Tile tl = tile_of(u);
       if (!tl.valid) continue;
+      if (p.res_kind) {
+        // the tile's residual rows into L2 now, so the epilogue (a whole tile
+        // of MMAs later) reads them from L2 instead of HBM: one contiguous TW-
+        // pixel NHWC segment per (image, output row)
+        for (int i = lane; i < G * TR; i += 32) {
+          const int img = tl.g * G + i % G, oy = tl.oy0 + i / G;
+          if (img < p.M)
+            bulk_prefetch_l2(
+                reinterpret_cast<const float*>(p.res) + ((static_cast<size_t>(img) * H + oy) * W + tl.x0) * p.ld_res,
+                static_cast<uint32_t>(TW * p.ld_res * 4));
+        }
+      }
       for (int kp = 0; kp < n_kb / KPX; ++kp, rx.next()) {
         mbar_wait(bar_xempty(rx.slot), rx.phase ^ 1);
         if (lane == 0 && KAN_DBG(p, 128)) {  // tuning only (flag 128): no activation loads (stale window)
