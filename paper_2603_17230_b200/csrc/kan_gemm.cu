@@ -1905,6 +1905,12 @@ cudaError_t launch_rows_to_levels(const float* x, int64_t M, int n, int ld_x, ui
 // row per output pixel (n, oy, ox), columns in the reference's channel-major
 // order c*K*K + ky*K + kx (layers.hpp:140-149), padded taps at level(0.0).
 // The layer then runs as a dense (c_in*K*K)-input GEMM.
+// One thread per output pixel: its whole patch row (channel-major, then ky,
+// kx: im2col's column order, layers.hpp:140-149) as lattice levels, written
+// as 16-byte chunks of the pitch-ld_o row; columns past the patch hold level 0
+// (their weights are zero and the zero-point row sums skip them).  Index math
+// per row, not per element (the earlier per-element 64-bit divisions made
+// this 1.8 ms on C5's stem).
 __global__ void __launch_bounds__(256) kan_im2col_levels_kernel(const float* __restrict__ x, int64_t n_img, int C,
                                                                 int H, int W, int K, int stride, int pad, int Ho,
                                                                 int Wo, uint16_t* __restrict__ out, int ld_o,
@@ -1913,30 +1919,51 @@ __global__ void __launch_bounds__(256) kan_im2col_levels_kernel(const float* __r
   pdl_wait();
   pdl_trigger();
   const int ncol = C * K * K;
-  const int64_t total = n_img * Ho * Wo * ncol;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int col = static_cast<int>(i % ncol);
-    const int64_t r = i / ncol;  // output pixel row
-    const int ox = static_cast<int>(r % Wo);
-    const int oy = static_cast<int>((r / Wo) % Ho);
-    const int64_t n = r / (static_cast<int64_t>(Wo) * Ho);
-    const int c = col / (K * K), t = col - c * K * K;
-    const int ky = t / K, kx = t - ky * K;
-    const int iy = oy * stride + ky - pad, ix = ox * stride + kx - pad;
-    int a = lvl0;
-    if (static_cast<unsigned>(iy) < static_cast<unsigned>(H) && static_cast<unsigned>(ix) < static_cast<unsigned>(W))
-      a = lattice_level_tie(x[((n * C + c) * H + iy) * W + ix], inv_step, nlo_step, L, thr);
-    out[r * ld_o + col] = static_cast<uint16_t>(a);
+  const int hw_o = Ho * Wo;
+  const int64_t rows = n_img * hw_o;
+  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < rows;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t n = r / hw_o;
+    const int pix = static_cast<int>(r - n * hw_o);
+    const int oy = pix / Wo, ox = pix - (pix / Wo) * Wo;
+    const float* xn = x + n * C * H * W;
+    uint16_t* o = out + r * ld_o;
+    int c = 0, ky = 0, kx = 0;
+    for (int col0 = 0; col0 < ld_o; col0 += 8) {
+      uint32_t w[4];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        int a = 0;
+        if (col0 + q < ncol) {
+          const int iy = oy * stride + ky - pad, ix = ox * stride + kx - pad;
+          a = lvl0;
+          if (static_cast<unsigned>(iy) < static_cast<unsigned>(H) && static_cast<unsigned>(ix) < static_cast<unsigned>(W))
+            a = lattice_level_tie(xn[(c * H + iy) * W + ix], inv_step, nlo_step, L, thr);
+          if (++kx == K) {
+            kx = 0;
+            if (++ky == K) {
+              ky = 0;
+              ++c;
+            }
+          }
+        }
+        if (q & 1)
+          w[q >> 1] |= static_cast<uint32_t>(a) << 16;
+        else
+          w[q >> 1] = static_cast<uint32_t>(a);
+      }
+      *reinterpret_cast<uint4*>(o + col0) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
   }
 }
 
 cudaError_t launch_im2col_levels(const float* x, int64_t n_img, int C, int H, int W, int K, int stride, int pad,
                                  int Ho, int Wo, uint16_t* out, int ld_o, const float* thr, float nlo_step,
                                  float inv_step, int L, int lvl0, cudaStream_t st) {
-  const int64_t total = n_img * Ho * Wo * C * K * K;
-  if (total == 0) return cudaSuccess;
-  const int64_t nb = (total + 255) / 256;
+  const int64_t rows = n_img * Ho * Wo;
+  if (rows == 0) return cudaSuccess;
+  if (ld_o % 8 != 0) return cudaErrorInvalidValue;  // 16-byte row chunks (pitch16 rows)
+  const int64_t nb = (rows + 255) / 256;
   const unsigned blocks = static_cast<unsigned>(nb < 148 * 32 ? nb : 148 * 32);
   return launch_pdl(kan_im2col_levels_kernel, dim3(blocks), dim3(256), 0, st, x, n_img, C, H, W, K, stride, pad, Ho,
                     Wo, out, ld_o, thr, nlo_step, inv_step, L, lvl0);
