@@ -37,22 +37,29 @@
 // Warp roles as in kan_gather_gemm_kernel (12 producers here), activation TMA,
 // MMA issuer, weight loader, 8 epilogue warps (two per TMEM lane quarter).
 
-// 12 producer warps (the window expansion is cheap here), so the epilogue's
-// 16-column fp64 chains get more registers than the 27-warp gather kernel's
-constexpr int CONVW_PRODUCER_WARPS = 12;
-constexpr int CONVW_THREADS = 32 * (CONVW_PRODUCER_WARPS + 3 + GEMM_EPI_WARPS);
-constexpr int CONVW_MAX_ROWS = 3 * 32 * CONVW_PRODUCER_WARPS;  // window rows: RPT rows per producer thread
+// Warp counts per output kind: the level epilogue (branch-free fp64 chains,
+// no fp32 staging) runs on 16 warps next to 8 producers; the fp32 + sidecar
+// epilogue needs more registers per thread, so it keeps 8 warps and 12
+// producers (measured: 16 epilogue warps make the levels layers 5-13 % faster
+// and the fp32 ones 4-14 % slower).  Window rows per producer thread (RPT)
+// bound the window at CONVW_MAX_ROWS rows either way.
+template <int OUT>
+struct ConvwWarps {
+  static constexpr int PW = OUT == EPI_LEVEL ? 8 : 12;
+  static constexpr int EW = OUT == EPI_LEVEL ? 16 : 8;  // a multiple of 4 (TMEM lane quarters)
+  static constexpr int RPT = OUT == EPI_LEVEL ? 4 : 3;
+  static constexpr int THREADS = 32 * (PW + 3 + EW);
+};
+constexpr int CONVW_MAX_ROWS = 1024;  // <= RPT * 32 * PW for both kinds
 
-// OUT: the epilogue's output, EPI_LEVEL (next-layer levels) or EPI_F32
-// (fp32 rows + levels sidecar); a separate instantiation each keeps the code
-// small enough for the instruction cache.
 template <int MODE, int OUT, int LG>
-__global__ void __launch_bounds__(CONVW_THREADS, 1)
+__global__ void __launch_bounds__(ConvwWarps<OUT>::THREADS, 1)
     kan_convw_kernel(const __grid_constant__ CUtensorMap xmap, const GemmParams p) {
-  constexpr int NPW = CONVW_PRODUCER_WARPS, NP = 32 * NPW;
+  constexpr int CONVW_EPI_WARPS = ConvwWarps<OUT>::EW;
+  constexpr int NPW = ConvwWarps<OUT>::PW, NP = 32 * NPW;
   constexpr int W_X = NPW, W_MMA = NPW + 1, W_B = NPW + 2, W_EPI = NPW + 3;
   constexpr bool ZP = (MODE == MODE_ZP);
-  constexpr int RPT = CONVW_MAX_ROWS / NP;  // window rows per producer thread (max)
+  constexpr int RPT = ConvwWarps<OUT>::RPT;  // window rows per producer thread (max)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
 
@@ -145,9 +152,9 @@ __global__ void __launch_bounds__(CONVW_THREADS, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(bar_accfull(b), 1);
-      mbar_init(bar_accempty(b), GEMM_EPI_WARPS);
+      mbar_init(bar_accempty(b), CONVW_EPI_WARPS);
       mbar_init(bar_wsfull(b), NPW);
-      mbar_init(bar_wsempty(b), GEMM_EPI_WARPS);
+      mbar_init(bar_wsempty(b), CONVW_EPI_WARPS);
     }
     mbar_init(bar_tab, 1);
     mbar_fence_init();
@@ -373,7 +380,8 @@ __global__ void __launch_bounds__(CONVW_THREADS, 1)
     if (tab_bytes > 0) mbar_wait(bar_tab, 0);
     const float* thr = reinterpret_cast<const float*>(sT + p.off_thr);
     const int wq = warp & 3;             // TMEM lane quarter
-    const int half = (warp - W_EPI) >> 2;  // alternate 16-column groups
+    constexpr int EQ = CONVW_EPI_WARPS / 4;  // warps per TMEM lane quarter
+    const int half = (warp - W_EPI) >> 2;  // this warp's 16-column groups: half, half + EQ, ...
     const int rloc = wq * 32 + lane;     // row within an accumulator
     const int img_l = rloc & (G - 1), pl_ = rloc >> lg;
     const uint32_t t_row = tmem + (static_cast<uint32_t>(wq * 32) << 16);
@@ -385,9 +393,9 @@ __global__ void __launch_bounds__(CONVW_THREADS, 1)
       if (!tl.valid) continue;
       const int ab = lt & 1;
       if (!ZP && tl.nt != staged_nt) {  // per-column scales (restaged when the N tile changes)
-        asm volatile("bar.sync 5, %0;" ::"r"(32 * GEMM_EPI_WARPS) : "memory");
-        for (int i = et; i < BN; i += 32 * GEMM_EPI_WARPS) s_cols[i] = p.fs[min(tl.nt * BN + i, p.N - 1)];
-        asm volatile("bar.sync 5, %0;" ::"r"(32 * GEMM_EPI_WARPS) : "memory");
+        asm volatile("bar.sync 5, %0;" ::"r"(32 * CONVW_EPI_WARPS) : "memory");
+        for (int i = et; i < BN; i += 32 * CONVW_EPI_WARPS) s_cols[i] = p.fs[min(tl.nt * BN + i, p.N - 1)];
+        asm volatile("bar.sync 5, %0;" ::"r"(32 * CONVW_EPI_WARPS) : "memory");
         staged_nt = tl.nt;
       }
       mbar_wait(bar_accfull(ab), (lt >> 1) & 1);
@@ -412,12 +420,12 @@ __global__ void __launch_bounds__(CONVW_THREADS, 1)
         }
         const uint32_t tacc = t_row + static_cast<uint32_t>(ab) * 256u + static_cast<uint32_t>(a * BN);
 #pragma unroll 1
-        for (int cl = half * 16; cl < (KAN_DBG(p, 8) ? 0 : BN); cl += 32) {  // (tuning: flag 8 skips the epilogue)
+        for (int cl = half * 16; cl < (KAN_DBG(p, 8) ? 0 : BN); cl += 16 * EQ) {  // (tuning: flag 8 skips the epilogue)
           const bool full = n0 + cl + 16 <= p.N;
           if (p.res_kind && valid) {
             // pull the NEXT group's residual segment into L1 while this one is processed
             size_t nrow = orow;
-            int ncl = cl + 32;
+            int ncl = cl + 16 * EQ;
             if (ncl >= BN && a + 1 < NACC) {
               nrow = orow + static_cast<size_t>(W);  // the next band row, same pixel
               ncl = half * 16;
@@ -524,6 +532,8 @@ __global__ void __launch_bounds__(CONVW_THREADS, 1)
   }
 }
 
+int convw_max_rows() { return CONVW_MAX_ROWS; }
+
 size_t convw_smem_bytes(int BN, int WR, int CX, int SA, int SB, int SX, int tab_bytes, bool zp) {
   const size_t b = static_cast<size_t>(9) * BN * 32;
   const size_t x = (static_cast<size_t>(WR) * CX * 2 + 1023) / 1024 * 1024;
@@ -536,13 +546,14 @@ cudaError_t launch_convw(int mode, const CUtensorMap& xmap, const GemmParams& p,
   static std::atomic<unsigned long long> optin[12];
   auto go = [&](auto kfn, int v) -> cudaError_t {
     if (cudaError_t e = smem_optin(kfn, optin[v]); e != cudaSuccess) return e;
+    const int threads = (v & 1) ? ConvwWarps<EPI_LEVEL>::THREADS : ConvwWarps<EPI_F32>::THREADS;  // odd v: levels out
     const int n_sm = device_sm_count();
     const int mc = p.mc > 1 ? p.mc : 1;
     const int units = ((p.M + p.bn_img - 1) / p.bn_img + mc - 1) / mc * (p.H / p.bh) * (p.W / p.Wo) * p.n_tiles_n;
     const int clusters = units < n_sm / mc ? units : n_sm / mc;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(clusters * mc));
-    cfg.blockDim = dim3(CONVW_THREADS);
+    cfg.blockDim = dim3(static_cast<unsigned>(threads));
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[2];

@@ -54,6 +54,7 @@ cudaError_t launch_conv3(int mode, const CUtensorMap& xmap, const GemmParams& p,
 size_t conv3_smem_bytes(int BN, int R, int SA, int SB, int SX, int x_kind, int tab_bytes, bool silu);
 cudaError_t launch_convw(int mode, const CUtensorMap& xmap, const GemmParams& p, size_t smem, cudaStream_t st);
 size_t convw_smem_bytes(int BN, int WR, int CX, int SA, int SB, int SX, int tab_bytes, bool zp);
+int convw_max_rows();
 size_t small_smem_bytes(const SmallParams& p);
 cudaError_t launch_im2col_levels(const float* x, int64_t n_img, int C, int H, int W, int K, int stride, int pad,
                                  int Ho, int Wo, uint16_t* out, int ld_o, const float* thr, float nlo_step,
@@ -927,7 +928,7 @@ void prepare_gemm_layer(kan_engine* e, const Layer& l, PreparedLayer& pl, bool b
     // buffers and the producers' window rows allow, dividing the map height
     int tr = 0;
     for (int t = 1; t <= 6; ++t)
-      if (t * bnw <= 256 && l.out.h % t == 0 && (t + 2) * (tw + 2) * gimg <= 1152) tr = t;  // CONVW_MAX_ROWS
+      if (t * bnw <= 256 && l.out.h % t == 0 && (t + 2) * (tw + 2) * gimg <= convw_max_rows()) tr = t;
     if (tr > 0) {
       pl.convw = true;
       pl.bnw = bnw;
