@@ -52,7 +52,9 @@ struct ConvwWarps {
 };
 constexpr int CONVW_MAX_ROWS = 1024;  // <= RPT * 32 * PW for both kinds
 
-template <int MODE, int OUT, int LG>
+// S: conv stride (1, or 2 for 16-wide outputs with G = 8: consecutive output
+// pixels are then every other window pixel, a core-matrix stride of 512 B).
+template <int MODE, int OUT, int LG, int S>
 __global__ void __launch_bounds__(ConvwWarps<OUT>::THREADS, 1)
     kan_convw_kernel(const __grid_constant__ CUtensorMap xmap, const GemmParams p) {
   constexpr int CONVW_EPI_WARPS = ConvwWarps<OUT>::EW;
@@ -65,9 +67,11 @@ __global__ void __launch_bounds__(ConvwWarps<OUT>::THREADS, 1)
 
   const int SA = p.SA, SB = p.SB, SX = p.SX;
   const int BN = p.BN;
-  const int W = p.W, H = p.H, TR = p.bh;
+  // input map H x W, output map Ho x Wo (= H x W at stride 1)
+  const int W = p.W, H = p.H, Ho = p.Ho, Wo = p.pimg, TR = p.bh;
   constexpr int G = 1 << LG;           // images per tile (8, 16, 32)
-  constexpr int TW = 128 / G, WP = TW + 2;  // tile width, window pitch in pixels
+  constexpr int TW = 128 / G;          // output columns per tile
+  constexpr int WP = (TW - 1) * S + 3;  // window pitch in input pixels
   constexpr int lg = LG;
   const int CX = p.cps;                // channels per activation load
   const int KPX = CX / 4;              // K blocks per activation load
@@ -103,7 +107,7 @@ __global__ void __launch_bounds__(ConvwWarps<OUT>::THREADS, 1)
   const int unit0 = MC > 1 ? static_cast<int>(cluster_id_x()) : static_cast<int>(blockIdx.x);
   const int unit_step = MC > 1 ? static_cast<int>(n_clusters_x()) : static_cast<int>(gridDim.x);
   const uint16_t mc_mask = static_cast<uint16_t>((1u << MC) - 1u);
-  const int bands = H / TR, cblocks = W / TW;
+  const int bands = Ho / TR, cblocks = Wo / TW;
   const int n_groups = (p.M + G - 1) / G;  // p.M = images
   const int n_units = (n_groups + MC - 1) / MC * bands * cblocks * p.n_tiles_n;
   struct Tile {
@@ -182,7 +186,7 @@ __global__ void __launch_bounds__(ConvwWarps<OUT>::THREADS, 1)
           const int img = tl.g * G + i % G, oy = tl.oy0 + i / G;
           if (img < p.M)
             bulk_prefetch_l2(
-                reinterpret_cast<const float*>(p.res) + ((static_cast<size_t>(img) * H + oy) * W + tl.x0) * p.ld_res,
+                reinterpret_cast<const float*>(p.res) + ((static_cast<size_t>(img) * Ho + oy) * Wo + tl.x0) * p.ld_res,
                 static_cast<uint32_t>(TW * p.ld_res * 4));
         }
       }
@@ -192,9 +196,10 @@ __global__ void __launch_bounds__(ConvwWarps<OUT>::THREADS, 1)
           mbar_arrive(bar_xfull(rx.slot));
         } else if (lane == 0) {
           mbar_arrive_tx(bar_xfull(rx.slot), static_cast<uint32_t>(WR) * x_row);
-          // box (CX channels, G images, TW+2 columns, TR+2 rows) from (c, img, x0-1, oy0-1)
-          tma_load_4d(smem_u32(sX + static_cast<size_t>(rx.slot) * x_bytes), &xmap, kp * CX, tl.g * G, tl.x0 - 1,
-                      tl.oy0 - 1, bar_xfull(rx.slot));
+          // box (CX channels, G images, WP columns, (TR-1)*S+3 rows) from
+          // (c, img, x0*S-1, oy0*S-1): every input pixel the tile's taps read
+          tma_load_4d(smem_u32(sX + static_cast<size_t>(rx.slot) * x_bytes), &xmap, kp * CX, tl.g * G, tl.x0 * S - 1,
+                      tl.oy0 * S - 1, bar_xfull(rx.slot));
         }
         __syncwarp();
       }
@@ -240,7 +245,8 @@ __global__ void __launch_bounds__(ConvwWarps<OUT>::THREADS, 1)
     // block: NACC accumulators (runtime loop) x 9 taps (unrolled, the taps'
     // row offsets are compile-time constants).
     const uint32_t d_hi = static_cast<uint32_t>(umma_desc_sw32(0u) >> 32);
-    const uint32_t acc_step = static_cast<uint32_t>(WP * G * 2);  // next accumulator = next band row
+    const uint32_t acc_step = static_cast<uint32_t>(S * WP * G * 2);  // next accumulator = next band row
+    const uint32_t a_hi = d_hi + static_cast<uint32_t>((S - 1) * (256 >> 4));  // A's core-matrix stride: S x 256 B
     const uint32_t b_tap = static_cast<uint32_t>(BN) * 2u;        // one tap's weight tile (BN x 32 B)
     Ring ra(SA), rb(SB);
     auto release_b = [&](uint32_t bar) {
@@ -277,7 +283,7 @@ __global__ void __launch_bounds__(ConvwWarps<OUT>::THREADS, 1)
 #pragma unroll
               for (int tap = 0; tap < 9; ++tap) {
                 constexpr int TR9[9] = {0, 1, 2, WP, WP + 1, WP + 2, 2 * WP, 2 * WP + 1, 2 * WP + 2};
-                mma_i8_lh(d, arow + static_cast<uint32_t>(TR9[tap] * G * 2), d_hi, b_lo + static_cast<uint32_t>(tap) * b_tap,
+                mma_i8_lh(d, arow + static_cast<uint32_t>(TR9[tap] * G * 2), a_hi, b_lo + static_cast<uint32_t>(tap) * b_tap,
                           d_hi, idesc, (kb | tap) != 0 ? 1u : 0u);
               }
             }
@@ -314,7 +320,7 @@ __global__ void __launch_bounds__(ConvwWarps<OUT>::THREADS, 1)
       for (int q = 0; q < RPT; ++q) {
         const int r = tid + q * NP;
         const int pix = r >> lg, wy = pix / WP, wx = pix - wy * WP;
-        const int iy = tl.oy0 - 1 + wy, ix = tl.x0 - 1 + wx;
+        const int iy = tl.oy0 * S - 1 + wy, ix = tl.x0 * S - 1 + wx;
         pad[q] = static_cast<unsigned>(iy) >= static_cast<unsigned>(H) || static_cast<unsigned>(ix) >= static_cast<unsigned>(W);
         rs[q] = 0u;
       }
@@ -409,13 +415,13 @@ __global__ void __launch_bounds__(ConvwWarps<OUT>::THREADS, 1)
       for (int a = 0; a < NACC; ++a) {
         const int py = a, px = pl_;  // accumulator a = band row a; its rows = TW pixels x G images
         const int oy = tl.oy0 + py;
-        const size_t orow = (static_cast<size_t>(img) * H + oy) * W + tl.x0 + px;  // NHWC row
+        const size_t orow = (static_cast<size_t>(img) * Ho + oy) * Wo + tl.x0 + px;  // NHWC row
         double zc = 0.0;
         if constexpr (ZP) {
           // the row's code sum: the 9 window rows its taps read (zero-point term)
           int s_ = 0;
 #pragma unroll
-          for (int tap = 0; tap < 9; ++tap) s_ += ws[(((py + tap / 3) * WP + px + tap % 3) << lg) + img_l];
+          for (int tap = 0; tap < 9; ++tap) s_ += ws[(((S * py + tap / 3) * WP + S * px + tap % 3) << lg) + img_l];
           zc = static_cast<double>(p.z_w * static_cast<long long>(s_));  // exact below 2^53
         }
         const uint32_t tacc = t_row + static_cast<uint32_t>(ab) * 256u + static_cast<uint32_t>(a * BN);
@@ -427,7 +433,7 @@ __global__ void __launch_bounds__(ConvwWarps<OUT>::THREADS, 1)
             size_t nrow = orow;
             int ncl = cl + 16 * EQ;
             if (ncl >= BN && a + 1 < NACC) {
-              nrow = orow + static_cast<size_t>(W);  // the next band row, same pixel
+              nrow = orow + static_cast<size_t>(Wo);  // the next band row, same pixel
               ncl = half * 16;
             }
             if (ncl < BN && n0 + ncl < p.N)
@@ -543,13 +549,13 @@ size_t convw_smem_bytes(int BN, int WR, int CX, int SA, int SB, int SX, int tab_
 }
 
 cudaError_t launch_convw(int mode, const CUtensorMap& xmap, const GemmParams& p, size_t smem, cudaStream_t st) {
-  static std::atomic<unsigned long long> optin[12];
+  static std::atomic<unsigned long long> optin[16];
   auto go = [&](auto kfn, int v) -> cudaError_t {
     if (cudaError_t e = smem_optin(kfn, optin[v]); e != cudaSuccess) return e;
     const int threads = (v & 1) ? ConvwWarps<EPI_LEVEL>::THREADS : ConvwWarps<EPI_F32>::THREADS;  // odd v: levels out
     const int n_sm = device_sm_count();
     const int mc = p.mc > 1 ? p.mc : 1;
-    const int units = ((p.M + p.bn_img - 1) / p.bn_img + mc - 1) / mc * (p.H / p.bh) * (p.W / p.Wo) * p.n_tiles_n;
+    const int units = ((p.M + p.bn_img - 1) / p.bn_img + mc - 1) / mc * (p.Ho / p.bh) * (p.pimg / p.Wo) * p.n_tiles_n;
     const int clusters = units < n_sm / mc ? units : n_sm / mc;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(clusters * mc));
@@ -568,14 +574,19 @@ cudaError_t launch_convw(int mode, const CUtensorMap& xmap, const GemmParams& p,
     return cudaLaunchKernelEx(&cfg, kfn, xmap, p);
   };
   const bool lvl = p.epi == EPI_LEVEL;
-  auto pick = [&](auto lgc) -> cudaError_t {
-    constexpr int LG = decltype(lgc)::value;
-    const int v = 4 * (LG - 3);
+  auto pick = [&](auto lgc, auto sc) -> cudaError_t {
+    constexpr int LG = decltype(lgc)::value, S = decltype(sc)::value;
+    const int v = 4 * (LG - 3) + (S == 2 ? 12 : 0);
     if (mode == MODE_ZP)
-      return lvl ? go(kan_convw_kernel<MODE_ZP, EPI_LEVEL, LG>, v + 3) : go(kan_convw_kernel<MODE_ZP, EPI_F32, LG>, v + 2);
-    return lvl ? go(kan_convw_kernel<MODE_PLAIN, EPI_LEVEL, LG>, v + 1) : go(kan_convw_kernel<MODE_PLAIN, EPI_F32, LG>, v);
+      return lvl ? go(kan_convw_kernel<MODE_ZP, EPI_LEVEL, LG, S>, v + 3)
+                 : go(kan_convw_kernel<MODE_ZP, EPI_F32, LG, S>, v + 2);
+    return lvl ? go(kan_convw_kernel<MODE_PLAIN, EPI_LEVEL, LG, S>, v + 1)
+               : go(kan_convw_kernel<MODE_PLAIN, EPI_F32, LG, S>, v);
   };
-  if (p.bn_img == 8) return pick(std::integral_constant<int, 3>{});
-  if (p.bn_img == 16) return pick(std::integral_constant<int, 4>{});
-  return pick(std::integral_constant<int, 5>{});
+  using I3 = std::integral_constant<int, 3>;
+  using S1 = std::integral_constant<int, 1>;
+  if (p.cstride == 2) return pick(I3{}, std::integral_constant<int, 2>{});  // 16-wide outputs, 8 images
+  if (p.bn_img == 8) return pick(I3{}, S1{});
+  if (p.bn_img == 16) return pick(std::integral_constant<int, 4>{}, S1{});
+  return pick(std::integral_constant<int, 5>{}, S1{});
 }

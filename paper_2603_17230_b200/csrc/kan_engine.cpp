@@ -915,10 +915,14 @@ void prepare_gemm_layer(kan_engine* e, const Layer& l, PreparedLayer& pl, bool b
   // window-shared 3x3 stride-1 pad-1 conv kernel (kan_convw.cuh): no SiLU
   // term, maps a multiple of 16 wide, whole 8-channel activation loads
   pl.convw = false;
+  // stride 1 (output = input size), or stride 2 onto a map a multiple of 16
+  // wide (8 images per tile: every other window pixel is one core matrix)
   const int tw = std::min(16, l.out.w);  // tile width; 128 / tw images per tile
-  if (!bf16 && l.type == L_CONV && !l.im2col && l.kernel == 3 && l.stride == 1 && l.padding == 1 && nbp == 8 &&
-      !pl.silu && !e->opt.no_convw && l.c_in % 8 == 0 && (tw == 16 || tw == 8 || tw == 4) && l.out.w % tw == 0 &&
-      l.out.h == l.in.h && l.out.w == l.in.w) {
+  const int cs = l.stride;
+  const bool geom_ok = (cs == 1 && l.out.h == l.in.h && l.out.w == l.in.w) ||
+                       (cs == 2 && tw == 16 && l.out.h == (l.in.h + 2 - 3) / 2 + 1 && l.out.w == (l.in.w + 2 - 3) / 2 + 1);
+  if (!bf16 && l.type == L_CONV && !l.im2col && l.kernel == 3 && l.padding == 1 && nbp == 8 && geom_ok &&
+      !pl.silu && !e->opt.no_convw && l.c_in % 8 == 0 && (tw == 16 || tw == 8 || tw == 4) && l.out.w % tw == 0) {
     // N tile: 128 columns at most by default (two MMA-rate N = 128 tiles per
     // 256 channels keep the weight slots small enough for a 4-deep A ring)
     const int bn_cap = e->opt.convw_bn > 0 ? e->opt.convw_bn : 128;
@@ -928,7 +932,7 @@ void prepare_gemm_layer(kan_engine* e, const Layer& l, PreparedLayer& pl, bool b
     // buffers and the producers' window rows allow, dividing the map height
     int tr = 0;
     for (int t = 1; t <= 6; ++t)
-      if (t * bnw <= 256 && l.out.h % t == 0 && (t + 2) * (tw + 2) * gimg <= convw_max_rows()) tr = t;
+      if (t * bnw <= 256 && l.out.h % t == 0 && ((t - 1) * cs + 3) * ((tw - 1) * cs + 3) * gimg <= convw_max_rows()) tr = t;
     if (tr > 0) {
       pl.convw = true;
       pl.bnw = bnw;
@@ -1855,9 +1859,10 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
     int CX = l.c_in % 32 == 0 ? 32 : (l.c_in % 16 == 0 ? 16 : 8);
     int SA = 4, SB = 3, SX = 2, WR = 0;
     int TRu = TR;
-    const int TW = std::min(16, l.out.w), G = 128 / TW;
+    const int TW = std::min(16, l.out.w), G = 128 / TW, CS = l.stride;
+    const int WPX = (TW - 1) * CS + 3;  // window columns
     for (;;) {
-      WR = (TRu + 2) * (TW + 2) * G;
+      WR = ((TRu - 1) * CS + 3) * WPX * G;
       SA = 4, SB = 3, SX = 2;
       if (const int rings = e->opt.convw_rings) {  // tuning: SA*100 + SB*10 + SX
         SA = rings / 100;
@@ -1900,6 +1905,9 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
       p.H = l.in.h;
       p.W = l.in.w;
       p.bh = TRu;
+      p.cstride = CS;
+      p.Ho = l.out.h;       // output map
+      p.pimg = l.out.w;
       p.Wo = TW;     // tile width
       p.bn_img = G;  // images per tile
       p.cps = CX;    // channels per activation load
@@ -1928,8 +1936,8 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
       cuuint64_t dims[4] = {static_cast<cuuint64_t>(l.c_in), static_cast<cuuint64_t>(io.n_img),
                             static_cast<cuuint64_t>(l.in.w), static_cast<cuuint64_t>(l.in.h)};
       cuuint64_t strides[3] = {ldb * l.in.w * l.in.h, ldb, ldb * l.in.w};
-      cuuint32_t box[4] = {static_cast<cuuint32_t>(CX), static_cast<cuuint32_t>(G), static_cast<cuuint32_t>(TW + 2),
-                           static_cast<cuuint32_t>(TRu + 2)};
+      cuuint32_t box[4] = {static_cast<cuuint32_t>(CX), static_cast<cuuint32_t>(G), static_cast<cuuint32_t>(WPX),
+                           static_cast<cuuint32_t>((TRu - 1) * CS + 3)};
       cuuint32_t estr[4] = {1u, 1u, 1u, 1u};
       const CUtensorMapSwizzle sw = CX == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
                                     : CX == 16 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE;

@@ -269,3 +269,27 @@ def test_convw_in_residual_stages_bit_exact(oracle, ws):
     np.testing.assert_array_equal(y, yg)
     yo = oracle.int_model_forward(desc, Ws, Bs, x, 8, 3, ws, 8)
     np.testing.assert_array_equal(y, yo.astype(np.float32))
+
+
+@pytest.mark.parametrize("C,H,co,ws,batch", [
+    (16, 32, 32, W_PER_TENSOR_ASYM, 11),   # 32x32 -> 16x16, partial image group
+    (64, 32, 128, W_PER_CHANNEL_SYM, 8),   # the ResKAN18 stage-2 entry conv
+    (8, 64, 24, W_PER_TENSOR_ASYM, 3),     # 64x64 -> 32x32: two 16-column blocks, ragged N
+])
+def test_convw_stride2_bit_exact(oracle, C, H, co, ws, batch):
+    """Stride-2 3x3 pad-1 convs onto 16-wide multiples take kan_convw's
+    stride-2 form (every other window pixel, a 512-byte core-matrix stride)."""
+    desc = conv_desc(C, H, H, C, 1, 1, 0, floor=True)
+    desc["layers"].append({"type": "conv", "c_in": C, "c_out": co, "kernel": 3, "stride": 2, "padding": 1})
+    desc["layers"].append({"type": "conv", "c_in": co, "c_out": 8, "kernel": 1, "stride": 1, "padding": 0})
+    Ws, Bs = weights_for(desc, seed=C + co + 1, silu=False)
+    x = np.random.default_rng(C * co + 1).uniform(-1.05, 1.05, (batch, C * H * H)).astype(np.float32)
+    opts = dict(mode="bspline-lut", lut_k=8, lut_h=3, bits_w=8, w_scheme=ws, silu_base=False)
+    e = build(desc, Ws, Bs, **opts)
+    e.set_option("record_plan", 1)
+    y = e.model_forward(to_dev(x)).cpu().numpy()
+    assert "convw layer=1" in e.last_plan
+    yg = build(desc, Ws, Bs, engine_options={"no_convw": 1}, **opts).model_forward(to_dev(x)).cpu().numpy()
+    np.testing.assert_array_equal(y, yg)
+    yo = oracle.int_model_forward(desc, Ws, Bs, x, 8, 3, ws, 8)
+    np.testing.assert_array_equal(y, yo.astype(np.float32).reshape(batch, -1))
