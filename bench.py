@@ -73,6 +73,8 @@ def parse():
     ap.add_argument("--streams", type=int, default=0,
                     help="batches in flight (one engine + stream each); 0 = per-config default")
     ap.add_argument("--split-k", type=int, default=0, help="force the K splits of split-K launches")
+    ap.add_argument("--opt", action="append", default=[],
+                    help="engine tuning option name=value (kan_engine_set_option; experiments only)")
     return ap.parse_args()
 
 
@@ -358,7 +360,7 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------------------------
-def build_engines(wl, dev_index, n, opts):
+def build_engines(wl, dev_index, n, opts, options=()):
     from paper_2603_17230_b200 import Engine
     Ws, Bs = wl.weights()
     out = []
@@ -366,6 +368,9 @@ def build_engines(wl, dev_index, n, opts):
         e = Engine(wl.descriptor(), dev_index)
         for i, (w, b) in enumerate(zip(Ws, Bs)):
             e.set_coeffs(i, w, b)
+        for kv in options:
+            k, v = kv.split("=")
+            e.set_option(k, int(v))
         e.configure(opts)
         out.append(e)
     return out
@@ -395,7 +400,7 @@ def main():
 
     n_streams = max(1, args.streams or per_config(STREAMS_DEFAULT, wl.key, 1))
     opts = EvalOptions(**wl.eval_options(), split_k=args.split_k or per_config(SPLIT_DEFAULT, wl.key, 0))
-    engines = build_engines(wl, local, n_streams, opts)
+    engines = build_engines(wl, local, n_streams, opts, args.opt)
     eng = engines[0]
 
     # rotating resident input shards, total > 2x L2
@@ -449,6 +454,18 @@ def main():
             graphs[key] = g
         return graphs[key]
 
+    fwd_graphs = {}
+
+    def fwd_graph(r):
+        """CUDA graph of one forward of resident input r (big configs: a step
+        is one graph replay, so host launch work stays off the device clock)."""
+        if r not in fwd_graphs:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=st):
+                engines[0].model_forward(xs[r], out=outs[r], stream=st)
+            fwd_graphs[r] = g
+        return fwd_graphs[r]
+
     def run_steps(n, start=0):
         """Exactly n forwards (steps) of this rank's shard, each followed by the
         logit gather to rank 0 (small configs: one gather per replayed graph,
@@ -464,13 +481,16 @@ def main():
                 done += c
             else:
                 r = (start + done) % R
-                engines[0].model_forward(xs[r], out=outs[r], stream=st)
+                fwd_graph(r).replay()
                 if world > 1:
                     gather(r)
                 done += 1
 
     with torch.cuda.stream(st):
         run_steps(args.warmup)
+        if not small:
+            for r in range(R):  # every step's graph exists before the timed region
+                fwd_graph(r)
         if small:
             graph_of(min(GRAPH_CHUNK, args.steps), args.warmup)
             if args.steps % GRAPH_CHUNK and args.steps > GRAPH_CHUNK:
@@ -587,7 +607,7 @@ def main():
             n_e2e = 2
             e2e_engines = list(engines[:n_e2e])
             if len(e2e_engines) < n_e2e:
-                e2e_engines += build_engines(wl, local, n_e2e - len(e2e_engines), opts)
+                e2e_engines += build_engines(wl, local, n_e2e - len(e2e_engines), opts, args.opt)
             e2e_streams = [torch.cuda.Stream(dev) for _ in range(n_e2e)]
             houts = [torch.empty((B, wl.out_size), dtype=out_dtype).pin_memory() for _ in range(n_e2e)]
             e2e_steps -= e2e_steps % n_e2e
@@ -655,10 +675,10 @@ def main():
             "roofline": roof, "whole_forward": whole, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks.summary(t_wall0, t_wall1),
-            "timing": {"streams": n_streams, "split_k": opts.split_k or "auto",
+            "timing": {"streams": n_streams, "split_k": opts.split_k or "auto", "engine_options": args.opt,
                        "concurrency": (f"{n_streams} batches in flight (one engine + CUDA stream each); "
                                        f"CUDA graphs holding exactly {args.steps} forwards"
-                                       if small else "one batch at a time"),
+                                       if small else "one batch at a time, one CUDA-graph replay per step"),
                        "inputs": f"rotate over {R} resident shards ({R * in_bytes / 2**20:.0f} MiB)",
                        "single_batch_ms": single_ms,
                        "gather": "NCCL gather of every step's logits to rank 0" if world > 1 else None,
