@@ -43,11 +43,14 @@
 // producers (measured: 16 epilogue warps make the levels layers 5-13 % faster
 // and the fp32 ones 4-14 % slower).  Window rows per producer thread (RPT)
 // bound the window at CONVW_MAX_ROWS rows either way.
-template <int OUT>
+// MODE_SILU (per-channel weights + the SiLU base term): the producers also
+// carry each window row's SiLU codes in registers (8 words per row), so those
+// instantiations keep 12 producer warps x 3 rows for both output kinds.
+template <int OUT, bool SILU = false>
 struct ConvwWarps {
-  static constexpr int PW = OUT == EPI_LEVEL ? 8 : 12;
-  static constexpr int EW = OUT == EPI_LEVEL ? 16 : 8;  // a multiple of 4 (TMEM lane quarters)
-  static constexpr int RPT = OUT == EPI_LEVEL ? 4 : 3;
+  static constexpr int PW = (OUT == EPI_LEVEL && !SILU) ? 8 : 12;
+  static constexpr int EW = (OUT == EPI_LEVEL && !SILU) ? 16 : 8;  // a multiple of 4 (TMEM lane quarters)
+  static constexpr int RPT = (OUT == EPI_LEVEL && !SILU) ? 4 : 3;
   static constexpr int THREADS = 32 * (PW + 3 + EW);
 };
 constexpr int CONVW_MAX_ROWS = 1024;  // <= RPT * 32 * PW for both kinds
@@ -55,13 +58,15 @@ constexpr int CONVW_MAX_ROWS = 1024;  // <= RPT * 32 * PW for both kinds
 // S: conv stride (1, or 2 for 16-wide outputs with G = 8: consecutive output
 // pixels are then every other window pixel, a core-matrix stride of 512 B).
 template <int MODE, int OUT, int LG, int S>
-__global__ void __launch_bounds__(ConvwWarps<OUT>::THREADS, 1)
+__global__ void __launch_bounds__(ConvwWarps<OUT, MODE == MODE_SILU>::THREADS, 1)
     kan_convw_kernel(const __grid_constant__ CUtensorMap xmap, const GemmParams p) {
-  constexpr int CONVW_EPI_WARPS = ConvwWarps<OUT>::EW;
-  constexpr int NPW = ConvwWarps<OUT>::PW, NP = 32 * NPW;
+  constexpr bool SILU = (MODE == MODE_SILU);
+  using WarpsT = ConvwWarps<OUT, SILU>;
+  constexpr int CONVW_EPI_WARPS = WarpsT::EW;
+  constexpr int NPW = WarpsT::PW, NP = 32 * NPW;
   constexpr int W_X = NPW, W_MMA = NPW + 1, W_B = NPW + 2, W_EPI = NPW + 3;
   constexpr bool ZP = (MODE == MODE_ZP);
-  constexpr int RPT = ConvwWarps<OUT>::RPT;  // window rows per producer thread (max)
+  constexpr int RPT = WarpsT::RPT;  // window rows per producer thread (max)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
 
@@ -78,6 +83,9 @@ __global__ void __launch_bounds__(ConvwWarps<OUT>::THREADS, 1)
   const int WR = p.ext_rows;           // window rows = (TR + 2) * WP * G
   const int NACC = p.nacc;             // accumulators per tile
   const int n_kb = p.n_ss;             // 32-byte K blocks (4 channels each)
+  // MODE_SILU: after every 8 K blocks (32 channels) one more 32-byte block of
+  // those channels' SiLU codes, against the base weights (n_kb % 8 == 0)
+  const int n_blk = SILU ? n_kb + (n_kb >> 3) : n_kb;
   const uint32_t a_bytes = (static_cast<uint32_t>(WR) * 32u + 1023u) & ~1023u;  // 1 KB-aligned slots
   const uint32_t x_row = static_cast<uint32_t>(CX) * 2u;      // bytes per window row of one load
   const uint32_t x_bytes = ((static_cast<uint32_t>(WR) * x_row + 1023u) & ~1023u);
@@ -89,8 +97,8 @@ __global__ void __launch_bounds__(ConvwWarps<OUT>::THREADS, 1)
   const int tab_bytes = p.tab_bytes;
   int32_t* s_wsum = reinterpret_cast<int32_t*>(sT + ((tab_bytes + 15) & ~15));  // [2][WR] (ZP)
   uint64_t* bars = reinterpret_cast<uint64_t*>(s_wsum + (ZP ? 2 * WR : 0));
-  double* s_cols = reinterpret_cast<double*>(bars + 2 * SA + 2 * SB + 2 * SX + 13);  // [BN]
-  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(s_cols + BN);
+  double* s_cols = reinterpret_cast<double*>(bars + 2 * SA + 2 * SB + 2 * SX + 13);  // [BN] (+ [BN] SiLU corrections)
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(s_cols + (SILU ? 2 * BN : BN));
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -215,12 +223,12 @@ __global__ void __launch_bounds__(ConvwWarps<OUT>::THREADS, 1)
     uint32_t fill = 0;
     for (int u = unit0; u < n_units; u += unit_step) {
       const Tile tl = tile_of(u);
-      for (int kb = 0; kb < n_kb; ++kb, rb.next(), ++fill) {
+      for (int kb = 0; kb < n_blk; ++kb, rb.next(), ++fill) {
         // released by every CTA of the cluster: safe to refill everywhere
         mbar_wait(bar_bempty(rb.slot), rb.phase ^ 1);
         if (lane == 0) {
           const uint32_t dst = smem_u32(sB + static_cast<size_t>(rb.slot) * b_slot);
-          const uint8_t* src = p.wt + (static_cast<size_t>(tl.nt) * n_kb + kb) * b_slot;
+          const uint8_t* src = p.wt + (static_cast<size_t>(tl.nt) * n_blk + kb) * b_slot;
           if (KAN_DBG(p, 32)) {  // tuning only: no weight loads (stale slots)
             mbar_arrive(bar_bfull(rb.slot));
           } else {
@@ -258,7 +266,7 @@ __global__ void __launch_bounds__(ConvwWarps<OUT>::THREADS, 1)
     int lt = 0;
     for (int u = unit0; u < n_units; u += unit_step) {
       if (!tile_of(u).valid) {  // no tile here: release the unit's weight slots
-        for (int kb = 0; kb < n_kb; ++kb, rb.next()) {
+        for (int kb = 0; kb < n_blk; ++kb, rb.next()) {
           mbar_wait_warp(bar_bfull(rb.slot), rb.phase);
           if (elect_one()) release_b(bar_bempty(rb.slot));
           __syncwarp();
@@ -269,7 +277,7 @@ __global__ void __launch_bounds__(ConvwWarps<OUT>::THREADS, 1)
       mbar_wait_warp(bar_accempty(ab), ((lt >> 1) & 1) ^ 1);
       tc_fence_after();
       const uint32_t dacc = tmem + static_cast<uint32_t>(ab) * 256u;
-      for (int kb = 0; kb < n_kb; ++kb, ra.next(), rb.next()) {
+      for (int kb = 0; kb < n_blk; ++kb, ra.next(), rb.next()) {
         mbar_wait_warp(bar_afull(ra.slot), ra.phase);
         mbar_wait_warp(bar_bfull(rb.slot), rb.phase);
         tc_fence_after();
@@ -306,6 +314,7 @@ __global__ void __launch_bounds__(ConvwWarps<OUT>::THREADS, 1)
     // ============ producers: expand the window once per K block =================
     if (tab_bytes > 0) mbar_wait(bar_tab, 0);
     const uint2* c64 = reinterpret_cast<const uint2*>(sT + p.off_c64);
+    const uint8_t* silu_tab = sT + p.off_silu;  // SiLU code per lattice level (MODE_SILU)
     const int tid = threadIdx.x;  // 0 .. NP-1
     Ring ra(SA), rx(SX);
     int lt = 0;
@@ -316,6 +325,7 @@ __global__ void __launch_bounds__(ConvwWarps<OUT>::THREADS, 1)
       // outside the map read level(0.0), as im2col's zero taps do)
       bool pad[RPT];
       uint32_t rs[RPT];
+      uint32_t sl[SILU ? RPT : 1][8];  // MODE_SILU: the rows' SiLU codes of the current 32 channels
 #pragma unroll
       for (int q = 0; q < RPT; ++q) {
         const int r = tid + q * NP;
@@ -343,6 +353,7 @@ __global__ void __launch_bounds__(ConvwWarps<OUT>::THREADS, 1)
             const uint2 lv = *reinterpret_cast<const uint2*>(xt + ur * x_row + ((chunk ^ sw) << 4) + off8);
             const uint32_t lw[2] = {lv.x, lv.y};
             uint32_t w[8];
+            uint32_t sw4 = 0u;
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               uint32_t a = pad[q] ? static_cast<uint32_t>(p.lvl0) : ((lw[e >> 1] >> (16 * (e & 1))) & 0xFFFFu);
@@ -351,6 +362,13 @@ __global__ void __launch_bounds__(ConvwWarps<OUT>::THREADS, 1)
               w[2 * e] = c.x;
               w[2 * e + 1] = c.y;
               if constexpr (ZP) rs[q] = __dp4a(c.y, 0x01010101u, __dp4a(c.x, 0x01010101u, rs[q]));
+              if constexpr (SILU) sw4 |= static_cast<uint32_t>(silu_tab[a]) << (8 * e);
+            }
+            if constexpr (SILU) {
+              // word kb % 8 of the row's SiLU block (channels 4*(kb % 8) ...)
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                if ((kb & 7) == j) sl[q][j] = sw4;
             }
             // row r of the SW32 K-major window: 16-byte chunk c at c ^ row bit 2
             const uint32_t sa = (ur >> 2) & 1u;
@@ -366,6 +384,27 @@ __global__ void __launch_bounds__(ConvwWarps<OUT>::THREADS, 1)
           mbar_arrive(bar_afull(ra.slot));
         }
         if (xh == KPX - 1) rx.next();
+        if constexpr (SILU) {
+          if ((kb & 7) == 7) {
+            // the SiLU block of these 32 channels: one more window in the A ring
+            ra.next();
+            mbar_wait(bar_aempty(ra.slot), ra.phase ^ 1);
+            uint8_t* as = sA + static_cast<size_t>(ra.slot) * a_bytes;
+#pragma unroll
+            for (int q = 0; q < RPT; ++q) {
+              const int r = tid + q * NP;
+              if (r < WR) {
+                const uint32_t sa = (static_cast<uint32_t>(r) >> 2) & 1u;
+                uint8_t* d = as + static_cast<size_t>(r) * 32;
+                *reinterpret_cast<uint4*>(d + (sa << 4)) = make_uint4(sl[q][0], sl[q][1], sl[q][2], sl[q][3]);
+                *reinterpret_cast<uint4*>(d + ((sa ^ 1u) << 4)) = make_uint4(sl[q][4], sl[q][5], sl[q][6], sl[q][7]);
+              }
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar_afull(ra.slot));
+          }
+        }
       }
       if constexpr (ZP) {
         // the window rows' code sums for the epilogue's zero-point term
@@ -400,7 +439,11 @@ __global__ void __launch_bounds__(ConvwWarps<OUT>::THREADS, 1)
       const int ab = lt & 1;
       if (!ZP && tl.nt != staged_nt) {  // per-column scales (restaged when the N tile changes)
         asm volatile("bar.sync 5, %0;" ::"r"(32 * CONVW_EPI_WARPS) : "memory");
-        for (int i = et; i < BN; i += 32 * CONVW_EPI_WARPS) s_cols[i] = p.fs[min(tl.nt * BN + i, p.N - 1)];
+        for (int i = et; i < BN; i += 32 * CONVW_EPI_WARPS) {
+          const int j = min(tl.nt * BN + i, p.N - 1);
+          s_cols[i] = p.fs[j];
+          if constexpr (SILU) s_cols[BN + i] = static_cast<double>(p.corr_b[j]);
+        }
         asm volatile("bar.sync 5, %0;" ::"r"(32 * CONVW_EPI_WARPS) : "memory");
         staged_nt = tl.nt;
       }
@@ -456,6 +499,8 @@ __global__ void __launch_bounds__(ConvwWarps<OUT>::THREADS, 1)
             double y;
             if constexpr (ZP)
               y = __dmul_rn(__dsub_rn(i32_to_f64(r16[e]), zc), p.f_tensor);
+            else if constexpr (SILU)  // minus z_s * colsum(base weight codes)
+              y = __dmul_rn(__dsub_rn(i32_to_f64(r16[e]), s_cols[BN + cl + e]), s_cols[cl + e]);
             else
               y = __dmul_rn(i32_to_f64(r16[e]), s_cols[cl + e]);
             if (p.res_kind) y = __dadd_rn(y, static_cast<double>((&rv4[e >> 2].x)[e & 3]));
@@ -472,6 +517,11 @@ __global__ void __launch_bounds__(ConvwWarps<OUT>::THREADS, 1)
               uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(p.out) + orow * p.ld_out + n0 + cl);
               o[0] = make_uint4(w[0], w[1], w[2], w[3]);
               o[1] = make_uint4(w[4], w[5], w[6], w[7]);
+            } else if (p.out_hw > 0) {  // EPI_F32, NCHW (a model output): lanes = 4 pixels x 8 images
+              float* o = reinterpret_cast<float*>(p.out) +
+                         (static_cast<size_t>(img) * p.N + n0 + cl) * p.out_hw + static_cast<size_t>(oy) * Wo + tl.x0 + px;
+#pragma unroll
+              for (int e = 0; e < 16; ++e) o[static_cast<size_t>(e) * p.out_hw] = __double2float_rn(yval(e));
             } else {  // EPI_F32 row-major (+ levels sidecar)
               float f[16];
 #pragma unroll
@@ -502,6 +552,8 @@ __global__ void __launch_bounds__(ConvwWarps<OUT>::THREADS, 1)
               double v;
               if constexpr (ZP)
                 v = __dmul_rn(__dsub_rn(i32_to_f64(r16[e]), zc), p.f_tensor);
+              else if constexpr (SILU)
+                v = __dmul_rn(__dsub_rn(i32_to_f64(r16[e]), s_cols[BN + cl + e]), s_cols[cl + e]);
               else
                 v = __dmul_rn(i32_to_f64(r16[e]), s_cols[cl + e]);
               if (p.res_kind) v = __dadd_rn(v, static_cast<double>(reinterpret_cast<const float*>(p.res)[orow * p.ld_res + j]));
@@ -510,6 +562,11 @@ __global__ void __launch_bounds__(ConvwWarps<OUT>::THREADS, 1)
                     static_cast<uint16_t>(lattice_level_fast(v, p.n_lo, p.n_hi_open, p.n_step, p.n_inv_step, p.n_L));
               } else {
                 const float f = __double2float_rn(v);
+                if (p.out_hw > 0) {
+                  reinterpret_cast<float*>(p.out)[(static_cast<size_t>(img) * p.N + j) * p.out_hw +
+                                                  static_cast<size_t>(oy) * Wo + tl.x0 + px] = f;
+                  continue;
+                }
                 reinterpret_cast<float*>(p.out)[orow * p.ld_out + j] = f;
                 if (p.out_lv)
                   p.out_lv[orow * p.ld_lv + j] = static_cast<uint16_t>(lattice_level_tie(f, p.inv_step_f, p.lo_f, p.L, thr));
@@ -540,19 +597,20 @@ __global__ void __launch_bounds__(ConvwWarps<OUT>::THREADS, 1)
 
 int convw_max_rows() { return CONVW_MAX_ROWS; }
 
-size_t convw_smem_bytes(int BN, int WR, int CX, int SA, int SB, int SX, int tab_bytes, bool zp) {
+size_t convw_smem_bytes(int BN, int WR, int CX, int SA, int SB, int SX, int tab_bytes, bool zp, bool silu) {
   const size_t b = static_cast<size_t>(9) * BN * 32;
   const size_t x = (static_cast<size_t>(WR) * CX * 2 + 1023) / 1024 * 1024;
   return 1024 + SB * b + SA * ((static_cast<size_t>(WR) * 32 + 1023) / 1024 * 1024) + SX * x +
          ((static_cast<size_t>(tab_bytes) + 15) & ~static_cast<size_t>(15)) + (zp ? 2 * static_cast<size_t>(WR) * 4 : 0) +
-         (2 * SA + 2 * SB + 2 * SX + 13) * 8 + static_cast<size_t>(BN) * 8 + 16;
+         (2 * SA + 2 * SB + 2 * SX + 13) * 8 + static_cast<size_t>(BN) * (silu ? 16 : 8) + 16;
 }
 
 cudaError_t launch_convw(int mode, const CUtensorMap& xmap, const GemmParams& p, size_t smem, cudaStream_t st) {
-  static std::atomic<unsigned long long> optin[16];
+  static std::atomic<unsigned long long> optin[24];
   auto go = [&](auto kfn, int v) -> cudaError_t {
     if (cudaError_t e = smem_optin(kfn, optin[v]); e != cudaSuccess) return e;
-    const int threads = (v & 1) ? ConvwWarps<EPI_LEVEL>::THREADS : ConvwWarps<EPI_F32>::THREADS;  // odd v: levels out
+    const int threads = v >= 16 ? ConvwWarps<EPI_F32, true>::THREADS  // MODE_SILU: one warp layout
+                        : (v & 1) ? ConvwWarps<EPI_LEVEL>::THREADS : ConvwWarps<EPI_F32>::THREADS;  // odd v: levels out
     const int n_sm = device_sm_count();
     const int mc = p.mc > 1 ? p.mc : 1;
     const int units = ((p.M + p.bn_img - 1) / p.bn_img + mc - 1) / mc * (p.Ho / p.bh) * (p.pimg / p.Wo) * p.n_tiles_n;
@@ -577,6 +635,9 @@ cudaError_t launch_convw(int mode, const CUtensorMap& xmap, const GemmParams& p,
   auto pick = [&](auto lgc, auto sc) -> cudaError_t {
     constexpr int LG = decltype(lgc)::value, S = decltype(sc)::value;
     const int v = 4 * (LG - 3) + (S == 2 ? 12 : 0);
+    if (mode == MODE_SILU)
+      return lvl ? go(kan_convw_kernel<MODE_SILU, EPI_LEVEL, LG, S>, 16 + v / 2 + 1)
+                 : go(kan_convw_kernel<MODE_SILU, EPI_F32, LG, S>, 16 + v / 2);
     if (mode == MODE_ZP)
       return lvl ? go(kan_convw_kernel<MODE_ZP, EPI_LEVEL, LG, S>, v + 3)
                  : go(kan_convw_kernel<MODE_ZP, EPI_F32, LG, S>, v + 2);

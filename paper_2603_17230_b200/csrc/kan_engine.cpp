@@ -53,7 +53,7 @@ cudaError_t launch_rows_to_levels(const float* x, int64_t M, int n, int ld_x, ui
 cudaError_t launch_conv3(int mode, const CUtensorMap& xmap, const GemmParams& p, size_t smem, cudaStream_t st);
 size_t conv3_smem_bytes(int BN, int R, int SA, int SB, int SX, int x_kind, int tab_bytes, bool silu);
 cudaError_t launch_convw(int mode, const CUtensorMap& xmap, const GemmParams& p, size_t smem, cudaStream_t st);
-size_t convw_smem_bytes(int BN, int WR, int CX, int SA, int SB, int SX, int tab_bytes, bool zp);
+size_t convw_smem_bytes(int BN, int WR, int CX, int SA, int SB, int SX, int tab_bytes, bool zp, bool silu);
 int convw_max_rows();
 size_t small_smem_bytes(const SmallParams& p);
 cudaError_t launch_im2col_levels(const float* x, int64_t n_img, int C, int H, int W, int K, int stride, int pad,
@@ -912,8 +912,9 @@ void prepare_gemm_layer(kan_engine* e, const Layer& l, PreparedLayer& pl, bool b
     }
   }
 
-  // window-shared 3x3 stride-1 pad-1 conv kernel (kan_convw.cuh): no SiLU
-  // term, maps a multiple of 16 wide, whole 8-channel activation loads
+  // window-shared 3x3 stride-1 pad-1 conv kernel (kan_convw.cuh): maps a
+  // multiple of the tile width wide, whole 8-channel activation loads; with
+  // the SiLU term, whole 32-channel groups (one SiLU block per 8 K blocks)
   pl.convw = false;
   // stride 1 (output = input size), or stride 2 onto a map a multiple of 16
   // wide (8 images per tile: every other window pixel is one core matrix)
@@ -922,7 +923,7 @@ void prepare_gemm_layer(kan_engine* e, const Layer& l, PreparedLayer& pl, bool b
   const bool geom_ok = (cs == 1 && l.out.h == l.in.h && l.out.w == l.in.w) ||
                        (cs == 2 && tw == 16 && l.out.h == (l.in.h + 2 - 3) / 2 + 1 && l.out.w == (l.in.w + 2 - 3) / 2 + 1);
   if (!bf16 && l.type == L_CONV && !l.im2col && l.kernel == 3 && l.padding == 1 && nbp == 8 && geom_ok &&
-      !pl.silu && !e->opt.no_convw && l.c_in % 8 == 0 && (tw == 16 || tw == 8 || tw == 4) && l.out.w % tw == 0) {
+      (!pl.silu || l.c_in % 32 == 0) && !e->opt.no_convw && l.c_in % 8 == 0 && (tw == 16 || tw == 8 || tw == 4) && l.out.w % tw == 0) {
     // N tile: 128 columns at most by default (two MMA-rate N = 128 tiles per
     // 256 channels keep the weight slots small enough for a 4-deep A ring)
     const int bn_cap = e->opt.convw_bn > 0 ? e->opt.convw_bn : 128;
@@ -940,20 +941,31 @@ void prepare_gemm_layer(kan_engine* e, const Layer& l, PreparedLayer& pl, bool b
       pl.ntw = (N + bnw - 1) / bnw;
       pl.b_slotw = 9 * bnw * 32;
       const int n_kb = l.c_in / 4;
-      std::vector<uint8_t> ww(static_cast<size_t>(pl.ntw) * n_kb * pl.b_slotw, 0);
+      // SiLU term: block 8 of every group of 9 holds the base weights of the
+      // group's 32 channels (one byte per channel), after its 8 spline blocks
+      const int n_blk = pl.silu ? n_kb + n_kb / 8 : n_kb;
+      std::vector<uint8_t> ww(static_cast<size_t>(pl.ntw) * n_blk * pl.b_slotw, 0);
       for (int nt = 0; nt < pl.ntw; ++nt)
-        for (int kb = 0; kb < n_kb; ++kb)
+        for (int blk = 0; blk < n_blk; ++blk)
           for (int t = 0; t < 9; ++t) {
-            uint8_t* tile = ww.data() + (static_cast<size_t>(nt) * n_kb + kb) * pl.b_slotw + static_cast<size_t>(t) * bnw * 32;
+            uint8_t* tile = ww.data() + (static_cast<size_t>(nt) * n_blk + blk) * pl.b_slotw + static_cast<size_t>(t) * bnw * 32;
+            const bool sblk = pl.silu && blk % 9 == 8;
+            const int kb = pl.silu ? blk / 9 * 8 + blk % 9 : blk;  // spline K block
             for (int n = 0; n < bnw; ++n) {
               const int j = nt * bnw + n;
               if (j >= N) continue;
               for (int kbyte = 0; kbyte < 32; ++kbyte) {
-                const int c = kb * 4 + kbyte / 8, b = kbyte % 8;
-                if (b >= nb) continue;
-                const int ir = c * 9 + t;  // reference im2col column (layers.hpp:140-149)
-                const size_t src = (static_cast<size_t>(ir) * nb + b) * N + j;
-                const uint8_t v = pl.b_signed ? static_cast<uint8_t>(qw_s8[src]) : qw_u8[src];
+                uint8_t v;
+                if (sblk) {
+                  const int c = blk / 9 * 32 + kbyte;
+                  v = static_cast<uint8_t>(qwb[static_cast<size_t>(c * 9 + t) * N + j]);
+                } else {
+                  const int c = kb * 4 + kbyte / 8, b = kbyte % 8;
+                  if (b >= nb) continue;
+                  const int ir = c * 9 + t;  // reference im2col column (layers.hpp:140-149)
+                  const size_t src = (static_cast<size_t>(ir) * nb + b) * N + j;
+                  v = pl.b_signed ? static_cast<uint8_t>(qw_s8[src]) : qw_u8[src];
+                }
                 // SW32 K-major: 16-byte chunk c of row n at chunk c ^ (n bit 2)
                 tile[n * 32 + ((((kbyte >> 4) ^ ((n >> 2) & 1))) << 4) + (kbyte & 15)] = v;
               }
@@ -1844,8 +1856,9 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
   // window-shared 3x3 conv kernel: 8 images per tile, all nine taps from one
   // expanded window (kan_convw.cuh)
   if (pl.convw && io.conv && io.x_kind == X_U16 && !io.fuse &&
-      (io.epi == EPI_LEVEL || (io.epi == EPI_F32 && io.out_hw == 0)) && (io.ld_x & 7) == 0 &&
-      (io.ld_out & 7) == 0 && (!io.res_kind || (io.ld_res & 3) == 0) &&
+      (io.epi == EPI_LEVEL || io.epi == EPI_F32) && (io.ld_x & 7) == 0 &&
+      ((io.ld_out & 7) == 0 || (io.epi == EPI_F32 && io.out_hw > 0)) && (!io.res_kind || (io.ld_res & 3) == 0) &&
+      (io.out_hw == 0 || (!io.res_kind && !io.out_lv)) &&
       (reinterpret_cast<uintptr_t>(io.out) & 15) == 0 && (reinterpret_cast<uintptr_t>(io.res) & 15) == 0 &&
       (reinterpret_cast<uintptr_t>(io.out_lv) & 15) == 0) {
     const Layer& l = *io.conv;
@@ -1853,6 +1866,7 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
     const int BNw = pl.bnw;
     if (const int t = e->opt.convw_tr; t > 0 && t < TR && l.out.h % t == 0) TR = t;  // tuning: fewer rows per tile
     const bool zp = pl.wscheme == KAN_W_PER_TENSOR_ASYM;
+    const bool wsilu = pl.silu != 0;
     const auto& ts = e->tabs[0];
     // activation loads: CX channels (64-byte rows where the channels allow),
     // and the deepest rings that fit, trading window height for them
@@ -1869,7 +1883,7 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
         SB = rings / 10 % 10;
         SX = rings % 10;
       }
-      auto fits = [&] { return convw_smem_bytes(BNw, WR, CX, SA, SB, SX, ts.bytes, zp) <= 232448; };
+      auto fits = [&] { return convw_smem_bytes(BNw, WR, CX, SA, SB, SX, ts.bytes, zp, wsilu) <= 232448; };
       while (!fits() && SB > 2) --SB;
       while (!fits() && SA > 3) --SA;
       while (!fits() && CX > 16) CX /= 2;
@@ -1878,7 +1892,7 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
       if (fits() || TRu == 1) break;
       do { --TRu; } while (TRu > 1 && l.out.h % TRu != 0);
     }
-    if (convw_smem_bytes(BNw, WR, CX, SA, SB, SX, ts.bytes, zp) <= 232448) {
+    if (convw_smem_bytes(BNw, WR, CX, SA, SB, SX, ts.bytes, zp, wsilu) <= 232448) {
       p.M = static_cast<int>(io.n_img);  // images
       p.N = pl.N;
       p.BN = BNw;
@@ -1916,6 +1930,7 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
       p.out = io.out;
       p.ld_out = static_cast<int>(io.ld_out);
       p.fs = pl.fs.p;
+      p.corr_b = pl.corr_b.p;
       p.f_tensor = pl.f_tensor;
       p.z_w = pl.z_w;
       p.n_lo = e->grid.lo;
@@ -1928,6 +1943,7 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
       p.ld_res = static_cast<int>(io.ld_res);
       p.out_lv = io.out_lv;
       p.ld_lv = static_cast<int>(io.ld_out);
+      p.out_hw = io.out_hw;
       // 4D map over the NHWC levels with the IMAGE dimension second fastest:
       // dims (C, N, W, H), box (CX channels, 8 images, 18 columns, TR + 2 rows)
       CUtensorMap xm;
@@ -1945,10 +1961,10 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
                                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
       if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (convw) failed (" + std::to_string(r) + ")");
-      const size_t smem = convw_smem_bytes(BNw, WR, CX, SA, SB, SX, ts.bytes, zp);
+      const size_t smem = convw_smem_bytes(BNw, WR, CX, SA, SB, SX, ts.bytes, zp, wsilu);
       if (e->opt.record_plan)
-        e->plan_add("convw", pl.layer_index, p.epi, p.res_kind, p.out_lv != nullptr, p.N, BNw, 1, zp ? 1 : 0);
-      ck(launch_convw(zp ? 1 : 0, xm, p, smem, st), "convw launch");  // MODE_ZP / MODE_PLAIN
+        e->plan_add("convw", pl.layer_index, p.epi, p.res_kind, p.out_lv != nullptr, p.N, BNw, 1, zp ? 1 : (wsilu ? 2 : 0));
+      ck(launch_convw(zp ? 1 : (wsilu ? 2 : 0), xm, p, smem, st), "convw launch");  // MODE_ZP / MODE_SILU / MODE_PLAIN
       e->last_launches += 1;
       return;
     }

@@ -293,3 +293,75 @@ def test_convw_stride2_bit_exact(oracle, C, H, co, ws, batch):
     np.testing.assert_array_equal(y, yg)
     yo = oracle.int_model_forward(desc, Ws, Bs, x, 8, 3, ws, 8)
     np.testing.assert_array_equal(y, yo.astype(np.float32).reshape(batch, -1))
+
+
+# kan_convw with the SiLU base term (per-channel weights): one extra 32-byte
+# K block of SiLU codes per 32 channels, against the base weights.
+CONVW_SILU_CASES = [
+    # C, H, W, c_out, batch
+    (64, 32, 32, 64, 13),    # C5pc stage 1, partial image group
+    (32, 16, 16, 128, 9),    # one 32-channel group, 16-wide maps
+    (64, 8, 8, 256, 20),     # 8-wide maps, two N tiles
+    (32, 4, 4, 40, 40),      # 4-wide maps, ragged N
+]
+
+
+@pytest.mark.parametrize("C,H,W,co,batch", CONVW_SILU_CASES)
+def test_convw_silu_bit_exact(oracle, C, H, W, co, batch):
+    desc = conv_desc(C, H, W, C, 1, 1, 0)
+    desc["layers"].append({"type": "conv", "c_in": C, "c_out": co, "kernel": 3, "stride": 1, "padding": 1})
+    desc["layers"].append({"type": "conv", "c_in": co, "c_out": 8, "kernel": 1, "stride": 1, "padding": 0})
+    Ws, Bs = weights_for(desc, seed=C + co + 2, silu=True)
+    x = np.random.default_rng(C * co + 2).uniform(-1.05, 1.05, (batch, C * H * W)).astype(np.float32)
+    opts = dict(mode="bspline-lut", lut_k=8, lut_h=8, bits_w=8, w_scheme=W_PER_CHANNEL_SYM, silu_base=True)
+    e = build(desc, Ws, Bs, **opts)
+    e.set_option("record_plan", 1)
+    y = e.model_forward(to_dev(x)).cpu().numpy()
+    assert "convw layer=1" in e.last_plan
+    yg = build(desc, Ws, Bs, engine_options={"no_convw": 1, "no_conv3": 1}, **opts).model_forward(to_dev(x)).cpu().numpy()
+    np.testing.assert_array_equal(y, yg)
+    yo = oracle.int_model_forward(desc, Ws, Bs, x, 8, 8, W_PER_CHANNEL_SYM, 8)
+    np.testing.assert_array_equal(y, yo.astype(np.float32).reshape(batch, -1))
+
+
+@pytest.mark.parametrize("C,H,W,co,silu,ws,batch", [
+    (64, 32, 32, 64, True, W_PER_CHANNEL_SYM, 11),    # the C4 layer: NCHW model input and output
+    (32, 16, 16, 40, True, W_PER_CHANNEL_SYM, 20),    # ragged N
+    (64, 32, 32, 64, False, W_PER_TENSOR_ASYM, 9),    # the reference scheme
+    (16, 8, 8, 300, False, W_PER_CHANNEL_SYM, 21),    # 8-wide maps, two N tiles
+])
+def test_convw_model_output_nchw_bit_exact(oracle, C, H, W, co, silu, ws, batch):
+    """A single 3x3 conv as the whole model (C4): the NCHW input is transposed
+    to NHWC levels, kan_convw writes the fp32 NCHW model output."""
+    desc = conv_desc(C, H, W, co, 3, 1, 1)
+    Ws, Bs = weights_for(desc, seed=C + co + 3, silu=silu)
+    x = np.random.default_rng(C * co + 3).uniform(-1.05, 1.05, (batch, C * H * W)).astype(np.float32)
+    opts = dict(mode="bspline-lut", lut_k=8, lut_h=8, bits_w=8, w_scheme=ws, silu_base=silu)
+    e = build(desc, Ws, Bs, **opts)
+    e.set_option("record_plan", 1)
+    y = e.model_forward(to_dev(x)).cpu().numpy()
+    assert "convw layer=0" in e.last_plan
+    yg = build(desc, Ws, Bs, engine_options={"no_convw": 1, "no_conv3": 1}, **opts).model_forward(to_dev(x)).cpu().numpy()
+    np.testing.assert_array_equal(y, yg)
+    yo = oracle.int_model_forward(desc, Ws, Bs, x, 8, 8, ws, 8)
+    np.testing.assert_array_equal(y, yo.astype(np.float32).reshape(batch, -1))
+
+
+def test_convw_silu_in_residual_stages_bit_exact(oracle):
+    """Reduced-width ResKAN18 (32/64 channels) with per-channel weights and the
+    SiLU term: the stride-1 convs take kan_convw's SiLU form (levels out; fp32
+    + residual + sidecar out), bit-identical to the general kernel and the oracle."""
+    layers = configs.reskan18_layers(width=(32, 64), n_classes=10, in_ch=3)
+    desc = {"name": "r", "grid": {"intervals": 5, "degree": 3}, "input": [3, 32, 32],
+            "conv_output": "floor", "layers": layers}
+    Ws, Bs = weights_for(desc, seed=29, silu=True)
+    x = np.random.default_rng(29).uniform(-1, 1, (11, 3 * 1024)).astype(np.float32)
+    opts = dict(mode="bspline-lut", lut_k=8, lut_h=3, bits_w=8, w_scheme=W_PER_CHANNEL_SYM, silu_base=True)
+    e = build(desc, Ws, Bs, **opts)
+    e.set_option("record_plan", 1)
+    y = e.model_forward(to_dev(x)).cpu().numpy()
+    assert e.last_plan.count("convw") >= 6
+    yg = build(desc, Ws, Bs, engine_options={"no_convw": 1, "no_conv3": 1}, **opts).model_forward(to_dev(x)).cpu().numpy()
+    np.testing.assert_array_equal(y, yg)
+    yo = oracle.int_model_forward(desc, Ws, Bs, x, 8, 3, W_PER_CHANNEL_SYM, 8)
+    np.testing.assert_array_equal(y, yo.astype(np.float32))
