@@ -248,7 +248,11 @@ typedef enum {
   KAN_OPT_CONVW_RINGS = 16,       /* kan_convw ring depths SA*100 + SB*10 + SX (0 = automatic) */
   KAN_OPT_CONVW_TR = 17,          /* kan_convw output rows per tile cap (0 = automatic) */
   KAN_OPT_CONVW_MC = 18,          /* kan_convw CTAs per weight-multicast cluster: 1, 2, 4 (0 = automatic) */
-  KAN_OPT_CONVW_BN = 19           /* kan_convw N tile cap, multiple of 16 (0 = automatic, 128) */
+  KAN_OPT_CONVW_BN = 19,          /* kan_convw N tile cap, multiple of 16 (0 = automatic, 128) */
+  KAN_OPT_NO_FUSE = 21,           /* 1: a small output layer always runs as its own launch (never inside the previous layer's kernel) */
+  KAN_OPT_FUSE_PERSISTENT = 22,   /* 1: persistent (unsplit) launches also run a small output layer after each tile's epilogue */
+  KAN_OPT_CONVW_NO_KYM = 23,      /* 1: kan_convw issues one MMA per (tap, output row) even where the ky-merged form applies */
+  KAN_OPT_CONVW_LOCK = 20         /* kan_convw window/weight rings in lockstep, one release per K block: -1 off, 1 on (0 = automatic) */
 } kan_option;
 kan_status kan_engine_set_option(kan_engine* e, int option, int64_t value);
 /* The launch plan of the most recent forward when KAN_OPT_RECORD_PLAN is on:

@@ -225,7 +225,8 @@ __global__ void __launch_bounds__(ConvwWarps<OUT, MODE == MODE_SILU>::THREADS, 1
       const Tile tl = tile_of(u);
       for (int kb = 0; kb < n_blk; ++kb, rb.next(), ++fill) {
         // released by every CTA of the cluster: safe to refill everywhere
-        mbar_wait(bar_bempty(rb.slot), rb.phase ^ 1);
+        // (lockstep rings: the weight slot is released by its window slot's commit)
+        mbar_wait(p.lock ? bar_aempty(rb.slot) : bar_bempty(rb.slot), rb.phase ^ 1);
         if (lane == 0) {
           const uint32_t dst = smem_u32(sB + static_cast<size_t>(rb.slot) * b_slot);
           const uint8_t* src = p.wt + (static_cast<size_t>(tl.nt) * n_blk + kb) * b_slot;
@@ -243,10 +244,12 @@ __global__ void __launch_bounds__(ConvwWarps<OUT, MODE == MODE_SILU>::THREADS, 1
       }
     }
     // drain: every peer's release of our slots has landed before the CTA exits
-    for (int s = 0; s < SB; ++s, rb.next()) mbar_wait(bar_bempty(rb.slot), rb.phase ^ 1);
+    if (!p.lock)
+      for (int s = 0; s < SB; ++s, rb.next()) mbar_wait(bar_bempty(rb.slot), rb.phase ^ 1);
   } else if (warp == W_MMA) {
     // ============ MMA issuer: 9 taps x NACC accumulators per K block ============
     const uint32_t idesc = idesc_i8(BN, p.b_signed != 0);
+    const uint32_t idesc2 = idesc_i8(2 * BN, p.b_signed != 0), idesc3 = idesc_i8(3 * BN, p.b_signed != 0);
     // Descriptor start addresses advance in 16-byte units: one window row
     // (32 B) is 2 units, and a start address below 256 KB never carries out of
     // the low word, so the issue loop moves 32-bit low words only.  Per K
@@ -284,7 +287,38 @@ __global__ void __launch_bounds__(ConvwWarps<OUT, MODE == MODE_SILU>::THREADS, 1
         const uint32_t a_lo = static_cast<uint32_t>(umma_desc_sw32(smem_u32(sA + static_cast<size_t>(ra.slot) * a_bytes)));
         const uint32_t b_lo = static_cast<uint32_t>(umma_desc_sw32(smem_u32(sB + static_cast<size_t>(rb.slot) * b_slot)));
         if (elect_one()) {
-          if (!KAN_DBG(p, 2)) {  // (tuning only: flag 2 skips the MMAs)
+          if (S == 1 && p.kym && !KAN_DBG(p, 2)) {
+            // ky-merged issue (3 * BN <= 256): the tile's accumulators are
+            // adjacent TMEM column blocks out[0 .. NACC-1], and the weight slot
+            // holds, per kx, the taps in REVERSED ky order [B(2,kx) | B(1,kx) |
+            // B(0,kx)].  Window row w feeds out[w - ky] for every valid ky, so
+            // ONE MMA of N = nky * BN columns starting at out[w - ky_hi] adds
+            // all of them: 3 * (NACC + 2) MMAs of up to 3 BN columns per K block
+            // instead of 9 * NACC of BN columns (an N = 64 MMA costs 55 cycles,
+            // N = 192 costs 96).  The accumulate flag is per MMA, so the first
+            // (kb, kx) of a tile initialises each out[a] with its ky = 0 tap alone.
+            for (int w = 0; w < NACC + 2; ++w) {
+              const int ky_lo = max(0, w - (NACC - 1)), ky_hi = min(2, w);
+              const uint32_t arow = a_lo + static_cast<uint32_t>(w) * acc_step;
+#pragma unroll
+              for (int kx = 0; kx < 3; ++kx) {
+                const uint32_t ak = arow + static_cast<uint32_t>(kx * G * 2);
+                const uint32_t bk = b_lo + static_cast<uint32_t>(kx * 3) * b_tap;
+                int hi = ky_hi;
+                if (kb == 0 && kx == 0) {
+                  if (ky_lo == 0) {  // out[w] starts with its ky = 0 tap
+                    mma_i8_lh(dacc + static_cast<uint32_t>(w * BN), ak, a_hi, bk + 2u * b_tap, d_hi, idesc, 0u);
+                    if (hi == 0) continue;
+                  }
+                }
+                const int lo = (kb == 0 && kx == 0) ? max(ky_lo, 1) : ky_lo;
+                if (lo > hi) continue;
+                const int nky = hi - lo + 1;
+                mma_i8_lh(dacc + static_cast<uint32_t>((w - hi) * BN), ak, a_hi, bk + static_cast<uint32_t>(2 - hi) * b_tap,
+                          d_hi, nky == 3 ? idesc3 : (nky == 2 ? idesc2 : idesc), 1u);
+              }
+            }
+          } else if (!KAN_DBG(p, 2)) {  // (tuning only: flag 2 skips the MMAs)
             for (int a = 0; a < NACC; ++a) {
               const uint32_t arow = a_lo + static_cast<uint32_t>(a) * acc_step;
               const uint32_t d = dacc + static_cast<uint32_t>(a * BN);
@@ -300,8 +334,10 @@ __global__ void __launch_bounds__(ConvwWarps<OUT, MODE == MODE_SILU>::THREADS, 1
             mbar_arrive(bar_aempty(ra.slot));
             mbar_arrive(bar_bempty(rb.slot));
           } else {
+            // one commit per K block when the rings run in lockstep (each
+            // commit costs the issuing thread a few hundred cycles)
             tc_commit(bar_aempty(ra.slot));
-            release_b(bar_bempty(rb.slot));
+            if (!p.lock) release_b(bar_bempty(rb.slot));
           }
         }
         __syncwarp();

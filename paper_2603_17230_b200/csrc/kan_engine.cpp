@@ -223,6 +223,7 @@ struct PreparedLayer {
   // window-shared 3x3 conv kernel (kan_convw.cuh): weights as
   // [n_tile][K block of 4 channels][9 taps][BNw rows][32 B] (SW32 K-major)
   bool convw = false;
+  bool kymw = false;  // weights laid out for the ky-merged MMA issue
   int bnw = 0, trw = 0, ntw = 0, b_slotw = 0;
   DevBuf<uint8_t> wtw;
   int IPS = 0, GS = 0, n_spline_stages = 0, n_groups = 0, total_stages = 0, silu = 0;
@@ -361,7 +362,8 @@ struct kan_engine {
   // into the fields above, so nothing is read from the environment
   struct Options {
     bool no_convw = false;
-    int convw_rings = 0, convw_tr = 0, convw_mc = 0, convw_bn = 0;
+    int convw_rings = 0, convw_tr = 0, convw_mc = 0, convw_bn = 0, convw_lock = 0;
+    bool no_fuse = false, fuse_persistent = false, no_kym = false;
     bool no_conv3 = false, no_im2col = false, epi_stage = true, lv_sidecar = true, st_prepass = true;
     bool timeline = false, force_nacc1 = false, record_plan = false;
     int force_bn = 0, tables = -1, conv3_mc = 2, st_slices = 0, dbg_flags = 0;
@@ -940,6 +942,9 @@ void prepare_gemm_layer(kan_engine* e, const Layer& l, PreparedLayer& pl, bool b
       pl.trw = tr;
       pl.ntw = (N + bnw - 1) / bnw;
       pl.b_slotw = 9 * bnw * 32;
+      // ky-merged MMA issue (kan_convw.cuh): stride 1 and three N tiles' worth
+      // of columns within one MMA; the taps of a kx then sit in reversed ky order
+      pl.kymw = cs == 1 && 3 * bnw <= 256 && !e->opt.no_kym;
       const int n_kb = l.c_in / 4;
       // SiLU term: block 8 of every group of 9 holds the base weights of the
       // group's 32 channels (one byte per channel), after its 8 spline blocks
@@ -948,7 +953,8 @@ void prepare_gemm_layer(kan_engine* e, const Layer& l, PreparedLayer& pl, bool b
       for (int nt = 0; nt < pl.ntw; ++nt)
         for (int blk = 0; blk < n_blk; ++blk)
           for (int t = 0; t < 9; ++t) {
-            uint8_t* tile = ww.data() + (static_cast<size_t>(nt) * n_blk + blk) * pl.b_slotw + static_cast<size_t>(t) * bnw * 32;
+            const int tpos = pl.kymw ? (t % 3) * 3 + (2 - t / 3) : t;  // t = ky * 3 + kx
+            uint8_t* tile = ww.data() + (static_cast<size_t>(nt) * n_blk + blk) * pl.b_slotw + static_cast<size_t>(tpos) * bnw * 32;
             const bool sblk = pl.silu && blk % 9 == 8;
             const int kb = pl.silu ? blk / 9 * 8 + blk % 9 : blk;  // spline K block
             for (int n = 0; n < bnw; ++n) {
@@ -1867,31 +1873,55 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
     if (const int t = e->opt.convw_tr; t > 0 && t < TR && l.out.h % t == 0) TR = t;  // tuning: fewer rows per tile
     const bool zp = pl.wscheme == KAN_W_PER_TENSOR_ASYM;
     const bool wsilu = pl.silu != 0;
-    const auto& ts = e->tabs[0];
+    const bool lock = e->opt.convw_lock > 0 && e->opt.convw_mc <= 1;
     // activation loads: CX channels (64-byte rows where the channels allow),
     // and the deepest rings that fit, trading window height for them
-    int CX = l.c_in % 32 == 0 ? 32 : (l.c_in % 16 == 0 ? 16 : 8);
-    int SA = 4, SB = 3, SX = 2, WR = 0;
-    int TRu = TR;
     const int TW = std::min(16, l.out.w), G = 128 / TW, CS = l.stride;
     const int WPX = (TW - 1) * CS + 3;  // window columns
-    for (;;) {
-      WR = ((TRu - 1) * CS + 3) * WPX * G;
-      SA = 4, SB = 3, SX = 2;
-      if (const int rings = e->opt.convw_rings) {  // tuning: SA*100 + SB*10 + SX
-        SA = rings / 100;
-        SB = rings / 10 % 10;
-        SX = rings % 10;
+    struct RingPick {
+      int CX, SA, SB, SX, WR, TRu;
+      bool ok;
+    };
+    auto pick_rings = [&](int tab_bytes) {
+      RingPick r{};
+      int CX = l.c_in % 32 == 0 ? 32 : (l.c_in % 16 == 0 ? 16 : 8);
+      int SA = 4, SB = 3, SX = 2, WR = 0;
+      int TRu = TR;
+      auto fits = [&] { return convw_smem_bytes(BNw, WR, CX, SA, SB, SX, tab_bytes, zp, wsilu) <= 232448; };
+      for (;;) {
+        WR = ((TRu - 1) * CS + 3) * WPX * G;
+        SA = 4, SB = 3, SX = 2;
+        if (const int rings = e->opt.convw_rings) {  // tuning: SA*100 + SB*10 + SX
+          SA = rings / 100;
+          SB = rings / 10 % 10;
+          SX = rings % 10;
+        }
+        if (lock) {  // equal window / weight ring depths
+          if (!e->opt.convw_rings) SA = SB = 3;
+          SB = SA = std::min(SA, SB);
+          while (!fits() && CX > 16) CX /= 2;
+          while (!fits() && SA > 2) SB = --SA;
+          while (!fits() && CX > 8) CX /= 2;
+        }
+        while (!fits() && SB > 2) --SB;
+        while (!fits() && SA > 3) --SA;
+        while (!fits() && CX > 16) CX /= 2;
+        while (!fits() && SA > 2) --SA;
+        while (!fits() && CX > 8) CX /= 2;
+        if (fits() || TRu == 1) break;
+        do { --TRu; } while (TRu > 1 && l.out.h % TRu != 0);
       }
-      auto fits = [&] { return convw_smem_bytes(BNw, WR, CX, SA, SB, SX, ts.bytes, zp, wsilu) <= 232448; };
-      while (!fits() && SB > 2) --SB;
-      while (!fits() && SA > 3) --SA;
-      while (!fits() && CX > 16) CX /= 2;
-      while (!fits() && SA > 2) --SA;
-      while (!fits() && CX > 8) CX /= 2;
-      if (fits() || TRu == 1) break;
-      do { --TRu; } while (TRu > 1 && l.out.h % TRu != 0);
-    }
+      r.CX = CX, r.SA = SA, r.SB = SB, r.SX = SX, r.WR = WR, r.TRu = TRu;
+      r.ok = fits();
+      return r;
+    };
+    // tables: the shared per-level code rows (variant 0).  Lane-private copies
+    // of vals (conflict-free lookups + a 64-bit shift) were measured slower here
+    // (more producer instructions and registers; stage-1 layers +7 %)
+    const RingPick rp = pick_rings(e->tabs[0].bytes);
+    const int tabv = 0;
+    const auto& ts = e->tabs[tabv];
+    const int CX = rp.CX, SA = rp.SA, SB = rp.SB, SX = rp.SX, WR = rp.WR, TRu = rp.TRu;
     if (convw_smem_bytes(BNw, WR, CX, SA, SB, SX, ts.bytes, zp, wsilu) <= 232448) {
       p.M = static_cast<int>(io.n_img);  // images
       p.N = pl.N;
@@ -1905,12 +1935,14 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
       // weight slots shared by a cluster of image groups (multicast): the
       // weights are re-streamed from L2 per tile, 9 taps x BN x 32 B per K block
       p.mc = e->opt.convw_mc > 0 ? e->opt.convw_mc : 1;
+      p.lock = lock && SA == SB ? 1 : 0;
+      p.kym = pl.kymw ? 1 : 0;
       p.tab = ts.buf.p;
       p.tab_bytes = ts.bytes;
       p.off_thr = ts.off_thr;
       p.off_silu = ts.off_silu;
       p.off_c64 = ts.off_c64;
-      p.rep = 0;
+      p.rep = tabv;
       p.wt = pl.wtw.p;
       p.ext_rows = WR;
       p.n_ss = l.c_in / 4;
@@ -2100,15 +2132,20 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
   const int gps = (pl.n_groups + splits - 1) / splits;
   p.splits = splits;
   p.groups_per_split = gps;
-  // fused output layer: only for split-K launches (each CTA reduces whole rows)
+  // fused output layer: split-K launches (each CTA reduces whole rows, then
+  // runs the small layer on them) and persistent launches (the epilogue warps
+  // run it on each finished 128-row tile)
   int fused_bytes = stg_bytes;
-  if (io.fuse && splits > 1 && pl.n_tiles_n == 1 && !io.conv && io.epi == EPI_LEVEL) {
+  // (persistent fusion is opt-in: the CUDA-core small layer on 8 epilogue warps
+  // is latency-bound, measured slower than its own launch on C1/C2)
+  if (io.fuse && (splits > 1 || e->opt.fuse_persistent) && pl.n_tiles_n == 1 && !io.conv && io.epi == EPI_LEVEL &&
+      !io.res_kind && !e->opt.no_fuse) {
     const PreparedLayer& f = *io.fuse;
     const int wq_b = (f.n_in * f.N * 8 + 15) / 16 * 16;
     const int wqb_b = f.silu ? (f.N * f.n_in + 15) / 16 * 16 : 0;
     const int fb = wq_b + wqb_b + 128 * pl.BN * 2;
     int SA2 = SA, SB2 = SB, SX2 = SX;
-    bool ok = f.n_in == pl.N && f.N <= 16 && 128 / splits >= 8;
+    bool ok = f.n_in == pl.N && f.N <= 16 && 128 / splits >= 8 && pl.wscheme == KAN_W_PER_CHANNEL_SYM;
     if (ok) {
       try {
         pick_stages(bf16, pl.nbp, pl.BN, io.x_kind, tb, pl.silu != 0, 1, SA2, SB2, SX2, fb);
@@ -2117,7 +2154,7 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
       }
     }
     // the split-K partials are exchanged through the (then idle) rings
-    if (ok && red_bytes > static_cast<size_t>(SB2) * pl.BN * KSTAGE +
+    if (ok && splits > 1 && red_bytes > static_cast<size_t>(SB2) * pl.BN * KSTAGE +
                               static_cast<size_t>(SX2) * 128 * pl.IPS * (io.x_kind == X_F32 ? 4 : 2))
       ok = false;
     if (ok) {
@@ -3187,6 +3224,13 @@ kan_status kan_engine_set_option(kan_engine* e, int option, int64_t value) {
       case KAN_OPT_CONVW_BN:
         if (v != 0 && (v < 16 || v > 256 || v % 16)) throw InvalidArgument("KAN_OPT_CONVW_BN: 0 or a multiple of 16 in 16..256");
         o.convw_bn = v;
+        break;
+      case KAN_OPT_NO_FUSE: o.no_fuse = value != 0; break;
+      case KAN_OPT_CONVW_NO_KYM: o.no_kym = value != 0; break;
+      case KAN_OPT_FUSE_PERSISTENT: o.fuse_persistent = value != 0; break;
+      case KAN_OPT_CONVW_LOCK:
+        if (v < -1 || v > 1) throw InvalidArgument("KAN_OPT_CONVW_LOCK: -1, 0 or 1");
+        o.convw_lock = v;
         break;
       case KAN_OPT_CONVW_MC:
         if (v < 0 || v > 4 || v == 3) throw InvalidArgument("KAN_OPT_CONVW_MC: 0 (auto), 1, 2 or 4");

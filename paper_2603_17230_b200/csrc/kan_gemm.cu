@@ -678,6 +678,79 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
     }
   };
+  // Fused output layer (LUT path, N2 <= 16, per-channel weights) over `rows`
+  // rows of this CTA's hidden-level buffer f_lv, starting at local row rl0, by
+  // `nthr` threads (tid 0 .. nthr-1): TPR = nthr / rows threads per row (a
+  // power of two <= 32, so a row's threads share a warp), inputs i = sub +
+  // TPR*e (all loads issued up front: shared-memory latency here is ~100
+  // cycles, so dependent chains are what costs), mixed-sign dp4a per (input,
+  // output), xor-shuffle reduction over the row's threads (offset-outer, so
+  // the outputs' shuffles overlap), then thread sub finishes outputs sub,
+  // sub + TPR, ... with the fp64 epilogue.  The same integer sums as
+  // kan_small_layer_kernel, so the same outputs.
+  auto fused_output = [&](int tid, int nthr, int rl0, int rows, int m0) {
+    const int TPR = nthr / rows;
+    const int lr = tid / TPR, sub = tid % TPR;
+    const int rl = rl0 + lr;
+    const int n2 = p.f_N, n_in2 = p.N;
+    const int row = m0 + rl;
+    const bool valid_row = row < p.M;  // rows past M were never written
+    const uint32_t* vals = reinterpret_cast<const uint32_t*>(sT);
+    const uint8_t* silu_tab = sT + p.off_silu;
+    const uint32_t mask = (1u << p.k) - 1u;
+    const uint16_t* lvr = f_lv + rl * BN;
+    int acc[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) acc[j] = 0;
+    for (int i0 = 0; i0 < n_in2; i0 += 8 * TPR) {
+      int av[8];
+      uint32_t vv[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int i = i0 + sub + e * TPR;
+        av[e] = (valid_row && i < n_in2) ? lvr[i] : 0;
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        vv[e] = p.rep ? vals[((static_cast<uint32_t>(av[e]) & mask) << 5) | static_cast<uint32_t>(lane)]
+                      : vals[static_cast<uint32_t>(av[e]) & mask];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int i = i0 + sub + e * TPR;
+        if (i < n_in2) {
+          const uint32_t sft = 8u * static_cast<uint32_t>(av[e] >> p.k);
+          const int sc = p.f_silu ? static_cast<int>(silu_tab[av[e]]) : 0;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            if (j < n2) {
+              acc[j] = dp4a_us(vv[e], static_cast<uint32_t>(f_wq[i * n2 + j] >> sft), acc[j]);
+              if (p.f_silu) acc[j] += sc * static_cast<int>(f_wqb[j * n_in2 + i]);
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1)
+      if (off < TPR)
+#pragma unroll
+        for (int j = 0; j < 16; ++j) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], off);
+    if (valid_row) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        if (j < n2 && (j & (TPR - 1)) == sub) {  // output j belongs to thread j mod TPR of the row
+          const size_t o = static_cast<size_t>(row) * p.f_ld_out + j;
+          const long long corr_j = p.f_silu ? p.f_corr[j] : 0ll;
+          const double y = __dmul_rn(static_cast<double>(static_cast<long long>(acc[j]) - corr_j), p.f_fs[j]);
+          if (p.f_epi == EPI_F32)
+            static_cast<float*>(p.f_out)[o] = __double2float_rn(y);
+          else
+            static_cast<int8_t*>(p.f_out)[o] = static_cast<int8_t>(requant_i8(y, p.out_scale, p.inv_out_scale));
+        }
+      }
+    }
+  };
+
   // Epilogue of 4 accumulator columns of one output row (fp64, then the
   // requested output: raw, fp32, next-layer level, int8), shared by the
   // persistent epilogue warps and the split-K reduction.
@@ -1275,6 +1348,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_accempty(ab));
+        if (p.f_on) {
+          // fused output layer (persistent launches): the tile's 128 rows of
+          // hidden levels are in f_lv; the epilogue warps run the small layer
+          // while the next tile's MMAs proceed
+          asm volatile("bar.sync 4, %0;" ::"r"(32 * GEMM_EPI_WARPS) : "memory");
+          fused_output(static_cast<int>(threadIdx.x) - 32 * W_EPI, 32 * GEMM_EPI_WARPS, 0, 128, tl.m0);
+          asm volatile("bar.sync 4, %0;" ::"r"(32 * GEMM_EPI_WARPS) : "memory");  // f_lv free for the next tile
+        }
       }
     } else if constexpr (MODE == MODE_ZP) {
       // split-K: this CTA's row sums for the reduction below
@@ -1344,76 +1425,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         finish4(tl.m0 + rl, tl.n_tile * BN + gq * 4, ra, rs);
       }
       if (p.f_on) {
-        // fused output layer over this CTA's rows: TPR threads per row, inputs
-        // i = sub + TPR*e (all loads issued up front: shared-memory latency
-        // here is ~100 cycles, so dependent chains are what costs), mixed-sign
-        // dp4a per (input, output), xor-shuffle reduction over the row's
-        // threads (offset-outer, so the outputs' shuffles overlap), then thread
-        // sub == j runs output j's fp64 epilogue
-        asm volatile("bar.sync 3, %0;" ::"r"(NP) : "memory");
-        const int TPR = NP / rows_per;  // 8, 16 or 32: a row's threads share a warp
-        const int lr = threadIdx.x / TPR, sub = threadIdx.x % TPR;
-        const int rl = static_cast<int>(rank) * rows_per + lr;
-        const int n2 = p.f_N, n_in2 = p.N;
-        const int row = tl.m0 + rl;
-        const bool valid_row = row < p.M;  // rows past M were never written
-        double fs_j = 0.0;
-        long long corr_j = 0;
-        if (sub < n2) {  // epilogue constants in flight during the contraction
-          fs_j = p.f_fs[sub];
-          if (p.f_silu) corr_j = p.f_corr[sub];
-        }
-        const uint32_t* vals = reinterpret_cast<const uint32_t*>(sT);
-        const uint8_t* silu_tab = sT + p.off_silu;
-        const uint32_t mask = (1u << p.k) - 1u;
-        const uint16_t* lvr = f_lv + rl * BN;
-        int acc[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) acc[j] = 0;
-        for (int i0 = 0; i0 < n_in2; i0 += 8 * TPR) {
-          int av[8];
-          uint32_t vv[8];
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const int i = i0 + sub + e * TPR;
-            av[e] = (valid_row && i < n_in2) ? lvr[i] : 0;
-          }
-#pragma unroll
-          for (int e = 0; e < 8; ++e)
-            vv[e] = p.rep ? vals[((static_cast<uint32_t>(av[e]) & mask) << 5) | static_cast<uint32_t>(lane)]
-                          : vals[static_cast<uint32_t>(av[e]) & mask];
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const int i = i0 + sub + e * TPR;
-            if (i < n_in2) {
-              const uint32_t sft = 8u * static_cast<uint32_t>(av[e] >> p.k);
-              const int sc = p.f_silu ? static_cast<int>(silu_tab[av[e]]) : 0;
-#pragma unroll
-              for (int j = 0; j < 16; ++j) {
-                if (j < n2) {
-                  acc[j] = dp4a_us(vv[e], static_cast<uint32_t>(f_wq[i * n2 + j] >> sft), acc[j]);
-                  if (p.f_silu) acc[j] += sc * static_cast<int>(f_wqb[j * n_in2 + i]);
-                }
-              }
-            }
-          }
-        }
-#pragma unroll
-        for (int off = 16; off >= 1; off >>= 1)
-          if (off < TPR)
-#pragma unroll
-            for (int j = 0; j < 16; ++j) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], off);
-        if (sub < n2 && valid_row) {
-          int v32 = acc[0];
-#pragma unroll
-          for (int j = 1; j < 16; ++j) v32 = sub == j ? acc[j] : v32;
-          const size_t o = static_cast<size_t>(row) * p.f_ld_out + sub;
-          const double y = __dmul_rn(static_cast<double>(static_cast<long long>(v32) - corr_j), fs_j);
-          if (p.f_epi == EPI_F32)
-            static_cast<float*>(p.f_out)[o] = __double2float_rn(y);
-          else
-            static_cast<int8_t*>(p.f_out)[o] = static_cast<int8_t>(requant_i8(y, p.out_scale, p.inv_out_scale));
-        }
+        asm volatile("bar.sync 3, %0;" ::"r"(NP) : "memory");  // the CTA's reduced rows are in f_lv
+        fused_output(static_cast<int>(threadIdx.x), NP, static_cast<int>(rank) * rows_per, rows_per, tl.m0);
       }
     }
     if (threadIdx.x == 0) stamp(7);

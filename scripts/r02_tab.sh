@@ -1,0 +1,5 @@
+timeout 900 python -m pytest tests/test_gpu_conv.py -m gpu -q -x -p no:cacheprovider -k "convw" 2>&1 | tail -5
+for o in "tables=0" "tables=-1"; do
+  echo "== c5 $o"; timeout 300 python scripts/prof_layer.py --config c5 --iters 3 --opt $o | tr '\n' ' '; echo
+  echo "== c4 $o"; timeout 300 python scripts/prof_layer.py --config c4 --iters 20 --opt $o | tr '\n' ' '; echo
+done

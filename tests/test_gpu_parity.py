@@ -284,23 +284,44 @@ def test_forward_host_equals_device_path():
     assert e.last_launches == 1
 
 
-@pytest.mark.parametrize("M", [4096, 1024, 300])
+@pytest.mark.parametrize("M", [4096, 1024, 300, 12800])
 def test_fused_output_layer_matches_separate_launches(oracle, M):
-    """Split-K launches fuse the small output layer into their reduction; a
-    persistent launch (split_k=1) runs it as its own kernel.  Both are the
-    same integer computation: bit-identical logits, and equal to the oracle."""
+    """The small output layer runs inside the previous layer's launch: in the
+    split-K reduction (auto split: 4, 8, 8 and 2 CTAs per tile here), or after
+    each tile's epilogue of a persistent launch (split_k=1 with option
+    fuse_persistent).  By default a persistent launch leaves it to its own kernel.  All are the same integer computation:
+    bit-identical logits, and equal to the oracle."""
     dims, G = [784, 64, 10], 5
     Ws, Bs = make_weights(dims, G, seed=6, silu=True)
     x = np.random.default_rng(M).uniform(-1, 1, (M, 784)).astype(np.float32)
     fused = build(dims, G, Ws, Bs, mode="bspline-lut", silu_base=True)
     yf = fused.model_forward(to_dev(x)).cpu().numpy()
     assert fused.last_launches == 1
+    pers = build(dims, G, Ws, Bs, engine_options={"fuse_persistent": 1}, mode="bspline-lut", silu_base=True, split_k=1)
+    yp = pers.model_forward(to_dev(x)).cpu().numpy()
+    assert pers.last_launches == 1
+    np.testing.assert_array_equal(yf, yp)
     sep = build(dims, G, Ws, Bs, mode="bspline-lut", silu_base=True, split_k=1)
     ys = sep.model_forward(to_dev(x)).cpu().numpy()
     assert sep.last_launches == 2
     np.testing.assert_array_equal(yf, ys)
     yo = oracle_int_model(oracle, G, 8, 8, W_PER_CHANNEL_SYM, 8, Ws, Bs, x)[-1]
     np.testing.assert_array_equal(yf, yo.astype(np.float32))
+
+
+def test_fused_output_layer_many_tiles_per_cta(oracle):
+    """Persistent fused launch with more tiles than SMs (several tiles per CTA,
+    the hidden-level buffer reused tile after tile), int8 logits, ragged batch."""
+    dims, G = [96, 48, 12], 5
+    Ws, Bs = make_weights(dims, G, seed=16, silu=True)
+    M = 128 * 300 + 77
+    x = np.random.default_rng(M).uniform(-1.05, 1.05, (M, 96)).astype(np.float32)
+    opts = dict(mode="bspline-lut", silu_base=True, out_kind=OUT_I8, out_scale=0.05)
+    e = build(dims, G, Ws, Bs, engine_options={"fuse_persistent": 1}, **opts)
+    y = e.model_forward(to_dev(x)).cpu().numpy()
+    assert e.last_launches == 1
+    ys = build(dims, G, Ws, Bs, **opts).model_forward(to_dev(x)).cpu().numpy()
+    np.testing.assert_array_equal(y, ys)
 
 
 def test_level_prepass_matches_in_kernel_levels(oracle):
