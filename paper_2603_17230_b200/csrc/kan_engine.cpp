@@ -2143,9 +2143,9 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
     const PreparedLayer& f = *io.fuse;
     const int wq_b = (f.n_in * f.N * 8 + 15) / 16 * 16;
     const int wqb_b = f.silu ? (f.N * f.n_in + 15) / 16 * 16 : 0;
-    const int fb = wq_b + wqb_b + 128 * pl.BN * 2;
+    const int fb = wq_b + wqb_b + 128 * (pl.BN + 4) * 2;  // weights + hidden-level rows (padded pitch)
     int SA2 = SA, SB2 = SB, SX2 = SX;
-    bool ok = f.n_in == pl.N && f.N <= 16 && 128 / splits >= 8 && pl.wscheme == KAN_W_PER_CHANNEL_SYM;
+    bool ok = f.n_in == pl.N && pl.N % 4 == 0 && f.N <= 16 && 128 / splits >= 8 && pl.wscheme == KAN_W_PER_CHANNEL_SYM;
     if (ok) {
       try {
         pick_stages(bf16, pl.nbp, pl.BN, io.x_kind, tb, pl.silu != 0, 1, SA2, SB2, SX2, fb);

@@ -679,15 +679,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
   };
   // Fused output layer (LUT path, N2 <= 16, per-channel weights) over `rows`
-  // rows of this CTA's hidden-level buffer f_lv, starting at local row rl0, by
-  // `nthr` threads (tid 0 .. nthr-1): TPR = nthr / rows threads per row (a
-  // power of two <= 32, so a row's threads share a warp), inputs i = sub +
-  // TPR*e (all loads issued up front: shared-memory latency here is ~100
-  // cycles, so dependent chains are what costs), mixed-sign dp4a per (input,
-  // output), xor-shuffle reduction over the row's threads (offset-outer, so
-  // the outputs' shuffles overlap), then thread sub finishes outputs sub,
-  // sub + TPR, ... with the fp64 epilogue.  The same integer sums as
-  // kan_small_layer_kernel, so the same outputs.
+  // rows of this CTA's hidden-level buffer f_lv (row pitch BN + 4 levels, so a
+  // warp's rows fall in different banks), starting at local row rl0, by `nthr`
+  // threads (tid 0 .. nthr-1): TPR = nthr / rows threads per row (a power of
+  // two <= 32, so a row's threads share a warp).  Thread sub takes `per`
+  // consecutive inputs, four at a time: their 8-byte code rows (vals[frac]
+  // shifted to byte jj) and one word of their SiLU codes, then for every output
+  // j the four 8-byte weight rows (two mixed-sign dp4a each) and one word of
+  // base weights (one dp4a): independent chains over j, every load issued
+  // before its use.  Xor-shuffle reduction over the row's threads, then thread
+  // j mod TPR finishes output j with the fp64 epilogue.  The same integer sums
+  // as kan_small_layer_kernel, so the same outputs.
   auto fused_output = [&](int tid, int nthr, int rl0, int rows, int m0) {
     const int TPR = nthr / rows;
     const int lr = tid / TPR, sub = tid % TPR;
@@ -698,34 +700,38 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const uint32_t* vals = reinterpret_cast<const uint32_t*>(sT);
     const uint8_t* silu_tab = sT + p.off_silu;
     const uint32_t mask = (1u << p.k) - 1u;
-    const uint16_t* lvr = f_lv + rl * BN;
+    const uint16_t* lvr = f_lv + rl * (BN + 4);
+    const int per = (((n_in2 + TPR - 1) / TPR) + 3) & ~3;
+    const int i_beg = sub * per, i_end = min(n_in2, i_beg + per);
     int acc[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) acc[j] = 0;
-    for (int i0 = 0; i0 < n_in2; i0 += 8 * TPR) {
-      int av[8];
-      uint32_t vv[8];
+    if (valid_row) {
+#pragma unroll 1
+      for (int i0 = i_beg; i0 < i_end; i0 += 4) {
+        const uint2 l4 = *reinterpret_cast<const uint2*>(lvr + i0);  // 4 levels (n_in2 % 4 == 0)
+        uint32_t clo[4], chi[4], sw = 0u;
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const int i = i0 + sub + e * TPR;
-        av[e] = (valid_row && i < n_in2) ? lvr[i] : 0;
-      }
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t a = ((e < 2 ? l4.x : l4.y) >> (16 * (e & 1))) & 0xFFFFu;
+          const uint32_t v = p.rep ? vals[((a & mask) << 5) | static_cast<uint32_t>(lane)] : vals[a & mask];
+          const unsigned long long pt = static_cast<unsigned long long>(v) << (8u * (a >> p.k));
+          clo[e] = static_cast<uint32_t>(pt);
+          chi[e] = static_cast<uint32_t>(pt >> 32);
+          if (p.f_silu) sw |= static_cast<uint32_t>(silu_tab[a]) << (8 * e);
+        }
 #pragma unroll
-      for (int e = 0; e < 8; ++e)
-        vv[e] = p.rep ? vals[((static_cast<uint32_t>(av[e]) & mask) << 5) | static_cast<uint32_t>(lane)]
-                      : vals[static_cast<uint32_t>(av[e]) & mask];
+        for (int j = 0; j < 16; ++j) {
+          if (j < n2) {
+            unsigned long long w[4];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const int i = i0 + sub + e * TPR;
-        if (i < n_in2) {
-          const uint32_t sft = 8u * static_cast<uint32_t>(av[e] >> p.k);
-          const int sc = p.f_silu ? static_cast<int>(silu_tab[av[e]]) : 0;
+            for (int e = 0; e < 4; ++e) w[e] = f_wq[(i0 + e) * n2 + j];
+            const uint32_t wb = p.f_silu ? *reinterpret_cast<const uint32_t*>(f_wqb + j * n_in2 + i0) : 0u;
+            int t = acc[j];
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            if (j < n2) {
-              acc[j] = dp4a_us(vv[e], static_cast<uint32_t>(f_wq[i * n2 + j] >> sft), acc[j]);
-              if (p.f_silu) acc[j] += sc * static_cast<int>(f_wqb[j * n_in2 + i]);
-            }
+            for (int e = 0; e < 4; ++e)
+              t = dp4a_us(chi[e], static_cast<uint32_t>(w[e] >> 32), dp4a_us(clo[e], static_cast<uint32_t>(w[e]), t));
+            acc[j] = dp4a_us(sw, wb, t);
           }
         }
       }
@@ -830,7 +836,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
     } else if (p.epi == EPI_LEVEL) {
       // fused output layer: the levels stay in this CTA's smem row buffer
-      uint16_t* o = p.f_on ? f_lv + (row & 127) * BN + (col0 % BN) : reinterpret_cast<uint16_t*>(p.out) + base;
+      uint16_t* o = p.f_on ? f_lv + (row & 127) * (BN + 4) + (col0 % BN) : reinterpret_cast<uint16_t*>(p.out) + base;
       uint32_t a[4];
 #pragma unroll
       for (int e = 0; e < 4; ++e)
