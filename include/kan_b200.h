@@ -185,6 +185,16 @@ kan_status kan_maxpool2_backward_f32(const float* in_dev, int64_t planes, int H,
                                      const float* dout_dev, float* din_dev, void* stream);
 /* softmax_cross_entropy (train.hpp:139-160): per-row loss [batch] (the mean is
  * their average) and dL/dlogits [batch, n] = (softmax - onehot) / batch. */
+/* One SGD-with-momentum update of a KAN layer's coefficients on the device:
+ * v = momentum * v - lr * g; w += v (train.hpp:361-366, 401-404), in fp64 on a
+ * device-resident master copy; the fp32 copies the forward and backward read
+ * are refreshed in the same launch.  dcoeffs_dev is the gradient from
+ * kan_engine_linear_backward / kan_engine_conv_backward ([n_in * (G+P), n_out]).
+ * The engine must be configured in fp32 mode.  kan_engine_set_coeffs resets the
+ * momentum; kan_engine_get_coeffs reads the current coefficients back. */
+kan_status kan_engine_sgd_step(kan_engine* e, int layer, const float* dcoeffs_dev, double lr, double momentum,
+                               void* stream);
+kan_status kan_engine_get_coeffs(kan_engine* e, int layer, double* out, int64_t n);
 kan_status kan_softmax_cross_entropy(const float* logits_dev, const int32_t* labels_dev, int64_t batch, int n,
                                      float* loss_rows_dev, float* dlogits_dev, void* stream);
 

@@ -142,6 +142,40 @@ __global__ void __launch_bounds__(256) kan_softmax_ce_kernel(const float* __rest
   for (int j = 0; j < n; ++j) dlogits[m * n + j] = (expf(row[j] - mx) / den - (j == y ? 1.f : 0.f)) * inv_m;
 }
 
+// SGD with momentum on a layer's coefficients (train.hpp:361-366, 401-404):
+// v = momentum * v - lr * g; w += v, in fp64 on the device-resident master
+// copy (nothing fused, the reference's operation order), then the two fp32
+// working copies: the reference layout [n_in * nb][N] the backward reads and
+// the padded layout [(i * nbp + b) * Npad + j] the fp32 forward reads.
+__global__ void kan_sgd_step_kernel(double* __restrict__ w, double* __restrict__ v, const float* __restrict__ g,
+                                    float* __restrict__ w_bw, float* __restrict__ w32, long long n, int nb, int nbp,
+                                    int N, int Npad, double lr, double momentum) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const double vn = __dsub_rn(__dmul_rn(momentum, v[i]), __dmul_rn(lr, static_cast<double>(g[i])));
+    const double wn = __dadd_rn(w[i], vn);
+    v[i] = vn;
+    w[i] = wn;
+    const float wf = static_cast<float>(wn);
+    if (w_bw) w_bw[i] = wf;
+    if (w32) {
+      const long long r = i / N;  // = input * nb + basis
+      const int j = static_cast<int>(i - r * N);
+      const long long in = r / nb;
+      const int b = static_cast<int>(r - in * nb);
+      w32[(in * nbp + b) * Npad + j] = wf;
+    }
+  }
+}
+
+cudaError_t launch_sgd_step(double* w, double* v, const float* g, float* w_bw, float* w32, long long n, int nb,
+                            int nbp, int N, int Npad, double lr, double momentum, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const unsigned blocks = static_cast<unsigned>(std::min<long long>((n + 255) / 256, 148 * 8));
+  kan_sgd_step_kernel<<<blocks, 256, 0, st>>>(w, v, g, w_bw, w32, n, nb, nbp, N, Npad, lr, momentum);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_linear_backward(const BwParams& p, cudaStream_t st) {
   if (p.M == 0) return cudaSuccess;
   kan_bw_dcoeffs_kernel<<<dim3(static_cast<unsigned>(p.n_in), static_cast<unsigned>((p.n_out + 127) / 128)), 128, 0,

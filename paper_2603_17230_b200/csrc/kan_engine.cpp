@@ -79,6 +79,8 @@ struct BwParams {
   float lo, hi_open, inv_delta;
 };
 cudaError_t launch_linear_backward(const BwParams& p, cudaStream_t st);
+cudaError_t launch_sgd_step(double* w, double* v, const float* g, float* w_bw, float* w32, long long n, int nb,
+                            int nbp, int N, int Npad, double lr, double momentum, cudaStream_t st);
 cudaError_t launch_softmax_ce(const float* logits, const int32_t* labels, int64_t M, int n, float* loss_rows,
                               float* dlogits, cudaStream_t st);
 cudaError_t launch_nchw_to_rows(const float* in, int64_t n_img, int HW, int N, float* rows, cudaStream_t st);
@@ -181,6 +183,10 @@ struct Layer {
   // fp32 copy of coeffs for the training backward (uploaded on first use after
   // set_coeffs)
   std::shared_ptr<DevBuf<float>> w_bw;
+  // training: fp64 master coefficients and momentum on the device
+  // (kan_engine_sgd_step); `coeffs` is stale while master_ahead is set
+  std::shared_ptr<DevBuf<double>> w_master, w_vel;
+  bool master_ahead = false;
   // spline-table mode: tables supplied by the caller (EvalOptions::tables,
   // eval.hpp:41; e.g. loaded from a .kant container) instead of built from
   // the coefficients; values in the reference layout [n_in][n_out][2^bits_a]
@@ -2743,6 +2749,9 @@ kan_status kan_engine_set_coeffs(kan_engine* e, int layer, const double* coeffs,
                           std::to_string(n));
     l.coeffs.assign(coeffs, coeffs + n);
     l.w_bw.reset();
+    l.w_master.reset();  // (the momentum restarts with new coefficients)
+    l.w_vel.reset();
+    l.master_ahead = false;
     if (base_w) {
       if (n_base != static_cast<int64_t>(l.n_in) * l.n_out)
         throw ShapeMismatch("set_coeffs: base weights must be [n_in, n_out]");
@@ -2754,9 +2763,61 @@ kan_status kan_engine_set_coeffs(kan_engine* e, int layer, const double* coeffs,
   });
 }
 
+// host copy of coefficients a device-side update (kan_engine_sgd_step) moved
+static void sync_master_to_host(kan_engine* e, Layer& l) {
+  if (!l.master_ahead || !l.w_master) return;
+  DeviceGuard dg(e->device);
+  ck(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+  ck(cudaMemcpy(l.coeffs.data(), l.w_master->p, l.coeffs.size() * sizeof(double), cudaMemcpyDeviceToHost), "cudaMemcpy");
+  l.master_ahead = false;
+}
+
 kan_status kan_engine_configure(kan_engine* e, const kan_config* cfg) {
   if (!e) return KAN_ERR_INVALID_ARGUMENT;
-  return guarded(e, [&] { configure(e, cfg); });
+  return guarded(e, [&] {
+    for (auto& l : e->layers)
+      if (l.type == L_LINEAR || l.type == L_CONV) sync_master_to_host(e, l);
+    configure(e, cfg);
+  });
+}
+
+kan_status kan_engine_sgd_step(kan_engine* e, int layer, const float* dcoeffs_dev, double lr, double momentum,
+                               void* stream) {
+  if (!e) return KAN_ERR_INVALID_ARGUMENT;
+  return guarded(e, [&] {
+    Layer& l = e->kan_layer(layer);
+    if (!e->configured || e->cfg.mode != KAN_MODE_FP32)
+      throw InvalidArgument("sgd_step: the engine must be configured in fp32 mode");
+    if (!dcoeffs_dev) throw InvalidArgument("sgd_step: null gradient");
+    const int nb = e->grid.nb();
+    const int n_ref = l.type == L_LINEAR ? l.n_in : l.kernel * l.kernel * l.c_in;
+    const int N = l.type == L_LINEAR ? l.n_out : l.c_out;
+    const long long n = static_cast<long long>(n_ref) * nb * N;
+    if (l.coeffs.size() != static_cast<size_t>(n)) throw InvalidArgument("sgd_step: coefficients not set");
+    DeviceGuard dg(e->device);
+    if (!l.w_master) {
+      l.w_master = std::make_shared<DevBuf<double>>();
+      l.w_master->upload(l.coeffs);
+      l.w_vel = std::make_shared<DevBuf<double>>();
+      l.w_vel->alloc(static_cast<size_t>(n), true);
+    }
+    PreparedLayer& pl = e->prep[static_cast<size_t>(l.kan_index)];
+    ck(launch_sgd_step(l.w_master->p, l.w_vel->p, dcoeffs_dev, l.w_bw ? l.w_bw->p : nullptr, pl.w32.p, n, nb, pl.nbp, N,
+                       pl.Npad, lr, momentum, static_cast<cudaStream_t>(stream)),
+       "sgd step launch");
+    l.master_ahead = true;
+  });
+}
+
+kan_status kan_engine_get_coeffs(kan_engine* e, int layer, double* out, int64_t n) {
+  if (!e) return KAN_ERR_INVALID_ARGUMENT;
+  return guarded(e, [&] {
+    Layer& l = e->kan_layer(layer);
+    if (!out || n != static_cast<int64_t>(l.coeffs.size()))
+      throw ShapeMismatch("get_coeffs: expected room for " + std::to_string(l.coeffs.size()) + " coefficients");
+    sync_master_to_host(e, l);
+    std::copy(l.coeffs.begin(), l.coeffs.end(), out);
+  });
 }
 
 kan_status kan_engine_forward(kan_engine* e, const float* x_dev, int64_t batch, void* out_dev,
@@ -2977,6 +3038,7 @@ kan_status kan_engine_linear_backward(kan_engine* e, int layer, const float* x_d
     if (batch > 0 && (!x_dev || !dout_dev || !dcoeffs_dev)) throw InvalidArgument("linear_backward: null buffer");
     DeviceGuard dg(e->device);
     if (!l.w_bw) {
+      sync_master_to_host(e, l);
       l.w_bw = std::make_shared<DevBuf<float>>();
       std::vector<float> w32(l.coeffs.begin(), l.coeffs.end());
       l.w_bw->upload(w32);
@@ -3020,6 +3082,7 @@ kan_status kan_engine_conv_backward(kan_engine* e, int layer, const float* x_dev
     if (batch > 0 && (!x_dev || !dout_dev || !dcoeffs_dev)) throw InvalidArgument("conv_backward: null buffer");
     DeviceGuard dg(e->device);
     if (!l.w_bw) {
+      sync_master_to_host(e, l);
       l.w_bw = std::make_shared<DevBuf<float>>();
       std::vector<float> w32(l.coeffs.begin(), l.coeffs.end());
       l.w_bw->upload(w32);

@@ -92,6 +92,8 @@ _lib.kan_engine_layer_timeline.argtypes = [_vp, C.c_int, _vp, C.c_int64]
 _lib.kan_engine_layer_timeline.restype = C.c_int64
 _lib.kan_engine_set_activation_ranges.argtypes = [_vp, _vp, C.c_int]
 _lib.kan_engine_linear_backward.argtypes = [_vp, C.c_int, _vp, C.c_int64, _vp, _vp, _vp, _vp]
+_lib.kan_engine_sgd_step.argtypes = [_vp, C.c_int, _vp, C.c_double, C.c_double, _vp]
+_lib.kan_engine_get_coeffs.argtypes = [_vp, C.c_int, _vp, C.c_int64]
 _lib.kan_softmax_cross_entropy.argtypes = [_vp, _vp, C.c_int64, C.c_int, _vp, _vp, _vp]
 _lib.kan_engine_conv_backward.argtypes = [_vp, C.c_int, _vp, C.c_int64, _vp, _vp, _vp, _vp]
 _lib.kan_maxpool2_f32.argtypes = [_vp, C.c_int64, C.c_int, C.c_int, C.c_int, _vp, _vp]
@@ -160,6 +162,7 @@ EXPORTED = [
     "kan_engine_linear_backward", "kan_softmax_cross_entropy", "kan_engine_conv_backward",
     "kan_maxpool2_f32", "kan_maxpool2_backward_f32", "kan_engine_set_option", "kan_engine_last_plan",
     "kan_engine_forward_sharded", "kan_engine_forward_sharded_host", "kan_shard_rows",
+    "kan_engine_sgd_step", "kan_engine_get_coeffs",
 ]
 
 
@@ -516,6 +519,22 @@ class Engine:
                                                   dc.data_ptr(), None if di is None else di.data_ptr(),
                                                   self._stream(stream)))
         return dc, di
+
+    def sgd_step(self, layer: int, dcoeffs, lr: float, momentum: float, stream=None):
+        """One SGD-with-momentum update of a layer's coefficients on the device
+        (train.hpp:361-366, 401-404): fp64 master copy and velocity stay resident,
+        the fp32 copies the forward / backward read are refreshed in the same launch."""
+        dcoeffs = dcoeffs.contiguous()
+        self._check(_lib.kan_engine_sgd_step(self._h, layer, dcoeffs.data_ptr(), float(lr), float(momentum),
+                                             self._stream(stream)))
+
+    def get_coeffs(self, layer: int) -> np.ndarray:
+        """The layer's current coefficients [n_in*(G+P), n_out] (after device-side updates)."""
+        n_in, n_out = self.layer_shape(layer)
+        nb = self.descriptor["grid"]["intervals"] + self.descriptor["grid"]["degree"]
+        out = np.empty((n_in * nb, n_out), dtype=np.float64)
+        self._check(_lib.kan_engine_get_coeffs(self._h, layer, out.ctypes.data, out.size))
+        return out
 
     # -- parity probes ---------------------------------------------------------------
     def layer_levels(self, layer: int, x, stream=None):

@@ -8,8 +8,10 @@ layer inputs the backward needs stay on the device.  Backward, last layer
 first: kan_engine_linear_backward / kan_engine_conv_backward (d_coeffs,
 d_inputs; the bottom layer skips d_inputs, train.hpp:358, 392), the pooling
 backward (train.hpp:407-431), softmax_cross_entropy on the GPU.  Update
-(train.hpp:361-366, 401-404): v = momentum * v - lr * g; w += v, in fp64 on
-the host copy, pushed back with set_coeffs (one upload per layer per step).
+(train.hpp:361-366, 401-404): v = momentum * v - lr * g; w += v, on the device
+(kan_engine_sgd_step: fp64 master coefficients and velocity stay resident, the
+fp32 working copies are refreshed in the same launch; nothing crosses PCIe in
+a step except the loss).  `coeffs` reads the current coefficients back.
 """
 from __future__ import annotations
 
@@ -40,8 +42,7 @@ class Trainer:
         self.cfg = cfg
         self.desc = descriptor
         self.shapes = _configs.walk_shapes(descriptor)
-        self.coeffs = [np.array(c, dtype=np.float64) for c in coeffs]
-        self.vel = [np.zeros_like(c) for c in self.coeffs]
+        init = [np.array(c, dtype=np.float64) for c in coeffs]
         self.engines = []  # per layer: an fp32 single-layer engine, or None
         ki = 0
         for s in self.shapes:
@@ -50,12 +51,17 @@ class Trainer:
                 if "domain" in descriptor:
                     d["domain"] = descriptor["domain"]
                 e = Engine(d, device)
-                e.set_coeffs(0, self.coeffs[ki])
+                e.set_coeffs(0, init[ki])
                 e.configure(EvalOptions(mode="fp32"))
                 self.engines.append(e)
                 ki += 1
             else:
                 self.engines.append(None)
+
+    @property
+    def coeffs(self) -> List[np.ndarray]:
+        """Current coefficients of every KAN layer (read back from the device)."""
+        return [e.get_coeffs(0) for e in self.engines if e is not None]
 
     def forward(self, x):
         """Per-layer inputs and the logits (rows [batch, values])."""
@@ -91,15 +97,7 @@ class Trainer:
                 continue
             else:
                 continue
-            g = dc.double().cpu().numpy()
-            self.vel[ki] = self.cfg.momentum * self.vel[ki] - self.cfg.lr * g
-            self.coeffs[ki] += self.vel[ki]
-        ki = 0
-        for e in self.engines:
-            if e is not None:
-                e.set_coeffs(0, self.coeffs[ki])
-                e.configure(EvalOptions(mode="fp32"))
-                ki += 1
+            e.sgd_step(0, dc, self.cfg.lr, self.cfg.momentum)
         return loss
 
 

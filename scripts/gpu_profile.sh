@@ -15,3 +15,13 @@ cap r02_c4_conv c4 convw 0        # C4: SiLU form, NCHW output
 cap r02_c3_l0 c3 gather 0         # C3 int8 layer 0
 cap r02_c3bf16_l0 c3bf16 gather 0 # C3 bf16 layer 0
 cap r02_c2_l0 c2 gather 0 --split 1   # C2 bench configuration (unsplit)
+# summarise on the box (the .ncu-rep files are too large to travel): details
+# pages + ncu_summary.json via make_profiles.py, stall/instruction summaries
+python scripts/make_profiles.py gpurun_out c5=r02_c5_l4 c5_l8=r02_c5_l8 c4=r02_c4_conv c3=r02_c3_l0 c3bf16=r02_c3bf16_l0 c2=r02_c2_l0
+for n in r02_c5_l4 r02_c5_l8 r02_c4_conv r02_c3_l0 r02_c3bf16_l0 r02_c2_l0; do
+  cp profiles/$n.txt gpurun_out/
+  python scripts/ncu_summary.py gpurun_out/$n.ncu-rep --tensor > gpurun_out/${n}_stalls.txt 2>&1
+  ncu -i gpurun_out/$n.ncu-rep --page raw --csv > gpurun_out/${n}_raw.csv 2>/dev/null
+  rm -f gpurun_out/$n.ncu-rep
+done
+cp profiles/ncu_summary.json gpurun_out/

@@ -161,3 +161,47 @@ def test_conv_backward_matches_reference_composition(ref):
                             col += 1
     assert _rel(dc.cpu().numpy().astype(np.float64), rdc) < TOL
     assert _rel(di.cpu().numpy().astype(np.float64), rdi) < TOL
+
+
+def test_sgd_step_on_device_is_the_reference_update():
+    """kan_engine_sgd_step: v = momentum*v - lr*g; w += v in fp64 on the device
+    master copy (train.hpp:361-366) -- bit-identical to the same fp64 arithmetic
+    on the host for the fp32 gradients it is given; the fp32 forward and backward
+    read the updated weights; set_coeffs resets the momentum."""
+    G, P, n_in, n_out, M = 5, 3, 37, 12, 65
+    rng = np.random.default_rng(5)
+    W = rng.normal(0, 0.1, (n_in * (G + P), n_out))
+    desc = {"name": "l", "grid": {"intervals": G, "degree": P}, "input": [n_in],
+            "layers": [{"type": "linear", "n_in": n_in, "n_out": n_out}]}
+    e = Engine(desc)
+    e.set_coeffs(0, W)
+    e.configure(EvalOptions(mode="fp32"))
+    x = torch.from_numpy(rng.uniform(-1, 1, (M, n_in)).astype(np.float32)).cuda()
+    w, v = W.copy(), np.zeros_like(W)
+    lr, mom = 0.05, 0.9
+    for step in range(3):
+        dout = torch.from_numpy(rng.normal(0, 1, (M, n_out)).astype(np.float32)).cuda()
+        dc, _ = e.linear_backward(0, x, dout)
+        e.sgd_step(0, dc, lr, mom)
+        v = mom * v - lr * dc.cpu().numpy().astype(np.float64)
+        w = w + v
+        np.testing.assert_array_equal(e.get_coeffs(0), w)
+    # the forward reads the updated weights: equal to a fresh engine on them
+    y = e.model_forward(x).cpu().numpy()
+    f = Engine(desc)
+    f.set_coeffs(0, w)
+    f.configure(EvalOptions(mode="fp32"))
+    np.testing.assert_array_equal(y, f.model_forward(x).cpu().numpy())
+    # and so does the backward (its fp32 copy was refreshed in the same launch)
+    dout = torch.from_numpy(rng.normal(0, 1, (M, n_out)).astype(np.float32)).cuda()
+    _, di = e.linear_backward(0, x, dout)
+    _, di_f = f.linear_backward(0, x, dout)
+    np.testing.assert_array_equal(di.cpu().numpy(), di_f.cpu().numpy())
+    # reconfiguring keeps the trained coefficients; set_coeffs restarts the momentum
+    e.configure(EvalOptions(mode="fp32"))
+    np.testing.assert_array_equal(e.get_coeffs(0), w)
+    e.set_coeffs(0, W)
+    e.configure(EvalOptions(mode="fp32"))
+    dc, _ = e.linear_backward(0, x, dout)
+    e.sgd_step(0, dc, lr, mom)
+    np.testing.assert_array_equal(e.get_coeffs(0), W - lr * dc.cpu().numpy().astype(np.float64))
