@@ -222,13 +222,14 @@ def measure_int8_peak(dev):
         return None
 
 
-def committed_traffic(key: str):
-    """DRAM bytes per launch of the dominant kernel from the committed ncu capture."""
+def committed_traffic(key: str, layer: int):
+    """DRAM bytes per launch of the dominant kernel (KAN layer `layer` of workload
+    `key`) from the committed ncu capture of that launch, or None without one."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(p):
         with open(p) as f:
             d = json.load(f)
-        return d.get(key, {}).get("dram_bytes_per_launch")
+        return d.get(f"{key}_l{layer}", {}).get("dram_bytes_per_launch")
     return None
 
 
@@ -554,6 +555,20 @@ def main():
     peaks, peak_src = measured_peaks()
     dom = int(np.argmax(layer_ms))
     bytes_l = wl.layer_bytes_per_launch(dom, B)
+    # residual blocks (the engine's descriptor extension): the launch plan says how
+    # the dominant layer's tensors are stored -- a block output kept as fp32
+    # values (epi=0) with its u16 levels sidecar (lv=1), and the fp32 residual
+    # it adds (res=2) -- so the algorithmic bytes count them too
+    for ln in plan.strip().splitlines():
+        f = dict(kv.split("=") for kv in ln.split()[1:])
+        if lut and int(f.get("layer", -1)) == dom and ln.split()[0] in ("convw", "conv3", "gather"):
+            kl = wl.kan_layers()[dom]
+            last = dom == wl.n_kan - 1
+            if not last:
+                out_b = (4 if f["epi"] == "0" else 2) + (2 if f["lv"] == "1" else 0) + (4 if f["res"] == "2" else 0)
+                bytes_l += B * kl["out_elems"] * (out_b - 2)  # layer_bytes_per_launch counted u16 levels out
+            elif f["res"] == "2":
+                bytes_l += B * kl["out_elems"] * 4
     ops_l = wl.layer_ops_per_launch(dom, B)
     if small:
         # several batches in flight: per-launch event brackets cannot isolate one
@@ -578,7 +593,7 @@ def main():
         roof = {"bound": "tensor", "achieved": ops_l / t_l / 1e12, "peak": tensor_peak / 1e12,
                 "unit": "TOP/s" if lut else "TFLOP/s"}
     roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["traffic"] = committed_traffic(wl.key) if not small else None
+    roof["traffic"] = committed_traffic(wl.key, dom) if not small else None
     kl = wl.kan_layers()[dom]
     roof["kernel"] = (f"KAN layer {dom} ({kl['n_in']}->{kl['n_out']}"
                       + (f", {kl['pix']} px/sample)" if kl["pix"] > 1 else ")"))

@@ -9,7 +9,8 @@ cap() {  # name config kernel-regex skip [extra prof_layer args]
   python scripts/prof_layer.py --config $cfg --iters 1 "$@" > gpurun_out/plain_$name.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:$rx -s $skip -c 1 -f -o gpurun_out/$name python scripts/prof_layer.py --config $cfg --iters 1 "$@" > gpurun_out/ncu_$name.log 2>&1; echo "$name rc=$?"
 }
-cap r02_c5_l4 c5 convw 3          # stage-1 conv with residual + fp32/sidecar output (the bench's dominant launch)
+cap r02_c5_l2 c5 convw 1          # stage-1 conv, residual add, fp32 + levels sidecar out (the bench's dominant launch)
+cap r02_c5_l4 c5 convw 3          # stage-1 conv, residual add, levels out
 cap r02_c5_l8 c5 convw 7          # stage-2 conv, levels out (N = 128)
 cap r02_c4_conv c4 convw 0        # C4: SiLU form, NCHW output
 cap r02_c3_l0 c3 gather 0         # C3 int8 layer 0
@@ -17,8 +18,8 @@ cap r02_c3bf16_l0 c3bf16 gather 0 # C3 bf16 layer 0
 cap r02_c2_l0 c2 gather 0 --split 1   # C2 bench configuration (unsplit)
 # summarise on the box (the .ncu-rep files are too large to travel): details
 # pages + ncu_summary.json via make_profiles.py, stall/instruction summaries
-python scripts/make_profiles.py gpurun_out c5=r02_c5_l4 c5_l8=r02_c5_l8 c4=r02_c4_conv c3=r02_c3_l0 c3bf16=r02_c3bf16_l0 c2=r02_c2_l0
-for n in r02_c5_l4 r02_c5_l8 r02_c4_conv r02_c3_l0 r02_c3bf16_l0 r02_c2_l0; do
+python scripts/make_profiles.py gpurun_out c5_l2=r02_c5_l2 c5_l4=r02_c5_l4 c5_l8=r02_c5_l8 c4_l0=r02_c4_conv c3_l0=r02_c3_l0 c3bf16_l0=r02_c3bf16_l0 c2_l0=r02_c2_l0
+for n in r02_c5_l2 r02_c5_l4 r02_c5_l8 r02_c4_conv r02_c3_l0 r02_c3bf16_l0 r02_c2_l0; do
   cp profiles/$n.txt gpurun_out/
   python scripts/ncu_summary.py gpurun_out/$n.ncu-rep --tensor > gpurun_out/${n}_stalls.txt 2>&1
   ncu -i gpurun_out/$n.ncu-rep --page raw --csv > gpurun_out/${n}_raw.csv 2>/dev/null

@@ -3,7 +3,7 @@ and ncu_summary.json (DRAM bytes per launch of each config's dominant kernel,
 read by bench.py for roofline.traffic).  Existing entries of other configs are
 kept.
 
-    python scripts/make_profiles.py gpurun_out c5=r02_c5_l4 [c3=r02_c3_l0 ...]
+    python scripts/make_profiles.py gpurun_out c5_l4=r02_c5_l4 [c3_l0=r02_c3_l0 ...]   (keys: <workload>_l<KAN layer>)
 """
 import csv
 import io
