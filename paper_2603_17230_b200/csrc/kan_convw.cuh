@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(ConvwWarps<OUT, MODE == MODE_SILU>::THREADS, 1
     for (int u = unit0; u < n_units; u += unit_step) {
       const Tile tl = tile_of(u);
       if (!tl.valid) continue;
-      if (p.res_kind) {
+      if (p.res_kind && !KAN_DBG(p, 4096)) {
         // the tile's residual rows into L2 now, so the epilogue (a whole tile
         // of MMAs later) reads them from L2 instead of HBM: one contiguous TW-
         // pixel NHWC segment per (image, output row)
@@ -507,7 +507,7 @@ __global__ void __launch_bounds__(ConvwWarps<OUT, MODE == MODE_SILU>::THREADS, 1
 #pragma unroll 1
         for (int cl = half * 16; cl < (KAN_DBG(p, 8) ? 0 : BN); cl += 16 * EQ) {  // (tuning: flag 8 skips the epilogue)
           const bool full = n0 + cl + 16 <= p.N;
-          if (p.res_kind && valid) {
+          if (p.res_kind && valid && !KAN_DBG(p, 4096)) {  // (tuning only: flag 4096 drops the residual reads)
             // pull the NEXT group's residual segment into L1 while this one is processed
             size_t nrow = orow;
             int ncl = cl + 16 * EQ;
@@ -519,7 +519,7 @@ __global__ void __launch_bounds__(ConvwWarps<OUT, MODE == MODE_SILU>::THREADS, 1
               asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const float*>(p.res) + nrow * p.ld_res + n0 + ncl));
           }
           float4 rv4[4] = {};
-          if (p.res_kind && valid && full) {
+          if (p.res_kind && valid && full && !KAN_DBG(p, 4096)) {
             const float4* rp =
                 reinterpret_cast<const float4*>(reinterpret_cast<const float*>(p.res) + orow * p.ld_res + n0 + cl);
 #pragma unroll

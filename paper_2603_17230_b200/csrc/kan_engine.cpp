@@ -950,6 +950,8 @@ void prepare_gemm_layer(kan_engine* e, const Layer& l, PreparedLayer& pl, bool b
       pl.b_slotw = 9 * bnw * 32;
       // ky-merged MMA issue (kan_convw.cuh): stride 1 and three N tiles' worth
       // of columns within one MMA; the taps of a kx then sit in reversed ky order
+      // (pairs of taps as N = 256 MMAs for 128-column tiles were measured slower:
+      // stages 2-4 +8...10 %, so the merged form stays with the <= 80-column tiles)
       pl.kymw = cs == 1 && 3 * bnw <= 256 && !e->opt.no_kym;
       const int n_kb = l.c_in / 4;
       // SiLU term: block 8 of every group of 9 holds the base weights of the
