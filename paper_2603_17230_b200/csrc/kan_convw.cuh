@@ -46,11 +46,14 @@
 // MODE_SILU (per-channel weights + the SiLU base term): the producers also
 // carry each window row's SiLU codes in registers (8 words per row), so those
 // instantiations keep 12 producer warps x 3 rows for both output kinds.
-template <int OUT, bool SILU = false>
+// The stride-2 form expands a (2 TR + 1)-row window per TR output rows, so it
+// is producer-heavy: 12 + 8 there too (measured: the stage-2 entry conv -14 %).
+template <int OUT, bool SILU = false, int S = 1>
 struct ConvwWarps {
-  static constexpr int PW = (OUT == EPI_LEVEL && !SILU) ? 8 : 12;
-  static constexpr int EW = (OUT == EPI_LEVEL && !SILU) ? 16 : 8;  // a multiple of 4 (TMEM lane quarters)
-  static constexpr int RPT = (OUT == EPI_LEVEL && !SILU) ? 4 : 3;
+  static constexpr bool WIDE_EPI = OUT == EPI_LEVEL && !SILU && S == 1;
+  static constexpr int PW = WIDE_EPI ? 8 : 12;
+  static constexpr int EW = WIDE_EPI ? 16 : 8;  // a multiple of 4 (TMEM lane quarters)
+  static constexpr int RPT = WIDE_EPI ? 4 : 3;
   static constexpr int THREADS = 32 * (PW + 3 + EW);
 };
 constexpr int CONVW_MAX_ROWS = 1024;  // <= RPT * 32 * PW for both kinds
@@ -58,10 +61,10 @@ constexpr int CONVW_MAX_ROWS = 1024;  // <= RPT * 32 * PW for both kinds
 // S: conv stride (1, or 2 for 16-wide outputs with G = 8: consecutive output
 // pixels are then every other window pixel, a core-matrix stride of 512 B).
 template <int MODE, int OUT, int LG, int S>
-__global__ void __launch_bounds__(ConvwWarps<OUT, MODE == MODE_SILU>::THREADS, 1)
+__global__ void __launch_bounds__(ConvwWarps<OUT, MODE == MODE_SILU, S>::THREADS, 1)
     kan_convw_kernel(const __grid_constant__ CUtensorMap xmap, const GemmParams p) {
   constexpr bool SILU = (MODE == MODE_SILU);
-  using WarpsT = ConvwWarps<OUT, SILU>;
+  using WarpsT = ConvwWarps<OUT, SILU, S>;
   constexpr int CONVW_EPI_WARPS = WarpsT::EW;
   constexpr int NPW = WarpsT::PW, NP = 32 * NPW;
   constexpr int W_X = NPW, W_MMA = NPW + 1, W_B = NPW + 2, W_EPI = NPW + 3;
@@ -643,10 +646,8 @@ size_t convw_smem_bytes(int BN, int WR, int CX, int SA, int SB, int SX, int tab_
 
 cudaError_t launch_convw(int mode, const CUtensorMap& xmap, const GemmParams& p, size_t smem, cudaStream_t st) {
   static std::atomic<unsigned long long> optin[24];
-  auto go = [&](auto kfn, int v) -> cudaError_t {
+  auto go = [&](auto kfn, int v, int threads) -> cudaError_t {
     if (cudaError_t e = smem_optin(kfn, optin[v]); e != cudaSuccess) return e;
-    const int threads = v >= 16 ? ConvwWarps<EPI_F32, true>::THREADS  // MODE_SILU: one warp layout
-                        : (v & 1) ? ConvwWarps<EPI_LEVEL>::THREADS : ConvwWarps<EPI_F32>::THREADS;  // odd v: levels out
     const int n_sm = device_sm_count();
     const int mc = p.mc > 1 ? p.mc : 1;
     const int units = ((p.M + p.bn_img - 1) / p.bn_img + mc - 1) / mc * (p.Ho / p.bh) * (p.pimg / p.Wo) * p.n_tiles_n;
@@ -671,14 +672,16 @@ cudaError_t launch_convw(int mode, const CUtensorMap& xmap, const GemmParams& p,
   auto pick = [&](auto lgc, auto sc) -> cudaError_t {
     constexpr int LG = decltype(lgc)::value, S = decltype(sc)::value;
     const int v = 4 * (LG - 3) + (S == 2 ? 12 : 0);
+    constexpr int TL = ConvwWarps<EPI_LEVEL, false, S>::THREADS, TF = ConvwWarps<EPI_F32, false, S>::THREADS;
+    constexpr int TS = ConvwWarps<EPI_F32, true, S>::THREADS;  // MODE_SILU: one warp layout
     if (mode == MODE_SILU)
-      return lvl ? go(kan_convw_kernel<MODE_SILU, EPI_LEVEL, LG, S>, 16 + v / 2 + 1)
-                 : go(kan_convw_kernel<MODE_SILU, EPI_F32, LG, S>, 16 + v / 2);
+      return lvl ? go(kan_convw_kernel<MODE_SILU, EPI_LEVEL, LG, S>, 16 + v / 2 + 1, TS)
+                 : go(kan_convw_kernel<MODE_SILU, EPI_F32, LG, S>, 16 + v / 2, TS);
     if (mode == MODE_ZP)
-      return lvl ? go(kan_convw_kernel<MODE_ZP, EPI_LEVEL, LG, S>, v + 3)
-                 : go(kan_convw_kernel<MODE_ZP, EPI_F32, LG, S>, v + 2);
-    return lvl ? go(kan_convw_kernel<MODE_PLAIN, EPI_LEVEL, LG, S>, v + 1)
-               : go(kan_convw_kernel<MODE_PLAIN, EPI_F32, LG, S>, v);
+      return lvl ? go(kan_convw_kernel<MODE_ZP, EPI_LEVEL, LG, S>, v + 3, TL)
+                 : go(kan_convw_kernel<MODE_ZP, EPI_F32, LG, S>, v + 2, TF);
+    return lvl ? go(kan_convw_kernel<MODE_PLAIN, EPI_LEVEL, LG, S>, v + 1, TL)
+               : go(kan_convw_kernel<MODE_PLAIN, EPI_F32, LG, S>, v, TF);
   };
   using I3 = std::integral_constant<int, 3>;
   using S1 = std::integral_constant<int, 1>;
