@@ -549,6 +549,28 @@ def main():
         e1.record(st)
     torch.cuda.synchronize()
     single_ms = e0.elapsed_time(e1) / 10
+    # the same single batch at the engine's automatic split (small configs: the
+    # layer-0 tiles spread over a cluster per tile, the output layer fused into
+    # the reduction, one launch): the latency a caller with one batch sees
+    single_auto_ms = None
+    if n_streams > 1 and opts.split_k != 0:
+        o2 = EvalOptions(**{**vars(opts), "split_k": 0})
+        ea = build_engines(wl, local, 1, o2, args.opt)[0]
+        ea.model_forward(xs[0], out=outs[0], stream=st)
+        torch.cuda.synchronize()
+        ag = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(ag, stream=st):
+            ea.model_forward(xs[0], out=outs[0], stream=st)
+        ag.replay()
+        torch.cuda.synchronize()
+        with torch.cuda.stream(st):
+            e0.record(st)
+            for _ in range(10):
+                ag.replay()
+            e1.record(st)
+        torch.cuda.synchronize()
+        single_auto_ms = e0.elapsed_time(e1) / 10
+        del ea
 
     lut = wl.mode == "bspline-lut"
     st_mode = wl.mode == "spline-table"
@@ -696,6 +718,7 @@ def main():
                                        if small else "one batch at a time, one CUDA-graph replay per step"),
                        "inputs": f"rotate over {R} resident shards ({R * in_bytes / 2**20:.0f} MiB)",
                        "single_batch_ms": single_ms,
+                       "single_batch_auto_split_ms": single_auto_ms,
                        "gather": "NCCL gather of every step's logits to rank 0" if world > 1 else None,
                        "launch_plan": plan.strip().splitlines(),
                        "vs_baseline_ref": ("PAPER.md:603 KANMLP2 G=5 8-bit LUT, RTX 3090, 1.69M samples/s"
