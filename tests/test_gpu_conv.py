@@ -365,3 +365,27 @@ def test_convw_silu_in_residual_stages_bit_exact(oracle):
     np.testing.assert_array_equal(y, yg)
     yo = oracle.int_model_forward(desc, Ws, Bs, x, 8, 3, W_PER_CHANNEL_SYM, 8)
     np.testing.assert_array_equal(y, yo.astype(np.float32))
+
+
+@pytest.mark.parametrize("opt", [{"convw_lock": 1}, {"convw_no_kym": 1}, {"convw_mc": 2}, {"convw_tr": 2}])
+def test_convw_issue_options_are_bit_identical(opt):
+    """kan_convw's issue / ring variants (lockstep rings with one commit per K
+    block, one MMA per tap instead of the ky-merged form, weight multicast over
+    CTA pairs, fewer rows per tile) compute the same int32 sums: stage-1-shaped
+    layers in both weight schemes, bit-identical to the default."""
+    for ws, silu in ((W_PER_TENSOR_ASYM, False), (W_PER_CHANNEL_SYM, True)):
+        desc = conv_desc(32, 32, 32, 32, 1, 1, 0)
+        desc["layers"].append({"type": "conv", "c_in": 32, "c_out": 64, "kernel": 3, "stride": 1, "padding": 1})
+        desc["layers"].append({"type": "conv", "c_in": 64, "c_out": 8, "kernel": 1, "stride": 1, "padding": 0})
+        Ws, Bs = weights_for(desc, seed=31, silu=silu)
+        x = np.random.default_rng(31).uniform(-1.05, 1.05, (19, 32 * 32 * 32)).astype(np.float32)
+        opts = dict(mode="bspline-lut", lut_k=8, lut_h=8, bits_w=8, w_scheme=ws, silu_base=silu)
+        e0 = build(desc, Ws, Bs, **opts)
+        e0.set_option("record_plan", 1)
+        y0 = e0.model_forward(to_dev(x)).cpu().numpy()
+        assert "convw layer=1" in e0.last_plan
+        e1 = build(desc, Ws, Bs, engine_options=opt, **opts)
+        e1.set_option("record_plan", 1)
+        y1 = e1.model_forward(to_dev(x)).cpu().numpy()
+        assert "convw layer=1" in e1.last_plan
+        np.testing.assert_array_equal(y0, y1)
