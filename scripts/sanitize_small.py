@@ -5,8 +5,9 @@ memcheck, synccheck; one tool per run):
     compute-sanitizer --tool racecheck python scripts/sanitize_small.py
 
 Covers: gather GEMM (persistent and split-K, fused output layer, int8 logits),
-small-N layer, kan_conv3 (SiLU, per-channel), kan_convw (zero point and
-per-channel, 8/16/32 images per tile), the general conv kernel, level
+small-N layer, kan_conv3 (SiLU, per-channel), kan_convw (zero point,
+per-channel and SiLU forms, 8/16/32 images per tile, ky-merged and per-tap
+issue, lockstep rings), the general conv kernel, level
 prepass, stem im2col, pooling, spline-table and fp32 paths.  Results are
 checked against each other (bit-identical across kernel choices) so a run
 that races also fails here.
@@ -47,6 +48,7 @@ def main():
     x = wl.inputs(300, seed=1)
     desc = wl.descriptor()
     base = dict(mode="bspline-lut", lut_k=8, lut_h=8, bits_w=8, w_scheme=1, silu_base=True)
+    Wm, Bm, xm = Ws, Bs, x
     y1 = run(build(desc, Ws, Bs, split_k=1, **base), x)
     y2 = run(build(desc, Ws, Bs, split_k=2, **base), x)
     assert np.array_equal(y1, y2), "MLP split-K differs"
@@ -77,9 +79,17 @@ def main():
     Ws, Bs = cw.weights()
     x = cw.inputs(20, seed=3)  # >= 148 tiles: kan_conv3 takes the 3x3 layers
     o = dict(mode="bspline-lut", lut_k=8, lut_h=8, bits_w=8, w_scheme=1, silu_base=True)
-    ya = run(build(cw.descriptor(), Ws, Bs, **o), x)
-    yb = run(build(cw.descriptor(), Ws, Bs, options={"no_conv3": 1}, **o), x)
-    assert np.array_equal(ya, yb), "conv3 vs gather differ"
+    ya = run(build(cw.descriptor(), Ws, Bs, **o), x)  # kan_convw, SiLU form
+    yc = run(build(cw.descriptor(), Ws, Bs, options={"no_convw": 1}, **o), x)  # kan_conv3
+    yb = run(build(cw.descriptor(), Ws, Bs, options={"no_convw": 1, "no_conv3": 1}, **o), x)  # gather GEMM
+    assert np.array_equal(ya, yb), "convw (SiLU) vs gather differ"
+    assert np.array_equal(yc, yb), "conv3 vs gather differ"
+    yl = run(build(cw.descriptor(), Ws, Bs, options={"convw_lock": 1}, **o), x)
+    yk = run(build(cw.descriptor(), Ws, Bs, options={"convw_no_kym": 1}, **o), x)
+    assert np.array_equal(ya, yl) and np.array_equal(ya, yk), "convw issue variants differ"
+    # persistent launch with the fused output layer (opt-in) vs its own launch
+    yp = run(build(desc, Wm, Bm, options={"fuse_persistent": 1}, split_k=1, **base), xm)
+    assert np.array_equal(yp, y1), "persistent fused output layer differs"
     print("sanitize_small: ok")
 
 
