@@ -222,15 +222,19 @@ def measure_int8_peak(dev):
         return None
 
 
-def committed_traffic(key: str, layer: int):
-    """DRAM bytes per launch of the dominant kernel (KAN layer `layer` of workload
-    `key`) from the committed ncu capture of that launch, or None without one."""
+def committed_traffic(key: str, kernel, layers):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu
+    captures (profiles/ncu_summary.json): the average over all of the kernel's
+    launches of a forward ("<workload>_<kernel>": one ncu pass over every launch),
+    or the capture of the single KAN layer ("<workload>_l<layer>"); None without one."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
-    if os.path.exists(p):
-        with open(p) as f:
-            d = json.load(f)
-        return d.get(f"{key}_l{layer}", {}).get("dram_bytes_per_launch")
-    return None
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    if kernel is not None and len(layers) > 1:
+        return d.get(f"{key}_{kernel}", {}).get("dram_bytes_per_launch")
+    return d.get(f"{key}_l{layers[0]}", {}).get("dram_bytes_per_launch")
 
 
 # ---------------------------------------------------------------------------------
@@ -575,59 +579,97 @@ def main():
     lut = wl.mode == "bspline-lut"
     st_mode = wl.mode == "spline-table"
     peaks, peak_src = measured_peaks()
-    dom = int(np.argmax(layer_ms))
-    bytes_l = wl.layer_bytes_per_launch(dom, B)
-    # residual blocks (the engine's descriptor extension): the launch plan says how
-    # the dominant layer's tensors are stored -- a block output kept as fp32
-    # values (epi=0) with its u16 levels sidecar (lv=1), and the fp32 residual
-    # it adds (res=2) -- so the algorithmic bytes count them too
+    # per-layer algorithmic bytes.  Residual blocks (the engine's descriptor
+    # extension): the launch plan says how a layer's tensors are stored -- a block
+    # output kept as fp32 values (epi=0) with its u16 levels sidecar (lv=1), and
+    # the fp32 residual it adds (res=2) -- so the algorithmic bytes count them too
+    layer_kernel = {}
+    layer_bytes = [wl.layer_bytes_per_launch(li, B) for li in range(wl.n_kan)]
     for ln in plan.strip().splitlines():
         f = dict(kv.split("=") for kv in ln.split()[1:])
-        if lut and int(f.get("layer", -1)) == dom and ln.split()[0] in ("convw", "conv3", "gather"):
-            kl = wl.kan_layers()[dom]
-            last = dom == wl.n_kan - 1
-            if not last:
+        li = int(f.get("layer", -1))
+        name = ln.split()[0]
+        if li < 0 or name in ("im2col_levels", "nchw_to_nhwc", "level_prepass"):
+            continue
+        layer_kernel[li] = name  # the layer's contraction kernel
+        if lut and name in ("convw", "conv3", "gather"):
+            kl = wl.kan_layers()[li]
+            if li != wl.n_kan - 1:
                 out_b = (4 if f["epi"] == "0" else 2) + (2 if f["lv"] == "1" else 0) + (4 if f["res"] == "2" else 0)
-                bytes_l += B * kl["out_elems"] * (out_b - 2)  # layer_bytes_per_launch counted u16 levels out
+                layer_bytes[li] += B * kl["out_elems"] * (out_b - 2)  # layer_bytes_per_launch counted u16 levels out
             elif f["res"] == "2":
-                bytes_l += B * kl["out_elems"] * 4
-    ops_l = wl.layer_ops_per_launch(dom, B)
+                layer_bytes[li] += B * kl["out_elems"] * 4
+    # the dominant kernel: the kernel function with the largest share of the step
+    # (ResKAN18: kan_convw, 15 launches per forward); its roofline averages over
+    # its launches (algorithmic work of all of them / their total duration), and
+    # the slowest single launch is reported next to it
+    groups = {}
+    for li in range(wl.n_kan):
+        groups.setdefault(layer_kernel.get(li, "layer"), []).append(li)
+    dom_name = max(groups, key=lambda k: sum(layer_ms[li] for li in groups[k]))
+    dom_layers = groups[dom_name]
+    dom = max(dom_layers, key=lambda li: layer_ms[li])  # its slowest launch
+    n_l = len(dom_layers)
+    bytes_l = sum(layer_bytes[li] for li in dom_layers) / n_l
+    ops_l = sum(wl.layer_ops_per_launch(li, B) for li in dom_layers) / n_l
+    t_ms = sum(layer_ms[li] for li in dom_layers) / n_l
     if small:
         # several batches in flight: per-launch event brackets cannot isolate one
         # launch, so the unit is the whole forward over the effective time per batch
         bytes_l = (B * wl.input_size * 4 + B * wl.out_size * (1 if wl.int8_out else 4)
                    + sum(wl.weight_bytes(li) for li in range(wl.n_kan)))
         ops_l = wl.ops_per_sample() * B
-        layer_ms[dom] = ms / args.steps
+        t_ms = ms / args.steps
+        layer_ms[dom] = t_ms
     int8_peak, int8_src = None, None
     if lut:
         int8_peak = measure_int8_peak(dev)
         int8_src = "measured in this run: torch._int_mm (cuBLASLt) int8 8192^3, best of 10"
         if int8_peak is None:
             int8_peak, int8_src = 4500.0, "datasheet 4.5 POPS dense int8 (measurement failed)"
-    t_l = layer_ms[dom] / 1e3
-    ai = ops_l / bytes_l
     tensor_peak = (int8_peak if lut else peaks.get("bf16_tflops", 1661.3)) * 1e12
     hbm_peak = peaks["hbm_gbs"] * 1e9
-    if st_mode or ai < tensor_peak / hbm_peak:
-        roof = {"bound": "hbm", "achieved": bytes_l / t_l / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s"}
-    else:
-        roof = {"bound": "tensor", "achieved": ops_l / t_l / 1e12, "peak": tensor_peak / 1e12,
-                "unit": "TOP/s" if lut else "TFLOP/s"}
-    roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["traffic"] = committed_traffic(wl.key, dom) if not small else None
-    kl = wl.kan_layers()[dom]
-    roof["kernel"] = (f"KAN layer {dom} ({kl['n_in']}->{kl['n_out']}"
-                      + (f", {kl['pix']} px/sample)" if kl["pix"] > 1 else ")"))
+
+    def roof_of(ops, nbytes, t_s):
+        if st_mode or ops / nbytes < tensor_peak / hbm_peak:
+            r = {"bound": "hbm", "achieved": nbytes / t_s / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s"}
+        else:
+            r = {"bound": "tensor", "achieved": ops / t_s / 1e12, "peak": tensor_peak / 1e12,
+                 "unit": "TOP/s" if lut else "TFLOP/s"}
+        r["frac"] = r["achieved"] / r["peak"]
+        return r
+
+    def layer_name(li):
+        kl = wl.kan_layers()[li]
+        return (f"KAN layer {li} ({kl['n_in']}->{kl['n_out']}" + (f", {kl['pix']} px/sample)" if kl["pix"] > 1 else ")"))
+
+    kfn = {"convw": "kan_convw_kernel", "conv3": "kan_conv3_kernel", "gather": "kan_gather_gemm_kernel",
+           "gather_bf16": "kan_gather_gemm_kernel (bf16)", "small_layer": "kan_small_layer_kernel"}.get(dom_name, dom_name)
+    roof = roof_of(ops_l, bytes_l, t_ms / 1e3)
+    roof["traffic"] = committed_traffic(wl.key, dom_name, dom_layers) if not small else None
     if small:
         roof["kernel"] = f"whole forward ({launches_per_step} launch(es) per batch, {n_streams} batches in flight)"
-    roof["per_launch"] = {"algorithmic_bytes": bytes_l, "algorithmic_ops": ops_l, "avg_ms": layer_ms[dom],
-                          "launches_timed": prof_steps,
+    elif n_l == 1:
+        roof["kernel"] = f"{kfn}: " + layer_name(dom)
+    else:
+        roof["kernel"] = (f"{kfn}: {n_l} launches per forward (KAN layers "
+                          + ",".join(str(li) for li in dom_layers) + "), averaged over its launches")
+    roof["per_launch"] = {"algorithmic_bytes": bytes_l, "algorithmic_ops": ops_l, "avg_ms": t_ms,
+                          "launches_per_forward": 1 if small else n_l,
+                          "launches_timed": prof_steps * (1 if small else n_l),
                           "timing": ("timed region / steps (batches in flight)" if small
-                                     else "CUDA event pair around the kernel node, graph replay")}
+                                     else "CUDA event pair around each kernel node, graph replay")}
     roof["peak_source"] = (int8_src if lut and roof["bound"] == "tensor" else peak_src)
     roof["layer_avg_ms"] = layer_ms
-    roof["share_of_step"] = layer_ms[dom] / (ms / args.steps)
+    # share of the forward, from the same per-launch brackets (their sum runs a few
+    # percent above the timed step: bracketed launches do not overlap their tails)
+    roof["share_of_step"] = 1.0 if small else t_ms * n_l / max(sum(layer_ms), 1e-12)
+    if not small and n_l > 1:
+        sl = roof_of(wl.layer_ops_per_launch(dom, B), layer_bytes[dom], layer_ms[dom] / 1e3)
+        roof["slowest_launch"] = {"kernel": layer_name(dom), "avg_ms": layer_ms[dom], "frac": sl["frac"],
+                                  "achieved": sl["achieved"], "algorithmic_bytes": layer_bytes[dom],
+                                  "algorithmic_ops": wl.layer_ops_per_launch(dom, B),
+                                  "traffic": committed_traffic(wl.key, None, [dom])}
     # whole-forward tensor roofline (every KAN layer's dense contraction)
     whole = {"ops_per_sample": wl.ops_per_sample(), "achieved": value * wl.ops_per_sample() / 1e12 / world,
              "unit": "TOP/s per GPU" if lut else "TFLOP/s per GPU"}

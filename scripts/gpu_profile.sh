@@ -16,6 +16,11 @@ cap r02_c4_conv c4 convw 0        # C4: SiLU form, NCHW output
 cap r02_c3_l0 c3 gather 0         # C3 int8 layer 0
 cap r02_c3bf16_l0 c3bf16 gather 0 # C3 bf16 layer 0
 cap r02_c2_l0 c2 gather 0 --split 1   # C2 bench configuration (unsplit)
+# DRAM bytes of EVERY kan_convw launch of one C5 forward (one light pass): the
+# per-launch average behind roofline.traffic of the kernel-level roofline
+ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:convw -c 15 --csv --log-file gpurun_out/r02_c5_convw_dram.csv python scripts/prof_layer.py --config c5 --iters 1 > gpurun_out/ncu_convw_dram.log 2>&1; echo "convw dram rc=$?"
+ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:gather -c 3 --csv --log-file gpurun_out/r02_c3_gather_dram.csv python scripts/prof_layer.py --config c3 --iters 1 > gpurun_out/ncu_c3_dram.log 2>&1; echo "c3 dram rc=$?"
+ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:gather -c 3 --csv --log-file gpurun_out/r02_c3bf16_gather_dram.csv python scripts/prof_layer.py --config c3bf16 --iters 1 > gpurun_out/ncu_c3bf16_dram.log 2>&1; echo "c3bf16 dram rc=$?"
 # summarise on the box (the .ncu-rep files are too large to travel): details
 # pages + ncu_summary.json via make_profiles.py, stall/instruction summaries
 python scripts/make_profiles.py gpurun_out c5_l2=r02_c5_l2 c5_l4=r02_c5_l4 c5_l8=r02_c5_l8 c4_l0=r02_c4_conv c3_l0=r02_c3_l0 c3bf16_l0=r02_c3bf16_l0 c2_l0=r02_c2_l0
@@ -25,4 +30,5 @@ for n in r02_c5_l2 r02_c5_l4 r02_c5_l8 r02_c4_conv r02_c3_l0 r02_c3bf16_l0 r02_c
   ncu -i gpurun_out/$n.ncu-rep --page raw --csv > gpurun_out/${n}_raw.csv 2>/dev/null
   rm -f gpurun_out/$n.ncu-rep
 done
+python scripts/make_profiles.py --dram-csv c5_convw=gpurun_out/r02_c5_convw_dram.csv c3_gather=gpurun_out/r02_c3_gather_dram.csv c3bf16_gather_bf16=gpurun_out/r02_c3bf16_gather_dram.csv
 cp profiles/ncu_summary.json gpurun_out/

@@ -48,5 +48,31 @@ def main(src, pairs):
         json.dump(out, f, indent=1)
 
 
+def dram_csv(key, csv_path):
+    """<workload>_<kernel> entry from one light ncu pass over EVERY launch of the
+    kernel in a forward (--metrics dram__bytes_read.sum,dram__bytes_write.sum,
+    gpu__time_duration.sum --csv --log-file ...): average DRAM bytes per launch."""
+    lines = open(csv_path).read().split("\n")
+    i = [k for k, l in enumerate(lines) if l.startswith('"ID"')][0]
+    rows = list(csv.reader(lines[i:]))
+    h = rows[0]
+    idc, mn, mu, mv = h.index("ID"), h.index("Metric Name"), h.index("Metric Unit"), h.index("Metric Value")
+    per = {}
+    for r in rows[1:]:
+        if len(r) > mv and r[mn].startswith("dram__bytes"):
+            per[r[idc]] = per.get(r[idc], 0.0) + to_bytes(r[mv], r[mu])
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    out = json.load(open(path)) if os.path.exists(path) else {"captures": {}}
+    out[key] = {"dram_bytes_per_launch": sum(per.values()) / max(len(per), 1), "launches": len(per),
+                "capture": os.path.basename(csv_path)}
+    print(key, out[key])
+    with open(path, "w") as f:
+        json.dump(out, f, indent=1)
+
+
 if __name__ == "__main__":
-    main(sys.argv[1], [a.split("=") for a in sys.argv[2:]])
+    if sys.argv[1] == "--dram-csv":  # python scripts/make_profiles.py --dram-csv c5_convw=gpurun_out/r02_c5_convw_dram.csv
+        for a in sys.argv[2:]:
+            dram_csv(*a.split("="))
+    else:
+        main(sys.argv[1], [a.split("=") for a in sys.argv[2:]])
