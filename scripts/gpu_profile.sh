@@ -18,7 +18,7 @@ cap r02_c3bf16_l0 c3bf16 gather 0 # C3 bf16 layer 0
 cap r02_c2_l0 c2 gather 0 --split 1   # C2 bench configuration (unsplit)
 # DRAM bytes of EVERY kan_convw launch of one C5 forward (one light pass): the
 # per-launch average behind roofline.traffic of the kernel-level roofline
-ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:convw -c 15 --csv --log-file gpurun_out/r02_c5_convw_dram.csv python scripts/prof_layer.py --config c5 --iters 1 > gpurun_out/ncu_convw_dram.log 2>&1; echo "convw dram rc=$?"
+ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:convw -c 14 --csv --log-file gpurun_out/r02_c5_convw_dram.csv python scripts/prof_layer.py --config c5 --iters 1 > gpurun_out/ncu_convw_dram.log 2>&1; echo "convw dram rc=$?"
 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:gather -c 3 --csv --log-file gpurun_out/r02_c3_gather_dram.csv python scripts/prof_layer.py --config c3 --iters 1 > gpurun_out/ncu_c3_dram.log 2>&1; echo "c3 dram rc=$?"
 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:gather -c 3 --csv --log-file gpurun_out/r02_c3bf16_gather_dram.csv python scripts/prof_layer.py --config c3bf16 --iters 1 > gpurun_out/ncu_c3bf16_dram.log 2>&1; echo "c3bf16 dram rc=$?"
 # summarise on the box (the .ncu-rep files are too large to travel): details
