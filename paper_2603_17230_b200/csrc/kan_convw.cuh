@@ -54,7 +54,20 @@ struct ConvwWarps {
   static constexpr int PW = WIDE_EPI ? 8 : 12;
   static constexpr int EW = WIDE_EPI ? 16 : 8;  // a multiple of 4 (TMEM lane quarters)
   static constexpr int RPT = WIDE_EPI ? 4 : 3;
-  static constexpr int THREADS = 32 * (PW + 3 + EW);
+  // MODE_SILU level outputs split the register file by role (setmaxnreg works
+  // on aligned groups of 4 warps, so one idle warp pads the three utility
+  // warps): the launch allocates 80 registers per thread (768 threads); the
+  // 12 producer warps give back 16 each and the 8 epilogue warps run their
+  // fp64 level chains at 104 without spilling (ResKAN18 per-channel + SiLU:
+  // stage-1 level layers -8...-17 %, the whole forward -4.7 %).  Measured
+  // neutral or slower on the other instantiations, which keep one budget.
+  static constexpr bool REGSPLIT = SILU && OUT == EPI_LEVEL;
+  static constexpr int UW = REGSPLIT ? 4 : 3;  // utility warps (+ the idle one)
+  static constexpr int THREADS = 32 * (PW + UW + EW);
+  static constexpr int R_LAUNCH = 80, R_PROD = 64, R_EPI = 104;
+  static_assert(!REGSPLIT || (PW * R_PROD + UW * R_LAUNCH + EW * R_EPI <= (PW + UW + EW) * R_LAUNCH &&
+                              R_LAUNCH * THREADS <= 65536 && PW % 4 == 0 && EW % 4 == 0),
+                "register pool");
 };
 constexpr int CONVW_MAX_ROWS = 1024;  // <= RPT * 32 * PW for both kinds
 
@@ -67,7 +80,7 @@ __global__ void __launch_bounds__(ConvwWarps<OUT, MODE == MODE_SILU, S>::THREADS
   using WarpsT = ConvwWarps<OUT, SILU, S>;
   constexpr int CONVW_EPI_WARPS = WarpsT::EW;
   constexpr int NPW = WarpsT::PW, NP = 32 * NPW;
-  constexpr int W_X = NPW, W_MMA = NPW + 1, W_B = NPW + 2, W_EPI = NPW + 3;
+  constexpr int W_X = NPW, W_MMA = NPW + 1, W_B = NPW + 2, W_EPI = NPW + WarpsT::UW;
   constexpr bool ZP = (MODE == MODE_ZP);
   constexpr int RPT = WarpsT::RPT;  // window rows per producer thread (max)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -351,6 +364,7 @@ __global__ void __launch_bounds__(ConvwWarps<OUT, MODE == MODE_SILU, S>::THREADS
     }
   } else if (warp < NPW) {
     // ============ producers: expand the window once per K block =================
+    if constexpr (WarpsT::REGSPLIT) reg_dealloc<WarpsT::R_PROD>();
     if (tab_bytes > 0) mbar_wait(bar_tab, 0);
     const uint2* c64 = reinterpret_cast<const uint2*>(sT + p.off_c64);
     const uint8_t* silu_tab = sT + p.off_silu;  // SiLU code per lattice level (MODE_SILU)
@@ -459,8 +473,9 @@ __global__ void __launch_bounds__(ConvwWarps<OUT, MODE == MODE_SILU, S>::THREADS
       }
       ++lt;
     }
-  } else {
+  } else if (warp >= W_EPI) {
     // ============ epilogue: NACC accumulators x BN columns -> NHWC rows ==========
+    if constexpr (WarpsT::REGSPLIT) reg_alloc<WarpsT::R_EPI>();
     if (tab_bytes > 0) mbar_wait(bar_tab, 0);
     const float* thr = reinterpret_cast<const float*>(sT + p.off_thr);
     const int wq = warp & 3;             // TMEM lane quarter
@@ -673,9 +688,10 @@ cudaError_t launch_convw(int mode, const CUtensorMap& xmap, const GemmParams& p,
     constexpr int LG = decltype(lgc)::value, S = decltype(sc)::value;
     const int v = 4 * (LG - 3) + (S == 2 ? 12 : 0);
     constexpr int TL = ConvwWarps<EPI_LEVEL, false, S>::THREADS, TF = ConvwWarps<EPI_F32, false, S>::THREADS;
-    constexpr int TS = ConvwWarps<EPI_F32, true, S>::THREADS;  // MODE_SILU: one warp layout
+    constexpr int TS = ConvwWarps<EPI_F32, true, S>::THREADS;  // MODE_SILU: one warp layout ...
+    constexpr int TSL = ConvwWarps<EPI_LEVEL, true, S>::THREADS;  // ... plus the idle warp of the register split
     if (mode == MODE_SILU)
-      return lvl ? go(kan_convw_kernel<MODE_SILU, EPI_LEVEL, LG, S>, 16 + v / 2 + 1, TS)
+      return lvl ? go(kan_convw_kernel<MODE_SILU, EPI_LEVEL, LG, S>, 16 + v / 2 + 1, TSL)
                  : go(kan_convw_kernel<MODE_SILU, EPI_F32, LG, S>, 16 + v / 2, TS);
     if (mode == MODE_ZP)
       return lvl ? go(kan_convw_kernel<MODE_ZP, EPI_LEVEL, LG, S>, v + 3, TL)

@@ -117,6 +117,17 @@ __device__ __forceinline__ void mbar_wait_warp(uint32_t bar, uint32_t parity) {
   }
 #endif
 }
+// Per-role register budgets: every warp of an aligned group of 4 warps gives
+// registers back to (dealloc) or takes them from (alloc, blocking until they
+// are free) the CTA's pool.  N: a multiple of 8 in [24, 256].
+template <int N>
+__device__ __forceinline__ void reg_dealloc() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
+}
+template <int N>
+__device__ __forceinline__ void reg_alloc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
+}
 // one lane of the (converged) warp
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;
