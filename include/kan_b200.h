@@ -262,7 +262,7 @@ typedef enum {
   KAN_OPT_NO_FUSE = 21,           /* 1: a small output layer always runs as its own launch (never inside the previous layer's kernel) */
   KAN_OPT_FUSE_PERSISTENT = 22,   /* 1: persistent (unsplit) launches also run a small output layer after each tile's epilogue */
   KAN_OPT_CONVW_NO_KYM = 23,      /* 1: kan_convw issues one MMA per (tap, output row) even where the ky-merged form applies */
-  KAN_OPT_CONVW_LOCK = 20         /* kan_convw window/weight rings in lockstep, one release per K block: -1 off, 1 on (0 = automatic) */
+  KAN_OPT_CONVW_LOCK = 20         /* kan_convw: one tcgen05.commit per K block releases the window slot and the weight slot (needs weight ring <= window ring): -1 off, 1 on, 0 = automatic (on for N tiles >= 128) */
 } kan_option;
 kan_status kan_engine_set_option(kan_engine* e, int option, int64_t value);
 /* The launch plan of the most recent forward when KAN_OPT_RECORD_PLAN is on:

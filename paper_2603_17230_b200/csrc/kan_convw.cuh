@@ -240,9 +240,18 @@ __global__ void __launch_bounds__(ConvwWarps<OUT, MODE == MODE_SILU, S>::THREADS
     for (int u = unit0; u < n_units; u += unit_step) {
       const Tile tl = tile_of(u);
       for (int kb = 0; kb < n_blk; ++kb, rb.next(), ++fill) {
-        // released by every CTA of the cluster: safe to refill everywhere
-        // (lockstep rings: the weight slot is released by its window slot's commit)
-        mbar_wait(p.lock ? bar_aempty(rb.slot) : bar_bempty(rb.slot), rb.phase ^ 1);
+        // released by every CTA of the cluster: safe to refill everywhere.
+        // One commit per K block (p.lock, SB <= SA): block g = fill - SB, the
+        // last reader of this weight slot, released window slot g % SA with
+        // its commit, in that barrier's phase g / SA
+        if (p.lock) {
+          if (fill >= static_cast<uint32_t>(SB)) {
+            const uint32_t g = fill - static_cast<uint32_t>(SB);
+            mbar_wait(bar_aempty(static_cast<int>(g % static_cast<uint32_t>(SA))), (g / static_cast<uint32_t>(SA)) & 1u);
+          }
+        } else {
+          mbar_wait(bar_bempty(rb.slot), rb.phase ^ 1);
+        }
         if (lane == 0) {
           const uint32_t dst = smem_u32(sB + static_cast<size_t>(rb.slot) * b_slot);
           const uint8_t* src = p.wt + (static_cast<size_t>(tl.nt) * n_blk + kb) * b_slot;

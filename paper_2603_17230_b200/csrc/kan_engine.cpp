@@ -1881,7 +1881,10 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
     if (const int t = e->opt.convw_tr; t > 0 && t < TR && l.out.h % t == 0) TR = t;  // tuning: fewer rows per tile
     const bool zp = pl.wscheme == KAN_W_PER_TENSOR_ASYM;
     const bool wsilu = pl.silu != 0;
-    const bool lock = e->opt.convw_lock > 0 && e->opt.convw_mc <= 1;
+    // one tcgen05.commit per K block (the window slot's; it also releases the
+    // weight slot): automatic for N tiles >= 128, where the MMA issue stream
+    // bounds the layer (measured -2...-3.4 % there, +-1 % on 64-column tiles)
+    const bool lock = (e->opt.convw_lock > 0 || (e->opt.convw_lock == 0 && BNw >= 128)) && e->opt.convw_mc <= 1;
     // activation loads: CX channels (64-byte rows where the channels allow),
     // and the deepest rings that fit, trading window height for them
     const int TW = std::min(16, l.out.w), G = 128 / TW, CS = l.stride;
@@ -1903,13 +1906,6 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
           SA = rings / 100;
           SB = rings / 10 % 10;
           SX = rings % 10;
-        }
-        if (lock) {  // equal window / weight ring depths
-          if (!e->opt.convw_rings) SA = SB = 3;
-          SB = SA = std::min(SA, SB);
-          while (!fits() && CX > 16) CX /= 2;
-          while (!fits() && SA > 2) SB = --SA;
-          while (!fits() && CX > 8) CX /= 2;
         }
         while (!fits() && SB > 2) --SB;
         while (!fits() && SA > 3) --SA;
@@ -1943,7 +1939,7 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
       // weight slots shared by a cluster of image groups (multicast): the
       // weights are re-streamed from L2 per tile, 9 taps x BN x 32 B per K block
       p.mc = e->opt.convw_mc > 0 ? e->opt.convw_mc : 1;
-      p.lock = lock && SA == SB ? 1 : 0;
+      p.lock = lock && SB <= SA ? 1 : 0;  // one commit per K block releases the window and the weight slot
       p.kym = pl.kymw ? 1 : 0;
       p.tab = ts.buf.p;
       p.tab_bytes = ts.bytes;
