@@ -262,6 +262,7 @@ typedef enum {
   KAN_OPT_NO_FUSE = 21,           /* 1: a small output layer always runs as its own launch (never inside the previous layer's kernel) */
   KAN_OPT_FUSE_PERSISTENT = 22,   /* 1: persistent (unsplit) launches also run a small output layer after each tile's epilogue */
   KAN_OPT_CONVW_NO_KYM = 23,      /* 1: kan_convw issues one MMA per (tap, output row) even where the ky-merged form applies */
+  KAN_OPT_CONVW_DUAL = 24,        /* kan_convw second MMA-issuing warp (even / odd accumulators; single-commit layers without the ky-merged issue): -1 off, 1 on, 0 = automatic (on with two or more N tiles) */
   KAN_OPT_CONVW_LOCK = 20         /* kan_convw: one tcgen05.commit per K block releases the window slot and the weight slot (needs weight ring <= window ring): -1 off, 1 on, 0 = automatic (on for N tiles >= 128) */
 } kan_option;
 kan_status kan_engine_set_option(kan_engine* e, int option, int64_t value);

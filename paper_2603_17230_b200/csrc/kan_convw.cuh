@@ -62,7 +62,7 @@ struct ConvwWarps {
   // stage-1 level layers -8...-17 %, the whole forward -4.7 %).  Measured
   // neutral or slower on the other instantiations, which keep one budget.
   static constexpr bool REGSPLIT = SILU && OUT == EPI_LEVEL;
-  static constexpr int UW = REGSPLIT ? 4 : 3;  // utility warps (+ the idle one)
+  static constexpr int UW = 4;  // utility warps: activation loader, MMA issuer, weight loader, second MMA issuer
   static constexpr int THREADS = 32 * (PW + UW + EW);
   static constexpr int R_LAUNCH = 80, R_PROD = 64, R_EPI = 104;
   static_assert(!REGSPLIT || (PW * R_PROD + UW * R_LAUNCH + EW * R_EPI <= (PW + UW + EW) * R_LAUNCH &&
@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(ConvwWarps<OUT, MODE == MODE_SILU, S>::THREADS
   using WarpsT = ConvwWarps<OUT, SILU, S>;
   constexpr int CONVW_EPI_WARPS = WarpsT::EW;
   constexpr int NPW = WarpsT::PW, NP = 32 * NPW;
-  constexpr int W_X = NPW, W_MMA = NPW + 1, W_B = NPW + 2, W_EPI = NPW + WarpsT::UW;
+  constexpr int W_X = NPW, W_MMA = NPW + 1, W_B = NPW + 2, W_MMA2 = NPW + 3, W_EPI = NPW + WarpsT::UW;
   constexpr bool ZP = (MODE == MODE_ZP);
   constexpr int RPT = WarpsT::RPT;  // window rows per producer thread (max)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -172,14 +172,14 @@ __global__ void __launch_bounds__(ConvwWarps<OUT, MODE == MODE_SILU, S>::THREADS
     }
     for (int s = 0; s < SA; ++s) {
       mbar_init(bar_afull(s), NPW);
-      mbar_init(bar_aempty(s), 1);
+      mbar_init(bar_aempty(s), p.dual ? 2 : 1);  // every MMA issuer commits its share of a K block
     }
     for (int s = 0; s < SB; ++s) {
       mbar_init(bar_bfull(s), 1);
       mbar_init(bar_bempty(s), MC);  // every CTA of the cluster releases the slot
     }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(bar_accfull(b), 1);
+      mbar_init(bar_accfull(b), p.dual ? 2 : 1);
       mbar_init(bar_accempty(b), CONVW_EPI_WARPS);
       mbar_init(bar_wsfull(b), NPW);
       mbar_init(bar_wsempty(b), CONVW_EPI_WARPS);
@@ -271,8 +271,14 @@ __global__ void __launch_bounds__(ConvwWarps<OUT, MODE == MODE_SILU, S>::THREADS
     // drain: every peer's release of our slots has landed before the CTA exits
     if (!p.lock)
       for (int s = 0; s < SB; ++s, rb.next()) mbar_wait(bar_bempty(rb.slot), rb.phase ^ 1);
-  } else if (warp == W_MMA) {
+  } else if (warp == W_MMA || (warp == W_MMA2 && p.dual)) {
     // ============ MMA issuer: 9 taps x NACC accumulators per K block ============
+    // p.dual (one commit per K block, no ky merge, no multicast): two issuing
+    // warps, the even accumulators on one and the odd ones on the other.  A
+    // single thread sustains one MMA per ~55-60 cycles and pays for the
+    // commits and barrier waits of every K block (scripts/mma_commit.cu), which
+    // leaves no slack against the 64 tensor cycles of an N = 128 MMA.
+    const int a_first = p.dual && warp == W_MMA2 ? 1 : 0, a_step = p.dual ? 2 : 1;
     const uint32_t idesc = idesc_i8(BN, p.b_signed != 0);
     const uint32_t idesc2 = idesc_i8(2 * BN, p.b_signed != 0), idesc3 = idesc_i8(3 * BN, p.b_signed != 0);
     // Descriptor start addresses advance in 16-byte units: one window row
@@ -344,7 +350,7 @@ __global__ void __launch_bounds__(ConvwWarps<OUT, MODE == MODE_SILU, S>::THREADS
               }
             }
           } else if (!KAN_DBG(p, 2)) {  // (tuning only: flag 2 skips the MMAs)
-            for (int a = 0; a < NACC; ++a) {
+            for (int a = a_first; a < NACC; a += a_step) {
               const uint32_t arow = a_lo + static_cast<uint32_t>(a) * acc_step;
               const uint32_t d = dacc + static_cast<uint32_t>(a * BN);
 #pragma unroll

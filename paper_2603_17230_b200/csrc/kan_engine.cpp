@@ -368,7 +368,7 @@ struct kan_engine {
   // into the fields above, so nothing is read from the environment
   struct Options {
     bool no_convw = false;
-    int convw_rings = 0, convw_tr = 0, convw_mc = 0, convw_bn = 0, convw_lock = 0;
+    int convw_rings = 0, convw_tr = 0, convw_mc = 0, convw_bn = 0, convw_lock = 0, convw_dual = 0;
     bool no_fuse = false, fuse_persistent = false, no_kym = false;
     bool no_conv3 = false, no_im2col = false, epi_stage = true, lv_sidecar = true, st_prepass = true;
     bool timeline = false, force_nacc1 = false, record_plan = false;
@@ -1941,6 +1941,11 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
       p.mc = e->opt.convw_mc > 0 ? e->opt.convw_mc : 1;
       p.lock = lock && SB <= SA ? 1 : 0;  // one commit per K block releases the window and the weight slot
       p.kym = pl.kymw ? 1 : 0;
+      // second MMA-issuing warp (even / odd accumulators): automatic with two or
+      // more N tiles (ResKAN18 stages 3-4: -2...-9 % per layer; one N tile of
+      // 128 columns measured +-2 % in the reference scheme, slower with SiLU)
+      p.dual = p.lock && !pl.kymw && p.mc <= 1 && TRu >= 2 &&
+                       (e->opt.convw_dual > 0 || (e->opt.convw_dual == 0 && pl.ntw >= 2)) ? 1 : 0;
       p.tab = ts.buf.p;
       p.tab_bytes = ts.bytes;
       p.off_thr = ts.off_thr;
@@ -3292,6 +3297,10 @@ kan_status kan_engine_set_option(kan_engine* e, int option, int64_t value) {
       case KAN_OPT_CONVW_LOCK:
         if (v < -1 || v > 1) throw InvalidArgument("KAN_OPT_CONVW_LOCK: -1, 0 or 1");
         o.convw_lock = v;
+        break;
+      case KAN_OPT_CONVW_DUAL:
+        if (v < -1 || v > 1) throw InvalidArgument("KAN_OPT_CONVW_DUAL: -1, 0 or 1");
+        o.convw_dual = v;
         break;
       case KAN_OPT_CONVW_MC:
         if (v < 0 || v > 4 || v == 3) throw InvalidArgument("KAN_OPT_CONVW_MC: 0 (auto), 1, 2 or 4");

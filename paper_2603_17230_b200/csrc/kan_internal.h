@@ -110,7 +110,8 @@ struct GemmParams {
   // per tile; b_slot = bytes of one tap's weight tile (spline + SiLU parts)
   int ext_rows, n_ss, b_slot;
   int kym;   // kan_convw: ky-merged MMA issue (weight taps per kx in reversed ky order)
-  int lock;  // kan_convw: window and weight rings of equal depth share one release barrier per slot
+  int lock;  // kan_convw: one commit per K block (the window slot's barrier also releases the weight slot)
+  int dual;  // kan_convw: two MMA-issuing warps (even / odd accumulators); needs lock, no ky merge, no multicast
   // fused output layer (split-K launches, LUT path): the reduced hidden levels
   // of each CTA's rows stay in smem and feed the next, small KAN layer
   // (N2 <= 16, NBP = 8, per-channel weights) inside this kernel, which writes

@@ -142,7 +142,7 @@ _lib.kan_shard_rows.restype = None
 OPTIONS = {"no_conv3": 1, "no_im2col": 2, "force_bn": 3, "tables": 4, "epi_stage": 5, "conv3_mc": 6,
            "lv_sidecar": 7, "level_prepass_min": 8, "st_prepass": 9, "st_slices": 10, "timeline": 11,
            "force_nacc1": 12, "record_plan": 13, "dbg_flags": 14, "no_convw": 15,
-           "convw_rings": 16, "convw_tr": 17, "convw_mc": 18, "convw_bn": 19, "convw_lock": 20, "no_fuse": 21, "fuse_persistent": 22, "convw_no_kym": 23}
+           "convw_rings": 16, "convw_tr": 17, "convw_mc": 18, "convw_bn": 19, "convw_lock": 20, "no_fuse": 21, "fuse_persistent": 22, "convw_no_kym": 23, "convw_dual": 24}
 
 # exported symbols declared in include/kan_b200.h (checked by the CPU tests)
 EXPORTED = [

@@ -393,14 +393,15 @@ def test_convw_issue_options_are_bit_identical(opt):
 
 def test_convw_single_commit_default_matches_two_commits_and_oracle(oracle):
     """128-column tiles run with one commit per K block by default (it releases
-    the window slot and the weight slot); the result equals the two-commit
-    form (convw_lock=-1), the general gather kernel and the oracle, bit for bit,
-    in both weight schemes."""
+    the window slot and the weight slot), and layers of two N tiles with two
+    MMA-issuing warps (even / odd accumulators); the result equals the
+    two-commit and single-issuer forms, the general gather kernel and the
+    oracle, bit for bit, in both weight schemes."""
     for ws, silu in ((W_PER_TENSOR_ASYM, False), (W_PER_CHANNEL_SYM, True)):
         desc = conv_desc(32, 16, 16, 32, 1, 1, 0)
         desc["layers"].append({"type": "conv", "c_in": 32, "c_out": 128, "kernel": 3, "stride": 1, "padding": 1})
-        desc["layers"].append({"type": "conv", "c_in": 128, "c_out": 128, "kernel": 3, "stride": 1, "padding": 1})
-        desc["layers"].append({"type": "conv", "c_in": 128, "c_out": 8, "kernel": 1, "stride": 1, "padding": 0})
+        desc["layers"].append({"type": "conv", "c_in": 128, "c_out": 256, "kernel": 3, "stride": 1, "padding": 1})
+        desc["layers"].append({"type": "conv", "c_in": 256, "c_out": 8, "kernel": 1, "stride": 1, "padding": 0})
         Ws, Bs = weights_for(desc, seed=37, silu=silu)
         x = np.random.default_rng(37).uniform(-1.05, 1.05, (21, 32 * 16 * 16)).astype(np.float32)
         opts = dict(mode="bspline-lut", lut_k=8, lut_h=3, bits_w=8, w_scheme=ws, silu_base=silu)
@@ -408,8 +409,10 @@ def test_convw_single_commit_default_matches_two_commits_and_oracle(oracle):
         e0.set_option("record_plan", 1)
         y0 = e0.model_forward(to_dev(x)).cpu().numpy()
         assert "convw layer=1" in e0.last_plan and "convw layer=2" in e0.last_plan
-        y1 = build(desc, Ws, Bs, engine_options={"convw_lock": -1}, **opts).model_forward(to_dev(x)).cpu().numpy()
-        np.testing.assert_array_equal(y0, y1)
+        # two commits, one issuer | one commit, one issuer | two issuers on the one-N-tile layer as well
+        for eo in ({"convw_lock": -1}, {"convw_dual": -1}, {"convw_dual": 1}):
+            y1 = build(desc, Ws, Bs, engine_options=eo, **opts).model_forward(to_dev(x)).cpu().numpy()
+            np.testing.assert_array_equal(y0, y1)
         yg = build(desc, Ws, Bs, engine_options={"no_convw": 1, "no_conv3": 1}, **opts).model_forward(to_dev(x)).cpu().numpy()
         np.testing.assert_array_equal(y0, yg)
         yo = oracle.int_model_forward(desc, Ws, Bs, x, 8, 3, ws, 8)
