@@ -35,7 +35,11 @@
 // each output row's code sum from the 9 window rows it read.
 //
 // Warp roles as in kan_gather_gemm_kernel (12 producers here), activation TMA,
-// MMA issuer, weight loader, 8 epilogue warps (two per TMEM lane quarter).
+// MMA issuer, weight loader, a second MMA issuer (p.dual: the odd accumulators;
+// idle otherwise), 8 epilogue warps (two per TMEM lane quarter).
+// One tcgen05.commit per K block where p.lock is set: the window slot's
+// barrier also releases the weight slot (the weight loader waits for the
+// commit of the K block that last read its slot; weight ring <= window ring).
 
 // Warp counts per output kind: the level epilogue (branch-free fp64 chains,
 // no fp32 staging) runs on 16 warps next to 8 producers; the fp32 + sidecar
