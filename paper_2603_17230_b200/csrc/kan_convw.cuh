@@ -59,7 +59,7 @@ struct ConvwWarps {
   static constexpr int EW = WIDE_EPI ? 16 : 8;  // a multiple of 4 (TMEM lane quarters)
   static constexpr int RPT = WIDE_EPI ? 4 : 3;
   // MODE_SILU level outputs split the register file by role (setmaxnreg works
-  // on aligned groups of 4 warps, so one idle warp pads the three utility
+  // on aligned groups of 4 warps: 12 producers, 4 utility warps, 8 epilogue
   // warps): the launch allocates 80 registers per thread (768 threads); the
   // 12 producer warps give back 16 each and the 8 epilogue warps run their
   // fp64 level chains at 104 without spilling (ResKAN18 per-channel + SiLU:
