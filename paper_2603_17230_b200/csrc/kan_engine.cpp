@@ -2094,7 +2094,9 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
   int variant = 0;
   // fp32 row-major output: the epilogue stages 32x16 blocks in smem so each
   // store instruction writes whole 64-byte row segments
-  bool stg = !bf16 && e->epi_stage && io.epi == EPI_F32 && io.out_hw == 0 && !io.res_kind;
+  // (not with a levels sidecar: the second staged pass and its warp syncs cost
+  // more than the half-sector stores; ResKAN18 stem 1.55 -> 1.42 ms)
+  bool stg = !bf16 && e->epi_stage && io.epi == EPI_F32 && io.out_hw == 0 && !io.res_kind && io.out_lv == nullptr;
   const int want_tab = e->force_tab >= 0 ? e->force_tab : 2;
   if (!bf16 && want_tab > 0 && e->tabs[want_tab].bytes > 0) {
     try {
