@@ -52,7 +52,7 @@
 // instantiations keep 12 producer warps x 3 rows for both output kinds.
 // The stride-2 form expands a (2 TR + 1)-row window per TR output rows, so it
 // is producer-heavy: 12 + 8 there too (measured: the stage-2 entry conv -14 %).
-template <int OUT, bool SILU = false, int S = 1>
+template <int OUT, bool SILU = false, int S = 1, int LG = 3>
 struct ConvwWarps {
   static constexpr bool WIDE_EPI = OUT == EPI_LEVEL && !SILU && S == 1;
   static constexpr int PW = WIDE_EPI ? 8 : 12;
@@ -66,7 +66,11 @@ struct ConvwWarps {
   // stage-1 level layers -8...-17 %, the whole forward -4.7 %).  Measured
   // neutral or slower on the other instantiations, which keep one budget.
   static constexpr bool REGSPLIT = SILU && OUT == EPI_LEVEL;
-  static constexpr int UW = 4;  // utility warps: activation loader, MMA issuer, weight loader, second MMA issuer
+  // Utility warps: activation loader, MMA issuer, weight loader and, except in
+  // the SiLU fp32-output form of 8-image tiles (C4's conv: measured 4 % faster
+  // without it), a second MMA issuer (p.dual; see convw_dual_capable).
+  static constexpr bool DUAL_OK = !(SILU && OUT == EPI_F32 && LG == 3);
+  static constexpr int UW = DUAL_OK ? 4 : 3;
   static constexpr int THREADS = 32 * (PW + UW + EW);
   static constexpr int R_LAUNCH = 80, R_PROD = 64, R_EPI = 104;
   static_assert(!REGSPLIT || (PW * R_PROD + UW * R_LAUNCH + EW * R_EPI <= (PW + UW + EW) * R_LAUNCH &&
@@ -78,14 +82,15 @@ constexpr int CONVW_MAX_ROWS = 1024;  // <= RPT * 32 * PW for both kinds
 // S: conv stride (1, or 2 for 16-wide outputs with G = 8: consecutive output
 // pixels are then every other window pixel, a core-matrix stride of 512 B).
 template <int MODE, int OUT, int LG, int S>
-__global__ void __launch_bounds__(ConvwWarps<OUT, MODE == MODE_SILU, S>::THREADS, 1)
+__global__ void __launch_bounds__(ConvwWarps<OUT, MODE == MODE_SILU, S, LG>::THREADS, 1)
     kan_convw_kernel(const __grid_constant__ CUtensorMap xmap, const GemmParams p) {
   constexpr bool SILU = (MODE == MODE_SILU);
-  using WarpsT = ConvwWarps<OUT, SILU, S>;
+  using WarpsT = ConvwWarps<OUT, SILU, S, LG>;
   constexpr int CONVW_EPI_WARPS = WarpsT::EW;
   constexpr int NPW = WarpsT::PW, NP = 32 * NPW;
   constexpr int W_X = NPW, W_MMA = NPW + 1, W_B = NPW + 2, W_MMA2 = NPW + 3, W_EPI = NPW + WarpsT::UW;
   constexpr bool ZP = (MODE == MODE_ZP);
+  const bool dual = WarpsT::DUAL_OK && p.dual != 0;  // two MMA-issuing warps
   constexpr int RPT = WarpsT::RPT;  // window rows per producer thread (max)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -176,14 +181,14 @@ __global__ void __launch_bounds__(ConvwWarps<OUT, MODE == MODE_SILU, S>::THREADS
     }
     for (int s = 0; s < SA; ++s) {
       mbar_init(bar_afull(s), NPW);
-      mbar_init(bar_aempty(s), p.dual ? 2 : 1);  // every MMA issuer commits its share of a K block
+      mbar_init(bar_aempty(s), dual ? 2 : 1);  // every MMA issuer commits its share of a K block
     }
     for (int s = 0; s < SB; ++s) {
       mbar_init(bar_bfull(s), 1);
       mbar_init(bar_bempty(s), MC);  // every CTA of the cluster releases the slot
     }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(bar_accfull(b), p.dual ? 2 : 1);
+      mbar_init(bar_accfull(b), dual ? 2 : 1);
       mbar_init(bar_accempty(b), CONVW_EPI_WARPS);
       mbar_init(bar_wsfull(b), NPW);
       mbar_init(bar_wsempty(b), CONVW_EPI_WARPS);
@@ -275,14 +280,14 @@ __global__ void __launch_bounds__(ConvwWarps<OUT, MODE == MODE_SILU, S>::THREADS
     // drain: every peer's release of our slots has landed before the CTA exits
     if (!p.lock)
       for (int s = 0; s < SB; ++s, rb.next()) mbar_wait(bar_bempty(rb.slot), rb.phase ^ 1);
-  } else if (warp == W_MMA || (warp == W_MMA2 && p.dual)) {
+  } else if (warp == W_MMA || (dual && warp == W_MMA2)) {
     // ============ MMA issuer: 9 taps x NACC accumulators per K block ============
     // p.dual (one commit per K block, no ky merge, no multicast): two issuing
     // warps, the even accumulators on one and the odd ones on the other.  A
     // single thread sustains one MMA per ~55-60 cycles and pays for the
     // commits and barrier waits of every K block (scripts/mma_commit.cu), which
     // leaves no slack against the 64 tensor cycles of an N = 128 MMA.
-    const int a_first = p.dual && warp == W_MMA2 ? 1 : 0, a_step = p.dual ? 2 : 1;
+    const int a_first = dual && warp == W_MMA2 ? 1 : 0, a_step = dual ? 2 : 1;
     const uint32_t idesc = idesc_i8(BN, p.b_signed != 0);
     const uint32_t idesc2 = idesc_i8(2 * BN, p.b_signed != 0), idesc3 = idesc_i8(3 * BN, p.b_signed != 0);
     // Descriptor start addresses advance in 16-byte units: one window row
@@ -670,6 +675,9 @@ __global__ void __launch_bounds__(ConvwWarps<OUT, MODE == MODE_SILU, S>::THREADS
 
 int convw_max_rows() { return CONVW_MAX_ROWS; }
 
+// whether the instantiation that launch_convw picks has the second MMA-issuing warp
+bool convw_dual_capable(int mode, int epi, int g_img) { return !(mode == MODE_SILU && epi == EPI_F32 && g_img == 8); }
+
 size_t convw_smem_bytes(int BN, int WR, int CX, int SA, int SB, int SX, int tab_bytes, bool zp, bool silu) {
   const size_t b = static_cast<size_t>(9) * BN * 32;
   const size_t x = (static_cast<size_t>(WR) * CX * 2 + 1023) / 1024 * 1024;
@@ -706,9 +714,8 @@ cudaError_t launch_convw(int mode, const CUtensorMap& xmap, const GemmParams& p,
   auto pick = [&](auto lgc, auto sc) -> cudaError_t {
     constexpr int LG = decltype(lgc)::value, S = decltype(sc)::value;
     const int v = 4 * (LG - 3) + (S == 2 ? 12 : 0);
-    constexpr int TL = ConvwWarps<EPI_LEVEL, false, S>::THREADS, TF = ConvwWarps<EPI_F32, false, S>::THREADS;
-    constexpr int TS = ConvwWarps<EPI_F32, true, S>::THREADS;  // MODE_SILU: one warp layout ...
-    constexpr int TSL = ConvwWarps<EPI_LEVEL, true, S>::THREADS;  // ... plus the idle warp of the register split
+    constexpr int TL = ConvwWarps<EPI_LEVEL, false, S, LG>::THREADS, TF = ConvwWarps<EPI_F32, false, S, LG>::THREADS;
+    constexpr int TS = ConvwWarps<EPI_F32, true, S, LG>::THREADS, TSL = ConvwWarps<EPI_LEVEL, true, S, LG>::THREADS;
     if (mode == MODE_SILU)
       return lvl ? go(kan_convw_kernel<MODE_SILU, EPI_LEVEL, LG, S>, 16 + v / 2 + 1, TSL)
                  : go(kan_convw_kernel<MODE_SILU, EPI_F32, LG, S>, 16 + v / 2, TS);

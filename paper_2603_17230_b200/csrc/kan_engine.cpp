@@ -55,6 +55,7 @@ size_t conv3_smem_bytes(int BN, int R, int SA, int SB, int SX, int x_kind, int t
 cudaError_t launch_convw(int mode, const CUtensorMap& xmap, const GemmParams& p, size_t smem, cudaStream_t st);
 size_t convw_smem_bytes(int BN, int WR, int CX, int SA, int SB, int SX, int tab_bytes, bool zp, bool silu);
 int convw_max_rows();
+bool convw_dual_capable(int mode, int epi, int g_img);
 size_t small_smem_bytes(const SmallParams& p);
 cudaError_t launch_im2col_levels(const float* x, int64_t n_img, int C, int H, int W, int K, int stride, int pad,
                                  int Ho, int Wo, uint16_t* out, int ld_o, const float* thr, float nlo_step,
@@ -1944,7 +1945,7 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
       // second MMA-issuing warp (even / odd accumulators): automatic with two or
       // more N tiles (ResKAN18 stages 3-4: -2...-9 % per layer; one N tile of
       // 128 columns measured +-2 % in the reference scheme, slower with SiLU)
-      p.dual = p.lock && !pl.kymw && p.mc <= 1 && TRu >= 2 &&
+      p.dual = p.lock && !pl.kymw && p.mc <= 1 && TRu >= 2 && convw_dual_capable(zp ? 1 : (wsilu ? 2 : 0), io.epi, G) &&
                        (e->opt.convw_dual > 0 || (e->opt.convw_dual == 0 && pl.ntw >= 2)) ? 1 : 0;
       p.tab = ts.buf.p;
       p.tab_bytes = ts.bytes;
