@@ -12,6 +12,7 @@ cap() {  # name config kernel-regex skip [extra prof_layer args]
 cap r02_c5_l2 c5 convw 1          # stage-1 conv, residual add, fp32 + levels sidecar out (the bench's dominant launch)
 cap r02_c5_l4 c5 convw 3          # stage-1 conv, residual add, levels out
 cap r02_c5_l8 c5 convw 7          # stage-2 conv, levels out (N = 128)
+cap r02_c5_l13 c5 convw 9         # stage-3 conv, levels out (two N tiles: two MMA-issuing warps)
 cap r02_c4_conv c4 convw 0        # C4: SiLU form, NCHW output
 cap r02_c3_l0 c3 gather 0         # C3 int8 layer 0
 cap r02_c3bf16_l0 c3bf16 gather 0 # C3 bf16 layer 0
@@ -23,8 +24,8 @@ ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum 
 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:gather -c 3 --csv --log-file gpurun_out/r02_c3bf16_gather_dram.csv python scripts/prof_layer.py --config c3bf16 --iters 1 > gpurun_out/ncu_c3bf16_dram.log 2>&1; echo "c3bf16 dram rc=$?"
 # summarise on the box (the .ncu-rep files are too large to travel): details
 # pages + ncu_summary.json via make_profiles.py, stall/instruction summaries
-python scripts/make_profiles.py gpurun_out c5_l2=r02_c5_l2 c5_l4=r02_c5_l4 c5_l8=r02_c5_l8 c4_l0=r02_c4_conv c3_l0=r02_c3_l0 c3bf16_l0=r02_c3bf16_l0 c2_l0=r02_c2_l0
-for n in r02_c5_l2 r02_c5_l4 r02_c5_l8 r02_c4_conv r02_c3_l0 r02_c3bf16_l0 r02_c2_l0; do
+python scripts/make_profiles.py gpurun_out c5_l2=r02_c5_l2 c5_l4=r02_c5_l4 c5_l8=r02_c5_l8 c5_l13=r02_c5_l13 c4_l0=r02_c4_conv c3_l0=r02_c3_l0 c3bf16_l0=r02_c3bf16_l0 c2_l0=r02_c2_l0
+for n in r02_c5_l2 r02_c5_l4 r02_c5_l8 r02_c5_l13 r02_c4_conv r02_c3_l0 r02_c3bf16_l0 r02_c2_l0; do
   cp profiles/$n.txt gpurun_out/
   python scripts/ncu_summary.py gpurun_out/$n.ncu-rep --tensor > gpurun_out/${n}_stalls.txt 2>&1
   ncu -i gpurun_out/$n.ncu-rep --page raw --csv > gpurun_out/${n}_raw.csv 2>/dev/null
