@@ -378,10 +378,11 @@ struct kan_engine {
   } opt;
   // launch plan of the last forward (opt.record_plan): one line per kernel
   std::string plan;
-  void plan_add(const char* kernel, int layer, int epi, int res, int lv, int N, int BN, int splits, int mode) {
-    char buf[160];
-    std::snprintf(buf, sizeof(buf), "%s layer=%d epi=%d res=%d lv=%d N=%d BN=%d splits=%d mode=%d\n", kernel, layer,
-                  epi, res, lv, N, BN, splits, mode);
+  void plan_add(const char* kernel, int layer, int epi, int res, int lv, int N, int BN, int splits, int mode,
+                const char* extra = "") {
+    char buf[200];
+    std::snprintf(buf, sizeof(buf), "%s layer=%d epi=%d res=%d lv=%d N=%d BN=%d splits=%d mode=%d%s\n", kernel, layer,
+                  epi, res, lv, N, BN, splits, mode, extra);
     plan += buf;
   }
   std::vector<DevBuf<unsigned long long>> timeline_buf;
@@ -2005,7 +2006,8 @@ void run_gemm_layer(kan_engine* e, PreparedLayer& pl, int64_t M, const LayerIO& 
       if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (convw) failed (" + std::to_string(r) + ")");
       const size_t smem = convw_smem_bytes(BNw, WR, CX, SA, SB, SX, ts.bytes, zp, wsilu);
       if (e->opt.record_plan)
-        e->plan_add("convw", pl.layer_index, p.epi, p.res_kind, p.out_lv != nullptr, p.N, BNw, 1, zp ? 1 : (wsilu ? 2 : 0));
+        e->plan_add("convw", pl.layer_index, p.epi, p.res_kind, p.out_lv != nullptr, p.N, BNw, 1, zp ? 1 : (wsilu ? 2 : 0),
+                    p.dual ? " commits=1 issuers=2" : (p.lock ? " commits=1 issuers=1" : " commits=2 issuers=1"));
       ck(launch_convw(zp ? 1 : (wsilu ? 2 : 0), xm, p, smem, st), "convw launch");  // MODE_ZP / MODE_SILU / MODE_PLAIN
       e->last_launches += 1;
       return;
